@@ -1,0 +1,182 @@
+"""Batches, the BASELINE synthetic corpora and P@k.
+
+* ``batches`` restates the seeded epoch shuffle of the reference
+  (reference data.py:118-123): ``default_rng(seed).permutation(n)`` cut into
+  batches, the last one possibly short.
+* ``precision_at_k`` restates reference data.py:126-133.
+* ``synthetic_corpus`` is the generator of SURVEY.md section 8(d) that stands
+  in for Delicious-200K / Amazon-670K (not in the container): bounded Zipf
+  feature and label ids mapped through fixed permutations, U(0,1] values,
+  optional L2 normalisation.  One ``default_rng(seed)`` stream is consumed per
+  sample in the order nnz count, features, values, label count, labels.
+
+Corpora are held as CSR (``Corpus``) because that is what the device step
+consumes; ``Corpus.example(i)`` gives the reference-style (SparseVector,
+labels) pair.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .sparse import SparseVector
+
+
+@dataclass
+class Corpus:
+    """CSR multi-label corpus.  Feature ids sorted per row, values float32
+    (nonzero), labels sorted unique per row."""
+
+    x_ptr: np.ndarray  # int64 (n+1,)
+    x_idx: np.ndarray  # int32
+    x_val: np.ndarray  # float32
+    y_ptr: np.ndarray  # int64 (n+1,)
+    y_idx: np.ndarray  # int32
+    num_features: int
+    num_labels: int
+
+    def __len__(self) -> int:
+        return len(self.x_ptr) - 1
+
+    def example(self, i: int):
+        a, b = self.x_ptr[i], self.x_ptr[i + 1]
+        c, d = self.y_ptr[i], self.y_ptr[i + 1]
+        x = SparseVector(self.x_idx[a:b].astype(np.int64), self.x_val[a:b].astype(np.float64), self.num_features)
+        return x, frozenset(self.y_idx[c:d].tolist())
+
+    def subset(self, rows) -> "Corpus":
+        rows = np.asarray(rows, dtype=np.int64)
+        xl = self.x_ptr[rows + 1] - self.x_ptr[rows]
+        yl = self.y_ptr[rows + 1] - self.y_ptr[rows]
+        x_ptr = np.zeros(rows.size + 1, dtype=np.int64)
+        y_ptr = np.zeros(rows.size + 1, dtype=np.int64)
+        np.cumsum(xl, out=x_ptr[1:])
+        np.cumsum(yl, out=y_ptr[1:])
+        xi = np.concatenate([np.arange(self.x_ptr[r], self.x_ptr[r + 1]) for r in rows]) if rows.size else np.empty(0, np.int64)
+        yi = np.concatenate([np.arange(self.y_ptr[r], self.y_ptr[r + 1]) for r in rows]) if rows.size else np.empty(0, np.int64)
+        return Corpus(x_ptr, self.x_idx[xi], self.x_val[xi], y_ptr, self.y_idx[yi], self.num_features, self.num_labels)
+
+    def triples(self):
+        """[(x_idx int64, x_val float64, labels sorted list)] for CPU checkers."""
+        out = []
+        for i in range(len(self)):
+            a, b = self.x_ptr[i], self.x_ptr[i + 1]
+            c, d = self.y_ptr[i], self.y_ptr[i + 1]
+            out.append((self.x_idx[a:b].astype(np.int64), self.x_val[a:b].astype(np.float64),
+                        self.y_idx[c:d].astype(np.int64).tolist()))
+        return out
+
+
+def corpus_from_examples(examples, num_features: int, num_labels: int) -> Corpus:
+    """Pack (SparseVector, labels) pairs into CSR (values rounded to float32)."""
+    x_ptr = [0]
+    y_ptr = [0]
+    xi, xv, yi = [], [], []
+    for x, labels in examples:
+        if x.dim != num_features:
+            raise ValueError(f"input dim {x.dim} != {num_features}")
+        xi.append(np.asarray(x.indices, dtype=np.int32))
+        xv.append(np.asarray(x.values, dtype=np.float32))
+        lab = np.array(sorted(set(int(l) for l in labels)), dtype=np.int32)
+        if lab.size and (lab[0] < 0 or lab[-1] >= num_labels):
+            raise ValueError(f"label outside [0, {num_labels})")
+        yi.append(lab)
+        x_ptr.append(x_ptr[-1] + len(x.indices))
+        y_ptr.append(y_ptr[-1] + lab.size)
+    cat = lambda parts, dt: np.concatenate(parts).astype(dt) if parts else np.empty(0, dt)
+    return Corpus(np.asarray(x_ptr, np.int64), cat(xi, np.int32), cat(xv, np.float32),
+                  np.asarray(y_ptr, np.int64), cat(yi, np.int32), num_features, num_labels)
+
+
+def batches(n_examples: int, batch_size: int, seed):
+    """Row-index batches of one epoch (reference data.py:118-123)."""
+    if not isinstance(batch_size, (int, np.integer)) or batch_size < 1:
+        raise ValueError(f"batch_size must be a positive integer, got {batch_size!r}")
+    order = np.random.default_rng(seed).permutation(n_examples)
+    for lo in range(0, len(order), batch_size):
+        yield order[lo : lo + batch_size]
+
+
+def precision_at_k(ranked, truth, k: int) -> float:
+    """|top-k of ranked that are true| / k; an empty ranking scores 0
+    (reference data.py:126-133)."""
+    if not isinstance(k, (int, np.integer)) or k < 1:
+        raise ValueError(f"k must be a positive integer, got {k!r}")
+    top = list(ranked[:k])
+    if not top:
+        return 0.0
+    truth = set(truth)
+    return sum(1 for r in top if r in truth) / k
+
+
+# ---------------------------------------------------------------------------
+# SURVEY 8(d) synthetic generator
+# ---------------------------------------------------------------------------
+
+
+class _Zipf:
+    """Bounded Zipf over ranks [0, n): P(r) ~ (r+1)^-a, inverse-CDF sampling,
+    rank -> id through ``perm``."""
+
+    def __init__(self, n: int, a: float, perm: np.ndarray):
+        w = np.arange(1, n + 1, dtype=np.float64) ** (-a)
+        self.cdf = np.cumsum(w) / w.sum()
+        self.n = n
+        self.perm = perm
+
+    def distinct(self, rng, count: int) -> np.ndarray:
+        count = min(count, self.n)
+        got: list = []
+        seen: set = set()
+        while len(got) < count:
+            u = rng.random(2 * (count - len(got)) + 8)
+            r = np.minimum(np.searchsorted(self.cdf, u, side="right"), self.n - 1)
+            for v in r.tolist():
+                if v not in seen:
+                    seen.add(v)
+                    got.append(v)
+        return self.perm[np.asarray(got[:count], dtype=np.int64)]
+
+
+@dataclass(frozen=True)
+class CorpusSpec:
+    num_features: int
+    num_labels: int
+    nnz: tuple  # ("uniform", lo, hi) or ("poisson", mean)
+    feat_zipf: float
+    labels: tuple  # ("uniform", lo, hi) or ("poisson", mean)
+    label_zipf: float
+    l2_normalize: bool
+
+
+def _count(rng, spec: tuple) -> int:
+    if spec[0] == "uniform":
+        return int(rng.integers(spec[1], spec[2] + 1))
+    return max(1, int(rng.poisson(spec[1])))
+
+
+def synthetic_corpus(spec: CorpusSpec, n: int, seed: int = 0) -> Corpus:
+    """SURVEY.md 8(d) procedure, consuming one default_rng(seed) stream."""
+    fz = _Zipf(spec.num_features, spec.feat_zipf, np.random.default_rng(101).permutation(spec.num_features))
+    lz = _Zipf(spec.num_labels, spec.label_zipf, np.random.default_rng(102).permutation(spec.num_labels))
+    rng = np.random.default_rng(seed)
+    x_ptr = np.zeros(n + 1, dtype=np.int64)
+    y_ptr = np.zeros(n + 1, dtype=np.int64)
+    xi, xv, yi = [], [], []
+    for s in range(n):
+        c = _count(rng, spec.nnz)
+        f = np.sort(fz.distinct(rng, c))
+        v = 1.0 - rng.random(f.size)
+        if spec.l2_normalize:
+            v = v / np.sqrt(np.dot(v, v))
+        cl = _count(rng, spec.labels)
+        lab = np.sort(lz.distinct(rng, cl))
+        xi.append(f.astype(np.int32))
+        xv.append(v.astype(np.float32))
+        yi.append(lab.astype(np.int32))
+        x_ptr[s + 1] = x_ptr[s] + f.size
+        y_ptr[s + 1] = y_ptr[s] + lab.size
+    return Corpus(x_ptr, np.concatenate(xi), np.concatenate(xv), y_ptr, np.concatenate(yi),
+                  spec.num_features, spec.num_labels)
