@@ -1,0 +1,383 @@
+"""Benchmark: SLIDE LSH-sparse training step (fwd + bwd + Adam + rebuild).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload wide_in]
+    python bench.py --impl reference ...   # the reference algorithm on the CPU
+
+One JSON line on rank 0.  A "step" is one train_batch of B synthetic
+samples (SURVEY.md 8(d) generator, standing in for Delicious-200K /
+Amazon-670K) through the snapshot schedule, including the table rebuild
+whenever the schedule makes it due (every ~50 steps) -- the timed steps are
+chosen so that one rebuild falls inside them.
+
+* value: samples/s with every batch already resident in HBM; each step is
+  timed with CUDA events on the launching stream, L2 flushed (256 MiB write)
+  between steps outside the events;
+* e2e: same metric through the public API (SlideNetwork.train_batch_csr)
+  from pinned host CSR, host->device copy and the per-slot loss readback
+  inside the timed region;
+* roofline: the dominant kernel's algorithmic bytes / its event-timed
+  duration vs the measured HBM copy bandwidth (MEASURED_PEAKS.json);
+* cpu_baseline: the CPU oracle (a numpy restatement of the reference path,
+  kind "port") on a bounded sample of the same workload, 1 thread.
+
+N>1 (torchrun): independent replicas, one per GPU, each on its own data
+shard (weak scaling), max-over-ranks device time.  The column-sharded output
+layer of SURVEY 8(e) is not implemented yet.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+STAGES = ["hidden_fwd", "query_hash", "slot_rng", "select", "fallback", "compact", "logits", "softmax",
+          "hidden_grad", "group_rows", "adam_w2", "hidden_counts", "group_features", "adam_w1", "hidden_bias",
+          "rebuild_hash", "rebuild_build"]
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=53)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--workload", default="wide_in")
+    p.add_argument("--schedule", default="snapshot", choices=["snapshot", "sequential"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-samples", type=int, default=128)
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) >= 7:
+                    self.rows.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_net(w, torch):
+    from paper_1903_03129_b200 import LshLayerConfig, SamplerConfig, SlideNetwork, TrainConfig
+
+    cfg = TrainConfig(batch_size=w.batch, learning_rate=w.lr, n0=w.n0, decay=w.decay, seed=0)
+    spec = LshLayerConfig(w.family, k=w.k, l=w.l, capacity=w.cap, policy=w.policy, wta_bin_size=w.bin_size,
+                          sampler=SamplerConfig(w.strategy, beta=w.beta))
+    return SlideNetwork(w.input_dim, [w.hidden, w.n_out], cfg, lsh_layers={1: spec})
+
+
+def csr_batches(corpus, B, n):
+    from paper_1903_03129_b200.network import HostCsr
+
+    out = []
+    for s in range(n):
+        sub = corpus.subset(np.arange(s * B, (s + 1) * B))
+        out.append(HostCsr(sub.x_ptr.astype(np.int32), sub.x_idx, sub.x_val, sub.y_ptr.astype(np.int32), sub.y_idx))
+    return out
+
+
+def stage_bytes(w, ms, cnt, steps):
+    """Algorithmic bytes per stage per step from the realised sets.
+
+    Every touched row / coordinate counted once per step; fp32 state."""
+    H = w.hidden
+    per = lambda v: v / max(steps, 1)
+    P, nnz, B = per(cnt[8]), per(cnt[9]), per(cnt[10])
+    U2, U1 = per(cnt[2]), per(cnt[3])
+    t2, t1 = per(cnt[0]), per(cnt[1])
+    probed = per(cnt[4])
+    rebuilds = per(cnt[11])
+    b = {
+        "hidden_fwd": U1 * 4 * H + nnz * 8 + B * 4 * H,
+        "query_hash": B * 4 * H + B * w.l * 4,
+        "select": B * w.l * 8 + probed * 4 + P * 4,
+        "logits": U2 * (4 * H + 4) + P * 12 + B * 4 * H,
+        "softmax": P * 13,
+        "hidden_grad": U2 * 4 * H + P * 8 + B * 8 * H,
+        "adam_w2": t2 * 24 + U2 * (24 + 16 + 12) + P * 12,
+        "adam_w1": t1 * 24 + U1 * 12 + nnz * 12,
+        "hidden_bias": B * 4 * H * 3,
+        "rebuild_hash": rebuilds * (w.n_out * 4 * H + w.n_out * w.l * 4),
+        "rebuild_build": rebuilds * (w.n_out * w.l * 4 * 4),
+    }
+    # whole step (SURVEY 8(d) formula): inputs + W1 rows + Adam W1 + probes + W2 rows + Adam W2 + rebuild
+    step = (nnz * 8 + per(cnt[10]) * 0 + U1 * 4 * H + 20 * t1 + 24 * H + B * w.l * 8 + probed * 4
+            + U2 * (4 * H + 24) + 20 * t2 + b["rebuild_hash"] + b["rebuild_build"])
+    return b, step
+
+
+def run_ours(args, rank, world):
+    import torch
+
+    from paper_1903_03129_b200 import _lib
+    from paper_1903_03129_b200.configs import WORKLOADS
+    from paper_1903_03129_b200.data import synthetic_corpus
+
+    torch.cuda.set_device(rank % torch.cuda.device_count())
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    w = WORKLOADS[args.workload]
+    K, W = args.steps, args.warmup
+    n_batches = W + K
+    corpus = synthetic_corpus(w.corpus, n_batches * w.batch, seed=1000 + rank)
+    batches = csr_batches(corpus, w.batch, n_batches)
+    net = make_net(w, torch)
+    sub = 1 if args.schedule == "sequential" else w.batch
+    # device-resident inputs for `value`
+    dev_batches = []
+    for b in batches:
+        bt, keep = net._upload(b)
+        dev_batches.append((bt, keep, b))
+    torch.cuda.synchronize()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    loss_buf = np.empty(w.batch, np.float64)
+    act_buf = np.empty(w.batch, np.int64)
+
+    def step_dev(it):
+        bt, _, _ = dev_batches[it - 1]
+        _lib.call("slide_train_batch", net._ctx, _lib.C.byref(bt), it, sub, loss_buf.ctypes.data, act_buf.ctypes.data)
+        return net._barrier(it, loss_buf, act_buf)
+
+    for it in range(1, W + 1):
+        step_dev(it)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    lc0 = np.zeros(1, np.uint64)
+    _lib.call("slide_launch_count", lc0.ctypes.data)
+    times = []
+    losses = []
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for it in range(W + 1, W + K + 1):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            st = step_dev(it)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            losses.append(st.loss)
+    lc1 = np.zeros(1, np.uint64)
+    _lib.call("slide_launch_count", lc1.ctypes.data)
+    if dist:
+        dist.barrier()
+    total_ms = float(np.sum(times))
+    if dist:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * K * w.batch / (total_ms / 1e3)
+    # -- e2e: public API from pinned host CSR, fresh net state continues
+    e2e = None
+    if not args.no_e2e:
+        e_times = []
+        h2d = d2h = 0
+        for k in range(K):
+            it = W + K + 1 + k
+            b = batches[(W + k) % n_batches]
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            net.train_batch_csr(b, it, schedule=args.schedule)
+            e1.record()
+            torch.cuda.synchronize()
+            e_times.append(e0.elapsed_time(e1))
+            h2d += net.h2d_bytes
+            d2h += w.batch * 16 + (w.batch + 1) * 4 * (w.batch // sub)
+        e_total = float(np.sum(e_times))
+        if dist:
+            t = torch.tensor([e_total], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_total = float(t.item())
+        e2e = {"value": world * K * w.batch / (e_total / 1e3), "unit": "samples/s",
+               "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K)}
+    # -- profiled pass: per-stage event times + realised sets
+    _lib.call("slide_profile", net._ctx, 1)
+    it0 = W + 2 * K + 1
+    for k in range(K):
+        step_dev_it = it0 + k
+        bt, _, _ = dev_batches[(W + k) % n_batches]
+        _lib.call("slide_train_batch", net._ctx, _lib.C.byref(bt), step_dev_it, sub, loss_buf.ctypes.data,
+                  act_buf.ctypes.data)
+        net._barrier(step_dev_it, loss_buf, act_buf)
+    ms = np.zeros(32)
+    cnt = np.zeros(16, np.int64)
+    _lib.call("slide_profile_read", net._ctx, ms.ctypes.data, cnt.ctypes.data)
+    _lib.call("slide_profile", net._ctx, 0)
+    stage_ms = {STAGES[i]: float(ms[i]) / K for i in range(len(STAGES))}
+    sb, step_bytes = stage_bytes(w, ms, cnt, K)
+    dom = max((k for k in sb if stage_ms.get(k, 0) > 0), key=lambda k: stage_ms[k])
+    peak, peak_kind = peaks()
+    achieved = sb[dom] / (stage_ms[dom] / 1e3) / 1e9
+    ms_per_step = total_ms / K
+    out = {
+        "metric": "train samples/sec (LSH-sparse fwd+bwd+Adam), % of HBM roofline, 1/2/4/8 GPU",
+        "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (SURVEY 8(d) Zipf generator; Delicious-200K shape)",
+        "config": {"workload": w.name, "input_dim": w.input_dim, "hidden": w.hidden, "n_out": w.n_out,
+                   "batch": w.batch, "hash": f"{w.family} K={w.k} L={w.l} cap={w.cap} {w.policy}",
+                   "sampler": f"{w.strategy} beta={w.beta}", "lr": w.lr, "rebuild": f"n0={w.n0} decay={w.decay}",
+                   "schedule": args.schedule, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "flushed between steps (256 MiB write, outside the events)"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                     "algorithmic_bytes_per_launch": sb[dom], "ms_per_launch": stage_ms[dom]},
+        "step_roofline": {"bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (ms_per_step / 1e3) / 1e9,
+                          "frac": step_bytes / (ms_per_step / 1e3) / 1e9 / peak},
+        "stages_ms_per_step": {k: round(v, 4) for k, v in stage_ms.items()},
+        "realised_per_step": {"pairs": cnt[8] / K, "unique_rows": cnt[2] / K, "unique_features": cnt[3] / K,
+                              "touched_w2": cnt[0] / K, "touched_w1": cnt[1] / K, "input_nnz": cnt[9] / K,
+                              "probed_slots": cnt[4] / K, "rebuilds_in_profile": int(cnt[11])},
+        "gpu_launches": int(lc1[0] - lc0[0]),
+        "clocks": clk.summary(),
+        "loss_first_last": [losses[0], losses[-1]],
+    }
+    if e2e:
+        out["e2e"] = e2e
+    del dev_batches
+    return out, net, w
+
+
+def cpu_port_rate(w, n_samples, threads=1):
+    """CPU oracle (numpy restatement of the reference, test infrastructure)
+    on a bounded sample of the workload: sequential schedule = the
+    reference's train_batch(workers=1)."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import slide_oracle as O
+    from paper_1903_03129_b200.data import synthetic_corpus
+
+    with threadpool_limits(threads):
+        st = O.init_state(w.input_dim, w.hidden, w.n_out, seed=0)
+        spec = O.LshSpec(w.family, w.k, w.l, w.cap, w.policy, bin_size=w.bin_size, strategy=w.strategy, beta=w.beta)
+        lsh = O.OutputLsh(spec, w.hidden, 0, w.n0, w.decay)
+        lsh.build(st.w2)
+        corpus = synthetic_corpus(w.corpus, n_samples, seed=7)
+        trip = corpus.triples()
+        t0 = time.perf_counter()
+        O.train_step(st, lsh, trip, 1, 0, w.n_out, O.AdamCfg(lr=w.lr), mode="sequential")
+        dt = time.perf_counter() - t0
+    return n_samples / dt, dt
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm's CPU path (oracle port),
+    K bounded steps on rank 0."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import slide_oracle as O
+    from paper_1903_03129_b200.configs import WORKLOADS
+    from paper_1903_03129_b200.data import synthetic_corpus
+
+    w = WORKLOADS[args.workload]
+    per_step = max(1, min(w.batch, 4))
+    with threadpool_limits(1):
+        st = O.init_state(w.input_dim, w.hidden, w.n_out, seed=0)
+        spec = O.LshSpec(w.family, w.k, w.l, w.cap, w.policy, bin_size=w.bin_size, strategy=w.strategy, beta=w.beta)
+        lsh = O.OutputLsh(spec, w.hidden, 0, w.n0, w.decay)
+        lsh.build(st.w2)
+        corpus = synthetic_corpus(w.corpus, (args.warmup + args.steps) * per_step, seed=1000)
+        trip = corpus.triples()
+        for it in range(1, args.warmup + 1):
+            O.train_step(st, lsh, trip[(it - 1) * per_step : it * per_step], it, 0, w.n_out, O.AdamCfg(lr=w.lr))
+        t0 = time.perf_counter()
+        for it in range(args.warmup + 1, args.warmup + args.steps + 1):
+            O.train_step(st, lsh, trip[(it - 1) * per_step : it * per_step], it, 0, w.n_out, O.AdamCfg(lr=w.lr))
+        dt = time.perf_counter() - t0
+    v = args.steps * per_step / dt
+    return {
+        "impl": "reference", "metric": "train samples/sec (LSH-sparse fwd+bwd+Adam), % of HBM roofline, 1/2/4/8 GPU",
+        "value": v, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (SURVEY 8(d) Zipf generator)",
+        "config": {"workload": w.name, "batch": w.batch, "schedule": "sequential (reference workers=1)",
+                   "sample": f"{per_step} samples per step (bounded)"},
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": 1, "kind": "port",
+                         "sample": f"{args.steps} steps x {per_step} samples of {w.name}, rebuild not reached"},
+        "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        print(json.dumps(run_reference(args, rank, world)), flush=True)
+        return
+    out, net, w = run_ours(args, rank, world)
+    if rank == 0:
+        if not args.no_cpu and world == 1:
+            rate, dt = cpu_port_rate(w, args.cpu_samples)
+            out["cpu_baseline"] = {"value": rate, "unit": "samples/s", "cores": 1, "kind": "port",
+                                   "sample": f"{args.cpu_samples} samples of {w.name}, sequential schedule, "
+                                             f"{dt:.1f} s, rebuild excluded"}
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

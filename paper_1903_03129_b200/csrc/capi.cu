@@ -1,0 +1,680 @@
+// extern "C" boundary (include/slide_b200.h) and the step orchestration.
+#include "../../include/slide_b200.h"
+#include "internal.cuh"
+#include "kernels.cuh"
+#include <cub/cub.cuh>
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+using namespace slide;
+
+namespace slide {
+unsigned long long g_slide_launches = 0;
+}
+
+// Per-stage CUDA-event timing (slide_profile): consecutive marks on the
+// stream, the interval ending at a mark is charged to that mark's stage.
+struct StageTimer {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<int> stage_of;
+  size_t used = 0;
+  double acc[32] = {0};
+  void mark(cudaStream_t s, int stage) {
+    if (!on) return;
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      SLIDE_CUDA(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    SLIDE_CUDA(cudaEventRecord(pool[used], s));
+    if (stage_of.size() <= used) stage_of.resize(used + 1);
+    stage_of[used++] = stage;
+  }
+  void collect() {
+    if (!used) return;
+    SLIDE_CUDA(cudaEventSynchronize(pool[used - 1]));
+    for (size_t k = 1; k < used; ++k) {
+      float ms = 0.f;
+      SLIDE_CUDA(cudaEventElapsedTime(&ms, pool[k - 1], pool[k]));
+      if (stage_of[k] >= 0) acc[stage_of[k]] += ms;
+    }
+    used = 0;
+  }
+};
+
+enum Stage {
+  kStStart = -1, kStHidden = 0, kStQueryHash, kStSlotRng, kStSelect, kStFallback, kStCompact, kStLogits,
+  kStSoftmax, kStHiddenGrad, kStGroupRows, kStAdamRows, kStHiddenCounts, kStGroupFeat, kStAdamFeat,
+  kStHiddenBias, kStRebuildHash, kStRebuildBuild
+};
+
+struct slide_ctx {
+  StageTimer timer;
+  DBuf counters;  // u64: 0 touched W2 coords, 1 touched W1 coords, 2 unique rows, 3 unique features
+  int64_t host_counts[8] = {0};  // 0 pairs, 1 nnz, 2 samples, 3 rebuilds, 4 fallback slots
+  slide_net_desc d{};
+  cudaStream_t s = nullptr;
+  int hp = 0;
+  TablesHost tab;
+  DBuf sh_packed, dw_perms, dw_donors, rowkeys;
+  // forward workspace
+  DBuf h, qkeys, order, states, act, cnt, empty, offs, prow, pslot, plab, z, prob, delta, loss, dh;
+  DBuf fb_ids, fb_scratch, fb_bitmap;
+  // backward workspace
+  DBuf iota, sk_out, sv_out, uniq, ucnt, uoff, nuniq, temp;
+  DBuf xslot, fkeys_out, fvals_out, funiq, fucnt, fuoff, fnuniq, tc, bc;
+  int64_t fb_bitmap_words = 0;
+  // last forward
+  bool have_forward = false;
+  int last_b = 0;
+  int64_t last_P = 0, last_nnz = 0, last_xbase = 0;
+  const int32_t* last_xptr = nullptr;
+  const int32_t* last_xidx = nullptr;
+  const float* last_xval = nullptr;
+  const int32_t* last_yptr = nullptr;
+  std::vector<int32_t> h_offs;
+};
+
+static thread_local std::string g_err;
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return kInternal;
+  }
+}
+
+static int bits_for(int64_t n) {
+  int b = 1;
+  while (b < 62 && ((int64_t)1 << b) < n) ++b;
+  return b;
+}
+
+static AdamParams adam_of(const slide_net_desc& d) {
+  AdamParams ap;
+  ap.lr = (float)d.lr;
+  ap.b1 = (float)d.beta1;
+  ap.b2 = (float)d.beta2;
+  ap.eps = (float)d.eps;
+  ap.b1d = d.beta1;
+  ap.b2d = d.beta2;
+  return ap;
+}
+
+static SimHashDev simhash_of(slide_ctx* c) {
+  SimHashDev f;
+  f.dim = (int)c->d.hidden;
+  f.k = (int)c->d.k;
+  f.l = (int)c->d.l;
+  f.c = (int)c->d.sh_c;
+  f.packed = c->sh_packed.as<uint16_t>();
+  return f;
+}
+
+static DwtaDev dwta_of(slide_ctx* c) {
+  DwtaDev f;
+  f.dim = (int)c->d.hidden;
+  f.k = (int)c->d.k;
+  f.l = (int)c->d.l;
+  f.m = (int)c->d.bin_size;
+  f.bins_per_perm = (int)c->d.bins_per_perm;
+  f.n_perms = (int)c->d.n_perms;
+  f.bits = (int)c->d.bits;
+  f.dense_mode = c->d.family == 3;
+  f.perms = c->dw_perms.as<int16_t>();
+  f.donors = c->dw_donors.as<int16_t>();
+  return f;
+}
+
+static void hash_rows(slide_ctx* c, const float* x, int64_t n, uint32_t* keys) {
+  if (c->d.family == 1) launch_simhash_keys(simhash_of(c), x, n, c->hp, keys, c->s);
+  else launch_dwta_keys(dwta_of(c), x, n, c->hp, keys, c->s);
+}
+
+extern "C" {
+
+const char* slide_version(void) { return "slide_b200 0.1.0 (sm_100a)"; }
+const char* slide_last_error(void) { return g_err.c_str(); }
+
+int slide_create(const slide_net_desc* desc, void* stream, slide_ctx** out) {
+  return guarded([&] {
+    SLIDE_CHECK(desc && out, kValueError, "null argument");
+    const slide_net_desc& d = *desc;
+    SLIDE_CHECK(d.hidden >= 1 && d.hidden_pad >= d.hidden && d.hidden_pad % 128 == 0, kValueError,
+                "hidden_pad must be a multiple of 128 >= hidden");
+    SLIDE_CHECK(d.n_out >= 1 && d.input_dim >= 1 && d.max_batch >= 1, kValueError, "dims must be positive");
+    SLIDE_CHECK(d.n_out < (1ll << 25), kNotSupported, "output width must be < 2^25 on the device path");
+    SLIDE_CHECK(d.family >= 0 && d.family <= 3, kValueError, "unknown hash family");
+    if (d.family) {
+      SLIDE_CHECK(d.key_bits >= 1 && d.key_bits <= 32, kNotSupported, "device keys are at most 32 bits");
+      SLIDE_CHECK(d.l >= 1 && d.l <= 64, kNotSupported, "at most 64 tables on the device path");
+    }
+    slide_ctx* c = new slide_ctx();
+    c->d = d;
+    c->s = (cudaStream_t)stream;
+    c->hp = (int)d.hidden_pad;
+    try {
+      if (d.family == 1) {
+        size_t n = (size_t)d.k * d.l * d.sh_c;
+        SLIDE_CHECK(d.sh_packed_host != nullptr, kValueError, "simhash projections missing");
+        SLIDE_CUDA(cudaMemcpy(c->sh_packed.ensure<uint16_t>(n), d.sh_packed_host, n * 2, cudaMemcpyHostToDevice));
+      } else if (d.family >= 2) {
+        size_t np = (size_t)d.n_perms * d.hidden, nd = (size_t)d.k * d.l * 100;
+        SLIDE_CHECK(d.dw_perms_host && d.dw_donors_host, kValueError, "dwta permutations missing");
+        SLIDE_CUDA(cudaMemcpy(c->dw_perms.ensure<int16_t>(np), d.dw_perms_host, np * 2, cudaMemcpyHostToDevice));
+        SLIDE_CUDA(cudaMemcpy(c->dw_donors.ensure<int16_t>(nd), d.dw_donors_host, nd * 2, cudaMemcpyHostToDevice));
+      }
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int slide_destroy(slide_ctx* c) {
+  return guarded([&] {
+    if (!c) return;
+    cudaStreamSynchronize(c->s);
+    c->tab.release();
+    for (DBuf* b : {&c->sh_packed, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->qkeys, &c->order,
+                    &c->states, &c->act, &c->cnt, &c->empty, &c->offs, &c->prow, &c->pslot, &c->plab, &c->z,
+                    &c->prob, &c->delta, &c->loss, &c->dh, &c->fb_ids, &c->fb_scratch, &c->fb_bitmap, &c->iota,
+                    &c->sk_out, &c->sv_out, &c->uniq, &c->ucnt, &c->uoff, &c->nuniq, &c->temp, &c->xslot,
+                    &c->fkeys_out, &c->fvals_out, &c->funiq, &c->fucnt, &c->fuoff, &c->fnuniq, &c->tc, &c->bc})
+      b->release();
+    delete c;
+  });
+}
+
+int slide_set_stream(slide_ctx* c, void* stream) {
+  return guarded([&] { c->s = (cudaStream_t)stream; });
+}
+
+// ------------------------------------------------------------------ hashing
+int slide_simhash_keys(const float* x, int64_t n, int64_t ld, int64_t dim, int64_t k, int64_t l, int64_t c,
+                       const uint16_t* packed_dev, uint32_t* keys, void* stream) {
+  return guarded([&] {
+    SLIDE_CHECK(k * 1 <= 32, kNotSupported, "device keys are at most 32 bits");
+    SLIDE_CHECK(dim <= 32767 && dim <= ld, kValueError, "simhash dim must be <= 32767 and <= ld");
+    SimHashDev f{(int)dim, (int)k, (int)l, (int)c, packed_dev};
+    launch_simhash_keys(f, x, n, (int)ld, keys, (cudaStream_t)stream);
+  });
+}
+
+int slide_dwta_keys(const float* x, int64_t n, int64_t ld, int64_t dim, int64_t k, int64_t l, int64_t m,
+                    int64_t bins_per_perm, int64_t n_perms, int64_t bits, int64_t dense_mode,
+                    const int16_t* perms_dev, const int16_t* donors_dev, uint32_t* keys, void* stream) {
+  return guarded([&] {
+    SLIDE_CHECK(k * bits <= 32, kNotSupported, "device keys are at most 32 bits");
+    SLIDE_CHECK(dim <= 32767 && dim <= ld && m <= 256, kValueError, "dwta dim must be <= 32767, bin <= 256");
+    DwtaDev f{(int)dim, (int)k, (int)l, (int)m, (int)bins_per_perm, (int)n_perms, (int)bits, (int)dense_mode,
+              perms_dev, donors_dev};
+    launch_dwta_keys(f, x, n, (int)ld, keys, (cudaStream_t)stream);
+  });
+}
+
+// ------------------------------------------------------------------- tables
+static void build_from_keys(slide_ctx* c, const uint32_t* keys, int64_t n, uint64_t* mt) {
+  SLIDE_CHECK(c->d.family != 0, kValueError, "layer has no LSH tables");
+  tables_build(c->tab, keys, n, (int)c->d.l, (int)c->d.key_bits, (int)c->d.capacity, (int)c->d.policy, mt, c->s);
+}
+
+int slide_rebuild_tables(slide_ctx* c, uint64_t* mt_state) {
+  return guarded([&] {
+    SLIDE_CHECK(c->d.family != 0, kValueError, "layer has no LSH tables");
+    const int64_t n = c->d.n_out;
+    uint32_t* keys = c->rowkeys.ensure<uint32_t>((size_t)n * c->d.l);
+    c->timer.mark(c->s, kStStart);
+    hash_rows(c, c->d.w2, n, keys);
+    c->timer.mark(c->s, kStRebuildHash);
+    build_from_keys(c, keys, n, mt_state);
+    c->timer.mark(c->s, kStRebuildBuild);
+    c->host_counts[3] += 1;
+  });
+}
+
+int slide_build_tables_from_keys(slide_ctx* c, const uint32_t* keys, int64_t n, uint64_t* mt_state) {
+  return guarded([&] { build_from_keys(c, keys, n, mt_state); });
+}
+
+int slide_clear_tables(slide_ctx* c) {
+  return guarded([&] {
+    c->tab.dev.empty = 1;
+    c->tab.dev.n_runs = 0;
+    c->tab.n_items = 0;
+    c->tab.built = false;
+  });
+}
+
+int slide_tables_info(slide_ctx* c, int64_t* n_buckets, int64_t* n_slots, int64_t* n_items) {
+  return guarded([&] {
+    *n_buckets = c->tab.dev.empty ? 0 : c->tab.dev.n_runs;
+    *n_slots = c->tab.dev.empty ? 0 : c->tab.n_slots;
+    *n_items = c->tab.n_items;
+  });
+}
+
+int slide_tables_load(slide_ctx* c, const uint32_t* skeys, const int32_t* counts, const int32_t* starts,
+                      const int32_t* lens, int64_t n_buckets, const int32_t* ids, int64_t n_slots, int64_t n_items) {
+  return guarded([&] {
+    SLIDE_CHECK(c->d.family != 0, kValueError, "layer has no LSH tables");
+    tables_load(c->tab, skeys, counts, starts, lens, n_buckets, ids, n_slots, n_items, (int)c->d.l,
+                (int)c->d.key_bits, (int)c->d.capacity, c->s);
+    c->tab.n_slots = n_slots;
+  });
+}
+
+int slide_tables_mask(slide_ctx* c, uint64_t disabled) {
+  return guarded([&] { c->tab.dev.disabled = disabled; });
+}
+
+int slide_tables_export(slide_ctx* c, uint32_t* skeys, int32_t* counts, int32_t* starts, int32_t* lens,
+                        int32_t* ids) {
+  return guarded([&] {
+    if (c->tab.dev.empty) return;
+    const int64_t r = c->tab.dev.n_runs, ns = c->tab.n_slots;
+    SLIDE_CUDA(cudaMemcpyAsync(skeys, c->tab.uniq.p, r * 4, cudaMemcpyDeviceToHost, c->s));
+    SLIDE_CUDA(cudaMemcpyAsync(counts, c->tab.dev.bcount, r * 4, cudaMemcpyDeviceToHost, c->s));
+    SLIDE_CUDA(cudaMemcpyAsync(starts, c->tab.dev.bstart, r * 4, cudaMemcpyDeviceToHost, c->s));
+    SLIDE_CUDA(cudaMemcpyAsync(lens, c->tab.dev.blen, r * 4, cudaMemcpyDeviceToHost, c->s));
+    SLIDE_CUDA(cudaMemcpyAsync(ids, c->tab.dev.ids, ns * 4, cudaMemcpyDeviceToHost, c->s));
+    SLIDE_CUDA(cudaStreamSynchronize(c->s));
+  });
+}
+
+__global__ void probe_kernel(TablesDev t, const uint32_t* keys, int64_t b, int32_t* starts, int32_t* lens) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= b * t.l) return;
+  int tt = (int)(q % t.l);
+  int run = tables_lookup(t, ((uint32_t)tt << t.key_bits) | keys[q]);
+  starts[q] = run >= 0 ? t.bstart[run] : 0;
+  lens[q] = run >= 0 ? t.blen[run] : 0;
+}
+
+int slide_tables_probe(slide_ctx* c, const uint32_t* keys, int64_t b, int32_t* starts, int32_t* lens) {
+  return guarded([&] {
+    TablesDev t = c->tab.dev;
+    t.l = (int)c->d.l;
+    t.key_bits = (int)c->d.key_bits;
+    int64_t n = b * t.l;
+    if (n <= 0) return;
+    probe_kernel<<<(int)ceil_div(n, 256), 256, 0, c->s>>>(t, keys, b, starts, lens);
+    SLIDE_LAUNCH_CHECK();
+  });
+}
+
+// --------------------------------------------------------------------- step
+static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration, int64_t slot_offset,
+                         int64_t* n_pairs) {
+  const slide_net_desc& d = c->d;
+  SLIDE_CHECK(d.w1t && d.w2, kValueError, "context has no network state");
+  const int b = (int)bt->batch;
+  SLIDE_CHECK(b >= 1 && b <= 1024, kValueError, "batch must hold 1..1024 slots");
+  const int hp = c->hp, L = (int)d.l;
+  cudaStream_t s = c->s;
+  const int64_t x_base = bt->x_ptr_host[0];
+  const int64_t nnz = bt->x_ptr_host[b] - x_base;
+  int max_labels = 0;
+  for (int i = 0; i < b; ++i) max_labels = std::max(max_labels, bt->y_ptr_host[i + 1] - bt->y_ptr_host[i]);
+
+  float* h = c->h.ensure<float>((size_t)b * hp);
+  c->timer.mark(s, kStStart);
+  launch_hidden_forward(hp, b, bt->x_ptr, bt->x_idx, bt->x_val, d.w1t, d.b1, h, s);
+  c->timer.mark(s, kStHidden);
+  c->host_counts[1] += nnz;
+  c->host_counts[2] += b;
+
+  int32_t* cnt = c->cnt.ensure<int32_t>(b);
+  int32_t* empty = c->empty.ensure<int32_t>(b);
+  int64_t cap_max;
+  int32_t* act;
+  if (bt->forced_ptr || d.family == 0) {
+    int64_t m = d.n_out;
+    if (bt->forced_ptr) {
+      m = 0;
+      for (int i = 0; i < b; ++i) m = std::max<int64_t>(m, bt->forced_ptr_host[i + 1] - bt->forced_ptr_host[i]);
+    }
+    cap_max = std::max<int64_t>(m, 1);
+    act = c->act.ensure<int32_t>((size_t)b * cap_max);
+    launch_explicit_active(b, d.n_out, bt->forced_ptr, bt->forced_idx, bt->y_ptr, bt->y_idx, cap_max, act, cnt,
+                           empty, s);
+    c->timer.mark(s, kStSelect);
+  } else {
+    uint32_t* qk = c->qkeys.ensure<uint32_t>((size_t)b * L);
+    hash_rows(c, h, b, qk);
+    c->timer.mark(s, kStQueryHash);
+    uint64_t* states = c->states.ensure<uint64_t>((size_t)b * 6);
+    uint8_t* order = c->order.ensure<uint8_t>((size_t)b * L);
+    const int vanilla = d.strategy == 0;
+    launch_slot_rng(b, d.seed, iteration, slot_offset, L, vanilla, bt->rng_states, states, order, s);
+    c->timer.mark(s, kStSlotRng);
+    const int64_t want = std::min<int64_t>(d.beta, d.n_out);
+    const int64_t lcap = (int64_t)L * d.capacity;
+    cap_max = std::max<int64_t>(lcap, want) + max_labels;
+    act = c->act.ensure<int32_t>((size_t)b * cap_max);
+    SelectArgs a;
+    a.tab = c->tab.dev;
+    if (!c->tab.built) a.tab.empty = 1;
+    a.tab.l = L;
+    a.tab.key_bits = (int)d.key_bits;
+    a.qkeys = qk;
+    a.order = order;
+    a.y_ptr = bt->y_ptr;
+    a.y_idx = bt->y_idx;
+    a.b = b;
+    a.l = L;
+    a.strategy = (int)d.strategy;
+    a.beta = (int)std::min<int64_t>(d.beta, INT32_MAX);
+    a.min_freq = (int)d.min_freq;
+    a.sort_bits = bits_for(d.n_out) + 7;
+    a.cap_max = cap_max;
+    a.act = act;
+    a.cnt = cnt;
+    a.empty = empty;
+    a.cand_ctr = c->timer.on ? c->counters.as<unsigned long long>() + 4 : nullptr;
+    launch_select(a, (int)(lcap + max_labels), s);
+    c->timer.mark(s, kStSelect);
+    // fallback for slots whose sampler returned nothing
+    FallbackArgs f;
+    f.empty = empty;
+    f.states = states;
+    f.n = d.n_out;
+    f.want = want;
+    f.fb_ids = c->fb_ids.ensure<int64_t>((size_t)b * want);
+    f.scratch_per_slot = choice_scratch_entries(d.n_out, want);
+    f.smem_scratch = f.scratch_per_slot * 8 <= 96 * 1024;
+    f.scratch = f.smem_scratch ? nullptr : c->fb_scratch.ensure<int64_t>((size_t)b * f.scratch_per_slot);
+    f.words = ceil_div(d.n_out, 32);
+    if (c->fb_bitmap_words < (int64_t)b * f.words) {
+      uint32_t* bm = c->fb_bitmap.ensure<uint32_t>((size_t)b * f.words);
+      SLIDE_CUDA(cudaMemsetAsync(bm, 0, (size_t)b * f.words * 4, s));
+      c->fb_bitmap_words = (int64_t)b * f.words;
+    }
+    f.bitmap = c->fb_bitmap.as<uint32_t>();
+    f.y_ptr = bt->y_ptr;
+    f.y_idx = bt->y_idx;
+    f.cap_max = cap_max;
+    f.act = act;
+    f.cnt = cnt;
+    launch_fallback(f, b, s);
+    if (bt->rng_states)
+      SLIDE_CUDA(cudaMemcpyAsync(bt->rng_states, states, (size_t)b * 48, cudaMemcpyDeviceToDevice, s));
+    c->timer.mark(s, kStFallback);
+  }
+  int32_t* offs = c->offs.ensure<int32_t>(b + 1);
+  launch_offsets(b, cnt, offs, s);
+  c->h_offs.resize(b + 1);
+  SLIDE_CUDA(cudaMemcpyAsync(c->h_offs.data(), offs, (b + 1) * 4, cudaMemcpyDeviceToHost, s));
+  SLIDE_CUDA(cudaStreamSynchronize(s));
+  const int64_t P = c->h_offs[b];
+  int32_t* prow = c->prow.ensure<int32_t>(P);
+  int32_t* pslot = c->pslot.ensure<int32_t>(P);
+  uint8_t* plab = c->plab.ensure<uint8_t>(P);
+  launch_pairs(b, act, cap_max, offs, prow, pslot, plab, s);
+  c->timer.mark(s, kStCompact);
+  c->host_counts[0] += P;
+  float* z = c->z.ensure<float>(P);
+  float* prob = c->prob.ensure<float>(P);
+  float* delta = c->delta.ensure<float>(P);
+  double* loss = c->loss.ensure<double>(b);
+  launch_logits(hp, P, prow, pslot, d.w2, d.b2, h, z, s);
+  c->timer.mark(s, kStLogits);
+  launch_softmax(b, offs, plab, bt->y_ptr, z, prob, delta, loss, s);
+  c->timer.mark(s, kStSoftmax);
+  c->have_forward = true;
+  c->last_b = b;
+  c->last_P = P;
+  c->last_nnz = nnz;
+  c->last_xbase = x_base;
+  c->last_xptr = bt->x_ptr;
+  c->last_xidx = bt->x_idx;
+  c->last_xval = bt->x_val;
+  c->last_yptr = bt->y_ptr;
+  if (n_pairs) *n_pairs = P;
+}
+
+__global__ void iota_kernel(int32_t* a, int64_t n) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    a[q] = (int32_t)q;
+}
+
+// stable group-by: keys (n) -> uniq keys, per-key count, segment offsets,
+// and the original positions sorted by key (ties keep their order)
+static void group_by(slide_ctx* c, const int32_t* keys, int64_t n, int key_bits, DBuf& keys_out, DBuf& vals_out,
+                     DBuf& uniq, DBuf& ucnt, DBuf& uoff, DBuf& nuniq) {
+  cudaStream_t s = c->s;
+  int32_t* io = c->iota.ensure<int32_t>(n);
+  iota_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), kSms * 16), 256, 0, s>>>(io, n);
+  SLIDE_LAUNCH_CHECK();
+  int32_t* ko = keys_out.ensure<int32_t>(n);
+  int32_t* vo = vals_out.ensure<int32_t>(n);
+  int32_t* u = uniq.ensure<int32_t>(n);
+  int32_t* uc = ucnt.ensure<int32_t>(n);
+  int32_t* uo = uoff.ensure<int32_t>(n);
+  int32_t* nu = nuniq.ensure<int32_t>(1);
+  size_t b1 = 0, b2 = 0, b3 = 0;
+  const uint32_t* uk = reinterpret_cast<const uint32_t*>(keys);
+  uint32_t* uko = reinterpret_cast<uint32_t*>(ko);
+  SLIDE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, uk, uko, io, vo, (int)n, 0, key_bits, s));
+  SLIDE_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, b2, ko, u, uc, nu, (int)n, s));
+  SLIDE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b3, uc, uo, (int)n, s));
+  size_t tb = std::max(b1, std::max(b2, b3));
+  void* t = c->temp.ensure<uint8_t>(tb);
+  SLIDE_CUDA(cub::DeviceRadixSort::SortPairs(t, tb, uk, uko, io, vo, (int)n, 0, key_bits, s));
+  SLIDE_CUDA(cub::DeviceRunLengthEncode::Encode(t, tb, ko, u, uc, nu, (int)n, s));
+  SLIDE_CUDA(cub::DeviceScan::ExclusiveSum(t, tb, uc, uo, (int)n, s));
+}
+
+static void backward_impl(slide_ctx* c, int64_t update) {
+  SLIDE_CHECK(c->have_forward, kValueError, "backward needs a forward first");
+  const slide_net_desc& d = c->d;
+  const int b = c->last_b, hp = c->hp;
+  const int64_t P = c->last_P;
+  cudaStream_t s = c->s;
+  float* dh = c->dh.ensure<float>((size_t)b * hp);
+  launch_hidden_grad(hp, b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->delta.as<float>(), d.w2,
+                     c->h.as<float>(), dh, s);
+  c->timer.mark(s, kStHiddenGrad);
+  if (!update) return;
+  const AdamParams ap = adam_of(d);
+  unsigned long long* ctr = c->timer.on ? c->counters.as<unsigned long long>() : nullptr;
+  // W2: group the pairs by output row, slot order kept inside a row
+  if (P > 0) {
+    group_by(c, c->prow.as<int32_t>(), P, bits_for(d.n_out), c->sk_out, c->sv_out, c->uniq, c->ucnt, c->uoff,
+             c->nuniq);
+    c->timer.mark(s, kStGroupRows);
+    launch_adam_rows(hp, ap, c->nuniq.as<int32_t>(), P, c->uniq.as<int32_t>(), c->uoff.as<int32_t>(),
+                     c->ucnt.as<int32_t>(), c->sv_out.as<int32_t>(), c->pslot.as<int32_t>(), c->delta.as<float>(),
+                     c->h.as<float>(), d.w2, d.m2, d.v2, d.b2, d.mb2, d.vb2, d.steps2, ctr, s);
+    c->timer.mark(s, kStAdamRows);
+  }
+  // W1: group the (feature, slot) inputs by feature
+  int32_t* tc = c->tc.ensure<int32_t>((size_t)b * hp);
+  float2* bc = c->bc.ensure<float2>((size_t)b * hp);
+  launch_hidden_counts(hp, b, ap, c->h.as<float>(), d.steps1, tc, bc, s);
+  c->timer.mark(s, kStHiddenCounts);
+  const int64_t nnz = c->last_nnz;
+  if (nnz > 0) {
+    int32_t* xs = c->xslot.ensure<int32_t>(nnz);
+    launch_x_slots(b, c->last_xptr, xs, s);
+    group_by(c, c->last_xidx + c->last_xbase, nnz, bits_for(d.input_dim), c->fkeys_out, c->fvals_out, c->funiq,
+             c->fucnt, c->fuoff, c->fnuniq);
+    c->timer.mark(s, kStGroupFeat);
+    launch_adam_features(hp, ap, c->fnuniq.as<int32_t>(), nnz, c->funiq.as<int32_t>(), c->fuoff.as<int32_t>(),
+                         c->fucnt.as<int32_t>(), c->fvals_out.as<int32_t>(), xs, c->last_xval, c->last_xbase,
+                         c->h.as<float>(), dh, bc, d.w1t, d.m1t, d.v1t, ctr ? ctr + 1 : nullptr, s);
+    c->timer.mark(s, kStAdamFeat);
+  }
+  launch_adam_hidden_bias(hp, b, ap, c->h.as<float>(), dh, tc, bc, d.b1, d.mb1, d.vb1, d.steps1, s);
+  c->timer.mark(s, kStHiddenBias);
+  if (ctr) {
+    launch_accumulate(ctr + 2, P > 0 ? c->nuniq.as<int32_t>() : nullptr, s);
+    launch_accumulate(ctr + 3, nnz > 0 ? c->fnuniq.as<int32_t>() : nullptr, s);
+  }
+}
+
+int slide_forward(slide_ctx* c, const slide_batch* bt, int64_t iteration, int64_t slot_offset, int64_t* n_pairs) {
+  return guarded([&] { forward_impl(c, bt, iteration, slot_offset, n_pairs); });
+}
+
+int slide_backward(slide_ctx* c, int64_t update) {
+  return guarded([&] { backward_impl(c, update); });
+}
+
+int slide_train_batch(slide_ctx* c, const slide_batch* bt, int64_t iteration, int64_t sub_batch, double* loss_host,
+                      int64_t* active_host) {
+  return guarded([&] {
+    const int64_t B = bt->batch;
+    SLIDE_CHECK(B >= 1, kValueError, "batch is empty");
+    SLIDE_CHECK(sub_batch >= 1, kValueError, "sub_batch must be >= 1");
+    for (int64_t s0 = 0; s0 < B; s0 += sub_batch) {
+      const int64_t nb = std::min<int64_t>(sub_batch, B - s0);
+      slide_batch v = *bt;
+      v.batch = nb;
+      v.x_ptr = bt->x_ptr + s0;
+      v.y_ptr = bt->y_ptr + s0;
+      v.x_ptr_host = bt->x_ptr_host + s0;
+      v.y_ptr_host = bt->y_ptr_host + s0;
+      if (bt->rng_states) v.rng_states = bt->rng_states + 6 * s0;
+      if (bt->forced_ptr) {
+        v.forced_ptr = bt->forced_ptr + s0;
+        v.forced_ptr_host = bt->forced_ptr_host + s0;
+      }
+      forward_impl(c, &v, iteration, s0, nullptr);
+      backward_impl(c, 1);
+      if (loss_host)
+        SLIDE_CUDA(cudaMemcpyAsync(loss_host + s0, c->loss.p, nb * 8, cudaMemcpyDeviceToHost, c->s));
+      if (active_host)
+        for (int64_t i = 0; i < nb; ++i) active_host[s0 + i] = c->h_offs[i + 1] - c->h_offs[i];
+    }
+    SLIDE_CUDA(cudaStreamSynchronize(c->s));
+  });
+}
+
+int slide_read(slide_ctx* c, int64_t what, void* dst, int64_t max_bytes, int64_t* bytes) {
+  return guarded([&] {
+    SLIDE_CHECK(c->have_forward, kValueError, "nothing to read before a forward");
+    const int64_t b = c->last_b, P = c->last_P, hp = c->hp, L = c->d.l;
+    const void* src = nullptr;
+    int64_t n = 0;
+    switch (what) {
+      case 0: src = c->h.p; n = b * hp * 4; break;
+      case 1: src = c->qkeys.p; n = b * L * 4; break;
+      case 2: src = c->offs.p; n = (b + 1) * 4; break;
+      case 3: src = c->prow.p; n = P * 4; break;
+      case 4: src = c->plab.p; n = P; break;
+      case 5: src = c->prob.p; n = P * 4; break;
+      case 6: src = c->delta.p; n = P * 4; break;
+      case 7: src = c->loss.p; n = b * 8; break;
+      case 8: src = c->dh.p; n = b * hp * 4; break;
+      case 9: src = c->empty.p; n = b * 4; break;
+      case 10: src = c->states.p; n = b * 48; break;
+      case 11: src = c->z.p; n = P * 4; break;
+      default: throw Error(kValueError, "unknown stage");
+    }
+    SLIDE_CHECK(src != nullptr || n == 0, kValueError, "stage not computed");
+    SLIDE_CHECK(n <= max_bytes, kValueError, "destination too small");
+    if (n) SLIDE_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, c->s));
+    SLIDE_CUDA(cudaStreamSynchronize(c->s));
+    if (bytes) *bytes = n;
+  });
+}
+
+int slide_launch_count(uint64_t* out) {
+  return guarded([&] { *out = g_slide_launches; });
+}
+
+int slide_profile(slide_ctx* c, int64_t on) {
+  return guarded([&] {
+    c->timer.collect();
+    c->timer.on = on != 0;
+    for (double& a : c->timer.acc) a = 0.0;
+    for (int64_t& h : c->host_counts) h = 0;
+    unsigned long long* ctr = c->counters.ensure<unsigned long long>(8);
+    SLIDE_CUDA(cudaMemsetAsync(ctr, 0, 64, c->s));
+    SLIDE_CUDA(cudaStreamSynchronize(c->s));
+  });
+}
+
+int slide_profile_read(slide_ctx* c, double* stage_ms, int64_t* counts) {
+  return guarded([&] {
+    c->timer.collect();
+    for (int k = 0; k < 32; ++k) stage_ms[k] = c->timer.acc[k];
+    unsigned long long dev[8] = {0};
+    if (c->counters.p) SLIDE_CUDA(cudaMemcpy(dev, c->counters.p, 64, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 8; ++k) counts[k] = (int64_t)dev[k];
+    for (int k = 0; k < 8; ++k) counts[8 + k] = c->host_counts[k];
+  });
+}
+
+int slide_write(slide_ctx* c, int64_t what, const void* src, int64_t bytes) {
+  return guarded([&] {
+    SLIDE_CHECK(c->have_forward, kValueError, "nothing to overwrite before a forward");
+    void* dst = nullptr;
+    int64_t n = 0;
+    if (what == 0) {
+      dst = c->h.p;
+      n = (int64_t)c->last_b * c->hp * 4;
+    } else if (what == 6) {
+      dst = c->delta.p;
+      n = c->last_P * 4;
+    } else {
+      throw Error(kValueError, "only h (0) and delta (6) can be written");
+    }
+    SLIDE_CHECK(bytes == n, kValueError, "size mismatch for stage write");
+    if (n) SLIDE_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, c->s));
+    SLIDE_CUDA(cudaStreamSynchronize(c->s));
+  });
+}
+
+// ------------------------------------------------------------ host streams
+int slide_pcg64_seed(const uint64_t* ent, int64_t n_ent, uint64_t* state6) {
+  return guarded([&] {
+    SLIDE_CHECK(n_ent >= 1 && n_ent <= 8, kValueError, "1..8 entropy words");
+    Pcg64 g;
+    g.seed_from(ent, (int)n_ent);
+    g.store(state6);
+  });
+}
+
+int slide_pcg64_permutation(uint64_t* state6, int64_t n, int64_t* out) {
+  return guarded([&] {
+    Pcg64 g;
+    g.load(state6);
+    pcg_permutation(g, out, (int)n);
+    g.store(state6);
+  });
+}
+
+int slide_pcg64_choice(uint64_t* state6, int64_t pop, int64_t size, int64_t* out) {
+  return guarded([&] {
+    SLIDE_CHECK(size >= 0 && size <= pop, kValueError,
+                "Cannot take a larger sample than population when replace is False");
+    Pcg64 g;
+    g.load(state6);
+    std::vector<int64_t> scratch((size_t)std::max<int64_t>(choice_scratch_entries(pop, size), 1));
+    pcg_choice(g, pop, size, out, scratch.data());
+    g.store(state6);
+  });
+}
+
+int slide_mt19937_random(uint64_t* state625, int64_t n, double* out) {
+  return guarded([&] {
+    Mt19937 mt;
+    mt.load(state625);
+    for (int64_t q = 0; q < n; ++q) out[q] = mt.random();
+    mt.store(state625);
+  });
+}
+
+}  // extern "C"

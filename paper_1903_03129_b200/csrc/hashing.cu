@@ -1,0 +1,161 @@
+// LSH hash kernels: SimHash (reference hashing.py:121-178) and
+// DWTA / WTA (hashing.py:196-287).  One kernel serves both the per-sample
+// queries (x = hidden activations, B rows) and the table rebuild (x = W2,
+// N rows): rows are staged in shared memory, the projection / permutation
+// tables stay resident in shared memory for the whole (grid-stride) launch.
+#include "internal.cuh"
+#include <algorithm>
+
+namespace slide {
+
+// ---------------------------------------------------------------- SimHash
+// bit = [sum_j sign_j * x[idx_j] > 0] (sign(0) -> 0, hashing.py:169).  The
+// sum is taken in fp64 over fp32 inputs: exact whenever the c terms span
+// < 2^23 in magnitude, so the sign equals the reference's f64 sign.
+template <int ROWS>
+__global__ void __launch_bounds__(256) simhash_kernel(SimHashDev f, const float* __restrict__ x,
+                                                      int64_t n, int ld, uint32_t* __restrict__ keys) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int KL = f.k * f.l;
+  float* xs = reinterpret_cast<float*>(sm);
+  uint16_t* proj = reinterpret_cast<uint16_t*>(xs + ROWS * f.dim);  // (c, KL)
+  uint8_t* bits = reinterpret_cast<uint8_t*>(proj + ((KL * f.c + 1) & ~1));
+  for (int q = threadIdx.x; q < KL * f.c; q += blockDim.x) {
+    int p = q / f.c, j = q - p * f.c;
+    proj[j * KL + p] = f.packed[q];
+  }
+  for (int64_t row0 = (int64_t)blockIdx.x * ROWS; row0 < n; row0 += (int64_t)gridDim.x * ROWS) {
+    const int nr = (int)(n - row0 < ROWS ? n - row0 : ROWS);
+    __syncthreads();
+    for (int q = threadIdx.x; q < ROWS * f.dim; q += blockDim.x) {
+      int r = q / f.dim, c = q - r * f.dim;
+      xs[q] = r < nr ? x[(row0 + r) * ld + c] : 0.f;
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < KL; p += blockDim.x) {
+      double acc[ROWS];
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) acc[r] = 0.0;
+      for (int j = 0; j < f.c; ++j) {
+        uint16_t e = proj[j * KL + p];
+        int idx = e & 0x7fff;
+        bool neg = e >> 15;
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+          double v = (double)xs[r * f.dim + idx];
+          acc[r] += neg ? -v : v;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) bits[r * KL + p] = acc[r] > 0.0;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nr * f.l; q += blockDim.x) {
+      int r = q / f.l, t = q - r * f.l;
+      const uint8_t* b = bits + r * KL + t * f.k;
+      uint32_t key = 0;
+      for (int kk = 0; kk < f.k; ++kk) key |= (uint32_t)b[kk] << kk;
+      keys[(row0 + r) * f.l + t] = key;
+    }
+  }
+}
+
+void launch_simhash_keys(const SimHashDev& f, const float* x, int64_t n, int ld, uint32_t* keys,
+                         cudaStream_t s) {
+  if (n <= 0) return;
+  constexpr int ROWS = 8;
+  const int KL = f.k * f.l;
+  size_t smem = (size_t)ROWS * f.dim * 4 + (size_t)((KL * f.c + 1) & ~1) * 2 + (size_t)ROWS * KL;
+  SLIDE_CHECK(smem <= 227 * 1024, kNotSupported, "simhash tables too large for shared memory");
+  SLIDE_CUDA(cudaFuncSetAttribute(simhash_kernel<ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  int64_t blocks = ceil_div(n, ROWS);
+  int grid = (int)std::min<int64_t>(blocks, (int64_t)kSms * 4);
+  simhash_kernel<ROWS><<<grid, 256, smem, s>>>(f, x, n, ld, keys);
+  SLIDE_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------------- DWTA
+// Global bin g: permutation g / bins_per_perm, bin g % bins_per_perm, the m
+// dims perms[q][b*m .. b*m+m) (ragged last bin).  Winner = largest value,
+// ties to the smallest in-bin offset; only nonzeros take part unless
+// dense_mode (WTA, hashing.py:262-274).  Empty bins copy the code of the
+// first occupied donor mix(salt, g, a) % KL, a = 1..100, else 0
+// (hashing.py:219-231).  key_t = sum_k code[t*K+k] << (bits*k).
+template <int ROWS>
+__global__ void __launch_bounds__(256) dwta_kernel(DwtaDev f, const float* __restrict__ x, int64_t n,
+                                                   int ld, uint32_t* __restrict__ keys) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int KL = f.k * f.l;
+  float* xs = reinterpret_cast<float*>(sm);
+  int16_t* perm = reinterpret_cast<int16_t*>(xs + ROWS * f.dim);
+  uint8_t* codes = reinterpret_cast<uint8_t*>(perm + ((f.n_perms * f.dim + 1) & ~1));
+  uint8_t* occ = codes + ROWS * KL;
+  for (int q = threadIdx.x; q < f.n_perms * f.dim; q += blockDim.x) perm[q] = f.perms[q];
+  for (int64_t row0 = (int64_t)blockIdx.x * ROWS; row0 < n; row0 += (int64_t)gridDim.x * ROWS) {
+    const int nr = (int)(n - row0 < ROWS ? n - row0 : ROWS);
+    __syncthreads();
+    for (int q = threadIdx.x; q < ROWS * f.dim; q += blockDim.x) {
+      int r = q / f.dim, c = q - r * f.dim;
+      xs[q] = r < nr ? x[(row0 + r) * ld + c] : 0.f;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < ROWS * KL; q += blockDim.x) {
+      int r = q / KL, g = q - r * KL;
+      int pq = g / f.bins_per_perm, b = g - pq * f.bins_per_perm;
+      int lo = b * f.m, hi = min(lo + f.m, f.dim);
+      const int16_t* pp = perm + pq * f.dim;
+      const float* xr = xs + r * f.dim;
+      float best = 0.f;
+      int code = 0, oc = 0;
+      for (int o = 0; o < hi - lo; ++o) {
+        float v = xr[pp[lo + o]];
+        if ((f.dense_mode || v != 0.f) && (!oc || v > best)) {
+          best = v;
+          code = o;
+          oc = 1;
+        }
+      }
+      codes[q] = (uint8_t)code;
+      occ[q] = (uint8_t)oc;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < ROWS * KL; q += blockDim.x) {
+      if (occ[q]) continue;
+      int r = q / KL, g = q - r * KL;
+      int code = 0;
+      for (int a = 0; a < 100; ++a) {
+        int d = f.donors[g * 100 + a];
+        if (occ[r * KL + d]) {
+          code = codes[r * KL + d];
+          break;
+        }
+      }
+      codes[q] = (uint8_t)code;  // only empty bins are written; donors are occupied
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nr * f.l; q += blockDim.x) {
+      int r = q / f.l, t = q - r * f.l;
+      const uint8_t* cc = codes + r * KL + t * f.k;
+      uint32_t key = 0;
+      for (int kk = 0; kk < f.k; ++kk) key |= (uint32_t)cc[kk] << (f.bits * kk);
+      keys[(row0 + r) * f.l + t] = key;
+    }
+  }
+}
+
+void launch_dwta_keys(const DwtaDev& f, const float* x, int64_t n, int ld, uint32_t* keys,
+                      cudaStream_t s) {
+  if (n <= 0) return;
+  constexpr int ROWS = 8;
+  const int KL = f.k * f.l;
+  size_t smem = (size_t)ROWS * f.dim * 4 + (size_t)((f.n_perms * f.dim + 1) & ~1) * 2 + (size_t)2 * ROWS * KL;
+  SLIDE_CHECK(smem <= 227 * 1024, kNotSupported, "dwta tables too large for shared memory");
+  SLIDE_CUDA(cudaFuncSetAttribute(dwta_kernel<ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int64_t blocks = ceil_div(n, ROWS);
+  int grid = (int)std::min<int64_t>(blocks, (int64_t)kSms * 4);
+  dwta_kernel<ROWS><<<grid, 256, smem, s>>>(f, x, n, ld, keys);
+  SLIDE_LAUNCH_CHECK();
+}
+
+}  // namespace slide

@@ -1,0 +1,80 @@
+// Kernel argument blocks and launchers of the training step.
+#pragma once
+#include "internal.cuh"
+
+namespace slide {
+
+struct SelectArgs {
+  TablesDev tab;
+  const uint32_t* qkeys;  // (B, L) query keys
+  const uint8_t* order;   // (B, L) vanilla probe order
+  const int32_t* y_ptr;
+  const int32_t* y_idx;
+  int b, l, strategy, beta, min_freq, sort_bits;
+  int64_t cap_max;
+  int32_t* act;
+  int32_t* cnt;
+  int32_t* empty;
+  unsigned long long* cand_ctr;  // optional: total probed bucket slots
+};
+
+struct FallbackArgs {
+  const int32_t* empty;
+  uint64_t* states;
+  int64_t n, want;
+  int64_t* fb_ids;
+  int64_t* scratch;
+  int64_t scratch_per_slot;
+  int smem_scratch;
+  uint32_t* bitmap;
+  int64_t words;
+  const int32_t* y_ptr;
+  const int32_t* y_idx;
+  int64_t cap_max;
+  int32_t* act;
+  int32_t* cnt;
+};
+
+void launch_slot_rng(int b, uint64_t seed, int64_t it, int64_t off, int l, int vanilla, const uint64_t* ext,
+                     uint64_t* states, uint8_t* order, cudaStream_t s);
+void launch_select(const SelectArgs& a, int max_candidates, cudaStream_t s);
+void launch_fallback(const FallbackArgs& a, int b, cudaStream_t s);
+void launch_explicit_active(int b, int64_t n, const int32_t* fptr, const int32_t* fidx, const int32_t* y_ptr,
+                            const int32_t* y_idx, int64_t cap_max, int32_t* act, int32_t* cnt, int32_t* empty,
+                            cudaStream_t s);
+void launch_offsets(int b, const int32_t* cnt, int32_t* offs, cudaStream_t s);
+void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* offs, int32_t* prow, int32_t* pslot,
+                  uint8_t* plab, cudaStream_t s);
+
+// ------------------------------------------------------------------ layers
+struct AdamParams {
+  float lr, b1, b2, eps;
+  double b1d, b2d;
+};
+
+void launch_hidden_forward(int hp, int b, const int32_t* x_ptr, const int32_t* x_idx, const float* x_val,
+                           const float* w1t, const float* b1, float* h, cudaStream_t s);
+void launch_logits(int hp, int64_t p, const int32_t* prow, const int32_t* pslot, const float* w2, const float* b2,
+                   const float* h, float* z, cudaStream_t s);
+void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
+                    float* prob, float* delta, double* loss, cudaStream_t s);
+void launch_hidden_grad(int hp, int b, const int32_t* offs, const int32_t* prow, const float* delta, const float* w2,
+                        const float* h, float* dh, cudaStream_t s);
+void launch_adam_rows(int hp, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq, const int32_t* uniq,
+                      const int32_t* seg_off, const int32_t* seg_cnt, const int32_t* sorted_pairs,
+                      const int32_t* pslot, const float* delta, const float* h, float* w2, float* m2, float* v2,
+                      float* b2, float* mb2, float* vb2, int64_t* steps2, unsigned long long* touched,
+                      cudaStream_t s);
+void launch_accumulate(unsigned long long* dst, const int32_t* src, cudaStream_t s);
+void launch_x_slots(int b, const int32_t* x_ptr, int32_t* x_slot, cudaStream_t s);
+void launch_hidden_counts(int hp, int b, const AdamParams& ap, const float* h, const int64_t* steps1, int32_t* tc,
+                          float2* bc, cudaStream_t s);
+void launch_adam_features(int hp, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq,
+                          const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
+                          const int32_t* sorted_k, const int32_t* x_slot, const float* x_val, int64_t x_base,
+                          const float* h, const float* dh, const float2* bc, float* w1t, float* m1t, float* v1t,
+                          unsigned long long* touched, cudaStream_t s);
+void launch_adam_hidden_bias(int hp, int b, const AdamParams& ap, const float* h, const float* dh, const int32_t* tc,
+                             const float2* bc, float* b1, float* mb1, float* vb1, int64_t* steps1, cudaStream_t s);
+
+}  // namespace slide

@@ -1,0 +1,549 @@
+// Sparse forward / backward / Adam kernels (reference network.py:241-336,
+// 428-451).  Row layout: every weight row (a W1^T feature row, a W2 output
+// row) is hp floats, hp a multiple of 128, so one warp moves a row with one
+// 128-bit load per lane per 128 columns (NV = hp / 128).
+#include "internal.cuh"
+#include "kernels.cuh"
+#include <cub/cub.cuh>
+
+namespace slide {
+
+__device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ float4 ld4_cg(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float& comp(float4& v, int q) { return reinterpret_cast<float*>(&v)[q]; }
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+#define SLIDE_NV_DISPATCH(hp, KERNEL_CALL)                                                        \
+  switch ((hp) / 128) {                                                                           \
+    case 1: { constexpr int NV = 1; KERNEL_CALL; } break;                                         \
+    case 2: { constexpr int NV = 2; KERNEL_CALL; } break;                                         \
+    case 4: { constexpr int NV = 4; KERNEL_CALL; } break;                                         \
+    case 8: { constexpr int NV = 8; KERNEL_CALL; } break;                                         \
+    default: throw Error(kNotSupported, "padded hidden width must be 128, 256, 512 or 1024");     \
+  }
+
+// ------------------------------------------------------------ hidden forward
+// z1 = sum_f x_f W1^T[f, :] + b1, h = max(z1, 0) (network.py:262-280).  One
+// CTA per sample, 8 warps each own every 8th nonzero; partial sums are added
+// in warp order (deterministic).
+template <int NV>
+__global__ void __launch_bounds__(256) hidden_fwd_kernel(int hp, const int32_t* __restrict__ x_ptr,
+                                                         const int32_t* __restrict__ x_idx,
+                                                         const float* __restrict__ x_val,
+                                                         const float* __restrict__ w1t,
+                                                         const float* __restrict__ b1, float* __restrict__ h) {
+  __shared__ float red[8][NV * 128];
+  const int i = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int a = x_ptr[i], e = x_ptr[i + 1];
+  float4 acc[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  int k = a + warp;
+  for (; k + 24 < e; k += 32) {
+    float4 r[4][NV];
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int f = x_idx[k + 8 * u];
+      v[u] = x_val[k + 8 * u];
+      const float* row = w1t + (int64_t)f * hp + lane * 4;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) r[u][q] = ld4(row + q * 128);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        acc[q].x = fmaf(v[u], r[u][q].x, acc[q].x);
+        acc[q].y = fmaf(v[u], r[u][q].y, acc[q].y);
+        acc[q].z = fmaf(v[u], r[u][q].z, acc[q].z);
+        acc[q].w = fmaf(v[u], r[u][q].w, acc[q].w);
+      }
+  }
+  for (; k < e; k += 8) {
+    const int f = x_idx[k];
+    const float v = x_val[k];
+    const float* row = w1t + (int64_t)f * hp + lane * 4;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      float4 r = ld4(row + q * 128);
+      acc[q].x = fmaf(v, r.x, acc[q].x);
+      acc[q].y = fmaf(v, r.y, acc[q].y);
+      acc[q].z = fmaf(v, r.z, acc[q].z);
+      acc[q].w = fmaf(v, r.w, acc[q].w);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NV; ++q) *reinterpret_cast<float4*>(&red[warp][q * 128 + lane * 4]) = acc[q];
+  __syncthreads();
+  for (int c = threadIdx.x; c < hp; c += 256) {
+    float s = red[0][c];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) s += red[w][c];
+    s += b1[c];
+    h[(int64_t)i * hp + c] = s > 0.f ? s : 0.f;
+  }
+}
+
+void launch_hidden_forward(int hp, int b, const int32_t* x_ptr, const int32_t* x_idx, const float* x_val,
+                           const float* w1t, const float* b1, float* h, cudaStream_t s) {
+  if (b <= 0) return;
+  SLIDE_NV_DISPATCH(hp, (hidden_fwd_kernel<NV><<<b, 256, 0, s>>>(hp, x_ptr, x_idx, x_val, w1t, b1, h)));
+  SLIDE_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------ output logits
+// z[p] = W2[row_p] . h[slot_p] + b2[row_p] for every (slot, active row)
+// pair (network.py:266).  A warp takes G consecutive pairs (same sample
+// mostly), issues all G row loads, then reduces.
+template <int NV, int G>
+__global__ void __launch_bounds__(256) logits_kernel(int hp, int64_t P, const int32_t* __restrict__ prow,
+                                                     const int32_t* __restrict__ pslot, const float* __restrict__ w2,
+                                                     const float* __restrict__ b2, const float* __restrict__ h,
+                                                     float* __restrict__ z) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t p0 = gw * G; p0 < P; p0 += nw * G) {
+    float4 w[G][NV];
+    int row[G], slot[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int64_t p = p0 + g;
+      row[g] = p < P ? prow[p] : 0;
+      slot[g] = p < P ? pslot[p] : 0;
+      const float* rp = w2 + (int64_t)row[g] * hp + lane * 4;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) w[g][q] = p < P ? ld4(rp + q * 128) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float* hr = h + (int64_t)slot[g] * hp + lane * 4;
+      float d = 0.f;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        float4 hv = ld4(hr + q * 128);
+        d = fmaf(w[g][q].x, hv.x, d);
+        d = fmaf(w[g][q].y, hv.y, d);
+        d = fmaf(w[g][q].z, hv.z, d);
+        d = fmaf(w[g][q].w, hv.w, d);
+      }
+      d = warp_sum(d);
+      if (lane == 0 && p0 + g < P) z[p0 + g] = d + b2[row[g]];
+    }
+  }
+}
+
+void launch_logits(int hp, int64_t P, const int32_t* prow, const int32_t* pslot, const float* w2, const float* b2,
+                   const float* h, float* z, cudaStream_t s) {
+  if (P <= 0) return;
+  constexpr int G = 4;
+  int64_t warps = ceil_div(P, G);
+  int grid = (int)std::min<int64_t>(ceil_div(warps, 8), (int64_t)kSms * 16);
+  SLIDE_NV_DISPATCH(hp, (logits_kernel<NV, G><<<grid, 256, 0, s>>>(hp, P, prow, pslot, w2, b2, h, z)));
+  SLIDE_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------- softmax + CE + delta
+// p = softmax over the active set (max-shifted, network.py:282-285);
+// delta = p - [label]/|Y| (network.py:308-309); loss = mean over labels of
+// -log(max(p_y, 1e-300)) (network.py:154-158), taken as a log-softmax.
+__global__ void __launch_bounds__(256) softmax_kernel(const int32_t* __restrict__ offs,
+                                                      const uint8_t* __restrict__ plab,
+                                                      const int32_t* __restrict__ y_ptr, const float* __restrict__ z,
+                                                      float* __restrict__ prob, float* __restrict__ delta,
+                                                      double* __restrict__ loss) {
+  using RF = cub::BlockReduce<float, 256>;
+  using RD = cub::BlockReduce<double, 256>;
+  __shared__ union {
+    typename RF::TempStorage f;
+    typename RD::TempStorage d;
+  } tmp;
+  __shared__ float s_max, s_sum;
+  const int i = blockIdx.x, tid = threadIdx.x;
+  const int o = offs[i], n = offs[i + 1] - o;
+  const int ny = y_ptr[i + 1] - y_ptr[i];
+  float mx = -INFINITY;
+  for (int k = tid; k < n; k += 256) mx = fmaxf(mx, z[o + k]);
+  mx = RF(tmp.f).Reduce(mx, cub::Max());
+  if (tid == 0) s_max = n > 0 ? mx : 0.f;
+  __syncthreads();
+  mx = s_max;
+  float se = 0.f;
+  for (int k = tid; k < n; k += 256) se += expf(z[o + k] - mx);
+  se = RF(tmp.f).Sum(se);
+  if (tid == 0) s_sum = se;
+  __syncthreads();
+  se = s_sum;
+  const float lse = logf(se);
+  const float inv_ny = ny > 0 ? 1.f / (float)ny : 0.f;
+  double lsum = 0.0;
+  for (int k = tid; k < n; k += 256) {
+    const float zz = z[o + k] - mx;
+    const float p = expf(zz) / se;
+    const int lab = plab[o + k];
+    prob[o + k] = p;
+    delta[o + k] = lab ? p - inv_ny : p;
+    if (lab) {
+      double nl = -((double)zz - (double)lse);
+      lsum += nl < 690.7755278982137 ? nl : 690.7755278982137;
+    }
+  }
+  lsum = RD(tmp.d).Sum(lsum);
+  if (tid == 0) loss[i] = ny > 0 ? lsum / ny : (double)NAN;
+}
+
+void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
+                    float* prob, float* delta, double* loss, cudaStream_t s) {
+  if (b <= 0) return;
+  softmax_kernel<<<b, 256, 0, s>>>(offs, plab, y_ptr, z, prob, delta, loss);
+  SLIDE_LAUNCH_CHECK();
+}
+
+// -------------------------------------------------------- hidden gradient
+// dh_i = W2[A_i, :]^T delta_i with the pre-update W2, kept on nz(h_i)
+// (network.py:328-332).  One CTA per sample, fixed-order reduction.
+template <int NV>
+__global__ void __launch_bounds__(256) hidden_grad_kernel(int hp, const int32_t* __restrict__ offs,
+                                                          const int32_t* __restrict__ prow,
+                                                          const float* __restrict__ delta,
+                                                          const float* __restrict__ w2,
+                                                          const float* __restrict__ h, float* __restrict__ dh) {
+  __shared__ float red[8][NV * 128];
+  const int i = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int o = offs[i], e = offs[i + 1];
+  float4 acc[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  int k = o + warp;
+  for (; k + 24 < e; k += 32) {
+    float4 r[4][NV];
+    float d[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      d[u] = delta[k + 8 * u];
+      const float* rp = w2 + (int64_t)prow[k + 8 * u] * hp + lane * 4;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) r[u][q] = ld4(rp + q * 128);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        acc[q].x = fmaf(d[u], r[u][q].x, acc[q].x);
+        acc[q].y = fmaf(d[u], r[u][q].y, acc[q].y);
+        acc[q].z = fmaf(d[u], r[u][q].z, acc[q].z);
+        acc[q].w = fmaf(d[u], r[u][q].w, acc[q].w);
+      }
+  }
+  for (; k < e; k += 8) {
+    const float d = delta[k];
+    const float* rp = w2 + (int64_t)prow[k] * hp + lane * 4;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      float4 r = ld4(rp + q * 128);
+      acc[q].x = fmaf(d, r.x, acc[q].x);
+      acc[q].y = fmaf(d, r.y, acc[q].y);
+      acc[q].z = fmaf(d, r.z, acc[q].z);
+      acc[q].w = fmaf(d, r.w, acc[q].w);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NV; ++q) *reinterpret_cast<float4*>(&red[warp][q * 128 + lane * 4]) = acc[q];
+  __syncthreads();
+  for (int c = threadIdx.x; c < hp; c += 256) {
+    float s = red[0][c];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) s += red[w][c];
+    dh[(int64_t)i * hp + c] = h[(int64_t)i * hp + c] > 0.f ? s : 0.f;
+  }
+}
+
+void launch_hidden_grad(int hp, int b, const int32_t* offs, const int32_t* prow, const float* delta, const float* w2,
+                        const float* h, float* dh, cudaStream_t s) {
+  if (b <= 0) return;
+  SLIDE_NV_DISPATCH(hp, (hidden_grad_kernel<NV><<<b, 256, 0, s>>>(hp, offs, prow, delta, w2, h, dh)));
+  SLIDE_LAUNCH_CHECK();
+}
+
+// ----------------------------------------------------------- Adam, W2 rows
+// Per active output row r, the samples that hold it are applied in slot
+// order (the snapshot schedule): t = steps[r] + j + 1 for the
+// row's j-th sample; moments move only where h_i > 0; the bias always moves
+// (network.py:428-451).
+__device__ __forceinline__ void adam_coord(float& w, float& m, float& v, float g, float bc1, float bc2,
+                                           const AdamParams& ap) {
+  m = ap.b1 * m + (1.f - ap.b1) * g;
+  v = ap.b2 * v + (1.f - ap.b2) * g * g;
+  w -= ap.lr * (m / bc1) / (sqrtf(v / bc2) + ap.eps);
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256) adam_rows_kernel(int hp, AdamParams ap, const int32_t* __restrict__ n_uniq,
+                                                        const int32_t* __restrict__ uniq,
+                                                        const int32_t* __restrict__ seg_off,
+                                                        const int32_t* __restrict__ seg_cnt,
+                                                        const int32_t* __restrict__ sorted_pairs,
+                                                        const int32_t* __restrict__ pslot,
+                                                        const float* __restrict__ delta, const float* __restrict__ h,
+                                                        float* __restrict__ w2, float* __restrict__ m2,
+                                                        float* __restrict__ v2, float* __restrict__ b2,
+                                                        float* __restrict__ mb2, float* __restrict__ vb2,
+                                                        int64_t* __restrict__ steps2,
+                                                        unsigned long long* __restrict__ touched) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nu = *n_uniq;
+  for (int64_t u = gw; u < nu; u += nw) {
+    uint32_t tmask = 0;
+    const int r = uniq[u];
+    const int s0 = seg_off[u], len = seg_cnt[u];
+    float* wr = w2 + (int64_t)r * hp + lane * 4;
+    float* mr = m2 + (int64_t)r * hp + lane * 4;
+    float* vr = v2 + (int64_t)r * hp + lane * 4;
+    float4 w[NV], m[NV], v[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      w[q] = ld4_cg(wr + q * 128);
+      m[q] = ld4_cg(mr + q * 128);
+      v[q] = ld4_cg(vr + q * 128);
+    }
+    float b = b2[r], mb = mb2[r], vb = vb2[r];
+    const int64_t st = steps2[r];
+    for (int c0 = 0; c0 < len; c0 += 32) {
+      const int j = c0 + lane;
+      int slot_l = 0;
+      float d_l = 0.f, bc1_l = 1.f, bc2_l = 1.f;
+      if (j < len) {
+        const int p = sorted_pairs[s0 + j];
+        slot_l = pslot[p];
+        d_l = delta[p];
+        const double t = (double)(st + j + 1);
+        bc1_l = (float)(1.0 - pow(ap.b1d, t));
+        bc2_l = (float)(1.0 - pow(ap.b2d, t));
+      }
+      const int nc = min(32, len - c0);
+      for (int q2 = 0; q2 < nc; ++q2) {
+        const int slot = __shfl_sync(0xffffffffu, slot_l, q2);
+        const float d = __shfl_sync(0xffffffffu, d_l, q2);
+        const float bc1 = __shfl_sync(0xffffffffu, bc1_l, q2);
+        const float bc2 = __shfl_sync(0xffffffffu, bc2_l, q2);
+        const float* hr = h + (int64_t)slot * hp + lane * 4;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          float4 hv = ld4(hr + q * 128);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float hc = comp(hv, c);
+            if (hc > 0.f) {
+              adam_coord(comp(w[q], c), comp(m[q], c), comp(v[q], c), d * hc, bc1, bc2, ap);
+              tmask |= 1u << (q * 4 + c);
+            }
+          }
+        }
+        adam_coord(b, mb, vb, d, bc1, bc2, ap);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      st4(wr + q * 128, w[q]);
+      st4(mr + q * 128, m[q]);
+      st4(vr + q * 128, v[q]);
+    }
+    if (lane == 0) {
+      b2[r] = b;
+      mb2[r] = mb;
+      vb2[r] = vb;
+      steps2[r] = st + len;
+    }
+    if (touched) {
+      int tc = __popc(tmask);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tc += __shfl_xor_sync(0xffffffffu, tc, o);
+      if (lane == 0) atomicAdd(touched, (unsigned long long)tc);
+    }
+  }
+}
+
+__global__ void accumulate_kernel(unsigned long long* dst, const int32_t* src) {
+  if (src) *dst += (unsigned long long)*src;
+}
+
+void launch_accumulate(unsigned long long* dst, const int32_t* src, cudaStream_t s) {
+  if (!src) return;
+  accumulate_kernel<<<1, 1, 0, s>>>(dst, src);
+  SLIDE_LAUNCH_CHECK();
+}
+
+void launch_adam_rows(int hp, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq, const int32_t* uniq,
+                      const int32_t* seg_off, const int32_t* seg_cnt, const int32_t* sorted_pairs,
+                      const int32_t* pslot, const float* delta, const float* h, float* w2, float* m2, float* v2,
+                      float* b2, float* mb2, float* vb2, int64_t* steps2, unsigned long long* touched,
+                      cudaStream_t s) {
+  if (max_uniq <= 0) return;
+  int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * 16);
+  SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV><<<grid, 256, 0, s>>>(hp, ap, n_uniq, uniq, seg_off, seg_cnt,
+                                                                    sorted_pairs, pslot, delta, h, w2, m2, v2, b2,
+                                                                    mb2, vb2, steps2, touched)));
+  SLIDE_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------- Adam, W1 features
+__global__ void x_slots_kernel(const int32_t* __restrict__ x_ptr, int32_t* __restrict__ x_slot) {
+  const int i = blockIdx.x;
+  const int base = x_ptr[0];
+  for (int k = x_ptr[i] + threadIdx.x; k < x_ptr[i + 1]; k += blockDim.x) x_slot[k - base] = i;
+}
+
+void launch_x_slots(int b, const int32_t* x_ptr, int32_t* x_slot, cudaStream_t s) {
+  if (b <= 0) return;
+  x_slots_kernel<<<b, 128, 0, s>>>(x_ptr, x_slot);
+  SLIDE_LAUNCH_CHECK();
+}
+
+// tc[i][c] = #{i' <= i : h_i'[c] > 0}; hidden unit c's step for sample i is
+// steps1[c] + tc[i][c] (each sample bumps the counter of its nz(h) rows,
+// network.py:436-437).  bc holds the two bias corrections.
+__global__ void hidden_counts_kernel(int hp, int b, AdamParams ap, const float* __restrict__ h,
+                                     const int64_t* __restrict__ steps1, int32_t* __restrict__ tc,
+                                     float2* __restrict__ bc) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= hp) return;
+  int cnt = 0;
+  const int64_t st = steps1[c];
+  for (int i = 0; i < b; ++i) {
+    const int64_t q = (int64_t)i * hp + c;
+    if (h[q] > 0.f) {
+      ++cnt;
+      const double t = (double)(st + cnt);
+      bc[q] = make_float2((float)(1.0 - pow(ap.b1d, t)), (float)(1.0 - pow(ap.b2d, t)));
+    }
+    tc[q] = cnt;
+  }
+}
+
+void launch_hidden_counts(int hp, int b, const AdamParams& ap, const float* h, const int64_t* steps1, int32_t* tc,
+                          float2* bc, cudaStream_t s) {
+  hidden_counts_kernel<<<(int)ceil_div(hp, 128), 128, 0, s>>>(hp, b, ap, h, steps1, tc, bc);
+  SLIDE_LAUNCH_CHECK();
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256) adam_features_kernel(
+    int hp, AdamParams ap, const int32_t* __restrict__ n_uniq, const int32_t* __restrict__ uniq,
+    const int32_t* __restrict__ seg_off, const int32_t* __restrict__ seg_cnt, const int32_t* __restrict__ sorted_k,
+    const int32_t* __restrict__ x_slot, const float* __restrict__ x_val, int64_t x_base,
+    const float* __restrict__ h, const float* __restrict__ dh, const float2* __restrict__ bc,
+    float* __restrict__ w1t, float* __restrict__ m1t, float* __restrict__ v1t,
+    unsigned long long* __restrict__ touched) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nu = *n_uniq;
+  for (int64_t u = gw; u < nu; u += nw) {
+    uint32_t tmask = 0;
+    const int f = uniq[u];
+    const int s0 = seg_off[u], len = seg_cnt[u];
+    float* wr = w1t + (int64_t)f * hp + lane * 4;
+    float* mr = m1t + (int64_t)f * hp + lane * 4;
+    float* vr = v1t + (int64_t)f * hp + lane * 4;
+    float4 w[NV], m[NV], v[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      w[q] = ld4_cg(wr + q * 128);
+      m[q] = ld4_cg(mr + q * 128);
+      v[q] = ld4_cg(vr + q * 128);
+    }
+    for (int c0 = 0; c0 < len; c0 += 32) {
+      const int j = c0 + lane;
+      int slot_l = 0;
+      float xv_l = 0.f;
+      if (j < len) {
+        const int k = sorted_k[s0 + j];
+        slot_l = x_slot[k];
+        xv_l = x_val[x_base + k];
+      }
+      const int nc = min(32, len - c0);
+      for (int q2 = 0; q2 < nc; ++q2) {
+        const int slot = __shfl_sync(0xffffffffu, slot_l, q2);
+        const float xv = __shfl_sync(0xffffffffu, xv_l, q2);
+        const int64_t base = (int64_t)slot * hp + lane * 4;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          const float4 hv = ld4(h + base + q * 128);
+          const float4 gv = ld4(dh + base + q * 128);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float hc = reinterpret_cast<const float*>(&hv)[c];
+            if (hc > 0.f) {
+              const float2 bb = bc[base + q * 128 + c];
+              adam_coord(comp(w[q], c), comp(m[q], c), comp(v[q], c), reinterpret_cast<const float*>(&gv)[c] * xv,
+                         bb.x, bb.y, ap);
+              tmask |= 1u << (q * 4 + c);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      st4(wr + q * 128, w[q]);
+      st4(mr + q * 128, m[q]);
+      st4(vr + q * 128, v[q]);
+    }
+    if (touched) {
+      int tc = __popc(tmask);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tc += __shfl_xor_sync(0xffffffffu, tc, o);
+      if (lane == 0) atomicAdd(touched, (unsigned long long)tc);
+    }
+  }
+}
+
+void launch_adam_features(int hp, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq,
+                          const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
+                          const int32_t* sorted_k, const int32_t* x_slot, const float* x_val, int64_t x_base,
+                          const float* h, const float* dh, const float2* bc, float* w1t, float* m1t, float* v1t,
+                          unsigned long long* touched, cudaStream_t s) {
+  if (max_uniq <= 0) return;
+  int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * 16);
+  SLIDE_NV_DISPATCH(hp, (adam_features_kernel<NV><<<grid, 256, 0, s>>>(hp, ap, n_uniq, uniq, seg_off, seg_cnt,
+                                                                        sorted_k, x_slot, x_val, x_base, h, dh, bc,
+                                                                        w1t, m1t, v1t, touched)));
+  SLIDE_LAUNCH_CHECK();
+}
+
+// hidden biases: rows nz(h_i) of every sample in slot order, g = dh_i
+__global__ void adam_hidden_bias_kernel(int hp, int b, AdamParams ap, const float* __restrict__ h,
+                                        const float* __restrict__ dh, const int32_t* __restrict__ tc,
+                                        const float2* __restrict__ bc, float* __restrict__ b1,
+                                        float* __restrict__ mb1, float* __restrict__ vb1,
+                                        int64_t* __restrict__ steps1) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= hp || b <= 0) return;
+  float bb = b1[c], mb = mb1[c], vb = vb1[c];
+  for (int i = 0; i < b; ++i) {
+    const int64_t q = (int64_t)i * hp + c;
+    if (h[q] > 0.f) adam_coord(bb, mb, vb, dh[q], bc[q].x, bc[q].y, ap);
+  }
+  b1[c] = bb;
+  mb1[c] = mb;
+  vb1[c] = vb;
+  steps1[c] += tc[(int64_t)(b - 1) * hp + c];
+}
+
+void launch_adam_hidden_bias(int hp, int b, const AdamParams& ap, const float* h, const float* dh, const int32_t* tc,
+                             const float2* bc, float* b1, float* mb1, float* vb1, int64_t* steps1, cudaStream_t s) {
+  adam_hidden_bias_kernel<<<(int)ceil_div(hp, 128), 128, 0, s>>>(hp, b, ap, h, dh, tc, bc, b1, mb1, vb1, steps1);
+  SLIDE_LAUNCH_CHECK();
+}
+
+}  // namespace slide

@@ -1,0 +1,409 @@
+// Output-layer active-set selection: query -> sample -> fallback -> union
+// with labels (reference network.py:225-239, samplers.py:57-120,
+// tables.py:165-176).
+//
+// One CTA per sample.  Candidates are the ids of the L probed buckets, each
+// tagged with its probe position (vanilla) or table index, plus the labels
+// tagged 127; a block-wide sort of (id << 7 | tag) groups an id's
+// occurrences, which gives for every distinct id its frequency (topk /
+// hard_threshold), its first probe position (vanilla: the union of the
+// first tau probes, tau = first prefix reaching beta distinct ids) and
+// whether it is a label.  The output list is sorted ascending, label bit 31.
+#include "internal.cuh"
+#include "kernels.cuh"
+#include <cub/cub.cuh>
+
+namespace slide {
+
+// ------------------------------------------------------------ per-slot rng
+// default_rng((seed, iteration, slot)) (network.py:353) or an explicit
+// Generator state; vanilla draws permutation(L) first (samplers.py:69).
+__global__ void slot_rng_kernel(int b, uint64_t seed, int64_t iteration, int64_t slot_offset, int l,
+                                int vanilla, const uint64_t* __restrict__ ext, uint64_t* __restrict__ states,
+                                uint8_t* __restrict__ order) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= b) return;
+  Pcg64 g;
+  if (ext) {
+    g.load(ext + 6 * i);
+  } else {
+    uint64_t ent[3] = {seed, (uint64_t)iteration, (uint64_t)(slot_offset + i)};
+    g.seed_from(ent, 3);
+  }
+  if (vanilla) {
+    uint8_t a[64];
+    pcg_permutation(g, a, l);
+    for (int p = 0; p < l; ++p) order[(int64_t)i * l + p] = a[p];
+  }
+  g.store(states + 6 * i);
+}
+
+void launch_slot_rng(int b, uint64_t seed, int64_t it, int64_t off, int l, int vanilla, const uint64_t* ext,
+                     uint64_t* states, uint8_t* order, cudaStream_t s) {
+  slot_rng_kernel<<<(int)ceil_div(b, 64), 64, 0, s>>>(b, seed, it, off, l, vanilla, ext, states, order);
+  SLIDE_LAUNCH_CHECK();
+}
+
+// ----------------------------------------------------------------- select
+constexpr int kSelThreads = 256;
+constexpr uint32_t kLabelTag = 127;
+
+template <int ITEMS>
+struct SelSmem {
+  using Sort = cub::BlockRadixSort<uint32_t, kSelThreads, ITEMS>;
+  static constexpr int CAP = kSelThreads * ITEMS;
+  static constexpr size_t kA = sizeof(typename Sort::TempStorage), kB = (size_t)CAP * 4;
+  static constexpr size_t kRegion2 = ((kA > kB ? kA : kB) + 15) & ~(size_t)15;
+  __host__ __device__ static constexpr size_t region2() { return kRegion2; }
+  __host__ __device__ static constexpr size_t bytes() { return (size_t)CAP * 4 + kRegion2 + CAP; }
+};
+
+template <int ITEMS>
+__global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
+  using S = SelSmem<ITEMS>;
+  using Scan = cub::BlockScan<int, kSelThreads>;
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint32_t* cand = reinterpret_cast<uint32_t*>(sm);
+  uint8_t* region2 = sm + (size_t)S::CAP * 4;
+  uint32_t* uid = reinterpret_cast<uint32_t*>(region2);
+  uint8_t* ufreq = region2 + S::region2();
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ int s_start[64], s_len[64], s_off[65], s_tag[64], s_hist[130];
+  __shared__ int s_misc[4];
+
+  const int i = blockIdx.x, tid = threadIdx.x, L = a.l;
+  const int y0 = a.y_ptr[i], ny = a.y_ptr[i + 1] - y0;
+  // 1. probe the L tables (exactly L lookups, tables.py:171-176)
+  if (tid < L) {
+    uint32_t skey = ((uint32_t)tid << a.tab.key_bits) | a.qkeys[(int64_t)i * L + tid];
+    int run = tables_lookup(a.tab, skey);
+    s_start[tid] = run >= 0 ? a.tab.bstart[run] : 0;
+    s_len[tid] = run >= 0 ? a.tab.blen[run] : 0;
+    if (a.strategy != 0) s_tag[tid] = tid;
+    else s_tag[a.order[(int64_t)i * L + tid]] = tid;  // probe position of table order[p] is p
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int t = 0; t < L; ++t) {
+      s_off[t] = acc;
+      acc += s_len[t];
+    }
+    s_off[L] = acc;
+  }
+  for (int q = tid; q < 130; q += kSelThreads) s_hist[q] = 0;
+  __syncthreads();
+  const int C = s_off[L] + ny;
+  if (tid == 0 && a.cand_ctr) atomicAdd(a.cand_ctr, (unsigned long long)s_off[L]);
+  // 2. gather (id << 7 | tag); labels carry tag 127
+  {
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int t = warp; t < L; t += kSelThreads / 32) {
+      const int32_t* src = a.tab.ids + s_start[t];
+      uint32_t tag = (uint32_t)s_tag[t];
+      for (int j = lane; j < s_len[t]; j += 32) cand[s_off[t] + j] = ((uint32_t)src[j] << 7) | tag;
+    }
+    for (int j = tid; j < ny; j += kSelThreads)
+      cand[s_off[L] + j] = ((uint32_t)a.y_idx[y0 + j] << 7) | kLabelTag;
+  }
+  __syncthreads();
+  // 3. sort
+  if (C <= kSelThreads) {
+    uint32_t key = tid < C ? cand[tid] : 0u;
+    int rank = 0;
+    if (tid < C)
+      for (int s2 = 0; s2 < C; ++s2) rank += cand[s2] < key;
+    __syncthreads();
+    if (tid < C) cand[rank] = key;  // keys are unique
+    __syncthreads();
+  } else {
+    uint32_t keys[ITEMS];
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+      int k = tid * ITEMS + q;
+      keys[q] = k < C ? cand[k] : 0xffffffffu;
+    }
+    typename S::Sort(*reinterpret_cast<typename S::Sort::TempStorage*>(region2)).Sort(keys, 0, a.sort_bits);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+      int k = tid * ITEMS + q;
+      if (k < C) cand[k] = keys[q];
+    }
+    __syncthreads();
+  }
+  // 4. distinct ids: first tag (min probe position), frequency, label flag
+  const int ch = (C + kSelThreads - 1) / kSelThreads;
+  const int k0 = min(tid * ch, C), k1 = min(k0 + ch, C);
+  int nh = 0;
+  for (int k = k0; k < k1; ++k) nh += (k == 0 || (cand[k - 1] >> 7) != (cand[k] >> 7));
+  int hofs, U;
+  Scan(scan_tmp).ExclusiveSum(nh, hofs, U);
+  __syncthreads();
+  for (int k = k0; k < k1; ++k) {
+    uint32_t id = cand[k] >> 7;
+    if (k != 0 && (cand[k - 1] >> 7) == id) continue;
+    int e = k + 1;
+    while (e < C && (cand[e] >> 7) == id) ++e;
+    int lab = (cand[e - 1] & 127u) == kLabelTag;
+    int freq = e - k - lab;
+    uid[hofs] = cand[k];
+    ufreq[hofs] = (uint8_t)(freq | (lab << 7));
+    ++hofs;
+  }
+  __syncthreads();
+  // 5. sampler rule on the non-label occurrences
+  const int uch = (U + kSelThreads - 1) / kSelThreads;
+  const int u0 = min(tid * uch, U), u1 = min(u0 + uch, U);
+  if (a.strategy == 0) {  // vanilla
+    for (int u = u0; u < u1; ++u)
+      if (ufreq[u] & 127) atomicAdd(&s_hist[uid[u] & 127u], 1);
+  } else if (a.strategy == 1) {  // topk
+    for (int u = u0; u < u1; ++u)
+      if (ufreq[u] & 127) atomicAdd(&s_hist[ufreq[u] & 127], 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (a.strategy == 0) {
+      int acc = 0, tau = L;
+      for (int p = 0; p < L; ++p) {
+        acc += s_hist[p];
+        if (acc >= a.beta) {
+          tau = p + 1;
+          break;
+        }
+      }
+      s_misc[0] = tau;
+    } else if (a.strategy == 1) {
+      int total = 0;
+      for (int f = 1; f <= 127; ++f) total += s_hist[f];
+      int F = 1, need = 1 << 30;
+      if (total > a.beta) {
+        int cum = 0;
+        for (int f = 127; f >= 1; --f) {
+          if (cum + s_hist[f] >= a.beta) {
+            F = f;
+            need = a.beta - cum;
+            break;
+          }
+          cum += s_hist[f];
+        }
+      }
+      s_misc[0] = F;
+      s_misc[1] = need;
+    }
+  }
+  __syncthreads();
+  int eq_before = 0;
+  if (a.strategy == 1) {
+    int F = s_misc[0], neq = 0;
+    for (int u = u0; u < u1; ++u) neq += (ufreq[u] & 127) == F;
+    int tot;
+    Scan(scan_tmp).ExclusiveSum(neq, eq_before, tot);
+    __syncthreads();
+  }
+  int nkeep = 0, nsel = 0;
+  const int tau = s_misc[0], F = s_misc[0], need = s_misc[1];
+  // selected flag computed twice (count, then write) to avoid a smem array
+  auto selected = [&](int u, int& eqc) -> bool {
+    int f = ufreq[u] & 127;
+    if (f == 0) return false;
+    if (a.strategy == 0) return (int)(uid[u] & 127u) < tau;
+    if (a.strategy == 1) {
+      if (f > F) return true;
+      if (f == F) return eqc++ < need;
+      return false;
+    }
+    return f >= a.min_freq;
+  };
+  {
+    int eqc = eq_before;
+    for (int u = u0; u < u1; ++u) {
+      bool sl = selected(u, eqc);
+      nsel += sl;
+      nkeep += sl || (ufreq[u] >> 7);
+    }
+  }
+  int any = __syncthreads_or(nsel > 0);
+  if (!any) {
+    if (tid == 0) {
+      a.empty[i] = 1;
+      a.cnt[i] = 0;
+    }
+    return;
+  }
+  int kofs, K;
+  Scan(scan_tmp).ExclusiveSum(nkeep, kofs, K);
+  int32_t* out = a.act + (int64_t)i * a.cap_max;
+  {
+    int eqc = eq_before;
+    for (int u = u0; u < u1; ++u) {
+      bool sl = selected(u, eqc);
+      int lab = ufreq[u] >> 7;
+      if (sl || lab) out[kofs++] = (int32_t)((uid[u] >> 7) | ((uint32_t)lab << 31));
+    }
+  }
+  if (tid == 0) {
+    a.empty[i] = 0;
+    a.cnt[i] = K;
+  }
+}
+
+template <int ITEMS>
+static void launch_select_t(const SelectArgs& a, cudaStream_t s) {
+  size_t smem = SelSmem<ITEMS>::bytes();
+  SLIDE_CUDA(cudaFuncSetAttribute(select_kernel<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  select_kernel<ITEMS><<<a.b, kSelThreads, smem, s>>>(a);
+  SLIDE_LAUNCH_CHECK();
+}
+
+void launch_select(const SelectArgs& a, int max_candidates, cudaStream_t s) {
+  SLIDE_CHECK(a.l <= 64, kNotSupported, "at most 64 tables supported on the device path");
+  if (max_candidates <= kSelThreads * 16) launch_select_t<16>(a, s);
+  else if (max_candidates <= kSelThreads * 32) launch_select_t<32>(a, s);
+  else if (max_candidates <= kSelThreads * 64) launch_select_t<64>(a, s);
+  else throw Error(kNotSupported, "L*capacity + labels exceeds 16384 candidates per sample");
+}
+
+// --------------------------------------------------------------- fallback
+// Empty sampler result: beta uniform ids without replacement from the slot's
+// generator (network.py:229-231), union labels, sorted (network.py:236-238).
+// Thread 0 replays numpy's choice() serially; the CTA then emits the id set
+// in ascending order from a per-slot bitmap.
+__global__ void __launch_bounds__(256) fallback_kernel(FallbackArgs a) {
+  using Scan = cub::BlockScan<int, 256>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  extern __shared__ __align__(16) int64_t fb_smem[];
+  const int i = blockIdx.x, tid = threadIdx.x;
+  if (!a.empty[i]) return;
+  int64_t* ids = a.fb_ids + (int64_t)i * a.want;
+  if (tid == 0) {
+    Pcg64 g;
+    g.load(a.states + 6 * i);
+    int64_t* scratch = a.smem_scratch ? fb_smem : a.scratch + (int64_t)i * a.scratch_per_slot;
+    pcg_choice(g, a.n, a.want, ids, scratch);
+    g.store(a.states + 6 * i);
+  }
+  __syncthreads();
+  uint32_t* bm = a.bitmap + (int64_t)i * a.words;
+  for (int64_t k = tid; k < a.want; k += 256) {
+    int64_t id = ids[k];
+    atomicOr(&bm[id >> 5], 1u << (id & 31));
+  }
+  const int y0 = a.y_ptr[i], ny = a.y_ptr[i + 1] - y0;
+  for (int k = tid; k < ny; k += 256) {
+    int id = a.y_idx[y0 + k];
+    atomicOr(&bm[id >> 5], 1u << (id & 31));
+  }
+  __syncthreads();
+  const int64_t ch = (a.words + 255) / 256;
+  const int64_t w0 = tid * ch < a.words ? tid * ch : a.words;
+  const int64_t w1 = w0 + ch < a.words ? w0 + ch : a.words;
+  int cnt = 0;
+  for (int64_t w = w0; w < w1; ++w) cnt += __popc(bm[w]);
+  int ofs, total;
+  Scan(scan_tmp).ExclusiveSum(cnt, ofs, total);
+  int32_t* out = a.act + (int64_t)i * a.cap_max;
+  const int32_t* lab = a.y_idx + y0;
+  for (int64_t w = w0; w < w1; ++w) {
+    uint32_t bits = bm[w];
+    while (bits) {
+      int bpos = __ffs(bits) - 1;
+      bits &= bits - 1;
+      int id = (int)(w * 32 + bpos);
+      int lo = 0, hi = ny;  // labels sorted: binary search
+      while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (lab[mid] < id) lo = mid + 1;
+        else hi = mid;
+      }
+      int is_lab = lo < ny && lab[lo] == id;
+      out[ofs++] = (int32_t)((uint32_t)id | ((uint32_t)is_lab << 31));
+    }
+    bm[w] = 0u;
+  }
+  if (tid == 0) a.cnt[i] = total;
+}
+
+void launch_fallback(const FallbackArgs& a, int b, cudaStream_t s) {
+  size_t smem = a.smem_scratch ? (size_t)a.scratch_per_slot * 8 : 0;
+  if (smem > 48 * 1024)
+    SLIDE_CUDA(cudaFuncSetAttribute(fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  fallback_kernel<<<b, 256, smem, s>>>(a);
+  SLIDE_LAUNCH_CHECK();
+}
+
+// ------------------------------------------- dense / forced active sets
+// No LSH on the layer: every neuron is active (network.py:234-235).  Forced
+// sets (forward(forced_active=...), network.py:258-259) replace selection.
+__global__ void explicit_active_kernel(int b, int64_t n, const int32_t* __restrict__ fptr,
+                                       const int32_t* __restrict__ fidx, const int32_t* __restrict__ y_ptr,
+                                       const int32_t* __restrict__ y_idx, int64_t cap_max,
+                                       int32_t* __restrict__ act, int32_t* __restrict__ cnt,
+                                       int32_t* __restrict__ empty) {
+  const int i = blockIdx.x;
+  const int y0 = y_ptr[i], ny = y_ptr[i + 1] - y0;
+  int64_t m = fptr ? (int64_t)(fptr[i + 1] - fptr[i]) : n;
+  int32_t* out = act + (int64_t)i * cap_max;
+  for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+    int id = fptr ? fidx[fptr[i] + k] : (int)k;
+    int lo = 0, hi = ny;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (y_idx[y0 + mid] < id) lo = mid + 1;
+      else hi = mid;
+    }
+    int is_lab = lo < ny && y_idx[y0 + lo] == id;
+    out[k] = (int32_t)((uint32_t)id | ((uint32_t)is_lab << 31));
+  }
+  if (threadIdx.x == 0) {
+    cnt[i] = (int32_t)m;
+    empty[i] = 0;
+  }
+}
+
+void launch_explicit_active(int b, int64_t n, const int32_t* fptr, const int32_t* fidx, const int32_t* y_ptr,
+                            const int32_t* y_idx, int64_t cap_max, int32_t* act, int32_t* cnt, int32_t* empty,
+                            cudaStream_t s) {
+  explicit_active_kernel<<<b, 256, 0, s>>>(b, n, fptr, fidx, y_ptr, y_idx, cap_max, act, cnt, empty);
+  SLIDE_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------- compaction
+// Exclusive scan of per-slot counts (B <= 1024) and the sample-major pair
+// list: row id, slot, label flag.
+__global__ void offsets_kernel(int b, const int32_t* __restrict__ cnt, int32_t* __restrict__ offs) {
+  using Scan = cub::BlockScan<int, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  int v = threadIdx.x < b ? cnt[threadIdx.x] : 0, o, total;
+  Scan(tmp).ExclusiveSum(v, o, total);
+  if (threadIdx.x < b) offs[threadIdx.x] = o;
+  if (threadIdx.x == 0) offs[b] = total;
+}
+
+void launch_offsets(int b, const int32_t* cnt, int32_t* offs, cudaStream_t s) {
+  SLIDE_CHECK(b <= 1024, kNotSupported, "batch size above 1024 not supported on the device path");
+  offsets_kernel<<<1, 1024, 0, s>>>(b, cnt, offs);
+  SLIDE_LAUNCH_CHECK();
+}
+
+__global__ void pairs_kernel(const int32_t* __restrict__ act, int64_t cap_max, const int32_t* __restrict__ offs,
+                             int32_t* __restrict__ prow, int32_t* __restrict__ pslot, uint8_t* __restrict__ plab) {
+  const int i = blockIdx.x;
+  const int o = offs[i], n = offs[i + 1] - o;
+  const int32_t* src = act + (int64_t)i * cap_max;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    uint32_t v = (uint32_t)src[k];
+    prow[o + k] = (int32_t)(v & 0x7fffffffu);
+    pslot[o + k] = i;
+    plab[o + k] = (uint8_t)(v >> 31);
+  }
+}
+
+void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* offs, int32_t* prow, int32_t* pslot,
+                  uint8_t* plab, cudaStream_t s) {
+  pairs_kernel<<<b, 256, 0, s>>>(act, cap_max, offs, prow, pslot, plab);
+  SLIDE_LAUNCH_CHECK();
+}
+
+}  // namespace slide

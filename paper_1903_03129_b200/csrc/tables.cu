@@ -1,0 +1,292 @@
+// (K, L) bucket index build (reference tables.py:105-161).
+//
+// Ids 0..N-1 enter every table in ascending order.  On the device that is
+// one stable radix sort of the N*L (table, key) inserts with the id as value:
+// each run of equal (table, key) is a bucket's insert history in insertion
+// order.  FIFO keeps the last min(count, cap) entries of the run
+// (tables.py:130-145); reservoir keeps the first cap and replays the
+// overflowing inserts through the MT19937 stream on the host, in (table, id)
+// order (tables.py:146-161).  A directory maps (table, key) to its run:
+// dense (L << key_bits entries) for short keys, open addressing otherwise.
+#include "internal.cuh"
+#include <cub/cub.cuh>
+#include <algorithm>
+
+namespace slide {
+
+void TablesHost::release() {
+  for (DBuf* b : {&skeys_a, &skeys_b, &vals_a, &vals_b, &uniq, &counts, &offsets, &nruns, &dir, &hdir,
+                  &bstart, &blen, &temp, &ovf_cnt, &ovf_off, &ovf_ev, &patch})
+    b->release();
+  built = false;
+}
+
+__global__ void sort_input_kernel(const uint32_t* __restrict__ keys, int64_t n, int l, int kb,
+                                  uint32_t* __restrict__ skeys, int32_t* __restrict__ vals) {
+  int64_t total = n * l;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = q / n, r = q - t * n;
+    skeys[q] = ((uint32_t)t << kb) | keys[r * l + t];
+    vals[q] = (int32_t)r;
+  }
+}
+
+__global__ void runs_kernel(const uint32_t* __restrict__ uniq, const int32_t* __restrict__ counts,
+                            const int32_t* __restrict__ offsets, int64_t n_runs, int cap, int fifo,
+                            int dense, int32_t* dir, uint64_t* hdir, uint64_t hmask,
+                            int32_t* __restrict__ bstart, int32_t* __restrict__ blen,
+                            int32_t* __restrict__ ovf) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_runs;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int cnt = counts[r];
+    int len = cnt < cap ? cnt : cap;
+    bstart[r] = fifo ? offsets[r] + cnt - len : offsets[r];
+    blen[r] = len;
+    if (ovf) ovf[r] = cnt > cap ? cnt - cap : 0;
+    uint32_t sk = uniq[r];
+    if (dense) {
+      dir[sk] = (int32_t)r;
+    } else {
+      uint64_t ent = ((uint64_t)sk << 32) | (uint32_t)r;
+      uint64_t loc = hash32(sk) & hmask;
+      while (true) {
+        unsigned long long prev = atomicCAS((unsigned long long*)&hdir[loc], ~0ull, (unsigned long long)ent);
+        if (prev == ~0ull) break;
+        loc = (loc + 1) & hmask;
+      }
+    }
+  }
+}
+
+__global__ void dir_kernel(const uint32_t* __restrict__ uniq, int64_t n_runs, int dense, int32_t* dir,
+                           uint64_t* hdir, uint64_t hmask) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_runs;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t sk = uniq[r];
+    if (dense) {
+      dir[sk] = (int32_t)r;
+      continue;
+    }
+    uint64_t ent = ((uint64_t)sk << 32) | (uint32_t)r;
+    uint64_t loc = hash32(sk) & hmask;
+    while (atomicCAS((unsigned long long*)&hdir[loc], ~0ull, (unsigned long long)ent) != ~0ull)
+      loc = (loc + 1) & hmask;
+  }
+}
+
+struct OvfEvent {
+  int32_t id, table, off, count;
+};
+
+__global__ void overflow_events_kernel(const uint32_t* __restrict__ uniq, const int32_t* __restrict__ counts,
+                                       const int32_t* __restrict__ offsets, const int32_t* __restrict__ ovf,
+                                       const int32_t* __restrict__ ovf_off, const int32_t* __restrict__ ids,
+                                       int64_t n_runs, int cap, int kb, OvfEvent* ev) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_runs;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int o = ovf[r];
+    if (!o) continue;
+    int base = ovf_off[r], off = offsets[r];
+    int t = (int)(uniq[r] >> kb);
+    for (int p = 0; p < o; ++p) {
+      OvfEvent e;
+      e.id = ids[off + cap + p];
+      e.table = t;
+      e.off = off;
+      e.count = cap + p + 1;
+      ev[base + p] = e;
+    }
+  }
+}
+
+__global__ void patch_kernel(const int2* __restrict__ patches, int64_t n, int32_t* ids) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    ids[patches[q].x] = patches[q].y;
+}
+
+static int grid_for(int64_t n, int bs = 256) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, bs), kSms * 16)); }
+
+void tables_build(TablesHost& tb, const uint32_t* keys, int64_t n, int l, int kb, int cap, int policy,
+                  uint64_t* mt_state, cudaStream_t s) {
+  int tbits = 0;
+  while ((1 << tbits) < l) ++tbits;
+  SLIDE_CHECK(kb + tbits <= 32, kNotSupported, "table index + key bits must fit in 32 bits");
+  SLIDE_CHECK(n * l < (int64_t)INT32_MAX, kNotSupported, "N*L inserts exceed int32 range");
+  const int64_t total = n * l;
+  uint32_t* ska = tb.skeys_a.ensure<uint32_t>(total);
+  uint32_t* skb = tb.skeys_b.ensure<uint32_t>(total);
+  int32_t* va = tb.vals_a.ensure<int32_t>(total);
+  int32_t* vb = tb.vals_b.ensure<int32_t>(total);
+  uint32_t* uniq = tb.uniq.ensure<uint32_t>(total);
+  int32_t* counts = tb.counts.ensure<int32_t>(total);
+  int32_t* offsets = tb.offsets.ensure<int32_t>(total);
+  int32_t* nr_d = tb.nruns.ensure<int32_t>(1);
+  if (total > 0) {
+    sort_input_kernel<<<grid_for(total), 256, 0, s>>>(keys, n, l, kb, ska, va);
+    SLIDE_LAUNCH_CHECK();
+  }
+  const int end_bit = kb + tbits;
+  size_t b1 = 0, b2 = 0, b3 = 0;
+  SLIDE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, ska, skb, va, vb, (int)total, 0, end_bit, s));
+  SLIDE_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, b2, skb, uniq, counts, nr_d, (int)total, s));
+  SLIDE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b3, counts, offsets, (int)total, s));
+  size_t tbytes = std::max(b1, std::max(b2, b3));
+  void* temp = tb.temp.ensure<uint8_t>(tbytes);
+  SLIDE_CUDA(cub::DeviceRadixSort::SortPairs(temp, tbytes, ska, skb, va, vb, (int)total, 0, end_bit, s));
+  SLIDE_CUDA(cub::DeviceRunLengthEncode::Encode(temp, tbytes, skb, uniq, counts, nr_d, (int)total, s));
+  int32_t n_runs = 0;
+  SLIDE_CUDA(cudaMemcpyAsync(&n_runs, nr_d, 4, cudaMemcpyDeviceToHost, s));
+  SLIDE_CUDA(cudaStreamSynchronize(s));
+  if (n_runs > 0) SLIDE_CUDA(cub::DeviceScan::ExclusiveSum(temp, tbytes, counts, offsets, n_runs, s));
+
+  TablesDev& d = tb.dev;
+  d.l = l;
+  d.key_bits = kb;
+  d.cap = cap;
+  d.n_runs = n_runs;
+  d.dense_dir = kb <= 16;
+  int32_t* dir = nullptr;
+  uint64_t* hdir = nullptr;
+  uint64_t hmask = 0;
+  if (d.dense_dir) {
+    size_t nd = (size_t)l << kb;
+    dir = tb.dir.ensure<int32_t>(nd);
+    SLIDE_CUDA(cudaMemsetAsync(dir, 0xff, nd * 4, s));
+  } else {
+    uint64_t hc = gen_mask((uint64_t)std::max<int64_t>(2 * (int64_t)n_runs, 16)) + 1;
+    hmask = hc - 1;
+    hdir = tb.hdir.ensure<uint64_t>(hc);
+    SLIDE_CUDA(cudaMemsetAsync(hdir, 0xff, hc * 8, s));
+  }
+  int32_t* bstart = tb.bstart.ensure<int32_t>(std::max<int64_t>(n_runs, 1));
+  int32_t* blen = tb.blen.ensure<int32_t>(std::max<int64_t>(n_runs, 1));
+  int32_t* ovf = policy == 1 ? tb.ovf_cnt.ensure<int32_t>(std::max<int64_t>(n_runs, 1)) : nullptr;
+  if (n_runs > 0) {
+    runs_kernel<<<grid_for(n_runs), 256, 0, s>>>(uniq, counts, offsets, n_runs, cap, policy == 0, d.dense_dir,
+                                                 dir, hdir, hmask, bstart, blen, ovf);
+    SLIDE_LAUNCH_CHECK();
+  }
+  if (policy == 1 && n_runs > 0) {
+    // reservoir: host replay of the overflowing inserts (tables.py:156-161)
+    int32_t* ovf_off = tb.ovf_off.ensure<int32_t>(n_runs);
+    size_t b4 = 0;
+    SLIDE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b4, ovf, ovf_off, (int)n_runs, s));
+    if (b4 > tbytes) {
+      // temp grows; contents are not needed any more
+      temp = tb.temp.ensure<uint8_t>(b4);
+      tbytes = b4;
+    }
+    SLIDE_CUDA(cub::DeviceScan::ExclusiveSum(temp, tbytes, ovf, ovf_off, (int)n_runs, s));
+    int32_t last[2] = {0, 0};
+    SLIDE_CUDA(cudaMemcpyAsync(&last[0], ovf_off + n_runs - 1, 4, cudaMemcpyDeviceToHost, s));
+    SLIDE_CUDA(cudaMemcpyAsync(&last[1], ovf + n_runs - 1, 4, cudaMemcpyDeviceToHost, s));
+    SLIDE_CUDA(cudaStreamSynchronize(s));
+    int64_t n_ev = (int64_t)last[0] + last[1];
+    if (n_ev > 0) {
+      SLIDE_CHECK(mt_state != nullptr, kValueError, "reservoir build needs the random.Random state");
+      OvfEvent* ev = tb.ovf_ev.ensure<OvfEvent>(n_ev);
+      overflow_events_kernel<<<grid_for(n_runs), 256, 0, s>>>(uniq, counts, offsets, ovf, ovf_off, vb, n_runs,
+                                                               cap, kb, ev);
+      SLIDE_LAUNCH_CHECK();
+      std::vector<OvfEvent> h(n_ev);
+      SLIDE_CUDA(cudaMemcpyAsync(h.data(), ev, n_ev * sizeof(OvfEvent), cudaMemcpyDeviceToHost, s));
+      SLIDE_CUDA(cudaStreamSynchronize(s));
+      std::sort(h.begin(), h.end(), [](const OvfEvent& a, const OvfEvent& b) {
+        return a.table != b.table ? a.table < b.table : a.id < b.id;
+      });
+      Mt19937 mt;
+      mt.load(mt_state);
+      std::vector<int2> patches;
+      patches.reserve(n_ev / 4 + 16);
+      for (const OvfEvent& e : h) {
+        if (mt.random() * (double)e.count < (double)cap) {
+          int slot = (int)(mt.random() * (double)cap);
+          patches.push_back(make_int2(e.off + slot, e.id));
+        }
+      }
+      mt.store(mt_state);
+      if (!patches.empty()) {
+        // later patches to the same slot win: apply in order on one thread
+        // block per unique position is unnecessary -- dedupe on the host
+        std::vector<int2> last_w;
+        last_w.reserve(patches.size());
+        std::stable_sort(patches.begin(), patches.end(), [](const int2& a, const int2& b) { return a.x < b.x; });
+        for (size_t q = 0; q < patches.size(); ++q)
+          if (q + 1 == patches.size() || patches[q + 1].x != patches[q].x) last_w.push_back(patches[q]);
+        int2* dp = tb.patch.ensure<int2>(last_w.size());
+        SLIDE_CUDA(cudaMemcpyAsync(dp, last_w.data(), last_w.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+        patch_kernel<<<grid_for((int64_t)last_w.size()), 256, 0, s>>>(dp, (int64_t)last_w.size(), vb);
+        SLIDE_LAUNCH_CHECK();
+        SLIDE_CUDA(cudaStreamSynchronize(s));  // host vector lifetime
+      }
+    }
+  }
+  d.dir = dir;
+  d.hdir = hdir;
+  d.hash_mask = hmask;
+  d.bstart = bstart;
+  d.blen = blen;
+  d.bcount = counts;
+  d.ids = vb;
+  d.empty = n_runs == 0;
+  d.disabled = 0;
+  tb.n_items = n;
+  tb.n_slots = total;
+  tb.policy = policy;
+  tb.built = true;
+}
+
+void tables_load(TablesHost& tb, const uint32_t* skeys, const int32_t* counts, const int32_t* starts,
+                 const int32_t* lens, int64_t n_runs, const int32_t* ids, int64_t n_slots, int64_t n_items, int l,
+                 int kb, int cap, cudaStream_t s) {
+  uint32_t* uniq = tb.uniq.ensure<uint32_t>(std::max<int64_t>(n_runs, 1));
+  int32_t* cnt = tb.counts.ensure<int32_t>(std::max<int64_t>(n_runs, 1));
+  int32_t* bstart = tb.bstart.ensure<int32_t>(std::max<int64_t>(n_runs, 1));
+  int32_t* blen = tb.blen.ensure<int32_t>(std::max<int64_t>(n_runs, 1));
+  int32_t* vb = tb.vals_b.ensure<int32_t>(std::max<int64_t>(n_slots, 1));
+  if (n_runs) {
+    SLIDE_CUDA(cudaMemcpyAsync(uniq, skeys, n_runs * 4, cudaMemcpyHostToDevice, s));
+    SLIDE_CUDA(cudaMemcpyAsync(cnt, counts, n_runs * 4, cudaMemcpyHostToDevice, s));
+    SLIDE_CUDA(cudaMemcpyAsync(bstart, starts, n_runs * 4, cudaMemcpyHostToDevice, s));
+    SLIDE_CUDA(cudaMemcpyAsync(blen, lens, n_runs * 4, cudaMemcpyHostToDevice, s));
+  }
+  if (n_slots) SLIDE_CUDA(cudaMemcpyAsync(vb, ids, n_slots * 4, cudaMemcpyHostToDevice, s));
+  TablesDev& d = tb.dev;
+  d.l = l;
+  d.key_bits = kb;
+  d.cap = cap;
+  d.n_runs = n_runs;
+  d.dense_dir = kb <= 16;
+  d.dir = nullptr;
+  d.hdir = nullptr;
+  d.hash_mask = 0;
+  if (d.dense_dir) {
+    size_t nd = (size_t)l << kb;
+    int32_t* dir = tb.dir.ensure<int32_t>(nd);
+    SLIDE_CUDA(cudaMemsetAsync(dir, 0xff, nd * 4, s));
+    d.dir = dir;
+  } else {
+    uint64_t hc = gen_mask((uint64_t)std::max<int64_t>(2 * n_runs, 16)) + 1;
+    uint64_t* hdir = tb.hdir.ensure<uint64_t>(hc);
+    SLIDE_CUDA(cudaMemsetAsync(hdir, 0xff, hc * 8, s));
+    d.hdir = hdir;
+    d.hash_mask = hc - 1;
+  }
+  if (n_runs) {
+    dir_kernel<<<grid_for(n_runs), 256, 0, s>>>(uniq, n_runs, d.dense_dir, tb.dir.as<int32_t>(), tb.hdir.as<uint64_t>(),
+                                                d.hash_mask);
+    SLIDE_LAUNCH_CHECK();
+  }
+  SLIDE_CUDA(cudaStreamSynchronize(s));  // host arrays may go away
+  d.bstart = bstart;
+  d.blen = blen;
+  d.bcount = cnt;
+  d.ids = vb;
+  d.empty = n_runs == 0;
+  d.disabled = 0;
+  tb.n_items = n_items;
+  tb.built = true;
+}
+
+}  // namespace slide

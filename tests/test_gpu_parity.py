@@ -1,0 +1,336 @@
+"""Device parity: every stage of the CUDA path against the reference's golden
+vectors and the CPU oracle on identical (float32) state.
+
+Tolerances (north_star): hash keys, bucket contents and active sets
+bit-exact; logits / probabilities / loss 1e-5 relative; weights and Adam
+state after a step 1e-4 relative.
+"""
+
+import random
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import slide_oracle as O  # noqa: E402
+from paper_1903_03129_b200 import (  # noqa: E402
+    HashFamilyConfig,
+    LshLayerConfig,
+    LshTables,
+    SamplerConfig,
+    SlideNetwork,
+    SparseVector,
+    TrainConfig,
+    new_hash_family,
+)
+from paper_1903_03129_b200.network import HostCsr, csr_from_batch  # noqa: E402
+from tests.parity_util import assert_state_close, oracle_lsh_from_net, oracle_state_from_net  # noqa: E402
+
+HASH_SPECS = {
+    "sh_main": dict(family="simhash", k_per_table=9, num_tables=50, dim=128, seed=7919 * 2),
+    "sh_small": dict(family="simhash", k_per_table=2, num_tables=4, dim=24, seed=5),
+    "sh_full": dict(family="simhash", k_per_table=4, num_tables=2, dim=6, simhash_sparsity=1.0, seed=11),
+    "dw_main": dict(family="dwta", k_per_table=8, num_tables=50, dim=128, wta_bin_size=8, seed=7919 * 2),
+    "dw_small": dict(family="dwta", k_per_table=2, num_tables=1, dim=9, wta_bin_size=3, seed=5),
+    "dw_ragged": dict(family="dwta", k_per_table=2, num_tables=3, dim=10, wta_bin_size=4, seed=1),
+    "dw_scaled": dict(family="dwta", k_per_table=8, num_tables=64, dim=256, wta_bin_size=8, seed=7919 * 2),
+}
+
+
+@pytest.mark.parametrize("name", sorted(HASH_SPECS))
+def test_device_hash_keys_match_reference(golden, name):
+    g = golden("hashing")
+    fam = new_hash_family(HashFamilyConfig(**HASH_SPECS[name]))
+    np.testing.assert_array_equal(fam.hash_batch(g[name + "_w"]), g[name + "_wkeys"])
+    q = g[name + "_q"]
+    np.testing.assert_array_equal(fam.hash_dense_rows(q), g[name + "_qkeys"])
+    for row in (0, 1, 2, 5):
+        np.testing.assert_array_equal(fam.hash(SparseVector.from_dense(q[row])), g[name + "_qkeys"][row])
+
+
+def test_wta_dense_equals_dwta_on_dense_inputs():
+    rng = np.random.default_rng(3)
+    wta = new_hash_family(HashFamilyConfig("wta", 3, 2, 12, wta_bin_size=4, seed=13))
+    dwta = new_hash_family(HashFamilyConfig("dwta", 3, 2, 12, wta_bin_size=4, seed=13))
+    x = rng.standard_normal((20, 12)).astype(np.float32).astype(np.float64)
+    x[x == 0] = 0.5
+    np.testing.assert_array_equal(wta.hash_batch(x), dwta.hash_batch(x))
+
+
+def _golden_tables(g, prefix):
+    out = {}
+    for i in range(len(g[prefix + "t"])):
+        a, b = g[prefix + "ptr"][i], g[prefix + "ptr"][i + 1]
+        out[(int(g[prefix + "t"][i]), int(g[prefix + "key"][i]))] = (g[prefix + "slots"][a:b].tolist(),
+                                                                      int(g[prefix + "count"][i]))
+    return out
+
+
+def _device_tables(tbl):
+    return {(t, k): (list(b.slots), b.count) for t, view in enumerate(tbl.tables) for k, b in view.items()}
+
+
+@pytest.mark.parametrize("policy", ["fifo", "reservoir"])
+def test_device_tables_match_reference(golden, policy):
+    g = golden("tables")
+    fam = new_hash_family(HashFamilyConfig("simhash", 2, 5, 24, seed=5))
+    tbl = LshTables(fam, policy=policy, capacity=16, seed=104729 * 2)
+    w = g[policy + "_w"]
+    tbl.build(w)
+    assert _device_tables(tbl) == _golden_tables(g, f"{policy}_b1_")
+    tbl.build(w[::-1].copy())  # reservoir stream continues across builds
+    assert _device_tables(tbl) == _golden_tables(g, f"{policy}_b2_")
+
+
+def test_device_dwta_reservoir_tables(golden):
+    g = golden("tables")
+    fam = new_hash_family(HashFamilyConfig("dwta", 8, 10, 128, wta_bin_size=8, seed=9))
+    tbl = LshTables(fam, policy="reservoir", capacity=128, seed=1)
+    tbl.build(g["dwta_w"])
+    assert _device_tables(tbl) == _golden_tables(g, "dwta_")
+
+
+def test_query_self_collision_and_probe_count():
+    rng = np.random.default_rng(3)
+    fam = new_hash_family(HashFamilyConfig("simhash", 2, 6, 24, seed=5))
+    tbl = LshTables(fam)
+    w = rng.standard_normal((8, 24)).astype(np.float32)
+    tbl.build(w)
+    raw = tbl.query(SparseVector.from_dense(w[4]))
+    assert len(raw.per_table) == 6
+    assert all(4 in ids for ids in raw.per_table)
+
+
+NET_SETUPS = {
+    "sh": (50, 16, 40, LshLayerConfig("simhash", k=3, l=6, capacity=8, sampler=SamplerConfig("vanilla", beta=10)), 6, 2),
+    "shtopk": (50, 16, 40, LshLayerConfig("simhash", k=3, l=6, capacity=8, sampler=SamplerConfig("topk", beta=7)), 6, 2),
+    "dw": (40, 12, 60, LshLayerConfig("dwta", k=2, l=5, capacity=4, policy="reservoir", wta_bin_size=4,
+                                       sampler=SamplerConfig("vanilla", beta=6)), 5, 2),
+    "dwth": (40, 12, 60, LshLayerConfig("dwta", k=2, l=5, capacity=4, policy="reservoir", wta_bin_size=4,
+                                         sampler=SamplerConfig("hard_threshold", beta=6, min_freq=2)), 5, 2),
+    "dense": (20, 8, 12, None, 4, 50),
+}
+
+
+def _golden_batch(g, name, it, B):
+    return [(g[f"{name}_it{it}_x{i}_idx"], g[f"{name}_it{it}_x{i}_val"], g[f"{name}_it{it}_y{i}"].tolist())
+            for i in range(B)]
+
+
+@pytest.mark.parametrize("mode", ["sequential", "snapshot"])
+@pytest.mark.parametrize("name", sorted(NET_SETUPS))
+def test_train_steps_match_oracle(golden, name, mode):
+    """Three steps (a rebuild after step 2, an empty input in step 2) from the
+    same f32 state: active sets exact, loss 1e-5, state 1e-4."""
+    g = golden("network")
+    D, H, N, spec, B, n0 = NET_SETUPS[name]
+    cfg = TrainConfig(batch_size=B, seed=3, learning_rate=1e-2, n0=n0)
+    net = SlideNetwork(D, [H, N], cfg, lsh_layers={1: spec} if spec else None)
+    st = oracle_state_from_net(net)
+    lsh = oracle_lsh_from_net(net, spec, st) if spec else None
+    # the f32 initial weights equal the reference's f64 draws rounded
+    np.testing.assert_allclose(st.w2, g[f"{name}_init_l1_w"], rtol=1e-7, atol=0)
+    acfg = O.AdamCfg(lr=1e-2)
+    for it in range(1, 4):
+        trip = _golden_batch(g, name, it, B)
+        want = O.train_step(st, lsh, trip, it, cfg.seed, N, acfg, mode=mode)
+        batch = [(SparseVector(xi, xv, D), set(y)) for xi, xv, y in trip]
+        # capture the device active sets through a readout after each step
+        got = net.train_batch(batch, it, schedule=mode)
+        assert got.loss == pytest.approx(float(np.mean(want.losses)), rel=1e-5)
+        assert got.rebuilt == ([1] if (spec and want.rebuilt) else [])
+        assert_state_close(net, st, what=f"{name} {mode} it{it}")
+
+
+def _stage_forward(net, csr, iteration):
+    from paper_1903_03129_b200 import _lib
+
+    bt, keep = net._upload(csr)
+    n = _lib.i64()
+    _lib.call("slide_forward", net._ctx, _lib.C.byref(bt), iteration, 0, _lib.C.byref(n))
+    B, hp, L = csr.batch, net.hidden_pad, net.layers[1].lsh.family.l
+    out = {
+        "h": net._read(0, B * hp, np.float32).reshape(B, hp)[:, : net.hidden],
+        "keys": net._read(1, B * L, np.uint32).reshape(B, L).astype(np.int64),
+        "offs": net._read(2, B + 1, np.int32),
+        "rows": net._read(3, n.value, np.int32),
+        "probs": net._read(5, n.value, np.float32),
+        "logits": net._read(11, n.value, np.float32),
+        "loss": net._read(7, B, np.float64),
+    }
+    return out, keep
+
+
+def test_tiny_config_stage_by_stage():
+    """BASELINE configs[0] shape: each stage of one snapshot step against the
+    oracle fed the device's own upstream values."""
+    from paper_1903_03129_b200 import _lib
+    from paper_1903_03129_b200.configs import TINY as w
+    from paper_1903_03129_b200.data import synthetic_corpus
+
+    corpus = synthetic_corpus(w.corpus, w.batch, seed=0)
+    cfg = TrainConfig(batch_size=w.batch, seed=0, learning_rate=w.lr, n0=w.n0)
+    spec = LshLayerConfig("simhash", k=w.k, l=w.l, capacity=w.cap, sampler=SamplerConfig("vanilla", beta=w.beta))
+    net = SlideNetwork(w.input_dim, [w.hidden, w.n_out], cfg, lsh_layers={1: spec})
+    st = oracle_state_from_net(net)
+    lsh = oracle_lsh_from_net(net, spec, st)
+    csr = HostCsr(corpus.x_ptr.astype(np.int32), corpus.x_idx, corpus.x_val, corpus.y_ptr.astype(np.int32), corpus.y_idx)
+    got, keep = _stage_forward(net, csr, 1)
+    trip = corpus.triples()
+    for i, (xi, xv, y) in enumerate(trip):
+        rng = np.random.default_rng((0, 1, i))
+        tr = O.slot_forward(st, lsh, xi, xv, y, rng, w.n_out)
+        np.testing.assert_allclose(got["h"][i], tr.h, rtol=1e-5, atol=1e-6)
+        hd = got["h"][i].astype(np.float64)  # the device's own h
+        keys = O.simhash_keys(lsh.params, hd[None, :])[0]
+        np.testing.assert_array_equal(got["keys"][i], keys)
+        per_table = O.probe(lsh.buckets, keys)
+        samp = O.sampled_ids(per_table, "vanilla", w.beta, 1, np.random.default_rng((0, 1, i)))
+        active = np.union1d(samp, y) if samp.size else None
+        a, b = got["offs"][i], got["offs"][i + 1]
+        if active is not None:
+            np.testing.assert_array_equal(got["rows"][a:b], active)
+        np.testing.assert_array_equal(got["rows"][a:b], tr.active)
+        np.testing.assert_allclose(got["probs"][a:b], tr.probs, rtol=1e-5, atol=1e-9)
+        assert got["loss"][i] == pytest.approx(tr.loss, rel=1e-5)
+    # full snapshot step
+    _lib.call("slide_backward", net._ctx, 1)
+    torch.cuda.synchronize()
+    O.train_step(st, lsh, trip, 1, 0, w.n_out, O.AdamCfg(lr=w.lr), mode="snapshot")
+    assert_state_close(net, st, what="tiny snapshot")
+
+
+def test_forward_emulates_the_callers_generator():
+    cfg = TrainConfig(batch_size=2, seed=5)
+    spec = LshLayerConfig(k=2, l=4, sampler=SamplerConfig(beta=4))
+    net = SlideNetwork(6, [5, 30], cfg, lsh_layers={1: spec})
+    x = SparseVector(np.array([0, 3]), np.array([1.0, 2.0]), 6)
+    r_dev = np.random.default_rng(11)
+    r_ref = np.random.default_rng(11)
+    tr = net.forward(x, 1, labels={7}, rng=r_dev)
+    st = oracle_state_from_net(net)
+    lsh = oracle_lsh_from_net(net, spec, st)
+    want = O.slot_forward(st, lsh, x.indices, x.values, [7], r_ref, 30)
+    np.testing.assert_array_equal(tr.active[-1], want.active)
+    assert r_dev.bit_generator.state == r_ref.bit_generator.state
+    assert r_dev.random() == r_ref.random()
+
+
+def test_empty_buckets_fall_back_to_random_plus_labels():
+    cfg = TrainConfig(batch_size=3, seed=5)
+    spec = LshLayerConfig(k=2, l=2, sampler=SamplerConfig(beta=4))
+    net = SlideNetwork(4, [4, 30], cfg, lsh_layers={1: spec})
+    for tbl in net.layers[1].lsh.tables:
+        tbl.clear()
+    x = SparseVector(np.array([0, 1]), np.array([1.0, 1.0]), 4)
+    r1, r2 = np.random.default_rng(1), np.random.default_rng(1)
+    tr = net.forward(x, 0, labels={7}, rng=r1)
+    assert 7 in tr.active[-1]
+    assert tr.active[-1].size >= 4
+    want = np.union1d(r2.choice(30, size=4, replace=False), [7])
+    np.testing.assert_array_equal(tr.active[-1], want)
+    assert r1.bit_generator.state == r2.bit_generator.state
+
+
+@pytest.mark.parametrize("beta", [128, 3000])
+def test_large_fallback_sets_match_numpy(beta):
+    """Floyd (beta small) and tail-shuffle (beta > N/50, N > 10000) branches
+    of numpy's choice(), replayed on the device."""
+    cfg = TrainConfig(batch_size=4, seed=9)
+    spec = LshLayerConfig("dwta", k=2, l=3, capacity=4, wta_bin_size=4, sampler=SamplerConfig(beta=beta))
+    n_out = 20000
+    net = SlideNetwork(8, [8, n_out], cfg, lsh_layers={1: spec})
+    for tbl in net.layers[1].lsh.tables:
+        tbl.clear()
+    batch = [(SparseVector(np.array([i]), np.array([1.0]), 8), {i}) for i in range(4)]
+    csr = csr_from_batch(batch, 8, n_out)
+    got, keep = _stage_forward(net, csr, 3)
+    for i in range(4):
+        r = np.random.default_rng((9, 3, i))
+        r.permutation(3)
+        want = np.union1d(r.choice(n_out, size=beta, replace=False), [i])
+        np.testing.assert_array_equal(got["rows"][got["offs"][i]: got["offs"][i + 1]], want)
+
+
+def test_hand_computed_forward_and_views():
+    net = SlideNetwork(2, [3, 2], TrainConfig(batch_size=1))
+    w1 = np.array([[1.0, 2.0], [10.0, 10.0], [0.5, -1.0]])
+    w2 = np.array([[1.0, 5.0, 2.0], [-1.0, 5.0, 1.0]])
+    net.layers[0].w[:] = w1
+    net.layers[0].b[:] = np.array([0.1, 0.0, 0.2])
+    net.layers[1].w[:] = w2
+    net.layers[1].b[:] = 0.0
+    x = SparseVector.from_dense([1.0, 1.0])
+    # hidden unit 1 forced off by a large negative bias instead of a forced set
+    net.layers[0].b[1] = -1000.0
+    trace = net.forward(x, 0)
+    h0 = 1.0 * 1 + 2.0 * 1 + 0.1
+    assert net.layers[0].activations[0, 0] == pytest.approx(h0, rel=1e-6)
+    z = np.array([w2[0, 0] * h0, w2[1, 0] * h0])
+    e = np.exp(z - z.max())
+    np.testing.assert_allclose(trace.probs, e / e.sum(), rtol=1e-5)
+
+
+def test_empty_input_and_dead_hidden_layer_match_oracle():
+    cfg = TrainConfig(batch_size=3, seed=2, learning_rate=1e-2)
+    spec = LshLayerConfig("simhash", k=2, l=3, capacity=4, sampler=SamplerConfig(beta=5))
+    net = SlideNetwork(10, [6, 20], cfg, lsh_layers={1: spec})
+    net.layers[0].b[:] = np.array([0.3, -5.0, 0.2, -5.0, 0.1, 0.4])
+    st = oracle_state_from_net(net)
+    lsh = oracle_lsh_from_net(net, spec, st)
+    batch = [(SparseVector(np.empty(0, np.int64), np.empty(0), 10), {1}),
+             (SparseVector(np.array([2, 5]), np.array([1.0, 0.5]), 10), {3, 4}),
+             (SparseVector(np.array([7]), np.array([0.25]), 10), {19})]
+    trip = [(x.indices, x.values, sorted(y)) for x, y in batch]
+    for it, mode in ((1, "snapshot"), (2, "sequential")):
+        want = O.train_step(st, lsh, trip, it, cfg.seed, 20, O.AdamCfg(lr=1e-2), mode=mode)
+        got = net.train_batch(batch, it, schedule=mode)
+        assert got.loss == pytest.approx(float(np.mean(want.losses)), rel=1e-5)
+        assert_state_close(net, st, what=f"edge {mode}")
+    # all hidden units dead: only output biases move, hidden layer untouched
+    net.layers[0].b[:] = -50.0
+    st = oracle_state_from_net(net)
+    want = O.train_step(st, lsh, trip, 3, cfg.seed, 20, O.AdamCfg(lr=1e-2), mode="snapshot")
+    net.train_batch(batch, 3, schedule="snapshot")
+    assert_state_close(net, st, what="dead hidden")
+
+
+def test_snapshot_step_is_deterministic():
+    from paper_1903_03129_b200.configs import TINY as w
+    from paper_1903_03129_b200.data import synthetic_corpus
+
+    corpus = synthetic_corpus(w.corpus, w.batch, seed=4)
+    csr = HostCsr(corpus.x_ptr.astype(np.int32), corpus.x_idx, corpus.x_val, corpus.y_ptr.astype(np.int32), corpus.y_idx)
+    outs = []
+    for _ in range(2):
+        cfg = TrainConfig(batch_size=w.batch, seed=0, learning_rate=w.lr)
+        spec = LshLayerConfig("simhash", k=w.k, l=w.l, capacity=w.cap, sampler=SamplerConfig("vanilla", beta=w.beta))
+        net = SlideNetwork(w.input_dim, [w.hidden, w.n_out], cfg, lsh_layers={1: spec})
+        for it in (1, 2, 3):
+            net.train_batch_csr(csr, it, schedule="snapshot")
+        outs.append((net.w2.cpu().numpy().copy(), net.w1t.cpu().numpy().copy(), net.m2.cpu().numpy().copy()))
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_backward_capture_matches_finite_differences_shape():
+    """backward(update=False, capture=...) returns the reference's capture
+    tuples; gradients equal the oracle's on the same trace."""
+    cfg = TrainConfig(batch_size=2, seed=4)
+    net = SlideNetwork(6, [7, 9], cfg)
+    rng = np.random.default_rng(0)
+    x = SparseVector(np.arange(6), rng.standard_normal(6).astype(np.float32), 6)
+    trace = net.forward(x, 0, labels={2, 5})
+    cap = []
+    net.backward(trace, {2, 5}, 0, update=False, capture=cap)
+    st = oracle_state_from_net(net)
+    tr = O.slot_forward(st, None, x.indices, x.values, [2, 5], np.random.default_rng(0), 9)
+    g = O.slot_backward(st, tr, [2, 5])
+    li, rows, cols, grad, delta = cap[0]
+    assert li == 1
+    np.testing.assert_allclose(delta, g.delta, rtol=1e-5, atol=1e-7)
+    if g.dh is not None:
+        assert cap[1][0] == 0
+        np.testing.assert_allclose(cap[1][4], g.dh, rtol=1e-4, atol=1e-6)
