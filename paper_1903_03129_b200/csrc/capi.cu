@@ -356,10 +356,14 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     uint64_t* states = c->states.ensure<uint64_t>((size_t)b * 6);
     uint8_t* order = c->order.ensure<uint8_t>((size_t)b * L);
     const int vanilla = d.strategy == 0;
-    launch_slot_rng(b, d.seed, iteration, slot_offset, L, vanilla, bt->rng_states, states, order, s);
-    c->timer.mark(s, kStSlotRng);
     const int64_t want = std::min<int64_t>(d.beta, d.n_out);
     const int64_t lcap = (int64_t)L * d.capacity;
+    // vanilla with beta >= L*cap probes every table whatever the order: the
+    // slot stream is only needed by the (rare) fallback, which derives it
+    const bool full_union = vanilla && d.beta >= lcap;
+    const bool rng_first = !full_union || bt->rng_states;
+    if (rng_first) launch_slot_rng(b, d.seed, iteration, slot_offset, L, vanilla, bt->rng_states, states, order, s);
+    c->timer.mark(s, kStSlotRng);
     cap_max = std::max<int64_t>(lcap, want) + max_labels;
     act = c->act.ensure<int32_t>((size_t)b * cap_max);
     SelectArgs a;
@@ -373,7 +377,7 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     a.y_idx = bt->y_idx;
     a.b = b;
     a.l = L;
-    a.strategy = (int)d.strategy;
+    a.strategy = full_union ? 3 : (int)d.strategy;
     a.beta = (int)std::min<int64_t>(d.beta, INT32_MAX);
     a.min_freq = (int)d.min_freq;
     a.sort_bits = bits_for(d.n_out) + 7;
@@ -388,6 +392,12 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     FallbackArgs f;
     f.empty = empty;
     f.states = states;
+    f.states_ready = rng_first;
+    f.seed = d.seed;
+    f.iteration = iteration;
+    f.slot_offset = slot_offset;
+    f.l = L;
+    f.vanilla = vanilla;
     f.n = d.n_out;
     f.want = want;
     f.fb_ids = c->fb_ids.ensure<int64_t>((size_t)b * want);

@@ -60,10 +60,8 @@ __global__ void __launch_bounds__(256) simhash_kernel(SimHashDev f, const float*
   }
 }
 
-void launch_simhash_keys(const SimHashDev& f, const float* x, int64_t n, int ld, uint32_t* keys,
-                         cudaStream_t s) {
-  if (n <= 0) return;
-  constexpr int ROWS = 8;
+template <int ROWS>
+static void launch_simhash_t(const SimHashDev& f, const float* x, int64_t n, int ld, uint32_t* keys, cudaStream_t s) {
   const int KL = f.k * f.l;
   size_t smem = (size_t)ROWS * f.dim * 4 + (size_t)((KL * f.c + 1) & ~1) * 2 + (size_t)ROWS * KL;
   SLIDE_CHECK(smem <= 227 * 1024, kNotSupported, "simhash tables too large for shared memory");
@@ -73,6 +71,14 @@ void launch_simhash_keys(const SimHashDev& f, const float* x, int64_t n, int ld,
   int grid = (int)std::min<int64_t>(blocks, (int64_t)kSms * 4);
   simhash_kernel<ROWS><<<grid, 256, smem, s>>>(f, x, n, ld, keys);
   SLIDE_LAUNCH_CHECK();
+}
+
+void launch_simhash_keys(const SimHashDev& f, const float* x, int64_t n, int ld, uint32_t* keys,
+                         cudaStream_t s) {
+  if (n <= 0) return;
+  // few rows (per-sample queries): one row per CTA fills the SMs
+  if (n <= (int64_t)kSms * 8) launch_simhash_t<1>(f, x, n, ld, keys, s);
+  else launch_simhash_t<8>(f, x, n, ld, keys, s);
 }
 
 // ------------------------------------------------------------------- DWTA
@@ -144,10 +150,8 @@ __global__ void __launch_bounds__(256) dwta_kernel(DwtaDev f, const float* __res
   }
 }
 
-void launch_dwta_keys(const DwtaDev& f, const float* x, int64_t n, int ld, uint32_t* keys,
-                      cudaStream_t s) {
-  if (n <= 0) return;
-  constexpr int ROWS = 8;
+template <int ROWS>
+static void launch_dwta_t(const DwtaDev& f, const float* x, int64_t n, int ld, uint32_t* keys, cudaStream_t s) {
   const int KL = f.k * f.l;
   size_t smem = (size_t)ROWS * f.dim * 4 + (size_t)((f.n_perms * f.dim + 1) & ~1) * 2 + (size_t)2 * ROWS * KL;
   SLIDE_CHECK(smem <= 227 * 1024, kNotSupported, "dwta tables too large for shared memory");
@@ -156,6 +160,12 @@ void launch_dwta_keys(const DwtaDev& f, const float* x, int64_t n, int ld, uint3
   int grid = (int)std::min<int64_t>(blocks, (int64_t)kSms * 4);
   dwta_kernel<ROWS><<<grid, 256, smem, s>>>(f, x, n, ld, keys);
   SLIDE_LAUNCH_CHECK();
+}
+
+void launch_dwta_keys(const DwtaDev& f, const float* x, int64_t n, int ld, uint32_t* keys, cudaStream_t s) {
+  if (n <= 0) return;
+  if (n <= (int64_t)kSms * 8) launch_dwta_t<1>(f, x, n, ld, keys, s);
+  else launch_dwta_t<8>(f, x, n, ld, keys, s);
 }
 
 }  // namespace slide

@@ -10,6 +10,7 @@ namespace slide {
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  // grows geometrically (x1.5) so steady-state steps never reallocate
   template <typename T>
   T* ensure(size_t n) {
     size_t need = n * sizeof(T);
@@ -17,8 +18,11 @@ struct DBuf {
     if (need > bytes) {
       if (p) SLIDE_CUDA(cudaFree(p));
       p = nullptr;
-      SLIDE_CUDA(cudaMalloc(&p, need));
-      bytes = need;
+      size_t grow = bytes ? bytes + bytes / 2 : 0;
+      size_t alloc = need > grow ? need : grow;
+      alloc = (alloc + 255) & ~(size_t)255;
+      SLIDE_CUDA(cudaMalloc(&p, alloc));
+      bytes = alloc;
     }
     return reinterpret_cast<T*>(p);
   }

@@ -21,6 +21,10 @@ struct SelectArgs {
 struct FallbackArgs {
   const int32_t* empty;
   uint64_t* states;
+  int states_ready;  // 0: derive default_rng((seed, iteration, slot)) (+ permutation(L) if vanilla)
+  uint64_t seed;
+  int64_t iteration, slot_offset;
+  int l, vanilla;
   int64_t n, want;
   int64_t* fb_ids;
   int64_t* scratch;

@@ -278,11 +278,49 @@ void launch_hidden_grad(int hp, int b, const int32_t* offs, const int32_t* prow,
 // order (the snapshot schedule): t = steps[r] + j + 1 for the
 // row's j-th sample; moments move only where h_i > 0; the bias always moves
 // (network.py:428-451).
-__device__ __forceinline__ void adam_coord(float& w, float& m, float& v, float g, float bc1, float bc2,
-                                           const AdamParams& ap) {
-  m = ap.b1 * m + (1.f - ap.b1) * g;
-  v = ap.b2 * v + (1.f - ap.b2) * g * g;
-  w -= ap.lr * (m / bc1) / (sqrtf(v / bc2) + ap.eps);
+// c1 = lr / (1 - b1^t), c2 = 1 / (1 - b2^t) (bias corrections in fp64, then
+// fp32): w -= c1 m / (sqrt(c2 v) + eps).  Approximate sqrt / divide (<= 2 ulp)
+// keep the update far inside the 1e-4 weight tolerance.
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// Hoisted optimizer constants (registers, not constant-bank reloads).
+struct AdamK {
+  float b1, omb1, b2, omb2, eps;
+  __device__ __forceinline__ explicit AdamK(const AdamParams& ap)
+      : b1(ap.b1), omb1(1.f - ap.b1), b2(ap.b2), omb2(1.f - ap.b2), eps(ap.eps) {}
+};
+
+__device__ __forceinline__ void adam_coord(float& w, float& m, float& v, float g, float c1, float c2,
+                                           const AdamK& k) {
+  m = fmaf(k.b1, m, k.omb1 * g);
+  v = fmaf(k.b2, v, k.omb2 * (g * g));
+  w -= (c1 * m) * rcp_approx(sqrt_approx(v * c2) + k.eps);
+}
+
+// predicated form: moments and weight move only when `on` (frozen otherwise)
+__device__ __forceinline__ void adam_coord_if(bool on, float& w, float& m, float& v, float g, float c1, float c2,
+                                              const AdamK& k) {
+  const float mn = fmaf(k.b1, m, k.omb1 * g);
+  const float vn = fmaf(k.b2, v, k.omb2 * (g * g));
+  const float wn = w - (c1 * mn) * rcp_approx(sqrt_approx(vn * c2) + k.eps);
+  m = on ? mn : m;
+  v = on ? vn : v;
+  w = on ? wn : w;
+}
+
+__device__ __forceinline__ float2 bias_corr(const AdamParams& ap, int64_t t) {
+  const double td = (double)t;
+  return make_float2((float)((double)ap.lr / (1.0 - pow(ap.b1d, td))), (float)(1.0 / (1.0 - pow(ap.b2d, td))));
 }
 
 template <int NV>
@@ -302,6 +340,7 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(int hp, AdamParams ap, c
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nu = *n_uniq;
+  const AdamK ak(ap);
   for (int64_t u = gw; u < nu; u += nw) {
     uint32_t tmask = 0;
     const int r = uniq[u];
@@ -321,35 +360,46 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(int hp, AdamParams ap, c
     for (int c0 = 0; c0 < len; c0 += 32) {
       const int j = c0 + lane;
       int slot_l = 0;
-      float d_l = 0.f, bc1_l = 1.f, bc2_l = 1.f;
+      float d_l = 0.f;
+      float2 bc_l = make_float2(0.f, 1.f);
       if (j < len) {
         const int p = sorted_pairs[s0 + j];
         slot_l = pslot[p];
         d_l = delta[p];
-        const double t = (double)(st + j + 1);
-        bc1_l = (float)(1.0 - pow(ap.b1d, t));
-        bc2_l = (float)(1.0 - pow(ap.b2d, t));
+        bc_l = bias_corr(ap, st + j + 1);
       }
       const int nc = min(32, len - c0);
+      // software pipeline: the next pair's h row is in flight during the math
+      float4 hn[NV];
+      {
+        const float* hr = h + (int64_t)__shfl_sync(0xffffffffu, slot_l, 0) * hp + lane * 4;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) hn[q] = ld4(hr + q * 128);
+      }
       for (int q2 = 0; q2 < nc; ++q2) {
-        const int slot = __shfl_sync(0xffffffffu, slot_l, q2);
+        float4 hv[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) hv[q] = hn[q];
         const float d = __shfl_sync(0xffffffffu, d_l, q2);
-        const float bc1 = __shfl_sync(0xffffffffu, bc1_l, q2);
-        const float bc2 = __shfl_sync(0xffffffffu, bc2_l, q2);
-        const float* hr = h + (int64_t)slot * hp + lane * 4;
+        const float c1 = __shfl_sync(0xffffffffu, bc_l.x, q2);
+        const float c2 = __shfl_sync(0xffffffffu, bc_l.y, q2);
+        const int nslot = __shfl_sync(0xffffffffu, slot_l, q2 + 1 < nc ? q2 + 1 : q2);
+        if (q2 + 1 < nc) {
+          const float* hr = h + (int64_t)nslot * hp + lane * 4;
+#pragma unroll
+          for (int q = 0; q < NV; ++q) hn[q] = ld4(hr + q * 128);
+        }
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
-          float4 hv = ld4(hr + q * 128);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const float hc = comp(hv, c);
-            if (hc > 0.f) {
-              adam_coord(comp(w[q], c), comp(m[q], c), comp(v[q], c), d * hc, bc1, bc2, ap);
-              tmask |= 1u << (q * 4 + c);
-            }
+            const float hc = comp(hv[q], c);
+            const bool on = hc > 0.f;
+            adam_coord_if(on, comp(w[q], c), comp(m[q], c), comp(v[q], c), d * hc, c1, c2, ak);
+            tmask |= (on ? 1u : 0u) << (q * 4 + c);
           }
         }
-        adam_coord(b, mb, vb, d, bc1, bc2, ap);
+        adam_coord(b, mb, vb, d, c1, c2, ak);
       }
     }
 #pragma unroll
@@ -412,27 +462,31 @@ void launch_x_slots(int b, const int32_t* x_ptr, int32_t* x_slot, cudaStream_t s
 // tc[i][c] = #{i' <= i : h_i'[c] > 0}; hidden unit c's step for sample i is
 // steps1[c] + tc[i][c] (each sample bumps the counter of its nz(h) rows,
 // network.py:436-437).  bc holds the two bias corrections.
+// One warp per hidden unit: ballot + popc prefix over the samples.
 __global__ void hidden_counts_kernel(int hp, int b, AdamParams ap, const float* __restrict__ h,
                                      const int64_t* __restrict__ steps1, int32_t* __restrict__ tc,
                                      float2* __restrict__ bc) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (c >= hp) return;
-  int cnt = 0;
   const int64_t st = steps1[c];
-  for (int i = 0; i < b; ++i) {
+  int run = 0;
+  for (int i0 = 0; i0 < b; i0 += 32) {
+    const int i = i0 + lane;
     const int64_t q = (int64_t)i * hp + c;
-    if (h[q] > 0.f) {
-      ++cnt;
-      const double t = (double)(st + cnt);
-      bc[q] = make_float2((float)(1.0 - pow(ap.b1d, t)), (float)(1.0 - pow(ap.b2d, t)));
+    const bool act = i < b && h[q] > 0.f;
+    const unsigned mask = __ballot_sync(0xffffffffu, act);
+    const int cnt = run + __popc(mask & ((1u << lane) - 1u)) + (act ? 1 : 0);
+    if (i < b) {
+      tc[q] = cnt;
+      if (act) bc[q] = bias_corr(ap, st + cnt);
     }
-    tc[q] = cnt;
+    run += __popc(mask);
   }
 }
 
 void launch_hidden_counts(int hp, int b, const AdamParams& ap, const float* h, const int64_t* steps1, int32_t* tc,
                           float2* bc, cudaStream_t s) {
-  hidden_counts_kernel<<<(int)ceil_div(hp, 128), 128, 0, s>>>(hp, b, ap, h, steps1, tc, bc);
+  hidden_counts_kernel<<<(int)ceil_div((int64_t)hp * 32, 256), 256, 0, s>>>(hp, b, ap, h, steps1, tc, bc);
   SLIDE_LAUNCH_CHECK();
 }
 
@@ -448,6 +502,7 @@ __global__ void __launch_bounds__(256) adam_features_kernel(
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nu = *n_uniq;
+  const AdamK ak(ap);
   for (int64_t u = gw; u < nu; u += nw) {
     uint32_t tmask = 0;
     const int f = uniq[u];
@@ -472,23 +527,42 @@ __global__ void __launch_bounds__(256) adam_features_kernel(
         xv_l = x_val[x_base + k];
       }
       const int nc = min(32, len - c0);
-      for (int q2 = 0; q2 < nc; ++q2) {
-        const int slot = __shfl_sync(0xffffffffu, slot_l, q2);
-        const float xv = __shfl_sync(0xffffffffu, xv_l, q2);
+      // the hidden error already carries the h > 0 mask (dh = 0 elsewhere);
+      // h itself decides which coordinates move
+      float4 hn[NV], gn[NV], bn[NV][2];
+      auto fetch = [&](int slot) {
         const int64_t base = (int64_t)slot * hp + lane * 4;
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
-          const float4 hv = ld4(h + base + q * 128);
-          const float4 gv = ld4(dh + base + q * 128);
+          hn[q] = ld4(h + base + q * 128);
+          gn[q] = ld4(dh + base + q * 128);
+          const float4* bp = reinterpret_cast<const float4*>(bc + base + q * 128);
+          bn[q][0] = __ldg(bp);
+          bn[q][1] = __ldg(bp + 1);
+        }
+      };
+      fetch(__shfl_sync(0xffffffffu, slot_l, 0));
+      for (int q2 = 0; q2 < nc; ++q2) {
+        float4 hv[NV], gv[NV], bv[NV][2];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          hv[q] = hn[q];
+          gv[q] = gn[q];
+          bv[q][0] = bn[q][0];
+          bv[q][1] = bn[q][1];
+        }
+        const float xv = __shfl_sync(0xffffffffu, xv_l, q2);
+        const int nslot = __shfl_sync(0xffffffffu, slot_l, q2 + 1 < nc ? q2 + 1 : q2);
+        if (q2 + 1 < nc) fetch(nslot);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          const float* bb = reinterpret_cast<const float*>(&bv[q][0]);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const float hc = reinterpret_cast<const float*>(&hv)[c];
-            if (hc > 0.f) {
-              const float2 bb = bc[base + q * 128 + c];
-              adam_coord(comp(w[q], c), comp(m[q], c), comp(v[q], c), reinterpret_cast<const float*>(&gv)[c] * xv,
-                         bb.x, bb.y, ap);
-              tmask |= 1u << (q * 4 + c);
-            }
+            const bool on = comp(hv[q], c) > 0.f;
+            adam_coord_if(on, comp(w[q], c), comp(m[q], c), comp(v[q], c), comp(gv[q], c) * xv, bb[2 * c],
+                          bb[2 * c + 1], ak);
+            tmask |= (on ? 1u : 0u) << (q * 4 + c);
           }
         }
       }
@@ -527,22 +601,38 @@ __global__ void adam_hidden_bias_kernel(int hp, int b, AdamParams ap, const floa
                                         const float2* __restrict__ bc, float* __restrict__ b1,
                                         float* __restrict__ mb1, float* __restrict__ vb1,
                                         int64_t* __restrict__ steps1) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per hidden unit: 32 samples' inputs loaded at once, the Adam
+  // recurrence then walks them in slot order (all lanes redundantly)
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (c >= hp || b <= 0) return;
+  const AdamK ak(ap);
   float bb = b1[c], mb = mb1[c], vb = vb1[c];
-  for (int i = 0; i < b; ++i) {
+  for (int i0 = 0; i0 < b; i0 += 32) {
+    const int i = i0 + lane;
     const int64_t q = (int64_t)i * hp + c;
-    if (h[q] > 0.f) adam_coord(bb, mb, vb, dh[q], bc[q].x, bc[q].y, ap);
+    const bool act = i < b && h[q] > 0.f;
+    const float g = act ? dh[q] : 0.f;
+    const float2 cc = act ? bc[q] : make_float2(0.f, 1.f);
+    unsigned mask = __ballot_sync(0xffffffffu, act);
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      adam_coord(bb, mb, vb, __shfl_sync(0xffffffffu, g, src), __shfl_sync(0xffffffffu, cc.x, src),
+                 __shfl_sync(0xffffffffu, cc.y, src), ak);
+    }
   }
-  b1[c] = bb;
-  mb1[c] = mb;
-  vb1[c] = vb;
-  steps1[c] += tc[(int64_t)(b - 1) * hp + c];
+  if (lane == 0) {
+    b1[c] = bb;
+    mb1[c] = mb;
+    vb1[c] = vb;
+    steps1[c] += tc[(int64_t)(b - 1) * hp + c];
+  }
 }
 
 void launch_adam_hidden_bias(int hp, int b, const AdamParams& ap, const float* h, const float* dh, const int32_t* tc,
                              const float2* bc, float* b1, float* mb1, float* vb1, int64_t* steps1, cudaStream_t s) {
-  adam_hidden_bias_kernel<<<(int)ceil_div(hp, 128), 128, 0, s>>>(hp, b, ap, h, dh, tc, bc, b1, mb1, vb1, steps1);
+  adam_hidden_bias_kernel<<<(int)ceil_div((int64_t)hp * 32, 256), 256, 0, s>>>(hp, b, ap, h, dh, tc, bc, b1, mb1,
+                                                                               vb1, steps1);
   SLIDE_LAUNCH_CHECK();
 }
 

@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
       if (f == F) return eqc++ < need;
       return false;
     }
+    if (a.strategy == 3) return true;  // vanilla with beta >= L*cap: every table is probed
     return f >= a.min_freq;
   };
   {
@@ -279,7 +280,16 @@ __global__ void __launch_bounds__(256) fallback_kernel(FallbackArgs a) {
   int64_t* ids = a.fb_ids + (int64_t)i * a.want;
   if (tid == 0) {
     Pcg64 g;
-    g.load(a.states + 6 * i);
+    if (a.states_ready) {
+      g.load(a.states + 6 * i);
+    } else {  // slot stream not drawn yet (full-union vanilla): seed + probe order first
+      uint64_t ent[3] = {a.seed, (uint64_t)a.iteration, (uint64_t)(a.slot_offset + i)};
+      g.seed_from(ent, 3);
+      if (a.vanilla) {
+        uint8_t perm[64];
+        pcg_permutation(g, perm, a.l);
+      }
+    }
     int64_t* scratch = a.smem_scratch ? fb_smem : a.scratch + (int64_t)i * a.scratch_per_slot;
     pcg_choice(g, a.n, a.want, ids, scratch);
     g.store(a.states + 6 * i);

@@ -504,6 +504,8 @@ class SlideNetwork:
         return self._barrier(iteration, loss, active)
 
     def _step(self, csr: HostCsr, iteration: int, sub_batch: int):
+        if self.layers[1].lsh is not None:
+            self.layers[1].lsh.sync_to_device()
         bt, keep = self._upload(csr)
         B = csr.batch
         loss = np.empty(B, dtype=np.float64)
