@@ -63,13 +63,18 @@ struct slide_ctx {
   DBuf h, qkeys, order, states, act, cnt, empty, offs, prow, pslot, plab, z, prob, delta, loss, dh;
   DBuf fb_ids, fb_scratch, fb_bitmap;
   // backward workspace
-  DBuf iota, sk_out, sv_out, uniq, ucnt, uoff, nuniq, temp;
-  DBuf xslot, fkeys_out, fvals_out, funiq, fucnt, fuoff, fnuniq, tc, bc;
+  GroupBy grow, gfeat;
+  bool grow_pending = false;  // grow holds a forward's grouping not yet cleared
+  bool use_rows_dh = false;
+  DBuf xslot, tc, bc, partial;
   int64_t fb_bitmap_words = 0;
+  double* pinned_loss = nullptr;
+  int32_t* pinned_cnt = nullptr;
+  int64_t pinned_n = 0;
   // last forward
   bool have_forward = false;
   int last_b = 0;
-  int64_t last_P = 0, last_nnz = 0, last_xbase = 0;
+  int64_t last_P = 0, last_Pmax = 0, last_nnz = 0, last_xbase = 0;
   const int32_t* last_xptr = nullptr;
   const int32_t* last_xidx = nullptr;
   const float* last_xval = nullptr;
@@ -135,6 +140,17 @@ static DwtaDev dwta_of(slide_ctx* c) {
   return f;
 }
 
+// pair count of the last forward (synchronises; API / test paths only)
+static int64_t host_pairs(slide_ctx* c) {
+  if (c->last_P < 0) {
+    int32_t p = 0;
+    SLIDE_CUDA(cudaMemcpyAsync(&p, c->offs.as<int32_t>() + c->last_b, 4, cudaMemcpyDeviceToHost, c->s));
+    SLIDE_CUDA(cudaStreamSynchronize(c->s));
+    c->last_P = p;
+  }
+  return c->last_P;
+}
+
 static void hash_rows(slide_ctx* c, const float* x, int64_t n, uint32_t* keys) {
   if (c->d.family == 1) launch_simhash_keys(simhash_of(c), x, n, c->hp, keys, c->s);
   else launch_dwta_keys(dwta_of(c), x, n, c->hp, keys, c->s);
@@ -188,10 +204,14 @@ int slide_destroy(slide_ctx* c) {
     c->tab.release();
     for (DBuf* b : {&c->sh_packed, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->qkeys, &c->order,
                     &c->states, &c->act, &c->cnt, &c->empty, &c->offs, &c->prow, &c->pslot, &c->plab, &c->z,
-                    &c->prob, &c->delta, &c->loss, &c->dh, &c->fb_ids, &c->fb_scratch, &c->fb_bitmap, &c->iota,
-                    &c->sk_out, &c->sv_out, &c->uniq, &c->ucnt, &c->uoff, &c->nuniq, &c->temp, &c->xslot,
-                    &c->fkeys_out, &c->fvals_out, &c->funiq, &c->fucnt, &c->fuoff, &c->fnuniq, &c->tc, &c->bc})
+                    &c->prob, &c->delta, &c->loss, &c->dh, &c->fb_ids, &c->fb_scratch, &c->fb_bitmap, &c->xslot,
+                    &c->tc, &c->bc, &c->counters, &c->partial})
       b->release();
+    c->grow.release();
+    c->gfeat.release();
+    if (c->pinned_loss) cudaFreeHost(c->pinned_loss);
+    if (c->pinned_cnt) cudaFreeHost(c->pinned_cnt);
+    for (cudaEvent_t e : c->timer.pool) cudaEventDestroy(e);
     delete c;
   });
 }
@@ -421,90 +441,71 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
       SLIDE_CUDA(cudaMemcpyAsync(bt->rng_states, states, (size_t)b * 48, cudaMemcpyDeviceToDevice, s));
     c->timer.mark(s, kStFallback);
   }
+  // pair count stays on the device (offs[b]); buffers are sized by the bound
   int32_t* offs = c->offs.ensure<int32_t>(b + 1);
   launch_offsets(b, cnt, offs, s);
-  c->h_offs.resize(b + 1);
-  SLIDE_CUDA(cudaMemcpyAsync(c->h_offs.data(), offs, (b + 1) * 4, cudaMemcpyDeviceToHost, s));
-  SLIDE_CUDA(cudaStreamSynchronize(s));
-  const int64_t P = c->h_offs[b];
-  int32_t* prow = c->prow.ensure<int32_t>(P);
-  int32_t* pslot = c->pslot.ensure<int32_t>(P);
-  uint8_t* plab = c->plab.ensure<uint8_t>(P);
+  const int64_t P_max = (int64_t)b * cap_max;
+  int32_t* prow = c->prow.ensure<int32_t>(P_max);
+  int32_t* pslot = c->pslot.ensure<int32_t>(P_max);
+  uint8_t* plab = c->plab.ensure<uint8_t>(P_max);
   launch_pairs(b, act, cap_max, offs, prow, pslot, plab, s);
   c->timer.mark(s, kStCompact);
-  c->host_counts[0] += P;
-  float* z = c->z.ensure<float>(P);
-  float* prob = c->prob.ensure<float>(P);
-  float* delta = c->delta.ensure<float>(P);
+  float* z = c->z.ensure<float>(P_max);
+  float* prob = c->prob.ensure<float>(P_max);
+  float* delta = c->delta.ensure<float>(P_max);
   double* loss = c->loss.ensure<double>(b);
-  launch_logits(hp, P, prow, pslot, d.w2, d.b2, h, z, s);
+  // group the pairs by output row (slot order inside a row): the row-major
+  // logits, hidden gradient and W2 Adam all walk this structure
+  GroupBy& gr = c->grow;
+  if (c->grow_pending) gr.clear(s);
+  gr.prepare(d.n_out, b, P_max);
+  gr.run(prow, pslot, offs + b, 0, P_max, s);
+  c->grow_pending = true;
+  c->timer.mark(s, kStGroupRows);
+  launch_logits_rows(hp, b, gr.n_uniq.as<int32_t>(), gr.u_max, gr.uniq.as<int32_t>(), gr.seg_off.as<int32_t>(),
+                     gr.seg_cnt.as<int32_t>(), gr.order.as<int32_t>(), pslot, d.w2, d.b2, h, z, s);
   c->timer.mark(s, kStLogits);
   launch_softmax(b, offs, plab, bt->y_ptr, z, prob, delta, loss, s);
   c->timer.mark(s, kStSoftmax);
   c->have_forward = true;
   c->last_b = b;
-  c->last_P = P;
+  c->last_P = -1;  // on the device; host_pairs() reads it when needed
+  c->last_Pmax = P_max;
   c->last_nnz = nnz;
   c->last_xbase = x_base;
   c->last_xptr = bt->x_ptr;
   c->last_xidx = bt->x_idx;
   c->last_xval = bt->x_val;
   c->last_yptr = bt->y_ptr;
-  if (n_pairs) *n_pairs = P;
-}
-
-__global__ void iota_kernel(int32_t* a, int64_t n) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
-    a[q] = (int32_t)q;
-}
-
-// stable group-by: keys (n) -> uniq keys, per-key count, segment offsets,
-// and the original positions sorted by key (ties keep their order)
-static void group_by(slide_ctx* c, const int32_t* keys, int64_t n, int key_bits, DBuf& keys_out, DBuf& vals_out,
-                     DBuf& uniq, DBuf& ucnt, DBuf& uoff, DBuf& nuniq) {
-  cudaStream_t s = c->s;
-  int32_t* io = c->iota.ensure<int32_t>(n);
-  iota_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), kSms * 16), 256, 0, s>>>(io, n);
-  SLIDE_LAUNCH_CHECK();
-  int32_t* ko = keys_out.ensure<int32_t>(n);
-  int32_t* vo = vals_out.ensure<int32_t>(n);
-  int32_t* u = uniq.ensure<int32_t>(n);
-  int32_t* uc = ucnt.ensure<int32_t>(n);
-  int32_t* uo = uoff.ensure<int32_t>(n);
-  int32_t* nu = nuniq.ensure<int32_t>(1);
-  size_t b1 = 0, b2 = 0, b3 = 0;
-  const uint32_t* uk = reinterpret_cast<const uint32_t*>(keys);
-  uint32_t* uko = reinterpret_cast<uint32_t*>(ko);
-  SLIDE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, uk, uko, io, vo, (int)n, 0, key_bits, s));
-  SLIDE_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, b2, ko, u, uc, nu, (int)n, s));
-  SLIDE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b3, uc, uo, (int)n, s));
-  size_t tb = std::max(b1, std::max(b2, b3));
-  void* t = c->temp.ensure<uint8_t>(tb);
-  SLIDE_CUDA(cub::DeviceRadixSort::SortPairs(t, tb, uk, uko, io, vo, (int)n, 0, key_bits, s));
-  SLIDE_CUDA(cub::DeviceRunLengthEncode::Encode(t, tb, ko, u, uc, nu, (int)n, s));
-  SLIDE_CUDA(cub::DeviceScan::ExclusiveSum(t, tb, uc, uo, (int)n, s));
+  if (n_pairs) *n_pairs = host_pairs(c);
 }
 
 static void backward_impl(slide_ctx* c, int64_t update) {
   SLIDE_CHECK(c->have_forward, kValueError, "backward needs a forward first");
   const slide_net_desc& d = c->d;
   const int b = c->last_b, hp = c->hp;
-  const int64_t P = c->last_P;
+  const int64_t P_max = c->last_Pmax;
   cudaStream_t s = c->s;
   float* dh = c->dh.ensure<float>((size_t)b * hp);
-  launch_hidden_grad(hp, b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->delta.as<float>(), d.w2,
-                     c->h.as<float>(), dh, s);
+  GroupBy& gr = c->grow;
+  const int parts = kSms;
+  float* partial = c->partial.ensure<float>((size_t)parts * b * hp);
+  // the row-major variant is kept for the tiled rewrite; the sample-major
+  // kernel is faster today (latency-bound bitmask walk)
+  if (!c->use_rows_dh ||
+      !launch_hidden_grad_rows(hp, b, gr.n_uniq.as<int32_t>(), gr.uniq.as<int32_t>(), gr.seg_off.as<int32_t>(),
+                               gr.mask.as<uint32_t>(), gr.wpk, gr.order.as<int32_t>(), c->offs.as<int32_t>() + b,
+                               c->delta.as<float>(), d.w2, c->h.as<float>(), partial, parts, dh, s))
+    launch_hidden_grad(hp, b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->delta.as<float>(), d.w2,
+                       c->h.as<float>(), dh, s);
   c->timer.mark(s, kStHiddenGrad);
   if (!update) return;
   const AdamParams ap = adam_of(d);
   unsigned long long* ctr = c->timer.on ? c->counters.as<unsigned long long>() : nullptr;
-  // W2: group the pairs by output row, slot order kept inside a row
-  if (P > 0) {
-    group_by(c, c->prow.as<int32_t>(), P, bits_for(d.n_out), c->sk_out, c->sv_out, c->uniq, c->ucnt, c->uoff,
-             c->nuniq);
-    c->timer.mark(s, kStGroupRows);
-    launch_adam_rows(hp, ap, c->nuniq.as<int32_t>(), P, c->uniq.as<int32_t>(), c->uoff.as<int32_t>(),
-                     c->ucnt.as<int32_t>(), c->sv_out.as<int32_t>(), c->pslot.as<int32_t>(), c->delta.as<float>(),
+  // W2: rows in ascending order, each row's samples in slot order
+  if (P_max > 0) {
+    launch_adam_rows(hp, ap, gr.n_uniq.as<int32_t>(), gr.u_max, gr.uniq.as<int32_t>(), gr.seg_off.as<int32_t>(),
+                     gr.seg_cnt.as<int32_t>(), gr.order.as<int32_t>(), c->pslot.as<int32_t>(), c->delta.as<float>(),
                      c->h.as<float>(), d.w2, d.m2, d.v2, d.b2, d.mb2, d.vb2, d.steps2, ctr, s);
     c->timer.mark(s, kStAdamRows);
   }
@@ -514,23 +515,30 @@ static void backward_impl(slide_ctx* c, int64_t update) {
   launch_hidden_counts(hp, b, ap, c->h.as<float>(), d.steps1, tc, bc, s);
   c->timer.mark(s, kStHiddenCounts);
   const int64_t nnz = c->last_nnz;
+  GroupBy& gf = c->gfeat;
   if (nnz > 0) {
     int32_t* xs = c->xslot.ensure<int32_t>(nnz);
     launch_x_slots(b, c->last_xptr, xs, s);
-    group_by(c, c->last_xidx + c->last_xbase, nnz, bits_for(d.input_dim), c->fkeys_out, c->fvals_out, c->funiq,
-             c->fucnt, c->fuoff, c->fnuniq);
+    gf.prepare(d.input_dim, b, nnz);
+    gf.run(c->last_xidx + c->last_xbase, xs, nullptr, nnz, nnz, s);
     c->timer.mark(s, kStGroupFeat);
-    launch_adam_features(hp, ap, c->fnuniq.as<int32_t>(), nnz, c->funiq.as<int32_t>(), c->fuoff.as<int32_t>(),
-                         c->fucnt.as<int32_t>(), c->fvals_out.as<int32_t>(), xs, c->last_xval, c->last_xbase,
+    launch_adam_features(hp, ap, gf.n_uniq.as<int32_t>(), gf.u_max, gf.uniq.as<int32_t>(), gf.seg_off.as<int32_t>(),
+                         gf.seg_cnt.as<int32_t>(), gf.order.as<int32_t>(), xs, c->last_xval, c->last_xbase,
                          c->h.as<float>(), dh, bc, d.w1t, d.m1t, d.v1t, ctr ? ctr + 1 : nullptr, s);
     c->timer.mark(s, kStAdamFeat);
   }
   launch_adam_hidden_bias(hp, b, ap, c->h.as<float>(), dh, tc, bc, d.b1, d.mb1, d.vb1, d.steps1, s);
   c->timer.mark(s, kStHiddenBias);
   if (ctr) {
-    launch_accumulate(ctr + 2, P > 0 ? c->nuniq.as<int32_t>() : nullptr, s);
-    launch_accumulate(ctr + 3, nnz > 0 ? c->fnuniq.as<int32_t>() : nullptr, s);
+    launch_accumulate(ctr + 2, P_max > 0 ? gr.n_uniq.as<int32_t>() : nullptr, s);
+    launch_accumulate(ctr + 3, nnz > 0 ? gf.n_uniq.as<int32_t>() : nullptr, s);
+    launch_accumulate(ctr + 5, c->offs.as<int32_t>() + b, s);
   }
+  if (c->grow_pending) {
+    gr.clear(s);
+    c->grow_pending = false;
+  }
+  if (nnz > 0) gf.clear(s);
 }
 
 int slide_forward(slide_ctx* c, const slide_batch* bt, int64_t iteration, int64_t slot_offset, int64_t* n_pairs) {
@@ -547,6 +555,13 @@ int slide_train_batch(slide_ctx* c, const slide_batch* bt, int64_t iteration, in
     const int64_t B = bt->batch;
     SLIDE_CHECK(B >= 1, kValueError, "batch is empty");
     SLIDE_CHECK(sub_batch >= 1, kValueError, "sub_batch must be >= 1");
+    if (c->pinned_n < B) {
+      if (c->pinned_loss) cudaFreeHost(c->pinned_loss);
+      if (c->pinned_cnt) cudaFreeHost(c->pinned_cnt);
+      SLIDE_CUDA(cudaHostAlloc((void**)&c->pinned_loss, B * 8, cudaHostAllocDefault));
+      SLIDE_CUDA(cudaHostAlloc((void**)&c->pinned_cnt, B * 4, cudaHostAllocDefault));
+      c->pinned_n = B;
+    }
     for (int64_t s0 = 0; s0 < B; s0 += sub_batch) {
       const int64_t nb = std::min<int64_t>(sub_batch, B - s0);
       slide_batch v = *bt;
@@ -562,19 +577,23 @@ int slide_train_batch(slide_ctx* c, const slide_batch* bt, int64_t iteration, in
       }
       forward_impl(c, &v, iteration, s0, nullptr);
       backward_impl(c, 1);
-      if (loss_host)
-        SLIDE_CUDA(cudaMemcpyAsync(loss_host + s0, c->loss.p, nb * 8, cudaMemcpyDeviceToHost, c->s));
-      if (active_host)
-        for (int64_t i = 0; i < nb; ++i) active_host[s0 + i] = c->h_offs[i + 1] - c->h_offs[i];
+      // results ride back asynchronously; one host sync per call
+      SLIDE_CUDA(cudaMemcpyAsync(c->pinned_loss + s0, c->loss.p, nb * 8, cudaMemcpyDeviceToHost, c->s));
+      SLIDE_CUDA(cudaMemcpyAsync(c->pinned_cnt + s0, c->cnt.p, nb * 4, cudaMemcpyDeviceToHost, c->s));
     }
     SLIDE_CUDA(cudaStreamSynchronize(c->s));
+    for (int64_t i = 0; i < B; ++i) {
+      if (loss_host) loss_host[i] = c->pinned_loss[i];
+      if (active_host) active_host[i] = c->pinned_cnt[i];
+      c->host_counts[0] += c->pinned_cnt[i];
+    }
   });
 }
 
 int slide_read(slide_ctx* c, int64_t what, void* dst, int64_t max_bytes, int64_t* bytes) {
   return guarded([&] {
     SLIDE_CHECK(c->have_forward, kValueError, "nothing to read before a forward");
-    const int64_t b = c->last_b, P = c->last_P, hp = c->hp, L = c->d.l;
+    const int64_t b = c->last_b, P = host_pairs(c), hp = c->hp, L = c->d.l;
     const void* src = nullptr;
     int64_t n = 0;
     switch (what) {
@@ -637,7 +656,7 @@ int slide_write(slide_ctx* c, int64_t what, const void* src, int64_t bytes) {
       n = (int64_t)c->last_b * c->hp * 4;
     } else if (what == 6) {
       dst = c->delta.p;
-      n = c->last_P * 4;
+      n = host_pairs(c) * 4;
     } else {
       throw Error(kValueError, "only h (0) and delta (6) can be written");
     }

@@ -50,6 +50,20 @@ void launch_offsets(int b, const int32_t* cnt, int32_t* offs, cudaStream_t s);
 void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* offs, int32_t* prow, int32_t* pslot,
                   uint8_t* plab, cudaStream_t s);
 
+// Stable (key, slot) group-by with device-side sizes (group.cu).
+struct GroupBy {
+  DBuf bits, key_rank, woff, uniq, seg_cnt, seg_off, n_uniq, mask, order, temp;
+  int64_t K = 0, nwords = 0, u_max = 0, bits_words = 0, mask_words = 0;
+  int wpk = 1;
+  size_t temp_bytes = 0;
+  void prepare(int64_t key_space, int64_t slots, int64_t items_max);
+  // items q < n (n = *n_dev if given, else n_host), keys[q] / slots[q]
+  void run(const int32_t* keys, const int32_t* slots, const int32_t* n_dev, int64_t n_host, int64_t n_max,
+           cudaStream_t s);
+  void clear(cudaStream_t s);
+  void release();
+};
+
 // ------------------------------------------------------------------ layers
 struct AdamParams {
   float lr, b1, b2, eps;
@@ -58,8 +72,16 @@ struct AdamParams {
 
 void launch_hidden_forward(int hp, int b, const int32_t* x_ptr, const int32_t* x_idx, const float* x_val,
                            const float* w1t, const float* b1, float* h, cudaStream_t s);
-void launch_logits(int hp, int64_t p, const int32_t* prow, const int32_t* pslot, const float* w2, const float* b2,
-                   const float* h, float* z, cudaStream_t s);
+void launch_logits(int hp, int64_t P_max, const int32_t* P_dev, const int32_t* prow, const int32_t* pslot,
+                   const float* w2, const float* b2, const float* h, float* z, cudaStream_t s);
+void launch_logits_rows(int hp, int b, const int32_t* n_uniq, int64_t u_max, const int32_t* uniq,
+                        const int32_t* seg_off, const int32_t* seg_cnt, const int32_t* order, const int32_t* pslot,
+                        const float* w2, const float* b2, const float* h, float* z, cudaStream_t s);
+// false when B*hp does not fit in shared memory (caller uses the sample-major kernel)
+bool launch_hidden_grad_rows(int hp, int b, const int32_t* n_uniq, const int32_t* uniq, const int32_t* seg_off,
+                             const uint32_t* mask, int wpk, const int32_t* order, const int32_t* P_dev,
+                             const float* delta, const float* w2, const float* h, float* partial_buf,
+                             int parts, float* dh, cudaStream_t s);
 void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
                     float* prob, float* delta, double* loss, cudaStream_t s);
 void launch_hidden_grad(int hp, int b, const int32_t* offs, const int32_t* prow, const float* delta, const float* w2,

@@ -104,10 +104,12 @@ void launch_hidden_forward(int hp, int b, const int32_t* x_ptr, const int32_t* x
 // pair (network.py:266).  A warp takes G consecutive pairs (same sample
 // mostly), issues all G row loads, then reduces.
 template <int NV, int G>
-__global__ void __launch_bounds__(256) logits_kernel(int hp, int64_t P, const int32_t* __restrict__ prow,
+__global__ void __launch_bounds__(256) logits_kernel(int hp, const int32_t* __restrict__ P_dev,
+                                                     const int32_t* __restrict__ prow,
                                                      const int32_t* __restrict__ pslot, const float* __restrict__ w2,
                                                      const float* __restrict__ b2, const float* __restrict__ h,
                                                      float* __restrict__ z) {
+  const int64_t P = *P_dev;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -141,14 +143,210 @@ __global__ void __launch_bounds__(256) logits_kernel(int hp, int64_t P, const in
   }
 }
 
-void launch_logits(int hp, int64_t P, const int32_t* prow, const int32_t* pslot, const float* w2, const float* b2,
-                   const float* h, float* z, cudaStream_t s) {
-  if (P <= 0) return;
+void launch_logits(int hp, int64_t P_max, const int32_t* P_dev, const int32_t* prow, const int32_t* pslot,
+                   const float* w2, const float* b2, const float* h, float* z, cudaStream_t s) {
+  if (P_max <= 0) return;
   constexpr int G = 4;
-  int64_t warps = ceil_div(P, G);
+  int64_t warps = ceil_div(P_max, G);
   int grid = (int)std::min<int64_t>(ceil_div(warps, 8), (int64_t)kSms * 16);
-  SLIDE_NV_DISPATCH(hp, (logits_kernel<NV, G><<<grid, 256, 0, s>>>(hp, P, prow, pslot, w2, b2, h, z)));
+  SLIDE_NV_DISPATCH(hp, (logits_kernel<NV, G><<<grid, 256, 0, s>>>(hp, P_dev, prow, pslot, w2, b2, h, z)));
   SLIDE_LAUNCH_CHECK();
+}
+
+// Row-major logits: one warp per distinct active row, the row read once into
+// registers, then dotted with every sample that holds it (the stable group-by
+// order).  4 pairs share one butterfly: 6 shuffles instead of 20.
+__device__ __forceinline__ float reduce4(float v0, float v1, float v2, float v3, int lane) {
+  const bool hi16 = lane & 16;
+  float k0 = hi16 ? v2 : v0, k1 = hi16 ? v3 : v1;
+  k0 += __shfl_xor_sync(0xffffffffu, hi16 ? v0 : v2, 16);
+  k1 += __shfl_xor_sync(0xffffffffu, hi16 ? v1 : v3, 16);
+  const bool hi8 = lane & 8;
+  float k = hi8 ? k1 : k0;
+  k += __shfl_xor_sync(0xffffffffu, hi8 ? k0 : k1, 8);
+  k += __shfl_xor_sync(0xffffffffu, k, 4);
+  k += __shfl_xor_sync(0xffffffffu, k, 2);
+  k += __shfl_xor_sync(0xffffffffu, k, 1);
+  return k;  // the sum for pair ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1)
+}
+
+template <int NV, bool SMEM_H>
+__global__ void __launch_bounds__(256) logits_rows_kernel(int hp, int b, const int32_t* __restrict__ n_uniq,
+                                                          const int32_t* __restrict__ uniq,
+                                                          const int32_t* __restrict__ seg_off,
+                                                          const int32_t* __restrict__ seg_cnt,
+                                                          const int32_t* __restrict__ order,
+                                                          const int32_t* __restrict__ pslot,
+                                                          const float* __restrict__ w2, const float* __restrict__ b2,
+                                                          const float* __restrict__ h, float* __restrict__ z) {
+  extern __shared__ __align__(16) float hs[];
+  if (SMEM_H) {
+    const float4* src = reinterpret_cast<const float4*>(h);
+    float4* dst = reinterpret_cast<float4*>(hs);
+    for (int q = threadIdx.x; q < b * hp / 4; q += blockDim.x) dst[q] = src[q];
+    __syncthreads();
+  }
+  const float* hsrc = SMEM_H ? hs : h;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nu = *n_uniq;
+  const int mine = ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+  for (int64_t u = gw; u < nu; u += nw) {
+    const int r = uniq[u];
+    const int s0 = seg_off[u], len = seg_cnt[u];
+    const float bias = b2[r];
+    float4 w[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) w[q] = ld4(w2 + (int64_t)r * hp + q * 128 + lane * 4);
+    for (int j0 = 0; j0 < len; j0 += 32) {
+      const int pl = j0 + lane < len ? order[s0 + j0 + lane] : 0;
+      const int sl = j0 + lane < len ? pslot[pl] : 0;
+      const int nc = min(32, len - j0);
+      for (int q2 = 0; q2 < nc; q2 += 4) {
+        float v[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int slot = __shfl_sync(0xffffffffu, sl, min(q2 + t, nc - 1));
+          const float* hr = hsrc + (int64_t)slot * hp + lane * 4;
+          float d = 0.f;
+#pragma unroll
+          for (int q = 0; q < NV; ++q) {
+            const float4 hv = SMEM_H ? *reinterpret_cast<const float4*>(hr + q * 128) : ld4(hr + q * 128);
+            d = fmaf(w[q].x, hv.x, d);
+            d = fmaf(w[q].y, hv.y, d);
+            d = fmaf(w[q].z, hv.z, d);
+            d = fmaf(w[q].w, hv.w, d);
+          }
+          v[t] = d;
+        }
+        const float sum = reduce4(v[0], v[1], v[2], v[3], lane);
+        const int p = __shfl_sync(0xffffffffu, pl, min(q2 + mine, nc - 1));
+        if ((lane & 7) == 0 && q2 + mine < nc) z[p] = sum + bias;
+      }
+    }
+  }
+}
+
+void launch_logits_rows(int hp, int b, const int32_t* n_uniq, int64_t u_max, const int32_t* uniq,
+                        const int32_t* seg_off, const int32_t* seg_cnt, const int32_t* order, const int32_t* pslot,
+                        const float* w2, const float* b2, const float* h, float* z, cudaStream_t s) {
+  if (u_max <= 0) return;
+  const size_t smem = (size_t)b * hp * 4;
+  const bool use_smem = smem <= 100 * 1024;
+  int grid = (int)std::min<int64_t>(ceil_div(u_max, 8), (int64_t)kSms * (use_smem ? 2 : 8));
+  if (use_smem) {
+    SLIDE_NV_DISPATCH(hp, ({
+      SLIDE_CUDA(cudaFuncSetAttribute(logits_rows_kernel<NV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+      logits_rows_kernel<NV, true><<<grid, 256, smem, s>>>(hp, b, n_uniq, uniq, seg_off, seg_cnt, order, pslot, w2,
+                                                           b2, h, z);
+    }));
+  } else {
+    SLIDE_NV_DISPATCH(hp, (logits_rows_kernel<NV, false><<<grid, 256, 0, s>>>(hp, b, n_uniq, uniq, seg_off, seg_cnt,
+                                                                              order, pslot, w2, b2, h, z)));
+  }
+  SLIDE_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------- hidden gradient, rows
+// dh_i = sum_r delta_ir W2[r] (pre-update W2) accumulated row-major: CTA g
+// takes the rows whose pairs fall in its 1/G share, warp w owns the samples
+// i = w (mod 8) and accumulates them in shared memory -- no atomics, fixed
+// order; the G partials are summed in order by a second kernel.
+template <int NV>
+__global__ void __launch_bounds__(256) hidden_grad_rows_kernel(
+    int hp, int b, const int32_t* __restrict__ n_uniq, const int32_t* __restrict__ uniq,
+    const int32_t* __restrict__ seg_off, const uint32_t* __restrict__ mask, int wpk,
+    const int32_t* __restrict__ order, const int32_t* __restrict__ P_dev, const float* __restrict__ delta,
+    const float* __restrict__ w2, float* __restrict__ partial) {
+  extern __shared__ __align__(16) float acc[];
+  for (int q = threadIdx.x; q < b * hp; q += blockDim.x) acc[q] = 0.f;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nu = *n_uniq;
+  const int64_t P = *P_dev;
+  const int64_t lo = P * blockIdx.x / gridDim.x, hi = P * (blockIdx.x + 1) / gridDim.x;
+  // rows whose first pair lies in [lo, hi)
+  auto lower = [&](int64_t key) {
+    int a = 0, c = nu;
+    while (a < c) {
+      const int mid = (a + c) >> 1;
+      if (seg_off[mid] < key) a = mid + 1;
+      else c = mid;
+    }
+    return a;
+  };
+  const int u0 = lower(lo), u1 = lower(hi);
+  const uint32_t own = 0x01010101u << warp;
+  for (int u = u0; u < u1; ++u) {
+    const uint32_t* m = mask + (int64_t)u * wpk;
+    const int base = seg_off[u];
+    const float* wr = w2 + (int64_t)uniq[u] * hp + lane * 4;
+    float4 w[NV];
+    bool loaded = false;
+    int rank_base = 0;
+    for (int k = 0; k < wpk; ++k) {
+      const uint32_t bits = m[k];
+      uint32_t mine = bits & own;
+      if (mine && !loaded) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) w[q] = ld4(wr + q * 128);
+        loaded = true;
+      }
+      while (mine) {
+        const int bit = __ffs(mine) - 1;
+        mine &= mine - 1;
+        const int slot = k * 32 + bit;
+        const int p = order[base + rank_base + __popc(bits & ((1u << bit) - 1u))];
+        const float d = delta[p];
+        float* a = acc + slot * hp + lane * 4;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          float4 t = *reinterpret_cast<float4*>(a + q * 128);
+          t.x = fmaf(d, w[q].x, t.x);
+          t.y = fmaf(d, w[q].y, t.y);
+          t.z = fmaf(d, w[q].z, t.z);
+          t.w = fmaf(d, w[q].w, t.w);
+          *reinterpret_cast<float4*>(a + q * 128) = t;
+        }
+      }
+      rank_base += __popc(bits);
+    }
+  }
+  __syncthreads();
+  float4* dst = reinterpret_cast<float4*>(partial + (int64_t)blockIdx.x * b * hp);
+  const float4* src = reinterpret_cast<const float4*>(acc);
+  for (int q = threadIdx.x; q < b * hp / 4; q += blockDim.x) dst[q] = src[q];
+}
+
+__global__ void hidden_grad_reduce_kernel(int hp, int b, int parts, const float* __restrict__ partial,
+                                          const float* __restrict__ h, float* __restrict__ dh) {
+  const int64_t n = (int64_t)b * hp;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int g = 0; g < parts; ++g) s += partial[(int64_t)g * n + q];
+    dh[q] = h[q] > 0.f ? s : 0.f;
+  }
+}
+
+bool launch_hidden_grad_rows(int hp, int b, const int32_t* n_uniq, const int32_t* uniq, const int32_t* seg_off,
+                             const uint32_t* mask, int wpk, const int32_t* order, const int32_t* P_dev,
+                             const float* delta, const float* w2, const float* h, float* partial_buf,
+                             int parts, float* dh, cudaStream_t s) {
+  const size_t smem = (size_t)b * hp * 4;
+  if (smem > 200 * 1024) return false;
+  SLIDE_NV_DISPATCH(hp, ({
+    SLIDE_CUDA(cudaFuncSetAttribute(hidden_grad_rows_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+    hidden_grad_rows_kernel<NV><<<parts, 256, smem, s>>>(hp, b, n_uniq, uniq, seg_off, mask, wpk, order, P_dev,
+                                                         delta, w2, partial_buf);
+  }));
+  SLIDE_LAUNCH_CHECK();
+  hidden_grad_reduce_kernel<<<(int)std::max<int64_t>(1, ceil_div((int64_t)b * hp, 256)), 256, 0, s>>>(
+      hp, b, parts, partial_buf, h, dh);
+  SLIDE_LAUNCH_CHECK();
+  return true;
 }
 
 // ---------------------------------------------------- softmax + CE + delta
