@@ -194,7 +194,11 @@ def run_ours(args, rank, world):
 
     def step_dev(it):
         bt, _, _ = dev_batches[it - 1]
-        _lib.call("slide_train_batch", net._ctx, _lib.C.byref(bt), it, sub, loss_buf.ctypes.data, act_buf.ctypes.data)
+        if sub == w.batch and net.use_graphs:  # the captured-graph snapshot step
+            _lib.call("slide_graph_step", net._ctx, _lib.C.byref(bt), it, loss_buf.ctypes.data, act_buf.ctypes.data)
+        else:
+            _lib.call("slide_train_batch", net._ctx, _lib.C.byref(bt), it, sub, loss_buf.ctypes.data,
+                      act_buf.ctypes.data)
         return net._barrier(it, loss_buf, act_buf)
 
     for it in range(1, W + 1):

@@ -142,6 +142,14 @@ int slide_backward(slide_ctx* ctx, int64_t update);
 int slide_train_batch(slide_ctx* ctx, const slide_batch* batch, int64_t iteration, int64_t sub_batch,
                       double* loss_host, int64_t* active_host);
 
+/* train_batch (snapshot schedule) as one CUDA graph: the batch (host or
+ * device CSR, absolute offsets) is copied into context buffers sized by
+ * capacities; the first call with new shapes runs eagerly, the second
+ * captures, later calls replay.  A batch above a capacity re-captures.
+ * Same outputs as slide_train_batch with sub_batch = batch. */
+int slide_graph_step(slide_ctx* ctx, const slide_batch* batch, int64_t iteration, double* loss_host,
+                     int64_t* active_host);
+
 /* stage readout of the last forward/backward (host copy), for parity:
  * 0 h (B, hp) f32 | 1 query keys (B, L) u32 | 2 offsets (B+1) i32 |
  * 3 pair rows (P) i32 | 4 pair label flag (P) u8 | 5 probs (P) f32 |

@@ -62,6 +62,7 @@ _SIGS = {
     "slide_forward": [vp, C.POINTER(Batch), i64, i64, C.POINTER(i64)],
     "slide_backward": [vp, i64],
     "slide_train_batch": [vp, C.POINTER(Batch), i64, i64, vp, vp],
+    "slide_graph_step": [vp, C.POINTER(Batch), i64, vp, vp],
     "slide_read": [vp, i64, vp, i64, C.POINTER(i64)],
     "slide_write": [vp, i64, vp, i64],
     "slide_profile": [vp, i64],

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <cmath>
 
 using namespace slide;
 
@@ -66,6 +67,26 @@ struct slide_ctx {
   GroupBy grow, gfeat;
   bool grow_pending = false;  // grow holds a forward's grouping not yet cleared
   bool use_rows_dh = false;
+  // CUDA-graph step (slide_graph_step): static shapes + context-owned batch
+  struct {
+    bool on = false;
+    int64_t batch = 0, nnz_cap = 0, lab_cap = 0, ylab_cap = 0;
+  } st;
+  bool st_active = false;  // forward/backward run with the static shapes above
+  DBuf iter_dev, gx_ptr, gx_idx, gx_val, gy_ptr, gy_idx;
+  int64_t g_last_pmax = 0;  // host bookkeeping of the captured step
+  unsigned long long g_kernels = 0;  // hand-written kernels per replay
+  int32_t* pinned_ptrs = nullptr;  // rebased x_ptr | y_ptr staging
+  int64_t* pinned_iter = nullptr;
+  int64_t pinned_ptrs_n = 0;
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t gev_in = nullptr, gev_out = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int graph_state = 0;  // 0: shapes new (run eagerly), 1: capture next, 2: replay
+  DBuf bias_table;
+  int64_t bias_n = 0;
+  int bias_exact = 1;
   DBuf xslot, tc, bc, partial;
   int64_t fb_bitmap_words = 0;
   double* pinned_loss = nullptr;
@@ -104,7 +125,12 @@ static int bits_for(int64_t n) {
   return b;
 }
 
-static AdamParams adam_of(const slide_net_desc& d) {
+// Bias-correction table (fp64 math, fp32 entries): (lr / (1 - b1^t),
+// 1 / (1 - b2^t)) up to the step where both become (lr, 1) in fp32.
+static void build_bias_table(slide_ctx* c);
+
+static AdamParams adam_of(slide_ctx* c) {
+  const slide_net_desc& d = c->d;
   AdamParams ap;
   ap.lr = (float)d.lr;
   ap.b1 = (float)d.beta1;
@@ -112,7 +138,31 @@ static AdamParams adam_of(const slide_net_desc& d) {
   ap.eps = (float)d.eps;
   ap.b1d = d.beta1;
   ap.b2d = d.beta2;
+  if (!c->bias_table.p) build_bias_table(c);
+  ap.table = c->bias_table.as<float2>();
+  ap.table_n = c->bias_n;
+  ap.table_exact = c->bias_exact;
   return ap;
+}
+
+static void build_bias_table(slide_ctx* c) {
+  const double b1 = c->d.beta1, b2 = c->d.beta2, lr = c->d.lr;
+  const double bmax = std::max(b1, b2);
+  // b^t < 2^-40 makes 1 - b^t == 1 in fp32 (and its reciprocal exactly 1)
+  int64_t need = bmax <= 0.0 ? 2 : (int64_t)std::ceil(40.0 * std::log(2.0) / -std::log(bmax)) + 2;
+  const int64_t cap = (int64_t)1 << 24;
+  c->bias_exact = need <= cap;
+  c->bias_n = std::min(need, cap);
+  std::vector<float2> tab((size_t)c->bias_n);
+  tab[0] = make_float2((float)lr, 1.f);
+  double p1 = 1.0, p2 = 1.0;
+  for (int64_t t = 1; t < c->bias_n; ++t) {
+    p1 = std::pow(b1, (double)t);
+    p2 = std::pow(b2, (double)t);
+    tab[(size_t)t] = make_float2((float)(lr / (1.0 - p1)), (float)(1.0 / (1.0 - p2)));
+  }
+  SLIDE_CUDA(cudaMemcpy(c->bias_table.ensure<float2>(c->bias_n), tab.data(), c->bias_n * sizeof(float2),
+                        cudaMemcpyHostToDevice));
 }
 
 static SimHashDev simhash_of(slide_ctx* c) {
@@ -205,10 +255,18 @@ int slide_destroy(slide_ctx* c) {
     for (DBuf* b : {&c->sh_packed, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->qkeys, &c->order,
                     &c->states, &c->act, &c->cnt, &c->empty, &c->offs, &c->prow, &c->pslot, &c->plab, &c->z,
                     &c->prob, &c->delta, &c->loss, &c->dh, &c->fb_ids, &c->fb_scratch, &c->fb_bitmap, &c->xslot,
-                    &c->tc, &c->bc, &c->counters, &c->partial})
+                    &c->tc, &c->bc, &c->counters, &c->partial, &c->bias_table})
       b->release();
     c->grow.release();
     c->gfeat.release();
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    if (c->graph) cudaGraphDestroy(c->graph);
+    for (DBuf* b : {&c->iter_dev, &c->gx_ptr, &c->gx_idx, &c->gx_val, &c->gy_ptr, &c->gy_idx}) b->release();
+    if (c->pinned_ptrs) cudaFreeHost(c->pinned_ptrs);
+    if (c->pinned_iter) cudaFreeHost(c->pinned_iter);
+    if (c->gev_in) cudaEventDestroy(c->gev_in);
+    if (c->gev_out) cudaEventDestroy(c->gev_out);
+    if (c->gstream) cudaStreamDestroy(c->gstream);
     if (c->pinned_loss) cudaFreeHost(c->pinned_loss);
     if (c->pinned_cnt) cudaFreeHost(c->pinned_cnt);
     for (cudaEvent_t e : c->timer.pool) cudaEventDestroy(e);
@@ -342,22 +400,34 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   SLIDE_CHECK(b >= 1 && b <= 1024, kValueError, "batch must hold 1..1024 slots");
   const int hp = c->hp, L = (int)d.l;
   cudaStream_t s = c->s;
-  const int64_t x_base = bt->x_ptr_host[0];
-  const int64_t nnz = bt->x_ptr_host[b] - x_base;
+  // static shapes (graph capture): capacities instead of this batch's sizes,
+  // the batch sits in the context's own buffers (offsets start at 0)
+  const bool stat = c->st_active;
+  int64_t x_base, nnz;
   int max_labels = 0;
-  for (int i = 0; i < b; ++i) max_labels = std::max(max_labels, bt->y_ptr_host[i + 1] - bt->y_ptr_host[i]);
+  if (stat) {
+    x_base = 0;
+    nnz = c->st.nnz_cap;
+    max_labels = (int)c->st.lab_cap;
+  } else {
+    x_base = bt->x_ptr_host[0];
+    nnz = bt->x_ptr_host[b] - x_base;
+    for (int i = 0; i < b; ++i) max_labels = std::max(max_labels, bt->y_ptr_host[i + 1] - bt->y_ptr_host[i]);
+    c->host_counts[1] += nnz;
+  }
+  const int64_t* iter_dev = stat ? c->iter_dev.as<int64_t>() : nullptr;
 
   float* h = c->h.ensure<float>((size_t)b * hp);
   c->timer.mark(s, kStStart);
   launch_hidden_forward(hp, b, bt->x_ptr, bt->x_idx, bt->x_val, d.w1t, d.b1, h, s);
   c->timer.mark(s, kStHidden);
-  c->host_counts[1] += nnz;
   c->host_counts[2] += b;
 
   int32_t* cnt = c->cnt.ensure<int32_t>(b);
   int32_t* empty = c->empty.ensure<int32_t>(b);
   int64_t cap_max;
   int32_t* act;
+  SLIDE_CHECK(!(stat && bt->forced_ptr), kValueError, "forced active sets are not graph-captured");
   if (bt->forced_ptr || d.family == 0) {
     int64_t m = d.n_out;
     if (bt->forced_ptr) {
@@ -382,7 +452,8 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     // slot stream is only needed by the (rare) fallback, which derives it
     const bool full_union = vanilla && d.beta >= lcap;
     const bool rng_first = !full_union || bt->rng_states;
-    if (rng_first) launch_slot_rng(b, d.seed, iteration, slot_offset, L, vanilla, bt->rng_states, states, order, s);
+    if (rng_first)
+      launch_slot_rng(b, d.seed, iteration, iter_dev, slot_offset, L, vanilla, bt->rng_states, states, order, s);
     c->timer.mark(s, kStSlotRng);
     cap_max = std::max<int64_t>(lcap, want) + max_labels;
     act = c->act.ensure<int32_t>((size_t)b * cap_max);
@@ -406,7 +477,7 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     a.cnt = cnt;
     a.empty = empty;
     a.cand_ctr = c->timer.on ? c->counters.as<unsigned long long>() + 4 : nullptr;
-    launch_select(a, (int)(lcap + max_labels), s);
+    if (!(full_union && launch_select_union(a, d.n_out, s))) launch_select(a, (int)(lcap + max_labels), s);
     c->timer.mark(s, kStSelect);
     // fallback for slots whose sampler returned nothing
     FallbackArgs f;
@@ -416,6 +487,7 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     f.seed = d.seed;
     f.iteration = iteration;
     f.slot_offset = slot_offset;
+    f.iter_dev = iter_dev;
     f.l = L;
     f.vanilla = vanilla;
     f.n = d.n_out;
@@ -497,14 +569,15 @@ static void backward_impl(slide_ctx* c, int64_t update) {
                                gr.mask.as<uint32_t>(), gr.wpk, gr.order.as<int32_t>(), c->offs.as<int32_t>() + b,
                                c->delta.as<float>(), d.w2, c->h.as<float>(), partial, parts, dh, s))
     launch_hidden_grad(hp, b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->delta.as<float>(), d.w2,
-                       c->h.as<float>(), dh, s);
+                       c->h.as<float>(), dh,
+                       c->partial.ensure<float>((size_t)std::max(parts, hidden_grad_slices(b)) * b * hp), s);
   c->timer.mark(s, kStHiddenGrad);
   if (!update) return;
-  const AdamParams ap = adam_of(d);
+  const AdamParams ap = adam_of(c);
   unsigned long long* ctr = c->timer.on ? c->counters.as<unsigned long long>() : nullptr;
   // W2: rows in ascending order, each row's samples in slot order
   if (P_max > 0) {
-    launch_adam_rows(hp, ap, gr.n_uniq.as<int32_t>(), gr.u_max, gr.uniq.as<int32_t>(), gr.seg_off.as<int32_t>(),
+    launch_adam_rows(hp, b, ap, gr.n_uniq.as<int32_t>(), gr.u_max, gr.uniq.as<int32_t>(), gr.seg_off.as<int32_t>(),
                      gr.seg_cnt.as<int32_t>(), gr.order.as<int32_t>(), c->pslot.as<int32_t>(), c->delta.as<float>(),
                      c->h.as<float>(), d.w2, d.m2, d.v2, d.b2, d.mb2, d.vb2, d.steps2, ctr, s);
     c->timer.mark(s, kStAdamRows);
@@ -512,7 +585,9 @@ static void backward_impl(slide_ctx* c, int64_t update) {
   // W1: group the (feature, slot) inputs by feature
   int32_t* tc = c->tc.ensure<int32_t>((size_t)b * hp);
   float2* bc = c->bc.ensure<float2>((size_t)b * hp);
-  launch_hidden_counts(hp, b, ap, c->h.as<float>(), d.steps1, tc, bc, s);
+  // per-unit step counts + bias corrections for the W1 Adam, and the hidden
+  // biases themselves (one fused pass)
+  launch_hidden_prep_bias(hp, b, ap, c->h.as<float>(), dh, d.steps1, tc, bc, d.b1, d.mb1, d.vb1, s);
   c->timer.mark(s, kStHiddenCounts);
   const int64_t nnz = c->last_nnz;
   GroupBy& gf = c->gfeat;
@@ -520,14 +595,14 @@ static void backward_impl(slide_ctx* c, int64_t update) {
     int32_t* xs = c->xslot.ensure<int32_t>(nnz);
     launch_x_slots(b, c->last_xptr, xs, s);
     gf.prepare(d.input_dim, b, nnz);
-    gf.run(c->last_xidx + c->last_xbase, xs, nullptr, nnz, nnz, s);
+    // static shapes: nnz is a capacity, the live count is x_ptr[b] (x_ptr[0] = 0)
+    gf.run(c->last_xidx + c->last_xbase, xs, c->st_active ? c->last_xptr + b : nullptr, nnz, nnz, s);
     c->timer.mark(s, kStGroupFeat);
     launch_adam_features(hp, ap, gf.n_uniq.as<int32_t>(), gf.u_max, gf.uniq.as<int32_t>(), gf.seg_off.as<int32_t>(),
                          gf.seg_cnt.as<int32_t>(), gf.order.as<int32_t>(), xs, c->last_xval, c->last_xbase,
                          c->h.as<float>(), dh, bc, d.w1t, d.m1t, d.v1t, ctr ? ctr + 1 : nullptr, s);
     c->timer.mark(s, kStAdamFeat);
   }
-  launch_adam_hidden_bias(hp, b, ap, c->h.as<float>(), dh, tc, bc, d.b1, d.mb1, d.vb1, d.steps1, s);
   c->timer.mark(s, kStHiddenBias);
   if (ctr) {
     launch_accumulate(ctr + 2, P_max > 0 ? gr.n_uniq.as<int32_t>() : nullptr, s);
@@ -582,6 +657,152 @@ int slide_train_batch(slide_ctx* c, const slide_batch* bt, int64_t iteration, in
       SLIDE_CUDA(cudaMemcpyAsync(c->pinned_cnt + s0, c->cnt.p, nb * 4, cudaMemcpyDeviceToHost, c->s));
     }
     SLIDE_CUDA(cudaStreamSynchronize(c->s));
+    for (int64_t i = 0; i < B; ++i) {
+      if (loss_host) loss_host[i] = c->pinned_loss[i];
+      if (active_host) active_host[i] = c->pinned_cnt[i];
+      c->host_counts[0] += c->pinned_cnt[i];
+    }
+  });
+}
+
+// One snapshot step as a CUDA graph (see header).  The first call with new
+// shapes runs eagerly (and sizes every buffer), the second captures, the
+// rest replay: no host work between the kernels, one sync per step.
+int slide_graph_step(slide_ctx* c, const slide_batch* bt, int64_t iteration, double* loss_host,
+                     int64_t* active_host) {
+  return guarded([&] {
+    const int64_t B = bt->batch;
+    SLIDE_CHECK(B >= 1 && B <= 1024, kValueError, "batch must hold 1..1024 slots");
+    SLIDE_CHECK(!bt->forced_ptr && !bt->rng_states, kValueError, "graph steps take plain training batches");
+    const int64_t x0 = bt->x_ptr_host[0], nnz = bt->x_ptr_host[B] - x0;
+    const int64_t y0 = bt->y_ptr_host[0], nlab = bt->y_ptr_host[B] - y0;
+    int64_t max_lab = 0;
+    for (int64_t i = 0; i < B; ++i) max_lab = std::max<int64_t>(max_lab, bt->y_ptr_host[i + 1] - bt->y_ptr_host[i]);
+    if (!c->gstream) {
+      SLIDE_CUDA(cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
+      SLIDE_CUDA(cudaEventCreateWithFlags(&c->gev_in, cudaEventDisableTiming));
+      SLIDE_CUDA(cudaEventCreateWithFlags(&c->gev_out, cudaEventDisableTiming));
+      SLIDE_CUDA(cudaHostAlloc((void**)&c->pinned_iter, 8, cudaHostAllocDefault));
+    }
+    auto& st = c->st;
+    if (!st.on || st.batch != B || nnz > st.nnz_cap || max_lab > st.lab_cap || nlab > st.ylab_cap) {
+      if (c->gexec) cudaGraphExecDestroy(c->gexec);
+      if (c->graph) cudaGraphDestroy(c->graph);
+      c->gexec = nullptr;
+      c->graph = nullptr;
+      st.on = true;
+      st.batch = B;
+      st.nnz_cap = std::max<int64_t>(nnz + nnz / 4, st.nnz_cap);
+      st.lab_cap = std::max<int64_t>(max_lab + max_lab / 4 + 4, st.lab_cap);
+      st.ylab_cap = std::max<int64_t>(nlab + nlab / 4 + 8, st.ylab_cap);
+      c->gx_ptr.ensure<int32_t>(B + 1);
+      c->gy_ptr.ensure<int32_t>(B + 1);
+      c->gx_idx.ensure<int32_t>(st.nnz_cap);
+      c->gx_val.ensure<float>(st.nnz_cap);
+      c->gy_idx.ensure<int32_t>(st.ylab_cap);
+      c->iter_dev.ensure<int64_t>(1);
+      c->graph_state = 0;
+    }
+    if (c->pinned_ptrs_n < 2 * (B + 1)) {
+      if (c->pinned_ptrs) cudaFreeHost(c->pinned_ptrs);
+      SLIDE_CUDA(cudaHostAlloc((void**)&c->pinned_ptrs, 2 * (B + 1) * 4, cudaHostAllocDefault));
+      c->pinned_ptrs_n = 2 * (B + 1);
+    }
+    cudaStream_t user = c->s, gs = c->gstream;
+    SLIDE_CUDA(cudaEventRecord(c->gev_in, user));
+    SLIDE_CUDA(cudaStreamWaitEvent(gs, c->gev_in, 0));
+    SLIDE_CUDA(cudaStreamSynchronize(gs));  // pinned staging is reused: previous step's copies are done
+    for (int64_t i = 0; i <= B; ++i) {
+      c->pinned_ptrs[i] = (int32_t)(bt->x_ptr_host[i] - x0);
+      c->pinned_ptrs[B + 1 + i] = (int32_t)(bt->y_ptr_host[i] - y0);
+    }
+    *c->pinned_iter = iteration;
+    SLIDE_CUDA(cudaMemcpyAsync(c->gx_ptr.p, c->pinned_ptrs, (B + 1) * 4, cudaMemcpyHostToDevice, gs));
+    SLIDE_CUDA(cudaMemcpyAsync(c->gy_ptr.p, c->pinned_ptrs + B + 1, (B + 1) * 4, cudaMemcpyHostToDevice, gs));
+    if (nnz) {
+      SLIDE_CUDA(cudaMemcpyAsync(c->gx_idx.p, bt->x_idx + x0, nnz * 4, cudaMemcpyDefault, gs));
+      SLIDE_CUDA(cudaMemcpyAsync(c->gx_val.p, bt->x_val + x0, nnz * 4, cudaMemcpyDefault, gs));
+    }
+    if (nlab) SLIDE_CUDA(cudaMemcpyAsync(c->gy_idx.p, bt->y_idx + y0, nlab * 4, cudaMemcpyDefault, gs));
+    SLIDE_CUDA(cudaMemcpyAsync(c->iter_dev.p, c->pinned_iter, 8, cudaMemcpyHostToDevice, gs));
+    slide_batch v{};
+    v.batch = B;
+    v.x_ptr = c->gx_ptr.as<int32_t>();
+    v.x_idx = c->gx_idx.as<int32_t>();
+    v.x_val = c->gx_val.as<float>();
+    v.y_ptr = c->gy_ptr.as<int32_t>();
+    v.y_idx = c->gy_idx.as<int32_t>();
+    v.x_ptr_host = c->pinned_ptrs;
+    v.y_ptr_host = c->pinned_ptrs + B + 1;
+    c->s = gs;
+    const bool timing = c->timer.on;
+    c->st_active = true;
+    try {
+      if (c->grow_pending) {  // a single-sample forward left its grouping behind
+        c->grow.clear(gs);
+        c->grow_pending = false;
+      }
+      if (c->graph_state < 2) c->timer.on = c->graph_state == 0 && timing;
+      if (c->graph_state == 0) {
+        forward_impl(c, &v, iteration, 0, nullptr);
+        backward_impl(c, 1);
+        c->graph_state = 1;
+      } else if (c->graph_state == 1) {
+        c->timer.on = false;
+        const unsigned long long lc0 = g_slide_launches;
+        SLIDE_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+        try {
+          forward_impl(c, &v, iteration, 0, nullptr);
+          backward_impl(c, 1);
+        } catch (...) {
+          cudaGraph_t g;
+          cudaStreamEndCapture(gs, &g);
+          if (g) cudaGraphDestroy(g);
+          throw;
+        }
+        SLIDE_CUDA(cudaStreamEndCapture(gs, &c->graph));
+        // captured launches were counted once; every replay runs them again
+        c->g_kernels = g_slide_launches - lc0;
+        SLIDE_CUDA(cudaGraphInstantiate(&c->gexec, c->graph, 0));
+        SLIDE_CUDA(cudaGraphLaunch(c->gexec, gs));
+        c->g_last_pmax = c->last_Pmax;
+        c->graph_state = 2;
+      } else {
+        SLIDE_CUDA(cudaGraphLaunch(c->gexec, gs));
+        g_slide_launches += c->g_kernels;
+        // host bookkeeping as if this step had run eagerly
+        c->have_forward = true;
+        c->last_b = (int)B;
+        c->last_P = -1;
+        c->last_Pmax = c->g_last_pmax;
+        c->last_nnz = st.nnz_cap;
+        c->last_xbase = 0;
+        c->last_xptr = v.x_ptr;
+        c->last_xidx = v.x_idx;
+        c->last_xval = v.x_val;
+        c->last_yptr = v.y_ptr;
+      }
+    } catch (...) {
+      c->s = user;
+      c->timer.on = timing;
+      c->st_active = false;
+      throw;
+    }
+    c->s = user;
+    c->timer.on = timing;
+    c->st_active = false;
+    if (c->pinned_n < B) {
+      if (c->pinned_loss) cudaFreeHost(c->pinned_loss);
+      if (c->pinned_cnt) cudaFreeHost(c->pinned_cnt);
+      SLIDE_CUDA(cudaHostAlloc((void**)&c->pinned_loss, B * 8, cudaHostAllocDefault));
+      SLIDE_CUDA(cudaHostAlloc((void**)&c->pinned_cnt, B * 4, cudaHostAllocDefault));
+      c->pinned_n = B;
+    }
+    SLIDE_CUDA(cudaMemcpyAsync(c->pinned_loss, c->loss.p, B * 8, cudaMemcpyDeviceToHost, gs));
+    SLIDE_CUDA(cudaMemcpyAsync(c->pinned_cnt, c->cnt.p, B * 4, cudaMemcpyDeviceToHost, gs));
+    SLIDE_CUDA(cudaEventRecord(c->gev_out, gs));
+    SLIDE_CUDA(cudaStreamWaitEvent(user, c->gev_out, 0));
+    SLIDE_CUDA(cudaStreamSynchronize(gs));
     for (int64_t i = 0; i < B; ++i) {
       if (loss_host) loss_host[i] = c->pinned_loss[i];
       if (active_host) active_host[i] = c->pinned_cnt[i];

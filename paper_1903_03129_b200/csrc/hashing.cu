@@ -17,6 +17,7 @@ __global__ void __launch_bounds__(256) simhash_kernel(SimHashDev f, const float*
                                                       int64_t n, int ld, uint32_t* __restrict__ keys) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int KL = f.k * f.l;
+  // rows transposed: xs[idx * ROWS + r], so one entry fetches all ROWS rows
   float* xs = reinterpret_cast<float*>(sm);
   uint16_t* proj = reinterpret_cast<uint16_t*>(xs + ROWS * f.dim);  // (c, KL)
   uint8_t* bits = reinterpret_cast<uint8_t*>(proj + ((KL * f.c + 1) & ~1));
@@ -29,7 +30,7 @@ __global__ void __launch_bounds__(256) simhash_kernel(SimHashDev f, const float*
     __syncthreads();
     for (int q = threadIdx.x; q < ROWS * f.dim; q += blockDim.x) {
       int r = q / f.dim, c = q - r * f.dim;
-      xs[q] = r < nr ? x[(row0 + r) * ld + c] : 0.f;
+      xs[c * ROWS + r] = r < nr ? x[(row0 + r) * ld + c] : 0.f;
     }
     __syncthreads();
     for (int p = threadIdx.x; p < KL; p += blockDim.x) {
@@ -40,9 +41,18 @@ __global__ void __launch_bounds__(256) simhash_kernel(SimHashDev f, const float*
         uint16_t e = proj[j * KL + p];
         int idx = e & 0x7fff;
         bool neg = e >> 15;
+        float vals[ROWS];
+        if constexpr (ROWS % 4 == 0) {
+#pragma unroll
+          for (int r4 = 0; r4 < ROWS / 4; ++r4)
+            *reinterpret_cast<float4*>(vals + 4 * r4) = *reinterpret_cast<const float4*>(xs + idx * ROWS + 4 * r4);
+        } else {
+#pragma unroll
+          for (int r = 0; r < ROWS; ++r) vals[r] = xs[idx * ROWS + r];
+        }
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
-          double v = (double)xs[r * f.dim + idx];
+          double v = (double)vals[r];
           acc[r] += neg ? -v : v;
         }
       }

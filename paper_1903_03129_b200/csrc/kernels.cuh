@@ -24,6 +24,7 @@ struct FallbackArgs {
   int states_ready;  // 0: derive default_rng((seed, iteration, slot)) (+ permutation(L) if vanilla)
   uint64_t seed;
   int64_t iteration, slot_offset;
+  const int64_t* iter_dev;  // when set, overrides iteration (graph replays)
   int l, vanilla;
   int64_t n, want;
   int64_t* fb_ids;
@@ -39,9 +40,11 @@ struct FallbackArgs {
   int32_t* cnt;
 };
 
-void launch_slot_rng(int b, uint64_t seed, int64_t it, int64_t off, int l, int vanilla, const uint64_t* ext,
-                     uint64_t* states, uint8_t* order, cudaStream_t s);
+void launch_slot_rng(int b, uint64_t seed, int64_t it, const int64_t* it_dev, int64_t off, int l, int vanilla,
+                     const uint64_t* ext, uint64_t* states, uint8_t* order, cudaStream_t s);
 void launch_select(const SelectArgs& a, int max_candidates, cudaStream_t s);
+// full-union selection through a shared-memory id bitmap; false if N is too wide
+bool launch_select_union(const SelectArgs& a, int64_t n_out, cudaStream_t s);
 void launch_fallback(const FallbackArgs& a, int b, cudaStream_t s);
 void launch_explicit_active(int b, int64_t n, const int32_t* fptr, const int32_t* fidx, const int32_t* y_ptr,
                             const int32_t* y_idx, int64_t cap_max, int32_t* act, int32_t* cnt, int32_t* empty,
@@ -68,6 +71,9 @@ struct GroupBy {
 struct AdamParams {
   float lr, b1, b2, eps;
   double b1d, b2d;
+  const float2* table;  // (lr / (1 - b1^t), 1 / (1 - b2^t)) for t < table_n
+  int64_t table_n;
+  int table_exact;      // beyond the table both factors are exactly (lr, 1) in fp32
 };
 
 void launch_hidden_forward(int hp, int b, const int32_t* x_ptr, const int32_t* x_idx, const float* x_val,
@@ -84,13 +90,15 @@ bool launch_hidden_grad_rows(int hp, int b, const int32_t* n_uniq, const int32_t
                              int parts, float* dh, cudaStream_t s);
 void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
                     float* prob, float* delta, double* loss, cudaStream_t s);
+int hidden_grad_slices(int b);
+// part: hidden_grad_slices(b) * b * hp floats of scratch
 void launch_hidden_grad(int hp, int b, const int32_t* offs, const int32_t* prow, const float* delta, const float* w2,
-                        const float* h, float* dh, cudaStream_t s);
-void launch_adam_rows(int hp, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq, const int32_t* uniq,
-                      const int32_t* seg_off, const int32_t* seg_cnt, const int32_t* sorted_pairs,
-                      const int32_t* pslot, const float* delta, const float* h, float* w2, float* m2, float* v2,
-                      float* b2, float* mb2, float* vb2, int64_t* steps2, unsigned long long* touched,
-                      cudaStream_t s);
+                        const float* h, float* dh, float* part, cudaStream_t s);
+void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq,
+                      const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
+                      const int32_t* sorted_pairs, const int32_t* pslot, const float* delta, const float* h,
+                      float* w2, float* m2, float* v2, float* b2, float* mb2, float* vb2, int64_t* steps2,
+                      unsigned long long* touched, cudaStream_t s);
 void launch_accumulate(unsigned long long* dst, const int32_t* src, cudaStream_t s);
 void launch_x_slots(int b, const int32_t* x_ptr, int32_t* x_slot, cudaStream_t s);
 void launch_hidden_counts(int hp, int b, const AdamParams& ap, const float* h, const int64_t* steps1, int32_t* tc,
@@ -100,6 +108,8 @@ void launch_adam_features(int hp, const AdamParams& ap, const int32_t* n_uniq, i
                           const int32_t* sorted_k, const int32_t* x_slot, const float* x_val, int64_t x_base,
                           const float* h, const float* dh, const float2* bc, float* w1t, float* m1t, float* v1t,
                           unsigned long long* touched, cudaStream_t s);
+void launch_hidden_prep_bias(int hp, int b, const AdamParams& ap, const float* h, const float* dh, int64_t* steps1,
+                             int32_t* tc, float2* bc, float* b1, float* mb1, float* vb1, cudaStream_t s);
 void launch_adam_hidden_bias(int hp, int b, const AdamParams& ap, const float* h, const float* dh, const int32_t* tc,
                              const float2* bc, float* b1, float* mb1, float* vb1, int64_t* steps1, cudaStream_t s);
 

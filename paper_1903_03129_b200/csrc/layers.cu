@@ -233,7 +233,7 @@ void launch_logits_rows(int hp, int b, const int32_t* n_uniq, int64_t u_max, con
                         const float* w2, const float* b2, const float* h, float* z, cudaStream_t s) {
   if (u_max <= 0) return;
   const size_t smem = (size_t)b * hp * 4;
-  const bool use_smem = smem <= 100 * 1024;
+  const bool use_smem = false && smem <= 100 * 1024;  // L1-resident h beats staging (ncu)
   int grid = (int)std::min<int64_t>(ceil_div(u_max, 8), (int64_t)kSms * (use_smem ? 2 : 8));
   if (use_smem) {
     SLIDE_NV_DISPATCH(hp, ({
@@ -407,32 +407,37 @@ void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32
 
 // -------------------------------------------------------- hidden gradient
 // dh_i = W2[A_i, :]^T delta_i with the pre-update W2, kept on nz(h_i)
-// (network.py:328-332).  One CTA per sample, fixed-order reduction.
+// (network.py:328-332).  Sample i's pairs are cut into S slices, one CTA
+// each (B*S CTAs fill the GPU); every slice sums in a fixed order, the
+// slices are added in slice order -- deterministic.
 template <int NV>
-__global__ void __launch_bounds__(256) hidden_grad_kernel(int hp, const int32_t* __restrict__ offs,
+__global__ void __launch_bounds__(256) hidden_grad_kernel(int hp, int b, int slices, const int32_t* __restrict__ offs,
                                                           const int32_t* __restrict__ prow,
                                                           const float* __restrict__ delta,
                                                           const float* __restrict__ w2,
-                                                          const float* __restrict__ h, float* __restrict__ dh) {
+                                                          const float* __restrict__ h, float* __restrict__ out) {
   __shared__ float red[8][NV * 128];
-  const int i = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int o = offs[i], e = offs[i + 1];
+  const int i = blockIdx.x / slices, sl = blockIdx.x - i * slices;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int o = offs[i], n = offs[i + 1] - o;
+  const int beg = o + (int)((int64_t)n * sl / slices), e = o + (int)((int64_t)n * (sl + 1) / slices);
   float4 acc[NV];
 #pragma unroll
   for (int q = 0; q < NV; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-  int k = o + warp;
-  for (; k + 24 < e; k += 32) {
-    float4 r[4][NV];
-    float d[4];
+  int k = beg + warp;
+  constexpr int U = 8;  // rows in flight per warp
+  for (; k + 8 * (U - 1) < e; k += 8 * U) {
+    float4 r[U][NV];
+    float d[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       d[u] = delta[k + 8 * u];
       const float* rp = w2 + (int64_t)prow[k + 8 * u] * hp + lane * 4;
 #pragma unroll
       for (int q = 0; q < NV; ++q) r[u][q] = ld4(rp + q * 128);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
         acc[q].x = fmaf(d[u], r[u][q].x, acc[q].x);
@@ -457,18 +462,38 @@ __global__ void __launch_bounds__(256) hidden_grad_kernel(int hp, const int32_t*
   for (int q = 0; q < NV; ++q) *reinterpret_cast<float4*>(&red[warp][q * 128 + lane * 4]) = acc[q];
   __syncthreads();
   for (int c = threadIdx.x; c < hp; c += 256) {
-    float s = red[0][c];
+    float sum = red[0][c];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) s += red[w][c];
-    dh[(int64_t)i * hp + c] = h[(int64_t)i * hp + c] > 0.f ? s : 0.f;
+    for (int w = 1; w < 8; ++w) sum += red[w][c];
+    const int64_t q = (int64_t)i * hp + c;
+    if (slices == 1) out[q] = h[q] > 0.f ? sum : 0.f;
+    else out[(int64_t)sl * b * hp + q] = sum;
   }
 }
 
+__global__ void slice_sum_kernel(int64_t n, int slices, const float* __restrict__ part, const float* __restrict__ h,
+                                 float* __restrict__ dh) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    float s = part[q];
+    for (int sl = 1; sl < slices; ++sl) s += part[(int64_t)sl * n + q];
+    dh[q] = h[q] > 0.f ? s : 0.f;
+  }
+}
+
+int hidden_grad_slices(int b) { return std::max(1, std::min(8, (int)ceil_div((int64_t)kSms * 4, b))); }
+
 void launch_hidden_grad(int hp, int b, const int32_t* offs, const int32_t* prow, const float* delta, const float* w2,
-                        const float* h, float* dh, cudaStream_t s) {
+                        const float* h, float* dh, float* part, cudaStream_t s) {
   if (b <= 0) return;
-  SLIDE_NV_DISPATCH(hp, (hidden_grad_kernel<NV><<<b, 256, 0, s>>>(hp, offs, prow, delta, w2, h, dh)));
+  const int S = hidden_grad_slices(b);
+  float* out = S == 1 ? dh : part;
+  SLIDE_NV_DISPATCH(hp, (hidden_grad_kernel<NV><<<b * S, 256, 0, s>>>(hp, b, S, offs, prow, delta, w2, h, out)));
   SLIDE_LAUNCH_CHECK();
+  if (S > 1) {
+    const int64_t n = (int64_t)b * hp;
+    slice_sum_kernel<<<(int)ceil_div(n, 256), 256, 0, s>>>(n, S, part, h, dh);
+    SLIDE_LAUNCH_CHECK();
+  }
 }
 
 // ----------------------------------------------------------- Adam, W2 rows
@@ -481,7 +506,7 @@ void launch_hidden_grad(int hp, int b, const int32_t* offs, const int32_t* prow,
 // keep the update far inside the 1e-4 weight tolerance.
 __device__ __forceinline__ float sqrt_approx(float x) {
   float r;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
 
@@ -516,13 +541,49 @@ __device__ __forceinline__ void adam_coord_if(bool on, float& w, float& m, float
   w = on ? wn : w;
 }
 
+// (c1, c2) for step t: a host-built fp64 table up to the point where both
+// corrections are exactly (lr, 1) in fp32; pow beyond only if the table was
+// capped (betas extremely close to 1).
 __device__ __forceinline__ float2 bias_corr(const AdamParams& ap, int64_t t) {
+  if (t < ap.table_n) return __ldg(ap.table + t);
+  if (ap.table_exact) return make_float2(ap.lr, 1.f);
   const double td = (double)t;
   return make_float2((float)((double)ap.lr / (1.0 - pow(ap.b1d, td))), (float)(1.0 / (1.0 - pow(ap.b2d, td))));
 }
 
-template <int NV>
-__global__ void __launch_bounds__(256) adam_rows_kernel(int hp, AdamParams ap, const int32_t* __restrict__ n_uniq,
+// predicated Adam step with the per-pair factors folded in:
+// e1 = (1-b1) d, e2 = (1-b2) d^2, coordinate gradient g = d h.
+__device__ __forceinline__ void adam_coord_h(bool on, float& w, float& m, float& v, float hc, float e1, float e2,
+                                             float c1, float c2, const AdamK& k) {
+  const float mn = fmaf(k.b1, m, e1 * hc);
+  const float vn = fmaf(k.b2, v, e2 * (hc * hc));
+  const float wn = fmaf(-(c1 * mn), rcp_approx(sqrt_approx(vn * c2) + k.eps), w);
+  m = on ? mn : m;
+  v = on ? vn : v;
+  w = on ? wn : w;
+}
+
+// Stage the batch's activations (b x hp floats) in shared memory: 4
+// independent 16-byte loads in flight per thread.
+__device__ __forceinline__ void stage_rows(float* dst, const float* src, int n_floats) {
+  const int n4 = n_floats / 4;
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  int q = threadIdx.x;
+  for (; q + 3 * (int)blockDim.x < n4; q += 4 * blockDim.x) {
+    const float4 a = __ldg(s4 + q), b = __ldg(s4 + q + blockDim.x), c = __ldg(s4 + q + 2 * blockDim.x),
+                 d = __ldg(s4 + q + 3 * blockDim.x);
+    d4[q] = a;
+    d4[q + blockDim.x] = b;
+    d4[q + 2 * blockDim.x] = c;
+    d4[q + 3 * blockDim.x] = d;
+  }
+  for (; q < n4; q += blockDim.x) d4[q] = __ldg(s4 + q);
+}
+
+template <int NV, bool SMEM_H>
+__global__ void __launch_bounds__(256) adam_rows_kernel(int hp, int b, AdamParams ap,
+                                                        const int32_t* __restrict__ n_uniq,
                                                         const int32_t* __restrict__ uniq,
                                                         const int32_t* __restrict__ seg_off,
                                                         const int32_t* __restrict__ seg_cnt,
@@ -534,6 +595,12 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(int hp, AdamParams ap, c
                                                         float* __restrict__ mb2, float* __restrict__ vb2,
                                                         int64_t* __restrict__ steps2,
                                                         unsigned long long* __restrict__ touched) {
+  extern __shared__ __align__(16) float hs[];
+  if (SMEM_H) {
+    stage_rows(hs, h, b * hp);
+    __syncthreads();
+  }
+  const float* hsrc = SMEM_H ? hs : h;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -553,51 +620,44 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(int hp, AdamParams ap, c
       m[q] = ld4_cg(mr + q * 128);
       v[q] = ld4_cg(vr + q * 128);
     }
-    float b = b2[r], mb = mb2[r], vb = vb2[r];
+    float bb = b2[r], mb = mb2[r], vb = vb2[r];
     const int64_t st = steps2[r];
     for (int c0 = 0; c0 < len; c0 += 32) {
+      // lane j holds the j-th pair of this chunk: its sample, e1, e2, c1, c2
       const int j = c0 + lane;
       int slot_l = 0;
-      float d_l = 0.f;
+      float e1_l = 0.f, e2_l = 0.f, d_l = 0.f;
       float2 bc_l = make_float2(0.f, 1.f);
       if (j < len) {
         const int p = sorted_pairs[s0 + j];
         slot_l = pslot[p];
         d_l = delta[p];
+        e1_l = ak.omb1 * d_l;
+        e2_l = ak.omb2 * d_l * d_l;
         bc_l = bias_corr(ap, st + j + 1);
       }
       const int nc = min(32, len - c0);
-      // software pipeline: the next pair's h row is in flight during the math
-      float4 hn[NV];
-      {
-        const float* hr = h + (int64_t)__shfl_sync(0xffffffffu, slot_l, 0) * hp + lane * 4;
-#pragma unroll
-        for (int q = 0; q < NV; ++q) hn[q] = ld4(hr + q * 128);
-      }
       for (int q2 = 0; q2 < nc; ++q2) {
-        float4 hv[NV];
-#pragma unroll
-        for (int q = 0; q < NV; ++q) hv[q] = hn[q];
+        const int slot = __shfl_sync(0xffffffffu, slot_l, q2);
+        const float e1 = __shfl_sync(0xffffffffu, e1_l, q2);
+        const float e2 = __shfl_sync(0xffffffffu, e2_l, q2);
         const float d = __shfl_sync(0xffffffffu, d_l, q2);
         const float c1 = __shfl_sync(0xffffffffu, bc_l.x, q2);
         const float c2 = __shfl_sync(0xffffffffu, bc_l.y, q2);
-        const int nslot = __shfl_sync(0xffffffffu, slot_l, q2 + 1 < nc ? q2 + 1 : q2);
-        if (q2 + 1 < nc) {
-          const float* hr = h + (int64_t)nslot * hp + lane * 4;
-#pragma unroll
-          for (int q = 0; q < NV; ++q) hn[q] = ld4(hr + q * 128);
-        }
+        const float* hr = hsrc + (int64_t)slot * hp + lane * 4;
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
+          const float4 hv = SMEM_H ? *reinterpret_cast<const float4*>(hr + q * 128) : ld4(hr + q * 128);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const float hc = comp(hv[q], c);
+            const float hc = reinterpret_cast<const float*>(&hv)[c];
             const bool on = hc > 0.f;
-            adam_coord_if(on, comp(w[q], c), comp(m[q], c), comp(v[q], c), d * hc, c1, c2, ak);
+            adam_coord_h(on, comp(w[q], c), comp(m[q], c), comp(v[q], c), hc, e1, e2, c1, c2, ak);
             tmask |= (on ? 1u : 0u) << (q * 4 + c);
           }
         }
-        adam_coord(b, mb, vb, d, c1, c2, ak);
+        adam_coord_h(true, bb, mb, vb, 1.f, e1, e2, c1, c2, ak);  // bias: g = d
+        (void)d;
       }
     }
 #pragma unroll
@@ -607,7 +667,7 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(int hp, AdamParams ap, c
       st4(vr + q * 128, v[q]);
     }
     if (lane == 0) {
-      b2[r] = b;
+      b2[r] = bb;
       mb2[r] = mb;
       vb2[r] = vb;
       steps2[r] = st + len;
@@ -631,16 +691,29 @@ void launch_accumulate(unsigned long long* dst, const int32_t* src, cudaStream_t
   SLIDE_LAUNCH_CHECK();
 }
 
-void launch_adam_rows(int hp, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq, const int32_t* uniq,
-                      const int32_t* seg_off, const int32_t* seg_cnt, const int32_t* sorted_pairs,
-                      const int32_t* pslot, const float* delta, const float* h, float* w2, float* m2, float* v2,
-                      float* b2, float* mb2, float* vb2, int64_t* steps2, unsigned long long* touched,
-                      cudaStream_t s) {
+void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq,
+                      const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
+                      const int32_t* sorted_pairs, const int32_t* pslot, const float* delta, const float* h,
+                      float* w2, float* m2, float* v2, float* b2, float* mb2, float* vb2, int64_t* steps2,
+                      unsigned long long* touched, cudaStream_t s) {
   if (max_uniq <= 0) return;
-  int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * 16);
-  SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV><<<grid, 256, 0, s>>>(hp, ap, n_uniq, uniq, seg_off, seg_cnt,
-                                                                    sorted_pairs, pslot, delta, h, w2, m2, v2, b2,
-                                                                    mb2, vb2, steps2, touched)));
+  const size_t smem = (size_t)b * hp * 4;
+  if (smem <= 100 * 1024) {
+    // persistent: each CTA stages h once, then walks rows grid-stride
+    const int per_sm = smem <= 72 * 1024 ? 3 : 2;
+    int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * per_sm);
+    SLIDE_NV_DISPATCH(hp, ({
+      SLIDE_CUDA(cudaFuncSetAttribute(adam_rows_kernel<NV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+      adam_rows_kernel<NV, true><<<grid, 256, smem, s>>>(hp, b, ap, n_uniq, uniq, seg_off, seg_cnt, sorted_pairs,
+                                                         pslot, delta, h, w2, m2, v2, b2, mb2, vb2, steps2, touched);
+    }));
+  } else {
+    int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * 16);
+    SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, false><<<grid, 256, 0, s>>>(
+                              hp, b, ap, n_uniq, uniq, seg_off, seg_cnt, sorted_pairs, pslot, delta, h, w2, m2, v2,
+                              b2, mb2, vb2, steps2, touched)));
+  }
   SLIDE_LAUNCH_CHECK();
 }
 
@@ -831,6 +904,67 @@ void launch_adam_hidden_bias(int hp, int b, const AdamParams& ap, const float* h
                              const float2* bc, float* b1, float* mb1, float* vb1, int64_t* steps1, cudaStream_t s) {
   adam_hidden_bias_kernel<<<(int)ceil_div((int64_t)hp * 32, 256), 256, 0, s>>>(hp, b, ap, h, dh, tc, bc, b1, mb1,
                                                                                vb1, steps1);
+  SLIDE_LAUNCH_CHECK();
+}
+
+}  // namespace slide
+
+namespace slide {
+
+// Hidden-unit bookkeeping and bias update in one pass, one warp per hidden
+// unit c: tc[i][c] = #{i' <= i : h_i'[c] > 0} (unit c's step for sample i is
+// steps1[c] + tc[i][c], network.py:436-437), the two bias corrections for the
+// W1 Adam, then the bias recurrence over those samples in slot order
+// (g = dh_i[c]) and the step counter.  Runs after the hidden gradient and
+// before the W1 Adam (which reads tc / bc, not steps1).
+__global__ void hidden_prep_bias_kernel(int hp, int b, AdamParams ap, const float* __restrict__ h,
+                                        const float* __restrict__ dh, int64_t* __restrict__ steps1,
+                                        int32_t* __restrict__ tc, float2* __restrict__ bc, float* __restrict__ b1,
+                                        float* __restrict__ mb1, float* __restrict__ vb1) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (c >= hp) return;
+  const AdamK ak(ap);
+  const int64_t st = steps1[c];
+  float bb = b1[c], mb = mb1[c], vb = vb1[c];
+  int run = 0;
+  for (int i0 = 0; i0 < b; i0 += 32) {
+    const int i = i0 + lane;
+    const int64_t q = (int64_t)i * hp + c;
+    const bool act = i < b && h[q] > 0.f;
+    const unsigned mask = __ballot_sync(0xffffffffu, act);
+    const int cnt = run + __popc(mask & ((1u << lane) - 1u)) + (act ? 1 : 0);
+    float g = 0.f;
+    float2 cc = make_float2(0.f, 1.f);
+    if (i < b) {
+      tc[q] = cnt;
+      if (act) {
+        cc = bias_corr(ap, st + cnt);
+        bc[q] = cc;
+        g = dh[q];
+      }
+    }
+    unsigned todo = mask;
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      adam_coord(bb, mb, vb, __shfl_sync(0xffffffffu, g, src), __shfl_sync(0xffffffffu, cc.x, src),
+                 __shfl_sync(0xffffffffu, cc.y, src), ak);
+    }
+    run += __popc(mask);
+  }
+  if (lane == 0) {
+    b1[c] = bb;
+    mb1[c] = mb;
+    vb1[c] = vb;
+    steps1[c] = st + run;
+  }
+}
+
+void launch_hidden_prep_bias(int hp, int b, const AdamParams& ap, const float* h, const float* dh, int64_t* steps1,
+                             int32_t* tc, float2* bc, float* b1, float* mb1, float* vb1, cudaStream_t s) {
+  if (b <= 0) return;
+  hidden_prep_bias_kernel<<<(int)ceil_div((int64_t)hp * 32, 256), 256, 0, s>>>(hp, b, ap, h, dh, steps1, tc, bc, b1,
+                                                                             mb1, vb1);
   SLIDE_LAUNCH_CHECK();
 }
 

@@ -18,11 +18,12 @@ namespace slide {
 // ------------------------------------------------------------ per-slot rng
 // default_rng((seed, iteration, slot)) (network.py:353) or an explicit
 // Generator state; vanilla draws permutation(L) first (samplers.py:69).
-__global__ void slot_rng_kernel(int b, uint64_t seed, int64_t iteration, int64_t slot_offset, int l,
-                                int vanilla, const uint64_t* __restrict__ ext, uint64_t* __restrict__ states,
-                                uint8_t* __restrict__ order) {
+__global__ void slot_rng_kernel(int b, uint64_t seed, int64_t iteration, const int64_t* iter_dev,
+                                int64_t slot_offset, int l, int vanilla, const uint64_t* __restrict__ ext,
+                                uint64_t* __restrict__ states, uint8_t* __restrict__ order) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= b) return;
+  if (iter_dev) iteration = *iter_dev;  // graph replays read the step number from memory
   Pcg64 g;
   if (ext) {
     g.load(ext + 6 * i);
@@ -38,9 +39,9 @@ __global__ void slot_rng_kernel(int b, uint64_t seed, int64_t iteration, int64_t
   g.store(states + 6 * i);
 }
 
-void launch_slot_rng(int b, uint64_t seed, int64_t it, int64_t off, int l, int vanilla, const uint64_t* ext,
-                     uint64_t* states, uint8_t* order, cudaStream_t s) {
-  slot_rng_kernel<<<(int)ceil_div(b, 64), 64, 0, s>>>(b, seed, it, off, l, vanilla, ext, states, order);
+void launch_slot_rng(int b, uint64_t seed, int64_t it, const int64_t* it_dev, int64_t off, int l, int vanilla,
+                     const uint64_t* ext, uint64_t* states, uint8_t* order, cudaStream_t s) {
+  slot_rng_kernel<<<(int)ceil_div(b, 64), 64, 0, s>>>(b, seed, it, it_dev, off, l, vanilla, ext, states, order);
   SLIDE_LAUNCH_CHECK();
 }
 
@@ -266,6 +267,98 @@ void launch_select(const SelectArgs& a, int max_candidates, cudaStream_t s) {
   else throw Error(kNotSupported, "L*capacity + labels exceeds 16384 candidates per sample");
 }
 
+// Full-union selection (vanilla with beta >= L*cap: every table is probed and
+// every id kept, samplers.py:57-87): a shared-memory bitmap over the N output
+// ids replaces the sort.  The sampler result is empty exactly when all L
+// probed buckets are empty.
+__global__ void __launch_bounds__(256) select_union_kernel(SelectArgs a, int words) {
+  using Scan = cub::BlockScan<int, 256>;
+  extern __shared__ __align__(16) uint32_t bm[];
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ int s_start[64], s_len[64], s_tot;
+  const int i = blockIdx.x, tid = threadIdx.x, L = a.l;
+  const int y0 = a.y_ptr[i], ny = a.y_ptr[i + 1] - y0;
+  for (int w = tid; w < words; w += 256) bm[w] = 0u;
+  if (tid < L) {
+    const uint32_t skey = ((uint32_t)tid << a.tab.key_bits) | a.qkeys[(int64_t)i * L + tid];
+    const int run = tables_lookup(a.tab, skey);
+    s_start[tid] = run >= 0 ? a.tab.bstart[run] : 0;
+    s_len[tid] = run >= 0 ? a.tab.blen[run] : 0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int t = 0;
+    for (int q = 0; q < L; ++q) t += s_len[q];
+    s_tot = t;
+    if (a.cand_ctr) atomicAdd(a.cand_ctr, (unsigned long long)t);
+  }
+  __syncthreads();
+  if (s_tot == 0) {  // nothing retrieved: the fallback kernel takes this slot
+    if (tid == 0) {
+      a.empty[i] = 1;
+      a.cnt[i] = 0;
+    }
+    return;
+  }
+  {
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int t = warp; t < L; t += 8) {
+      const int32_t* src = a.tab.ids + s_start[t];
+      for (int j = lane; j < s_len[t]; j += 32) {
+        const uint32_t id = (uint32_t)src[j];
+        atomicOr(&bm[id >> 5], 1u << (id & 31));
+      }
+    }
+    for (int j = tid; j < ny; j += 256) {
+      const uint32_t id = (uint32_t)a.y_idx[y0 + j];
+      atomicOr(&bm[id >> 5], 1u << (id & 31));
+    }
+  }
+  __syncthreads();
+  const int ch = (words + 255) / 256;
+  const int w0 = min(tid * ch, words), w1 = min(w0 + ch, words);
+  int cnt = 0;
+  for (int w = w0; w < w1; ++w) cnt += __popc(bm[w]);
+  int ofs, total;
+  Scan(scan_tmp).ExclusiveSum(cnt, ofs, total);
+  int32_t* out = a.act + (int64_t)i * a.cap_max;
+  const int32_t* lab = a.y_idx + y0;
+  int lpos = 0;  // labels are sorted and so are the ids of this thread's chunk
+  for (int w = w0; w < w1; ++w) {
+    uint32_t bits = bm[w];
+    while (bits) {
+      const int id = w * 32 + __ffs(bits) - 1;
+      bits &= bits - 1;
+      if (lpos < ny && lab[lpos] < id) {  // first label >= id (binary search)
+        int lo = lpos, hi = ny;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (lab[mid] < id) lo = mid + 1;
+          else hi = mid;
+        }
+        lpos = lo;
+      }
+      const int is_lab = lpos < ny && lab[lpos] == id;
+      out[ofs++] = (int32_t)((uint32_t)id | ((uint32_t)is_lab << 31));
+    }
+  }
+  if (tid == 0) {
+    a.empty[i] = 0;
+    a.cnt[i] = total;
+  }
+}
+
+bool launch_select_union(const SelectArgs& a, int64_t n_out, cudaStream_t s) {
+  const int words = (int)ceil_div(n_out, 32);
+  const size_t smem = (size_t)words * 4;
+  if (smem > 160 * 1024) return false;
+  if (smem > 48 * 1024)
+    SLIDE_CUDA(cudaFuncSetAttribute(select_union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  select_union_kernel<<<a.b, 256, smem, s>>>(a, words);
+  SLIDE_LAUNCH_CHECK();
+  return true;
+}
+
 // --------------------------------------------------------------- fallback
 // Empty sampler result: beta uniform ids without replacement from the slot's
 // generator (network.py:229-231), union labels, sorted (network.py:236-238).
@@ -283,7 +376,8 @@ __global__ void __launch_bounds__(256) fallback_kernel(FallbackArgs a) {
     if (a.states_ready) {
       g.load(a.states + 6 * i);
     } else {  // slot stream not drawn yet (full-union vanilla): seed + probe order first
-      uint64_t ent[3] = {a.seed, (uint64_t)a.iteration, (uint64_t)(a.slot_offset + i)};
+      const int64_t it = a.iter_dev ? *a.iter_dev : a.iteration;
+      uint64_t ent[3] = {a.seed, (uint64_t)it, (uint64_t)(a.slot_offset + i)};
       g.seed_from(ent, 3);
       if (a.vanilla) {
         uint8_t perm[64];

@@ -503,15 +503,51 @@ class SlideNetwork:
         loss, active = self._step(csr, iteration, 1 if schedule == "sequential" else B)
         return self._barrier(iteration, loss, active)
 
+    #: snapshot steps replay one captured CUDA graph per batch shape
+    use_graphs = True
+
+    def _pinned_batch(self, csr: HostCsr):
+        """Batch struct over pinned host copies of the CSR (graph steps copy
+        them into the context's own device buffers)."""
+        import torch
+
+        self.h2d_bytes = 0
+        keep = []
+
+        def pin(name, a, dt):
+            a = np.ascontiguousarray(a, dtype=dt)
+            buf = self._pinned.get(("g", name))
+            if buf is None or buf.numel() < max(a.size, 1):
+                buf = torch.empty(max(a.size, 1) * 2, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
+                self._pinned[("g", name)] = buf
+            buf.numpy()[: a.size] = a
+            self.h2d_bytes += a.nbytes
+            keep.append(buf)
+            return buf.data_ptr()
+
+        bt = _lib.Batch()
+        bt.batch = csr.batch
+        bt.x_ptr_host = bt.x_ptr = pin("xp", csr.x_ptr, np.int32)
+        bt.x_idx = pin("xi", csr.x_idx, np.int32)
+        bt.x_val = pin("xv", csr.x_val, np.float32)
+        bt.y_ptr_host = bt.y_ptr = pin("yp", csr.y_ptr, np.int32)
+        bt.y_idx = pin("yi", csr.y_idx, np.int32)
+        return bt, keep
+
     def _step(self, csr: HostCsr, iteration: int, sub_batch: int):
         if self.layers[1].lsh is not None:
             self.layers[1].lsh.sync_to_device()
-        bt, keep = self._upload(csr)
         B = csr.batch
         loss = np.empty(B, dtype=np.float64)
         active = np.empty(B, dtype=np.int64)
-        _lib.call("slide_train_batch", self._ctx, _lib.C.byref(bt), iteration, sub_batch, loss.ctypes.data,
-                  active.ctypes.data)
+        if sub_batch == B and self.use_graphs:
+            bt, keep = self._pinned_batch(csr)
+            _lib.call("slide_graph_step", self._ctx, _lib.C.byref(bt), iteration, loss.ctypes.data,
+                      active.ctypes.data)
+        else:
+            bt, keep = self._upload(csr)
+            _lib.call("slide_train_batch", self._ctx, _lib.C.byref(bt), iteration, sub_batch, loss.ctypes.data,
+                      active.ctypes.data)
         del keep
         return loss, active
 

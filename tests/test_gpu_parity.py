@@ -114,6 +114,31 @@ NET_SETUPS = {
 }
 
 
+@pytest.mark.parametrize("family", ["simhash", "dwta"])
+def test_full_union_vanilla_matches_oracle(family):
+    """beta >= L*cap: every table is probed (the bitmap selection path)."""
+    rng = np.random.default_rng(8)
+    D, H, N, B = 60, 16, 300, 8
+    spec = LshLayerConfig(family, k=2, l=6, capacity=8, wta_bin_size=4, policy="fifo",
+                          sampler=SamplerConfig("vanilla", beta=100))
+    cfg = TrainConfig(batch_size=B, seed=4, learning_rate=1e-2, n0=2)
+    net = SlideNetwork(D, [H, N], cfg, lsh_layers={1: spec})
+    st = oracle_state_from_net(net)
+    lsh = oracle_lsh_from_net(net, spec, st)
+    for it in (1, 2, 3):
+        batch = []
+        for _ in range(B):
+            idx = np.sort(rng.choice(D, size=int(rng.integers(1, 10)), replace=False))
+            vals = (np.abs(rng.standard_normal(idx.size)) + 0.1).astype(np.float32).astype(np.float64)
+            batch.append((SparseVector(idx, vals, D), set(rng.choice(N, size=2, replace=False).tolist())))
+        trip = [(x.indices, x.values, sorted(y)) for x, y in batch]
+        want = O.train_step(st, lsh, trip, it, cfg.seed, N, O.AdamCfg(lr=1e-2), mode="snapshot")
+        got = net.train_batch(batch, it, schedule="snapshot")
+        assert got.loss == pytest.approx(float(np.mean(want.losses)), rel=1e-5)
+        assert got.active_fraction[1] == pytest.approx(want.active_fraction, rel=1e-12)
+        assert_state_close(net, st, what=f"full-union {family} it{it}")
+
+
 def _golden_batch(g, name, it, B):
     return [(g[f"{name}_it{it}_x{i}_idx"], g[f"{name}_it{it}_x{i}_val"], g[f"{name}_it{it}_y{i}"].tolist())
             for i in range(B)]
@@ -315,6 +340,34 @@ def test_snapshot_step_is_deterministic():
         outs.append((net.w2.cpu().numpy().copy(), net.w1t.cpu().numpy().copy(), net.m2.cpu().numpy().copy()))
     for a, b in zip(*outs):
         np.testing.assert_array_equal(a, b)
+
+
+def test_graph_steps_equal_eager_steps():
+    """The captured-graph snapshot step (eager run, capture, replays, a
+    re-capture on a larger batch) is bit-identical to eager snapshot steps."""
+    from paper_1903_03129_b200.configs import TINY as w
+    from paper_1903_03129_b200.data import synthetic_corpus
+
+    corpus = synthetic_corpus(w.corpus, 6 * 64, seed=5)
+
+    def run(graphs):
+        cfg = TrainConfig(batch_size=64, seed=0, learning_rate=w.lr, n0=3)
+        spec = LshLayerConfig("simhash", k=w.k, l=w.l, capacity=w.cap, sampler=SamplerConfig("vanilla", beta=w.beta))
+        net = SlideNetwork(w.input_dim, [w.hidden, w.n_out], cfg, lsh_layers={1: spec})
+        net.use_graphs = graphs
+        losses = []
+        for it in range(1, 7):
+            sub = corpus.subset(np.arange((it - 1) * 64, it * 64))
+            if it == 5:  # heavier batch: grows the capacities -> re-capture
+                sub = corpus.subset(np.concatenate([np.arange(0, 64)] * 1)[:64])
+            csr = HostCsr(sub.x_ptr.astype(np.int32), sub.x_idx, sub.x_val, sub.y_ptr.astype(np.int32), sub.y_idx)
+            losses.append(net.train_batch_csr(csr, it, schedule="snapshot").loss)
+        return losses, net.w2.cpu().numpy(), net.w1t.cpu().numpy(), net.v2.cpu().numpy()
+
+    a, b = run(True), run(False)
+    assert a[0] == b[0]
+    for x, y in zip(a[1:], b[1:]):
+        np.testing.assert_array_equal(x, y)
 
 
 def test_backward_capture_matches_finite_differences_shape():
