@@ -59,7 +59,7 @@ struct slide_ctx {
   cudaStream_t s = nullptr;
   int hp = 0;
   TablesHost tab;
-  DBuf sh_packed, dw_perms, dw_donors, rowkeys;
+  DBuf sh_packed, sh_packed_t, dw_perms, dw_donors, rowkeys;
   // forward workspace
   DBuf h, qkeys, order, states, act, cnt, empty, offs, prow, pslot, plab, z, prob, delta, loss, dh;
   DBuf fb_ids, fb_scratch, fb_bitmap;
@@ -172,6 +172,7 @@ static SimHashDev simhash_of(slide_ctx* c) {
   f.l = (int)c->d.l;
   f.c = (int)c->d.sh_c;
   f.packed = c->sh_packed.as<uint16_t>();
+  f.packed_t = c->sh_packed_t.as<uint16_t>();
   return f;
 }
 
@@ -233,6 +234,12 @@ int slide_create(const slide_net_desc* desc, void* stream, slide_ctx** out) {
         size_t n = (size_t)d.k * d.l * d.sh_c;
         SLIDE_CHECK(d.sh_packed_host != nullptr, kValueError, "simhash projections missing");
         SLIDE_CUDA(cudaMemcpy(c->sh_packed.ensure<uint16_t>(n), d.sh_packed_host, n * 2, cudaMemcpyHostToDevice));
+        // (c, K*L) transposed copy for the per-sample query kernel
+        const int64_t KL = d.k * d.l;
+        std::vector<uint16_t> tr(n);
+        for (int64_t p = 0; p < KL; ++p)
+          for (int64_t j = 0; j < d.sh_c; ++j) tr[j * KL + p] = d.sh_packed_host[p * d.sh_c + j];
+        SLIDE_CUDA(cudaMemcpy(c->sh_packed_t.ensure<uint16_t>(n), tr.data(), n * 2, cudaMemcpyHostToDevice));
       } else if (d.family >= 2) {
         size_t np = (size_t)d.n_perms * d.hidden, nd = (size_t)d.k * d.l * 100;
         SLIDE_CHECK(d.dw_perms_host && d.dw_donors_host, kValueError, "dwta permutations missing");
@@ -252,7 +259,7 @@ int slide_destroy(slide_ctx* c) {
     if (!c) return;
     cudaStreamSynchronize(c->s);
     c->tab.release();
-    for (DBuf* b : {&c->sh_packed, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->qkeys, &c->order,
+    for (DBuf* b : {&c->sh_packed, &c->sh_packed_t, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->qkeys, &c->order,
                     &c->states, &c->act, &c->cnt, &c->empty, &c->offs, &c->prow, &c->pslot, &c->plab, &c->z,
                     &c->prob, &c->delta, &c->loss, &c->dh, &c->fb_ids, &c->fb_scratch, &c->fb_bitmap, &c->xslot,
                     &c->tc, &c->bc, &c->counters, &c->partial, &c->bias_table})

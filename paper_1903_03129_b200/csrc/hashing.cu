@@ -83,9 +83,48 @@ static void launch_simhash_t(const SimHashDev& f, const float* x, int64_t n, int
   SLIDE_LAUNCH_CHECK();
 }
 
+// Per-sample queries: one row per CTA, the row in shared memory, the
+// transposed projection table read straight from L1/L2 (coalesced across
+// the projections) instead of being staged by every CTA.
+__global__ void __launch_bounds__(512) simhash_query_kernel(SimHashDev f, const float* __restrict__ x, int ld,
+                                                            uint32_t* __restrict__ keys) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int KL = f.k * f.l;
+  float* xs = reinterpret_cast<float*>(sm);
+  uint8_t* bits = reinterpret_cast<uint8_t*>(xs + f.dim);
+  const int64_t row = blockIdx.x;
+  for (int c = threadIdx.x; c < f.dim; c += blockDim.x) xs[c] = x[row * ld + c];
+  __syncthreads();
+  for (int p = threadIdx.x; p < KL; p += blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < f.c; ++j) {
+      const uint16_t e = __ldg(f.packed_t + j * KL + p);
+      const double v = (double)xs[e & 0x7fff];
+      acc += (e >> 15) ? -v : v;
+    }
+    bits[p] = acc > 0.0;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < f.l; t += blockDim.x) {
+    uint32_t key = 0;
+    for (int kk = 0; kk < f.k; ++kk) key |= (uint32_t)bits[t * f.k + kk] << kk;
+    keys[row * f.l + t] = key;
+  }
+}
+
 void launch_simhash_keys(const SimHashDev& f, const float* x, int64_t n, int ld, uint32_t* keys,
                          cudaStream_t s) {
   if (n <= 0) return;
+  const int KL = f.k * f.l;
+  if (f.packed_t && n <= (int64_t)kSms * 8) {
+    const size_t smem = (size_t)f.dim * 4 + KL;
+    SLIDE_CHECK(smem <= 200 * 1024, kNotSupported, "simhash dim too large for shared memory");
+    if (smem > 48 * 1024)
+      SLIDE_CUDA(cudaFuncSetAttribute(simhash_query_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    simhash_query_kernel<<<(int)n, 512, smem, s>>>(f, x, ld, keys);
+    SLIDE_LAUNCH_CHECK();
+    return;
+  }
   // few rows (per-sample queries): one row per CTA fills the SMs
   if (n <= (int64_t)kSms * 8) launch_simhash_t<1>(f, x, n, ld, keys, s);
   else launch_simhash_t<8>(f, x, n, ld, keys, s);

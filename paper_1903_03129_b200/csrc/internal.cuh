@@ -39,6 +39,7 @@ struct DBuf {
 struct SimHashDev {
   int dim, k, l, c;
   const uint16_t* packed;  // (K*L, c): idx | (sign<0) << 15
+  const uint16_t* packed_t = nullptr;  // optional (c, K*L) copy: queries read it from L1/L2
 };
 struct DwtaDev {
   int dim, k, l, m, bins_per_perm, n_perms, bits;

@@ -31,34 +31,41 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 // ------------------------------------------------------------ hidden forward
 // z1 = sum_f x_f W1^T[f, :] + b1, h = max(z1, 0) (network.py:262-280).  One
-// CTA per sample, 8 warps each own every 8th nonzero; partial sums are added
-// in warp order (deterministic).
+// CTA of 32 warps per sample (a sample has ~75-300 nonzeros: enough rows in
+// flight per SM), warp w owns every 32nd nonzero; partial sums are added in
+// warp order (deterministic).
 template <int NV>
-__global__ void __launch_bounds__(256) hidden_fwd_kernel(int hp, const int32_t* __restrict__ x_ptr,
-                                                         const int32_t* __restrict__ x_idx,
-                                                         const float* __restrict__ x_val,
-                                                         const float* __restrict__ w1t,
-                                                         const float* __restrict__ b1, float* __restrict__ h) {
-  __shared__ float red[8][NV * 128];
+struct FwdWarps {
+  static constexpr int value = NV <= 2 ? 32 : 8;  // static smem: warps x hp floats <= 32 KB
+};
+
+template <int NV, int kFwdWarps = FwdWarps<NV>::value>
+__global__ void __launch_bounds__(kFwdWarps * 32) hidden_fwd_kernel(int hp, const int32_t* __restrict__ x_ptr,
+                                                                    const int32_t* __restrict__ x_idx,
+                                                                    const float* __restrict__ x_val,
+                                                                    const float* __restrict__ w1t,
+                                                                    const float* __restrict__ b1,
+                                                                    float* __restrict__ h) {
+  __shared__ float red[kFwdWarps][NV * 128];
   const int i = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int a = x_ptr[i], e = x_ptr[i + 1];
   float4 acc[NV];
 #pragma unroll
   for (int q = 0; q < NV; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   int k = a + warp;
-  for (; k + 24 < e; k += 32) {
-    float4 r[4][NV];
-    float v[4];
+  for (; k + kFwdWarps < e; k += 2 * kFwdWarps) {
+    float4 r[2][NV];
+    float v[2];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int f = x_idx[k + 8 * u];
-      v[u] = x_val[k + 8 * u];
+    for (int u = 0; u < 2; ++u) {
+      const int f = x_idx[k + kFwdWarps * u];
+      v[u] = x_val[k + kFwdWarps * u];
       const float* row = w1t + (int64_t)f * hp + lane * 4;
 #pragma unroll
       for (int q = 0; q < NV; ++q) r[u][q] = ld4(row + q * 128);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < 2; ++u)
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
         acc[q].x = fmaf(v[u], r[u][q].x, acc[q].x);
@@ -67,7 +74,7 @@ __global__ void __launch_bounds__(256) hidden_fwd_kernel(int hp, const int32_t* 
         acc[q].w = fmaf(v[u], r[u][q].w, acc[q].w);
       }
   }
-  for (; k < e; k += 8) {
+  for (; k < e; k += kFwdWarps) {
     const int f = x_idx[k];
     const float v = x_val[k];
     const float* row = w1t + (int64_t)f * hp + lane * 4;
@@ -83,10 +90,10 @@ __global__ void __launch_bounds__(256) hidden_fwd_kernel(int hp, const int32_t* 
 #pragma unroll
   for (int q = 0; q < NV; ++q) *reinterpret_cast<float4*>(&red[warp][q * 128 + lane * 4]) = acc[q];
   __syncthreads();
-  for (int c = threadIdx.x; c < hp; c += 256) {
+  for (int c = threadIdx.x; c < hp; c += kFwdWarps * 32) {
     float s = red[0][c];
-#pragma unroll
-    for (int w = 1; w < 8; ++w) s += red[w][c];
+#pragma unroll 8
+    for (int w = 1; w < kFwdWarps; ++w) s += red[w][c];
     s += b1[c];
     h[(int64_t)i * hp + c] = s > 0.f ? s : 0.f;
   }
@@ -95,7 +102,7 @@ __global__ void __launch_bounds__(256) hidden_fwd_kernel(int hp, const int32_t* 
 void launch_hidden_forward(int hp, int b, const int32_t* x_ptr, const int32_t* x_idx, const float* x_val,
                            const float* w1t, const float* b1, float* h, cudaStream_t s) {
   if (b <= 0) return;
-  SLIDE_NV_DISPATCH(hp, (hidden_fwd_kernel<NV><<<b, 256, 0, s>>>(hp, x_ptr, x_idx, x_val, w1t, b1, h)));
+  SLIDE_NV_DISPATCH(hp, (hidden_fwd_kernel<NV><<<b, FwdWarps<NV>::value * 32, 0, s>>>(hp, x_ptr, x_idx, x_val, w1t, b1, h)));
   SLIDE_LAUNCH_CHECK();
 }
 
@@ -353,13 +360,13 @@ bool launch_hidden_grad_rows(int hp, int b, const int32_t* n_uniq, const int32_t
 // p = softmax over the active set (max-shifted, network.py:282-285);
 // delta = p - [label]/|Y| (network.py:308-309); loss = mean over labels of
 // -log(max(p_y, 1e-300)) (network.py:154-158), taken as a log-softmax.
-__global__ void __launch_bounds__(256) softmax_kernel(const int32_t* __restrict__ offs,
+__global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict__ offs,
                                                       const uint8_t* __restrict__ plab,
                                                       const int32_t* __restrict__ y_ptr, const float* __restrict__ z,
                                                       float* __restrict__ prob, float* __restrict__ delta,
                                                       double* __restrict__ loss) {
-  using RF = cub::BlockReduce<float, 256>;
-  using RD = cub::BlockReduce<double, 256>;
+  using RF = cub::BlockReduce<float, 1024>;
+  using RD = cub::BlockReduce<double, 1024>;
   __shared__ union {
     typename RF::TempStorage f;
     typename RD::TempStorage d;
@@ -369,13 +376,13 @@ __global__ void __launch_bounds__(256) softmax_kernel(const int32_t* __restrict_
   const int o = offs[i], n = offs[i + 1] - o;
   const int ny = y_ptr[i + 1] - y_ptr[i];
   float mx = -INFINITY;
-  for (int k = tid; k < n; k += 256) mx = fmaxf(mx, z[o + k]);
+  for (int k = tid; k < n; k += 1024) mx = fmaxf(mx, z[o + k]);
   mx = RF(tmp.f).Reduce(mx, cub::Max());
   if (tid == 0) s_max = n > 0 ? mx : 0.f;
   __syncthreads();
   mx = s_max;
   float se = 0.f;
-  for (int k = tid; k < n; k += 256) se += expf(z[o + k] - mx);
+  for (int k = tid; k < n; k += 1024) se += expf(z[o + k] - mx);
   se = RF(tmp.f).Sum(se);
   if (tid == 0) s_sum = se;
   __syncthreads();
@@ -383,7 +390,7 @@ __global__ void __launch_bounds__(256) softmax_kernel(const int32_t* __restrict_
   const float lse = logf(se);
   const float inv_ny = ny > 0 ? 1.f / (float)ny : 0.f;
   double lsum = 0.0;
-  for (int k = tid; k < n; k += 256) {
+  for (int k = tid; k < n; k += 1024) {
     const float zz = z[o + k] - mx;
     const float p = expf(zz) / se;
     const int lab = plab[o + k];
@@ -401,7 +408,7 @@ __global__ void __launch_bounds__(256) softmax_kernel(const int32_t* __restrict_
 void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
                     float* prob, float* delta, double* loss, cudaStream_t s) {
   if (b <= 0) return;
-  softmax_kernel<<<b, 256, 0, s>>>(offs, plab, y_ptr, z, prob, delta, loss);
+  softmax_kernel<<<b, 1024, 0, s>>>(offs, plab, y_ptr, z, prob, delta, loss);
   SLIDE_LAUNCH_CHECK();
 }
 

@@ -271,14 +271,17 @@ void launch_select(const SelectArgs& a, int max_candidates, cudaStream_t s) {
 // every id kept, samplers.py:57-87): a shared-memory bitmap over the N output
 // ids replaces the sort.  The sampler result is empty exactly when all L
 // probed buckets are empty.
-__global__ void __launch_bounds__(256) select_union_kernel(SelectArgs a, int words) {
-  using Scan = cub::BlockScan<int, 256>;
-  extern __shared__ __align__(16) uint32_t bm[];
+constexpr int kUnionThreads = 1024;
+
+__global__ void __launch_bounds__(kUnionThreads) select_union_kernel(SelectArgs a, int words) {
+  using Scan = cub::BlockScan<int, kUnionThreads>;
+  extern __shared__ __align__(16) uint32_t bm[];  // [words] ids, then [words] labels
+  uint32_t* lb = bm + words;
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ int s_start[64], s_len[64], s_tot;
   const int i = blockIdx.x, tid = threadIdx.x, L = a.l;
   const int y0 = a.y_ptr[i], ny = a.y_ptr[i + 1] - y0;
-  for (int w = tid; w < words; w += 256) bm[w] = 0u;
+  for (int w = tid; w < 2 * words; w += kUnionThreads) bm[w] = 0u;
   if (tid < L) {
     const uint32_t skey = ((uint32_t)tid << a.tab.key_bits) | a.qkeys[(int64_t)i * L + tid];
     const int run = tables_lookup(a.tab, skey);
@@ -302,44 +305,34 @@ __global__ void __launch_bounds__(256) select_union_kernel(SelectArgs a, int wor
   }
   {
     const int warp = tid >> 5, lane = tid & 31;
-    for (int t = warp; t < L; t += 8) {
+    for (int t = warp; t < L; t += kUnionThreads / 32) {
       const int32_t* src = a.tab.ids + s_start[t];
       for (int j = lane; j < s_len[t]; j += 32) {
         const uint32_t id = (uint32_t)src[j];
         atomicOr(&bm[id >> 5], 1u << (id & 31));
       }
     }
-    for (int j = tid; j < ny; j += 256) {
+    for (int j = tid; j < ny; j += kUnionThreads) {
       const uint32_t id = (uint32_t)a.y_idx[y0 + j];
       atomicOr(&bm[id >> 5], 1u << (id & 31));
+      atomicOr(&lb[id >> 5], 1u << (id & 31));
     }
   }
   __syncthreads();
-  const int ch = (words + 255) / 256;
+  const int ch = (words + kUnionThreads - 1) / kUnionThreads;
   const int w0 = min(tid * ch, words), w1 = min(w0 + ch, words);
   int cnt = 0;
   for (int w = w0; w < w1; ++w) cnt += __popc(bm[w]);
   int ofs, total;
   Scan(scan_tmp).ExclusiveSum(cnt, ofs, total);
   int32_t* out = a.act + (int64_t)i * a.cap_max;
-  const int32_t* lab = a.y_idx + y0;
-  int lpos = 0;  // labels are sorted and so are the ids of this thread's chunk
   for (int w = w0; w < w1; ++w) {
     uint32_t bits = bm[w];
+    const uint32_t labs = lb[w];
     while (bits) {
-      const int id = w * 32 + __ffs(bits) - 1;
+      const int bit = __ffs(bits) - 1;
       bits &= bits - 1;
-      if (lpos < ny && lab[lpos] < id) {  // first label >= id (binary search)
-        int lo = lpos, hi = ny;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (lab[mid] < id) lo = mid + 1;
-          else hi = mid;
-        }
-        lpos = lo;
-      }
-      const int is_lab = lpos < ny && lab[lpos] == id;
-      out[ofs++] = (int32_t)((uint32_t)id | ((uint32_t)is_lab << 31));
+      out[ofs++] = (int32_t)((uint32_t)(w * 32 + bit) | (((labs >> bit) & 1u) << 31));
     }
   }
   if (tid == 0) {
@@ -350,11 +343,11 @@ __global__ void __launch_bounds__(256) select_union_kernel(SelectArgs a, int wor
 
 bool launch_select_union(const SelectArgs& a, int64_t n_out, cudaStream_t s) {
   const int words = (int)ceil_div(n_out, 32);
-  const size_t smem = (size_t)words * 4;
-  if (smem > 160 * 1024) return false;
+  const size_t smem = (size_t)words * 8;
+  if (smem > 200 * 1024) return false;
   if (smem > 48 * 1024)
     SLIDE_CUDA(cudaFuncSetAttribute(select_union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  select_union_kernel<<<a.b, 256, smem, s>>>(a, words);
+  select_union_kernel<<<a.b, kUnionThreads, smem, s>>>(a, words);
   SLIDE_LAUNCH_CHECK();
   return true;
 }
