@@ -60,6 +60,11 @@ typedef struct slide_net_desc {
   int64_t* steps1;
   float *w2, *m2, *v2, *b2, *mb2, *vb2;
   int64_t* steps2;
+  /* column sharding of the output layer: this context owns
+   * the rows id with id % shard_count == shard_rank, stored at local row
+   * id / shard_count (W2 and its state hold only those rows).  0 / 1 =
+   * unsharded. */
+  int64_t shard_rank, shard_count;
 } slide_net_desc;
 
 /* One batch as device CSR (int32 offsets are absolute into idx/val).  The
@@ -154,13 +159,34 @@ int slide_graph_step(slide_ctx* ctx, const slide_batch* batch, int64_t iteration
  * 0 h (B, hp) f32 | 1 query keys (B, L) u32 | 2 offsets (B+1) i32 |
  * 3 pair rows (P) i32 | 4 pair label flag (P) u8 | 5 probs (P) f32 |
  * 6 delta (P) f32 | 7 loss (B) f64 | 8 dh (B, hp) f32 | 9 empty (B) i32 |
- * 10 rng states (B, 6) u64 | 11 logits (P) f32 (before softmax) */
+ * 10 rng states (B, 6) u64 | 11 logits (P) f32 (before softmax) |
+ * 12 global active-set size per slot (B) i32 */
 int slide_read(slide_ctx* ctx, int64_t what, void* host_dst, int64_t max_bytes, int64_t* bytes);
 /* overwrite stage 0 (h) or 6 (delta) of the last forward with host values
  * (exact size): backward(trace) replays a trace's forward-time activations
  * and errors, as the reference's backward reads them from the trace
  * (network.py:303-313). */
 int slide_write(slide_ctx* ctx, int64_t what, const void* host_src, int64_t bytes);
+
+/* -- sharded step (shard_count > 1): the caller all-reduces between the
+ *    stages over its process group (torch.distributed / NCCL).  Tables are
+ *    built from the all-gathered keys of every rank's rows, so selection is
+ *    replicated and identical to the single-GPU path; each rank keeps its
+ *    owned (sample, row) pairs. -------------------------------------------- */
+/* keys (dev, local_rows x L) of this rank's W2 rows */
+int slide_shard_hash_rows(slide_ctx* ctx, uint32_t* keys);
+/* forward up to the local logits; max_out (dev, B): per-sample max over
+ * owned pairs (-inf when none) -> all-reduce MAX */
+int slide_shard_forward(slide_ctx* ctx, const slide_batch* batch, int64_t iteration, float* max_out);
+/* sum_out (dev, B): sum of exp(z - gmax) over owned pairs -> all-reduce SUM */
+int slide_shard_softmax_sum(slide_ctx* ctx, const float* gmax, float* sum_out);
+/* p, delta on owned pairs; loss_out (dev, B, f64): sum over owned labels of
+ * min(-log p, 690.78) -> all-reduce SUM, then divide by |Y_i| */
+int slide_shard_softmax_finish(slide_ctx* ctx, const float* gmax, const float* gsum, double* loss_out);
+/* dh_out (dev, B x hidden_pad): W2_local^T delta (pre-update) -> all-reduce SUM */
+int slide_shard_hidden_grad(slide_ctx* ctx, float* dh_out);
+/* Adam on the owned W2 rows and (replicated) W1 with the all-reduced dh */
+int slide_shard_update(slide_ctx* ctx, const float* dh);
 
 /* -- measurement -------------------------------------------------------- */
 /* on != 0: time every stage with CUDA events on the ctx stream and count the

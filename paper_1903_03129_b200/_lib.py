@@ -33,6 +33,7 @@ class NetDesc(C.Structure):
         ("lr", dbl), ("beta1", dbl), ("beta2", dbl), ("eps", dbl), ("seed", u64),
         ("w1t", vp), ("m1t", vp), ("v1t", vp), ("b1", vp), ("mb1", vp), ("vb1", vp), ("steps1", vp),
         ("w2", vp), ("m2", vp), ("v2", vp), ("b2", vp), ("mb2", vp), ("vb2", vp), ("steps2", vp),
+        ("shard_rank", i64), ("shard_count", i64),
     ]
 
 
@@ -68,6 +69,12 @@ _SIGS = {
     "slide_profile": [vp, i64],
     "slide_profile_read": [vp, vp, vp],
     "slide_launch_count": [vp],
+    "slide_shard_hash_rows": [vp, vp],
+    "slide_shard_forward": [vp, C.POINTER(Batch), i64, vp],
+    "slide_shard_softmax_sum": [vp, vp, vp],
+    "slide_shard_softmax_finish": [vp, vp, vp, vp],
+    "slide_shard_hidden_grad": [vp, vp],
+    "slide_shard_update": [vp, vp],
     "slide_pcg64_seed": [vp, i64, vp],
     "slide_pcg64_permutation": [vp, i64, vp],
     "slide_pcg64_choice": [vp, i64, i64, vp],

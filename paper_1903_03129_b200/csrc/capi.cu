@@ -66,7 +66,10 @@ struct slide_ctx {
   // backward workspace
   GroupBy grow, gfeat;
   bool grow_pending = false;  // grow holds a forward's grouping not yet cleared
-  bool use_rows_dh = false;
+  // output-layer sharding: rank g of G owns ids with id % G == g
+  int g = 0, G = 1;
+  int64_t n_local = 0;
+  DBuf cnt_all;  // per-slot global active-set size (sharded statistics)
   // CUDA-graph step (slide_graph_step): static shapes + context-owned batch
   struct {
     bool on = false;
@@ -225,10 +228,15 @@ int slide_create(const slide_net_desc* desc, void* stream, slide_ctx** out) {
       SLIDE_CHECK(d.key_bits >= 1 && d.key_bits <= 32, kNotSupported, "device keys are at most 32 bits");
       SLIDE_CHECK(d.l >= 1 && d.l <= 64, kNotSupported, "at most 64 tables on the device path");
     }
+    const int64_t G = d.shard_count < 1 ? 1 : d.shard_count;
+    SLIDE_CHECK(d.shard_rank >= 0 && d.shard_rank < G, kValueError, "shard_rank must lie in [0, shard_count)");
     slide_ctx* c = new slide_ctx();
     c->d = d;
     c->s = (cudaStream_t)stream;
     c->hp = (int)d.hidden_pad;
+    c->g = (int)d.shard_rank;
+    c->G = (int)G;
+    c->n_local = (d.n_out - d.shard_rank + G - 1) / G;
     try {
       if (d.family == 1) {
         size_t n = (size_t)d.k * d.l * d.sh_c;
@@ -262,7 +270,7 @@ int slide_destroy(slide_ctx* c) {
     for (DBuf* b : {&c->sh_packed, &c->sh_packed_t, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->qkeys, &c->order,
                     &c->states, &c->act, &c->cnt, &c->empty, &c->offs, &c->prow, &c->pslot, &c->plab, &c->z,
                     &c->prob, &c->delta, &c->loss, &c->dh, &c->fb_ids, &c->fb_scratch, &c->fb_bitmap, &c->xslot,
-                    &c->tc, &c->bc, &c->counters, &c->partial, &c->bias_table})
+                    &c->tc, &c->bc, &c->counters, &c->partial, &c->bias_table, &c->cnt_all})
       b->release();
     c->grow.release();
     c->gfeat.release();
@@ -317,6 +325,7 @@ static void build_from_keys(slide_ctx* c, const uint32_t* keys, int64_t n, uint6
 int slide_rebuild_tables(slide_ctx* c, uint64_t* mt_state) {
   return guarded([&] {
     SLIDE_CHECK(c->d.family != 0, kValueError, "layer has no LSH tables");
+    SLIDE_CHECK(c->G == 1, kValueError, "sharded contexts rebuild from all-gathered keys (slide_shard_hash_rows)");
     const int64_t n = c->d.n_out;
     uint32_t* keys = c->rowkeys.ensure<uint32_t>((size_t)n * c->d.l);
     c->timer.mark(c->s, kStStart);
@@ -520,6 +529,9 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
       SLIDE_CUDA(cudaMemcpyAsync(bt->rng_states, states, (size_t)b * 48, cudaMemcpyDeviceToDevice, s));
     c->timer.mark(s, kStFallback);
   }
+  // sharded: every rank selected the global active sets; keep the owned ids
+  if (c->G > 1)
+    launch_own_filter(b, act, cap_max, c->g, c->G, cnt, c->cnt_all.ensure<int32_t>(b), s);
   // pair count stays on the device (offs[b]); buffers are sized by the bound
   int32_t* offs = c->offs.ensure<int32_t>(b + 1);
   launch_offsets(b, cnt, offs, s);
@@ -527,7 +539,7 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   int32_t* prow = c->prow.ensure<int32_t>(P_max);
   int32_t* pslot = c->pslot.ensure<int32_t>(P_max);
   uint8_t* plab = c->plab.ensure<uint8_t>(P_max);
-  launch_pairs(b, act, cap_max, offs, prow, pslot, plab, s);
+  launch_pairs(b, act, cap_max, offs, c->G, prow, pslot, plab, s);
   c->timer.mark(s, kStCompact);
   float* z = c->z.ensure<float>(P_max);
   float* prob = c->prob.ensure<float>(P_max);
@@ -537,14 +549,15 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   // logits, hidden gradient and W2 Adam all walk this structure
   GroupBy& gr = c->grow;
   if (c->grow_pending) gr.clear(s);
-  gr.prepare(d.n_out, b, P_max);
+  gr.prepare(c->n_local, b, P_max);
   gr.run(prow, pslot, offs + b, 0, P_max, s);
   c->grow_pending = true;
   c->timer.mark(s, kStGroupRows);
   launch_logits_rows(hp, b, gr.n_uniq.as<int32_t>(), gr.u_max, gr.uniq.as<int32_t>(), gr.seg_off.as<int32_t>(),
                      gr.seg_cnt.as<int32_t>(), gr.order.as<int32_t>(), pslot, d.w2, d.b2, h, z, s);
   c->timer.mark(s, kStLogits);
-  launch_softmax(b, offs, plab, bt->y_ptr, z, prob, delta, loss, s);
+  // sharded: the softmax is completed by the slide_shard_softmax_* stages
+  if (c->G == 1) launch_softmax(b, offs, plab, bt->y_ptr, z, prob, delta, loss, s);
   c->timer.mark(s, kStSoftmax);
   c->have_forward = true;
   c->last_b = b;
@@ -559,25 +572,22 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   if (n_pairs) *n_pairs = host_pairs(c);
 }
 
-static void backward_impl(slide_ctx* c, int64_t update) {
+// ext_dh: the hidden gradient already computed (sharded step: all-reduced
+// partials); otherwise it is computed here from this context's W2.
+static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nullptr) {
   SLIDE_CHECK(c->have_forward, kValueError, "backward needs a forward first");
   const slide_net_desc& d = c->d;
   const int b = c->last_b, hp = c->hp;
   const int64_t P_max = c->last_Pmax;
   cudaStream_t s = c->s;
-  float* dh = c->dh.ensure<float>((size_t)b * hp);
   GroupBy& gr = c->grow;
-  const int parts = kSms;
-  float* partial = c->partial.ensure<float>((size_t)parts * b * hp);
-  // the row-major variant is kept for the tiled rewrite; the sample-major
-  // kernel is faster today (latency-bound bitmask walk)
-  if (!c->use_rows_dh ||
-      !launch_hidden_grad_rows(hp, b, gr.n_uniq.as<int32_t>(), gr.uniq.as<int32_t>(), gr.seg_off.as<int32_t>(),
-                               gr.mask.as<uint32_t>(), gr.wpk, gr.order.as<int32_t>(), c->offs.as<int32_t>() + b,
-                               c->delta.as<float>(), d.w2, c->h.as<float>(), partial, parts, dh, s))
+  const float* dh = ext_dh;
+  if (!dh) {
+    float* out = c->dh.ensure<float>((size_t)b * hp);
     launch_hidden_grad(hp, b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->delta.as<float>(), d.w2,
-                       c->h.as<float>(), dh,
-                       c->partial.ensure<float>((size_t)std::max(parts, hidden_grad_slices(b)) * b * hp), s);
+                       c->h.as<float>(), out, c->partial.ensure<float>((size_t)hidden_grad_slices(b) * b * hp), s);
+    dh = out;
+  }
   c->timer.mark(s, kStHiddenGrad);
   if (!update) return;
   const AdamParams ap = adam_of(c);
@@ -637,6 +647,7 @@ int slide_train_batch(slide_ctx* c, const slide_batch* bt, int64_t iteration, in
     const int64_t B = bt->batch;
     SLIDE_CHECK(B >= 1, kValueError, "batch is empty");
     SLIDE_CHECK(sub_batch >= 1, kValueError, "sub_batch must be >= 1");
+    SLIDE_CHECK(c->G == 1, kValueError, "sharded contexts step through slide_shard_*");
     if (c->pinned_n < B) {
       if (c->pinned_loss) cudaFreeHost(c->pinned_loss);
       if (c->pinned_cnt) cudaFreeHost(c->pinned_cnt);
@@ -681,6 +692,7 @@ int slide_graph_step(slide_ctx* c, const slide_batch* bt, int64_t iteration, dou
     const int64_t B = bt->batch;
     SLIDE_CHECK(B >= 1 && B <= 1024, kValueError, "batch must hold 1..1024 slots");
     SLIDE_CHECK(!bt->forced_ptr && !bt->rng_states, kValueError, "graph steps take plain training batches");
+    SLIDE_CHECK(c->G == 1, kValueError, "sharded contexts step through slide_shard_*");
     const int64_t x0 = bt->x_ptr_host[0], nnz = bt->x_ptr_host[B] - x0;
     const int64_t y0 = bt->y_ptr_host[0], nlab = bt->y_ptr_host[B] - y0;
     int64_t max_lab = 0;
@@ -837,6 +849,7 @@ int slide_read(slide_ctx* c, int64_t what, void* dst, int64_t max_bytes, int64_t
       case 9: src = c->empty.p; n = b * 4; break;
       case 10: src = c->states.p; n = b * 48; break;
       case 11: src = c->z.p; n = P * 4; break;
+      case 12: src = c->G > 1 ? c->cnt_all.p : c->cnt.p; n = b * 4; break;
       default: throw Error(kValueError, "unknown stage");
     }
     SLIDE_CHECK(src != nullptr || n == 0, kValueError, "stage not computed");
@@ -845,6 +858,54 @@ int slide_read(slide_ctx* c, int64_t what, void* dst, int64_t max_bytes, int64_t
     SLIDE_CUDA(cudaStreamSynchronize(c->s));
     if (bytes) *bytes = n;
   });
+}
+
+// ------------------------------------------------------------- sharded step
+int slide_shard_hash_rows(slide_ctx* c, uint32_t* keys) {
+  return guarded([&] {
+    SLIDE_CHECK(c->d.family != 0, kValueError, "layer has no LSH tables");
+    c->timer.mark(c->s, kStStart);
+    hash_rows(c, c->d.w2, c->n_local, keys);
+    c->timer.mark(c->s, kStRebuildHash);
+  });
+}
+
+int slide_shard_forward(slide_ctx* c, const slide_batch* bt, int64_t iteration, float* max_out) {
+  return guarded([&] {
+    SLIDE_CHECK(c->G > 1, kValueError, "slide_shard_* needs a sharded context");
+    forward_impl(c, bt, iteration, 0, nullptr);
+    launch_softmax_max(c->last_b, c->offs.as<int32_t>(), c->z.as<float>(), max_out, c->s);
+  });
+}
+
+int slide_shard_softmax_sum(slide_ctx* c, const float* gmax, float* sum_out) {
+  return guarded([&] {
+    SLIDE_CHECK(c->have_forward, kValueError, "no forward");
+    launch_softmax_sum(c->last_b, c->offs.as<int32_t>(), c->z.as<float>(), gmax, sum_out, c->s);
+  });
+}
+
+int slide_shard_softmax_finish(slide_ctx* c, const float* gmax, const float* gsum, double* loss_out) {
+  return guarded([&] {
+    SLIDE_CHECK(c->have_forward, kValueError, "no forward");
+    const int b = c->last_b;
+    launch_softmax_finish(b, c->offs.as<int32_t>(), c->plab.as<uint8_t>(), c->last_yptr, c->z.as<float>(), gmax,
+                          gsum, c->prob.as<float>(), c->delta.as<float>(), loss_out, c->s);
+  });
+}
+
+int slide_shard_hidden_grad(slide_ctx* c, float* dh_out) {
+  return guarded([&] {
+    SLIDE_CHECK(c->have_forward, kValueError, "no forward");
+    const int b = c->last_b, hp = c->hp;
+    // unmasked partial (h = null): masking commutes with the all-reduce
+    launch_hidden_grad(hp, b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->delta.as<float>(), c->d.w2, nullptr,
+                       dh_out, c->partial.ensure<float>((size_t)hidden_grad_slices(b) * b * hp), c->s);
+  });
+}
+
+int slide_shard_update(slide_ctx* c, const float* dh) {
+  return guarded([&] { backward_impl(c, 1, dh); });
 }
 
 int slide_launch_count(uint64_t* out) {

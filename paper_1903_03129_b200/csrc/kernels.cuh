@@ -50,8 +50,16 @@ void launch_explicit_active(int b, int64_t n, const int32_t* fptr, const int32_t
                             const int32_t* y_idx, int64_t cap_max, int32_t* act, int32_t* cnt, int32_t* empty,
                             cudaStream_t s);
 void launch_offsets(int b, const int32_t* cnt, int32_t* offs, cudaStream_t s);
-void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* offs, int32_t* prow, int32_t* pslot,
-                  uint8_t* plab, cudaStream_t s);
+void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* offs, int shard_count, int32_t* prow,
+                  int32_t* pslot, uint8_t* plab, cudaStream_t s);
+void launch_own_filter(int b, int32_t* act, int64_t cap_max, int g, int G, int32_t* cnt, int32_t* cnt_all,
+                       cudaStream_t s);
+// sharded softmax phases (per sample over the owned pairs)
+void launch_softmax_max(int b, const int32_t* offs, const float* z, float* out, cudaStream_t s);
+void launch_softmax_sum(int b, const int32_t* offs, const float* z, const float* gmax, float* out, cudaStream_t s);
+void launch_softmax_finish(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
+                           const float* gmax, const float* gsum, float* prob, float* delta, double* loss_part,
+                           cudaStream_t s);
 
 // Stable (key, slot) group-by with device-side sizes (group.cu).
 struct GroupBy {

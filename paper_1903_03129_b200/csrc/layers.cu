@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(256) hidden_grad_kernel(int hp, int b, int sli
 #pragma unroll
     for (int w = 1; w < 8; ++w) sum += red[w][c];
     const int64_t q = (int64_t)i * hp + c;
-    if (slices == 1) out[q] = h[q] > 0.f ? sum : 0.f;
+    if (slices == 1) out[q] = (h == nullptr || h[q] > 0.f) ? sum : 0.f;  // h == null: unmasked partial
     else out[(int64_t)sl * b * hp + q] = sum;
   }
 }
@@ -483,7 +483,7 @@ __global__ void slice_sum_kernel(int64_t n, int slices, const float* __restrict_
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
     float s = part[q];
     for (int sl = 1; sl < slices; ++sl) s += part[(int64_t)sl * n + q];
-    dh[q] = h[q] > 0.f ? s : 0.f;
+    dh[q] = (h == nullptr || h[q] > 0.f) ? s : 0.f;
   }
 }
 
@@ -972,6 +972,85 @@ void launch_hidden_prep_bias(int hp, int b, const AdamParams& ap, const float* h
   if (b <= 0) return;
   hidden_prep_bias_kernel<<<(int)ceil_div((int64_t)hp * 32, 256), 256, 0, s>>>(hp, b, ap, h, dh, steps1, tc, bc, b1,
                                                                              mb1, vb1);
+  SLIDE_LAUNCH_CHECK();
+}
+
+}  // namespace slide
+
+namespace slide {
+
+// ---------------------------------------------- sharded softmax (3 phases)
+// The active set of a sample is split across ranks; the max and the sum of
+// exponentials are combined by the caller's all-reduces between phases.
+__global__ void __launch_bounds__(1024) softmax_max_kernel(const int32_t* __restrict__ offs, const float* __restrict__ z,
+                                                          float* __restrict__ out) {
+  using RF = cub::BlockReduce<float, 1024>;
+  __shared__ typename RF::TempStorage tmp;
+  const int i = blockIdx.x;
+  const int o = offs[i], n = offs[i + 1] - o;
+  float mx = -INFINITY;
+  for (int k = threadIdx.x; k < n; k += 1024) mx = fmaxf(mx, z[o + k]);
+  mx = RF(tmp).Reduce(mx, cub::Max());
+  if (threadIdx.x == 0) out[i] = mx;
+}
+
+__global__ void __launch_bounds__(1024) softmax_sum_kernel(const int32_t* __restrict__ offs, const float* __restrict__ z,
+                                                          const float* __restrict__ gmax, float* __restrict__ out) {
+  using RF = cub::BlockReduce<float, 1024>;
+  __shared__ typename RF::TempStorage tmp;
+  const int i = blockIdx.x;
+  const int o = offs[i], n = offs[i + 1] - o;
+  const float mx = gmax[i];
+  float se = 0.f;
+  for (int k = threadIdx.x; k < n; k += 1024) se += expf(z[o + k] - mx);
+  se = RF(tmp).Sum(se);
+  if (threadIdx.x == 0) out[i] = se;
+}
+
+__global__ void __launch_bounds__(1024) softmax_finish_kernel(const int32_t* __restrict__ offs,
+                                                             const uint8_t* __restrict__ plab,
+                                                             const int32_t* __restrict__ y_ptr,
+                                                             const float* __restrict__ z,
+                                                             const float* __restrict__ gmax,
+                                                             const float* __restrict__ gsum, float* __restrict__ prob,
+                                                             float* __restrict__ delta, double* __restrict__ loss) {
+  using RD = cub::BlockReduce<double, 1024>;
+  __shared__ typename RD::TempStorage tmp;
+  const int i = blockIdx.x;
+  const int o = offs[i], n = offs[i + 1] - o;
+  const int ny = y_ptr[i + 1] - y_ptr[i];
+  const float mx = gmax[i], se = gsum[i], lse = logf(se);
+  const float inv_ny = ny > 0 ? 1.f / (float)ny : 0.f;
+  double lsum = 0.0;
+  for (int k = threadIdx.x; k < n; k += 1024) {
+    const float zz = z[o + k] - mx;
+    const float p = expf(zz) / se;
+    const int lab = plab[o + k];
+    prob[o + k] = p;
+    delta[o + k] = lab ? p - inv_ny : p;
+    if (lab) {
+      const double nl = -((double)zz - (double)lse);
+      lsum += nl < 690.7755278982137 ? nl : 690.7755278982137;
+    }
+  }
+  lsum = RD(tmp).Sum(lsum);
+  if (threadIdx.x == 0) loss[i] = lsum;  // sum over this rank's labels; / |Y| after the all-reduce
+}
+
+void launch_softmax_max(int b, const int32_t* offs, const float* z, float* out, cudaStream_t s) {
+  softmax_max_kernel<<<b, 1024, 0, s>>>(offs, z, out);
+  SLIDE_LAUNCH_CHECK();
+}
+
+void launch_softmax_sum(int b, const int32_t* offs, const float* z, const float* gmax, float* out, cudaStream_t s) {
+  softmax_sum_kernel<<<b, 1024, 0, s>>>(offs, z, gmax, out);
+  SLIDE_LAUNCH_CHECK();
+}
+
+void launch_softmax_finish(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
+                           const float* gmax, const float* gsum, float* prob, float* delta, double* loss_part,
+                           cudaStream_t s) {
+  softmax_finish_kernel<<<b, 1024, 0, s>>>(offs, plab, y_ptr, z, gmax, gsum, prob, delta, loss_part);
   SLIDE_LAUNCH_CHECK();
 }
 

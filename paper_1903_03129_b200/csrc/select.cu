@@ -484,22 +484,61 @@ void launch_offsets(int b, const int32_t* cnt, int32_t* offs, cudaStream_t s) {
   SLIDE_LAUNCH_CHECK();
 }
 
+// Pair rows are local W2 rows: id / shard_count (identity when unsharded).
 __global__ void pairs_kernel(const int32_t* __restrict__ act, int64_t cap_max, const int32_t* __restrict__ offs,
-                             int32_t* __restrict__ prow, int32_t* __restrict__ pslot, uint8_t* __restrict__ plab) {
+                             int shard_count, int32_t* __restrict__ prow, int32_t* __restrict__ pslot,
+                             uint8_t* __restrict__ plab) {
   const int i = blockIdx.x;
   const int o = offs[i], n = offs[i + 1] - o;
   const int32_t* src = act + (int64_t)i * cap_max;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     uint32_t v = (uint32_t)src[k];
-    prow[o + k] = (int32_t)(v & 0x7fffffffu);
+    prow[o + k] = (int32_t)((v & 0x7fffffffu) / (uint32_t)shard_count);
     pslot[o + k] = i;
     plab[o + k] = (uint8_t)(v >> 31);
   }
 }
 
-void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* offs, int32_t* prow, int32_t* pslot,
-                  uint8_t* plab, cudaStream_t s) {
-  pairs_kernel<<<b, 256, 0, s>>>(act, cap_max, offs, prow, pslot, plab);
+void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* offs, int shard_count, int32_t* prow,
+                  int32_t* pslot, uint8_t* plab, cudaStream_t s) {
+  pairs_kernel<<<b, 256, 0, s>>>(act, cap_max, offs, shard_count, prow, pslot, plab);
+  SLIDE_LAUNCH_CHECK();
+}
+
+// Sharded step: keep only the ids this rank owns (id % G == g), in order,
+// in place; cnt_all keeps the global active-set size for the statistics.
+constexpr int kOwnThreads = 1024;
+constexpr int kOwnPer = 64;  // cap_max <= 65536
+
+__global__ void __launch_bounds__(kOwnThreads) own_filter_kernel(int32_t* __restrict__ act, int64_t cap_max,
+                                                                 int g, int G, int32_t* __restrict__ cnt,
+                                                                 int32_t* __restrict__ cnt_all) {
+  using Scan = cub::BlockScan<int, kOwnThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  const int i = blockIdx.x;
+  const int n = cnt[i];
+  int32_t* a = act + (int64_t)i * cap_max;
+  const int ch = (n + kOwnThreads - 1) / kOwnThreads;
+  const int k0 = min((int)threadIdx.x * ch, n), k1 = min(k0 + ch, n);
+  int32_t mine[kOwnPer];
+  int m = 0;
+  for (int k = k0; k < k1; ++k) {
+    const int32_t v = a[k];
+    if ((int)((uint32_t)(v & 0x7fffffff) % (uint32_t)G) == g) mine[m++] = v;
+  }
+  int ofs, total;
+  Scan(tmp).ExclusiveSum(m, ofs, total);  // block-wide barrier: every read is done
+  for (int q = 0; q < m; ++q) a[ofs + q] = mine[q];
+  if (threadIdx.x == 0) {
+    cnt_all[i] = n;
+    cnt[i] = total;
+  }
+}
+
+void launch_own_filter(int b, int32_t* act, int64_t cap_max, int g, int G, int32_t* cnt, int32_t* cnt_all,
+                       cudaStream_t s) {
+  SLIDE_CHECK(cap_max <= (int64_t)kOwnThreads * kOwnPer, kNotSupported, "active sets above 65536 ids per sample");
+  own_filter_kernel<<<b, kOwnThreads, 0, s>>>(act, cap_max, g, G, cnt, cnt_all);
   SLIDE_LAUNCH_CHECK();
 }
 

@@ -309,7 +309,7 @@ class SlideNetwork:
     """Input -> ReLU hidden (dense) -> LSH-sampled softmax output, on the device."""
 
     def __init__(self, input_dim: int, widths, cfg: TrainConfig, lsh_layers: dict | None = None,
-                 static_layers: dict | None = None):
+                 static_layers: dict | None = None, *, shard: tuple | None = None, group=None):
         import torch
 
         from . import _device
@@ -330,8 +330,14 @@ class SlideNetwork:
         self.input_dim = input_dim
         self.hidden, self.n_out = widths
         self.access_log = None
+        # output-layer column shard: rank g of G owns ids % G == g
+        self.shard_rank, self.shard_count = shard if shard is not None else (0, 1)
+        self.group = group
         dev = _device.device()
         H, N, D = self.hidden, self.n_out, input_dim
+        g, G = self.shard_rank, self.shard_count
+        n_local = (N - g + G - 1) // G
+        self.n_local = n_local
         hp = _device.round_up(H, 128)
         self.hidden_pad = hp
         f32 = dict(dtype=torch.float32, device=dev)
@@ -350,19 +356,22 @@ class SlideNetwork:
         self.mb1 = torch.zeros(hp, **f32)
         self.vb1 = torch.zeros(hp, **f32)
         self.steps1 = torch.zeros(hp, dtype=torch.int64, device=dev)
-        self.w2 = torch.zeros((N, hp), **f32)
+        self.w2 = torch.zeros((n_local, hp), **f32)
         bound = 1.0 / np.sqrt(H)
-        rows = max(1, (1 << 22) // H)
-        for r0 in range(0, N, rows):
+        rows = max(G, ((1 << 22) // H) // G * G)
+        for r0 in range(0, N, rows):  # the whole stream is drawn; a shard keeps its rows
             r1 = min(N, r0 + rows)
             chunk = rng.uniform(-bound, bound, size=(r1 - r0, H)).astype(np.float32)
-            self.w2[r0:r1, :H] = torch.from_numpy(chunk).to(dev)
-        self.m2 = torch.zeros((N, hp), **f32)
-        self.v2 = torch.zeros((N, hp), **f32)
-        self.b2 = torch.zeros(N, **f32)
-        self.mb2 = torch.zeros(N, **f32)
-        self.vb2 = torch.zeros(N, **f32)
-        self.steps2 = torch.zeros(N, dtype=torch.int64, device=dev)
+            if G > 1:
+                chunk = chunk[(g - r0) % G :: G]
+            l0 = (r0 + G - 1 - g) // G if r0 > g else 0
+            self.w2[l0 : l0 + chunk.shape[0], :H] = torch.from_numpy(np.ascontiguousarray(chunk)).to(dev)
+        self.m2 = torch.zeros((n_local, hp), **f32)
+        self.v2 = torch.zeros((n_local, hp), **f32)
+        self.b2 = torch.zeros(n_local, **f32)
+        self.mb2 = torch.zeros(n_local, **f32)
+        self.vb2 = torch.zeros(n_local, **f32)
+        self.steps2 = torch.zeros(n_local, dtype=torch.int64, device=dev)
         self.layers = [Layer(self, 0, H, D, "relu"), Layer(self, 1, N, H, "softmax")]
         # -- device context
         desc = _lib.NetDesc()
@@ -373,6 +382,7 @@ class SlideNetwork:
         for name in ("w1t", "m1t", "v1t", "b1", "mb1", "vb1", "steps1", "w2", "m2", "v2", "b2", "mb2", "vb2",
                      "steps2"):
             setattr(desc, name, getattr(self, name).data_ptr())
+        desc.shard_rank, desc.shard_count = g, G
         self._keep = []
         spec = lsh_layers.get(1)
         family = None
@@ -410,7 +420,13 @@ class SlideNetwork:
     def _rebuild_tables(self):
         lsh = self.layers[1].lsh
         st = _lib.mt_state_from_random(lsh._rng)
-        _lib.call("slide_rebuild_tables", self._ctx, st.ctypes.data)
+        if self.shard_count > 1:
+            from .sharded import gather_row_keys
+
+            keys = gather_row_keys(self, self.group)
+            _lib.call("slide_build_tables_from_keys", self._ctx, keys.data_ptr(), self.n_out, st.ctypes.data)
+        else:
+            _lib.call("slide_rebuild_tables", self._ctx, st.ctypes.data)
         _lib.mt_state_to_random(st, lsh._rng)
         lsh.n_items = self.n_out
         lsh._views = None
@@ -500,7 +516,14 @@ class SlideNetwork:
         B = csr.batch
         if B < 1 or B > self.cfg.batch_size:
             raise ValueError(f"batch of {B} outside 1..{self.cfg.batch_size}")
-        loss, active = self._step(csr, iteration, 1 if schedule == "sequential" else B)
+        if self.shard_count > 1:
+            if schedule != "snapshot":
+                raise NotImplementedError("the sharded output layer runs the snapshot schedule")
+            from .sharded import GpuShardBackend, sharded_step
+
+            loss, active = sharded_step(GpuShardBackend(self), csr, iteration, self.group)
+        else:
+            loss, active = self._step(csr, iteration, 1 if schedule == "sequential" else B)
         return self._barrier(iteration, loss, active)
 
     #: snapshot steps replay one captured CUDA graph per batch shape

@@ -1,0 +1,96 @@
+"""Sharded output layer on the device: 2 ranks (processes) on one GPU with
+host-mediated gloo collectives (no kernel waits on another rank), checked
+against the unsharded device step from the same initial state."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+D, H, N, B = 300, 128, 997, 16
+
+
+def _setup(family):
+    from paper_1903_03129_b200 import LshLayerConfig, SamplerConfig, TrainConfig
+
+    cfg = TrainConfig(batch_size=B, seed=5, learning_rate=1e-2, n0=2)
+    if family == "simhash":
+        spec = LshLayerConfig("simhash", k=4, l=8, capacity=16, sampler=SamplerConfig("vanilla", beta=40))
+    else:
+        spec = LshLayerConfig("dwta", k=3, l=6, capacity=8, policy="reservoir", wta_bin_size=8,
+                              sampler=SamplerConfig("vanilla", beta=12))
+    return cfg, spec
+
+
+def _csrs():
+    from paper_1903_03129_b200.data import CorpusSpec, synthetic_corpus
+    from paper_1903_03129_b200.network import HostCsr
+
+    corpus = synthetic_corpus(CorpusSpec(D, N, ("uniform", 3, 20), 1.1, ("uniform", 1, 4), 1.1, True), 3 * B, seed=9)
+    out = []
+    for s in range(3):
+        sub = corpus.subset(np.arange(s * B, (s + 1) * B))
+        out.append(HostCsr(sub.x_ptr.astype(np.int32), sub.x_idx, sub.x_val, sub.y_ptr.astype(np.int32), sub.y_idx))
+    return out
+
+
+def _worker(rank, world, port, family, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1903_03129_b200 import SlideNetwork, sharded
+
+        cfg, spec = _setup(family)
+        net = SlideNetwork(D, [H, N], cfg, lsh_layers={1: spec}, shard=(rank, world))
+        losses, fracs = [], []
+        for it, csr in enumerate(_csrs(), start=1):
+            st = net.train_batch_csr(csr, it, schedule="snapshot")
+            losses.append(st.loss)
+            fracs.append(st.active_fraction[1])
+        w2 = sharded.all_gather_rows(net.w2.cpu(), N).numpy()
+        v2 = sharded.all_gather_rows(net.v2.cpu(), N).numpy()
+        q.put((rank, losses, fracs, net.w1t.cpu().numpy(), w2, v2))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("family", ["simhash", "dwta"])
+def test_two_shards_match_one_gpu(family):
+    from paper_1903_03129_b200 import SlideNetwork
+
+    cfg, spec = _setup(family)
+    ref = SlideNetwork(D, [H, N], cfg, lsh_layers={1: spec})
+    ref.use_graphs = False
+    want_l, want_f = [], []
+    for it, csr in enumerate(_csrs(), start=1):
+        st = ref.train_batch_csr(csr, it, schedule="snapshot")
+        want_l.append(st.loss)
+        want_f.append(st.active_fraction[1])
+    w1_ref, w2_ref = ref.w1t.cpu().numpy(), ref.w2.cpu().numpy()
+    del ref
+    torch.cuda.empty_cache()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, family, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, losses, fracs, w1t, w2, v2 in res:
+        np.testing.assert_allclose(losses, want_l, rtol=1e-5)
+        np.testing.assert_allclose(fracs, want_f, rtol=0, atol=0)  # identical active sets
+        np.testing.assert_allclose(w1t, w1_ref, rtol=1e-4, atol=1e-6)
+        np.testing.assert_allclose(w2, w2_ref[:, : w2.shape[1]], rtol=1e-4, atol=1e-6)
