@@ -20,9 +20,11 @@ chosen so that one rebuild falls inside them.
 * cpu_baseline: the CPU oracle (a numpy restatement of the reference path,
   kind "port") on a bounded sample of the same workload, 1 thread.
 
-N>1 (torchrun): independent replicas, one per GPU, each on its own data
-shard (weak scaling), max-over-ranks device time.  The column-sharded output
-layer of SURVEY 8(e) is not implemented yet.
+N>1 (torchrun): the output layer is column-sharded over the N GPUs (SURVEY
+8(e), paper_1903_03129_b200/sharded.py): every rank processes the same global
+batch, owns 1/N of the output rows, and the step all-reduces the softmax
+max / sum, the loss terms and the hidden gradient over NCCL (strong
+scaling); max-over-ranks device time.
 """
 
 from __future__ import annotations
@@ -115,13 +117,14 @@ class ClockSampler:
                 "samples": len(self.rows), "source": "nvml"}
 
 
-def make_net(w, torch):
+def make_net(w, torch, rank=0, world=1):
     from paper_1903_03129_b200 import LshLayerConfig, SamplerConfig, SlideNetwork, TrainConfig
 
     cfg = TrainConfig(batch_size=w.batch, learning_rate=w.lr, n0=w.n0, decay=w.decay, seed=0)
     spec = LshLayerConfig(w.family, k=w.k, l=w.l, capacity=w.cap, policy=w.policy, wta_bin_size=w.bin_size,
                           sampler=SamplerConfig(w.strategy, beta=w.beta))
-    return SlideNetwork(w.input_dim, [w.hidden, w.n_out], cfg, lsh_layers={1: spec})
+    shard = (rank, world) if world > 1 else None
+    return SlideNetwork(w.input_dim, [w.hidden, w.n_out], cfg, lsh_layers={1: spec}, shard=shard)
 
 
 def csr_batches(corpus, B, n):
@@ -180,9 +183,10 @@ def run_ours(args, rank, world):
     w = WORKLOADS[args.workload]
     K, W = args.steps, args.warmup
     n_batches = W + K
-    corpus = synthetic_corpus(w.corpus, n_batches * w.batch, seed=1000 + rank)
+    # every rank sees the same global batch: the output layer is sharded
+    corpus = synthetic_corpus(w.corpus, n_batches * w.batch, seed=1000)
     batches = csr_batches(corpus, w.batch, n_batches)
-    net = make_net(w, torch)
+    net = make_net(w, torch, rank, world)
     sub = 1 if args.schedule == "sequential" else w.batch
     # device-resident inputs for `value`
     dev_batches = []
@@ -195,7 +199,13 @@ def run_ours(args, rank, world):
     act_buf = np.empty(w.batch, np.int64)
 
     def step_dev(it):
-        bt, _, _ = dev_batches[it - 1]
+        bt, keep, hb = dev_batches[it - 1]
+        if world > 1:  # column-sharded output layer: stages + all-reduces
+            from paper_1903_03129_b200.sharded import GpuShardBackend, sharded_step
+
+            hb.dev = (bt, keep)
+            loss, act = sharded_step(GpuShardBackend(net), hb, it, None)
+            return net._barrier(it, loss, act)
         if sub == w.batch and net.use_graphs:  # the captured-graph snapshot step
             _lib.call("slide_graph_step", net._ctx, _lib.C.byref(bt), it, loss_buf.ctypes.data, act_buf.ctypes.data)
         else:
@@ -232,7 +242,8 @@ def run_ours(args, rank, world):
         t = torch.tensor([total_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    value = world * K * w.batch / (total_ms / 1e3)
+    # N > 1: the ranks share one global batch per step (sharded output layer)
+    value = K * w.batch / (total_ms / 1e3)
     # -- e2e: public API from pinned host CSR, fresh net state continues
     e2e = None
     if not args.no_e2e:
@@ -256,14 +267,21 @@ def run_ours(args, rank, world):
             t = torch.tensor([e_total], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_total = float(t.item())
-        e2e = {"value": world * K * w.batch / (e_total / 1e3), "unit": "samples/s",
+        e2e = {"value": K * w.batch / (e_total / 1e3), "unit": "samples/s",
                "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K)}
     # -- profiled pass: per-stage event times + realised sets
     _lib.call("slide_profile", net._ctx, 1)
     it0 = W + 2 * K + 1
     for k in range(K):
         step_dev_it = it0 + k
-        bt, _, _ = dev_batches[(W + k) % n_batches]
+        bt, keep, hb = dev_batches[(W + k) % n_batches]
+        if world > 1:
+            from paper_1903_03129_b200.sharded import GpuShardBackend, sharded_step
+
+            hb.dev = (bt, keep)
+            loss, act = sharded_step(GpuShardBackend(net), hb, step_dev_it, None)
+            net._barrier(step_dev_it, loss, act)
+            continue
         _lib.call("slide_train_batch", net._ctx, _lib.C.byref(bt), step_dev_it, sub, loss_buf.ctypes.data,
                   act_buf.ctypes.data)
         net._barrier(step_dev_it, loss_buf, act_buf)
@@ -288,12 +306,14 @@ def run_ours(args, rank, world):
     out = {
         "metric": "train samples/sec (LSH-sparse fwd+bwd+Adam), % of HBM roofline, 1/2/4/8 GPU",
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (SURVEY 8(d) Zipf generator; Delicious-200K shape)",
         "config": {"workload": w.name, "input_dim": w.input_dim, "hidden": w.hidden, "n_out": w.n_out,
                    "batch": w.batch, "hash": f"{w.family} K={w.k} L={w.l} cap={w.cap} {w.policy}",
                    "sampler": f"{w.strategy} beta={w.beta}", "lr": w.lr, "rebuild": f"n0={w.n0} decay={w.decay}",
-                   "schedule": args.schedule, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "schedule": args.schedule,
+                   "parallelism": f"output layer column-sharded x{world} (NCCL all-reduces)" if world > 1 else "1 GPU",
                    "l2": "flushed between steps (256 MiB write, outside the events)"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,

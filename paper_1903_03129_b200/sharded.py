@@ -100,7 +100,8 @@ class GpuShardBackend:
         net = self.net
         if net.layers[1].lsh is not None:
             net.layers[1].lsh.sync_to_device()
-        bt, keep = net._upload(csr)
+        pre = getattr(csr, "dev", None)  # batch already resident on the device (bench)
+        bt, keep = pre if pre is not None else net._upload(csr)
         self.keep = (bt, keep)
         self.B = csr.batch
         mx = torch.empty(csr.batch, dtype=torch.float32, device=net.w2.device)
