@@ -570,6 +570,17 @@ __device__ __forceinline__ void adam_coord_h(bool on, float& w, float& m, float&
   w = on ? wn : w;
 }
 
+// as adam_coord_h with sqrt(c2) hoisted per pair: den = sqrt(v) sqrt(c2) + eps
+__device__ __forceinline__ void adam_coord_hs(bool on, float& w, float& m, float& v, float hc, float e1, float e2,
+                                              float c1, float s2, const AdamK& k) {
+  const float mn = fmaf(k.b1, m, e1 * hc);
+  const float vn = fmaf(k.b2, v, e2 * (hc * hc));
+  const float wn = fmaf(-(c1 * mn), rcp_approx(fmaf(sqrt_approx(vn), s2, k.eps)), w);
+  m = on ? mn : m;
+  v = on ? vn : v;
+  w = on ? wn : w;
+}
+
 // Stage the batch's activations (b x hp floats) in shared memory: 4
 // independent 16-byte loads in flight per thread.
 __device__ __forceinline__ void stage_rows(float* dst, const float* src, int n_floats) {
@@ -588,7 +599,7 @@ __device__ __forceinline__ void stage_rows(float* dst, const float* src, int n_f
   for (; q < n4; q += blockDim.x) d4[q] = __ldg(s4 + q);
 }
 
-template <int NV, bool SMEM_H>
+template <int NV, bool SMEM_H, bool COUNT>
 __global__ void __launch_bounds__(256) adam_rows_kernel(int hp, int b, AdamParams ap,
                                                         const int32_t* __restrict__ n_uniq,
                                                         const int32_t* __restrict__ uniq,
@@ -603,12 +614,16 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(int hp, int b, AdamParam
                                                         int64_t* __restrict__ steps2,
                                                         unsigned long long* __restrict__ touched) {
   extern __shared__ __align__(16) float hs[];
+  // per-warp broadcast of the current chunk's pair scalars:
+  // (h row offset, e1, e2, c1) and sqrt(c2)
+  __shared__ float4 pq[8][32];
+  __shared__ float ps2[8][32];
   if (SMEM_H) {
     stage_rows(hs, h, b * hp);
     __syncthreads();
   }
   const float* hsrc = SMEM_H ? hs : h;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nu = *n_uniq;
@@ -630,28 +645,53 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(int hp, int b, AdamParam
     float bb = b2[r], mb = mb2[r], vb = vb2[r];
     const int64_t st = steps2[r];
     for (int c0 = 0; c0 < len; c0 += 32) {
-      // lane j holds the j-th pair of this chunk: its sample, e1, e2, c1, c2
+      // lane j holds the j-th pair of this chunk
       const int j = c0 + lane;
+      const bool valid = j < len;
       int slot_l = 0;
-      float e1_l = 0.f, e2_l = 0.f, d_l = 0.f;
+      float d_l = 0.f;
       float2 bc_l = make_float2(0.f, 1.f);
-      if (j < len) {
+      if (valid) {
         const int p = sorted_pairs[s0 + j];
         slot_l = pslot[p];
         d_l = delta[p];
-        e1_l = ak.omb1 * d_l;
-        e2_l = ak.omb2 * d_l * d_l;
         bc_l = bias_corr(ap, st + j + 1);
+      }
+      const float e1_l = ak.omb1 * d_l, e2_l = ak.omb2 * d_l * d_l;
+      const float s2_l = sqrt_approx(bc_l.y);
+      __syncwarp();
+      pq[wid][lane] = make_float4(__int_as_float(slot_l * hp), e1_l, e2_l, bc_l.x);
+      ps2[wid][lane] = s2_l;
+      __syncwarp();
+      // Bias (gradient d, always moves): its moments are linear recurrences
+      // in the chunk's pairs -> two warp scans; the weight update does not
+      // feed back, so the chunk's bias steps are summed.
+      {
+        float a1 = valid ? ak.b1 : 1.f, x1 = e1_l, a2 = valid ? ak.b2 : 1.f, x2 = e2_l;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const float pa1 = __shfl_up_sync(0xffffffffu, a1, o), px1 = __shfl_up_sync(0xffffffffu, x1, o);
+          const float pa2 = __shfl_up_sync(0xffffffffu, a2, o), px2 = __shfl_up_sync(0xffffffffu, x2, o);
+          if (lane >= o) {
+            x1 = fmaf(a1, px1, x1);
+            a1 *= pa1;
+            x2 = fmaf(a2, px2, x2);
+            a2 *= pa2;
+          }
+        }
+        const float mj = fmaf(a1, mb, x1), vj = fmaf(a2, vb, x2);
+        float upd = valid ? (bc_l.x * mj) * rcp_approx(fmaf(sqrt_approx(vj), s2_l, ak.eps)) : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) upd += __shfl_xor_sync(0xffffffffu, upd, o);
+        bb -= upd;
+        mb = __shfl_sync(0xffffffffu, mj, 31);
+        vb = __shfl_sync(0xffffffffu, vj, 31);
       }
       const int nc = min(32, len - c0);
       for (int q2 = 0; q2 < nc; ++q2) {
-        const int slot = __shfl_sync(0xffffffffu, slot_l, q2);
-        const float e1 = __shfl_sync(0xffffffffu, e1_l, q2);
-        const float e2 = __shfl_sync(0xffffffffu, e2_l, q2);
-        const float d = __shfl_sync(0xffffffffu, d_l, q2);
-        const float c1 = __shfl_sync(0xffffffffu, bc_l.x, q2);
-        const float c2 = __shfl_sync(0xffffffffu, bc_l.y, q2);
-        const float* hr = hsrc + (int64_t)slot * hp + lane * 4;
+        const float4 P = pq[wid][q2];
+        const float s2 = ps2[wid][q2];
+        const float* hr = hsrc + __float_as_int(P.x) + lane * 4;
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
           const float4 hv = SMEM_H ? *reinterpret_cast<const float4*>(hr + q * 128) : ld4(hr + q * 128);
@@ -659,12 +699,10 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(int hp, int b, AdamParam
           for (int c = 0; c < 4; ++c) {
             const float hc = reinterpret_cast<const float*>(&hv)[c];
             const bool on = hc > 0.f;
-            adam_coord_h(on, comp(w[q], c), comp(m[q], c), comp(v[q], c), hc, e1, e2, c1, c2, ak);
-            tmask |= (on ? 1u : 0u) << (q * 4 + c);
+            adam_coord_hs(on, comp(w[q], c), comp(m[q], c), comp(v[q], c), hc, P.y, P.z, P.w, s2, ak);
+            if (COUNT) tmask |= (on ? 1u : 0u) << (q * 4 + c);
           }
         }
-        adam_coord_h(true, bb, mb, vb, 1.f, e1, e2, c1, c2, ak);  // bias: g = d
-        (void)d;
       }
     }
 #pragma unroll
@@ -679,7 +717,7 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(int hp, int b, AdamParam
       vb2[r] = vb;
       steps2[r] = st + len;
     }
-    if (touched) {
+    if (COUNT) {
       int tc = __popc(tmask);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) tc += __shfl_xor_sync(0xffffffffu, tc, o);
@@ -707,19 +745,33 @@ void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq
   const size_t smem = (size_t)b * hp * 4;
   if (smem <= 100 * 1024) {
     // persistent: each CTA stages h once, then walks rows grid-stride
-    const int per_sm = smem <= 72 * 1024 ? 3 : 2;
+    const int per_sm = smem <= 68 * 1024 ? 3 : 2;
     int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * per_sm);
-    SLIDE_NV_DISPATCH(hp, ({
-      SLIDE_CUDA(cudaFuncSetAttribute(adam_rows_kernel<NV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-      adam_rows_kernel<NV, true><<<grid, 256, smem, s>>>(hp, b, ap, n_uniq, uniq, seg_off, seg_cnt, sorted_pairs,
-                                                         pslot, delta, h, w2, m2, v2, b2, mb2, vb2, steps2, touched);
-    }));
+#define SLIDE_ADAM_ROWS(CNT)                                                                                  \
+  SLIDE_NV_DISPATCH(hp, ({                                                                                    \
+    SLIDE_CUDA(cudaFuncSetAttribute(adam_rows_kernel<NV, true, CNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                    (int)smem));                                                              \
+    adam_rows_kernel<NV, true, CNT><<<grid, 256, smem, s>>>(hp, b, ap, n_uniq, uniq, seg_off, seg_cnt,         \
+                                                            sorted_pairs, pslot, delta, h, w2, m2, v2, b2, mb2, \
+                                                            vb2, steps2, touched);                            \
+  }))
+    if (touched) {
+      SLIDE_ADAM_ROWS(true);
+    } else {
+      SLIDE_ADAM_ROWS(false);
+    }
+#undef SLIDE_ADAM_ROWS
   } else {
     int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * 16);
-    SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, false><<<grid, 256, 0, s>>>(
-                              hp, b, ap, n_uniq, uniq, seg_off, seg_cnt, sorted_pairs, pslot, delta, h, w2, m2, v2,
-                              b2, mb2, vb2, steps2, touched)));
+    if (touched) {
+      SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, false, true><<<grid, 256, 0, s>>>(
+                                hp, b, ap, n_uniq, uniq, seg_off, seg_cnt, sorted_pairs, pslot, delta, h, w2, m2, v2,
+                                b2, mb2, vb2, steps2, touched)));
+    } else {
+      SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, false, false><<<grid, 256, 0, s>>>(
+                                hp, b, ap, n_uniq, uniq, seg_off, seg_cnt, sorted_pairs, pslot, delta, h, w2, m2, v2,
+                                b2, mb2, vb2, steps2, touched)));
+    }
   }
   SLIDE_LAUNCH_CHECK();
 }

@@ -493,7 +493,8 @@ __global__ void pairs_kernel(const int32_t* __restrict__ act, int64_t cap_max, c
   const int32_t* src = act + (int64_t)i * cap_max;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     uint32_t v = (uint32_t)src[k];
-    prow[o + k] = (int32_t)((v & 0x7fffffffu) / (uint32_t)shard_count);
+    const uint32_t id = v & 0x7fffffffu;
+    prow[o + k] = (int32_t)(shard_count == 1 ? id : id / (uint32_t)shard_count);
     pslot[o + k] = i;
     plab[o + k] = (uint8_t)(v >> 31);
   }
@@ -501,7 +502,7 @@ __global__ void pairs_kernel(const int32_t* __restrict__ act, int64_t cap_max, c
 
 void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* offs, int shard_count, int32_t* prow,
                   int32_t* pslot, uint8_t* plab, cudaStream_t s) {
-  pairs_kernel<<<b, 256, 0, s>>>(act, cap_max, offs, shard_count, prow, pslot, plab);
+  pairs_kernel<<<b, 1024, 0, s>>>(act, cap_max, offs, shard_count, prow, pslot, plab);
   SLIDE_LAUNCH_CHECK();
 }
 
