@@ -63,10 +63,9 @@ void launch_softmax_finish(int b, const int32_t* offs, const uint8_t* plab, cons
 
 // Stable (key, slot) group-by with device-side sizes (group.cu).
 struct GroupBy {
-  DBuf bits, key_rank, woff, uniq, seg_cnt, seg_off, n_uniq, mask, order, temp;
-  int64_t K = 0, nwords = 0, u_max = 0, bits_words = 0, mask_words = 0;
+  DBuf bits, key_rank, uniq, seg_cnt, seg_off, n_uniq, mask, order, status, ctrs;
+  int64_t K = 0, nwords = 0, u_max = 0, bits_words = 0, mask_words = 0, tiles_bits = 0, tiles_seg = 0;
   int wpk = 1;
-  size_t temp_bytes = 0;
   void prepare(int64_t key_space, int64_t slots, int64_t items_max);
   // items q < n (n = *n_dev if given, else n_host), keys[q] / slots[q]
   void run(const int32_t* keys, const int32_t* slots, const int32_t* n_dev, int64_t n_host, int64_t n_max,
