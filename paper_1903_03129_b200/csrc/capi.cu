@@ -553,8 +553,7 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   gr.run(prow, pslot, offs + b, 0, P_max, s);
   c->grow_pending = true;
   c->timer.mark(s, kStGroupRows);
-  launch_logits_rows(hp, b, gr.n_uniq.as<int32_t>(), gr.u_max, gr.uniq.as<int32_t>(), gr.seg_off.as<int32_t>(),
-                     gr.seg_cnt.as<int32_t>(), gr.order.as<int32_t>(), pslot, d.w2, d.b2, h, z, s);
+  launch_logits_rows(hp, b, gr.view(), pslot, d.w2, d.b2, h, z, s);
   c->timer.mark(s, kStLogits);
   // sharded: the softmax is completed by the slide_shard_softmax_* stages
   if (c->G == 1) launch_softmax(b, offs, plab, bt->y_ptr, z, prob, delta, loss, s);
@@ -585,7 +584,8 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
   if (!dh) {
     float* out = c->dh.ensure<float>((size_t)b * hp);
     launch_hidden_grad(hp, b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->delta.as<float>(), d.w2,
-                       c->h.as<float>(), out, c->partial.ensure<float>((size_t)hidden_grad_slices(b) * b * hp), s);
+                       c->h.as<float>(), out,
+                       c->partial.ensure<float>(hidden_grad_scratch(b, hp)), s);
     dh = out;
   }
   c->timer.mark(s, kStHiddenGrad);
@@ -900,7 +900,8 @@ int slide_shard_hidden_grad(slide_ctx* c, float* dh_out) {
     const int b = c->last_b, hp = c->hp;
     // unmasked partial (h = null): masking commutes with the all-reduce
     launch_hidden_grad(hp, b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->delta.as<float>(), c->d.w2, nullptr,
-                       dh_out, c->partial.ensure<float>((size_t)hidden_grad_slices(b) * b * hp), c->s);
+                       dh_out,
+                       c->partial.ensure<float>(hidden_grad_scratch(b, hp)), c->s);
   });
 }
 

@@ -62,6 +62,14 @@ void launch_softmax_finish(int b, const int32_t* offs, const uint8_t* plab, cons
                            cudaStream_t s);
 
 // Stable (key, slot) group-by with device-side sizes (group.cu).
+// the group-by result a kernel walks (device pointers)
+struct GroupView {
+  const int32_t *n_uniq, *uniq, *seg_off, *seg_cnt, *order;
+  const uint32_t* mask;
+  int wpk;
+  int64_t u_max;
+};
+
 struct GroupBy {
   DBuf bits, key_rank, uniq, seg_cnt, seg_off, n_uniq, mask, order, status, ctrs;
   int64_t K = 0, nwords = 0, u_max = 0, bits_words = 0, mask_words = 0, tiles_bits = 0, tiles_seg = 0;
@@ -72,6 +80,10 @@ struct GroupBy {
            cudaStream_t s);
   void clear(cudaStream_t s);
   void release();
+  GroupView view() {
+    return GroupView{n_uniq.as<int32_t>(), uniq.as<int32_t>(), seg_off.as<int32_t>(), seg_cnt.as<int32_t>(),
+                     order.as<int32_t>(), mask.as<uint32_t>(), wpk, u_max};
+  }
 };
 
 // ------------------------------------------------------------------ layers
@@ -85,20 +97,14 @@ struct AdamParams {
 
 void launch_hidden_forward(int hp, int b, const int32_t* x_ptr, const int32_t* x_idx, const float* x_val,
                            const float* w1t, const float* b1, float* h, cudaStream_t s);
-void launch_logits(int hp, int64_t P_max, const int32_t* P_dev, const int32_t* prow, const int32_t* pslot,
-                   const float* w2, const float* b2, const float* h, float* z, cudaStream_t s);
-void launch_logits_rows(int hp, int b, const int32_t* n_uniq, int64_t u_max, const int32_t* uniq,
-                        const int32_t* seg_off, const int32_t* seg_cnt, const int32_t* order, const int32_t* pslot,
-                        const float* w2, const float* b2, const float* h, float* z, cudaStream_t s);
-// false when B*hp does not fit in shared memory (caller uses the sample-major kernel)
-bool launch_hidden_grad_rows(int hp, int b, const int32_t* n_uniq, const int32_t* uniq, const int32_t* seg_off,
-                             const uint32_t* mask, int wpk, const int32_t* order, const int32_t* P_dev,
-                             const float* delta, const float* w2, const float* h, float* partial_buf,
-                             int parts, float* dh, cudaStream_t s);
+
+void launch_logits_rows(int hp, int b, const GroupView& g, const int32_t* pslot, const float* w2, const float* b2,
+                        const float* h, float* z, cudaStream_t s);
+
 void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
                     float* prob, float* delta, double* loss, cudaStream_t s);
-int hidden_grad_slices(int b);
-// part: hidden_grad_slices(b) * b * hp floats of scratch
+// floats of scratch launch_hidden_grad needs
+size_t hidden_grad_scratch(int b, int hp);
 void launch_hidden_grad(int hp, int b, const int32_t* offs, const int32_t* prow, const float* delta, const float* w2,
                         const float* h, float* dh, float* part, cudaStream_t s);
 void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq,

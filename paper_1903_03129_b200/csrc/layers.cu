@@ -108,61 +108,16 @@ void launch_hidden_forward(int hp, int b, const int32_t* x_ptr, const int32_t* x
 
 // ------------------------------------------------------------ output logits
 // z[p] = W2[row_p] . h[slot_p] + b2[row_p] for every (slot, active row)
-// pair (network.py:266).  A warp takes G consecutive pairs (same sample
-// mostly), issues all G row loads, then reduces.
-template <int NV, int G>
-__global__ void __launch_bounds__(256) logits_kernel(int hp, const int32_t* __restrict__ P_dev,
-                                                     const int32_t* __restrict__ prow,
-                                                     const int32_t* __restrict__ pslot, const float* __restrict__ w2,
-                                                     const float* __restrict__ b2, const float* __restrict__ h,
-                                                     float* __restrict__ z) {
-  const int64_t P = *P_dev;
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t p0 = gw * G; p0 < P; p0 += nw * G) {
-    float4 w[G][NV];
-    int row[G], slot[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const int64_t p = p0 + g;
-      row[g] = p < P ? prow[p] : 0;
-      slot[g] = p < P ? pslot[p] : 0;
-      const float* rp = w2 + (int64_t)row[g] * hp + lane * 4;
-#pragma unroll
-      for (int q = 0; q < NV; ++q) w[g][q] = p < P ? ld4(rp + q * 128) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const float* hr = h + (int64_t)slot[g] * hp + lane * 4;
-      float d = 0.f;
-#pragma unroll
-      for (int q = 0; q < NV; ++q) {
-        float4 hv = ld4(hr + q * 128);
-        d = fmaf(w[g][q].x, hv.x, d);
-        d = fmaf(w[g][q].y, hv.y, d);
-        d = fmaf(w[g][q].z, hv.z, d);
-        d = fmaf(w[g][q].w, hv.w, d);
-      }
-      d = warp_sum(d);
-      if (lane == 0 && p0 + g < P) z[p0 + g] = d + b2[row[g]];
-    }
-  }
-}
-
-void launch_logits(int hp, int64_t P_max, const int32_t* P_dev, const int32_t* prow, const int32_t* pslot,
-                   const float* w2, const float* b2, const float* h, float* z, cudaStream_t s) {
-  if (P_max <= 0) return;
-  constexpr int G = 4;
-  int64_t warps = ceil_div(P_max, G);
-  int grid = (int)std::min<int64_t>(ceil_div(warps, 8), (int64_t)kSms * 16);
-  SLIDE_NV_DISPATCH(hp, (logits_kernel<NV, G><<<grid, 256, 0, s>>>(hp, P_dev, prow, pslot, w2, b2, h, z)));
-  SLIDE_LAUNCH_CHECK();
-}
-
-// Row-major logits: one warp per distinct active row, the row read once into
-// registers, then dotted with every sample that holds it (the stable group-by
-// order).  4 pairs share one butterfly: 6 shuffles instead of 20.
+// pair (network.py:266).
+// Row-major logits.  The distinct active rows (ascending, the stable group-by)
+// are cut into 64-row tiles; each tile picks its path from its own pair
+// density:
+//  * dense (>= 1/8 of the tile's rows x B cells are pairs): a register-tiled
+//    fp32 product of the tile's W2 rows with all of h (64 x 128 outputs per
+//    CTA, k in chunks of 32 through shared memory), then the pairs are picked
+//    out through the slot masks -- wide-in rows are held by ~half the batch;
+//  * sparse: one warp per row, the row in registers, dotted with each of its
+//    samples; 4 pairs share one butterfly (6 shuffles instead of 20).
 __device__ __forceinline__ float reduce4(float v0, float v1, float v2, float v3, int lane) {
   const bool hi16 = lane & 16;
   float k0 = hi16 ? v2 : v0, k1 = hi16 ? v3 : v1;
@@ -177,183 +132,199 @@ __device__ __forceinline__ float reduce4(float v0, float v1, float v2, float v3,
   return k;  // the sum for pair ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1)
 }
 
-template <int NV, bool SMEM_H>
-__global__ void __launch_bounds__(256) logits_rows_kernel(int hp, int b, const int32_t* __restrict__ n_uniq,
-                                                          const int32_t* __restrict__ uniq,
-                                                          const int32_t* __restrict__ seg_off,
-                                                          const int32_t* __restrict__ seg_cnt,
-                                                          const int32_t* __restrict__ order,
-                                                          const int32_t* __restrict__ pslot,
-                                                          const float* __restrict__ w2, const float* __restrict__ b2,
-                                                          const float* __restrict__ h, float* __restrict__ z) {
-  extern __shared__ __align__(16) float hs[];
-  if (SMEM_H) {
-    const float4* src = reinterpret_cast<const float4*>(h);
-    float4* dst = reinterpret_cast<float4*>(hs);
-    for (int q = threadIdx.x; q < b * hp / 4; q += blockDim.x) dst[q] = src[q];
-    __syncthreads();
-  }
-  const float* hsrc = SMEM_H ? hs : h;
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t nu = *n_uniq;
-  const int mine = ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
-  for (int64_t u = gw; u < nu; u += nw) {
-    const int r = uniq[u];
-    const int s0 = seg_off[u], len = seg_cnt[u];
-    const float bias = b2[r];
-    float4 w[NV];
-#pragma unroll
-    for (int q = 0; q < NV; ++q) w[q] = ld4(w2 + (int64_t)r * hp + q * 128 + lane * 4);
-    for (int j0 = 0; j0 < len; j0 += 32) {
-      const int pl = j0 + lane < len ? order[s0 + j0 + lane] : 0;
-      const int sl = j0 + lane < len ? pslot[pl] : 0;
-      const int nc = min(32, len - j0);
-      for (int q2 = 0; q2 < nc; q2 += 4) {
-        float v[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int slot = __shfl_sync(0xffffffffu, sl, min(q2 + t, nc - 1));
-          const float* hr = hsrc + (int64_t)slot * hp + lane * 4;
-          float d = 0.f;
-#pragma unroll
-          for (int q = 0; q < NV; ++q) {
-            const float4 hv = SMEM_H ? *reinterpret_cast<const float4*>(hr + q * 128) : ld4(hr + q * 128);
-            d = fmaf(w[q].x, hv.x, d);
-            d = fmaf(w[q].y, hv.y, d);
-            d = fmaf(w[q].z, hv.z, d);
-            d = fmaf(w[q].w, hv.w, d);
-          }
-          v[t] = d;
-        }
-        const float sum = reduce4(v[0], v[1], v[2], v[3], lane);
-        const int p = __shfl_sync(0xffffffffu, pl, min(q2 + mine, nc - 1));
-        if ((lane & 7) == 0 && q2 + mine < nc) z[p] = sum + bias;
-      }
-    }
-  }
-}
-
-void launch_logits_rows(int hp, int b, const int32_t* n_uniq, int64_t u_max, const int32_t* uniq,
-                        const int32_t* seg_off, const int32_t* seg_cnt, const int32_t* order, const int32_t* pslot,
-                        const float* w2, const float* b2, const float* h, float* z, cudaStream_t s) {
-  if (u_max <= 0) return;
-  const size_t smem = (size_t)b * hp * 4;
-  const bool use_smem = false && smem <= 100 * 1024;  // L1-resident h beats staging (ncu)
-  int grid = (int)std::min<int64_t>(ceil_div(u_max, 8), (int64_t)kSms * (use_smem ? 2 : 8));
-  if (use_smem) {
-    SLIDE_NV_DISPATCH(hp, ({
-      SLIDE_CUDA(cudaFuncSetAttribute(logits_rows_kernel<NV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-      logits_rows_kernel<NV, true><<<grid, 256, smem, s>>>(hp, b, n_uniq, uniq, seg_off, seg_cnt, order, pslot, w2,
-                                                           b2, h, z);
-    }));
-  } else {
-    SLIDE_NV_DISPATCH(hp, (logits_rows_kernel<NV, false><<<grid, 256, 0, s>>>(hp, b, n_uniq, uniq, seg_off, seg_cnt,
-                                                                              order, pslot, w2, b2, h, z)));
-  }
-  SLIDE_LAUNCH_CHECK();
-}
-
-// ------------------------------------------------- hidden gradient, rows
-// dh_i = sum_r delta_ir W2[r] (pre-update W2) accumulated row-major: CTA g
-// takes the rows whose pairs fall in its 1/G share, warp w owns the samples
-// i = w (mod 8) and accumulates them in shared memory -- no atomics, fixed
-// order; the G partials are summed in order by a second kernel.
 template <int NV>
-__global__ void __launch_bounds__(256) hidden_grad_rows_kernel(
-    int hp, int b, const int32_t* __restrict__ n_uniq, const int32_t* __restrict__ uniq,
-    const int32_t* __restrict__ seg_off, const uint32_t* __restrict__ mask, int wpk,
-    const int32_t* __restrict__ order, const int32_t* __restrict__ P_dev, const float* __restrict__ delta,
-    const float* __restrict__ w2, float* __restrict__ partial) {
-  extern __shared__ __align__(16) float acc[];
-  for (int q = threadIdx.x; q < b * hp; q += blockDim.x) acc[q] = 0.f;
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nu = *n_uniq;
-  const int64_t P = *P_dev;
-  const int64_t lo = P * blockIdx.x / gridDim.x, hi = P * (blockIdx.x + 1) / gridDim.x;
-  // rows whose first pair lies in [lo, hi)
-  auto lower = [&](int64_t key) {
-    int a = 0, c = nu;
-    while (a < c) {
-      const int mid = (a + c) >> 1;
-      if (seg_off[mid] < key) a = mid + 1;
-      else c = mid;
-    }
-    return a;
-  };
-  const int u0 = lower(lo), u1 = lower(hi);
-  const uint32_t own = 0x01010101u << warp;
-  for (int u = u0; u < u1; ++u) {
-    const uint32_t* m = mask + (int64_t)u * wpk;
-    const int base = seg_off[u];
-    const float* wr = w2 + (int64_t)uniq[u] * hp + lane * 4;
-    float4 w[NV];
-    bool loaded = false;
-    int rank_base = 0;
-    for (int k = 0; k < wpk; ++k) {
-      const uint32_t bits = m[k];
-      uint32_t mine = bits & own;
-      if (mine && !loaded) {
+__device__ __forceinline__ void logits_row_warp(int hp, int64_t u, const GroupView& g, const int32_t* __restrict__ pslot,
+                                                const float* __restrict__ w2, const float* __restrict__ b2,
+                                                const float* __restrict__ h, float* __restrict__ z) {
+  const int lane = threadIdx.x & 31;
+  const int mine = ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+  const int r = g.uniq[u];
+  const int s0 = g.seg_off[u], len = g.seg_cnt[u];
+  const float bias = b2[r];
+  float4 w[NV];
 #pragma unroll
-        for (int q = 0; q < NV; ++q) w[q] = ld4(wr + q * 128);
-        loaded = true;
-      }
-      while (mine) {
-        const int bit = __ffs(mine) - 1;
-        mine &= mine - 1;
-        const int slot = k * 32 + bit;
-        const int p = order[base + rank_base + __popc(bits & ((1u << bit) - 1u))];
-        const float d = delta[p];
-        float* a = acc + slot * hp + lane * 4;
+  for (int q = 0; q < NV; ++q) w[q] = ld4(w2 + (int64_t)r * hp + q * 128 + lane * 4);
+  for (int j0 = 0; j0 < len; j0 += 32) {
+    const int pl = j0 + lane < len ? g.order[s0 + j0 + lane] : 0;
+    const int sl = j0 + lane < len ? pslot[pl] : 0;
+    const int nc = min(32, len - j0);
+    for (int q2 = 0; q2 < nc; q2 += 4) {
+      float v[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int slot = __shfl_sync(0xffffffffu, sl, min(q2 + t, nc - 1));
+        const float* hr = h + (int64_t)slot * hp + lane * 4;
+        float d = 0.f;
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
-          float4 t = *reinterpret_cast<float4*>(a + q * 128);
-          t.x = fmaf(d, w[q].x, t.x);
-          t.y = fmaf(d, w[q].y, t.y);
-          t.z = fmaf(d, w[q].z, t.z);
-          t.w = fmaf(d, w[q].w, t.w);
-          *reinterpret_cast<float4*>(a + q * 128) = t;
+          const float4 hv = ld4(hr + q * 128);
+          d = fmaf(w[q].x, hv.x, d);
+          d = fmaf(w[q].y, hv.y, d);
+          d = fmaf(w[q].z, hv.z, d);
+          d = fmaf(w[q].w, hv.w, d);
         }
+        v[t] = d;
       }
-      rank_base += __popc(bits);
+      const float sum = reduce4(v[0], v[1], v[2], v[3], lane);
+      const int p = __shfl_sync(0xffffffffu, pl, min(q2 + mine, nc - 1));
+      if ((lane & 7) == 0 && q2 + mine < nc) z[p] = sum + bias;
     }
   }
-  __syncthreads();
-  float4* dst = reinterpret_cast<float4*>(partial + (int64_t)blockIdx.x * b * hp);
-  const float4* src = reinterpret_cast<const float4*>(acc);
-  for (int q = threadIdx.x; q < b * hp / 4; q += blockDim.x) dst[q] = src[q];
 }
 
-__global__ void hidden_grad_reduce_kernel(int hp, int b, int parts, const float* __restrict__ partial,
-                                          const float* __restrict__ h, float* __restrict__ dh) {
-  const int64_t n = (int64_t)b * hp;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int g = 0; g < parts; ++g) s += partial[(int64_t)g * n + q];
-    dh[q] = h[q] > 0.f ? s : 0.f;
+constexpr int kTM = 64;         // rows per tile
+constexpr int kTN = 64;         // samples per tile
+constexpr int kKC = 128;        // k per shared-memory stage
+constexpr int kLd = kKC + 4;    // padded row stride (conflict-free float4 reads)
+constexpr int kMaskWords = 32;  // B <= 1024
+constexpr int kTileSmem = (2 * kTM * kLd) * 4 + kTM * kMaskWords * 4 + kTM * 8;
+
+// dense work item = (64-row tile, 64-sample block).  A row tile goes dense
+// unless its pairs cover < 1/64 of its rows x B cells (then the per-row
+// kernel is cheaper); wide-in tiles are 10-50% full.
+__device__ __forceinline__ bool tile_is_dense(const GroupView& g, int64_t u0, int nrow, int b) {
+  const int64_t last = u0 + nrow - 1;
+  const int64_t npairs = (int64_t)g.seg_off[last] + g.seg_cnt[last] - g.seg_off[u0];
+  return npairs * 64 >= (int64_t)nrow * b;
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256, 2) logits_tiles_kernel(int hp, int b, GroupView g,
+                                                              const int32_t* __restrict__ pslot,
+                                                              const float* __restrict__ w2,
+                                                              const float* __restrict__ b2,
+                                                              const float* __restrict__ h, float* __restrict__ z) {
+  extern __shared__ __align__(16) float tsm[];
+  float* ws = tsm;                                   // [kTM][kLd]
+  float* hs = ws + kTM * kLd;                        // [kTN][kLd]
+  int* cum = reinterpret_cast<int*>(hs + kTN * kLd);  // [kTM][kMaskWords] mask popc prefix per row
+  int* base_s = cum + kTM * kMaskWords;              // [kTM]
+  float* bias_s = reinterpret_cast<float*>(base_s + kTM);
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int64_t nu = *g.n_uniq;
+  const int64_t tiles = (nu + kTM - 1) / kTM;
+  const int nsb = (b + kTN - 1) / kTN;
+  for (int64_t item = blockIdx.x; item < tiles * nsb; item += gridDim.x) {
+    const int64_t tile = item / nsb;
+    const int s0 = (int)(item - tile * nsb) * kTN;
+    const int64_t u0 = tile * kTM;
+    const int nrow = (int)min((int64_t)kTM, nu - u0);
+    if (!tile_is_dense(g, u0, nrow, b)) continue;  // sparse tile: logits_rows_kernel
+    if (tid < nrow) {
+      const int64_t u = u0 + tid;
+      const uint32_t* mrow = g.mask + u * g.wpk;
+      int run = 0;
+      for (int w = 0; w < g.wpk; ++w) {
+        cum[tid * kMaskWords + w] = run;
+        run += __popc(mrow[w]);
+      }
+      base_s[tid] = g.seg_off[u];
+      bias_s[tid] = b2[g.uniq[u]];
+    }
+    float acc[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) acc[j][jj] = 0.f;
+    for (int k0 = 0; k0 < hp; k0 += kKC) {
+      // stage 64 W rows and 64 h rows of this k range: 16 float4 loads in
+      // flight per thread
+      float4 lw[8], lh[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int idx = tid + q * 256, row = idx >> 5, c = (idx & 31) * 4;
+        lw[q] = row < nrow ? ld4(w2 + (int64_t)g.uniq[u0 + row] * hp + k0 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        lh[q] = s0 + row < b ? ld4(h + (int64_t)(s0 + row) * hp + k0 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      __syncthreads();  // previous readers of ws / hs are done
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int idx = tid + q * 256, row = idx >> 5, c = (idx & 31) * 4;
+        *reinterpret_cast<float4*>(&ws[row * kLd + c]) = lw[q];
+        *reinterpret_cast<float4*>(&hs[row * kLd + c]) = lh[q];
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int kk = 0; kk < kKC; kk += 4) {
+        float4 wv[4], hv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) wv[j] = *reinterpret_cast<const float4*>(&ws[(ty + 16 * j) * kLd + kk]);
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) hv[jj] = *reinterpret_cast<const float4*>(&hs[(tx + 16 * jj) * kLd + kk]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) acc[j][jj] = fmaf(wv[j].x, hv[jj].x, acc[j][jj]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) acc[j][jj] = fmaf(wv[j].y, hv[jj].y, acc[j][jj]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) acc[j][jj] = fmaf(wv[j].z, hv[jj].z, acc[j][jj]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) acc[j][jj] = fmaf(wv[j].w, hv[jj].w, acc[j][jj]);
+      }
+    }
+    // pick the pairs out of the 64 x 64 block (cum / base / bias are visible
+    // after the staging barriers)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int row = ty + 16 * j;
+      if (row >= nrow) continue;
+      const uint32_t* mrow = g.mask + (u0 + row) * g.wpk;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int i = s0 + tx + 16 * jj;
+        if (i >= b) continue;
+        const uint32_t word = mrow[i >> 5];
+        if ((word >> (i & 31)) & 1u) {
+          const int rank = cum[row * kMaskWords + (i >> 5)] + __popc(word & ((1u << (i & 31)) - 1u));
+          z[g.order[base_s[row] + rank]] = acc[j][jj] + bias_s[row];
+        }
+      }
+    }
+    __syncthreads();  // cum / base / bias reuse by the next item
   }
 }
 
-bool launch_hidden_grad_rows(int hp, int b, const int32_t* n_uniq, const int32_t* uniq, const int32_t* seg_off,
-                             const uint32_t* mask, int wpk, const int32_t* order, const int32_t* P_dev,
-                             const float* delta, const float* w2, const float* h, float* partial_buf,
-                             int parts, float* dh, cudaStream_t s) {
-  const size_t smem = (size_t)b * hp * 4;
-  if (smem > 200 * 1024) return false;
-  SLIDE_NV_DISPATCH(hp, ({
-    SLIDE_CUDA(cudaFuncSetAttribute(hidden_grad_rows_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-    hidden_grad_rows_kernel<NV><<<parts, 256, smem, s>>>(hp, b, n_uniq, uniq, seg_off, mask, wpk, order, P_dev,
-                                                         delta, w2, partial_buf);
-  }));
+// rows of the sparse tiles: one warp per row
+template <int NV>
+__global__ void __launch_bounds__(256) logits_rows_kernel(int hp, int b, GroupView g, const int32_t* __restrict__ pslot,
+                                                          const float* __restrict__ w2, const float* __restrict__ b2,
+                                                          const float* __restrict__ h, float* __restrict__ z,
+                                                          int dense_ok) {
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nu = *g.n_uniq;
+  for (int64_t u = gw; u < nu; u += nw) {
+    const int64_t u0 = u / kTM * kTM;
+    if (dense_ok && tile_is_dense(g, u0, (int)min((int64_t)kTM, nu - u0), b)) continue;  // logits_tiles_kernel
+    logits_row_warp<NV>(hp, u, g, pslot, w2, b2, h, z);
+  }
+}
+
+void launch_logits_rows(int hp, int b, const GroupView& g, const int32_t* pslot, const float* w2, const float* b2,
+                        const float* h, float* z, cudaStream_t s) {
+  if (g.u_max <= 0) return;
+  // dense tiles need the whole batch's slot masks in 32 words and k in whole stages
+  const int dense_ok = b <= 32 * kMaskWords && hp % kKC == 0;
+  if (dense_ok) {
+    const int grid = (int)std::min<int64_t>(ceil_div(g.u_max, kTM) * ceil_div(b, kTN), (int64_t)kSms * 2);
+    SLIDE_NV_DISPATCH(hp, ({
+      SLIDE_CUDA(cudaFuncSetAttribute(logits_tiles_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kTileSmem));
+      logits_tiles_kernel<NV><<<grid, 256, kTileSmem, s>>>(hp, b, g, pslot, w2, b2, h, z);
+    }));
+    SLIDE_LAUNCH_CHECK();
+  }
+  const int rgrid = (int)std::min<int64_t>(ceil_div(g.u_max, 8), (int64_t)kSms * 8);
+  SLIDE_NV_DISPATCH(hp, (logits_rows_kernel<NV><<<rgrid, 256, 0, s>>>(hp, b, g, pslot, w2, b2, h, z, dense_ok)));
   SLIDE_LAUNCH_CHECK();
-  hidden_grad_reduce_kernel<<<(int)std::max<int64_t>(1, ceil_div((int64_t)b * hp, 256)), 256, 0, s>>>(
-      hp, b, parts, partial_buf, h, dh);
-  SLIDE_LAUNCH_CHECK();
-  return true;
 }
 
 // ---------------------------------------------------- softmax + CE + delta
@@ -416,7 +387,9 @@ void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32
 // dh_i = W2[A_i, :]^T delta_i with the pre-update W2, kept on nz(h_i)
 // (network.py:328-332).  Sample i's pairs are cut into S slices, one CTA
 // each (B*S CTAs fill the GPU); every slice sums in a fixed order, the
-// slices are added in slice order -- deterministic.
+// slices are added in slice order -- deterministic.  (A dense register-tiled
+// Delta^T W2 over the distinct rows was tried: the Delta scatter and the
+// partial reduction cost more than the L2 re-reads of W2 rows it saves.)
 template <int NV>
 __global__ void __launch_bounds__(256) hidden_grad_kernel(int hp, int b, int slices, const int32_t* __restrict__ offs,
                                                           const int32_t* __restrict__ prow,
@@ -488,6 +461,8 @@ __global__ void slice_sum_kernel(int64_t n, int slices, const float* __restrict_
 }
 
 int hidden_grad_slices(int b) { return std::max(1, std::min(8, (int)ceil_div((int64_t)kSms * 4, b))); }
+
+size_t hidden_grad_scratch(int b, int hp) { return (size_t)hidden_grad_slices(b) * b * hp; }
 
 void launch_hidden_grad(int hp, int b, const int32_t* offs, const int32_t* prow, const float* delta, const float* w2,
                         const float* h, float* dh, float* part, cudaStream_t s) {

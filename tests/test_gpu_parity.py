@@ -139,6 +139,35 @@ def test_full_union_vanilla_matches_oracle(family):
         assert_state_close(net, st, what=f"full-union {family} it{it}")
 
 
+@pytest.mark.parametrize("shape", ["sparse", "mixed", "dense"])
+def test_dense_and_sparse_tiles_match_oracle(shape):
+    """The logits pick a register-tiled dense path or the per-row path for
+    each 64-row tile from its pair density; every mix must equal the
+    oracle."""
+    rng = np.random.default_rng(21)
+    D, H = 80, 24
+    N, B, beta, cap, l = {"sparse": (3000, 32, 4, 2, 3), "mixed": (700, 40, 60, 8, 8),
+                          "dense": (150, 48, 150, 32, 8)}[shape]
+    spec = LshLayerConfig("simhash", k=2, l=l, capacity=cap, sampler=SamplerConfig("vanilla", beta=beta))
+    cfg = TrainConfig(batch_size=B, seed=6, learning_rate=1e-2, n0=2)
+    net = SlideNetwork(D, [H, N], cfg, lsh_layers={1: spec})
+    st = oracle_state_from_net(net)
+    lsh = oracle_lsh_from_net(net, spec, st)
+    for it in (1, 2, 3):
+        trip = []
+        for _ in range(B):
+            idx = np.sort(rng.choice(D, size=int(rng.integers(1, 12)), replace=False))
+            vals = (np.abs(rng.standard_normal(idx.size)) + 0.1).astype(np.float32).astype(np.float64)
+            # Zipf-ish labels: a few hot rows held by most samples, a long tail
+            lab = sorted(set(int(v) % N for v in rng.zipf(1.3, size=3)))
+            trip.append((idx, vals, lab))
+        want = O.train_step(st, lsh, trip, it, cfg.seed, N, O.AdamCfg(lr=1e-2), mode="snapshot")
+        got = net.train_batch([(SparseVector(xi, xv, D), set(y)) for xi, xv, y in trip], it, schedule="snapshot")
+        assert got.loss == pytest.approx(float(np.mean(want.losses)), rel=1e-5)
+        assert got.active_fraction[1] == pytest.approx(want.active_fraction, rel=1e-12)
+        assert_state_close(net, st, what=f"{shape} it{it}", adam_lr=1e-2)
+
+
 def _golden_batch(g, name, it, B):
     return [(g[f"{name}_it{it}_x{i}_idx"], g[f"{name}_it{it}_x{i}_val"], g[f"{name}_it{it}_y{i}"].tolist())
             for i in range(B)]
