@@ -556,25 +556,7 @@ __device__ __forceinline__ void adam_coord_hs(bool on, float& w, float& m, float
   w = on ? wn : w;
 }
 
-// Stage the batch's activations (b x hp floats) in shared memory: 4
-// independent 16-byte loads in flight per thread.
-__device__ __forceinline__ void stage_rows(float* dst, const float* src, int n_floats) {
-  const int n4 = n_floats / 4;
-  const float4* s4 = reinterpret_cast<const float4*>(src);
-  float4* d4 = reinterpret_cast<float4*>(dst);
-  int q = threadIdx.x;
-  for (; q + 3 * (int)blockDim.x < n4; q += 4 * blockDim.x) {
-    const float4 a = __ldg(s4 + q), b = __ldg(s4 + q + blockDim.x), c = __ldg(s4 + q + 2 * blockDim.x),
-                 d = __ldg(s4 + q + 3 * blockDim.x);
-    d4[q] = a;
-    d4[q + blockDim.x] = b;
-    d4[q + 2 * blockDim.x] = c;
-    d4[q + 3 * blockDim.x] = d;
-  }
-  for (; q < n4; q += blockDim.x) d4[q] = __ldg(s4 + q);
-}
-
-template <int NV, bool SMEM_H, bool COUNT>
+template <int NV, bool COUNT>
 __global__ void __launch_bounds__(256) adam_rows_kernel(int hp, int b, AdamParams ap,
                                                         const int32_t* __restrict__ n_uniq,
                                                         const int32_t* __restrict__ uniq,
@@ -588,16 +570,11 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(int hp, int b, AdamParam
                                                         float* __restrict__ mb2, float* __restrict__ vb2,
                                                         int64_t* __restrict__ steps2,
                                                         unsigned long long* __restrict__ touched) {
-  extern __shared__ __align__(16) float hs[];
   // per-warp broadcast of the current chunk's pair scalars:
-  // (h row offset, e1, e2, c1) and sqrt(c2)
+  // (h row offset, e1, e2, c1) and sqrt(c2); h itself is read through L1
+  // (64 KB at B = 128: resident; staging it in shared memory cost occupancy)
   __shared__ float4 pq[8][32];
   __shared__ float ps2[8][32];
-  if (SMEM_H) {
-    stage_rows(hs, h, b * hp);
-    __syncthreads();
-  }
-  const float* hsrc = SMEM_H ? hs : h;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -666,10 +643,10 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(int hp, int b, AdamParam
       for (int q2 = 0; q2 < nc; ++q2) {
         const float4 P = pq[wid][q2];
         const float s2 = ps2[wid][q2];
-        const float* hr = hsrc + __float_as_int(P.x) + lane * 4;
+        const float* hr = h + __float_as_int(P.x) + lane * 4;
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
-          const float4 hv = SMEM_H ? *reinterpret_cast<const float4*>(hr + q * 128) : ld4(hr + q * 128);
+          const float4 hv = ld4(hr + q * 128);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const float hc = reinterpret_cast<const float*>(&hv)[c];
@@ -717,36 +694,15 @@ void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq
                       float* w2, float* m2, float* v2, float* b2, float* mb2, float* vb2, int64_t* steps2,
                       unsigned long long* touched, cudaStream_t s) {
   if (max_uniq <= 0) return;
-  const size_t smem = (size_t)b * hp * 4;
-  if (smem <= 100 * 1024) {
-    // persistent: each CTA stages h once, then walks rows grid-stride
-    const int per_sm = smem <= 68 * 1024 ? 3 : 2;
-    int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * per_sm);
-#define SLIDE_ADAM_ROWS(CNT)                                                                                  \
-  SLIDE_NV_DISPATCH(hp, ({                                                                                    \
-    SLIDE_CUDA(cudaFuncSetAttribute(adam_rows_kernel<NV, true, CNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                    (int)smem));                                                              \
-    adam_rows_kernel<NV, true, CNT><<<grid, 256, smem, s>>>(hp, b, ap, n_uniq, uniq, seg_off, seg_cnt,         \
-                                                            sorted_pairs, pslot, delta, h, w2, m2, v2, b2, mb2, \
-                                                            vb2, steps2, touched);                            \
-  }))
-    if (touched) {
-      SLIDE_ADAM_ROWS(true);
-    } else {
-      SLIDE_ADAM_ROWS(false);
-    }
-#undef SLIDE_ADAM_ROWS
+  const int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * 16);
+  if (touched) {
+    SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, true><<<grid, 256, 0, s>>>(hp, b, ap, n_uniq, uniq, seg_off, seg_cnt,
+                                                                          sorted_pairs, pslot, delta, h, w2, m2, v2,
+                                                                          b2, mb2, vb2, steps2, touched)));
   } else {
-    int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * 16);
-    if (touched) {
-      SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, false, true><<<grid, 256, 0, s>>>(
-                                hp, b, ap, n_uniq, uniq, seg_off, seg_cnt, sorted_pairs, pslot, delta, h, w2, m2, v2,
-                                b2, mb2, vb2, steps2, touched)));
-    } else {
-      SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, false, false><<<grid, 256, 0, s>>>(
-                                hp, b, ap, n_uniq, uniq, seg_off, seg_cnt, sorted_pairs, pslot, delta, h, w2, m2, v2,
-                                b2, mb2, vb2, steps2, touched)));
-    }
+    SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, false><<<grid, 256, 0, s>>>(hp, b, ap, n_uniq, uniq, seg_off, seg_cnt,
+                                                                           sorted_pairs, pslot, delta, h, w2, m2, v2,
+                                                                           b2, mb2, vb2, steps2, touched)));
   }
   SLIDE_LAUNCH_CHECK();
 }
