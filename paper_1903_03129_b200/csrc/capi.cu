@@ -5,6 +5,7 @@
 #include <cub/cub.cuh>
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <cmath>
 
@@ -90,7 +91,7 @@ struct slide_ctx {
   DBuf bias_table;
   int64_t bias_n = 0;
   int bias_exact = 1;
-  DBuf xslot, tc, bc, partial;
+  DBuf xslot, tc, bc, partial, tc_scratch;
   int64_t fb_bitmap_words = 0;
   double* pinned_loss = nullptr;
   int32_t* pinned_cnt = nullptr;
@@ -206,7 +207,7 @@ static int64_t host_pairs(slide_ctx* c) {
 }
 
 static void hash_rows(slide_ctx* c, const float* x, int64_t n, uint32_t* keys) {
-  if (c->d.family == 1) launch_simhash_keys(simhash_of(c), x, n, c->hp, keys, c->s);
+  if (c->d.family == 1) launch_simhash_keys(simhash_of(c), x, n, c->hp, keys, c->s, &c->tc_scratch);
   else launch_dwta_keys(dwta_of(c), x, n, c->hp, keys, c->s);
 }
 
@@ -270,7 +271,7 @@ int slide_destroy(slide_ctx* c) {
     for (DBuf* b : {&c->sh_packed, &c->sh_packed_t, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->qkeys, &c->order,
                     &c->states, &c->act, &c->cnt, &c->empty, &c->offs, &c->prow, &c->pslot, &c->plab, &c->z,
                     &c->prob, &c->delta, &c->loss, &c->dh, &c->fb_ids, &c->fb_scratch, &c->fb_bitmap, &c->xslot,
-                    &c->tc, &c->bc, &c->counters, &c->partial, &c->bias_table, &c->cnt_all})
+                    &c->tc, &c->bc, &c->counters, &c->partial, &c->tc_scratch, &c->bias_table, &c->cnt_all})
       b->release();
     c->grow.release();
     c->gfeat.release();
@@ -300,7 +301,11 @@ int slide_simhash_keys(const float* x, int64_t n, int64_t ld, int64_t dim, int64
     SLIDE_CHECK(k * 1 <= 32, kNotSupported, "device keys are at most 32 bits");
     SLIDE_CHECK(dim <= 32767 && dim <= ld, kValueError, "simhash dim must be <= 32767 and <= ld");
     SimHashDev f{(int)dim, (int)k, (int)l, (int)c, packed_dev};
-    launch_simhash_keys(f, x, n, (int)ld, keys, (cudaStream_t)stream);
+    // large batches take the tensor-core path (its fix-up list is shared scratch)
+    static std::mutex mu;
+    static DBuf scratch;
+    std::lock_guard<std::mutex> lock(mu);
+    launch_simhash_keys(f, x, n, (int)ld, keys, (cudaStream_t)stream, &scratch);
   });
 }
 

@@ -113,8 +113,9 @@ __global__ void __launch_bounds__(512) simhash_query_kernel(SimHashDev f, const 
 }
 
 void launch_simhash_keys(const SimHashDev& f, const float* x, int64_t n, int ld, uint32_t* keys,
-                         cudaStream_t s) {
+                         cudaStream_t s, DBuf* tc_scratch) {
   if (n <= 0) return;
+  if (tc_scratch && n >= (int64_t)kSms * 128 && launch_simhash_keys_tc(f, x, n, ld, keys, *tc_scratch, s)) return;
   const int KL = f.k * f.l;
   if (f.packed_t && n <= (int64_t)kSms * 8) {
     const size_t smem = (size_t)f.dim * 4 + KL;

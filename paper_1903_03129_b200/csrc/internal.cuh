@@ -48,8 +48,13 @@ struct DwtaDev {
   const int16_t* donors;   // (K*L, 100)
 };
 
+// Tensor-core rebuild path (tc_hash.cu); false when the shape does not fit.
+bool launch_simhash_keys_tc(const SimHashDev& f, const float* x, int64_t n, int ld, uint32_t* keys, DBuf& scratch,
+                            cudaStream_t s);
+// tc_scratch: when given, large row counts (table rebuilds) go to the
+// tensor-core path
 void launch_simhash_keys(const SimHashDev& f, const float* x, int64_t n, int ld, uint32_t* keys,
-                         cudaStream_t s);
+                         cudaStream_t s, DBuf* tc_scratch = nullptr);
 void launch_dwta_keys(const DwtaDev& f, const float* x, int64_t n, int ld, uint32_t* keys,
                       cudaStream_t s);
 

@@ -50,6 +50,29 @@ def test_device_hash_keys_match_reference(golden, name):
         np.testing.assert_array_equal(fam.hash(SparseVector.from_dense(q[row])), g[name + "_qkeys"][row])
 
 
+def test_tensor_core_rebuild_hash_matches_oracle():
+    """>= 148 x 128 rows take the tcgen05 path (bf16x3 split, fp32 TMEM
+    accumulation, certified signs + exact fp64 fix-up): keys bit-exact against
+    the oracle, including rows whose projections cancel exactly (sign(0) -> 0),
+    all-zero rows and rows spanning a huge dynamic range."""
+    spec = HASH_SPECS["sh_main"]
+    fam = new_hash_family(HashFamilyConfig(**spec))
+    rng = np.random.default_rng(17)
+    n, d = 30000, spec["dim"]
+    w = rng.standard_normal((n, d)).astype(np.float32)
+    w[::97] = 0.0  # all-zero rows: every dot is exactly 0
+    for r in range(1, n, 101):  # exact cancellations inside projections
+        p = rng.integers(fam.n_codes)
+        i = fam.proj_indices[p]
+        w[r] = 0.0
+        w[r, i[0]], w[r, i[1]] = 0.75, 0.75 * fam.proj_signs[p, 0] * fam.proj_signs[p, 1] * -1
+    w[5::211] *= np.float32(1e18)
+    w[7::223, :3] = np.float32(1e-30)
+    w = w.astype(np.float64)
+    params = O.SimHashParams(d, spec["k_per_table"], spec["num_tables"], fam.proj_indices, fam.proj_signs)
+    np.testing.assert_array_equal(fam.hash_batch(w), O.simhash_keys(params, w))
+
+
 def test_wta_dense_equals_dwta_on_dense_inputs():
     rng = np.random.default_rng(3)
     wta = new_hash_family(HashFamilyConfig("wta", 3, 2, 12, wta_bin_size=4, seed=13))
