@@ -33,6 +33,8 @@ constexpr int kTcThreads = 256;           // 8 warps: warp w reads TMEM lanes 32
 constexpr int kTcMaxCols = 512;           // TMEM columns (fp32 accumulators)
 constexpr double kTcBoundRel = 384.0 / 1048576.0;  // 384 * 2^-20
 constexpr int kBitsLd = kTcMaxCols / 32 + 1;       // sign-bit words per row (+1: banks)
+constexpr int kTcK = 128;                          // hidden width of the tensor-core path
+constexpr int kTcChunks = kTcK / 16;               // 8-column chunks per thread (two threads per row)
 
 struct TcFix {
   int32_t row, bit;
@@ -143,24 +145,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) simhash_tc_kernel(SimHashDev f,
   const uint32_t a_lbo = agroups * 128, p_lbo = pgroups * 128;
   uint32_t phase = 0;
   const int64_t tiles = (n + kTcRows - 1) / kTcRows;
+  // W rows of a tile: thread (row, half) loads k chunks [8 half, 8 half + 8)
+  // of 8 floats (kdim = 128), kept in registers so the next tile's loads are
+  // in flight during this tile's MMAs and epilogue
+  float4 wbuf[kTcChunks * 2];
+  auto load_w = [&](int64_t row0) {
+    const int64_t gr = row0 + row;
+    const float* xr = x + gr * ld + half * kTcChunks * 8;
+#pragma unroll
+    for (int q = 0; q < kTcChunks * 2; ++q)
+      wbuf[q] = gr < n ? *reinterpret_cast<const float4*>(xr + q * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  if ((int64_t)blockIdx.x < tiles) load_w((int64_t)blockIdx.x * kTcRows);
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int64_t row0 = tile * kTcRows;
-    // W tile -> hi / mid / lo parts.  Threads (row, half) own the row's k
-    // chunks half*kdim/16 ..: per 8-column chunk two 16-byte loads and one
-    // 16-byte store per part (a core-matrix row; a warp's stores are
-    // contiguous); S_r = sum |w| accumulates in place.
+    // split into hi / mid / lo: per 8-column chunk one 16-byte store per part
+    // (a core-matrix row; a warp's stores are contiguous); S_r = sum |w|
     {
-      const int64_t gr = row0 + row;
-      const float* xr = x + gr * ld;
       float s = 0.f;
-      const int kc0 = half * (kdim / 16), kc1 = kc0 + kdim / 16;
-#pragma unroll 4
-      for (int kc = kc0; kc < kc1; ++kc) {
-        float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
-        if (gr < n) {
-          v0 = *reinterpret_cast<const float4*>(xr + kc * 8);
-          v1 = *reinterpret_cast<const float4*>(xr + kc * 8 + 4);
-        }
+#pragma unroll
+      for (int c = 0; c < kTcChunks; ++c) {
+        const int kc = half * kTcChunks + c;
+        const float4 v0 = wbuf[2 * c], v1 = wbuf[2 * c + 1];
         const float e[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
         uint32_t hw[4], mw[4], lw[4];
 #pragma unroll
@@ -208,6 +214,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) simhash_tc_kernel(SimHashDev f,
                        smem_u32(bar))
                    : "memory");
     }
+    if (tile + gridDim.x < tiles) load_w((tile + gridDim.x) * kTcRows);  // next tile, in flight
     mbar_wait(smem_u32(bar), phase);
     phase ^= 1;
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -262,7 +269,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) simhash_tc_kernel(SimHashDev f,
       }
     }
     __syncthreads();  // both halves of every row's bits are in shared memory
-    if (gr < n) {  // keys of `row`: tables split between the two threads
+    // keys of the tile into shared memory (the A parts are free once the
+    // MMAs completed), then one coalesced copy: rows are consecutive
+    uint32_t* keys_s = reinterpret_cast<uint32_t*>(a_s);
+    const int nrow = (int)min((int64_t)kTcRows, n - row0);
+    if (row < nrow) {  // tables split between the row's two threads
       const uint32_t kmask = (uint32_t)((1ull << f.k) - 1);
       const uint32_t* bw = bits_s + row * kBitsLd;
       const int t0 = half ? f.l / 2 : 0, t1 = half ? f.l : f.l / 2;
@@ -270,8 +281,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) simhash_tc_kernel(SimHashDev f,
         const int w0 = b0 >> 5, sh = b0 & 31;
         uint64_t two = bw[w0];
         if (sh + f.k > 32) two |= (uint64_t)bw[w0 + 1] << 32;
-        keys[gr * f.l + t] = (uint32_t)(two >> sh) & kmask;
+        keys_s[row * f.l + t] = (uint32_t)(two >> sh) & kmask;
       }
+    }
+    __syncthreads();
+    {
+      uint32_t* dst = keys + row0 * f.l;
+      const int nk = nrow * f.l;
+      for (int q = tid; q < nk; q += kTcThreads) dst[q] = keys_s[q];
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();  // accumulators read before the next tile's MMAs; A reusable
@@ -307,8 +324,8 @@ __global__ void simhash_fix_kernel(SimHashDev f, const float* __restrict__ x, in
 bool launch_simhash_keys_tc(const SimHashDev& f, const float* x, int64_t n, int ld, uint32_t* keys, DBuf& scratch,
                             cudaStream_t s) {
   const int KL = f.k * f.l;
-  const int kdim = (f.dim + 15) / 16 * 16;
-  if (KL > kTcMaxCols || kdim > ld || kdim % 16 != 0 || ld % 4 != 0 || n < kTcRows) return false;
+  const int kdim = kTcK;  // W rows padded to 128 columns (hp = 128)
+  if (KL > kTcMaxCols || f.dim > kTcK || kdim > ld || ld % 4 != 0 || n < kTcRows) return false;
   const int np_pad = (KL + 15) / 16 * 16;
   const size_t smem =
       (size_t)np_pad * kdim * 2 + 3 * (size_t)kTcRows * kdim * 2 + 16 + 2 * kTcRows * 4 + kTcRows * kBitsLd * 4;
