@@ -307,11 +307,18 @@ __global__ void simhash_fix_kernel(SimHashDev f, const float* __restrict__ x, in
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nf; q += gridDim.x * blockDim.x) {
     const TcFix e = fix[q];
     const float* xr = x + (int64_t)e.row * ld;
+    const uint16_t* pp = f.packed + (int64_t)e.bit * f.c;
     double acc = 0.0;
-    for (int j = 0; j < f.c; ++j) {
-      const uint16_t pe = f.packed[e.bit * f.c + j];
-      const double v = (double)xr[pe & 0x7fff];
-      acc += (pe >> 15) ? -v : v;
+    for (int j0 = 0; j0 < f.c; j0 += 8) {  // 8 gathers in flight, terms added in order
+      uint16_t pe[8];
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) pe[u] = j0 + u < f.c ? pp[j0 + u] : (uint16_t)0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = j0 + u < f.c ? xr[pe[u] & 0x7fff] : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j0 + u < f.c) acc += (pe[u] >> 15) ? -(double)v[u] : (double)v[u];
     }
     const int t = e.bit / f.k, kk = e.bit - t * f.k;
     uint32_t* kw = keys + (int64_t)e.row * f.l + t;
