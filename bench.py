@@ -84,20 +84,28 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
         self.err = None
-
-    def _run(self):
-        try:
+        self._hnd = None
+        try:  # NVML init here, in the caller's thread and outside any timed region
             import pynvml
 
             pynvml.nvmlInit()
-            hnd = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            mx = pynvml.nvmlDeviceGetMaxClockInfo(hnd, pynvml.NVML_CLOCK_SM)
-            while not self._stop.is_set():
-                sm = pynvml.nvmlDeviceGetClockInfo(hnd, pynvml.NVML_CLOCK_SM)
-                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(hnd)
-                self.rows.append((sm, mx, rs))
-                self._stop.wait(0.002)
+            self._nvml = pynvml
+            self._hnd = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(self._hnd, pynvml.NVML_CLOCK_SM)
         except Exception as e:  # no NVML: report it rather than invent clocks
+            self.err = repr(e)
+
+    def _run(self):
+        if self._hnd is None:
+            return
+        nv, hnd = self._nvml, self._hnd
+        try:
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(hnd, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(hnd)
+                self.rows.append((sm, self._max, rs))
+                self._stop.wait(0.002)
+        except Exception as e:
             self.err = repr(e)
 
     def __enter__(self):
@@ -213,6 +221,7 @@ def run_ours(args, rank, world):
                       act_buf.ctypes.data)
         return net._barrier(it, loss_buf, act_buf)
 
+    sampler = ClockSampler(torch.cuda.current_device())  # NVML init before the warm-up
     for it in range(1, W + 1):
         step_dev(it)
     torch.cuda.synchronize()
@@ -222,7 +231,7 @@ def run_ours(args, rank, world):
     _lib.call("slide_launch_count", lc0.ctypes.data)
     times = []
     losses = []
-    with ClockSampler(torch.cuda.current_device()) as clk:
+    with sampler as clk:
         for it in range(W + 1, W + K + 1):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

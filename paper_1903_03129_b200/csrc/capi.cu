@@ -91,7 +91,7 @@ struct slide_ctx {
   DBuf bias_table;
   int64_t bias_n = 0;
   int bias_exact = 1;
-  DBuf xslot, tc, bc, partial, tc_scratch;
+  DBuf xslot, tc, bc, partial, tc_scratch, long_list, n_long;
   int64_t fb_bitmap_words = 0;
   double* pinned_loss = nullptr;
   int32_t* pinned_cnt = nullptr;
@@ -271,7 +271,7 @@ int slide_destroy(slide_ctx* c) {
     for (DBuf* b : {&c->sh_packed, &c->sh_packed_t, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->qkeys, &c->order,
                     &c->states, &c->act, &c->cnt, &c->empty, &c->offs, &c->prow, &c->pslot, &c->plab, &c->z,
                     &c->prob, &c->delta, &c->loss, &c->dh, &c->fb_ids, &c->fb_scratch, &c->fb_bitmap, &c->xslot,
-                    &c->tc, &c->bc, &c->counters, &c->partial, &c->tc_scratch, &c->bias_table, &c->cnt_all})
+                    &c->tc, &c->bc, &c->counters, &c->partial, &c->long_list, &c->n_long, &c->tc_scratch, &c->bias_table, &c->cnt_all})
       b->release();
     c->grow.release();
     c->gfeat.release();
@@ -622,7 +622,8 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
     c->timer.mark(s, kStGroupFeat);
     launch_adam_features(hp, ap, gf.n_uniq.as<int32_t>(), gf.u_max, gf.uniq.as<int32_t>(), gf.seg_off.as<int32_t>(),
                          gf.seg_cnt.as<int32_t>(), gf.order.as<int32_t>(), xs, c->last_xval, c->last_xbase,
-                         c->h.as<float>(), dh, bc, d.w1t, d.m1t, d.v1t, ctr ? ctr + 1 : nullptr, s);
+                         c->h.as<float>(), dh, bc, d.w1t, d.m1t, d.v1t, ctr ? ctr + 1 : nullptr,
+                         c->long_list.ensure<int32_t>(std::max<int64_t>(gf.u_max, 1)), c->n_long.ensure<int32_t>(1), s);
     c->timer.mark(s, kStAdamFeat);
   }
   c->timer.mark(s, kStHiddenBias);

@@ -120,7 +120,7 @@ void launch_adam_features(int hp, const AdamParams& ap, const int32_t* n_uniq, i
                           const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
                           const int32_t* sorted_k, const int32_t* x_slot, const float* x_val, int64_t x_base,
                           const float* h, const float* dh, const float2* bc, float* w1t, float* m1t, float* v1t,
-                          unsigned long long* touched, cudaStream_t s);
+                          unsigned long long* touched, int32_t* long_list, int32_t* n_long, cudaStream_t s);
 void launch_hidden_prep_bias(int hp, int b, const AdamParams& ap, const float* h, const float* dh, int64_t* steps1,
                              int32_t* tc, float2* bc, float* b1, float* mb1, float* vb1, cudaStream_t s);
 void launch_adam_hidden_bias(int hp, int b, const AdamParams& ap, const float* h, const float* dh, const int32_t* tc,

@@ -751,6 +751,76 @@ void launch_hidden_counts(int hp, int b, const AdamParams& ap, const float* h, c
   SLIDE_LAUNCH_CHECK();
 }
 
+constexpr int kLongChain = 16;
+constexpr int kColGroup = 8;  // pairs per prefetch group of the column path
+
+// One 32-column group of a long W1 row chain: lane = column c.  Pairs in
+// groups of 8; the next group's h / dh / bias corrections are loaded while
+// this group updates.
+__device__ __forceinline__ void adam_feature_column(int hp, const AdamParams& ap, const AdamK& ak, int f, int s0,
+                                                    int len, int c, const int32_t* __restrict__ sorted_k,
+                                                    const int32_t* __restrict__ x_slot,
+                                                    const float* __restrict__ x_val, int64_t x_base,
+                                                    const float* __restrict__ h, const float* __restrict__ dh,
+                                                    const float2* __restrict__ bc, float* __restrict__ w1t,
+                                                    float* __restrict__ m1t, float* __restrict__ v1t,
+                                                    unsigned long long* __restrict__ touched) {
+  const int lane = threadIdx.x & 31;
+  const int64_t ro = (int64_t)f * hp + c;
+  float w = __ldcg(w1t + ro), m = __ldcg(m1t + ro), v = __ldcg(v1t + ro);
+  int moved = 0;
+  for (int c0 = 0; c0 < len; c0 += 32) {
+    const int j = c0 + lane;
+    int slot_l = 0;
+    float xv_l = 0.f;
+    if (j < len) {
+      const int k = sorted_k[s0 + j];
+      slot_l = x_slot[k];
+      xv_l = x_val[x_base + k];
+    }
+    const int nc = min(32, len - c0);
+    float hc[kColGroup], gc[kColGroup], hn[kColGroup], gn[kColGroup];
+    float2 bcc[kColGroup], bn[kColGroup];
+    auto fetch = [&](int g0, float (&hh)[kColGroup], float (&gg)[kColGroup], float2 (&bb)[kColGroup]) {
+#pragma unroll
+      for (int t = 0; t < kColGroup; ++t) {
+        const int slot = __shfl_sync(0xffffffffu, slot_l, (g0 + t) & 31);
+        const int64_t q = (int64_t)slot * hp + c;
+        const bool ok = g0 + t < nc;
+        hh[t] = ok ? __ldg(h + q) : 0.f;
+        gg[t] = ok ? __ldg(dh + q) : 0.f;
+        bb[t] = ok ? __ldg(bc + q) : make_float2(0.f, 1.f);
+      }
+    };
+    fetch(0, hc, gc, bcc);
+    for (int g0 = 0; g0 < nc; g0 += kColGroup) {
+      if (g0 + kColGroup < nc) fetch(g0 + kColGroup, hn, gn, bn);
+#pragma unroll
+      for (int t = 0; t < kColGroup; ++t) {  // predicated, no branch: the 8 updates interleave
+        const float xv = __shfl_sync(0xffffffffu, xv_l, (g0 + t) & 31);
+        const bool on = hc[t] > 0.f;  // padding pairs carry h = 0
+        adam_coord_if(on, w, m, v, gc[t] * xv, bcc[t].x, bcc[t].y, ak);
+        moved |= on;
+      }
+#pragma unroll
+      for (int t = 0; t < kColGroup; ++t) {
+        hc[t] = hn[t];
+        gc[t] = gn[t];
+        bcc[t] = bn[t];
+      }
+    }
+  }
+  if (c < hp) {
+    w1t[ro] = w;
+    m1t[ro] = m;
+    v1t[ro] = v;
+  }
+  if (touched) {
+    const int tcnt = __popc(__ballot_sync(0xffffffffu, moved != 0));
+    if (lane == 0) atomicAdd(touched, (unsigned long long)tcnt);
+  }
+}
+
 template <int NV>
 __global__ void __launch_bounds__(256) adam_features_kernel(
     int hp, AdamParams ap, const int32_t* __restrict__ n_uniq, const int32_t* __restrict__ uniq,
@@ -758,16 +828,23 @@ __global__ void __launch_bounds__(256) adam_features_kernel(
     const int32_t* __restrict__ x_slot, const float* __restrict__ x_val, int64_t x_base,
     const float* __restrict__ h, const float* __restrict__ dh, const float2* __restrict__ bc,
     float* __restrict__ w1t, float* __restrict__ m1t, float* __restrict__ v1t,
-    unsigned long long* __restrict__ touched) {
+    unsigned long long* __restrict__ touched, int32_t* __restrict__ long_list, int32_t* __restrict__ n_long) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nu = *n_uniq;
   const AdamK ak(ap);
+  // a long chain (a hot feature held by many samples) goes to the column
+  // kernel: appended to long_list here
   for (int64_t u = gw; u < nu; u += nw) {
+    const int len = seg_cnt[u];
+    if (len > kLongChain) {
+      if (lane == 0) long_list[atomicAdd(n_long, 1)] = (int32_t)u;
+      continue;
+    }
     uint32_t tmask = 0;
     const int f = uniq[u];
-    const int s0 = seg_off[u], len = seg_cnt[u];
+    const int s0 = seg_off[u];
     float* wr = w1t + (int64_t)f * hp + lane * 4;
     float* mr = m1t + (int64_t)f * hp + lane * 4;
     float* vr = v1t + (int64_t)f * hp + lane * 4;
@@ -843,16 +920,45 @@ __global__ void __launch_bounds__(256) adam_features_kernel(
   }
 }
 
+// long chains: work item (list entry, 32-column group)
+__global__ void __launch_bounds__(256) adam_features_long_kernel(
+    int hp, AdamParams ap, const int32_t* __restrict__ long_list, const int32_t* __restrict__ n_long,
+    const int32_t* __restrict__ uniq, const int32_t* __restrict__ seg_off, const int32_t* __restrict__ seg_cnt,
+    const int32_t* __restrict__ sorted_k, const int32_t* __restrict__ x_slot, const float* __restrict__ x_val,
+    int64_t x_base, const float* __restrict__ h, const float* __restrict__ dh, const float2* __restrict__ bc,
+    float* __restrict__ w1t, float* __restrict__ m1t, float* __restrict__ v1t,
+    unsigned long long* __restrict__ touched) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int G = hp / 32;
+  const int64_t items = (int64_t)*n_long * G;
+  const AdamK ak(ap);
+  for (int64_t item = gw; item < items; item += nw) {
+    const int u = long_list[item / G];
+    const int grp = (int)(item % G);
+    adam_feature_column(hp, ap, ak, uniq[u], seg_off[u], seg_cnt[u], grp * 32 + lane, sorted_k, x_slot, x_val,
+                        x_base, h, dh, bc, w1t, m1t, v1t, touched);
+  }
+}
+
 void launch_adam_features(int hp, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq,
                           const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
                           const int32_t* sorted_k, const int32_t* x_slot, const float* x_val, int64_t x_base,
                           const float* h, const float* dh, const float2* bc, float* w1t, float* m1t, float* v1t,
-                          unsigned long long* touched, cudaStream_t s) {
+                          unsigned long long* touched, int32_t* long_list, int32_t* n_long, cudaStream_t s) {
   if (max_uniq <= 0) return;
+  SLIDE_CUDA(cudaMemsetAsync(n_long, 0, 4, s));
   int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * 16);
   SLIDE_NV_DISPATCH(hp, (adam_features_kernel<NV><<<grid, 256, 0, s>>>(hp, ap, n_uniq, uniq, seg_off, seg_cnt,
                                                                         sorted_k, x_slot, x_val, x_base, h, dh, bc,
-                                                                        w1t, m1t, v1t, touched)));
+                                                                        w1t, m1t, v1t, touched, long_list, n_long)));
+  SLIDE_LAUNCH_CHECK();
+  // long chains: at most max_uniq * (1 / (kLongChain + 1)) of them
+  const int64_t max_long = std::min<int64_t>(max_uniq, ceil_div(max_uniq, kLongChain)) * (hp / 32);
+  const int lgrid = (int)std::min<int64_t>(std::max<int64_t>(ceil_div(max_long, 8), 1), (int64_t)kSms * 8);
+  adam_features_long_kernel<<<lgrid, 256, 0, s>>>(hp, ap, long_list, n_long, uniq, seg_off, seg_cnt, sorted_k, x_slot,
+                                                  x_val, x_base, h, dh, bc, w1t, m1t, v1t, touched);
   SLIDE_LAUNCH_CHECK();
 }
 
