@@ -91,7 +91,7 @@ struct slide_ctx {
   DBuf bias_table;
   int64_t bias_n = 0;
   int bias_exact = 1;
-  DBuf xslot, tc, bc, partial, tc_scratch, long_list, n_long;
+  DBuf xslot, tc, bc, partial, tc_scratch, long_list, n_long, work;
   int64_t fb_bitmap_words = 0;
   double* pinned_loss = nullptr;
   int32_t* pinned_cnt = nullptr;
@@ -271,7 +271,7 @@ int slide_destroy(slide_ctx* c) {
     for (DBuf* b : {&c->sh_packed, &c->sh_packed_t, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->qkeys, &c->order,
                     &c->states, &c->act, &c->cnt, &c->empty, &c->offs, &c->prow, &c->pslot, &c->plab, &c->z,
                     &c->prob, &c->delta, &c->loss, &c->dh, &c->fb_ids, &c->fb_scratch, &c->fb_bitmap, &c->xslot,
-                    &c->tc, &c->bc, &c->counters, &c->partial, &c->long_list, &c->n_long, &c->tc_scratch, &c->bias_table, &c->cnt_all})
+                    &c->tc, &c->bc, &c->counters, &c->partial, &c->long_list, &c->n_long, &c->work, &c->tc_scratch, &c->bias_table, &c->cnt_all})
       b->release();
     c->grow.release();
     c->gfeat.release();
@@ -601,7 +601,8 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
   if (P_max > 0) {
     launch_adam_rows(hp, b, ap, gr.n_uniq.as<int32_t>(), gr.u_max, gr.uniq.as<int32_t>(), gr.seg_off.as<int32_t>(),
                      gr.seg_cnt.as<int32_t>(), gr.order.as<int32_t>(), c->pslot.as<int32_t>(), c->delta.as<float>(),
-                     c->h.as<float>(), d.w2, d.m2, d.v2, d.b2, d.mb2, d.vb2, d.steps2, ctr, s);
+                     c->h.as<float>(), d.w2, d.m2, d.v2, d.b2, d.mb2, d.vb2, d.steps2, ctr,
+                     c->work.ensure<int32_t>(4), s);
     c->timer.mark(s, kStAdamRows);
   }
   // W1: group the (feature, slot) inputs by feature

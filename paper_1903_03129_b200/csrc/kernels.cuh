@@ -111,7 +111,7 @@ void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq
                       const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
                       const int32_t* sorted_pairs, const int32_t* pslot, const float* delta, const float* h,
                       float* w2, float* m2, float* v2, float* b2, float* mb2, float* vb2, int64_t* steps2,
-                      unsigned long long* touched, cudaStream_t s);
+                      unsigned long long* touched, int32_t* work, cudaStream_t s);
 void launch_accumulate(unsigned long long* dst, const int32_t* src, cudaStream_t s);
 void launch_x_slots(int b, const int32_t* x_ptr, int32_t* x_slot, cudaStream_t s);
 void launch_hidden_counts(int hp, int b, const AdamParams& ap, const float* h, const int64_t* steps1, int32_t* tc,

@@ -569,18 +569,23 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(int hp, int b, AdamParam
                                                         float* __restrict__ v2, float* __restrict__ b2,
                                                         float* __restrict__ mb2, float* __restrict__ vb2,
                                                         int64_t* __restrict__ steps2,
-                                                        unsigned long long* __restrict__ touched) {
+                                                        unsigned long long* __restrict__ touched,
+                                                        int32_t* __restrict__ work) {
   // per-warp broadcast of the current chunk's pair scalars:
   // (h row offset, e1, e2, c1) and sqrt(c2); h itself is read through L1
   // (64 KB at B = 128: resident; staging it in shared memory cost occupancy)
   __shared__ float4 pq[8][32];
   __shared__ float ps2[8][32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t nu = *n_uniq;
+  const int nu = *n_uniq;
   const AdamK ak(ap);
-  for (int64_t u = gw; u < nu; u += nw) {
+  // persistent warps take rows from a counter: a CTA's slot is never held
+  // by idle warps waiting on one long row
+  for (;;) {
+    int u = 0;
+    if (lane == 0) u = atomicAdd(work, 1);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= nu) break;
     uint32_t tmask = 0;
     const int r = uniq[u];
     const int s0 = seg_off[u], len = seg_cnt[u];
@@ -692,17 +697,20 @@ void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq
                       const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
                       const int32_t* sorted_pairs, const int32_t* pslot, const float* delta, const float* h,
                       float* w2, float* m2, float* v2, float* b2, float* mb2, float* vb2, int64_t* steps2,
-                      unsigned long long* touched, cudaStream_t s) {
+                      unsigned long long* touched, int32_t* work, cudaStream_t s) {
   if (max_uniq <= 0) return;
-  const int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * 16);
+  SLIDE_CUDA(cudaMemsetAsync(work, 0, 4, s));
+  // persistent: as many CTAs as are resident at once
+  const int per_sm = hp <= 128 ? 3 : 2;
+  const int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * per_sm);
   if (touched) {
     SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, true><<<grid, 256, 0, s>>>(hp, b, ap, n_uniq, uniq, seg_off, seg_cnt,
                                                                           sorted_pairs, pslot, delta, h, w2, m2, v2,
-                                                                          b2, mb2, vb2, steps2, touched)));
+                                                                          b2, mb2, vb2, steps2, touched, work)));
   } else {
     SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, false><<<grid, 256, 0, s>>>(hp, b, ap, n_uniq, uniq, seg_off, seg_cnt,
                                                                            sorted_pairs, pslot, delta, h, w2, m2, v2,
-                                                                           b2, mb2, vb2, steps2, touched)));
+                                                                           b2, mb2, vb2, steps2, touched, work)));
   }
   SLIDE_LAUNCH_CHECK();
 }
