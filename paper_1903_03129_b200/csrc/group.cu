@@ -186,6 +186,111 @@ __global__ void g_place_kernel(const int32_t* __restrict__ keys, const int32_t* 
   }
 }
 
+// ---- dense-mask mode: one B-bit slot mask per key of the whole key space
+// (used when K x B bits is small: W2 rows, W1 features at the BASELINE
+// sizes).  mark + mask are one atomicOr pass, the unique-key ranks and the
+// segment offsets come out of one two-value look-back scan over the keys
+// (rank in the high half, pair offset in the low half of the status word),
+// and the masks of the used keys are cleared after the consumers ran.
+__global__ void gd_mask_kernel(const int32_t* __restrict__ keys, const int32_t* __restrict__ slots, const int32_t* n_dev,
+                               int64_t n_host, int wpk, uint32_t* __restrict__ mask, TileCtl next, int64_t next_tiles) {
+  tile_reset(next, next_tiles);
+  const int64_t n = dev_count(n_dev, n_host);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int s = slots[q];
+    atomicOr(&mask[(int64_t)keys[q] * wpk + (s >> 5)], 1u << (s & 31));
+  }
+}
+
+// warp 0 of a tile: publish (rank count, pair count) and resolve the
+// exclusive prefix of both; values packed rank << 31 | pairs (each < 2^31)
+__device__ __forceinline__ unsigned long long tile_lookback2(int tile, unsigned long long agg,
+                                                             unsigned long long* status) {
+  const int lane = threadIdx.x & 31;
+  // flag in the top 2 bits would collide with the values: keep it in a
+  // separate bit pattern -- status = value + 1 (aggregate) or value + 1 with
+  // bit 63 set (inclusive); 0 = not yet published
+  constexpr unsigned long long kInc = 1ull << 63;
+  if (tile == 0) {
+    if (lane == 0) st_release(status, kInc | (agg + 1));
+    return 0;
+  }
+  if (lane == 0) st_release(status + tile, agg + 1);
+  unsigned long long acc = 0;
+  for (int top = tile - 1;;) {
+    const int idx = top - lane;
+    const unsigned long long v = idx >= 0 ? ld_acquire(status + idx) : (kInc | 1ull);
+    const unsigned inc = __ballot_sync(0xffffffffu, (v & kInc) != 0), none = __ballot_sync(0xffffffffu, v == 0);
+    const unsigned need = inc ? (inc & (0u - inc)) * 2u - 1u : 0xffffffffu;
+    if (none & need) continue;
+    unsigned long long x = (need >> lane) & 1u ? ((v & ~kInc) - 1) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    acc += x;
+    if (inc) break;
+    top -= 32;
+  }
+  if (lane == 0) st_release(status + tile, kInc | (acc + agg + 1));
+  return acc;
+}
+
+__global__ void __launch_bounds__(kGT) gd_scan_kernel(int64_t K, int wpk, const uint32_t* __restrict__ mask,
+                                                      int32_t* __restrict__ uniq, int32_t* __restrict__ key_rank,
+                                                      int32_t* __restrict__ seg_off, int32_t* __restrict__ seg_cnt,
+                                                      int32_t* __restrict__ n_uniq, TileCtl tc) {
+  using Scan2 = cub::BlockScan<unsigned long long, kGT>;
+  __shared__ typename Scan2::TempStorage tmp;
+  __shared__ int s_tile;
+  __shared__ unsigned long long s_base;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tc.ctr, 1);
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t key = (int64_t)tile * kGT + threadIdx.x;
+  int c = 0;
+  if (key < K)
+    for (int w = 0; w < wpk; ++w) c += __popc(mask[key * wpk + w]);
+  const unsigned long long mine = c ? ((1ull << 31) | (unsigned long long)c) : 0ull;
+  unsigned long long off, agg;
+  Scan2(tmp).ExclusiveSum(mine, off, agg);
+  if (threadIdx.x < 32) {
+    const unsigned long long base = tile_lookback2(tile, agg, tc.status);
+    if (threadIdx.x == 0) s_base = base;
+  }
+  __syncthreads();
+  const unsigned long long pre = s_base + off;
+  const int r = (int)(pre >> 31), po = (int)(pre & 0x7fffffffull);
+  if (c) {
+    uniq[r] = (int32_t)key;
+    key_rank[key] = r;
+    seg_off[r] = po;
+    seg_cnt[r] = c;
+  }
+  if (key == K - 1) *n_uniq = r + (c ? 1 : 0);
+}
+
+__global__ void gd_place_kernel(const int32_t* __restrict__ keys, const int32_t* __restrict__ slots, const int32_t* n_dev,
+                                int64_t n_host, const int32_t* __restrict__ key_rank, int wpk,
+                                const uint32_t* __restrict__ mask, const int32_t* __restrict__ seg_off,
+                                int32_t* __restrict__ order) {
+  const int64_t n = dev_count(n_dev, n_host);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int key = keys[q];
+    const int s = slots[q];
+    const uint32_t* m = mask + (int64_t)key * wpk;
+    int r = 0;
+    for (int w = 0; w < (s >> 5); ++w) r += __popc(m[w]);
+    r += __popc(m[s >> 5] & ((1u << (s & 31)) - 1u));
+    order[seg_off[key_rank[key]] + r] = (int32_t)q;
+  }
+}
+
+__global__ void gd_clear_kernel(const int32_t* __restrict__ uniq, const int32_t* __restrict__ n_uniq, int wpk,
+                                uint32_t* __restrict__ mask) {
+  const int64_t n = (int64_t)*n_uniq * wpk;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    mask[(int64_t)uniq[q / wpk] * wpk + q % wpk] = 0u;
+}
+
 static int grid_of(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), kSms * 8)); }
 
 void GroupBy::prepare(int64_t key_space, int64_t slots, int64_t items_max) {
@@ -193,6 +298,30 @@ void GroupBy::prepare(int64_t key_space, int64_t slots, int64_t items_max) {
   nwords = ceil_div(key_space, 32);
   wpk = (int)ceil_div(slots, 32);
   u_max = std::min<int64_t>(key_space, std::max<int64_t>(items_max, 1));
+  // dense-mask mode when the whole key space's masks are small (<= 32 MB)
+  // and the scan over the key space is not much longer than the item list
+  dense = key_space * wpk * 4 <= ((int64_t)32 << 20) && key_space <= 4 * std::max<int64_t>(items_max, 1);
+  key_rank.ensure<int32_t>(key_space);
+  uniq.ensure<int32_t>(u_max);
+  seg_cnt.ensure<int32_t>(u_max);
+  seg_off.ensure<int32_t>(u_max);
+  n_uniq.ensure<int32_t>(1);
+  order.ensure<int32_t>(std::max<int64_t>(items_max, 1));
+  ctrs.ensure<int32_t>(2);
+  if (dense) {
+    const int64_t need = key_space * wpk;
+    if (mask_words < need || !mask_dense) {
+      uint32_t* m = mask.ensure<uint32_t>(need);
+      SLIDE_CUDA(cudaMemset(m, 0, need * 4));  // kept zero between runs by clear()
+      mask_words = need;
+      mask_dense = true;
+    }
+    tiles_bits = ceil_div(key_space, kGT);
+    tiles_seg = 0;
+    status.ensure<unsigned long long>(tiles_bits);
+    return;
+  }
+  mask_dense = false;
   const int64_t words_pad = ceil_div(nwords, kGT) * kGT;  // whole scan tiles
   if (bits_words < words_pad) {
     uint32_t* b = bits.ensure<uint32_t>(words_pad);
@@ -201,20 +330,26 @@ void GroupBy::prepare(int64_t key_space, int64_t slots, int64_t items_max) {
   }
   const int64_t need_mask = u_max * wpk;
   if (mask_words < need_mask) mask.ensure<uint32_t>(need_mask), mask_words = need_mask;  // rows zeroed on use
-  key_rank.ensure<int32_t>(key_space);
-  uniq.ensure<int32_t>(u_max);
-  seg_cnt.ensure<int32_t>(u_max);
-  seg_off.ensure<int32_t>(u_max);
-  n_uniq.ensure<int32_t>(1);
-  order.ensure<int32_t>(std::max<int64_t>(items_max, 1));
   tiles_bits = words_pad / kGT;
   tiles_seg = ceil_div(u_max, kGT);
   status.ensure<unsigned long long>(tiles_bits + tiles_seg);
-  ctrs.ensure<int32_t>(2);
 }
 
 void GroupBy::run(const int32_t* keys, const int32_t* slots, const int32_t* n_dev, int64_t n_host, int64_t n_max,
                   cudaStream_t s) {
+  if (dense) {
+    const TileCtl t{status.as<unsigned long long>(), ctrs.as<int32_t>()};
+    gd_mask_kernel<<<grid_of(n_max), 256, 0, s>>>(keys, slots, n_dev, n_host, wpk, mask.as<uint32_t>(), t, tiles_bits);
+    SLIDE_LAUNCH_CHECK();
+    gd_scan_kernel<<<(int)tiles_bits, kGT, 0, s>>>(K, wpk, mask.as<uint32_t>(), uniq.as<int32_t>(),
+                                                   key_rank.as<int32_t>(), seg_off.as<int32_t>(),
+                                                   seg_cnt.as<int32_t>(), n_uniq.as<int32_t>(), t);
+    SLIDE_LAUNCH_CHECK();
+    gd_place_kernel<<<grid_of(n_max), 256, 0, s>>>(keys, slots, n_dev, n_host, key_rank.as<int32_t>(), wpk,
+                                                   mask.as<uint32_t>(), seg_off.as<int32_t>(), order.as<int32_t>());
+    SLIDE_LAUNCH_CHECK();
+    return;
+  }
   uint32_t* b = bits.as<uint32_t>();
   const TileCtl t1{status.as<unsigned long long>(), ctrs.as<int32_t>()};
   const TileCtl t2{status.as<unsigned long long>() + tiles_bits, ctrs.as<int32_t>() + 1};
@@ -234,13 +369,21 @@ void GroupBy::run(const int32_t* keys, const int32_t* slots, const int32_t* n_de
   SLIDE_LAUNCH_CHECK();
 }
 
-// Every buffer is reset by the next run itself (bitmap words as they are
-// scanned, mask rows as ranks are assigned, scan status by the kernel before).
-void GroupBy::clear(cudaStream_t) {}
+// Bitmap mode: every buffer is reset by the next run itself (bitmap words as
+// they are scanned, mask rows as ranks are assigned, scan status by the
+// kernel before).  Dense mode: the used keys' masks are zeroed here, after
+// the last consumer.
+void GroupBy::clear(cudaStream_t s) {
+  if (!dense) return;
+  gd_clear_kernel<<<grid_of(u_max * wpk), 256, 0, s>>>(uniq.as<int32_t>(), n_uniq.as<int32_t>(), wpk,
+                                                       mask.as<uint32_t>());
+  SLIDE_LAUNCH_CHECK();
+}
 
 void GroupBy::release() {
   for (DBuf* b : {&bits, &key_rank, &uniq, &seg_cnt, &seg_off, &n_uniq, &mask, &order, &status, &ctrs}) b->release();
   bits_words = mask_words = 0;
+  mask_dense = false;
 }
 
 }  // namespace slide

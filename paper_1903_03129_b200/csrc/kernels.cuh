@@ -65,15 +65,20 @@ void launch_softmax_finish(int b, const int32_t* offs, const uint8_t* plab, cons
 // the group-by result a kernel walks (device pointers)
 struct GroupView {
   const int32_t *n_uniq, *uniq, *seg_off, *seg_cnt, *order;
-  const uint32_t* mask;
+  const uint32_t* mask;  // slot masks: row u (bitmap mode) or row uniq[u] (dense mode)
   int wpk;
   int64_t u_max;
+  int mask_by_key;
+  __device__ __forceinline__ const uint32_t* mask_of(int64_t u) const {
+    return mask + (mask_by_key ? (int64_t)uniq[u] : u) * wpk;
+  }
 };
 
 struct GroupBy {
   DBuf bits, key_rank, uniq, seg_cnt, seg_off, n_uniq, mask, order, status, ctrs;
   int64_t K = 0, nwords = 0, u_max = 0, bits_words = 0, mask_words = 0, tiles_bits = 0, tiles_seg = 0;
   int wpk = 1;
+  bool dense = false, mask_dense = false;  // dense: one mask per key of the whole key space
   void prepare(int64_t key_space, int64_t slots, int64_t items_max);
   // items q < n (n = *n_dev if given, else n_host), keys[q] / slots[q]
   void run(const int32_t* keys, const int32_t* slots, const int32_t* n_dev, int64_t n_host, int64_t n_max,
@@ -82,7 +87,7 @@ struct GroupBy {
   void release();
   GroupView view() {
     return GroupView{n_uniq.as<int32_t>(), uniq.as<int32_t>(), seg_off.as<int32_t>(), seg_cnt.as<int32_t>(),
-                     order.as<int32_t>(), mask.as<uint32_t>(), wpk, u_max};
+                     order.as<int32_t>(), mask.as<uint32_t>(), wpk, u_max, dense ? 1 : 0};
   }
 };
 

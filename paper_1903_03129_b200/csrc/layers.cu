@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(256, 2) logits_tiles_kernel(int hp, int b, Gro
     if (!tile_is_dense(g, u0, nrow, b)) continue;  // sparse tile: logits_rows_kernel
     if (tid < nrow) {
       const int64_t u = u0 + tid;
-      const uint32_t* mrow = g.mask + u * g.wpk;
+      const uint32_t* mrow = g.mask_of(u);
       int run = 0;
       for (int w = 0; w < g.wpk; ++w) {
         cum[tid * kMaskWords + w] = run;
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(256, 2) logits_tiles_kernel(int hp, int b, Gro
     for (int j = 0; j < 4; ++j) {
       const int row = ty + 16 * j;
       if (row >= nrow) continue;
-      const uint32_t* mrow = g.mask + (u0 + row) * g.wpk;
+      const uint32_t* mrow = g.mask_of(u0 + row);
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
         const int i = s0 + tx + 16 * jj;
