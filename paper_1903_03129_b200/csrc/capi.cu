@@ -58,6 +58,11 @@ struct slide_ctx {
   int64_t host_counts[8] = {0};  // 0 pairs, 1 nnz, 2 samples, 3 rebuilds, 4 fallback slots
   slide_net_desc d{};
   cudaStream_t s = nullptr;
+  // side stream of the backward pass (W1 grouping and W1 Adam run beside
+  // the W2 path); forked from and joined back into `s` with events, so a
+  // captured step is one graph with two branches
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_dh = nullptr, ev_join = nullptr;
   int hp = 0;
   TablesHost tab;
   DBuf sh_packed, sh_packed_t, dw_perms, dw_donors, rowkeys;
@@ -275,6 +280,10 @@ int slide_destroy(slide_ctx* c) {
       b->release();
     c->grow.release();
     c->gfeat.release();
+    if (c->s2) cudaStreamSynchronize(c->s2);
+    for (cudaEvent_t e : {c->ev_fork, c->ev_dh, c->ev_join})
+      if (e) cudaEventDestroy(e);
+    if (c->s2) cudaStreamDestroy(c->s2);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     if (c->graph) cudaGraphDestroy(c->graph);
     for (DBuf* b : {&c->iter_dev, &c->gx_ptr, &c->gx_idx, &c->gx_val, &c->gy_ptr, &c->gy_idx}) b->release();
@@ -578,6 +587,13 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
 
 // ext_dh: the hidden gradient already computed (sharded step: all-reduced
 // partials); otherwise it is computed here from this context's W2.
+static void side_stream_init(slide_ctx* c) {
+  if (c->s2) return;
+  SLIDE_CUDA(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&c->ev_fork, &c->ev_dh, &c->ev_join})
+    SLIDE_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+}
+
 static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nullptr) {
   SLIDE_CHECK(c->have_forward, kValueError, "backward needs a forward first");
   const slide_net_desc& d = c->d;
@@ -585,6 +601,28 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
   const int64_t P_max = c->last_Pmax;
   cudaStream_t s = c->s;
   GroupBy& gr = c->grow;
+  GroupBy& gf = c->gfeat;
+  const int64_t nnz = c->last_nnz;
+  // W1 branch on the side stream: its grouping needs only the inputs, its
+  // Adam only dh -- both overlap the hidden gradient and the W2 Adam.  The
+  // profiled pass keeps one stream so the stage timers stay serial.
+  const bool fork = update && !c->timer.on;
+  cudaStream_t sw = s;
+  if (fork) {
+    side_stream_init(c);
+    sw = c->s2;
+    SLIDE_CUDA(cudaEventRecord(c->ev_fork, s));
+    SLIDE_CUDA(cudaStreamWaitEvent(sw, c->ev_fork, 0));
+  }
+  int32_t* xs = nnz > 0 ? c->xslot.ensure<int32_t>(nnz) : nullptr;
+  if (nnz > 0) gf.prepare(d.input_dim, b, nnz);  // host-side sizing before any branch launches
+  auto group_features = [&](cudaStream_t st) {
+    if (nnz <= 0) return;
+    launch_x_slots(b, c->last_xptr, xs, st);
+    // static shapes: nnz is a capacity, the live count is x_ptr[b] (x_ptr[0] = 0)
+    gf.run(c->last_xidx + c->last_xbase, xs, c->st_active ? c->last_xptr + b : nullptr, nnz, nnz, st);
+  };
+  if (fork) group_features(sw);
   const float* dh = ext_dh;
   if (!dh) {
     float* out = c->dh.ensure<float>((size_t)b * hp);
@@ -597,36 +635,41 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
   if (!update) return;
   const AdamParams ap = adam_of(c);
   unsigned long long* ctr = c->timer.on ? c->counters.as<unsigned long long>() : nullptr;
+  int32_t* tc = c->tc.ensure<int32_t>((size_t)b * hp);
+  float2* bc = c->bc.ensure<float2>((size_t)b * hp);
+  int32_t* work = c->work.ensure<int32_t>(4);
+  int32_t* long_list = c->long_list.ensure<int32_t>(std::max<int64_t>(gf.u_max, 1));
+  int32_t* n_long = c->n_long.ensure<int32_t>(1);
+  // W1 branch: per-unit step counts + bias corrections and the hidden biases
+  // (one fused pass), then the W1 Adam over the feature grouping
+  auto w1_update = [&](cudaStream_t st) {
+    launch_hidden_prep_bias(hp, b, ap, c->h.as<float>(), dh, d.steps1, tc, bc, d.b1, d.mb1, d.vb1, st);
+    c->timer.mark(st, kStHiddenCounts);
+    if (nnz <= 0) return;
+    if (!fork) {
+      group_features(st);
+      c->timer.mark(st, kStGroupFeat);
+    }
+    launch_adam_features(hp, ap, gf.n_uniq.as<int32_t>(), gf.u_max, gf.uniq.as<int32_t>(), gf.seg_off.as<int32_t>(),
+                         gf.seg_cnt.as<int32_t>(), gf.order.as<int32_t>(), xs, c->last_xval, c->last_xbase,
+                         c->h.as<float>(), dh, bc, d.w1t, d.m1t, d.v1t, ctr ? ctr + 1 : nullptr, long_list, n_long,
+                         st);
+    c->timer.mark(st, kStAdamFeat);
+    gf.clear(st);
+  };
+  if (fork) {
+    SLIDE_CUDA(cudaEventRecord(c->ev_dh, s));
+    SLIDE_CUDA(cudaStreamWaitEvent(sw, c->ev_dh, 0));
+    w1_update(sw);
+  }
   // W2: rows in ascending order, each row's samples in slot order
   if (P_max > 0) {
     launch_adam_rows(hp, b, ap, gr.n_uniq.as<int32_t>(), gr.u_max, gr.uniq.as<int32_t>(), gr.seg_off.as<int32_t>(),
                      gr.seg_cnt.as<int32_t>(), gr.order.as<int32_t>(), c->pslot.as<int32_t>(), c->delta.as<float>(),
-                     c->h.as<float>(), d.w2, d.m2, d.v2, d.b2, d.mb2, d.vb2, d.steps2, ctr,
-                     c->work.ensure<int32_t>(4), s);
+                     c->h.as<float>(), d.w2, d.m2, d.v2, d.b2, d.mb2, d.vb2, d.steps2, ctr, work, s);
     c->timer.mark(s, kStAdamRows);
   }
-  // W1: group the (feature, slot) inputs by feature
-  int32_t* tc = c->tc.ensure<int32_t>((size_t)b * hp);
-  float2* bc = c->bc.ensure<float2>((size_t)b * hp);
-  // per-unit step counts + bias corrections for the W1 Adam, and the hidden
-  // biases themselves (one fused pass)
-  launch_hidden_prep_bias(hp, b, ap, c->h.as<float>(), dh, d.steps1, tc, bc, d.b1, d.mb1, d.vb1, s);
-  c->timer.mark(s, kStHiddenCounts);
-  const int64_t nnz = c->last_nnz;
-  GroupBy& gf = c->gfeat;
-  if (nnz > 0) {
-    int32_t* xs = c->xslot.ensure<int32_t>(nnz);
-    launch_x_slots(b, c->last_xptr, xs, s);
-    gf.prepare(d.input_dim, b, nnz);
-    // static shapes: nnz is a capacity, the live count is x_ptr[b] (x_ptr[0] = 0)
-    gf.run(c->last_xidx + c->last_xbase, xs, c->st_active ? c->last_xptr + b : nullptr, nnz, nnz, s);
-    c->timer.mark(s, kStGroupFeat);
-    launch_adam_features(hp, ap, gf.n_uniq.as<int32_t>(), gf.u_max, gf.uniq.as<int32_t>(), gf.seg_off.as<int32_t>(),
-                         gf.seg_cnt.as<int32_t>(), gf.order.as<int32_t>(), xs, c->last_xval, c->last_xbase,
-                         c->h.as<float>(), dh, bc, d.w1t, d.m1t, d.v1t, ctr ? ctr + 1 : nullptr,
-                         c->long_list.ensure<int32_t>(std::max<int64_t>(gf.u_max, 1)), c->n_long.ensure<int32_t>(1), s);
-    c->timer.mark(s, kStAdamFeat);
-  }
+  if (!fork) w1_update(s);
   c->timer.mark(s, kStHiddenBias);
   if (ctr) {
     launch_accumulate(ctr + 2, P_max > 0 ? gr.n_uniq.as<int32_t>() : nullptr, s);
@@ -637,7 +680,10 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
     gr.clear(s);
     c->grow_pending = false;
   }
-  if (nnz > 0) gf.clear(s);
+  if (fork) {  // join: the next step reads W1, h and the side stream's buffers
+    SLIDE_CUDA(cudaEventRecord(c->ev_join, sw));
+    SLIDE_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+  }
 }
 
 int slide_forward(slide_ctx* c, const slide_batch* bt, int64_t iteration, int64_t slot_offset, int64_t* n_pairs) {
@@ -712,7 +758,11 @@ int slide_graph_step(slide_ctx* c, const slide_batch* bt, int64_t iteration, dou
     }
     auto& st = c->st;
     if (!st.on || st.batch != B || nnz > st.nnz_cap || max_lab > st.lab_cap || nlab > st.ylab_cap) {
-      if (c->gexec) cudaGraphExecDestroy(c->gexec);
+      if (c->s2) cudaStreamSynchronize(c->s2);
+    for (cudaEvent_t e : {c->ev_fork, c->ev_dh, c->ev_join})
+      if (e) cudaEventDestroy(e);
+    if (c->s2) cudaStreamDestroy(c->s2);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
       if (c->graph) cudaGraphDestroy(c->graph);
       c->gexec = nullptr;
       c->graph = nullptr;
