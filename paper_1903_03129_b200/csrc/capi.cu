@@ -62,7 +62,10 @@ struct slide_ctx {
   // the W2 path); forked from and joined back into `s` with events, so a
   // captured step is one graph with two branches
   cudaStream_t s2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_dh = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_dh = nullptr, ev_join = nullptr, ev_pre = nullptr;
+  // set by the fused step callers: forward already queues the W1 grouping
+  // on the side stream (it needs only the inputs)
+  bool w1_prefork = false, w1_grouped = false;
   int hp = 0;
   TablesHost tab;
   DBuf sh_packed, sh_packed_t, dw_perms, dw_donors, rowkeys;
@@ -281,7 +284,7 @@ int slide_destroy(slide_ctx* c) {
     c->grow.release();
     c->gfeat.release();
     if (c->s2) cudaStreamSynchronize(c->s2);
-    for (cudaEvent_t e : {c->ev_fork, c->ev_dh, c->ev_join})
+    for (cudaEvent_t e : {c->ev_fork, c->ev_dh, c->ev_join, c->ev_pre})
       if (e) cudaEventDestroy(e);
     if (c->s2) cudaStreamDestroy(c->s2);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
@@ -422,6 +425,13 @@ int slide_tables_probe(slide_ctx* c, const uint32_t* keys, int64_t b, int32_t* s
 }
 
 // --------------------------------------------------------------------- step
+static void side_stream_init(slide_ctx* c) {
+  if (c->s2) return;
+  SLIDE_CUDA(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&c->ev_fork, &c->ev_dh, &c->ev_join, &c->ev_pre})
+    SLIDE_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+}
+
 static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration, int64_t slot_offset,
                          int64_t* n_pairs) {
   const slide_net_desc& d = c->d;
@@ -446,6 +456,20 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     c->host_counts[1] += nnz;
   }
   const int64_t* iter_dev = stat ? c->iter_dev.as<int64_t>() : nullptr;
+
+  // fused step: the W1 feature grouping needs only the inputs -- queue it on
+  // the side stream now, beside the whole forward pass (backward joins it)
+  c->w1_grouped = false;
+  if (c->w1_prefork && !c->timer.on && nnz > 0) {
+    side_stream_init(c);
+    SLIDE_CUDA(cudaEventRecord(c->ev_pre, s));
+    SLIDE_CUDA(cudaStreamWaitEvent(c->s2, c->ev_pre, 0));
+    int32_t* xs = c->xslot.ensure<int32_t>(nnz);
+    c->gfeat.prepare(d.input_dim, b, nnz);
+    launch_x_slots(b, bt->x_ptr, xs, c->s2);
+    c->gfeat.run(bt->x_idx + x_base, xs, stat ? bt->x_ptr + b : nullptr, nnz, nnz, c->s2);
+    c->w1_grouped = true;
+  }
 
   float* h = c->h.ensure<float>((size_t)b * hp);
   c->timer.mark(s, kStStart);
@@ -587,13 +611,6 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
 
 // ext_dh: the hidden gradient already computed (sharded step: all-reduced
 // partials); otherwise it is computed here from this context's W2.
-static void side_stream_init(slide_ctx* c) {
-  if (c->s2) return;
-  SLIDE_CUDA(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
-  for (cudaEvent_t* e : {&c->ev_fork, &c->ev_dh, &c->ev_join})
-    SLIDE_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-}
-
 static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nullptr) {
   SLIDE_CHECK(c->have_forward, kValueError, "backward needs a forward first");
   const slide_net_desc& d = c->d;
@@ -622,7 +639,7 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
     // static shapes: nnz is a capacity, the live count is x_ptr[b] (x_ptr[0] = 0)
     gf.run(c->last_xidx + c->last_xbase, xs, c->st_active ? c->last_xptr + b : nullptr, nnz, nnz, st);
   };
-  if (fork) group_features(sw);
+  if (fork && !c->w1_grouped) group_features(sw);
   const float* dh = ext_dh;
   if (!dh) {
     float* out = c->dh.ensure<float>((size_t)b * hp);
@@ -632,7 +649,15 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
     dh = out;
   }
   c->timer.mark(s, kStHiddenGrad);
-  if (!update) return;
+  if (!update) {
+    if (c->w1_grouped) {  // a pre-forked grouping must still be joined
+      side_stream_init(c);
+      SLIDE_CUDA(cudaEventRecord(c->ev_join, c->s2));
+      SLIDE_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+      c->w1_grouped = false;
+    }
+    return;
+  }
   const AdamParams ap = adam_of(c);
   unsigned long long* ctr = c->timer.on ? c->counters.as<unsigned long long>() : nullptr;
   int32_t* tc = c->tc.ensure<int32_t>((size_t)b * hp);
@@ -650,6 +675,7 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
       group_features(st);
       c->timer.mark(st, kStGroupFeat);
     }
+    c->w1_grouped = false;
     launch_adam_features(hp, ap, gf.n_uniq.as<int32_t>(), gf.u_max, gf.uniq.as<int32_t>(), gf.seg_off.as<int32_t>(),
                          gf.seg_cnt.as<int32_t>(), gf.order.as<int32_t>(), xs, c->last_xval, c->last_xbase,
                          c->h.as<float>(), dh, bc, d.w1t, d.m1t, d.v1t, ctr ? ctr + 1 : nullptr, long_list, n_long,
@@ -721,7 +747,9 @@ int slide_train_batch(slide_ctx* c, const slide_batch* bt, int64_t iteration, in
         v.forced_ptr = bt->forced_ptr + s0;
         v.forced_ptr_host = bt->forced_ptr_host + s0;
       }
+      c->w1_prefork = true;
       forward_impl(c, &v, iteration, s0, nullptr);
+      c->w1_prefork = false;
       backward_impl(c, 1);
       // results ride back asynchronously; one host sync per call
       SLIDE_CUDA(cudaMemcpyAsync(c->pinned_loss + s0, c->loss.p, nb * 8, cudaMemcpyDeviceToHost, c->s));
@@ -759,7 +787,7 @@ int slide_graph_step(slide_ctx* c, const slide_batch* bt, int64_t iteration, dou
     auto& st = c->st;
     if (!st.on || st.batch != B || nnz > st.nnz_cap || max_lab > st.lab_cap || nlab > st.ylab_cap) {
       if (c->s2) cudaStreamSynchronize(c->s2);
-    for (cudaEvent_t e : {c->ev_fork, c->ev_dh, c->ev_join})
+    for (cudaEvent_t e : {c->ev_fork, c->ev_dh, c->ev_join, c->ev_pre})
       if (e) cudaEventDestroy(e);
     if (c->s2) cudaStreamDestroy(c->s2);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
@@ -820,7 +848,9 @@ int slide_graph_step(slide_ctx* c, const slide_batch* bt, int64_t iteration, dou
       }
       if (c->graph_state < 2) c->timer.on = c->graph_state == 0 && timing;
       if (c->graph_state == 0) {
+        c->w1_prefork = true;
         forward_impl(c, &v, iteration, 0, nullptr);
+        c->w1_prefork = false;
         backward_impl(c, 1);
         c->graph_state = 1;
       } else if (c->graph_state == 1) {
@@ -828,9 +858,12 @@ int slide_graph_step(slide_ctx* c, const slide_batch* bt, int64_t iteration, dou
         const unsigned long long lc0 = g_slide_launches;
         SLIDE_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
         try {
+          c->w1_prefork = true;
           forward_impl(c, &v, iteration, 0, nullptr);
+          c->w1_prefork = false;
           backward_impl(c, 1);
         } catch (...) {
+          c->w1_prefork = false;
           cudaGraph_t g;
           cudaStreamEndCapture(gs, &g);
           if (g) cudaGraphDestroy(g);
