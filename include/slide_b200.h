@@ -162,6 +162,12 @@ int slide_graph_step(slide_ctx* ctx, const slide_batch* batch, int64_t iteration
  * 10 rng states (B, 6) u64 | 11 logits (P) f32 (before softmax) |
  * 12 global active-set size per slot (B) i32 */
 int slide_read(slide_ctx* ctx, int64_t what, void* host_dst, int64_t max_bytes, int64_t* bytes);
+
+/* Ranked sampled inference for the last forward (reference network.py:383-391,
+ * estimator.py:203-223): per slot the k best active ids by probability,
+ * ties to the lower id (np.argsort(-p, kind="stable")), -1 padded; counts =
+ * min(k, |A_i|).  ids_out: host (B x k) int32, counts_out: host (B) int32. */
+int slide_topk(slide_ctx* ctx, int64_t k, int32_t* ids_out, int32_t* counts_out);
 /* overwrite stage 0 (h) or 6 (delta) of the last forward with host values
  * (exact size): backward(trace) replays a trace's forward-time activations
  * and errors, as the reference's backward reads them from the trace

@@ -99,7 +99,7 @@ struct slide_ctx {
   DBuf bias_table;
   int64_t bias_n = 0;
   int bias_exact = 1;
-  DBuf xslot, tc, bc, partial, tc_scratch, long_list, n_long, work;
+  DBuf xslot, tc, bc, partial, tc_scratch, long_list, n_long, work, topk_out, topk_cnt;
   int64_t fb_bitmap_words = 0;
   double* pinned_loss = nullptr;
   int32_t* pinned_cnt = nullptr;
@@ -279,7 +279,7 @@ int slide_destroy(slide_ctx* c) {
     for (DBuf* b : {&c->sh_packed, &c->sh_packed_t, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->qkeys, &c->order,
                     &c->states, &c->act, &c->cnt, &c->empty, &c->offs, &c->prow, &c->pslot, &c->plab, &c->z,
                     &c->prob, &c->delta, &c->loss, &c->dh, &c->fb_ids, &c->fb_scratch, &c->fb_bitmap, &c->xslot,
-                    &c->tc, &c->bc, &c->counters, &c->partial, &c->long_list, &c->n_long, &c->work, &c->tc_scratch, &c->bias_table, &c->cnt_all})
+                    &c->tc, &c->bc, &c->counters, &c->partial, &c->long_list, &c->n_long, &c->work, &c->topk_out, &c->topk_cnt, &c->tc_scratch, &c->bias_table, &c->cnt_all})
       b->release();
     c->grow.release();
     c->gfeat.release();
@@ -947,6 +947,22 @@ int slide_read(slide_ctx* c, int64_t what, void* dst, int64_t max_bytes, int64_t
     if (n) SLIDE_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, c->s));
     SLIDE_CUDA(cudaStreamSynchronize(c->s));
     if (bytes) *bytes = n;
+  });
+}
+
+int slide_topk(slide_ctx* c, int64_t k, int32_t* ids_out, int32_t* counts_out) {
+  return guarded([&] {
+    SLIDE_CHECK(c->have_forward, kValueError, "ranking needs a forward first");
+    SLIDE_CHECK(k >= 1 && k <= 4096, kValueError, "k must be in 1..4096");
+    SLIDE_CHECK(c->G == 1, kNotSupported, "ranking a sharded layer needs the gathered probabilities");
+    const int b = c->last_b;
+    int32_t* out = c->topk_out.ensure<int32_t>((size_t)b * k);
+    int32_t* cnt = c->topk_cnt.ensure<int32_t>(b);
+    launch_topk(b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->G, c->g, c->prob.as<float>(), (int)k, out, cnt,
+                c->s);
+    SLIDE_CUDA(cudaMemcpyAsync(ids_out, out, (size_t)b * k * 4, cudaMemcpyDeviceToHost, c->s));
+    SLIDE_CUDA(cudaMemcpyAsync(counts_out, cnt, (size_t)b * 4, cudaMemcpyDeviceToHost, c->s));
+    SLIDE_CUDA(cudaStreamSynchronize(c->s));
   });
 }
 

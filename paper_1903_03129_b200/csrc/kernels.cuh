@@ -118,6 +118,9 @@ void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq
                       float* w2, float* m2, float* v2, float* b2, float* mb2, float* vb2, int64_t* steps2,
                       unsigned long long* touched, int32_t* work, cudaStream_t s);
 void launch_accumulate(unsigned long long* dst, const int32_t* src, cudaStream_t s);
+// per slot: the k best active ids by probability (ties: lower id), -1 padded
+void launch_topk(int b, const int32_t* offs, const int32_t* rows, int shard_count, int shard_rank, const float* prob,
+                 int k, int32_t* out, int32_t* cnt, cudaStream_t s);
 void launch_x_slots(int b, const int32_t* x_ptr, int32_t* x_slot, cudaStream_t s);
 void launch_hidden_counts(int hp, int b, const AdamParams& ap, const float* h, const int64_t* steps1, int32_t* tc,
                           float2* bc, cudaStream_t s);

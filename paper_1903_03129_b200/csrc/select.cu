@@ -544,3 +544,61 @@ void launch_own_filter(int b, int32_t* act, int64_t cap_max, int g, int G, int32
 }
 
 }  // namespace slide
+
+namespace slide {
+
+// ----------------------------------------------------------- ranked top-k
+// Sampled inference ranking (network.py:383-391): per slot, the active ids
+// (ascending) ordered by descending probability, ties to the earlier (lower)
+// id -- np.argsort(-p, kind="stable") -- truncated to k.  One CTA per slot,
+// k rounds of a block argmax over (p, -position).
+constexpr int kTopThreads = 256;
+
+__global__ void __launch_bounds__(kTopThreads) topk_kernel(const int32_t* __restrict__ offs,
+                                                          const int32_t* __restrict__ rows, int shard_count,
+                                                          int shard_rank, const float* __restrict__ prob, int k,
+                                                          int32_t* __restrict__ out, int32_t* __restrict__ cnt_out) {
+  using Red = cub::BlockReduce<unsigned long long, kTopThreads>;
+  __shared__ typename Red::TempStorage tmp;
+  __shared__ unsigned long long s_best;
+  const int i = blockIdx.x;
+  const int o = offs[i], n = offs[i + 1] - o;
+  const int kk = min(k, n);
+  int prev = -1;  // position taken in the previous round
+  float prev_p = 0.f;
+  for (int r = 0; r < kk; ++r) {
+    // key: p (non-negative, so its bits order like the float) high, then
+    // the complement of the position (earlier wins ties); positions already
+    // taken are excluded by (p, position) <= (prev_p, prev) ordering
+    unsigned long long best = 0ull;
+    for (int q = threadIdx.x; q < n; q += kTopThreads) {
+      const float p = prob[o + q];
+      const bool after = r == 0 || p < prev_p || (p == prev_p && q > prev);
+      if (!after) continue;
+      const unsigned long long key = ((unsigned long long)__float_as_uint(p) << 32) | (uint32_t)(0x7fffffff - q);
+      best = key > best ? key : best;
+    }
+    best = Red(tmp).Reduce(best, cub::Max());
+    if (threadIdx.x == 0) s_best = best;
+    __syncthreads();
+    const unsigned long long b = s_best;
+    prev = 0x7fffffff - (int)(uint32_t)b;
+    prev_p = __uint_as_float((uint32_t)(b >> 32));
+    if (threadIdx.x == 0) {
+      const int row = rows[o + prev];
+      out[(int64_t)i * k + r] = row * shard_count + shard_rank;  // global id
+    }
+    __syncthreads();
+  }
+  for (int r = kk + threadIdx.x; r < k; r += kTopThreads) out[(int64_t)i * k + r] = -1;
+  if (threadIdx.x == 0) cnt_out[i] = kk;
+}
+
+void launch_topk(int b, const int32_t* offs, const int32_t* rows, int shard_count, int shard_rank, const float* prob,
+                 int k, int32_t* out, int32_t* cnt, cudaStream_t s) {
+  if (b <= 0 || k <= 0) return;
+  topk_kernel<<<b, kTopThreads, 0, s>>>(offs, rows, shard_count, shard_rank, prob, k, out, cnt);
+  SLIDE_LAUNCH_CHECK();
+}
+
+}  // namespace slide

@@ -99,6 +99,16 @@ def batches(n_examples: int, batch_size: int, seed):
         yield order[lo : lo + batch_size]
 
 
+def score_precision_at_k(net, examples, k: int = 1, seed: int = 0) -> float:
+    """Mean P@k over (x, labels) examples, ranked on the device with one
+    ``default_rng(seed)`` shared across the queries in order -- the
+    evaluator's semantics (reference estimator.py:203-223, ``score``; the
+    facade's l2 normalisation of inputs is the caller's)."""
+    rng = np.random.default_rng(seed)
+    ranked = net.predict_batch([x for x, _ in examples], topn=k, rng=rng)
+    return float(np.mean([precision_at_k(r, y, k) for r, (_, y) in zip(ranked, examples)])) if examples else 0.0
+
+
 def precision_at_k(ranked, truth, k: int) -> float:
     """|top-k of ranked that are true| / k; an empty ranking scores 0
     (reference data.py:126-133)."""

@@ -446,7 +446,7 @@ class SlideNetwork:
 
         def up(a, dt):
             # stage through a pinned host buffer so the copy is a true async DMA
-            a = np.ascontiguousarray(a, dtype=dt)
+            a = np.ascontiguousarray(a, dtype=dt).reshape(-1)
             key = (len(self._pinned), a.dtype.str)
             key = next((k for k in self._pinned if k[1] == a.dtype.str and k not in used), key)
             buf = self._pinned.get(key)
@@ -698,6 +698,66 @@ class SlideNetwork:
         trace = self.forward(x, 0, labels=None, rng=rng, forced_active=forced)
         order = np.argsort(-trace.probs, kind="stable")
         return trace.active[-1][order]
+
+    def predict_batch(self, xs, topn: int = 5, rng=None, sampled: bool = True) -> list:
+        """Ranked label ids (best first, at most ``topn``) for many inputs,
+        equal to ``[self.predict(x, rng=rng)[:topn] for x in xs]`` with one
+        generator shared across the queries in order -- the evaluator's
+        semantics (reference estimator.py:203-207) -- but ``batch_size``
+        queries per device pass.
+
+        The generator's draws depend on the data only through whether a
+        query's sampled set is empty (then ``choice(N, beta)`` follows its
+        probe ``permutation(L)``), and emptiness does not depend on the probe
+        order.  So each chunk runs twice: a first pass yields the empty
+        flags, the host advances the caller's generator through exactly the
+        reference's draws recording each query's starting state, and the
+        second pass replays every slot from its own state; the device then
+        ranks each slot (``slide_topk``)."""
+        check_positive_int(topn, "topn")
+        xs = list(xs)
+        for x in xs:
+            if x.dim != self.input_dim:
+                raise ValueError(f"input dim {x.dim} != network input dim {self.input_dim}")
+        if rng is None:
+            rng = np.random.default_rng(0)
+        lsh = self.layers[1].lsh
+        cfg = self.layers[1].sampler_cfg
+        out = []
+        B = self.cfg.batch_size
+        for lo in range(0, len(xs), B):
+            chunk = xs[lo : lo + B]
+            nb = len(chunk)
+            csr = csr_from_batch([(x, []) for x in chunk], self.input_dim, self.n_out)
+            forced = None
+            states = None
+            if not sampled or lsh is None:
+                forced = (np.arange(nb + 1, dtype=np.int64) * self.n_out,
+                          np.tile(np.arange(self.n_out, dtype=np.int32), nb))
+            else:
+                lsh.sync_to_device()
+                # any valid generator state will do for the emptiness pass (an
+                # all-zero PCG64 state would never leave numpy's rejection loops)
+                probe = np.tile(_lib.pcg64_state_from_generator(np.random.default_rng(0)), (nb, 1))
+                bt, keep = self._upload(csr, probe, None)
+                _lib.call("slide_forward", self._ctx, _lib.C.byref(bt), 0, 0, None)
+                empty = self._read(9, nb, np.int32)
+                states = np.empty((nb, 6), np.uint64)
+                L = lsh.family.l
+                for i in range(nb):
+                    states[i] = _lib.pcg64_state_from_generator(rng)
+                    if cfg.strategy == "vanilla":
+                        rng.permutation(L)
+                    if empty[i]:
+                        rng.choice(self.n_out, size=min(cfg.beta, self.n_out), replace=False)
+            bt, keep = self._upload(csr, states, forced)
+            _lib.call("slide_forward", self._ctx, _lib.C.byref(bt), 0, 0, None)
+            ids = np.empty((nb, topn), np.int32)
+            cnt = np.empty(nb, np.int32)
+            _lib.call("slide_topk", self._ctx, topn, ids.ctypes.data, cnt.ctypes.data)
+            out.extend(ids[i, : cnt[i]].astype(np.int64) for i in range(nb))
+            self._live = keep
+        return out
 
 
 def train_network(net: SlideNetwork, dataset, *, workers: int = 1, on_batch=None, schedule: str | None = None) -> int:

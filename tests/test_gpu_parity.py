@@ -441,3 +441,45 @@ def test_backward_capture_matches_finite_differences_shape():
     if g.dh is not None:
         assert cap[1][0] == 0
         np.testing.assert_allclose(cap[1][4], g.dh, rtol=1e-4, atol=1e-6)
+
+
+@pytest.mark.parametrize("strategy", ["vanilla", "topk"])
+def test_batched_ranking_equals_sequential_predict(strategy):
+    """predict_batch (the evaluator: one generator shared across queries,
+    B queries per device pass, device top-k) equals query-by-query predict
+    with the same generator -- including queries whose buckets are all empty
+    (the fallback draw advances the shared generator) and empty inputs."""
+    from paper_1903_03129_b200.data import precision_at_k, score_precision_at_k
+
+    rng = np.random.default_rng(31)
+    D, H, N, B = 60, 16, 300, 16
+    spec = LshLayerConfig("simhash", k=3, l=4, capacity=8, sampler=SamplerConfig(strategy, beta=10))
+    cfg = TrainConfig(batch_size=B, seed=2, learning_rate=1e-2, n0=5)
+    net = SlideNetwork(D, [H, N], cfg, lsh_layers={1: spec})
+    ex = []
+    for _ in range(45):
+        nnz = int(rng.integers(0, 8))
+        idx = np.sort(rng.choice(D, size=nnz, replace=False))
+        ex.append((SparseVector(idx, np.abs(rng.standard_normal(nnz)) + 0.1, D), sorted(rng.choice(N, 2, replace=False).tolist())))
+    net.train_batch(ex[:B], 1)
+    lsh = net.layers[1].lsh
+    for view in lsh.tables:  # drop half of every table's buckets: some queries come back empty
+        for key in list(view.keys())[::2]:
+            del view[key]
+    lsh.sync_to_device()
+    xs = [x for x, _ in ex]
+    n_empty = 0
+    for x in xs:
+        net.forward(x, 0, rng=np.random.default_rng(0))
+        n_empty += int(net._read(9, 1, np.int32)[0])
+    assert 0 < n_empty < len(xs)
+    r1, r2 = np.random.default_rng(7), np.random.default_rng(7)
+    want = [net.predict(x, rng=r1)[:5] for x in xs]
+    got = net.predict_batch(xs, topn=5, rng=r2)
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        np.testing.assert_array_equal(g, w)
+    assert r1.bit_generator.state == r2.bit_generator.state
+    p1 = score_precision_at_k(net, ex, k=1, seed=3)
+    r3 = np.random.default_rng(3)
+    assert p1 == pytest.approx(float(np.mean([precision_at_k(net.predict(x, rng=r3)[:1], y, 1) for x, y in ex])))
