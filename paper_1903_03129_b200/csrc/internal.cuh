@@ -64,6 +64,8 @@ void launch_dwta_keys(const DwtaDev& f, const float* x, int64_t n, int ld, uint3
 struct TablesDev {
   int l = 0, key_bits = 0, cap = 0;
   int dense_dir = 0;          // 1: dir is (L << key_bits) int32 run ids
+  int validated = 0;          // dense dir never cleared: an entry counts only if run_keys[r] == key
+  const uint32_t* run_keys = nullptr;  // per run: its (table << key_bits | key)
   int empty = 1;              // no buckets (unbuilt or cleared)
   uint64_t disabled = 0;      // bit t: table t reads as empty
   uint64_t hash_mask = 0;     // hash directory size - 1
@@ -87,7 +89,11 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
 
 __device__ __forceinline__ int tables_lookup(const TablesDev& t, uint32_t skey) {
   if (t.empty || ((t.disabled >> (skey >> t.key_bits)) & 1ull)) return -1;
-  if (t.dense_dir) return t.dir[skey];
+  if (t.dense_dir) {
+    const int r = t.dir[skey];
+    if (t.validated && ((uint64_t)(uint32_t)r >= (uint64_t)t.n_runs || t.run_keys[r] != skey)) return -1;
+    return r;
+  }
   uint64_t loc = hash32(skey) & t.hash_mask;
   while (true) {
     uint64_t e = t.hdir[loc];

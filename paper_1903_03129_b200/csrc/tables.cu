@@ -21,14 +21,25 @@ void TablesHost::release() {
   built = false;
 }
 
-__global__ void sort_input_kernel(const uint32_t* __restrict__ keys, int64_t n, int l, int kb,
-                                  uint32_t* __restrict__ skeys, int32_t* __restrict__ vals) {
-  int64_t total = n * l;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    int64_t t = q / n, r = q - t * n;
-    skeys[q] = ((uint32_t)t << kb) | keys[r * l + t];
-    vals[q] = (int32_t)r;
+// (n, L) row-major keys -> table-major (t << kb | key, id) inserts.  A CTA
+// stages 64 rows x L keys through shared memory so both the row-major reads
+// and the table-major writes are coalesced.
+constexpr int kSortRows = 64;
+
+__global__ void __launch_bounds__(256) sort_input_kernel(const uint32_t* __restrict__ keys, int64_t n, int l, int kb,
+                                                         uint32_t* __restrict__ skeys, int32_t* __restrict__ vals) {
+  extern __shared__ uint32_t tile[];  // [kSortRows][l + 1] (padded: conflict-free column reads)
+  for (int64_t r0 = (int64_t)blockIdx.x * kSortRows; r0 < n; r0 += (int64_t)gridDim.x * kSortRows) {
+    const int nr = (int)min((int64_t)kSortRows, n - r0);
+    __syncthreads();
+    for (int q = threadIdx.x; q < nr * l; q += blockDim.x) tile[q + q / l] = keys[r0 * l + q];
+    __syncthreads();
+    for (int q = threadIdx.x; q < nr * l; q += blockDim.x) {
+      const int t = q / nr, i = q - t * nr;
+      const int64_t o = (int64_t)t * n + r0 + i;
+      skeys[o] = ((uint32_t)t << kb) | tile[i * (l + 1) + t];
+      vals[o] = (int32_t)(r0 + i);
+    }
   }
 }
 
@@ -105,6 +116,33 @@ __global__ void patch_kernel(const int2* __restrict__ patches, int64_t n, int32_
     ids[patches[q].x] = patches[q].y;
 }
 
+
+// Directory choice.  Short keys (<= 16 bits): a dense (table, key) -> run
+// table, reset per build.  Longer keys with a key space at most 64x the
+// inserts and <= 2^30 entries (DWTA 24-bit keys at wide-out / scaled): the
+// same dense table but never cleared -- a lookup validates the entry against
+// the run's own key (stale entries of earlier builds fail the check), so a
+// build only scatters its runs.  Otherwise an open-addressing hash.
+static void choose_dir(TablesHost& tb, TablesDev& d, int l, int kb, int64_t n_items, int64_t n_runs, cudaStream_t s) {
+  const uint64_t nd = (uint64_t)l << kb;
+  d.dense_dir = kb <= 16 || (nd <= (1ull << 30) && nd <= 64ull * (uint64_t)std::max<int64_t>(n_items, 1));
+  d.validated = kb > 16;
+  d.dir = nullptr;
+  d.hdir = nullptr;
+  d.hash_mask = 0;
+  if (d.dense_dir) {
+    int32_t* dir = tb.dir.ensure<int32_t>(nd);
+    if (!d.validated) SLIDE_CUDA(cudaMemsetAsync(dir, 0xff, nd * 4, s));
+    d.dir = dir;
+  } else {
+    uint64_t hc = gen_mask((uint64_t)std::max<int64_t>(2 * n_runs, 16)) + 1;
+    uint64_t* hdir = tb.hdir.ensure<uint64_t>(hc);
+    SLIDE_CUDA(cudaMemsetAsync(hdir, 0xff, hc * 8, s));
+    d.hdir = hdir;
+    d.hash_mask = hc - 1;
+  }
+}
+
 static int grid_for(int64_t n, int bs = 256) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, bs), kSms * 16)); }
 
 void tables_build(TablesHost& tb, const uint32_t* keys, int64_t n, int l, int kb, int cap, int policy,
@@ -123,7 +161,8 @@ void tables_build(TablesHost& tb, const uint32_t* keys, int64_t n, int l, int kb
   int32_t* offsets = tb.offsets.ensure<int32_t>(total);
   int32_t* nr_d = tb.nruns.ensure<int32_t>(1);
   if (total > 0) {
-    sort_input_kernel<<<grid_for(total), 256, 0, s>>>(keys, n, l, kb, ska, va);
+    sort_input_kernel<<<grid_for(ceil_div(n, kSortRows), 1), 256, (size_t)kSortRows * (l + 1) * 4, s>>>(keys, n, l, kb, ska,
+                                                                                               va);
     SLIDE_LAUNCH_CHECK();
   }
   const int end_bit = kb + tbits;
@@ -145,20 +184,11 @@ void tables_build(TablesHost& tb, const uint32_t* keys, int64_t n, int l, int kb
   d.key_bits = kb;
   d.cap = cap;
   d.n_runs = n_runs;
-  d.dense_dir = kb <= 16;
-  int32_t* dir = nullptr;
-  uint64_t* hdir = nullptr;
-  uint64_t hmask = 0;
-  if (d.dense_dir) {
-    size_t nd = (size_t)l << kb;
-    dir = tb.dir.ensure<int32_t>(nd);
-    SLIDE_CUDA(cudaMemsetAsync(dir, 0xff, nd * 4, s));
-  } else {
-    uint64_t hc = gen_mask((uint64_t)std::max<int64_t>(2 * (int64_t)n_runs, 16)) + 1;
-    hmask = hc - 1;
-    hdir = tb.hdir.ensure<uint64_t>(hc);
-    SLIDE_CUDA(cudaMemsetAsync(hdir, 0xff, hc * 8, s));
-  }
+  choose_dir(tb, d, l, kb, total, n_runs, s);
+  d.run_keys = uniq;
+  int32_t* dir = const_cast<int32_t*>(d.dir);
+  uint64_t* hdir = const_cast<uint64_t*>(d.hdir);
+  const uint64_t hmask = d.hash_mask;
   int32_t* bstart = tb.bstart.ensure<int32_t>(std::max<int64_t>(n_runs, 1));
   int32_t* blen = tb.blen.ensure<int32_t>(std::max<int64_t>(n_runs, 1));
   int32_t* ovf = policy == 1 ? tb.ovf_cnt.ensure<int32_t>(std::max<int64_t>(n_runs, 1)) : nullptr;
@@ -257,22 +287,8 @@ void tables_load(TablesHost& tb, const uint32_t* skeys, const int32_t* counts, c
   d.key_bits = kb;
   d.cap = cap;
   d.n_runs = n_runs;
-  d.dense_dir = kb <= 16;
-  d.dir = nullptr;
-  d.hdir = nullptr;
-  d.hash_mask = 0;
-  if (d.dense_dir) {
-    size_t nd = (size_t)l << kb;
-    int32_t* dir = tb.dir.ensure<int32_t>(nd);
-    SLIDE_CUDA(cudaMemsetAsync(dir, 0xff, nd * 4, s));
-    d.dir = dir;
-  } else {
-    uint64_t hc = gen_mask((uint64_t)std::max<int64_t>(2 * n_runs, 16)) + 1;
-    uint64_t* hdir = tb.hdir.ensure<uint64_t>(hc);
-    SLIDE_CUDA(cudaMemsetAsync(hdir, 0xff, hc * 8, s));
-    d.hdir = hdir;
-    d.hash_mask = hc - 1;
-  }
+  choose_dir(tb, d, l, kb, n_items, n_runs, s);
+  d.run_keys = uniq;
   if (n_runs) {
     dir_kernel<<<grid_for(n_runs), 256, 0, s>>>(uniq, n_runs, d.dense_dir, tb.dir.as<int32_t>(), tb.hdir.as<uint64_t>(),
                                                 d.hash_mask);
