@@ -129,6 +129,14 @@ int slide_tables_mask(slide_ctx* ctx, uint64_t disabled);
  * and occupancy of each probed bucket (0 when the key is absent) */
 int slide_tables_probe(slide_ctx* ctx, const uint32_t* keys, int64_t b, int32_t* starts, int32_t* lens);
 
+/* Query + union (rebuild microbenchmark): hash n query rows
+ * (device, stride hidden_pad) and write per query the ascending union of its
+ * L buckets -- hard_threshold(min_freq=1), reference samplers.py:109-112.
+ * cnt_out: device (n) int32; ids_out: device (n x cap_stride) int32,
+ * cap_stride >= L * capacity; n_ids bounds the ids (rows in the tables). */
+int slide_query_union(slide_ctx* ctx, const float* q_dev, int64_t n, int64_t n_ids, int64_t cap_stride,
+                      int32_t* cnt_out, int32_t* ids_out);
+
 /* -- the step --------------------------------------------------------- */
 /* forward of a (sub-)batch (network.py:241-286, 225-239): hidden layer,
  * query hash, per-slot rng, sampler, fallback, label union, logits,

@@ -66,6 +66,7 @@ _SIGS = {
     "slide_graph_step": [vp, C.POINTER(Batch), i64, vp, vp],
     "slide_read": [vp, i64, vp, i64, C.POINTER(i64)],
     "slide_topk": [vp, i64, vp, vp],
+    "slide_query_union": [vp, vp, i64, i64, i64, vp, vp],
     "slide_write": [vp, i64, vp, i64],
     "slide_profile": [vp, i64],
     "slide_profile_read": [vp, vp, vp],

@@ -424,6 +424,54 @@ int slide_tables_probe(slide_ctx* c, const uint32_t* keys, int64_t b, int32_t* s
   });
 }
 
+// Query + union (the rebuild microbenchmark's second half):
+// hash n query rows (device, row stride ld = hidden_pad) and return, per
+// query, the ascending union of its L buckets -- hard_threshold(min_freq=1)
+// (reference samplers.py:109-112).  cnt_out (n) and ids_out (n x cap_stride)
+// are device arrays; cap_stride >= L * capacity.
+int slide_query_union(slide_ctx* c, const float* q, int64_t n, int64_t n_ids, int64_t cap_stride, int32_t* cnt_out,
+                      int32_t* ids_out) {
+  return guarded([&] {
+    SLIDE_CHECK(c->d.family != 0, kValueError, "layer has no LSH tables");
+    SLIDE_CHECK(c->tab.built, kValueError, "tables are not built");
+    const int L = (int)c->d.l;
+    SLIDE_CHECK(cap_stride >= (int64_t)L * c->d.capacity, kValueError, "cap_stride must be >= L * capacity");
+    cudaStream_t s = c->s;
+    const int chunk = 1024;
+    uint32_t* keys = c->qkeys.ensure<uint32_t>((size_t)chunk * L);
+    int32_t* yp = c->cnt_all.ensure<int32_t>(chunk + 1);
+    int32_t* empty = c->empty.ensure<int32_t>(chunk);
+    SLIDE_CUDA(cudaMemsetAsync(yp, 0, (chunk + 1) * 4, s));
+    for (int64_t o = 0; o < n; o += chunk) {
+      const int nb = (int)std::min<int64_t>(chunk, n - o);
+      hash_rows(c, q + o * c->hp, nb, keys);
+      SelectArgs a;
+      a.tab = c->tab.dev;
+      a.tab.l = L;
+      a.tab.key_bits = (int)c->d.key_bits;
+      a.qkeys = keys;
+      a.order = nullptr;
+      a.y_ptr = yp;
+      a.y_idx = nullptr;
+      a.b = nb;
+      a.l = L;
+      a.strategy = 3;  // union of every probed bucket
+      a.beta = INT32_MAX;
+      a.min_freq = 1;
+      a.sort_bits = bits_for(n_ids) + 7;
+      a.cap_max = cap_stride;
+      a.act = ids_out + o * cap_stride;
+      a.cnt = cnt_out + o;
+      a.empty = empty;
+      a.cand_ctr = nullptr;
+      if (!launch_select_union(a, n_ids, s)) {
+        a.strategy = 2;  // hard_threshold(min_freq = 1) through the sort path
+        launch_select(a, (int)((int64_t)L * c->d.capacity), s);
+      }
+    }
+  });
+}
+
 // --------------------------------------------------------------------- step
 static void side_stream_init(slide_ctx* c) {
   if (c->s2) return;

@@ -284,6 +284,40 @@ class LshTables:
         self._dirty = False
 
     # -- queries --------------------------------------------------------------
+    def query_union_batch(self, queries, *, return_device: bool = False):
+        """Ascending union of every probed bucket for each dense query row --
+        the sampler's ``hard_threshold(min_freq=1)`` over all L tables
+        (reference samplers.py:109-112) -- for a whole batch on the device
+        (``slide_query_union``: hash, probe, union).  Returns a list of int64
+        arrays, or the device (counts, ids) pair with ``return_device``."""
+        import torch
+
+        from . import _device
+
+        q = np.asarray(queries, dtype=np.float64)
+        if q.ndim != 2 or q.shape[1] != self.family.dim:
+            raise ValueError(f"expected query rows of shape (n, {self.family.dim}), got {q.shape}")
+        n = q.shape[0]
+        self.sync_to_device()
+        if self._ctx is None or not self.n_items or n == 0:
+            return [np.zeros(0, dtype=np.int64) for _ in range(n)]
+        x = q if isinstance(queries, torch.Tensor) else _device.pad_rows(q, _device.round_up(self.family.dim, 128))
+        return self._query_union_dev(x, n, return_device)
+
+    def _query_union_dev(self, x_dev, n: int, return_device: bool = False):
+        import torch
+
+        stride = self.family.l * self.capacity
+        cnt = torch.empty(n, dtype=torch.int32, device=x_dev.device)
+        ids = torch.empty((n, stride), dtype=torch.int32, device=x_dev.device)
+        _lib.call("slide_query_union", self._context(), x_dev.data_ptr(), n, self.n_items, stride, cnt.data_ptr(),
+                  ids.data_ptr())
+        if return_device:
+            return cnt, ids
+        c = cnt.cpu().numpy()
+        got = ids.cpu().numpy()
+        return [(got[i, : c[i]] & 0x7FFFFFFF).astype(np.int64) for i in range(n)]
+
     def query(self, v: SparseVector) -> RawCandidates:
         """Hash the query and probe each table once (reference tables.py:165-169)."""
         if v.dim != self.family.dim:

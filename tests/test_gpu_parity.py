@@ -483,3 +483,23 @@ def test_batched_ranking_equals_sequential_predict(strategy):
     p1 = score_precision_at_k(net, ex, k=1, seed=3)
     r3 = np.random.default_rng(3)
     assert p1 == pytest.approx(float(np.mean([precision_at_k(net.predict(x, rng=r3)[:1], y, 1) for x, y in ex])))
+
+
+@pytest.mark.parametrize("family", ["simhash", "dwta"])
+def test_batched_query_union_equals_per_query_probes(family):
+    """slide_query_union (hash + L probes + union for a batch) equals the
+    union of each query's own L probes (reference tables.py:165-176,
+    samplers.py:109-112 with min_freq=1)."""
+    rng = np.random.default_rng(4)
+    if family == "simhash":
+        fam = new_hash_family(HashFamilyConfig("simhash", 4, 6, 32, seed=3))
+    else:
+        fam = new_hash_family(HashFamilyConfig("dwta", 3, 6, 32, wta_bin_size=4, seed=3))
+    tbl = LshTables(fam, policy="fifo", capacity=8, seed=1)
+    tbl.build(rng.standard_normal((500, 32)).astype(np.float32))
+    q = rng.standard_normal((70, 32)).astype(np.float32).astype(np.float64)
+    got = tbl.query_union_batch(q)
+    for i in range(q.shape[0]):
+        raw = tbl.query(SparseVector.from_dense(q[i]))
+        want = np.unique(np.concatenate([np.asarray(p, dtype=np.int64) for p in raw.per_table] + [np.zeros(0, np.int64)]))
+        np.testing.assert_array_equal(got[i], want)
