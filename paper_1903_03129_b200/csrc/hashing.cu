@@ -200,6 +200,85 @@ __global__ void __launch_bounds__(256) dwta_kernel(DwtaDev f, const float* __res
   }
 }
 
+// Rebuild path: 16 rows at a time, transposed in shared memory so one
+// 16-byte load fetches a dimension for 4 rows; one thread per bin keeps the
+// bin's m permutation positions in registers for all 16 rows.  Same winner /
+// tie / nonzero rules and the same donor densification as dwta_kernel.
+constexpr int kDwRows = 16;
+constexpr int kDwMaxM = 16;
+
+__global__ void __launch_bounds__(256) dwta_rows_kernel(DwtaDev f, const float* __restrict__ x, int64_t n, int ld,
+                                                        uint32_t* __restrict__ keys) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int KL = f.k * f.l;
+  float* xs = reinterpret_cast<float*>(sm);  // [dim][kDwRows]
+  int16_t* perm = reinterpret_cast<int16_t*>(xs + kDwRows * f.dim);
+  uint8_t* codes = reinterpret_cast<uint8_t*>(perm + ((f.n_perms * f.dim + 7) & ~7));
+  uint8_t* occ = codes + kDwRows * KL;
+  for (int q = threadIdx.x; q < f.n_perms * f.dim; q += blockDim.x) perm[q] = f.perms[q];
+  for (int64_t row0 = (int64_t)blockIdx.x * kDwRows; row0 < n; row0 += (int64_t)gridDim.x * kDwRows) {
+    const int nr = (int)(n - row0 < kDwRows ? n - row0 : kDwRows);
+    __syncthreads();
+    for (int q = threadIdx.x; q < kDwRows * f.dim; q += blockDim.x) {
+      const int r = q / f.dim, c = q - r * f.dim;
+      xs[c * kDwRows + r] = r < nr ? x[(row0 + r) * ld + c] : 0.f;
+    }
+    __syncthreads();
+    for (int g = threadIdx.x; g < KL; g += blockDim.x) {
+      const int pq = g / f.bins_per_perm, b = g - pq * f.bins_per_perm;
+      const int lo = b * f.m, cnt = min(f.m, f.dim - lo);
+      int idx[kDwMaxM];
+#pragma unroll
+      for (int o = 0; o < kDwMaxM; ++o) idx[o] = o < cnt ? perm[pq * f.dim + lo + o] : 0;
+#pragma unroll
+      for (int r4 = 0; r4 < kDwRows / 4; ++r4) {
+        float best[4] = {0.f, 0.f, 0.f, 0.f};
+        int code[4] = {0, 0, 0, 0}, oc[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int o = 0; o < kDwMaxM; ++o) {
+          if (o >= cnt) break;
+          const float4 v4 = *reinterpret_cast<const float4*>(xs + idx[o] * kDwRows + r4 * 4);
+          const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const bool take = (f.dense_mode || v[e] != 0.f) && (!oc[e] || v[e] > best[e]);
+            best[e] = take ? v[e] : best[e];
+            code[e] = take ? o : code[e];
+            oc[e] = take ? 1 : oc[e];
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          codes[(r4 * 4 + e) * KL + g] = (uint8_t)code[e];
+          occ[(r4 * 4 + e) * KL + g] = (uint8_t)oc[e];
+        }
+      }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nr * KL; q += blockDim.x) {
+      if (occ[q]) continue;
+      const int r = q / KL, g = q - r * KL;
+      int code = 0;
+      for (int a = 0; a < 100; ++a) {
+        const int d = f.donors[g * 100 + a];
+        if (occ[r * KL + d]) {
+          code = codes[r * KL + d];
+          break;
+        }
+      }
+      codes[q] = (uint8_t)code;  // only empty bins are written; donors are occupied
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nr * f.l; q += blockDim.x) {
+      const int r = q / f.l, t = q - r * f.l;
+      const uint8_t* cc = codes + r * KL + t * f.k;
+      uint32_t key = 0;
+      for (int kk = 0; kk < f.k; ++kk) key |= (uint32_t)cc[kk] << (f.bits * kk);
+      keys[(row0 + r) * f.l + t] = key;
+    }
+  }
+}
+
 template <int ROWS>
 static void launch_dwta_t(const DwtaDev& f, const float* x, int64_t n, int ld, uint32_t* keys, cudaStream_t s) {
   const int KL = f.k * f.l;
@@ -214,8 +293,20 @@ static void launch_dwta_t(const DwtaDev& f, const float* x, int64_t n, int ld, u
 
 void launch_dwta_keys(const DwtaDev& f, const float* x, int64_t n, int ld, uint32_t* keys, cudaStream_t s) {
   if (n <= 0) return;
-  if (n <= (int64_t)kSms * 8) launch_dwta_t<1>(f, x, n, ld, keys, s);
-  else launch_dwta_t<8>(f, x, n, ld, keys, s);
+  if (n <= (int64_t)kSms * 8) {
+    launch_dwta_t<1>(f, x, n, ld, keys, s);
+    return;
+  }
+  const int KL = f.k * f.l;
+  const size_t smem = (size_t)kDwRows * f.dim * 4 + (size_t)((f.n_perms * f.dim + 7) & ~7) * 2 + (size_t)2 * kDwRows * KL;
+  if (f.m > kDwMaxM || smem > 227 * 1024) {
+    launch_dwta_t<8>(f, x, n, ld, keys, s);
+    return;
+  }
+  SLIDE_CUDA(cudaFuncSetAttribute(dwta_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = (int)std::min<int64_t>(ceil_div(n, kDwRows), (int64_t)kSms * 4);
+  dwta_rows_kernel<<<grid, 256, smem, s>>>(f, x, n, ld, keys);
+  SLIDE_LAUNCH_CHECK();
 }
 
 }  // namespace slide

@@ -503,3 +503,20 @@ def test_batched_query_union_equals_per_query_probes(family):
         raw = tbl.query(SparseVector.from_dense(q[i]))
         want = np.unique(np.concatenate([np.asarray(p, dtype=np.int64) for p in raw.per_table] + [np.zeros(0, np.int64)]))
         np.testing.assert_array_equal(got[i], want)
+
+
+@pytest.mark.parametrize("name", ["dw_main", "dw_scaled"])
+def test_dwta_rebuild_path_matches_oracle(name):
+    """> 148 x 8 rows take the 16-row transposed rebuild kernel: keys equal
+    the oracle's, including sparse rows whose empty bins borrow donor codes
+    and rows with ties."""
+    spec = HASH_SPECS[name]
+    fam = new_hash_family(HashFamilyConfig(**spec))
+    rng = np.random.default_rng(12)
+    n, d = 5000, spec["dim"]
+    w = rng.standard_normal((n, d)).astype(np.float32)
+    w[::3] *= rng.random((w[::3].shape[0], d)) < 0.05  # mostly-zero rows: empty bins, donors
+    w[1::7] = np.round(w[1::7])  # many ties: lowest in-bin offset wins
+    w = w.astype(np.float64)
+    params = O.dwta_params(d, spec["k_per_table"], spec["num_tables"], spec["wta_bin_size"], spec["seed"])
+    np.testing.assert_array_equal(fam.hash_batch(w), O.dwta_keys(params, w))
