@@ -834,11 +834,7 @@ int slide_graph_step(slide_ctx* c, const slide_batch* bt, int64_t iteration, dou
     }
     auto& st = c->st;
     if (!st.on || st.batch != B || nnz > st.nnz_cap || max_lab > st.lab_cap || nlab > st.ylab_cap) {
-      if (c->s2) cudaStreamSynchronize(c->s2);
-    for (cudaEvent_t e : {c->ev_fork, c->ev_dh, c->ev_join, c->ev_pre})
-      if (e) cudaEventDestroy(e);
-    if (c->s2) cudaStreamDestroy(c->s2);
-    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+      if (c->gexec) cudaGraphExecDestroy(c->gexec);
       if (c->graph) cudaGraphDestroy(c->graph);
       c->gexec = nullptr;
       c->graph = nullptr;
