@@ -253,14 +253,34 @@ def run_ours(args, rank, world):
         total_ms = float(t.item())
     # N > 1: the ranks share one global batch per step (sharded output layer)
     value = K * w.batch / (total_ms / 1e3)
-    # -- e2e: public API from pinned host CSR, fresh net state continues
+    # -- e2e: public API from host CSR, fresh net state continues.
+    # (1) pipelined SlideNetwork.train_batches_csr over the K batches, timed
+    #     as one region (each step: H2D of its batch, the step, D2H of its
+    #     losses; the next batch is staged while the device runs); L2 flushed
+    #     once before -- the step's inputs include the 1.5 GB model state,
+    #     far above the 126 MB L2;
+    # (2) one synchronous train_batch_csr call per step, L2 flushed between
+    #     steps outside the events (reported as e2e.sync_value).
     e2e = None
     if not args.no_e2e:
+        it0 = W + K + 1
+        order = [batches[(W + k) % n_batches] for k in range(K)]
+        pipelined = world == 1 and args.schedule == "snapshot"
+        if pipelined:
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            net.train_batches_csr(order, first_iteration=it0, schedule=args.schedule)
+            e1.record()
+            torch.cuda.synchronize()
+            p_total = e0.elapsed_time(e1)
+            it0 += K
         e_times = []
         h2d = d2h = 0
         for k in range(K):
-            it = W + K + 1 + k
-            b = batches[(W + k) % n_batches]
+            it = it0 + k
+            b = order[k]
             flush.zero_()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -276,11 +296,17 @@ def run_ours(args, rank, world):
             t = torch.tensor([e_total], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_total = float(t.item())
-        e2e = {"value": K * w.batch / (e_total / 1e3), "unit": "samples/s",
-               "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K)}
+        sync_value = K * w.batch / (e_total / 1e3)
+        e2e = {"value": K * w.batch / (p_total / 1e3) if pipelined else sync_value, "unit": "samples/s",
+               "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K),
+               "api": ("SlideNetwork.train_batches_csr (pipelined: batch k+1 staged while step k runs), "
+                       "L2 flushed once before the K steps" if pipelined else "SlideNetwork.train_batch_csr"),
+               "sync_value": sync_value,
+               "sync_api": "SlideNetwork.train_batch_csr per step, L2 flushed between steps outside the events"}
+    # -- profiled pass: per-stage event times + realised sets
     # -- profiled pass: per-stage event times + realised sets
     _lib.call("slide_profile", net._ctx, 1)
-    it0 = W + 2 * K + 1
+    it0 = W + 3 * K + 1
     for k in range(K):
         step_dev_it = it0 + k
         bt, keep, hb = dev_batches[(W + k) % n_batches]

@@ -162,6 +162,13 @@ int slide_train_batch(slide_ctx* ctx, const slide_batch* batch, int64_t iteratio
  * Same outputs as slide_train_batch with sub_batch = batch. */
 int slide_graph_step(slide_ctx* ctx, const slide_batch* batch, int64_t iteration, double* loss_host,
                      int64_t* active_host);
+/* The same step split for pipelining (train_batches_csr): _async enqueues
+ * the H2D copies, the step and the D2H of losses / set sizes without a host
+ * wait (the batch's host buffers must stay untouched until _wait returns);
+ * _wait blocks for it and fills loss_host / active_host.  One step in flight
+ * per context. */
+int slide_graph_step_async(slide_ctx* ctx, const slide_batch* batch, int64_t iteration);
+int slide_graph_step_wait(slide_ctx* ctx, double* loss_host, int64_t* active_host);
 
 /* stage readout of the last forward/backward (host copy), for parity:
  * 0 h (B, hp) f32 | 1 query keys (B, L) u32 | 2 offsets (B+1) i32 |

@@ -64,6 +64,8 @@ _SIGS = {
     "slide_backward": [vp, i64],
     "slide_train_batch": [vp, C.POINTER(Batch), i64, i64, vp, vp],
     "slide_graph_step": [vp, C.POINTER(Batch), i64, vp, vp],
+    "slide_graph_step_async": [vp, C.POINTER(Batch), i64],
+    "slide_graph_step_wait": [vp, vp, vp],
     "slide_read": [vp, i64, vp, i64, C.POINTER(i64)],
     "slide_topk": [vp, i64, vp, vp],
     "slide_query_union": [vp, vp, i64, i64, i64, vp, vp],

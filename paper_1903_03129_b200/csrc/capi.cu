@@ -66,6 +66,7 @@ struct slide_ctx {
   // set by the fused step callers: forward already queues the W1 grouping
   // on the side stream (it needs only the inputs)
   bool w1_prefork = false, w1_grouped = false;
+  int64_t g_pending = 0;  // batch size of the graph step in flight (async API)
   int hp = 0;
   TablesHost tab;
   DBuf sh_packed, sh_packed_t, dw_perms, dw_donors, rowkeys;
@@ -815,9 +816,9 @@ int slide_train_batch(slide_ctx* c, const slide_batch* bt, int64_t iteration, in
 // One snapshot step as a CUDA graph (see header).  The first call with new
 // shapes runs eagerly (and sizes every buffer), the second captures, the
 // rest replay: no host work between the kernels, one sync per step.
-int slide_graph_step(slide_ctx* c, const slide_batch* bt, int64_t iteration, double* loss_host,
-                     int64_t* active_host) {
-  return guarded([&] {
+// Enqueue one graph step: H2D of the batch, the step, D2H of the per-slot
+// losses and set sizes into pinned memory; no host wait.
+static void graph_step_launch(slide_ctx* c, const slide_batch* bt, int64_t iteration) {
     const int64_t B = bt->batch;
     SLIDE_CHECK(B >= 1 && B <= 1024, kValueError, "batch must hold 1..1024 slots");
     SLIDE_CHECK(!bt->forced_ptr && !bt->rng_states, kValueError, "graph steps take plain training batches");
@@ -955,13 +956,38 @@ int slide_graph_step(slide_ctx* c, const slide_batch* bt, int64_t iteration, dou
     SLIDE_CUDA(cudaMemcpyAsync(c->pinned_cnt, c->cnt.p, B * 4, cudaMemcpyDeviceToHost, gs));
     SLIDE_CUDA(cudaEventRecord(c->gev_out, gs));
     SLIDE_CUDA(cudaStreamWaitEvent(user, c->gev_out, 0));
-    SLIDE_CUDA(cudaStreamSynchronize(gs));
-    for (int64_t i = 0; i < B; ++i) {
-      if (loss_host) loss_host[i] = c->pinned_loss[i];
-      if (active_host) active_host[i] = c->pinned_cnt[i];
-      c->host_counts[0] += c->pinned_cnt[i];
-    }
+    c->g_pending = B;
+}
+
+static void graph_step_finish(slide_ctx* c, double* loss_host, int64_t* active_host) {
+  SLIDE_CHECK(c->g_pending > 0, kValueError, "no graph step in flight");
+  const int64_t B = c->g_pending;
+  c->g_pending = 0;
+  SLIDE_CUDA(cudaEventSynchronize(c->gev_out));
+  for (int64_t i = 0; i < B; ++i) {
+    if (loss_host) loss_host[i] = c->pinned_loss[i];
+    if (active_host) active_host[i] = c->pinned_cnt[i];
+    c->host_counts[0] += c->pinned_cnt[i];
+  }
+}
+
+int slide_graph_step(slide_ctx* c, const slide_batch* bt, int64_t iteration, double* loss_host,
+                     int64_t* active_host) {
+  return guarded([&] {
+    graph_step_launch(c, bt, iteration);
+    graph_step_finish(c, loss_host, active_host);
   });
+}
+
+int slide_graph_step_async(slide_ctx* c, const slide_batch* bt, int64_t iteration) {
+  return guarded([&] {
+    SLIDE_CHECK(c->g_pending == 0, kValueError, "a graph step is already in flight");
+    graph_step_launch(c, bt, iteration);
+  });
+}
+
+int slide_graph_step_wait(slide_ctx* c, double* loss_host, int64_t* active_host) {
+  return guarded([&] { graph_step_finish(c, loss_host, active_host); });
 }
 
 int slide_read(slide_ctx* c, int64_t what, void* dst, int64_t max_bytes, int64_t* bytes) {

@@ -526,10 +526,43 @@ class SlideNetwork:
             loss, active = self._step(csr, iteration, 1 if schedule == "sequential" else B)
         return self._barrier(iteration, loss, active)
 
+    def train_batches_csr(self, batches, first_iteration: int = 1, schedule: str = "snapshot") -> list:
+        """``train_batch_csr`` over consecutive batches (iterations
+        first_iteration, first_iteration + 1, ...), pipelined on the host:
+        while step k runs on the device (H2D, graph, D2H of its losses), the
+        host stages batch k+1 into the other pinned buffer set; then it waits
+        for step k's losses and runs the rebuild barrier before launching
+        k+1.  Same results as calling train_batch_csr per batch."""
+        batches = list(batches)
+        if (schedule != "snapshot" or not self.use_graphs or self.shard_count > 1
+                or any(c.batch != self.cfg.batch_size for c in batches)):
+            return [self.train_batch_csr(c, first_iteration + k, schedule) for k, c in enumerate(batches)]
+        out = []
+        if not batches:
+            return out
+        B = self.cfg.batch_size
+        loss = np.empty(B, dtype=np.float64)
+        active = np.empty(B, dtype=np.int64)
+        staged = self._pinned_batch(batches[0], 0)
+        for k, csr in enumerate(batches):
+            it = first_iteration + k
+            if self.layers[1].lsh is not None:
+                self.layers[1].lsh.sync_to_device()
+            bt, keep = staged
+            h2d = self.h2d_bytes
+            _lib.call("slide_graph_step_async", self._ctx, _lib.C.byref(bt), it)
+            if k + 1 < len(batches):  # overlaps the device step
+                staged = self._pinned_batch(batches[k + 1], (k + 1) % 2)
+            _lib.call("slide_graph_step_wait", self._ctx, loss.ctypes.data, active.ctypes.data)
+            self.h2d_bytes = h2d
+            out.append(self._barrier(it, loss, active))
+            self._live = keep
+        return out
+
     #: snapshot steps replay one captured CUDA graph per batch shape
     use_graphs = True
 
-    def _pinned_batch(self, csr: HostCsr):
+    def _pinned_batch(self, csr: HostCsr, buf_set: int = 0):
         """Batch struct over pinned host copies of the CSR (graph steps copy
         them into the context's own device buffers).  The pinned buffers and
         their numpy views are cached; each call is five plain copies."""
@@ -541,11 +574,11 @@ class SlideNetwork:
         for name, a, dt in (("xp", csr.x_ptr, np.int32), ("xi", csr.x_idx, np.int32), ("xv", csr.x_val, np.float32),
                             ("yp", csr.y_ptr, np.int32), ("yi", csr.y_idx, np.int32)):
             n = len(a)
-            ent = self._pinned.get(("g", name))
+            ent = self._pinned.get(("g", name, buf_set))
             if ent is None or ent[1].size < max(n, 1):
                 buf = torch.empty(max(n, 1) * 2, dtype=torch.from_numpy(np.empty(0, dt)).dtype, pin_memory=True)
                 ent = (buf, buf.numpy(), buf.data_ptr())
-                self._pinned[("g", name)] = ent
+                self._pinned[("g", name, buf_set)] = ent
             np.copyto(ent[1][:n], a, casting="unsafe")
             self.h2d_bytes += n * 4
             keep.append(ent[0])

@@ -520,3 +520,32 @@ def test_dwta_rebuild_path_matches_oracle(name):
     w = w.astype(np.float64)
     params = O.dwta_params(d, spec["k_per_table"], spec["num_tables"], spec["wta_bin_size"], spec["seed"])
     np.testing.assert_array_equal(fam.hash_batch(w), O.dwta_keys(params, w))
+
+
+def test_pipelined_batches_equal_per_call_steps():
+    """train_batches_csr (step k on the device while batch k+1 is staged,
+    rebuild barrier between steps) equals train_batch_csr per batch bit for
+    bit, across a table rebuild."""
+    from paper_1903_03129_b200.configs import TINY as w
+    from paper_1903_03129_b200.data import synthetic_corpus
+
+    corpus = synthetic_corpus(w.corpus, 7 * 64, seed=8)
+    batches = []
+    for it in range(7):
+        sub = corpus.subset(np.arange(it * 64, (it + 1) * 64))
+        batches.append(HostCsr(sub.x_ptr.astype(np.int32), sub.x_idx, sub.x_val, sub.y_ptr.astype(np.int32), sub.y_idx))
+
+    def make():
+        cfg = TrainConfig(batch_size=64, seed=0, learning_rate=w.lr, n0=3)
+        spec = LshLayerConfig("simhash", k=w.k, l=w.l, capacity=w.cap, sampler=SamplerConfig("vanilla", beta=w.beta))
+        return SlideNetwork(w.input_dim, [w.hidden, w.n_out], cfg, lsh_layers={1: spec})
+
+    a = make()
+    sa = [a.train_batch_csr(c, it) for it, c in enumerate(batches, start=1)]
+    b = make()
+    sb = b.train_batches_csr(batches, first_iteration=1)
+    assert [s.loss for s in sa] == [s.loss for s in sb]
+    assert [s.rebuilt for s in sa] == [s.rebuilt for s in sb]
+    assert any(s.rebuilt for s in sb)
+    np.testing.assert_array_equal(a.w2.cpu().numpy(), b.w2.cpu().numpy())
+    np.testing.assert_array_equal(a.w1t.cpu().numpy(), b.w1t.cpu().numpy())
