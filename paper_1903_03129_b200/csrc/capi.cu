@@ -63,6 +63,11 @@ struct slide_ctx {
   // captured step is one graph with two branches
   cudaStream_t s2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_dh = nullptr, ev_join = nullptr, ev_pre = nullptr;
+  // third stream: the per-row logits beside the dense-tile logits
+  cudaStream_t s3 = nullptr;
+  cudaEvent_t ev_lg = nullptr, ev_lg_join = nullptr;
+  DBuf hg_done;  // per-sample slice tickets of the hidden gradient (self-resetting)
+  int64_t hg_done_n = 0;
   // set by the fused step callers: forward already queues the W1 grouping
   // on the side stream (it needs only the inputs)
   bool w1_prefork = false, w1_grouped = false;
@@ -285,9 +290,12 @@ int slide_destroy(slide_ctx* c) {
     c->grow.release();
     c->gfeat.release();
     if (c->s2) cudaStreamSynchronize(c->s2);
-    for (cudaEvent_t e : {c->ev_fork, c->ev_dh, c->ev_join, c->ev_pre})
+    if (c->s3) cudaStreamSynchronize(c->s3);
+    for (cudaEvent_t e : {c->ev_fork, c->ev_dh, c->ev_join, c->ev_pre, c->ev_lg, c->ev_lg_join})
       if (e) cudaEventDestroy(e);
     if (c->s2) cudaStreamDestroy(c->s2);
+    if (c->s3) cudaStreamDestroy(c->s3);
+    c->hg_done.release();
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     if (c->graph) cudaGraphDestroy(c->graph);
     for (DBuf* b : {&c->iter_dev, &c->gx_ptr, &c->gx_idx, &c->gx_val, &c->gy_ptr, &c->gy_idx}) b->release();
@@ -477,8 +485,18 @@ int slide_query_union(slide_ctx* c, const float* q, int64_t n, int64_t n_ids, in
 static void side_stream_init(slide_ctx* c) {
   if (c->s2) return;
   SLIDE_CUDA(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
-  for (cudaEvent_t* e : {&c->ev_fork, &c->ev_dh, &c->ev_join, &c->ev_pre})
+  SLIDE_CUDA(cudaStreamCreateWithFlags(&c->s3, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&c->ev_fork, &c->ev_dh, &c->ev_join, &c->ev_pre, &c->ev_lg, &c->ev_lg_join})
     SLIDE_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+}
+
+static int32_t* hg_tickets(slide_ctx* c, int b) {
+  if (c->hg_done_n < b) {
+    int32_t* p = c->hg_done.ensure<int32_t>(b);
+    SLIDE_CUDA(cudaMemset(p, 0, (size_t)b * 4));
+    c->hg_done_n = b;
+  }
+  return c->hg_done.as<int32_t>();
 }
 
 static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration, int64_t slot_offset,
@@ -640,7 +658,22 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   gr.run(prow, pslot, offs + b, 0, P_max, s);
   c->grow_pending = true;
   c->timer.mark(s, kStGroupRows);
-  launch_logits_rows(hp, b, gr.view(), pslot, d.w2, d.b2, h, z, s);
+  {
+    // per-row logits of the sparse tiles beside the dense tiles (third stream)
+    const bool fork = !c->timer.on;
+    cudaStream_t sr = s;
+    if (fork) {
+      side_stream_init(c);
+      sr = c->s3;
+      SLIDE_CUDA(cudaEventRecord(c->ev_lg, s));
+      SLIDE_CUDA(cudaStreamWaitEvent(sr, c->ev_lg, 0));
+    }
+    launch_logits_rows(hp, b, gr.view(), pslot, d.w2, d.b2, h, z, s, sr);
+    if (fork) {
+      SLIDE_CUDA(cudaEventRecord(c->ev_lg_join, sr));
+      SLIDE_CUDA(cudaStreamWaitEvent(s, c->ev_lg_join, 0));
+    }
+  }
   c->timer.mark(s, kStLogits);
   // sharded: the softmax is completed by the slide_shard_softmax_* stages
   if (c->G == 1) launch_softmax(b, offs, plab, bt->y_ptr, z, prob, delta, loss, s);
@@ -679,6 +712,13 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
     sw = c->s2;
     SLIDE_CUDA(cudaEventRecord(c->ev_fork, s));
     SLIDE_CUDA(cudaStreamWaitEvent(sw, c->ev_fork, 0));
+    if (c->grow_pending && update) {
+      // the row grouping's masks were last read by the logits: clear them on
+      // the third stream beside the rest of the backward pass
+      SLIDE_CUDA(cudaStreamWaitEvent(c->s3, c->ev_fork, 0));
+      gr.clear(c->s3);
+      c->grow_pending = false;
+    }
   }
   int32_t* xs = nnz > 0 ? c->xslot.ensure<int32_t>(nnz) : nullptr;
   if (nnz > 0) gf.prepare(d.input_dim, b, nnz);  // host-side sizing before any branch launches
@@ -693,8 +733,8 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
   if (!dh) {
     float* out = c->dh.ensure<float>((size_t)b * hp);
     launch_hidden_grad(hp, b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->delta.as<float>(), d.w2,
-                       c->h.as<float>(), out,
-                       c->partial.ensure<float>(hidden_grad_scratch(b, hp)), s);
+                       c->h.as<float>(), out, c->partial.ensure<float>(hidden_grad_scratch(b, hp)),
+                       hg_tickets(c, b), update ? c->work.ensure<int32_t>(4) : nullptr, s);
     dh = out;
   }
   c->timer.mark(s, kStHiddenGrad);
@@ -741,7 +781,8 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
   if (P_max > 0) {
     launch_adam_rows(hp, b, ap, gr.n_uniq.as<int32_t>(), gr.u_max, gr.uniq.as<int32_t>(), gr.seg_off.as<int32_t>(),
                      gr.seg_cnt.as<int32_t>(), gr.order.as<int32_t>(), c->pslot.as<int32_t>(), c->delta.as<float>(),
-                     c->h.as<float>(), d.w2, d.m2, d.v2, d.b2, d.mb2, d.vb2, d.steps2, ctr, work, s);
+                     c->h.as<float>(), d.w2, d.m2, d.v2, d.b2, d.mb2, d.vb2, d.steps2, ctr, work,
+                     /*work_zeroed=*/ext_dh == nullptr, s);
     c->timer.mark(s, kStAdamRows);
   }
   if (!fork) w1_update(s);
@@ -755,9 +796,11 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
     gr.clear(s);
     c->grow_pending = false;
   }
-  if (fork) {  // join: the next step reads W1, h and the side stream's buffers
+  if (fork) {  // join: the next step reads W1, h and the side streams' buffers
     SLIDE_CUDA(cudaEventRecord(c->ev_join, sw));
     SLIDE_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+    SLIDE_CUDA(cudaEventRecord(c->ev_lg_join, c->s3));
+    SLIDE_CUDA(cudaStreamWaitEvent(s, c->ev_lg_join, 0));
   }
 }
 
@@ -1076,8 +1119,8 @@ int slide_shard_hidden_grad(slide_ctx* c, float* dh_out) {
     const int b = c->last_b, hp = c->hp;
     // unmasked partial (h = null): masking commutes with the all-reduce
     launch_hidden_grad(hp, b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->delta.as<float>(), c->d.w2, nullptr,
-                       dh_out,
-                       c->partial.ensure<float>(hidden_grad_scratch(b, hp)), c->s);
+                       dh_out, c->partial.ensure<float>(hidden_grad_scratch(b, hp)), hg_tickets(c, b), nullptr,
+                       c->s);
   });
 }
 

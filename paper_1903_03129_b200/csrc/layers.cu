@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(256) logits_rows_kernel(int hp, int b, GroupVi
 }
 
 void launch_logits_rows(int hp, int b, const GroupView& g, const int32_t* pslot, const float* w2, const float* b2,
-                        const float* h, float* z, cudaStream_t s) {
+                        const float* h, float* z, cudaStream_t s, cudaStream_t s_rows) {
   if (g.u_max <= 0) return;
   // dense tiles need the whole batch's slot masks in 32 words and k in whole stages
   const int dense_ok = b <= 32 * kMaskWords && hp % kKC == 0;
@@ -323,7 +323,7 @@ void launch_logits_rows(int hp, int b, const GroupView& g, const int32_t* pslot,
     SLIDE_LAUNCH_CHECK();
   }
   const int rgrid = (int)std::min<int64_t>(ceil_div(g.u_max, 8), (int64_t)kSms * 8);
-  SLIDE_NV_DISPATCH(hp, (logits_rows_kernel<NV><<<rgrid, 256, 0, s>>>(hp, b, g, pslot, w2, b2, h, z, dense_ok)));
+  SLIDE_NV_DISPATCH(hp, (logits_rows_kernel<NV><<<rgrid, 256, 0, s_rows>>>(hp, b, g, pslot, w2, b2, h, z, dense_ok)));
   SLIDE_LAUNCH_CHECK();
 }
 
@@ -395,8 +395,13 @@ __global__ void __launch_bounds__(256) hidden_grad_kernel(int hp, int b, int sli
                                                           const int32_t* __restrict__ prow,
                                                           const float* __restrict__ delta,
                                                           const float* __restrict__ w2,
-                                                          const float* __restrict__ h, float* __restrict__ out) {
+                                                          const float* __restrict__ h, float* __restrict__ part,
+                                                          float* __restrict__ dh, int32_t* __restrict__ done,
+                                                          int32_t* __restrict__ work_reset) {
   __shared__ float red[8][NV * 128];
+  __shared__ int s_last;
+  // the W2 Adam's row counter: its previous use is over, its next comes after
+  if (work_reset && blockIdx.x == 0 && threadIdx.x == 0) *work_reset = 0;
   const int i = blockIdx.x / slices, sl = blockIdx.x - i * slices;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int o = offs[i], n = offs[i + 1] - o;
@@ -446,18 +451,24 @@ __global__ void __launch_bounds__(256) hidden_grad_kernel(int hp, int b, int sli
 #pragma unroll
     for (int w = 1; w < 8; ++w) sum += red[w][c];
     const int64_t q = (int64_t)i * hp + c;
-    if (slices == 1) out[q] = (h == nullptr || h[q] > 0.f) ? sum : 0.f;  // h == null: unmasked partial
-    else out[(int64_t)sl * b * hp + q] = sum;
+    if (slices == 1) dh[q] = (h == nullptr || h[q] > 0.f) ? sum : 0.f;  // h == null: unmasked partial
+    else part[(int64_t)sl * b * hp + q] = sum;
   }
-}
-
-__global__ void slice_sum_kernel(int64_t n, int slices, const float* __restrict__ part, const float* __restrict__ h,
-                                 float* __restrict__ dh) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-    float s = part[q];
-    for (int sl = 1; sl < slices; ++sl) s += part[(int64_t)sl * n + q];
-    dh[q] = (h == nullptr || h[q] > 0.f) ? s : 0.f;
+  if (slices == 1) return;
+  // the sample's last slice to finish adds the slices in slice order
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(done + i, 1) == slices - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int c = threadIdx.x; c < hp; c += 256) {
+    const int64_t q = (int64_t)i * hp + c;
+    float sum = __ldcg(part + q);
+    for (int t = 1; t < slices; ++t) sum += __ldcg(part + (int64_t)t * b * hp + q);
+    dh[q] = (h == nullptr || h[q] > 0.f) ? sum : 0.f;
   }
+  if (threadIdx.x == 0) done[i] = 0;  // self-resetting
 }
 
 int hidden_grad_slices(int b) { return std::max(1, std::min(8, (int)ceil_div((int64_t)kSms * 4, b))); }
@@ -465,17 +476,12 @@ int hidden_grad_slices(int b) { return std::max(1, std::min(8, (int)ceil_div((in
 size_t hidden_grad_scratch(int b, int hp) { return (size_t)hidden_grad_slices(b) * b * hp; }
 
 void launch_hidden_grad(int hp, int b, const int32_t* offs, const int32_t* prow, const float* delta, const float* w2,
-                        const float* h, float* dh, float* part, cudaStream_t s) {
+                        const float* h, float* dh, float* part, int32_t* done, int32_t* work_reset, cudaStream_t s) {
   if (b <= 0) return;
   const int S = hidden_grad_slices(b);
-  float* out = S == 1 ? dh : part;
-  SLIDE_NV_DISPATCH(hp, (hidden_grad_kernel<NV><<<b * S, 256, 0, s>>>(hp, b, S, offs, prow, delta, w2, h, out)));
+  SLIDE_NV_DISPATCH(hp, (hidden_grad_kernel<NV><<<b * S, 256, 0, s>>>(hp, b, S, offs, prow, delta, w2, h, part, dh, done,
+                                                                      work_reset)));
   SLIDE_LAUNCH_CHECK();
-  if (S > 1) {
-    const int64_t n = (int64_t)b * hp;
-    slice_sum_kernel<<<(int)ceil_div(n, 256), 256, 0, s>>>(n, S, part, h, dh);
-    SLIDE_LAUNCH_CHECK();
-  }
 }
 
 // ----------------------------------------------------------- Adam, W2 rows
@@ -697,9 +703,9 @@ void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq
                       const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
                       const int32_t* sorted_pairs, const int32_t* pslot, const float* delta, const float* h,
                       float* w2, float* m2, float* v2, float* b2, float* mb2, float* vb2, int64_t* steps2,
-                      unsigned long long* touched, int32_t* work, cudaStream_t s) {
+                      unsigned long long* touched, int32_t* work, bool work_zeroed, cudaStream_t s) {
   if (max_uniq <= 0) return;
-  SLIDE_CUDA(cudaMemsetAsync(work, 0, 4, s));
+  if (!work_zeroed) SLIDE_CUDA(cudaMemsetAsync(work, 0, 4, s));
   // persistent: as many CTAs as are resident at once
   const int per_sm = hp <= 128 ? 3 : 2;
   const int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * per_sm);
