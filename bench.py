@@ -57,6 +57,7 @@ def parse():
     p.add_argument("--workload", default="wide_in")
     p.add_argument("--schedule", default="snapshot", choices=["snapshot", "sequential"])
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-flush", action="store_true", help="experiments only: keep L2 warm between steps")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-samples", type=int, default=128)
     return p.parse_args()
@@ -233,7 +234,8 @@ def run_ours(args, rank, world):
     losses = []
     with sampler as clk:
         for it in range(W + 1, W + K + 1):
-            flush.zero_()
+            if not args.no_flush:
+                flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record()

@@ -14,7 +14,8 @@ import threading
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libslide_b200.so")
+LIB_PATH = os.environ.get("SLIDE_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                             "libslide_b200.so")
 
 i64 = C.c_int64
 u64 = C.c_uint64
