@@ -13,6 +13,7 @@ using namespace slide;
 
 namespace slide {
 unsigned long long g_slide_launches = 0;
+unsigned long long g_slide_realloc_gen = 0;
 }
 
 // Per-stage CUDA-event timing (slide_profile): consecutive marks on the
@@ -102,6 +103,7 @@ struct slide_ctx {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   int graph_state = 0;  // 0: shapes new (run eagerly), 1: capture next, 2: replay
+  unsigned long long graph_gen = 0;  // g_slide_realloc_gen the graph was captured under
   DBuf bias_table;
   int64_t bias_n = 0;
   int bias_exact = 1;
@@ -934,6 +936,10 @@ static void graph_step_launch(slide_ctx* c, const slide_batch* bt, int64_t itera
         c->grow.clear(gs);
         c->grow_pending = false;
       }
+      // a buffer the graph points into moved (e.g. a table rebuild with more
+      // bucket runs than before): one eager step re-sizes every buffer for
+      // the new tables (a capture must not allocate), then capture again
+      if (c->graph_state == 2 && c->graph_gen != g_slide_realloc_gen) c->graph_state = 0;
       if (c->graph_state < 2) c->timer.on = c->graph_state == 0 && timing;
       if (c->graph_state == 0) {
         c->w1_prefork = true;
@@ -944,6 +950,12 @@ static void graph_step_launch(slide_ctx* c, const slide_batch* bt, int64_t itera
       } else if (c->graph_state == 1) {
         c->timer.on = false;
         const unsigned long long lc0 = g_slide_launches;
+        if (c->gexec) {  // the previous graph's last replay is complete (stream synchronised above)
+          cudaGraphExecDestroy(c->gexec);
+          cudaGraphDestroy(c->graph);
+          c->gexec = nullptr;
+          c->graph = nullptr;
+        }
         SLIDE_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
         try {
           c->w1_prefork = true;
@@ -958,6 +970,7 @@ static void graph_step_launch(slide_ctx* c, const slide_batch* bt, int64_t itera
           throw;
         }
         SLIDE_CUDA(cudaStreamEndCapture(gs, &c->graph));
+        c->graph_gen = g_slide_realloc_gen;
         // captured launches were counted once; every replay runs them again
         c->g_kernels = g_slide_launches - lc0;
         SLIDE_CUDA(cudaGraphInstantiate(&c->gexec, c->graph, 0));

@@ -28,7 +28,8 @@ enum Status : int {
   do {                                                                                \
     cudaError_t _e = (expr);                                                          \
     if (_e != cudaSuccess)                                                            \
-      throw ::slide::Error(::slide::kCudaError, std::string(#expr) + ": " +          \
+      throw ::slide::Error(::slide::kCudaError, std::string(#expr) + " (" + __FILE__ + ":" +   \
+                                                    std::to_string(__LINE__) + "): " +               \
                                                     cudaGetErrorString(_e));         \
   } while (0)
 

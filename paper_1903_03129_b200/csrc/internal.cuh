@@ -6,6 +6,10 @@
 
 namespace slide {
 
+// Bumped whenever any DBuf changes its address: a captured step graph holds
+// raw pointers, so a step graph captured before the bump must be re-captured.
+extern unsigned long long g_slide_realloc_gen;
+
 // Growable device buffer (cudaMalloc'd; contents undefined after grow).
 struct DBuf {
   void* p = nullptr;
@@ -18,6 +22,7 @@ struct DBuf {
     if (need > bytes) {
       if (p) SLIDE_CUDA(cudaFree(p));
       p = nullptr;
+      ++g_slide_realloc_gen;
       size_t grow = bytes ? bytes + bytes / 2 : 0;
       size_t alloc = need > grow ? need : grow;
       alloc = (alloc + 255) & ~(size_t)255;
@@ -29,7 +34,10 @@ struct DBuf {
   template <typename T>
   T* as() const { return reinterpret_cast<T*>(p); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      cudaFree(p);
+      ++g_slide_realloc_gen;
+    }
     p = nullptr;
     bytes = 0;
   }

@@ -114,3 +114,40 @@ def test_full_size_training_lowers_the_loss_and_keeps_sets_bounded():
     assert np.mean(losses[-5:]) < np.mean(losses[:5])
     # full-union vanilla: |A_i| <= L * cap + |Y_i|
     assert max(fracs) * W.n_out <= W.l * W.cap + 400
+
+
+def test_graph_steps_across_a_rebuild_that_moves_table_buffers():
+    """Scaled-family shape (DWTA K8 L64, H=256, B=1024) at 1M rows with a
+    rebuild after every other step: a rebuild can need more bucket runs than
+    any earlier build, which moves the table buffers the captured step graph
+    points into; the graph must be re-captured (it used to replay stale
+    pointers: illegal address).  Graph steps stay bit-identical to eager."""
+    import dataclasses
+
+    from paper_1903_03129_b200.configs import SCALED
+    from paper_1903_03129_b200.data import synthetic_corpus
+
+    w = dataclasses.replace(SCALED, n_out=1_000_000, n0=2)
+    corpus = synthetic_corpus(dataclasses.replace(w.corpus, num_labels=w.n_out), 4 * w.batch, seed=0)
+    batches = []
+    for s in range(4):
+        sub = corpus.subset(np.arange(s * w.batch, (s + 1) * w.batch))
+        batches.append(HostCsr(sub.x_ptr.astype(np.int32), sub.x_idx, sub.x_val, sub.y_ptr.astype(np.int32), sub.y_idx))
+
+    def run(graphs):
+        cfg = TrainConfig(batch_size=w.batch, learning_rate=w.lr, n0=w.n0, seed=0)
+        spec = LshLayerConfig(w.family, k=w.k, l=w.l, capacity=w.cap, policy=w.policy, wta_bin_size=w.bin_size,
+                              sampler=SamplerConfig(w.strategy, beta=w.beta))
+        net = SlideNetwork(w.input_dim, [w.hidden, w.n_out], cfg, lsh_layers={1: spec})
+        net.use_graphs = graphs
+        stats = [net.train_batch_csr(b, it, schedule="snapshot") for it, b in enumerate(batches, start=1)]
+        out = ([s.loss for s in stats], [s.rebuilt for s in stats], net.w2.cpu().numpy(), net.v2.cpu().numpy())
+        del net
+        torch.cuda.empty_cache()
+        return out
+
+    a, b = run(True), run(False)
+    assert a[0] == b[0] and a[1] == b[1]
+    assert sum(bool(r) for r in a[1]) >= 2
+    for x, y in zip(a[2:], b[2:]):
+        np.testing.assert_array_equal(x, y)
