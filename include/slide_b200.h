@@ -175,7 +175,8 @@ int slide_graph_step_wait(slide_ctx* ctx, double* loss_host, int64_t* active_hos
  * 3 pair rows (P) i32 | 4 pair label flag (P) u8 | 5 probs (P) f32 |
  * 6 delta (P) f32 | 7 loss (B) f64 | 8 dh (B, hp) f32 | 9 empty (B) i32 |
  * 10 rng states (B, 6) u64 | 11 logits (P) f32 (before softmax) |
- * 12 global active-set size per slot (B) i32 */
+ * 12 global active-set size per slot (B) i32 | 13 live hidden units (1 + hp) i32:
+ * the count, then the units nonzero in some sample ascending, then the rest */
 int slide_read(slide_ctx* ctx, int64_t what, void* host_dst, int64_t max_bytes, int64_t* bytes);
 
 /* Ranked sampled inference for the last forward (reference network.py:383-391,

@@ -78,6 +78,8 @@ struct slide_ctx {
   DBuf sh_packed, sh_packed_t, dw_perms, dw_donors, rowkeys;
   // forward workspace
   DBuf h, qkeys, order, states, act, cnt, empty, offs, prow, pslot, plab, z, prob, delta, loss, dh;
+  // live hidden units of the last forward (see launch_hidden_forward)
+  DBuf hmask, live, live_ticket;
   DBuf fb_ids, fb_scratch, fb_bitmap;
   // backward workspace
   GroupBy grow, gfeat;
@@ -284,7 +286,7 @@ int slide_destroy(slide_ctx* c) {
     if (!c) return;
     cudaStreamSynchronize(c->s);
     c->tab.release();
-    for (DBuf* b : {&c->sh_packed, &c->sh_packed_t, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->qkeys, &c->order,
+    for (DBuf* b : {&c->sh_packed, &c->sh_packed_t, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->hmask, &c->live, &c->live_ticket, &c->qkeys, &c->order,
                     &c->states, &c->act, &c->cnt, &c->empty, &c->offs, &c->prow, &c->pslot, &c->plab, &c->z,
                     &c->prob, &c->delta, &c->loss, &c->dh, &c->fb_ids, &c->fb_scratch, &c->fb_bitmap, &c->xslot,
                     &c->tc, &c->bc, &c->counters, &c->partial, &c->long_list, &c->n_long, &c->work, &c->topk_out, &c->topk_cnt, &c->tc_scratch, &c->bias_table, &c->cnt_all})
@@ -492,6 +494,13 @@ static void side_stream_init(slide_ctx* c) {
     SLIDE_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
 }
 
+static int32_t* live_ticket(slide_ctx* c) {
+  if (c->live_ticket.bytes == 0) {
+    SLIDE_CUDA(cudaMemset(c->live_ticket.ensure<int32_t>(1), 0, 4));
+  }
+  return c->live_ticket.as<int32_t>();
+}
+
 static int32_t* hg_tickets(slide_ctx* c, int b) {
   if (c->hg_done_n < b) {
     int32_t* p = c->hg_done.ensure<int32_t>(b);
@@ -541,8 +550,10 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   }
 
   float* h = c->h.ensure<float>((size_t)b * hp);
+  uint32_t* hmask = c->hmask.ensure<uint32_t>((size_t)b * (hp / 32));
+  int32_t* live = c->live.ensure<int32_t>(1 + hp);
   c->timer.mark(s, kStStart);
-  launch_hidden_forward(hp, b, bt->x_ptr, bt->x_idx, bt->x_val, d.w1t, d.b1, h, s);
+  launch_hidden_forward(hp, b, bt->x_ptr, bt->x_idx, bt->x_val, d.w1t, d.b1, h, hmask, live, live_ticket(c), s);
   c->timer.mark(s, kStHidden);
   c->host_counts[2] += b;
 
@@ -670,7 +681,7 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
       SLIDE_CUDA(cudaEventRecord(c->ev_lg, s));
       SLIDE_CUDA(cudaStreamWaitEvent(sr, c->ev_lg, 0));
     }
-    launch_logits_rows(hp, b, gr.view(), pslot, d.w2, d.b2, h, z, s, sr);
+    launch_logits_rows(hp, b, gr.view(), pslot, d.w2, d.b2, h, live, z, s, sr);
     if (fork) {
       SLIDE_CUDA(cudaEventRecord(c->ev_lg_join, sr));
       SLIDE_CUDA(cudaStreamWaitEvent(s, c->ev_lg_join, 0));
@@ -735,7 +746,8 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
   if (!dh) {
     float* out = c->dh.ensure<float>((size_t)b * hp);
     launch_hidden_grad(hp, b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->delta.as<float>(), d.w2,
-                       c->h.as<float>(), out, c->partial.ensure<float>(hidden_grad_scratch(b, hp)),
+                       c->h.as<float>(), c->live.as<int32_t>(), out,
+                       c->partial.ensure<float>(hidden_grad_scratch(b, hp)),
                        hg_tickets(c, b), update ? c->work.ensure<int32_t>(4) : nullptr, s);
     dh = out;
   }
@@ -769,8 +781,8 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
     c->w1_grouped = false;
     launch_adam_features(hp, ap, gf.n_uniq.as<int32_t>(), gf.u_max, gf.uniq.as<int32_t>(), gf.seg_off.as<int32_t>(),
                          gf.seg_cnt.as<int32_t>(), gf.order.as<int32_t>(), xs, c->last_xval, c->last_xbase,
-                         c->h.as<float>(), dh, bc, d.w1t, d.m1t, d.v1t, ctr ? ctr + 1 : nullptr, long_list, n_long,
-                         st);
+                         c->h.as<float>(), dh, bc, c->live.as<int32_t>(), d.w1t, d.m1t, d.v1t,
+                         ctr ? ctr + 1 : nullptr, long_list, n_long, st);
     c->timer.mark(st, kStAdamFeat);
     gf.clear(st);
   };
@@ -783,7 +795,8 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
   if (P_max > 0) {
     launch_adam_rows(hp, b, ap, gr.n_uniq.as<int32_t>(), gr.u_max, gr.uniq.as<int32_t>(), gr.seg_off.as<int32_t>(),
                      gr.seg_cnt.as<int32_t>(), gr.order.as<int32_t>(), c->pslot.as<int32_t>(), c->delta.as<float>(),
-                     c->h.as<float>(), d.w2, d.m2, d.v2, d.b2, d.mb2, d.vb2, d.steps2, ctr, work,
+                     c->h.as<float>(), c->live.as<int32_t>(), d.w2, d.m2, d.v2, d.b2, d.mb2, d.vb2, d.steps2, ctr,
+                     work,
                      /*work_zeroed=*/ext_dh == nullptr, s);
     c->timer.mark(s, kStAdamRows);
   }
@@ -1066,6 +1079,7 @@ int slide_read(slide_ctx* c, int64_t what, void* dst, int64_t max_bytes, int64_t
       case 10: src = c->states.p; n = b * 48; break;
       case 11: src = c->z.p; n = P * 4; break;
       case 12: src = c->G > 1 ? c->cnt_all.p : c->cnt.p; n = b * 4; break;
+      case 13: src = c->live.p; n = (1 + hp) * 4; break;
       default: throw Error(kValueError, "unknown stage");
     }
     SLIDE_CHECK(src != nullptr || n == 0, kValueError, "stage not computed");
@@ -1132,8 +1146,8 @@ int slide_shard_hidden_grad(slide_ctx* c, float* dh_out) {
     const int b = c->last_b, hp = c->hp;
     // unmasked partial (h = null): masking commutes with the all-reduce
     launch_hidden_grad(hp, b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->delta.as<float>(), c->d.w2, nullptr,
-                       dh_out, c->partial.ensure<float>(hidden_grad_scratch(b, hp)), hg_tickets(c, b), nullptr,
-                       c->s);
+                       c->live.as<int32_t>(), dh_out, c->partial.ensure<float>(hidden_grad_scratch(b, hp)),
+                       hg_tickets(c, b), nullptr, c->s);
   });
 }
 
@@ -1184,6 +1198,9 @@ int slide_write(slide_ctx* c, int64_t what, const void* src, int64_t bytes) {
     }
     SLIDE_CHECK(bytes == n, kValueError, "size mismatch for stage write");
     if (n) SLIDE_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, c->s));
+    // a replayed h has its own live units
+    if (what == 0)
+      launch_live_cols_from_h(c->hp, c->last_b, c->h.as<float>(), c->hmask.as<uint32_t>(), c->live.as<int32_t>(), c->s);
     SLIDE_CUDA(cudaStreamSynchronize(c->s));
   });
 }

@@ -100,13 +100,20 @@ struct AdamParams {
   int table_exact;      // beyond the table both factors are exactly (lr, 1) in fp32
 };
 
+// h = relu(x W1 + b1); hmask (b x hp/32) = per-sample nonzero bits; the last
+// CTA writes live (1 + hp ints): the number of units nonzero anywhere in the
+// batch, then the live units ascending followed by the dead ones.  ticket:
+// one zero-initialised int (self-resetting).
 void launch_hidden_forward(int hp, int b, const int32_t* x_ptr, const int32_t* x_idx, const float* x_val,
-                           const float* w1t, const float* b1, float* h, cudaStream_t s);
+                           const float* w1t, const float* b1, float* h, uint32_t* hmask, int32_t* live,
+                           int32_t* ticket, cudaStream_t s);
+// the same live-unit list from an h written by other means
+void launch_live_cols_from_h(int hp, int b, const float* h, uint32_t* hmask, int32_t* live, cudaStream_t s);
 
 // s_rows: the stream of the per-row (sparse tile) kernel, concurrent with
 // the dense tiles on s (the caller joins it)
 void launch_logits_rows(int hp, int b, const GroupView& g, const int32_t* pslot, const float* w2, const float* b2,
-                        const float* h, float* z, cudaStream_t s, cudaStream_t s_rows);
+                        const float* h, const int32_t* live, float* z, cudaStream_t s, cudaStream_t s_rows);
 
 void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
                     float* prob, float* delta, double* loss, cudaStream_t s);
@@ -115,12 +122,13 @@ size_t hidden_grad_scratch(int b, int hp);
 // done: b zero-initialised ints (self-resetting); work_reset (optional): the
 // W2 Adam's row counter, zeroed here
 void launch_hidden_grad(int hp, int b, const int32_t* offs, const int32_t* prow, const float* delta, const float* w2,
-                        const float* h, float* dh, float* part, int32_t* done, int32_t* work_reset, cudaStream_t s);
+                        const float* h, const int32_t* live, float* dh, float* part, int32_t* done,
+                        int32_t* work_reset, cudaStream_t s);
 void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq,
                       const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
                       const int32_t* sorted_pairs, const int32_t* pslot, const float* delta, const float* h,
-                      float* w2, float* m2, float* v2, float* b2, float* mb2, float* vb2, int64_t* steps2,
-                      unsigned long long* touched, int32_t* work, bool work_zeroed, cudaStream_t s);
+                      const int32_t* live, float* w2, float* m2, float* v2, float* b2, float* mb2, float* vb2,
+                      int64_t* steps2, unsigned long long* touched, int32_t* work, bool work_zeroed, cudaStream_t s);
 void launch_accumulate(unsigned long long* dst, const int32_t* src, cudaStream_t s);
 // per slot: the k best active ids by probability (ties: lower id), -1 padded
 void launch_topk(int b, const int32_t* offs, const int32_t* rows, int shard_count, int shard_rank, const float* prob,
@@ -131,8 +139,9 @@ void launch_hidden_counts(int hp, int b, const AdamParams& ap, const float* h, c
 void launch_adam_features(int hp, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq,
                           const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
                           const int32_t* sorted_k, const int32_t* x_slot, const float* x_val, int64_t x_base,
-                          const float* h, const float* dh, const float2* bc, float* w1t, float* m1t, float* v1t,
-                          unsigned long long* touched, int32_t* long_list, int32_t* n_long, cudaStream_t s);
+                          const float* h, const float* dh, const float2* bc, const int32_t* live, float* w1t,
+                          float* m1t, float* v1t, unsigned long long* touched, int32_t* long_list, int32_t* n_long,
+                          cudaStream_t s);
 void launch_hidden_prep_bias(int hp, int b, const AdamParams& ap, const float* h, const float* dh, int64_t* steps1,
                              int32_t* tc, float2* bc, float* b1, float* mb1, float* vb1, cudaStream_t s);
 void launch_adam_hidden_bias(int hp, int b, const AdamParams& ap, const float* h, const float* dh, const int32_t* tc,

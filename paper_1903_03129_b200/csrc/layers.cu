@@ -39,13 +39,69 @@ struct FwdWarps {
   static constexpr int value = NV <= 2 ? 32 : 8;  // static smem: warps x hp floats <= 32 KB
 };
 
+// ------------------------------------------------------------ live columns
+// The hidden units that are nonzero in at least one sample of the batch.  A
+// unit c with h_i[c] = 0 for every i moves nothing downstream: its logit
+// terms are exact zeros, its hidden-error entries are masked, its W1 / W2
+// Adam coordinates stay frozen -- the reference itself only touches
+// W[A, nz(h)] (network.py:266, 322-332).  live[0] = n live units,
+// live[1..hp] = a permutation of the units: the live ones ascending, then the
+// dead ones ascending.  Row kernels map lane l of 32-column group g to unit
+// live[1 + 32 g + l] and walk only the ceil(n / 32) groups that hold live
+// units; the tail lanes of the last group land on dead units (h = 0
+// everywhere), so they need no predicate.  After the first step of the
+// BASELINE workloads ~26 of 128 units stay live batch-wide.
+// Whole CTA; hmask (b x hp/32 words, bit = h > 0) written by other CTAs.
+__device__ void build_live_cols(int hp, int b, const uint32_t* hmask, int32_t* __restrict__ live) {
+  __shared__ uint32_t words[32];
+  const int mw = hp >> 5;
+  for (int w = threadIdx.x; w < mw; w += blockDim.x) words[w] = 0u;
+  __syncthreads();
+  for (int q = threadIdx.x; q < b * mw; q += blockDim.x) {
+    const uint32_t v = __ldcg(hmask + q);
+    if (v) atomicOr(&words[q % mw], v);
+  }
+  __syncthreads();
+  int n = 0;
+  for (int w = 0; w < mw; ++w) n += __popc(words[w]);
+  for (int c = threadIdx.x; c < hp; c += blockDim.x) {
+    const int w = c >> 5;
+    int before = 0;  // live units below c
+    for (int k = 0; k < w; ++k) before += __popc(words[k]);
+    before += __popc(words[w] & ((1u << (c & 31)) - 1u));
+    const bool on = (words[w] >> (c & 31)) & 1u;
+    live[1 + (on ? before : n + (c - before))] = c;
+  }
+  if (threadIdx.x == 0) live[0] = n;
+}
+
+__global__ void __launch_bounds__(1024) live_cols_from_h_kernel(int hp, int b, const float* __restrict__ h,
+                                                                uint32_t* __restrict__ hmask, int32_t* __restrict__ live) {
+  const int mw = hp >> 5;
+  for (int q = threadIdx.x; q < b * hp; q += blockDim.x) {  // hp % 32 == 0: warps stay inside one word
+    const unsigned bal = __ballot_sync(0xffffffffu, h[q] > 0.f);
+    if ((threadIdx.x & 31) == 0) hmask[(q / hp) * mw + (q % hp) / 32] = bal;
+  }
+  __threadfence_block();
+  __syncthreads();
+  build_live_cols(hp, b, hmask, live);
+}
+
+void launch_live_cols_from_h(int hp, int b, const float* h, uint32_t* hmask, int32_t* live, cudaStream_t s) {
+  if (b <= 0) return;
+  live_cols_from_h_kernel<<<1, 1024, 0, s>>>(hp, b, h, hmask, live);
+  SLIDE_LAUNCH_CHECK();
+}
+
 template <int NV, int kFwdWarps = FwdWarps<NV>::value>
 __global__ void __launch_bounds__(kFwdWarps * 32) hidden_fwd_kernel(int hp, const int32_t* __restrict__ x_ptr,
                                                                     const int32_t* __restrict__ x_idx,
                                                                     const float* __restrict__ x_val,
                                                                     const float* __restrict__ w1t,
                                                                     const float* __restrict__ b1,
-                                                                    float* __restrict__ h) {
+                                                                    float* __restrict__ h, uint32_t* __restrict__ hmask,
+                                                                    int32_t* __restrict__ live,
+                                                                    int32_t* __restrict__ ticket) {
   __shared__ float red[kFwdWarps][NV * 128];
   const int i = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int a = x_ptr[i], e = x_ptr[i + 1];
@@ -95,16 +151,56 @@ __global__ void __launch_bounds__(kFwdWarps * 32) hidden_fwd_kernel(int hp, cons
 #pragma unroll 8
     for (int w = 1; w < kFwdWarps; ++w) s += red[w][c];
     s += b1[c];
-    h[(int64_t)i * hp + c] = s > 0.f ? s : 0.f;
+    const float hv = s > 0.f ? s : 0.f;
+    h[(int64_t)i * hp + c] = hv;
+    // warps cover 32 consecutive units (hp % 32 == 0): one mask word each
+    const unsigned bal = __ballot_sync(0xffffffffu, hv > 0.f);
+    if (lane == 0) hmask[(int64_t)i * (hp >> 5) + (c >> 5)] = bal;
   }
+  // the batch's last CTA to finish builds the live-unit permutation
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  build_live_cols(hp, gridDim.x, hmask, live);
+  if (threadIdx.x == 0) *ticket = 0;  // self-resetting
 }
 
 void launch_hidden_forward(int hp, int b, const int32_t* x_ptr, const int32_t* x_idx, const float* x_val,
-                           const float* w1t, const float* b1, float* h, cudaStream_t s) {
+                           const float* w1t, const float* b1, float* h, uint32_t* hmask, int32_t* live,
+                           int32_t* ticket, cudaStream_t s) {
   if (b <= 0) return;
-  SLIDE_NV_DISPATCH(hp, (hidden_fwd_kernel<NV><<<b, FwdWarps<NV>::value * 32, 0, s>>>(hp, x_ptr, x_idx, x_val, w1t, b1, h)));
+  SLIDE_NV_DISPATCH(hp, (hidden_fwd_kernel<NV><<<b, FwdWarps<NV>::value * 32, 0, s>>>(hp, x_ptr, x_idx, x_val, w1t, b1,
+                                                                                     h, hmask, live, ticket)));
   SLIDE_LAUNCH_CHECK();
 }
+
+// lane's unit in each of the G = hp / 32 groups (see build_live_cols); returns
+// the number of groups that hold live units
+template <int G>
+__device__ __forceinline__ int live_lanes(const int32_t* __restrict__ live, int (&col)[G]) {
+  const int lane = threadIdx.x & 31;
+  const int n = __ldg(live);
+#pragma unroll
+  for (int g = 0; g < G; ++g) col[g] = __ldg(live + 1 + g * 32 + lane);
+  return (n + 31) >> 5;
+}
+
+// Device-side dispatch on the live group count ng (read on the device, so
+// graph replays adapt): FN<NG>(...) with NG >= max(ng, 1) from a short list.
+#define SLIDE_NG_DISPATCH(NV, ng, FN, ...)                                  \
+  do {                                                                      \
+    if ((ng) <= 1) FN<1>(__VA_ARGS__);                                      \
+    else if ((ng) == 2) FN<2>(__VA_ARGS__);                                 \
+    else if ((NV) == 1) FN<4>(__VA_ARGS__);                                 \
+    else if ((ng) <= 4) FN<4>(__VA_ARGS__);                                 \
+    else if ((NV) == 2) FN<(NV) * 4>(__VA_ARGS__);                          \
+    else if ((ng) <= 8) FN<8>(__VA_ARGS__);                                 \
+    else FN<(NV) * 4>(__VA_ARGS__);                                         \
+  } while (0)
 
 // ------------------------------------------------------------ output logits
 // z[p] = W2[row_p] . h[slot_p] + b2[row_p] for every (slot, active row)
@@ -135,15 +231,17 @@ __device__ __forceinline__ float reduce4(float v0, float v1, float v2, float v3,
 template <int NV>
 __device__ __forceinline__ void logits_row_warp(int hp, int64_t u, const GroupView& g, const int32_t* __restrict__ pslot,
                                                 const float* __restrict__ w2, const float* __restrict__ b2,
-                                                const float* __restrict__ h, float* __restrict__ z) {
+                                                const float* __restrict__ h, float* __restrict__ z,
+                                                const int (&col)[NV * 4], int ng) {
+  constexpr int G = NV * 4;
   const int lane = threadIdx.x & 31;
   const int mine = ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
   const int r = g.uniq[u];
   const int s0 = g.seg_off[u], len = g.seg_cnt[u];
   const float bias = b2[r];
-  float4 w[NV];
+  float w[G];
 #pragma unroll
-  for (int q = 0; q < NV; ++q) w[q] = ld4(w2 + (int64_t)r * hp + q * 128 + lane * 4);
+  for (int q = 0; q < G; ++q) w[q] = q < ng ? __ldg(w2 + (int64_t)r * hp + col[q]) : 0.f;
   for (int j0 = 0; j0 < len; j0 += 32) {
     const int pl = j0 + lane < len ? g.order[s0 + j0 + lane] : 0;
     const int sl = j0 + lane < len ? pslot[pl] : 0;
@@ -153,16 +251,11 @@ __device__ __forceinline__ void logits_row_warp(int hp, int64_t u, const GroupVi
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const int slot = __shfl_sync(0xffffffffu, sl, min(q2 + t, nc - 1));
-        const float* hr = h + (int64_t)slot * hp + lane * 4;
+        const float* hr = h + (int64_t)slot * hp;
         float d = 0.f;
 #pragma unroll
-        for (int q = 0; q < NV; ++q) {
-          const float4 hv = ld4(hr + q * 128);
-          d = fmaf(w[q].x, hv.x, d);
-          d = fmaf(w[q].y, hv.y, d);
-          d = fmaf(w[q].z, hv.z, d);
-          d = fmaf(w[q].w, hv.w, d);
-        }
+        for (int q = 0; q < G; ++q)
+          if (q < ng) d = fmaf(w[q], __ldg(hr + col[q]), d);
         v[t] = d;
       }
       const float sum = reduce4(v[0], v[1], v[2], v[3], lane);
@@ -174,10 +267,10 @@ __device__ __forceinline__ void logits_row_warp(int hp, int64_t u, const GroupVi
 
 constexpr int kTM = 64;         // rows per tile
 constexpr int kTN = 64;         // samples per tile
-constexpr int kKC = 128;        // k per shared-memory stage
+constexpr int kKC = 32;         // k (live units) per shared-memory stage
 constexpr int kLd = kKC + 4;    // padded row stride (conflict-free float4 reads)
 constexpr int kMaskWords = 32;  // B <= 1024
-constexpr int kTileSmem = (2 * kTM * kLd) * 4 + kTM * kMaskWords * 4 + kTM * 8;
+constexpr int kTileSmem = (2 * kTM * kLd) * 4 + kTM * kMaskWords * 4 + kTM * 8 + kTM * 4;
 
 // dense work item = (64-row tile, 64-sample block).  A row tile goes dense
 // unless its pairs cover < 1/64 of its rows x B cells (then the per-row
@@ -193,18 +286,25 @@ __global__ void __launch_bounds__(256, 2) logits_tiles_kernel(int hp, int b, Gro
                                                               const int32_t* __restrict__ pslot,
                                                               const float* __restrict__ w2,
                                                               const float* __restrict__ b2,
-                                                              const float* __restrict__ h, float* __restrict__ z) {
+                                                              const float* __restrict__ h,
+                                                              const int32_t* __restrict__ live,
+                                                              float* __restrict__ z) {
   extern __shared__ __align__(16) float tsm[];
   float* ws = tsm;                                   // [kTM][kLd]
   float* hs = ws + kTM * kLd;                        // [kTN][kLd]
   int* cum = reinterpret_cast<int*>(hs + kTN * kLd);  // [kTM][kMaskWords] mask popc prefix per row
   int* base_s = cum + kTM * kMaskWords;              // [kTM]
   float* bias_s = reinterpret_cast<float*>(base_s + kTM);
+  int* wrow_s = reinterpret_cast<int*>(bias_s + kTM);  // [kTM] W2 row of each tile row
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const int64_t nu = *g.n_uniq;
   const int64_t tiles = (nu + kTM - 1) / kTM;
   const int nsb = (b + kTN - 1) / kTN;
+  // k runs over the live units only (32 per stage, the last stage's tail on
+  // dead units, whose h is 0): the lane's unit of every stage
+  const int kn = ((__ldg(live) + 31) >> 5) * 32;
+  const int my_c = tid & 31;
   for (int64_t item = blockIdx.x; item < tiles * nsb; item += gridDim.x) {
     const int64_t tile = item / nsb;
     const int s0 = (int)(item - tile * nsb) * kTN;
@@ -220,32 +320,35 @@ __global__ void __launch_bounds__(256, 2) logits_tiles_kernel(int hp, int b, Gro
         run += __popc(mrow[w]);
       }
       base_s[tid] = g.seg_off[u];
-      bias_s[tid] = b2[g.uniq[u]];
+      const int r = g.uniq[u];
+      bias_s[tid] = b2[r];
+      wrow_s[tid] = r;
     }
+    __syncthreads();
     float acc[4][4];
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) acc[j][jj] = 0.f;
-    for (int k0 = 0; k0 < hp; k0 += kKC) {
-      // stage 64 W rows and 64 h rows of this k range: 16 float4 loads in
-      // flight per thread
-      float4 lw[8], lh[8];
+    for (int k0 = 0; k0 < kn; k0 += kKC) {
+      // stage 64 W rows and 64 h rows of these 32 units: 16 loads in flight
+      const int c = __ldg(live + 1 + k0 + my_c);
+      float lw[8], lh[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const int idx = tid + q * 256, row = idx >> 5, c = (idx & 31) * 4;
-        lw[q] = row < nrow ? ld4(w2 + (int64_t)g.uniq[u0 + row] * hp + k0 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-        lh[q] = s0 + row < b ? ld4(h + (int64_t)(s0 + row) * hp + k0 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const int row = (tid >> 5) + q * 8;
+        lw[q] = row < nrow ? __ldg(w2 + (int64_t)wrow_s[row] * hp + c) : 0.f;
+        lh[q] = s0 + row < b ? __ldg(h + (int64_t)(s0 + row) * hp + c) : 0.f;
       }
       __syncthreads();  // previous readers of ws / hs are done
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const int idx = tid + q * 256, row = idx >> 5, c = (idx & 31) * 4;
-        *reinterpret_cast<float4*>(&ws[row * kLd + c]) = lw[q];
-        *reinterpret_cast<float4*>(&hs[row * kLd + c]) = lh[q];
+        const int row = (tid >> 5) + q * 8;
+        ws[row * kLd + my_c] = lw[q];
+        hs[row * kLd + my_c] = lh[q];
       }
       __syncthreads();
-#pragma unroll 4
+#pragma unroll
       for (int kk = 0; kk < kKC; kk += 4) {
         float4 wv[4], hv[4];
 #pragma unroll
@@ -270,8 +373,7 @@ __global__ void __launch_bounds__(256, 2) logits_tiles_kernel(int hp, int b, Gro
           for (int jj = 0; jj < 4; ++jj) acc[j][jj] = fmaf(wv[j].w, hv[jj].w, acc[j][jj]);
       }
     }
-    // pick the pairs out of the 64 x 64 block (cum / base / bias are visible
-    // after the staging barriers)
+    // pick the pairs out of the 64 x 64 block
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int row = ty + 16 * j;
@@ -288,7 +390,7 @@ __global__ void __launch_bounds__(256, 2) logits_tiles_kernel(int hp, int b, Gro
         }
       }
     }
-    __syncthreads();  // cum / base / bias reuse by the next item
+    __syncthreads();  // cum / base / bias / wrow reuse by the next item
   }
 }
 
@@ -296,34 +398,38 @@ __global__ void __launch_bounds__(256, 2) logits_tiles_kernel(int hp, int b, Gro
 template <int NV>
 __global__ void __launch_bounds__(256) logits_rows_kernel(int hp, int b, GroupView g, const int32_t* __restrict__ pslot,
                                                           const float* __restrict__ w2, const float* __restrict__ b2,
-                                                          const float* __restrict__ h, float* __restrict__ z,
+                                                          const float* __restrict__ h,
+                                                          const int32_t* __restrict__ live, float* __restrict__ z,
                                                           int dense_ok) {
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nu = *g.n_uniq;
+  int col[NV * 4];
+  const int ng = live_lanes<NV * 4>(live, col);
   for (int64_t u = gw; u < nu; u += nw) {
     const int64_t u0 = u / kTM * kTM;
     if (dense_ok && tile_is_dense(g, u0, (int)min((int64_t)kTM, nu - u0), b)) continue;  // logits_tiles_kernel
-    logits_row_warp<NV>(hp, u, g, pslot, w2, b2, h, z);
+    logits_row_warp<NV>(hp, u, g, pslot, w2, b2, h, z, col, ng);
   }
 }
 
 void launch_logits_rows(int hp, int b, const GroupView& g, const int32_t* pslot, const float* w2, const float* b2,
-                        const float* h, float* z, cudaStream_t s, cudaStream_t s_rows) {
+                        const float* h, const int32_t* live, float* z, cudaStream_t s, cudaStream_t s_rows) {
   if (g.u_max <= 0) return;
-  // dense tiles need the whole batch's slot masks in 32 words and k in whole stages
-  const int dense_ok = b <= 32 * kMaskWords && hp % kKC == 0;
+  // dense tiles need the whole batch's slot masks in 32 words
+  const int dense_ok = b <= 32 * kMaskWords;
   if (dense_ok) {
     const int grid = (int)std::min<int64_t>(ceil_div(g.u_max, kTM) * ceil_div(b, kTN), (int64_t)kSms * 2);
     SLIDE_NV_DISPATCH(hp, ({
       SLIDE_CUDA(cudaFuncSetAttribute(logits_tiles_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kTileSmem));
-      logits_tiles_kernel<NV><<<grid, 256, kTileSmem, s>>>(hp, b, g, pslot, w2, b2, h, z);
+      logits_tiles_kernel<NV><<<grid, 256, kTileSmem, s>>>(hp, b, g, pslot, w2, b2, h, live, z);
     }));
     SLIDE_LAUNCH_CHECK();
   }
   const int rgrid = (int)std::min<int64_t>(ceil_div(g.u_max, 8), (int64_t)kSms * 8);
-  SLIDE_NV_DISPATCH(hp, (logits_rows_kernel<NV><<<rgrid, 256, 0, s_rows>>>(hp, b, g, pslot, w2, b2, h, z, dense_ok)));
+  SLIDE_NV_DISPATCH(hp, (logits_rows_kernel<NV><<<rgrid, 256, 0, s_rows>>>(hp, b, g, pslot, w2, b2, h, live, z,
+                                                                            dense_ok)));
   SLIDE_LAUNCH_CHECK();
 }
 
@@ -390,85 +496,105 @@ void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32
 // slices are added in slice order -- deterministic.  (A dense register-tiled
 // Delta^T W2 over the distinct rows was tried: the Delta scatter and the
 // partial reduction cost more than the L2 re-reads of W2 rows it saves.)
-template <int NV>
-__global__ void __launch_bounds__(256) hidden_grad_kernel(int hp, int b, int slices, const int32_t* __restrict__ offs,
-                                                          const int32_t* __restrict__ prow,
-                                                          const float* __restrict__ delta,
-                                                          const float* __restrict__ w2,
-                                                          const float* __restrict__ h, float* __restrict__ part,
-                                                          float* __restrict__ dh, int32_t* __restrict__ done,
-                                                          int32_t* __restrict__ work_reset) {
-  __shared__ float red[8][NV * 128];
-  __shared__ int s_last;
-  // the W2 Adam's row counter: its previous use is over, its next comes after
-  if (work_reset && blockIdx.x == 0 && threadIdx.x == 0) *work_reset = 0;
-  const int i = blockIdx.x / slices, sl = blockIdx.x - i * slices;
+struct HiddenGradArgs {
+  int hp, b, slices;
+  const int32_t *offs, *prow;
+  const float *delta, *w2, *h;
+  const int32_t* live;
+  float *part, *dh;
+  int32_t *done, *work_reset;
+};
+
+// the sample's slice [beg, e) of pairs: acc[q] = sum_k delta_k W2[row_k, col[q]]
+template <int NG>
+__device__ __forceinline__ void hidden_grad_acc(const HiddenGradArgs& A, int beg, int e, float* red_w) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int o = offs[i], n = offs[i + 1] - o;
-  const int beg = o + (int)((int64_t)n * sl / slices), e = o + (int)((int64_t)n * (sl + 1) / slices);
-  float4 acc[NV];
+  int col[NG];
 #pragma unroll
-  for (int q = 0; q < NV; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int q = 0; q < NG; ++q) col[q] = __ldg(A.live + 1 + q * 32 + lane);
+  float acc[NG];
+#pragma unroll
+  for (int q = 0; q < NG; ++q) acc[q] = 0.f;
   int k = beg + warp;
-  constexpr int U = 8;  // rows in flight per warp
+  constexpr int U = NG <= 2 ? 8 : 4;  // rows in flight per warp
   for (; k + 8 * (U - 1) < e; k += 8 * U) {
-    float4 r[U][NV];
+    float r[U][NG];
     float d[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      d[u] = delta[k + 8 * u];
-      const float* rp = w2 + (int64_t)prow[k + 8 * u] * hp + lane * 4;
+      d[u] = A.delta[k + 8 * u];
+      const float* rp = A.w2 + (int64_t)A.prow[k + 8 * u] * A.hp;
 #pragma unroll
-      for (int q = 0; q < NV; ++q) r[u][q] = ld4(rp + q * 128);
+      for (int q = 0; q < NG; ++q) r[u][q] = __ldg(rp + col[q]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int q = 0; q < NV; ++q) {
-        acc[q].x = fmaf(d[u], r[u][q].x, acc[q].x);
-        acc[q].y = fmaf(d[u], r[u][q].y, acc[q].y);
-        acc[q].z = fmaf(d[u], r[u][q].z, acc[q].z);
-        acc[q].w = fmaf(d[u], r[u][q].w, acc[q].w);
-      }
+      for (int q = 0; q < NG; ++q) acc[q] = fmaf(d[u], r[u][q], acc[q]);
   }
   for (; k < e; k += 8) {
-    const float d = delta[k];
-    const float* rp = w2 + (int64_t)prow[k] * hp + lane * 4;
+    const float d = A.delta[k];
+    const float* rp = A.w2 + (int64_t)A.prow[k] * A.hp;
 #pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      float4 r = ld4(rp + q * 128);
-      acc[q].x = fmaf(d, r.x, acc[q].x);
-      acc[q].y = fmaf(d, r.y, acc[q].y);
-      acc[q].z = fmaf(d, r.z, acc[q].z);
-      acc[q].w = fmaf(d, r.w, acc[q].w);
-    }
+    for (int q = 0; q < NG; ++q) acc[q] = fmaf(d, __ldg(rp + col[q]), acc[q]);
   }
 #pragma unroll
-  for (int q = 0; q < NV; ++q) *reinterpret_cast<float4*>(&red[warp][q * 128 + lane * 4]) = acc[q];
+  for (int q = 0; q < NG; ++q) red_w[warp * (NG * 32) + q * 32 + lane] = acc[q];
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256) hidden_grad_kernel(HiddenGradArgs A) {
+  constexpr int G = NV * 4;
+  __shared__ float red[8 * G * 32];
+  __shared__ int s_last;
+  const int hp = A.hp, b = A.b, slices = A.slices;
+  // the W2 Adam's row counter: its previous use is over, its next comes after
+  if (A.work_reset && blockIdx.x == 0 && threadIdx.x == 0) *A.work_reset = 0;
+  const int i = blockIdx.x / slices, sl = blockIdx.x - i * slices;
+  const int o = A.offs[i], n = A.offs[i + 1] - o;
+  const int beg = o + (int)((int64_t)n * sl / slices), e = o + (int)((int64_t)n * (sl + 1) / slices);
+  // only the live units' columns of W2 are read (dh is masked by h > 0)
+  const int ng = (__ldg(A.live) + 31) >> 5;
+  const int ngp = ng <= 2 ? (ng < 1 ? 1 : ng) : (NV == 1 || ng <= 4 ? 4 : (NV == 2 || ng > 8 ? G : 8));
+  SLIDE_NG_DISPATCH(NV, ng, hidden_grad_acc, A, beg, e, red);
   __syncthreads();
-  for (int c = threadIdx.x; c < hp; c += 256) {
-    float sum = red[0][c];
+  const int kn = ngp * 32;  // red holds [8][kn]
+  // column k of the compact order is unit live[1 + k]; the units past the
+  // live groups are dead (dh = 0), and so is h on the live groups' tail
+  const float* __restrict__ h = A.h;
+  for (int kk = threadIdx.x; kk < hp; kk += 256) {
+    float sum = 0.f;
+    if (kk < kn) {
+      sum = red[kk];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) sum += red[w][c];
-    const int64_t q = (int64_t)i * hp + c;
-    if (slices == 1) dh[q] = (h == nullptr || h[q] > 0.f) ? sum : 0.f;  // h == null: unmasked partial
-    else part[(int64_t)sl * b * hp + q] = sum;
+      for (int w = 1; w < 8; ++w) sum += red[w * kn + kk];
+    }
+    if (slices == 1) {
+      const int64_t q = (int64_t)i * hp + __ldg(A.live + 1 + kk);
+      A.dh[q] = (h == nullptr || h[q] > 0.f) ? sum : 0.f;  // h == null: unmasked partial
+    } else if (kk < kn) {
+      A.part[(int64_t)sl * b * hp + (int64_t)i * hp + kk] = sum;
+    }
   }
   if (slices == 1) return;
   // the sample's last slice to finish adds the slices in slice order
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(done + i, 1) == slices - 1;
+  if (threadIdx.x == 0) s_last = atomicAdd(A.done + i, 1) == slices - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int c = threadIdx.x; c < hp; c += 256) {
-    const int64_t q = (int64_t)i * hp + c;
-    float sum = __ldcg(part + q);
-    for (int t = 1; t < slices; ++t) sum += __ldcg(part + (int64_t)t * b * hp + q);
-    dh[q] = (h == nullptr || h[q] > 0.f) ? sum : 0.f;
+  for (int kk = threadIdx.x; kk < hp; kk += 256) {
+    float sum = 0.f;
+    if (kk < kn) {
+      const int64_t q = (int64_t)i * hp + kk;
+      sum = __ldcg(A.part + q);
+      for (int t = 1; t < slices; ++t) sum += __ldcg(A.part + (int64_t)t * b * hp + q);
+    }
+    const int64_t q = (int64_t)i * hp + __ldg(A.live + 1 + kk);
+    A.dh[q] = (h == nullptr || h[q] > 0.f) ? sum : 0.f;
   }
-  if (threadIdx.x == 0) done[i] = 0;  // self-resetting
+  if (threadIdx.x == 0) A.done[i] = 0;  // self-resetting
 }
 
 int hidden_grad_slices(int b) { return std::max(1, std::min(8, (int)ceil_div((int64_t)kSms * 4, b))); }
@@ -476,11 +602,12 @@ int hidden_grad_slices(int b) { return std::max(1, std::min(8, (int)ceil_div((in
 size_t hidden_grad_scratch(int b, int hp) { return (size_t)hidden_grad_slices(b) * b * hp; }
 
 void launch_hidden_grad(int hp, int b, const int32_t* offs, const int32_t* prow, const float* delta, const float* w2,
-                        const float* h, float* dh, float* part, int32_t* done, int32_t* work_reset, cudaStream_t s) {
+                        const float* h, const int32_t* live, float* dh, float* part, int32_t* done, int32_t* work_reset,
+                        cudaStream_t s) {
   if (b <= 0) return;
   const int S = hidden_grad_slices(b);
-  SLIDE_NV_DISPATCH(hp, (hidden_grad_kernel<NV><<<b * S, 256, 0, s>>>(hp, b, S, offs, prow, delta, w2, h, part, dh, done,
-                                                                      work_reset)));
+  HiddenGradArgs A{hp, b, S, offs, prow, delta, w2, h, live, part, dh, done, work_reset};
+  SLIDE_NV_DISPATCH(hp, (hidden_grad_kernel<NV><<<b * S, 256, 0, s>>>(A)));
   SLIDE_LAUNCH_CHECK();
 }
 
@@ -562,51 +689,57 @@ __device__ __forceinline__ void adam_coord_hs(bool on, float& w, float& m, float
   w = on ? wn : w;
 }
 
-template <int NV, bool COUNT>
-__global__ void __launch_bounds__(256) adam_rows_kernel(int hp, int b, AdamParams ap,
-                                                        const int32_t* __restrict__ n_uniq,
-                                                        const int32_t* __restrict__ uniq,
-                                                        const int32_t* __restrict__ seg_off,
-                                                        const int32_t* __restrict__ seg_cnt,
-                                                        const int32_t* __restrict__ sorted_pairs,
-                                                        const int32_t* __restrict__ pslot,
-                                                        const float* __restrict__ delta, const float* __restrict__ h,
-                                                        float* __restrict__ w2, float* __restrict__ m2,
-                                                        float* __restrict__ v2, float* __restrict__ b2,
-                                                        float* __restrict__ mb2, float* __restrict__ vb2,
-                                                        int64_t* __restrict__ steps2,
-                                                        unsigned long long* __restrict__ touched,
-                                                        int32_t* __restrict__ work) {
-  // per-warp broadcast of the current chunk's pair scalars:
-  // (h row offset, e1, e2, c1) and sqrt(c2); h itself is read through L1
-  // (64 KB at B = 128: resident; staging it in shared memory cost occupancy)
-  __shared__ float4 pq[8][32];
-  __shared__ float ps2[8][32];
+struct AdamRowsArgs {
+  int hp;
+  AdamParams ap;
+  const int32_t *n_uniq, *uniq, *seg_off, *seg_cnt, *sorted_pairs, *pslot;
+  const float *delta, *h;
+  const int32_t* live;
+  float *w2, *m2, *v2, *b2, *mb2, *vb2;
+  int64_t* steps2;
+  unsigned long long* touched;
+  int32_t* work;
+};
+
+// pairs whose activations are loaded ahead of their updates (8 / NG)
+template <int NG>
+struct AdamPf {
+  static constexpr int value = NG >= 4 ? 2 : 8 / NG;
+};
+
+// The persistent row loop for NG live 32-unit groups (compile-time, so the
+// per-pair body has no group guards and the next kAdamPf pairs' activations
+// are in flight before their updates start).
+template <int NG, bool COUNT>
+__device__ __forceinline__ void adam_rows_loop(const AdamRowsArgs& A, const int (&col)[NG], float4 (*pq)[32],
+                                               int (*poff)[32]) {
+  constexpr int kAdamPf = AdamPf<NG>::value;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nu = *n_uniq;
-  const AdamK ak(ap);
+  const int hp = A.hp;
+  const int nu = *A.n_uniq;
+  const AdamK ak(A.ap);
   // persistent warps take rows from a counter: a CTA's slot is never held
   // by idle warps waiting on one long row
   for (;;) {
     int u = 0;
-    if (lane == 0) u = atomicAdd(work, 1);
+    if (lane == 0) u = atomicAdd(A.work, 1);
     u = __shfl_sync(0xffffffffu, u, 0);
     if (u >= nu) break;
     uint32_t tmask = 0;
-    const int r = uniq[u];
-    const int s0 = seg_off[u], len = seg_cnt[u];
-    float* wr = w2 + (int64_t)r * hp + lane * 4;
-    float* mr = m2 + (int64_t)r * hp + lane * 4;
-    float* vr = v2 + (int64_t)r * hp + lane * 4;
-    float4 w[NV], m[NV], v[NV];
+    const int r = A.uniq[u];
+    const int s0 = A.seg_off[u], len = A.seg_cnt[u];
+    float* wr = A.w2 + (int64_t)r * hp;
+    float* mr = A.m2 + (int64_t)r * hp;
+    float* vr = A.v2 + (int64_t)r * hp;
+    float w[NG], m[NG], v[NG];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      w[q] = ld4_cg(wr + q * 128);
-      m[q] = ld4_cg(mr + q * 128);
-      v[q] = ld4_cg(vr + q * 128);
+    for (int q = 0; q < NG; ++q) {
+      w[q] = wr[col[q]];
+      m[q] = mr[col[q]];
+      v[q] = vr[col[q]];
     }
-    float bb = b2[r], mb = mb2[r], vb = vb2[r];
-    const int64_t st = steps2[r];
+    float bb = A.b2[r], mb = A.mb2[r], vb = A.vb2[r];
+    const int64_t st = A.steps2[r];
     for (int c0 = 0; c0 < len; c0 += 32) {
       // lane j holds the j-th pair of this chunk
       const int j = c0 + lane;
@@ -615,16 +748,18 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(int hp, int b, AdamParam
       float d_l = 0.f;
       float2 bc_l = make_float2(0.f, 1.f);
       if (valid) {
-        const int p = sorted_pairs[s0 + j];
-        slot_l = pslot[p];
-        d_l = delta[p];
-        bc_l = bias_corr(ap, st + j + 1);
+        const int p = A.sorted_pairs[s0 + j];
+        slot_l = A.pslot[p];
+        d_l = A.delta[p];
+        bc_l = bias_corr(A.ap, st + j + 1);
       }
       const float e1_l = ak.omb1 * d_l, e2_l = ak.omb2 * d_l * d_l;
       const float s2_l = sqrt_approx(bc_l.y);
       __syncwarp();
-      pq[wid][lane] = make_float4(__int_as_float(slot_l * hp), e1_l, e2_l, bc_l.x);
-      ps2[wid][lane] = s2_l;
+      // past the chunk's end: a zero gradient from h row 0 leaves the moments
+      // and weights as they are (the update is selected off below)
+      pq[wid][lane] = make_float4(e1_l, e2_l, bc_l.x, s2_l);
+      poff[wid][lane] = valid ? slot_l * hp : -1;
       __syncwarp();
       // Bias (gradient d, always moves): its moments are linear recurrences
       // in the chunk's pairs -> two warp scans; the weight update does not
@@ -651,41 +786,97 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(int hp, int b, AdamParam
         vb = __shfl_sync(0xffffffffu, vj, 31);
       }
       const int nc = min(32, len - c0);
-      for (int q2 = 0; q2 < nc; ++q2) {
-        const float4 P = pq[wid][q2];
-        const float s2 = ps2[wid][q2];
-        const float* hr = h + __float_as_int(P.x) + lane * 4;
+      // kAdamPf pairs at a time: their activations are loaded before the
+      // first of their updates; pairs past the chunk (offset -1) are off
+      const float* hq[NG];
 #pragma unroll
-        for (int q = 0; q < NV; ++q) {
-          const float4 hv = ld4(hr + q * 128);
+      for (int q = 0; q < NG; ++q) hq[q] = A.h + col[q];
+      for (int q0 = 0; q0 < nc; q0 += kAdamPf) {
+        float hv[kAdamPf][NG];
+        bool in[kAdamPf];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const float hc = reinterpret_cast<const float*>(&hv)[c];
-            const bool on = hc > 0.f;
-            adam_coord_hs(on, comp(w[q], c), comp(m[q], c), comp(v[q], c), hc, P.y, P.z, P.w, s2, ak);
-            if (COUNT) tmask |= (on ? 1u : 0u) << (q * 4 + c);
+        for (int t = 0; t < kAdamPf; ++t) {
+          const int off = poff[wid][(q0 + t) & 31];
+          in[t] = q0 + t < nc && off >= 0;
+#pragma unroll
+          for (int q = 0; q < NG; ++q) hv[t][q] = __ldg(hq[q] + (off < 0 ? 0 : off));
+        }
+#pragma unroll
+        for (int t = 0; t < kAdamPf; ++t) {
+          const float4 P = pq[wid][(q0 + t) & 31];
+#pragma unroll
+          for (int q = 0; q < NG; ++q) {
+            const bool on = in[t] && hv[t][q] > 0.f;
+            adam_coord_hs(on, w[q], m[q], v[q], hv[t][q], P.x, P.y, P.z, P.w, ak);
+            if (COUNT) tmask |= (on ? 1u : 0u) << q;
           }
         }
       }
     }
 #pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      st4(wr + q * 128, w[q]);
-      st4(mr + q * 128, m[q]);
-      st4(vr + q * 128, v[q]);
+    for (int q = 0; q < NG; ++q) {
+      wr[col[q]] = w[q];
+      mr[col[q]] = m[q];
+      vr[col[q]] = v[q];
     }
     if (lane == 0) {
-      b2[r] = bb;
-      mb2[r] = mb;
-      vb2[r] = vb;
-      steps2[r] = st + len;
+      A.b2[r] = bb;
+      A.mb2[r] = mb;
+      A.vb2[r] = vb;
+      A.steps2[r] = st + len;
     }
     if (COUNT) {
       int tc = __popc(tmask);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) tc += __shfl_xor_sync(0xffffffffu, tc, o);
-      if (lane == 0) atomicAdd(touched, (unsigned long long)tc);
+      if (lane == 0) atomicAdd(A.touched, (unsigned long long)tc);
     }
+  }
+}
+
+template <int NG, bool COUNT>
+__device__ __forceinline__ void adam_rows_ng(const AdamRowsArgs& A, float4 (*pq)[32], int (*poff)[32]) {
+  int col[NG];
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < NG; ++q) col[q] = __ldg(A.live + 1 + q * 32 + lane);
+  adam_rows_loop<NG, COUNT>(A, col, pq, poff);
+}
+
+// lane l owns unit live[1 + 32 q + l] of live group q: only the groups
+// holding live units are walked (dead units' coordinates never move).  The
+// group count is read on the device (graph replays); one loop body per count.
+template <int NV, bool COUNT>
+__global__ void __launch_bounds__(256, NV == 1 ? 3 : 2) adam_rows_kernel(AdamRowsArgs A) {
+  // per-warp broadcast of the current chunk's pair scalars: (e1, e2, c1,
+  // sqrt(c2)) and the h row offset; h itself is read through L1
+  __shared__ float4 pq[8][32];
+  __shared__ int poff[8][32];
+  const int ng = (__ldg(A.live) + 31) >> 5;
+  if (NV == 1) {
+    switch (ng) {
+      case 0:  // no live unit: group 0's lanes sit on dead units, nothing moves
+      case 1: adam_rows_ng<1, COUNT>(A, pq, poff); break;
+      case 2: adam_rows_ng<2, COUNT>(A, pq, poff); break;
+      case 3: adam_rows_ng<3, COUNT>(A, pq, poff); break;
+      default: adam_rows_ng<4, COUNT>(A, pq, poff); break;
+    }
+  } else if (NV == 2) {
+    switch (ng) {
+      case 0:
+      case 1: adam_rows_ng<1, COUNT>(A, pq, poff); break;
+      case 2: adam_rows_ng<2, COUNT>(A, pq, poff); break;
+      case 3: case 4: adam_rows_ng<4, COUNT>(A, pq, poff); break;
+      default: adam_rows_ng<8, COUNT>(A, pq, poff); break;
+    }
+  } else {
+    // wide hidden layers: the live groups rounded up to a power of two
+    if (ng <= 1) adam_rows_ng<1, COUNT>(A, pq, poff);
+    else if (ng <= 2) adam_rows_ng<2, COUNT>(A, pq, poff);
+    else if (ng <= 4) adam_rows_ng<4, COUNT>(A, pq, poff);
+    else if (ng <= 8) adam_rows_ng<8, COUNT>(A, pq, poff);
+    else if (NV == 4 || ng <= 16) adam_rows_ng<NV * 4 < 16 ? NV * 4 : 16, COUNT>(A, pq, poff);
+    else adam_rows_ng<NV * 4, COUNT>(A, pq, poff);
   }
 }
 
@@ -702,21 +893,19 @@ void launch_accumulate(unsigned long long* dst, const int32_t* src, cudaStream_t
 void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq,
                       const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
                       const int32_t* sorted_pairs, const int32_t* pslot, const float* delta, const float* h,
-                      float* w2, float* m2, float* v2, float* b2, float* mb2, float* vb2, int64_t* steps2,
-                      unsigned long long* touched, int32_t* work, bool work_zeroed, cudaStream_t s) {
+                      const int32_t* live, float* w2, float* m2, float* v2, float* b2, float* mb2, float* vb2,
+                      int64_t* steps2, unsigned long long* touched, int32_t* work, bool work_zeroed, cudaStream_t s) {
   if (max_uniq <= 0) return;
   if (!work_zeroed) SLIDE_CUDA(cudaMemsetAsync(work, 0, 4, s));
   // persistent: as many CTAs as are resident at once
   const int per_sm = hp <= 128 ? 3 : 2;
   const int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * per_sm);
+  AdamRowsArgs A{hp, ap, n_uniq, uniq, seg_off, seg_cnt, sorted_pairs, pslot, delta, h, live,
+                 w2, m2, v2, b2, mb2, vb2, steps2, touched, work};
   if (touched) {
-    SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, true><<<grid, 256, 0, s>>>(hp, b, ap, n_uniq, uniq, seg_off, seg_cnt,
-                                                                          sorted_pairs, pslot, delta, h, w2, m2, v2,
-                                                                          b2, mb2, vb2, steps2, touched, work)));
+    SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, true><<<grid, 256, 0, s>>>(A)));
   } else {
-    SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, false><<<grid, 256, 0, s>>>(hp, b, ap, n_uniq, uniq, seg_off, seg_cnt,
-                                                                           sorted_pairs, pslot, delta, h, w2, m2, v2,
-                                                                           b2, mb2, vb2, steps2, touched, work)));
+    SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, false><<<grid, 256, 0, s>>>(A)));
   }
   SLIDE_LAUNCH_CHECK();
 }
@@ -768,7 +957,8 @@ void launch_hidden_counts(int hp, int b, const AdamParams& ap, const float* h, c
 constexpr int kLongChain = 16;
 constexpr int kColGroup = 8;  // pairs per prefetch group of the column path
 
-// One 32-column group of a long W1 row chain: lane = column c.  Pairs in
+// One 32-unit group of a long W1 row chain: lane = unit c (a live-group unit;
+// the tail lanes land on dead units, h = 0: nothing moves).  Pairs in
 // groups of 8; the next group's h / dh / bias corrections are loaded while
 // this group updates.
 __device__ __forceinline__ void adam_feature_column(int hp, const AdamParams& ap, const AdamK& ak, int f, int s0,
@@ -824,155 +1014,160 @@ __device__ __forceinline__ void adam_feature_column(int hp, const AdamParams& ap
       }
     }
   }
-  if (c < hp) {
-    w1t[ro] = w;
-    m1t[ro] = m;
-    v1t[ro] = v;
-  }
+  w1t[ro] = w;
+  m1t[ro] = m;
+  v1t[ro] = v;
   if (touched) {
     const int tcnt = __popc(__ballot_sync(0xffffffffu, moved != 0));
     if (lane == 0) atomicAdd(touched, (unsigned long long)tcnt);
   }
 }
 
-template <int NV>
-__global__ void __launch_bounds__(256) adam_features_kernel(
-    int hp, AdamParams ap, const int32_t* __restrict__ n_uniq, const int32_t* __restrict__ uniq,
-    const int32_t* __restrict__ seg_off, const int32_t* __restrict__ seg_cnt, const int32_t* __restrict__ sorted_k,
-    const int32_t* __restrict__ x_slot, const float* __restrict__ x_val, int64_t x_base,
-    const float* __restrict__ h, const float* __restrict__ dh, const float2* __restrict__ bc,
-    float* __restrict__ w1t, float* __restrict__ m1t, float* __restrict__ v1t,
-    unsigned long long* __restrict__ touched, int32_t* __restrict__ long_list, int32_t* __restrict__ n_long) {
+struct AdamFeatArgs {
+  int hp;
+  AdamParams ap;
+  const int32_t *n_uniq, *uniq, *seg_off, *seg_cnt, *sorted_k, *x_slot;
+  const float* x_val;
+  int64_t x_base;
+  const float *h, *dh;
+  const float2* bc;
+  const int32_t* live;
+  float *w1t, *m1t, *v1t;
+  unsigned long long* touched;
+  int32_t *long_list, *n_long;
+};
+
+// Short chains (<= kLongChain samples hold the feature), one warp per
+// feature row, lane l on unit live[1 + 32 q + l] of live group q; every
+// pair's (h, dh, bias corrections) loads are issued before its updates.
+template <int NG>
+__device__ __forceinline__ void adam_features_loop(const AdamFeatArgs& A) {
+  constexpr int PF = NG >= 4 ? 2 : 8 / NG;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t nu = *n_uniq;
-  const AdamK ak(ap);
+  const int64_t nu = *A.n_uniq;
+  const int hp = A.hp;
+  const AdamK ak(A.ap);
+  int col[NG];
+#pragma unroll
+  for (int q = 0; q < NG; ++q) col[q] = __ldg(A.live + 1 + q * 32 + lane);
   // a long chain (a hot feature held by many samples) goes to the column
   // kernel: appended to long_list here
   for (int64_t u = gw; u < nu; u += nw) {
-    const int len = seg_cnt[u];
+    const int len = A.seg_cnt[u];
     if (len > kLongChain) {
-      if (lane == 0) long_list[atomicAdd(n_long, 1)] = (int32_t)u;
+      if (lane == 0) A.long_list[atomicAdd(A.n_long, 1)] = (int32_t)u;
       continue;
     }
     uint32_t tmask = 0;
-    const int f = uniq[u];
-    const int s0 = seg_off[u];
-    float* wr = w1t + (int64_t)f * hp + lane * 4;
-    float* mr = m1t + (int64_t)f * hp + lane * 4;
-    float* vr = v1t + (int64_t)f * hp + lane * 4;
-    float4 w[NV], m[NV], v[NV];
-#pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      w[q] = ld4_cg(wr + q * 128);
-      m[q] = ld4_cg(mr + q * 128);
-      v[q] = ld4_cg(vr + q * 128);
+    const int f = A.uniq[u];
+    const int s0 = A.seg_off[u];
+    float* wr = A.w1t + (int64_t)f * hp;
+    float* mr = A.m1t + (int64_t)f * hp;
+    float* vr = A.v1t + (int64_t)f * hp;
+    // lane j < len: pair j's h row offset and input value
+    int off_l = 0;
+    float xv_l = 0.f;
+    if (lane < len) {
+      const int k = A.sorted_k[s0 + lane];
+      off_l = A.x_slot[k] * hp;
+      xv_l = A.x_val[A.x_base + k];
     }
-    for (int c0 = 0; c0 < len; c0 += 32) {
-      const int j = c0 + lane;
-      int slot_l = 0;
-      float xv_l = 0.f;
-      if (j < len) {
-        const int k = sorted_k[s0 + j];
-        slot_l = x_slot[k];
-        xv_l = x_val[x_base + k];
+    float w[NG], m[NG], v[NG];
+#pragma unroll
+    for (int q = 0; q < NG; ++q) {
+      w[q] = wr[col[q]];
+      m[q] = mr[col[q]];
+      v[q] = vr[col[q]];
+    }
+    for (int t0 = 0; t0 < len; t0 += PF) {
+      float hv[PF][NG], gv[PF][NG];
+      float2 bv[PF][NG];
+#pragma unroll
+      for (int t = 0; t < PF; ++t) {
+        const int off = __shfl_sync(0xffffffffu, off_l, (t0 + t) & 31);  // past len: lane's 0 offset, off below
+#pragma unroll
+        for (int q = 0; q < NG; ++q) {
+          hv[t][q] = __ldg(A.h + off + col[q]);
+          gv[t][q] = __ldg(A.dh + off + col[q]);
+          bv[t][q] = __ldg(A.bc + off + col[q]);
+        }
       }
-      const int nc = min(32, len - c0);
-      // the hidden error already carries the h > 0 mask (dh = 0 elsewhere);
-      // h itself decides which coordinates move
-      float4 hn[NV], gn[NV], bn[NV][2];
-      auto fetch = [&](int slot) {
-        const int64_t base = (int64_t)slot * hp + lane * 4;
 #pragma unroll
-        for (int q = 0; q < NV; ++q) {
-          hn[q] = ld4(h + base + q * 128);
-          gn[q] = ld4(dh + base + q * 128);
-          const float4* bp = reinterpret_cast<const float4*>(bc + base + q * 128);
-          bn[q][0] = __ldg(bp);
-          bn[q][1] = __ldg(bp + 1);
-        }
-      };
-      fetch(__shfl_sync(0xffffffffu, slot_l, 0));
-      for (int q2 = 0; q2 < nc; ++q2) {
-        float4 hv[NV], gv[NV], bv[NV][2];
+      for (int t = 0; t < PF; ++t) {
+        const float xv = __shfl_sync(0xffffffffu, xv_l, (t0 + t) & 31);
 #pragma unroll
-        for (int q = 0; q < NV; ++q) {
-          hv[q] = hn[q];
-          gv[q] = gn[q];
-          bv[q][0] = bn[q][0];
-          bv[q][1] = bn[q][1];
-        }
-        const float xv = __shfl_sync(0xffffffffu, xv_l, q2);
-        const int nslot = __shfl_sync(0xffffffffu, slot_l, q2 + 1 < nc ? q2 + 1 : q2);
-        if (q2 + 1 < nc) fetch(nslot);
-#pragma unroll
-        for (int q = 0; q < NV; ++q) {
-          const float* bb = reinterpret_cast<const float*>(&bv[q][0]);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const bool on = comp(hv[q], c) > 0.f;
-            adam_coord_if(on, comp(w[q], c), comp(m[q], c), comp(v[q], c), comp(gv[q], c) * xv, bb[2 * c],
-                          bb[2 * c + 1], ak);
-            tmask |= (on ? 1u : 0u) << (q * 4 + c);
-          }
+        for (int q = 0; q < NG; ++q) {
+          // the hidden error already carries the h > 0 mask; h decides which
+          // coordinates move
+          const bool on = t0 + t < len && hv[t][q] > 0.f;
+          adam_coord_if(on, w[q], m[q], v[q], gv[t][q] * xv, bv[t][q].x, bv[t][q].y, ak);
+          tmask |= (on ? 1u : 0u) << q;
         }
       }
     }
 #pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      st4(wr + q * 128, w[q]);
-      st4(mr + q * 128, m[q]);
-      st4(vr + q * 128, v[q]);
+    for (int q = 0; q < NG; ++q) {
+      wr[col[q]] = w[q];
+      mr[col[q]] = m[q];
+      vr[col[q]] = v[q];
     }
-    if (touched) {
+    if (A.touched) {
       int tc = __popc(tmask);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) tc += __shfl_xor_sync(0xffffffffu, tc, o);
-      if (lane == 0) atomicAdd(touched, (unsigned long long)tc);
+      if (lane == 0) atomicAdd(A.touched, (unsigned long long)tc);
     }
   }
 }
 
-// long chains: work item (list entry, 32-column group)
+template <int NV>
+__global__ void __launch_bounds__(256, NV == 1 ? 3 : 2) adam_features_kernel(AdamFeatArgs A) {
+  const int ng = (__ldg(A.live) + 31) >> 5;
+  SLIDE_NG_DISPATCH(NV, ng, adam_features_loop, A);
+}
+
+// long chains: work item (list entry, live 32-unit group)
 __global__ void __launch_bounds__(256) adam_features_long_kernel(
     int hp, AdamParams ap, const int32_t* __restrict__ long_list, const int32_t* __restrict__ n_long,
     const int32_t* __restrict__ uniq, const int32_t* __restrict__ seg_off, const int32_t* __restrict__ seg_cnt,
     const int32_t* __restrict__ sorted_k, const int32_t* __restrict__ x_slot, const float* __restrict__ x_val,
     int64_t x_base, const float* __restrict__ h, const float* __restrict__ dh, const float2* __restrict__ bc,
-    float* __restrict__ w1t, float* __restrict__ m1t, float* __restrict__ v1t,
+    const int32_t* __restrict__ live, float* __restrict__ w1t, float* __restrict__ m1t, float* __restrict__ v1t,
     unsigned long long* __restrict__ touched) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int G = hp / 32;
+  const int G = (__ldg(live) + 31) >> 5;
   const int64_t items = (int64_t)*n_long * G;
   const AdamK ak(ap);
   for (int64_t item = gw; item < items; item += nw) {
     const int u = long_list[item / G];
     const int grp = (int)(item % G);
-    adam_feature_column(hp, ap, ak, uniq[u], seg_off[u], seg_cnt[u], grp * 32 + lane, sorted_k, x_slot, x_val,
-                        x_base, h, dh, bc, w1t, m1t, v1t, touched);
+    adam_feature_column(hp, ap, ak, uniq[u], seg_off[u], seg_cnt[u], __ldg(live + 1 + grp * 32 + lane), sorted_k,
+                        x_slot, x_val, x_base, h, dh, bc, w1t, m1t, v1t, touched);
   }
 }
 
 void launch_adam_features(int hp, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq,
                           const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
                           const int32_t* sorted_k, const int32_t* x_slot, const float* x_val, int64_t x_base,
-                          const float* h, const float* dh, const float2* bc, float* w1t, float* m1t, float* v1t,
-                          unsigned long long* touched, int32_t* long_list, int32_t* n_long, cudaStream_t s) {
+                          const float* h, const float* dh, const float2* bc, const int32_t* live, float* w1t,
+                          float* m1t, float* v1t, unsigned long long* touched, int32_t* long_list, int32_t* n_long,
+                          cudaStream_t s) {
   if (max_uniq <= 0) return;
   SLIDE_CUDA(cudaMemsetAsync(n_long, 0, 4, s));
   int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * 16);
-  SLIDE_NV_DISPATCH(hp, (adam_features_kernel<NV><<<grid, 256, 0, s>>>(hp, ap, n_uniq, uniq, seg_off, seg_cnt,
-                                                                        sorted_k, x_slot, x_val, x_base, h, dh, bc,
-                                                                        w1t, m1t, v1t, touched, long_list, n_long)));
+  AdamFeatArgs A{hp, ap, n_uniq, uniq, seg_off, seg_cnt, sorted_k, x_slot, x_val, x_base, h, dh, bc, live,
+                 w1t, m1t, v1t, touched, long_list, n_long};
+  SLIDE_NV_DISPATCH(hp, (adam_features_kernel<NV><<<grid, 256, 0, s>>>(A)));
   SLIDE_LAUNCH_CHECK();
   // long chains: at most max_uniq * (1 / (kLongChain + 1)) of them
   const int64_t max_long = std::min<int64_t>(max_uniq, ceil_div(max_uniq, kLongChain)) * (hp / 32);
   const int lgrid = (int)std::min<int64_t>(std::max<int64_t>(ceil_div(max_long, 8), 1), (int64_t)kSms * 8);
   adam_features_long_kernel<<<lgrid, 256, 0, s>>>(hp, ap, long_list, n_long, uniq, seg_off, seg_cnt, sorted_k, x_slot,
-                                                  x_val, x_base, h, dh, bc, w1t, m1t, v1t, touched);
+                                                  x_val, x_base, h, dh, bc, live, w1t, m1t, v1t, touched);
   SLIDE_LAUNCH_CHECK();
 }
 
