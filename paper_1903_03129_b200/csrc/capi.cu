@@ -77,7 +77,7 @@ struct slide_ctx {
   TablesHost tab;
   DBuf sh_packed, sh_packed_t, dw_perms, dw_donors, rowkeys;
   // forward workspace
-  DBuf h, qkeys, order, states, act, cnt, empty, offs, prow, pslot, plab, z, prob, delta, loss, dh;
+  DBuf h, qkeys, order, states, act, cnt, empty, offs, prow, pslot, plab, z, prob, delta, loss, dh, dsort;
   // live hidden units of the last forward (see launch_hidden_forward)
   DBuf hmask, live, live_ticket;
   DBuf fb_ids, fb_scratch, fb_bitmap;
@@ -286,7 +286,7 @@ int slide_destroy(slide_ctx* c) {
     if (!c) return;
     cudaStreamSynchronize(c->s);
     c->tab.release();
-    for (DBuf* b : {&c->sh_packed, &c->sh_packed_t, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->hmask, &c->live, &c->live_ticket, &c->qkeys, &c->order,
+    for (DBuf* b : {&c->sh_packed, &c->sh_packed_t, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->dsort, &c->hmask, &c->live, &c->live_ticket, &c->qkeys, &c->order,
                     &c->states, &c->act, &c->cnt, &c->empty, &c->offs, &c->prow, &c->pslot, &c->plab, &c->z,
                     &c->prob, &c->delta, &c->loss, &c->dh, &c->fb_ids, &c->fb_scratch, &c->fb_bitmap, &c->xslot,
                     &c->tc, &c->bc, &c->counters, &c->partial, &c->long_list, &c->n_long, &c->work, &c->topk_out, &c->topk_cnt, &c->tc_scratch, &c->bias_table, &c->cnt_all})
@@ -667,7 +667,9 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   // logits, hidden gradient and W2 Adam all walk this structure
   GroupBy& gr = c->grow;
   if (c->grow_pending) gr.clear(s);
+  gr.want_inv = true;  // the softmax scatters the errors into row-grouped order
   gr.prepare(c->n_local, b, P_max);
+  float* dsort = c->dsort.ensure<float>(P_max);
   gr.run(prow, pslot, offs + b, 0, P_max, s);
   c->grow_pending = true;
   c->timer.mark(s, kStGroupRows);
@@ -689,7 +691,7 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   }
   c->timer.mark(s, kStLogits);
   // sharded: the softmax is completed by the slide_shard_softmax_* stages
-  if (c->G == 1) launch_softmax(b, offs, plab, bt->y_ptr, z, prob, delta, loss, s);
+  if (c->G == 1) launch_softmax(b, offs, plab, bt->y_ptr, z, prob, delta, loss, gr.inv.as<int32_t>(), dsort, s);
   c->timer.mark(s, kStSoftmax);
   c->have_forward = true;
   c->last_b = b;
@@ -794,7 +796,7 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
   // W2: rows in ascending order, each row's samples in slot order
   if (P_max > 0) {
     launch_adam_rows(hp, b, ap, gr.n_uniq.as<int32_t>(), gr.u_max, gr.uniq.as<int32_t>(), gr.seg_off.as<int32_t>(),
-                     gr.seg_cnt.as<int32_t>(), gr.order.as<int32_t>(), c->pslot.as<int32_t>(), c->delta.as<float>(),
+                     gr.seg_cnt.as<int32_t>(), gr.sslot.as<int32_t>(), c->dsort.as<float>(),
                      c->h.as<float>(), c->live.as<int32_t>(), d.w2, d.m2, d.v2, d.b2, d.mb2, d.vb2, d.steps2, ctr,
                      work,
                      /*work_zeroed=*/ext_dh == nullptr, s);
@@ -1136,7 +1138,8 @@ int slide_shard_softmax_finish(slide_ctx* c, const float* gmax, const float* gsu
     SLIDE_CHECK(c->have_forward, kValueError, "no forward");
     const int b = c->last_b;
     launch_softmax_finish(b, c->offs.as<int32_t>(), c->plab.as<uint8_t>(), c->last_yptr, c->z.as<float>(), gmax,
-                          gsum, c->prob.as<float>(), c->delta.as<float>(), loss_out, c->s);
+                          gsum, c->prob.as<float>(), c->delta.as<float>(), loss_out, c->grow.inv.as<int32_t>(),
+                          c->dsort.as<float>(), c->s);
   });
 }
 
@@ -1198,6 +1201,10 @@ int slide_write(slide_ctx* c, int64_t what, const void* src, int64_t bytes) {
     }
     SLIDE_CHECK(bytes == n, kValueError, "size mismatch for stage write");
     if (n) SLIDE_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, c->s));
+    // replayed errors in the W2 Adam's row-grouped order
+    if (what == 6)
+      launch_scatter_sorted(c->offs.as<int32_t>() + c->last_b, c->last_Pmax, c->grow.inv.as<int32_t>(),
+                            c->delta.as<float>(), c->dsort.as<float>(), c->s);
     // a replayed h has its own live units
     if (what == 0)
       launch_live_cols_from_h(c->hp, c->last_b, c->h.as<float>(), c->hmask.as<uint32_t>(), c->live.as<int32_t>(), c->s);

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kGT) g_seg_kernel(const uint32_t* __restrict__
 __global__ void g_place_kernel(const int32_t* __restrict__ keys, const int32_t* __restrict__ slots, const int32_t* n_dev,
                                int64_t n_host, const int32_t* __restrict__ key_rank, int words_per_key,
                                const uint32_t* __restrict__ mask, const int32_t* __restrict__ seg_off,
-                               int32_t* __restrict__ order) {
+                               int32_t* __restrict__ order, int32_t* __restrict__ inv, int32_t* __restrict__ sslot) {
   const int64_t n = dev_count(n_dev, n_host);
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
     const int u = key_rank[keys[q]];
@@ -182,7 +182,12 @@ __global__ void g_place_kernel(const int32_t* __restrict__ keys, const int32_t* 
     int r = 0;
     for (int w = 0; w < (s >> 5); ++w) r += __popc(m[w]);
     r += __popc(m[s >> 5] & ((1u << (s & 31)) - 1u));
-    order[seg_off[u] + r] = (int32_t)q;
+    const int pos = seg_off[u] + r;
+    order[pos] = (int32_t)q;
+    if (inv) {
+      inv[q] = pos;
+      sslot[pos] = s;
+    }
   }
 }
 
@@ -271,7 +276,7 @@ __global__ void __launch_bounds__(kGT) gd_scan_kernel(int64_t K, int wpk, const 
 __global__ void gd_place_kernel(const int32_t* __restrict__ keys, const int32_t* __restrict__ slots, const int32_t* n_dev,
                                 int64_t n_host, const int32_t* __restrict__ key_rank, int wpk,
                                 const uint32_t* __restrict__ mask, const int32_t* __restrict__ seg_off,
-                                int32_t* __restrict__ order) {
+                                int32_t* __restrict__ order, int32_t* __restrict__ inv, int32_t* __restrict__ sslot) {
   const int64_t n = dev_count(n_dev, n_host);
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
     const int key = keys[q];
@@ -280,7 +285,12 @@ __global__ void gd_place_kernel(const int32_t* __restrict__ keys, const int32_t*
     int r = 0;
     for (int w = 0; w < (s >> 5); ++w) r += __popc(m[w]);
     r += __popc(m[s >> 5] & ((1u << (s & 31)) - 1u));
-    order[seg_off[key_rank[key]] + r] = (int32_t)q;
+    const int pos = seg_off[key_rank[key]] + r;
+    order[pos] = (int32_t)q;
+    if (inv) {
+      inv[q] = pos;
+      sslot[pos] = s;
+    }
   }
 }
 
@@ -307,6 +317,10 @@ void GroupBy::prepare(int64_t key_space, int64_t slots, int64_t items_max) {
   seg_off.ensure<int32_t>(u_max);
   n_uniq.ensure<int32_t>(1);
   order.ensure<int32_t>(std::max<int64_t>(items_max, 1));
+  if (want_inv) {
+    inv.ensure<int32_t>(std::max<int64_t>(items_max, 1));
+    sslot.ensure<int32_t>(std::max<int64_t>(items_max, 1));
+  }
   ctrs.ensure<int32_t>(2);
   if (dense) {
     const int64_t need = key_space * wpk;
@@ -346,7 +360,8 @@ void GroupBy::run(const int32_t* keys, const int32_t* slots, const int32_t* n_de
                                                    seg_cnt.as<int32_t>(), n_uniq.as<int32_t>(), t);
     SLIDE_LAUNCH_CHECK();
     gd_place_kernel<<<grid_of(n_max), 256, 0, s>>>(keys, slots, n_dev, n_host, key_rank.as<int32_t>(), wpk,
-                                                   mask.as<uint32_t>(), seg_off.as<int32_t>(), order.as<int32_t>());
+                                                   mask.as<uint32_t>(), seg_off.as<int32_t>(), order.as<int32_t>(),
+                                                   want_inv ? inv.as<int32_t>() : nullptr, sslot.as<int32_t>());
     SLIDE_LAUNCH_CHECK();
     return;
   }
@@ -365,7 +380,8 @@ void GroupBy::run(const int32_t* keys, const int32_t* slots, const int32_t* n_de
                                               seg_cnt.as<int32_t>(), t2);
   SLIDE_LAUNCH_CHECK();
   g_place_kernel<<<grid_of(n_max), 256, 0, s>>>(keys, slots, n_dev, n_host, key_rank.as<int32_t>(), wpk,
-                                                 mask.as<uint32_t>(), seg_off.as<int32_t>(), order.as<int32_t>());
+                                                 mask.as<uint32_t>(), seg_off.as<int32_t>(), order.as<int32_t>(),
+                                                 want_inv ? inv.as<int32_t>() : nullptr, sslot.as<int32_t>());
   SLIDE_LAUNCH_CHECK();
 }
 
@@ -381,7 +397,8 @@ void GroupBy::clear(cudaStream_t s) {
 }
 
 void GroupBy::release() {
-  for (DBuf* b : {&bits, &key_rank, &uniq, &seg_cnt, &seg_off, &n_uniq, &mask, &order, &status, &ctrs}) b->release();
+  for (DBuf* b : {&bits, &key_rank, &uniq, &seg_cnt, &seg_off, &n_uniq, &mask, &order, &inv, &sslot, &status, &ctrs})
+    b->release();
   bits_words = mask_words = 0;
   mask_dense = false;
 }

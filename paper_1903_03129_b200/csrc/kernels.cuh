@@ -59,7 +59,7 @@ void launch_softmax_max(int b, const int32_t* offs, const float* z, float* out, 
 void launch_softmax_sum(int b, const int32_t* offs, const float* z, const float* gmax, float* out, cudaStream_t s);
 void launch_softmax_finish(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
                            const float* gmax, const float* gsum, float* prob, float* delta, double* loss_part,
-                           cudaStream_t s);
+                           const int32_t* inv, float* dsort, cudaStream_t s);
 
 // Stable (key, slot) group-by with device-side sizes (group.cu).
 // the group-by result a kernel walks (device pointers)
@@ -76,6 +76,9 @@ struct GroupView {
 
 struct GroupBy {
   DBuf bits, key_rank, uniq, seg_cnt, seg_off, n_uniq, mask, order, status, ctrs;
+  // want_inv: also inv[q] = sorted position of item q and sslot[pos] = its slot
+  bool want_inv = false;
+  DBuf inv, sslot;
   int64_t K = 0, nwords = 0, u_max = 0, bits_words = 0, mask_words = 0, tiles_bits = 0, tiles_seg = 0;
   int wpk = 1;
   bool dense = false, mask_dense = false;  // dense: one mask per key of the whole key space
@@ -116,7 +119,10 @@ void launch_logits_rows(int hp, int b, const GroupView& g, const int32_t* pslot,
                         const float* h, const int32_t* live, float* z, cudaStream_t s, cudaStream_t s_rows);
 
 void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
-                    float* prob, float* delta, double* loss, cudaStream_t s);
+                    float* prob, float* delta, double* loss, const int32_t* inv, float* dsort, cudaStream_t s);
+// dst[inv[q]] = src[q] for q < *n_dev
+void launch_scatter_sorted(const int32_t* n_dev, int64_t n_max, const int32_t* inv, const float* src, float* dst,
+                           cudaStream_t s);
 // floats of scratch launch_hidden_grad needs
 size_t hidden_grad_scratch(int b, int hp);
 // done: b zero-initialised ints (self-resetting); work_reset (optional): the
@@ -126,9 +132,9 @@ void launch_hidden_grad(int hp, int b, const int32_t* offs, const int32_t* prow,
                         int32_t* work_reset, cudaStream_t s);
 void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq,
                       const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
-                      const int32_t* sorted_pairs, const int32_t* pslot, const float* delta, const float* h,
-                      const int32_t* live, float* w2, float* m2, float* v2, float* b2, float* mb2, float* vb2,
-                      int64_t* steps2, unsigned long long* touched, int32_t* work, bool work_zeroed, cudaStream_t s);
+                      const int32_t* sslot, const float* dsort, const float* h, const int32_t* live, float* w2,
+                      float* m2, float* v2, float* b2, float* mb2, float* vb2, int64_t* steps2,
+                      unsigned long long* touched, int32_t* work, bool work_zeroed, cudaStream_t s);
 void launch_accumulate(unsigned long long* dst, const int32_t* src, cudaStream_t s);
 // per slot: the k best active ids by probability (ties: lower id), -1 padded
 void launch_topk(int b, const int32_t* offs, const int32_t* rows, int shard_count, int shard_rank, const float* prob,

@@ -5,6 +5,7 @@
 #include "internal.cuh"
 #include "kernels.cuh"
 #include <cub/cub.cuh>
+#include <type_traits>
 
 namespace slide {
 
@@ -441,7 +442,8 @@ __global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict
                                                       const uint8_t* __restrict__ plab,
                                                       const int32_t* __restrict__ y_ptr, const float* __restrict__ z,
                                                       float* __restrict__ prob, float* __restrict__ delta,
-                                                      double* __restrict__ loss) {
+                                                      double* __restrict__ loss, const int32_t* __restrict__ inv,
+                                                      float* __restrict__ dsort) {
   using RF = cub::BlockReduce<float, 1024>;
   using RD = cub::BlockReduce<double, 1024>;
   __shared__ union {
@@ -472,7 +474,9 @@ __global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict
     const float p = expf(zz) / se;
     const int lab = plab[o + k];
     prob[o + k] = p;
-    delta[o + k] = lab ? p - inv_ny : p;
+    const float dl = lab ? p - inv_ny : p;
+    delta[o + k] = dl;
+    if (inv) dsort[inv[o + k]] = dl;  // the W2 Adam reads the errors in row-grouped order
     if (lab) {
       double nl = -((double)zz - (double)lse);
       lsum += nl < 690.7755278982137 ? nl : 690.7755278982137;
@@ -482,10 +486,24 @@ __global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict
   if (tid == 0) loss[i] = ny > 0 ? lsum / ny : (double)NAN;
 }
 
+__global__ void scatter_sorted_kernel(const int32_t* __restrict__ n_dev, const int32_t* __restrict__ inv,
+                                      const float* __restrict__ src, float* __restrict__ dst) {
+  const int n = *n_dev;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) dst[inv[q]] = src[q];
+}
+
+void launch_scatter_sorted(const int32_t* n_dev, int64_t n_max, const int32_t* inv, const float* src, float* dst,
+                           cudaStream_t s) {
+  if (n_max <= 0) return;
+  scatter_sorted_kernel<<<(int)std::min<int64_t>(ceil_div(n_max, 256), (int64_t)kSms * 8), 256, 0, s>>>(n_dev, inv, src,
+                                                                                                       dst);
+  SLIDE_LAUNCH_CHECK();
+}
+
 void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
-                    float* prob, float* delta, double* loss, cudaStream_t s) {
+                    float* prob, float* delta, double* loss, const int32_t* inv, float* dsort, cudaStream_t s) {
   if (b <= 0) return;
-  softmax_kernel<<<b, 1024, 0, s>>>(offs, plab, y_ptr, z, prob, delta, loss);
+  softmax_kernel<<<b, 1024, 0, s>>>(offs, plab, y_ptr, z, prob, delta, loss, inv, dsort);
   SLIDE_LAUNCH_CHECK();
 }
 
@@ -692,8 +710,9 @@ __device__ __forceinline__ void adam_coord_hs(bool on, float& w, float& m, float
 struct AdamRowsArgs {
   int hp;
   AdamParams ap;
-  const int32_t *n_uniq, *uniq, *seg_off, *seg_cnt, *sorted_pairs, *pslot;
-  const float *delta, *h;
+  // sslot / dsort: each pair's slot and output error in row-grouped order
+  const int32_t *n_uniq, *uniq, *seg_off, *seg_cnt, *sslot;
+  const float *dsort, *h;
   const int32_t* live;
   float *w2, *m2, *v2, *b2, *mb2, *vb2;
   int64_t* steps2;
@@ -719,12 +738,14 @@ __device__ __forceinline__ void adam_rows_loop(const AdamRowsArgs& A, const int 
   const int nu = *A.n_uniq;
   const AdamK ak(A.ap);
   // persistent warps take rows from a counter: a CTA's slot is never held
-  // by idle warps waiting on one long row
-  for (;;) {
-    int u = 0;
-    if (lane == 0) u = atomicAdd(A.work, 1);
-    u = __shfl_sync(0xffffffffu, u, 0);
-    if (u >= nu) break;
+  // by idle warps waiting on one long row; the next row is claimed while
+  // this one is updated
+  int u = 0;
+  if (lane == 0) u = atomicAdd(A.work, 1);
+  u = __shfl_sync(0xffffffffu, u, 0);
+  while (u < nu) {
+    int u_next = 0;
+    if (lane == 0) u_next = atomicAdd(A.work, 1);
     uint32_t tmask = 0;
     const int r = A.uniq[u];
     const int s0 = A.seg_off[u], len = A.seg_cnt[u];
@@ -748,18 +769,15 @@ __device__ __forceinline__ void adam_rows_loop(const AdamRowsArgs& A, const int 
       float d_l = 0.f;
       float2 bc_l = make_float2(0.f, 1.f);
       if (valid) {
-        const int p = A.sorted_pairs[s0 + j];
-        slot_l = A.pslot[p];
-        d_l = A.delta[p];
+        slot_l = A.sslot[s0 + j];
+        d_l = A.dsort[s0 + j];
         bc_l = bias_corr(A.ap, st + j + 1);
       }
       const float e1_l = ak.omb1 * d_l, e2_l = ak.omb2 * d_l * d_l;
       const float s2_l = sqrt_approx(bc_l.y);
       __syncwarp();
-      // past the chunk's end: a zero gradient from h row 0 leaves the moments
-      // and weights as they are (the update is selected off below)
       pq[wid][lane] = make_float4(e1_l, e2_l, bc_l.x, s2_l);
-      poff[wid][lane] = valid ? slot_l * hp : -1;
+      poff[wid][lane] = slot_l * hp;
       __syncwarp();
       // Bias (gradient d, always moves): its moments are linear recurrences
       // in the chunk's pairs -> two warp scans; the weight update does not
@@ -787,31 +805,31 @@ __device__ __forceinline__ void adam_rows_loop(const AdamRowsArgs& A, const int 
       }
       const int nc = min(32, len - c0);
       // kAdamPf pairs at a time: their activations are loaded before the
-      // first of their updates; pairs past the chunk (offset -1) are off
-      const float* hq[NG];
-#pragma unroll
-      for (int q = 0; q < NG; ++q) hq[q] = A.h + col[q];
-      for (int q0 = 0; q0 < nc; q0 += kAdamPf) {
+      // first of their updates; in the chunk's tail batch the pairs past nc
+      // are off
+      auto batch = [&](int q0, auto tail) {
         float hv[kAdamPf][NG];
-        bool in[kAdamPf];
 #pragma unroll
         for (int t = 0; t < kAdamPf; ++t) {
-          const int off = poff[wid][(q0 + t) & 31];
-          in[t] = q0 + t < nc && off >= 0;
+          const unsigned off = (unsigned)poff[wid][(q0 + t) & 31];
 #pragma unroll
-          for (int q = 0; q < NG; ++q) hv[t][q] = __ldg(hq[q] + (off < 0 ? 0 : off));
+          for (int q = 0; q < NG; ++q) hv[t][q] = __ldg(A.h + (off + (unsigned)col[q]));
         }
 #pragma unroll
         for (int t = 0; t < kAdamPf; ++t) {
           const float4 P = pq[wid][(q0 + t) & 31];
+          const bool in = !decltype(tail)::value || q0 + t < nc;
 #pragma unroll
           for (int q = 0; q < NG; ++q) {
-            const bool on = in[t] && hv[t][q] > 0.f;
+            const bool on = in && hv[t][q] > 0.f;
             adam_coord_hs(on, w[q], m[q], v[q], hv[t][q], P.x, P.y, P.z, P.w, ak);
             if (COUNT) tmask |= (on ? 1u : 0u) << q;
           }
         }
-      }
+      };
+      int q0 = 0;
+      for (; q0 + kAdamPf <= nc; q0 += kAdamPf) batch(q0, std::false_type{});
+      if (q0 < nc) batch(q0, std::true_type{});
     }
 #pragma unroll
     for (int q = 0; q < NG; ++q) {
@@ -831,6 +849,7 @@ __device__ __forceinline__ void adam_rows_loop(const AdamRowsArgs& A, const int 
       for (int o = 16; o > 0; o >>= 1) tc += __shfl_xor_sync(0xffffffffu, tc, o);
       if (lane == 0) atomicAdd(A.touched, (unsigned long long)tc);
     }
+    u = __shfl_sync(0xffffffffu, u_next, 0);
   }
 }
 
@@ -892,15 +911,15 @@ void launch_accumulate(unsigned long long* dst, const int32_t* src, cudaStream_t
 
 void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq,
                       const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
-                      const int32_t* sorted_pairs, const int32_t* pslot, const float* delta, const float* h,
-                      const int32_t* live, float* w2, float* m2, float* v2, float* b2, float* mb2, float* vb2,
-                      int64_t* steps2, unsigned long long* touched, int32_t* work, bool work_zeroed, cudaStream_t s) {
+                      const int32_t* sslot, const float* dsort, const float* h, const int32_t* live, float* w2,
+                      float* m2, float* v2, float* b2, float* mb2, float* vb2, int64_t* steps2,
+                      unsigned long long* touched, int32_t* work, bool work_zeroed, cudaStream_t s) {
   if (max_uniq <= 0) return;
   if (!work_zeroed) SLIDE_CUDA(cudaMemsetAsync(work, 0, 4, s));
   // persistent: as many CTAs as are resident at once
   const int per_sm = hp <= 128 ? 3 : 2;
   const int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * per_sm);
-  AdamRowsArgs A{hp, ap, n_uniq, uniq, seg_off, seg_cnt, sorted_pairs, pslot, delta, h, live,
+  AdamRowsArgs A{hp, ap, n_uniq, uniq, seg_off, seg_cnt, sslot, dsort, h, live,
                  w2, m2, v2, b2, mb2, vb2, steps2, touched, work};
   if (touched) {
     SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, true><<<grid, 256, 0, s>>>(A)));
@@ -1311,7 +1330,9 @@ __global__ void __launch_bounds__(1024) softmax_finish_kernel(const int32_t* __r
                                                              const float* __restrict__ z,
                                                              const float* __restrict__ gmax,
                                                              const float* __restrict__ gsum, float* __restrict__ prob,
-                                                             float* __restrict__ delta, double* __restrict__ loss) {
+                                                             float* __restrict__ delta, double* __restrict__ loss,
+                                                             const int32_t* __restrict__ inv,
+                                                             float* __restrict__ dsort) {
   using RD = cub::BlockReduce<double, 1024>;
   __shared__ typename RD::TempStorage tmp;
   const int i = blockIdx.x;
@@ -1325,7 +1346,9 @@ __global__ void __launch_bounds__(1024) softmax_finish_kernel(const int32_t* __r
     const float p = expf(zz) / se;
     const int lab = plab[o + k];
     prob[o + k] = p;
-    delta[o + k] = lab ? p - inv_ny : p;
+    const float dl = lab ? p - inv_ny : p;
+    delta[o + k] = dl;
+    if (inv) dsort[inv[o + k]] = dl;
     if (lab) {
       const double nl = -((double)zz - (double)lse);
       lsum += nl < 690.7755278982137 ? nl : 690.7755278982137;
@@ -1347,8 +1370,8 @@ void launch_softmax_sum(int b, const int32_t* offs, const float* z, const float*
 
 void launch_softmax_finish(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
                            const float* gmax, const float* gsum, float* prob, float* delta, double* loss_part,
-                           cudaStream_t s) {
-  softmax_finish_kernel<<<b, 1024, 0, s>>>(offs, plab, y_ptr, z, gmax, gsum, prob, delta, loss_part);
+                           const int32_t* inv, float* dsort, cudaStream_t s) {
+  softmax_finish_kernel<<<b, 1024, 0, s>>>(offs, plab, y_ptr, z, gmax, gsum, prob, delta, loss_part, inv, dsort);
   SLIDE_LAUNCH_CHECK();
 }
 
