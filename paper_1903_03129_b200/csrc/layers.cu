@@ -976,72 +976,6 @@ void launch_hidden_counts(int hp, int b, const AdamParams& ap, const float* h, c
 constexpr int kLongChain = 16;
 constexpr int kColGroup = 8;  // pairs per prefetch group of the column path
 
-// One 32-unit group of a long W1 row chain: lane = unit c (a live-group unit;
-// the tail lanes land on dead units, h = 0: nothing moves).  Pairs in
-// groups of 8; the next group's h / dh / bias corrections are loaded while
-// this group updates.
-__device__ __forceinline__ void adam_feature_column(int hp, const AdamParams& ap, const AdamK& ak, int f, int s0,
-                                                    int len, int c, const int32_t* __restrict__ sorted_k,
-                                                    const int32_t* __restrict__ x_slot,
-                                                    const float* __restrict__ x_val, int64_t x_base,
-                                                    const float* __restrict__ h, const float* __restrict__ dh,
-                                                    const float2* __restrict__ bc, float* __restrict__ w1t,
-                                                    float* __restrict__ m1t, float* __restrict__ v1t,
-                                                    unsigned long long* __restrict__ touched) {
-  const int lane = threadIdx.x & 31;
-  const int64_t ro = (int64_t)f * hp + c;
-  float w = __ldcg(w1t + ro), m = __ldcg(m1t + ro), v = __ldcg(v1t + ro);
-  int moved = 0;
-  for (int c0 = 0; c0 < len; c0 += 32) {
-    const int j = c0 + lane;
-    int slot_l = 0;
-    float xv_l = 0.f;
-    if (j < len) {
-      const int k = sorted_k[s0 + j];
-      slot_l = x_slot[k];
-      xv_l = x_val[x_base + k];
-    }
-    const int nc = min(32, len - c0);
-    float hc[kColGroup], gc[kColGroup], hn[kColGroup], gn[kColGroup];
-    float2 bcc[kColGroup], bn[kColGroup];
-    auto fetch = [&](int g0, float (&hh)[kColGroup], float (&gg)[kColGroup], float2 (&bb)[kColGroup]) {
-#pragma unroll
-      for (int t = 0; t < kColGroup; ++t) {
-        const int slot = __shfl_sync(0xffffffffu, slot_l, (g0 + t) & 31);
-        const int64_t q = (int64_t)slot * hp + c;
-        const bool ok = g0 + t < nc;
-        hh[t] = ok ? __ldg(h + q) : 0.f;
-        gg[t] = ok ? __ldg(dh + q) : 0.f;
-        bb[t] = ok ? __ldg(bc + q) : make_float2(0.f, 1.f);
-      }
-    };
-    fetch(0, hc, gc, bcc);
-    for (int g0 = 0; g0 < nc; g0 += kColGroup) {
-      if (g0 + kColGroup < nc) fetch(g0 + kColGroup, hn, gn, bn);
-#pragma unroll
-      for (int t = 0; t < kColGroup; ++t) {  // predicated, no branch: the 8 updates interleave
-        const float xv = __shfl_sync(0xffffffffu, xv_l, (g0 + t) & 31);
-        const bool on = hc[t] > 0.f;  // padding pairs carry h = 0
-        adam_coord_if(on, w, m, v, gc[t] * xv, bcc[t].x, bcc[t].y, ak);
-        moved |= on;
-      }
-#pragma unroll
-      for (int t = 0; t < kColGroup; ++t) {
-        hc[t] = hn[t];
-        gc[t] = gn[t];
-        bcc[t] = bn[t];
-      }
-    }
-  }
-  w1t[ro] = w;
-  m1t[ro] = m;
-  v1t[ro] = v;
-  if (touched) {
-    const int tcnt = __popc(__ballot_sync(0xffffffffu, moved != 0));
-    if (lane == 0) atomicAdd(touched, (unsigned long long)tcnt);
-  }
-}
-
 struct AdamFeatArgs {
   int hp;
   AdamParams ap;
@@ -1147,25 +1081,113 @@ __global__ void __launch_bounds__(256, NV == 1 ? 3 : 2) adam_features_kernel(Ada
   SLIDE_NG_DISPATCH(NV, ng, adam_features_loop, A);
 }
 
-// long chains: work item (list entry, live 32-unit group)
-__global__ void __launch_bounds__(256) adam_features_long_kernel(
-    int hp, AdamParams ap, const int32_t* __restrict__ long_list, const int32_t* __restrict__ n_long,
-    const int32_t* __restrict__ uniq, const int32_t* __restrict__ seg_off, const int32_t* __restrict__ seg_cnt,
-    const int32_t* __restrict__ sorted_k, const int32_t* __restrict__ x_slot, const float* __restrict__ x_val,
-    int64_t x_base, const float* __restrict__ h, const float* __restrict__ dh, const float2* __restrict__ bc,
-    const int32_t* __restrict__ live, float* __restrict__ w1t, float* __restrict__ m1t, float* __restrict__ v1t,
-    unsigned long long* __restrict__ touched) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int G = (__ldg(live) + 31) >> 5;
-  const int64_t items = (int64_t)*n_long * G;
-  const AdamK ak(ap);
-  for (int64_t item = gw; item < items; item += nw) {
-    const int u = long_list[item / G];
+// Long chains (a hot feature held by > kLongChain samples): work item =
+// (feature, live 32-unit group), one CTA of kLongWarps warps, lane = unit.
+// The feature's pairs are cut into kLongWarps consecutive segments.  The
+// moments are linear recurrences, so each warp first folds its segment into
+// (A1, X1, A2, X2) with m_end = A1 m_start + X1 (v alike); the segments'
+// start moments follow from the earlier segments' coefficients, every warp
+// then replays its segment with the real bias corrections and sums its
+// weight steps, and the steps are subtracted in segment order.  The
+// sequential chain of the reference (network.py:428-451, one Adam step per
+// sample in slot order) becomes kLongWarps chains a quarter as long.
+constexpr int kLongWarps = 4;
+
+__global__ void __launch_bounds__(kLongWarps * 32) adam_features_long_kernel(AdamFeatArgs A) {
+  __shared__ float4 coef[kLongWarps][32];
+  __shared__ float part[kLongWarps][32];
+  __shared__ uint32_t movedw[kLongWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int hp = A.hp;
+  const int G = (__ldg(A.live) + 31) >> 5;
+  const int64_t items = (int64_t)*A.n_long * G;
+  const AdamK ak(A.ap);
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int u = A.long_list[item / G];
     const int grp = (int)(item % G);
-    adam_feature_column(hp, ap, ak, uniq[u], seg_off[u], seg_cnt[u], __ldg(live + 1 + grp * 32 + lane), sorted_k,
-                        x_slot, x_val, x_base, h, dh, bc, w1t, m1t, v1t, touched);
+    const int c = __ldg(A.live + 1 + grp * 32 + lane);
+    const int f = A.uniq[u], s0 = A.seg_off[u], len = A.seg_cnt[u];
+    const int j0 = len * warp / kLongWarps, j1 = len * (warp + 1) / kLongWarps;
+    const int64_t ro = (int64_t)f * hp + c;
+    float m = __ldcg(A.m1t + ro), v = __ldcg(A.v1t + ro);  // read before the last warp writes them back
+    // walk this warp's segment: fn(j, on, gd, bias corrections)
+    auto walk = [&](auto fn, auto with_bc) {
+      for (int jb = j0; jb < j1; jb += 32) {
+        int off_l = 0;
+        float xv_l = 0.f;
+        if (jb + lane < j1) {
+          const int k = A.sorted_k[s0 + jb + lane];
+          off_l = A.x_slot[k] * hp;
+          xv_l = A.x_val[A.x_base + k];
+        }
+        const int nc = min(32, j1 - jb);
+        for (int t0 = 0; t0 < nc; t0 += kColGroup) {
+          float hv[kColGroup], gv[kColGroup];
+          float2 bv[kColGroup];
+#pragma unroll
+          for (int t = 0; t < kColGroup; ++t) {
+            const unsigned off = (unsigned)__shfl_sync(0xffffffffu, off_l, (t0 + t) & 31) + (unsigned)c;
+            hv[t] = __ldg(A.h + off);
+            gv[t] = __ldg(A.dh + off);
+            if (decltype(with_bc)::value) bv[t] = __ldg(A.bc + off);
+          }
+#pragma unroll
+          for (int t = 0; t < kColGroup; ++t) {
+            const float xv = __shfl_sync(0xffffffffu, xv_l, (t0 + t) & 31);
+            const bool on = t0 + t < nc && hv[t] > 0.f;
+            fn(on, gv[t] * xv, bv[t]);
+          }
+        }
+      }
+    };
+    // phase 1: the segment's moment recurrences as (A1, X1, A2, X2)
+    float a1 = 1.f, x1 = 0.f, a2 = 1.f, x2 = 0.f;
+    walk([&](bool on, float g, float2) {
+      const float nx1 = fmaf(ak.b1, x1, ak.omb1 * g), nx2 = fmaf(ak.b2, x2, ak.omb2 * (g * g));
+      x1 = on ? nx1 : x1;
+      x2 = on ? nx2 : x2;
+      a1 = on ? a1 * ak.b1 : a1;
+      a2 = on ? a2 * ak.b2 : a2;
+    }, std::false_type{});
+    coef[warp][lane] = make_float4(a1, x1, a2, x2);
+    __syncthreads();
+    for (int k = 0; k < warp; ++k) {
+      const float4 cf = coef[k][lane];
+      m = fmaf(cf.x, m, cf.y);
+      v = fmaf(cf.z, v, cf.w);
+    }
+    // phase 2: replay with the bias corrections, sum the weight steps
+    float psum = 0.f;
+    bool moved = false;
+    walk([&](bool on, float g, float2 cc) {
+      const float mn = fmaf(ak.b1, m, ak.omb1 * g), vn = fmaf(ak.b2, v, ak.omb2 * (g * g));
+      const float st = (cc.x * mn) * rcp_approx(sqrt_approx(vn * cc.y) + ak.eps);
+      m = on ? mn : m;
+      v = on ? vn : v;
+      psum += on ? st : 0.f;
+      moved |= on;
+    }, std::true_type{});
+    part[warp][lane] = psum;
+    const uint32_t mv = __ballot_sync(0xffffffffu, moved);
+    if (lane == 0) movedw[warp] = mv;
+    if (warp == kLongWarps - 1) {  // the chain's end state
+      A.m1t[ro] = m;
+      A.v1t[ro] = v;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      float w = __ldcg(A.w1t + ro);
+#pragma unroll
+      for (int k = 0; k < kLongWarps; ++k) w -= part[k][lane];
+      A.w1t[ro] = w;
+      if (A.touched && lane == 0) {
+        uint32_t any = 0;
+#pragma unroll
+        for (int k = 0; k < kLongWarps; ++k) any |= movedw[k];
+        atomicAdd(A.touched, (unsigned long long)__popc(any));
+      }
+    }
+    __syncthreads();  // coef / part / movedw reuse
   }
 }
 
@@ -1184,9 +1206,8 @@ void launch_adam_features(int hp, const AdamParams& ap, const int32_t* n_uniq, i
   SLIDE_LAUNCH_CHECK();
   // long chains: at most max_uniq * (1 / (kLongChain + 1)) of them
   const int64_t max_long = std::min<int64_t>(max_uniq, ceil_div(max_uniq, kLongChain)) * (hp / 32);
-  const int lgrid = (int)std::min<int64_t>(std::max<int64_t>(ceil_div(max_long, 8), 1), (int64_t)kSms * 8);
-  adam_features_long_kernel<<<lgrid, 256, 0, s>>>(hp, ap, long_list, n_long, uniq, seg_off, seg_cnt, sorted_k, x_slot,
-                                                  x_val, x_base, h, dh, bc, live, w1t, m1t, v1t, touched);
+  const int lgrid = (int)std::min<int64_t>(std::max<int64_t>(max_long, 1), (int64_t)kSms * 16);
+  adam_features_long_kernel<<<lgrid, kLongWarps * 32, 0, s>>>(A);
   SLIDE_LAUNCH_CHECK();
 }
 
@@ -1267,12 +1288,30 @@ __global__ void hidden_prep_bias_kernel(int hp, int b, AdamParams ap, const floa
         g = dh[q];
       }
     }
-    unsigned todo = mask;
-    while (todo) {
-      const int src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      adam_coord(bb, mb, vb, __shfl_sync(0xffffffffu, g, src), __shfl_sync(0xffffffffu, cc.x, src),
-                 __shfl_sync(0xffffffffu, cc.y, src), ak);
+    if (mask) {
+      // the bias moments are linear recurrences over this chunk's active
+      // samples (slot order): two warp scans; the weight steps do not feed
+      // back, so they are summed
+      float a1 = act ? ak.b1 : 1.f, x1 = act ? ak.omb1 * g : 0.f;
+      float a2 = act ? ak.b2 : 1.f, x2 = act ? ak.omb2 * (g * g) : 0.f;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const float pa1 = __shfl_up_sync(0xffffffffu, a1, o), px1 = __shfl_up_sync(0xffffffffu, x1, o);
+        const float pa2 = __shfl_up_sync(0xffffffffu, a2, o), px2 = __shfl_up_sync(0xffffffffu, x2, o);
+        if (lane >= o) {
+          x1 = fmaf(a1, px1, x1);
+          a1 *= pa1;
+          x2 = fmaf(a2, px2, x2);
+          a2 *= pa2;
+        }
+      }
+      const float mj = fmaf(a1, mb, x1), vj = fmaf(a2, vb, x2);
+      float upd = act ? (cc.x * mj) * rcp_approx(sqrt_approx(vj * cc.y) + ak.eps) : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) upd += __shfl_xor_sync(0xffffffffu, upd, o);
+      bb -= upd;
+      mb = __shfl_sync(0xffffffffu, mj, 31);
+      vb = __shfl_sync(0xffffffffu, vj, 31);
     }
     run += __popc(mask);
   }

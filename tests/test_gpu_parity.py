@@ -554,33 +554,32 @@ def test_pipelined_batches_equal_per_call_steps():
 def test_live_unit_permutation_tracks_the_batch():
     """The hidden forward's live-unit list (the units nonzero in some sample,
     ascending, then the dead ones) equals h's nonzero columns after every
-    step, including steps where most units die; the row kernels walk only
-    its live groups, so the trained state still matches the oracle."""
+    step; with half the hidden units dead (bias -5) the row kernels walk only
+    the live groups and the trained state still matches the oracle."""
     from paper_1903_03129_b200.configs import TINY as w
     from paper_1903_03129_b200.data import synthetic_corpus
 
-    corpus = synthetic_corpus(w.corpus, 4 * 64, seed=12)
-    cfg = TrainConfig(batch_size=64, seed=0, learning_rate=3e-2, n0=50)
+    corpus = synthetic_corpus(w.corpus, 3 * 64, seed=12)
+    cfg = TrainConfig(batch_size=64, seed=0, learning_rate=w.lr, n0=50)
     spec = LshLayerConfig("simhash", k=w.k, l=w.l, capacity=w.cap, sampler=SamplerConfig("vanilla", beta=w.beta))
     net = SlideNetwork(w.input_dim, [w.hidden, w.n_out], cfg, lsh_layers={1: spec})
+    b = np.array(net.layers[0].b)
+    b[::2] = -5.0  # even units dead for every input
+    net.layers[0].b[:] = b
     hp = net.hidden_pad
-    seen = []
-    for it in range(1, 5):
+    lsh = oracle_lsh_from_net(net, spec)  # the tables as built at construction (no rebuild in these steps)
+    for it in range(1, 4):
         sub = corpus.subset(np.arange((it - 1) * 64, it * 64))
         csr = HostCsr(sub.x_ptr.astype(np.int32), sub.x_idx, sub.x_val, sub.y_ptr.astype(np.int32), sub.y_idx)
-        if it == 4:  # last step against the oracle from the device's own state
-            st = oracle_state_from_net(net)
-            lsh = oracle_lsh_from_net(net, spec, st)
-            O.train_step(st, lsh, sub.triples(), it, 0, w.n_out, O.AdamCfg(lr=3e-2), mode="snapshot")
+        st = oracle_state_from_net(net)  # teacher forcing: each step from the device's own state
+        O.train_step(st, lsh, sub.triples(), it, 0, w.n_out, O.AdamCfg(lr=w.lr), mode="snapshot")
         net.train_batch_csr(csr, it, schedule="snapshot")
         h = net._read(0, 64 * hp, np.float32).reshape(64, hp)
         live = net._read(13, 1 + hp, np.int32)
         on = np.flatnonzero((h > 0).any(0))
         n = int(live[0])
-        assert n == on.size
+        assert 0 < n <= hp // 2 and n == on.size
         np.testing.assert_array_equal(live[1:1 + n], on)
         np.testing.assert_array_equal(np.sort(live[1:]), np.arange(hp))
         assert np.all(np.diff(live[1 + n:]) > 0)
-        seen.append(n)
-    assert min(seen) < hp  # some units died (the compact path ran)
-    assert_state_close(net, st, what="live-unit step")
+        assert_state_close(net, st, what=f"live-unit step {it}")
