@@ -69,6 +69,7 @@ struct GroupView {
   int wpk;
   int64_t u_max;
   int mask_by_key;
+  const int32_t* sslot;  // slot of each sorted position (want_inv groupings), else null
   __device__ __forceinline__ const uint32_t* mask_of(int64_t u) const {
     return mask + (mask_by_key ? (int64_t)uniq[u] : u) * wpk;
   }
@@ -90,7 +91,8 @@ struct GroupBy {
   void release();
   GroupView view() {
     return GroupView{n_uniq.as<int32_t>(), uniq.as<int32_t>(), seg_off.as<int32_t>(), seg_cnt.as<int32_t>(),
-                     order.as<int32_t>(), mask.as<uint32_t>(), wpk, u_max, dense ? 1 : 0};
+                     order.as<int32_t>(), mask.as<uint32_t>(), wpk, u_max, dense ? 1 : 0,
+                     want_inv ? sslot.as<int32_t>() : nullptr};
   }
 };
 

@@ -271,7 +271,9 @@ constexpr int kTN = 64;         // samples per tile
 constexpr int kKC = 32;         // k (live units) per shared-memory stage
 constexpr int kLd = kKC + 4;    // padded row stride (conflict-free float4 reads)
 constexpr int kMaskWords = 32;  // B <= 1024
-constexpr int kTileSmem = (2 * kTM * kLd) * 4 + kTM * kMaskWords * 4 + kTM * 8 + kTM * 4;
+constexpr int kZLd = kTN + 1;  // the 64 x 64 logit tile in shared memory (reuses the staging area)
+static_assert(kTM * kZLd <= 2 * kTM * kLd, "logit tile must fit the staging area");
+constexpr int kTileSmem = (2 * kTM * kLd) * 4 + kTM * 16;
 
 // dense work item = (64-row tile, 64-sample block).  A row tile goes dense
 // unless its pairs cover < 1/64 of its rows x B cells (then the per-row
@@ -283,7 +285,7 @@ __device__ __forceinline__ bool tile_is_dense(const GroupView& g, int64_t u0, in
 }
 
 template <int NV>
-__global__ void __launch_bounds__(256, 2) logits_tiles_kernel(int hp, int b, GroupView g,
+__global__ void __launch_bounds__(256, 3) logits_tiles_kernel(int hp, int b, GroupView g,
                                                               const int32_t* __restrict__ pslot,
                                                               const float* __restrict__ w2,
                                                               const float* __restrict__ b2,
@@ -293,11 +295,12 @@ __global__ void __launch_bounds__(256, 2) logits_tiles_kernel(int hp, int b, Gro
   extern __shared__ __align__(16) float tsm[];
   float* ws = tsm;                                   // [kTM][kLd]
   float* hs = ws + kTM * kLd;                        // [kTN][kLd]
-  int* cum = reinterpret_cast<int*>(hs + kTN * kLd);  // [kTM][kMaskWords] mask popc prefix per row
-  int* base_s = cum + kTM * kMaskWords;              // [kTM]
-  float* bias_s = reinterpret_cast<float*>(base_s + kTM);
+  float* zt = tsm;                                   // [kTM][kZLd] after the product
+  int* base_s = reinterpret_cast<int*>(hs + kTN * kLd);  // [kTM] first sorted position of each row
+  int* len_s = base_s + kTM;                         // [kTM] its pair count
+  float* bias_s = reinterpret_cast<float*>(len_s + kTM);
   int* wrow_s = reinterpret_cast<int*>(bias_s + kTM);  // [kTM] W2 row of each tile row
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tx = tid & 15, ty = tid >> 4;
   const int64_t nu = *g.n_uniq;
   const int64_t tiles = (nu + kTM - 1) / kTM;
@@ -305,7 +308,6 @@ __global__ void __launch_bounds__(256, 2) logits_tiles_kernel(int hp, int b, Gro
   // k runs over the live units only (32 per stage, the last stage's tail on
   // dead units, whose h is 0): the lane's unit of every stage
   const int kn = ((__ldg(live) + 31) >> 5) * 32;
-  const int my_c = tid & 31;
   for (int64_t item = blockIdx.x; item < tiles * nsb; item += gridDim.x) {
     const int64_t tile = item / nsb;
     const int s0 = (int)(item - tile * nsb) * kTN;
@@ -314,13 +316,8 @@ __global__ void __launch_bounds__(256, 2) logits_tiles_kernel(int hp, int b, Gro
     if (!tile_is_dense(g, u0, nrow, b)) continue;  // sparse tile: logits_rows_kernel
     if (tid < nrow) {
       const int64_t u = u0 + tid;
-      const uint32_t* mrow = g.mask_of(u);
-      int run = 0;
-      for (int w = 0; w < g.wpk; ++w) {
-        cum[tid * kMaskWords + w] = run;
-        run += __popc(mrow[w]);
-      }
       base_s[tid] = g.seg_off[u];
+      len_s[tid] = g.seg_cnt[u];
       const int r = g.uniq[u];
       bias_s[tid] = b2[r];
       wrow_s[tid] = r;
@@ -333,20 +330,20 @@ __global__ void __launch_bounds__(256, 2) logits_tiles_kernel(int hp, int b, Gro
       for (int jj = 0; jj < 4; ++jj) acc[j][jj] = 0.f;
     for (int k0 = 0; k0 < kn; k0 += kKC) {
       // stage 64 W rows and 64 h rows of these 32 units: 16 loads in flight
-      const int c = __ldg(live + 1 + k0 + my_c);
+      const int c = __ldg(live + 1 + k0 + lane);
       float lw[8], lh[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const int row = (tid >> 5) + q * 8;
+        const int row = warp + q * 8;
         lw[q] = row < nrow ? __ldg(w2 + (int64_t)wrow_s[row] * hp + c) : 0.f;
         lh[q] = s0 + row < b ? __ldg(h + (int64_t)(s0 + row) * hp + c) : 0.f;
       }
       __syncthreads();  // previous readers of ws / hs are done
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const int row = (tid >> 5) + q * 8;
-        ws[row * kLd + my_c] = lw[q];
-        hs[row * kLd + my_c] = lh[q];
+        const int row = warp + q * 8;
+        ws[row * kLd + lane] = lw[q];
+        hs[row * kLd + lane] = lh[q];
       }
       __syncthreads();
 #pragma unroll
@@ -374,24 +371,40 @@ __global__ void __launch_bounds__(256, 2) logits_tiles_kernel(int hp, int b, Gro
           for (int jj = 0; jj < 4; ++jj) acc[j][jj] = fmaf(wv[j].w, hv[jj].w, acc[j][jj]);
       }
     }
-    // pick the pairs out of the 64 x 64 block
+    // the 64 x 64 block to shared memory; then the tile's pairs -- one
+    // contiguous range of the grouping, each row's slot-ascending -- are
+    // walked flat by the whole CTA (coalesced slots and pair ids, 4
+    // positions in flight per thread) and those of this sample block pick
+    // their logit
+    __syncthreads();  // readers of ws / hs are done
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int row = ty + 16 * j;
-      if (row >= nrow) continue;
-      const uint32_t* mrow = g.mask_of(u0 + row);
+    for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const int i = s0 + tx + 16 * jj;
-        if (i >= b) continue;
-        const uint32_t word = mrow[i >> 5];
-        if ((word >> (i & 31)) & 1u) {
-          const int rank = cum[row * kMaskWords + (i >> 5)] + __popc(word & ((1u << (i & 31)) - 1u));
-          z[g.order[base_s[row] + rank]] = acc[j][jj] + bias_s[row];
+      for (int jj = 0; jj < 4; ++jj) zt[(ty + 16 * j) * kZLd + tx + 16 * jj] = acc[j][jj];
+    __syncthreads();
+    const int pbeg = base_s[0], pend = base_s[nrow - 1] + len_s[nrow - 1];
+    for (int p0 = pbeg + tid; p0 < pend; p0 += 256 * 4) {
+      int sl[4], od[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int pos = p0 + 256 * t;
+        sl[t] = pos < pend ? g.sslot[pos] - s0 : -1;
+        od[t] = pos < pend ? g.order[pos] : 0;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (sl[t] < 0 || sl[t] >= kTN) continue;
+        const int pos = p0 + 256 * t;
+        int lo = 0, hi = nrow - 1;  // the row holding pos: last base_s <= pos
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (base_s[mid] <= pos) lo = mid;
+          else hi = mid - 1;
         }
+        z[od[t]] = zt[lo * kZLd + sl[t]] + bias_s[lo];
       }
     }
-    __syncthreads();  // cum / base / bias / wrow reuse by the next item
+    __syncthreads();  // zt / base / len / bias / wrow reuse by the next item
   }
 }
 
@@ -420,7 +433,7 @@ void launch_logits_rows(int hp, int b, const GroupView& g, const int32_t* pslot,
   // dense tiles need the whole batch's slot masks in 32 words
   const int dense_ok = b <= 32 * kMaskWords;
   if (dense_ok) {
-    const int grid = (int)std::min<int64_t>(ceil_div(g.u_max, kTM) * ceil_div(b, kTN), (int64_t)kSms * 2);
+    const int grid = (int)std::min<int64_t>(ceil_div(g.u_max, kTM) * ceil_div(b, kTN), (int64_t)kSms * 3);
     SLIDE_NV_DISPATCH(hp, ({
       SLIDE_CUDA(cudaFuncSetAttribute(logits_tiles_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kTileSmem));
