@@ -753,12 +753,13 @@ __device__ __forceinline__ void adam_rows_loop(const AdamRowsArgs& A, const int 
   // persistent warps take rows from a counter: a CTA's slot is never held
   // by idle warps waiting on one long row; the next row is claimed while
   // this one is updated
-  int u = 0;
-  if (lane == 0) u = atomicAdd(A.work, 1);
-  u = __shfl_sync(0xffffffffu, u, 0);
+  // (the first row of every warp is its own index: no burst of claims on
+  // the counter at launch; later rows come from the counter past them)
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  int u = blockIdx.x * (blockDim.x >> 5) + wid;
   while (u < nu) {
     int u_next = 0;
-    if (lane == 0) u_next = atomicAdd(A.work, 1);
+    if (lane == 0) u_next = nwarps + atomicAdd(A.work, 1);
     uint32_t tmask = 0;
     const int r = A.uniq[u];
     const int s0 = A.seg_off[u], len = A.seg_cnt[u];
@@ -774,17 +775,24 @@ __device__ __forceinline__ void adam_rows_loop(const AdamRowsArgs& A, const int 
     }
     float bb = A.b2[r], mb = A.mb2[r], vb = A.vb2[r];
     const int64_t st = A.steps2[r];
+    // lane j holds the j-th pair of a chunk; the next chunk's slot and error
+    // are loaded while this one updates
+    int slot_n = 0;
+    float d_n = 0.f;
+    if (lane < len) {
+      slot_n = A.sslot[s0 + lane];
+      d_n = A.dsort[s0 + lane];
+    }
     for (int c0 = 0; c0 < len; c0 += 32) {
-      // lane j holds the j-th pair of this chunk
       const int j = c0 + lane;
       const bool valid = j < len;
-      int slot_l = 0;
-      float d_l = 0.f;
+      const int slot_l = valid ? slot_n : 0;
+      const float d_l = valid ? d_n : 0.f;
       float2 bc_l = make_float2(0.f, 1.f);
-      if (valid) {
-        slot_l = A.sslot[s0 + j];
-        d_l = A.dsort[s0 + j];
-        bc_l = bias_corr(A.ap, st + j + 1);
+      if (valid) bc_l = bias_corr(A.ap, st + j + 1);
+      if (j + 32 < len) {
+        slot_n = A.sslot[s0 + j + 32];
+        d_n = A.dsort[s0 + j + 32];
       }
       const float e1_l = ak.omb1 * d_l, e2_l = ak.omb2 * d_l * d_l;
       const float s2_l = sqrt_approx(bc_l.y);
