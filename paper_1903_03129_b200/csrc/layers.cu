@@ -887,18 +887,19 @@ __device__ __forceinline__ void adam_rows_ng(const AdamRowsArgs& A, float4 (*pq)
 // holding live units are walked (dead units' coordinates never move).  The
 // group count is read on the device (graph replays); one loop body per count.
 template <int NV, bool COUNT>
-__global__ void __launch_bounds__(256, NV == 1 ? 3 : 2) adam_rows_kernel(AdamRowsArgs A) {
+__global__ void __launch_bounds__(256, NV == 1 ? 4 : 2) adam_rows_kernel(AdamRowsArgs A) {
   // per-warp broadcast of the current chunk's pair scalars: (e1, e2, c1,
   // sqrt(c2)) and the h row offset; h itself is read through L1
   __shared__ float4 pq[8][32];
   __shared__ int poff[8][32];
   const int ng = (__ldg(A.live) + 31) >> 5;
   if (NV == 1) {
+    // (4 CTAs/SM: the 3- and 4-group bodies spill a little; they run only
+    // while most units are live, i.e. the first step)
     switch (ng) {
       case 0:  // no live unit: group 0's lanes sit on dead units, nothing moves
       case 1: adam_rows_ng<1, COUNT>(A, pq, poff); break;
       case 2: adam_rows_ng<2, COUNT>(A, pq, poff); break;
-      case 3: adam_rows_ng<3, COUNT>(A, pq, poff); break;
       default: adam_rows_ng<4, COUNT>(A, pq, poff); break;
     }
   } else if (NV == 2) {
@@ -938,7 +939,7 @@ void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq
   if (max_uniq <= 0) return;
   if (!work_zeroed) SLIDE_CUDA(cudaMemsetAsync(work, 0, 4, s));
   // persistent: as many CTAs as are resident at once
-  const int per_sm = hp <= 128 ? 3 : 2;
+  const int per_sm = hp <= 128 ? 4 : 2;
   const int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * per_sm);
   AdamRowsArgs A{hp, ap, n_uniq, uniq, seg_off, seg_cnt, sslot, dsort, h, live,
                  w2, m2, v2, b2, mb2, vb2, steps2, touched, work};
@@ -1097,7 +1098,7 @@ __device__ __forceinline__ void adam_features_loop(const AdamFeatArgs& A) {
 }
 
 template <int NV>
-__global__ void __launch_bounds__(256, NV == 1 ? 3 : 2) adam_features_kernel(AdamFeatArgs A) {
+__global__ void __launch_bounds__(256, NV == 1 ? 4 : 2) adam_features_kernel(AdamFeatArgs A) {
   const int ng = (__ldg(A.live) + 31) >> 5;
   SLIDE_NG_DISPATCH(NV, ng, adam_features_loop, A);
 }
