@@ -345,6 +345,8 @@ def run_ours(args, rank, world):
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None,
+        # per-step spread (the steps whose barrier rebuilt the tables are the max)
+        "ms_per_step_p50": float(np.median(times)), "ms_per_step_max": float(np.max(times)),
         "dtype": "f32", "data": "synthetic (SURVEY 8(d) Zipf generator; Delicious-200K shape)",
         "config": {"workload": w.name, "input_dim": w.input_dim, "hidden": w.hidden, "n_out": w.n_out,
                    "batch": w.batch, "hash": f"{w.family} K={w.k} L={w.l} cap={w.cap} {w.policy}",

@@ -66,7 +66,7 @@ struct slide_ctx {
   cudaEvent_t ev_fork = nullptr, ev_dh = nullptr, ev_join = nullptr, ev_pre = nullptr;
   // third stream: the per-row logits beside the dense-tile logits
   cudaStream_t s3 = nullptr;
-  cudaEvent_t ev_lg = nullptr, ev_lg_join = nullptr;
+  cudaEvent_t ev_lg = nullptr, ev_lg_join = nullptr, ev_w1l = nullptr;
   DBuf hg_done;  // per-sample slice tickets of the hidden gradient (self-resetting)
   int64_t hg_done_n = 0;
   // set by the fused step callers: forward already queues the W1 grouping
@@ -295,7 +295,7 @@ int slide_destroy(slide_ctx* c) {
     c->gfeat.release();
     if (c->s2) cudaStreamSynchronize(c->s2);
     if (c->s3) cudaStreamSynchronize(c->s3);
-    for (cudaEvent_t e : {c->ev_fork, c->ev_dh, c->ev_join, c->ev_pre, c->ev_lg, c->ev_lg_join})
+    for (cudaEvent_t e : {c->ev_fork, c->ev_dh, c->ev_join, c->ev_pre, c->ev_lg, c->ev_lg_join, c->ev_w1l})
       if (e) cudaEventDestroy(e);
     if (c->s2) cudaStreamDestroy(c->s2);
     if (c->s3) cudaStreamDestroy(c->s3);
@@ -490,7 +490,7 @@ static void side_stream_init(slide_ctx* c) {
   if (c->s2) return;
   SLIDE_CUDA(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
   SLIDE_CUDA(cudaStreamCreateWithFlags(&c->s3, cudaStreamNonBlocking));
-  for (cudaEvent_t* e : {&c->ev_fork, &c->ev_dh, &c->ev_join, &c->ev_pre, &c->ev_lg, &c->ev_lg_join})
+  for (cudaEvent_t* e : {&c->ev_fork, &c->ev_dh, &c->ev_join, &c->ev_pre, &c->ev_lg, &c->ev_lg_join, &c->ev_w1l})
     SLIDE_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
 }
 
@@ -543,6 +543,7 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     SLIDE_CUDA(cudaEventRecord(c->ev_pre, s));
     SLIDE_CUDA(cudaStreamWaitEvent(c->s2, c->ev_pre, 0));
     int32_t* xs = c->xslot.ensure<int32_t>(nnz);
+    c->gfeat.long_min = kW1LongChain;
     c->gfeat.prepare(d.input_dim, b, nnz);
     launch_x_slots(b, bt->x_ptr, xs, c->s2);
     c->gfeat.run(bt->x_idx + x_base, xs, stat ? bt->x_ptr + b : nullptr, nnz, nnz, c->s2);
@@ -736,6 +737,7 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
     }
   }
   int32_t* xs = nnz > 0 ? c->xslot.ensure<int32_t>(nnz) : nullptr;
+  gf.long_min = kW1LongChain;  // the grouping lists the long chains for the W1 Adam
   if (nnz > 0) gf.prepare(d.input_dim, b, nnz);  // host-side sizing before any branch launches
   auto group_features = [&](cudaStream_t st) {
     if (nnz <= 0) return;
@@ -768,8 +770,6 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
   int32_t* tc = c->tc.ensure<int32_t>((size_t)b * hp);
   float2* bc = c->bc.ensure<float2>((size_t)b * hp);
   int32_t* work = c->work.ensure<int32_t>(4);
-  int32_t* long_list = c->long_list.ensure<int32_t>(std::max<int64_t>(gf.u_max, 1));
-  int32_t* n_long = c->n_long.ensure<int32_t>(1);
   // W1 branch: per-unit step counts + bias corrections and the hidden biases
   // (one fused pass), then the W1 Adam over the feature grouping
   auto w1_update = [&](cudaStream_t st) {
@@ -781,10 +781,17 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
       c->timer.mark(st, kStGroupFeat);
     }
     c->w1_grouped = false;
+    // the long chains on the third stream, beside the short ones
+    cudaStream_t sl = st;
+    if (fork) {
+      sl = c->s3;
+      SLIDE_CUDA(cudaEventRecord(c->ev_w1l, st));
+      SLIDE_CUDA(cudaStreamWaitEvent(sl, c->ev_w1l, 0));
+    }
     launch_adam_features(hp, ap, gf.n_uniq.as<int32_t>(), gf.u_max, gf.uniq.as<int32_t>(), gf.seg_off.as<int32_t>(),
                          gf.seg_cnt.as<int32_t>(), gf.order.as<int32_t>(), xs, c->last_xval, c->last_xbase,
                          c->h.as<float>(), dh, bc, c->live.as<int32_t>(), d.w1t, d.m1t, d.v1t,
-                         ctr ? ctr + 1 : nullptr, long_list, n_long, st);
+                         ctr ? ctr + 1 : nullptr, gf.long_list.as<int32_t>(), gf.n_long.as<int32_t>(), st, sl);
     c->timer.mark(st, kStAdamFeat);
     gf.clear(st);
   };

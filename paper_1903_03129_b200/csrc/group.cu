@@ -144,7 +144,7 @@ __global__ void g_mask_kernel(const int32_t* __restrict__ keys, const int32_t* _
 // segment sizes (popc of each unique key's slot mask) -> exclusive offsets
 __global__ void __launch_bounds__(kGT) g_seg_kernel(const uint32_t* __restrict__ mask, int wpk,
                                                     const int32_t* __restrict__ n_uniq, int32_t* __restrict__ seg_off,
-                                                    int32_t* __restrict__ seg_cnt, TileCtl tc) {
+                                                    int32_t* __restrict__ seg_cnt, TileCtl tc, LongList ll) {
   __shared__ typename GScan::TempStorage tmp;
   __shared__ int s_tile, s_base;
   const int64_t nu = *n_uniq;
@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(kGT) g_seg_kernel(const uint32_t* __restrict__
   if (u < nu) {
     seg_off[u] = s_base + off;
     seg_cnt[u] = c;
+    if (ll.list && c > ll.min_len) ll.list[atomicAdd(ll.n, 1)] = (int32_t)u;
   }
 }
 
@@ -242,7 +243,7 @@ __device__ __forceinline__ unsigned long long tile_lookback2(int tile, unsigned 
 __global__ void __launch_bounds__(kGT) gd_scan_kernel(int64_t K, int wpk, const uint32_t* __restrict__ mask,
                                                       int32_t* __restrict__ uniq, int32_t* __restrict__ key_rank,
                                                       int32_t* __restrict__ seg_off, int32_t* __restrict__ seg_cnt,
-                                                      int32_t* __restrict__ n_uniq, TileCtl tc) {
+                                                      int32_t* __restrict__ n_uniq, TileCtl tc, LongList ll) {
   using Scan2 = cub::BlockScan<unsigned long long, kGT>;
   __shared__ typename Scan2::TempStorage tmp;
   __shared__ int s_tile;
@@ -269,6 +270,7 @@ __global__ void __launch_bounds__(kGT) gd_scan_kernel(int64_t K, int wpk, const 
     key_rank[key] = r;
     seg_off[r] = po;
     seg_cnt[r] = c;
+    if (ll.list && c > ll.min_len) ll.list[atomicAdd(ll.n, 1)] = r;
   }
   if (key == K - 1) *n_uniq = r + (c ? 1 : 0);
 }
@@ -351,13 +353,20 @@ void GroupBy::prepare(int64_t key_space, int64_t slots, int64_t items_max) {
 
 void GroupBy::run(const int32_t* keys, const int32_t* slots, const int32_t* n_dev, int64_t n_host, int64_t n_max,
                   cudaStream_t s) {
+  // optional list of the segments longer than long_min (in no fixed order)
+  LongList long_out{nullptr, nullptr, long_min};
+  if (long_min >= 0) {
+    long_out.list = long_list.ensure<int32_t>(std::max<int64_t>(u_max, 1));
+    long_out.n = n_long.ensure<int32_t>(1);
+    SLIDE_CUDA(cudaMemsetAsync(long_out.n, 0, 4, s));
+  }
   if (dense) {
     const TileCtl t{status.as<unsigned long long>(), ctrs.as<int32_t>()};
     gd_mask_kernel<<<grid_of(n_max), 256, 0, s>>>(keys, slots, n_dev, n_host, wpk, mask.as<uint32_t>(), t, tiles_bits);
     SLIDE_LAUNCH_CHECK();
     gd_scan_kernel<<<(int)tiles_bits, kGT, 0, s>>>(K, wpk, mask.as<uint32_t>(), uniq.as<int32_t>(),
                                                    key_rank.as<int32_t>(), seg_off.as<int32_t>(),
-                                                   seg_cnt.as<int32_t>(), n_uniq.as<int32_t>(), t);
+                                                   seg_cnt.as<int32_t>(), n_uniq.as<int32_t>(), t, long_out);
     SLIDE_LAUNCH_CHECK();
     gd_place_kernel<<<grid_of(n_max), 256, 0, s>>>(keys, slots, n_dev, n_host, key_rank.as<int32_t>(), wpk,
                                                    mask.as<uint32_t>(), seg_off.as<int32_t>(), order.as<int32_t>(),
@@ -377,7 +386,7 @@ void GroupBy::run(const int32_t* keys, const int32_t* slots, const int32_t* n_de
                                                 mask.as<uint32_t>(), t2, tiles_seg);
   SLIDE_LAUNCH_CHECK();
   g_seg_kernel<<<(int)tiles_seg, kGT, 0, s>>>(mask.as<uint32_t>(), wpk, n_uniq.as<int32_t>(), seg_off.as<int32_t>(),
-                                              seg_cnt.as<int32_t>(), t2);
+                                              seg_cnt.as<int32_t>(), t2, long_out);
   SLIDE_LAUNCH_CHECK();
   g_place_kernel<<<grid_of(n_max), 256, 0, s>>>(keys, slots, n_dev, n_host, key_rank.as<int32_t>(), wpk,
                                                  mask.as<uint32_t>(), seg_off.as<int32_t>(), order.as<int32_t>(),
@@ -397,7 +406,8 @@ void GroupBy::clear(cudaStream_t s) {
 }
 
 void GroupBy::release() {
-  for (DBuf* b : {&bits, &key_rank, &uniq, &seg_cnt, &seg_off, &n_uniq, &mask, &order, &inv, &sslot, &status, &ctrs})
+  for (DBuf* b : {&bits, &key_rank, &uniq, &seg_cnt, &seg_off, &n_uniq, &mask, &order, &inv, &sslot, &status, &ctrs,
+                  &long_list, &n_long})
     b->release();
   bits_words = mask_words = 0;
   mask_dense = false;

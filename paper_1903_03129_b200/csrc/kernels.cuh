@@ -75,8 +75,18 @@ struct GroupView {
   }
 };
 
+struct LongList {
+  int32_t* list;
+  int32_t* n;
+  int min_len;
+};
+
 struct GroupBy {
   DBuf bits, key_rank, uniq, seg_cnt, seg_off, n_uniq, mask, order, status, ctrs;
+  // long_min >= 0: run() also lists the segments with more than long_min
+  // items (long_list[0 .. *n_long), unordered)
+  int long_min = -1;
+  DBuf long_list, n_long;
   // want_inv: also inv[q] = sorted position of item q and sslot[pos] = its slot
   bool want_inv = false;
   DBuf inv, sslot;
@@ -148,8 +158,10 @@ void launch_adam_features(int hp, const AdamParams& ap, const int32_t* n_uniq, i
                           const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
                           const int32_t* sorted_k, const int32_t* x_slot, const float* x_val, int64_t x_base,
                           const float* h, const float* dh, const float2* bc, const int32_t* live, float* w1t,
-                          float* m1t, float* v1t, unsigned long long* touched, int32_t* long_list, int32_t* n_long,
-                          cudaStream_t s);
+                          float* m1t, float* v1t, unsigned long long* touched, const int32_t* long_list,
+                          const int32_t* n_long, cudaStream_t s, cudaStream_t s_long);
+// chains longer than this go to the segmented long-chain kernel
+constexpr int kW1LongChain = 16;
 void launch_hidden_prep_bias(int hp, int b, const AdamParams& ap, const float* h, const float* dh, int64_t* steps1,
                              int32_t* tc, float2* bc, float* b1, float* mb1, float* vb1, cudaStream_t s);
 void launch_adam_hidden_bias(int hp, int b, const AdamParams& ap, const float* h, const float* dh, const int32_t* tc,

@@ -738,16 +738,28 @@ template <int NG>
 struct AdamPf {
   static constexpr int value = NG >= 4 ? 2 : 8 / NG;
 };
+constexpr int kAdamExtra = 8;  // live units past whole groups taken in scan form
 
 // The persistent row loop for NG live 32-unit groups (compile-time, so the
 // per-pair body has no group guards and the next kAdamPf pairs' activations
 // are in flight before their updates start).
-template <int NG, bool COUNT>
+// EX > 0: besides the NG full groups, up to EX further live units (the
+// count ne is read on the device) go through the scan form of the
+// recurrences -- lanes = the chunk's pairs, one unit at a time, like the
+// bias -- instead of a whole extra group of lanes (a batch with 33 live
+// units would otherwise pay a second 32-unit group for one unit).  Lane e
+// keeps extra unit e's (w, m, v).
+template <int NG, int EX, bool COUNT>
 __device__ __forceinline__ void adam_rows_loop(const AdamRowsArgs& A, const int (&col)[NG], float4 (*pq)[32],
                                                int (*poff)[32]) {
   constexpr int kAdamPf = AdamPf<NG>::value;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int hp = A.hp;
+  int ne = 0, xc = 0;
+  if (EX > 0) {
+    ne = min(EX, max(0, __ldg(A.live) - NG * 32));
+    xc = __ldg(A.live + 1 + NG * 32 + (lane < ne ? lane : 0));
+  }
   const int nu = *A.n_uniq;
   const AdamK ak(A.ap);
   // persistent warps take rows from a counter: a CTA's slot is never held
@@ -772,6 +784,12 @@ __device__ __forceinline__ void adam_rows_loop(const AdamRowsArgs& A, const int 
       w[q] = wr[col[q]];
       m[q] = mr[col[q]];
       v[q] = vr[col[q]];
+    }
+    float xw = 0.f, xm = 0.f, xv = 0.f;  // lane e < ne: extra unit e
+    if (EX > 0 && lane < ne) {
+      xw = wr[xc];
+      xm = mr[xc];
+      xv = vr[xc];
     }
     float bb = A.b2[r], mb = A.mb2[r], vb = A.vb2[r];
     const int64_t st = A.steps2[r];
@@ -824,6 +842,38 @@ __device__ __forceinline__ void adam_rows_loop(const AdamRowsArgs& A, const int 
         mb = __shfl_sync(0xffffffffu, mj, 31);
         vb = __shfl_sync(0xffffffffu, vj, 31);
       }
+      // extra units: the same scans with the pair's activation as a factor
+      for (int e = 0; e < ne; ++e) {
+        const int c = __shfl_sync(0xffffffffu, xc, e);
+        const float hc = valid ? __ldg(A.h + ((unsigned)(slot_l * hp) + (unsigned)c)) : 0.f;
+        const bool on = hc > 0.f;
+        float a1 = on ? ak.b1 : 1.f, x1 = on ? e1_l * hc : 0.f;
+        float a2 = on ? ak.b2 : 1.f, x2 = on ? e2_l * (hc * hc) : 0.f;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const float pa1 = __shfl_up_sync(0xffffffffu, a1, o), px1 = __shfl_up_sync(0xffffffffu, x1, o);
+          const float pa2 = __shfl_up_sync(0xffffffffu, a2, o), px2 = __shfl_up_sync(0xffffffffu, x2, o);
+          if (lane >= o) {
+            x1 = fmaf(a1, px1, x1);
+            a1 *= pa1;
+            x2 = fmaf(a2, px2, x2);
+            a2 *= pa2;
+          }
+        }
+        const float mj = fmaf(a1, __shfl_sync(0xffffffffu, xm, e), x1);
+        const float vj = fmaf(a2, __shfl_sync(0xffffffffu, xv, e), x2);
+        float upd = on ? (bc_l.x * mj) * rcp_approx(fmaf(sqrt_approx(vj), s2_l, ak.eps)) : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) upd += __shfl_xor_sync(0xffffffffu, upd, o);
+        const float ml = __shfl_sync(0xffffffffu, mj, 31), vl = __shfl_sync(0xffffffffu, vj, 31);
+        const unsigned moved = __ballot_sync(0xffffffffu, on);
+        if (lane == e) {
+          xw -= upd;
+          xm = ml;
+          xv = vl;
+          if (COUNT) tmask |= (moved ? 1u : 0u) << 31;  // (a distinct bit per lane: summed by popc below)
+        }
+      }
       const int nc = min(32, len - c0);
       // kAdamPf pairs at a time: their activations are loaded before the
       // first of their updates; in the chunk's tail batch the pairs past nc
@@ -858,6 +908,11 @@ __device__ __forceinline__ void adam_rows_loop(const AdamRowsArgs& A, const int 
       mr[col[q]] = m[q];
       vr[col[q]] = v[q];
     }
+    if (EX > 0 && lane < ne) {
+      wr[xc] = xw;
+      mr[xc] = xm;
+      vr[xc] = xv;
+    }
     if (lane == 0) {
       A.b2[r] = bb;
       A.mb2[r] = mb;
@@ -874,13 +929,13 @@ __device__ __forceinline__ void adam_rows_loop(const AdamRowsArgs& A, const int 
   }
 }
 
-template <int NG, bool COUNT>
+template <int NG, bool COUNT, int EX = 0>
 __device__ __forceinline__ void adam_rows_ng(const AdamRowsArgs& A, float4 (*pq)[32], int (*poff)[32]) {
   int col[NG];
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int q = 0; q < NG; ++q) col[q] = __ldg(A.live + 1 + q * 32 + lane);
-  adam_rows_loop<NG, COUNT>(A, col, pq, poff);
+  adam_rows_loop<NG, EX, COUNT>(A, col, pq, poff);
 }
 
 // lane l owns unit live[1 + 32 q + l] of live group q: only the groups
@@ -892,7 +947,17 @@ __global__ void __launch_bounds__(256, NV == 1 ? 4 : 2) adam_rows_kernel(AdamRow
   // sqrt(c2)) and the h row offset; h itself is read through L1
   __shared__ float4 pq[8][32];
   __shared__ int poff[8][32];
-  const int ng = (__ldg(A.live) + 31) >> 5;
+  const int nl = __ldg(A.live);
+  const int ng = (nl + 31) >> 5;
+  // a few units past a whole group: the group plus scan-form extras
+  if (nl > 32 && nl <= 32 + kAdamExtra) {
+    adam_rows_ng<1, COUNT, kAdamExtra>(A, pq, poff);
+    return;
+  }
+  if (NV >= 2 && nl > 64 && nl <= 64 + kAdamExtra) {
+    adam_rows_ng<2, COUNT, kAdamExtra>(A, pq, poff);
+    return;
+  }
   if (NV == 1) {
     // (4 CTAs/SM: the 3- and 4-group bodies spill a little; they run only
     // while most units are live, i.e. the first step)
@@ -995,7 +1060,6 @@ void launch_hidden_counts(int hp, int b, const AdamParams& ap, const float* h, c
   SLIDE_LAUNCH_CHECK();
 }
 
-constexpr int kLongChain = 16;
 constexpr int kColGroup = 8;  // pairs per prefetch group of the column path
 
 struct AdamFeatArgs {
@@ -1009,10 +1073,10 @@ struct AdamFeatArgs {
   const int32_t* live;
   float *w1t, *m1t, *v1t;
   unsigned long long* touched;
-  int32_t *long_list, *n_long;
+  const int32_t *long_list, *n_long;  // the grouping's chains longer than kW1LongChain
 };
 
-// Short chains (<= kLongChain samples hold the feature), one warp per
+// Short chains (<= kW1LongChain samples hold the feature), one warp per
 // feature row, lane l on unit live[1 + 32 q + l] of live group q; every
 // pair's (h, dh, bias corrections) loads are issued before its updates.
 template <int NG>
@@ -1027,14 +1091,11 @@ __device__ __forceinline__ void adam_features_loop(const AdamFeatArgs& A) {
   int col[NG];
 #pragma unroll
   for (int q = 0; q < NG; ++q) col[q] = __ldg(A.live + 1 + q * 32 + lane);
-  // a long chain (a hot feature held by many samples) goes to the column
-  // kernel: appended to long_list here
+  // a long chain (a hot feature held by many samples) is the long-chain
+  // kernel's (the grouping listed it)
   for (int64_t u = gw; u < nu; u += nw) {
     const int len = A.seg_cnt[u];
-    if (len > kLongChain) {
-      if (lane == 0) A.long_list[atomicAdd(A.n_long, 1)] = (int32_t)u;
-      continue;
-    }
+    if (len > kW1LongChain) continue;
     uint32_t tmask = 0;
     const int f = A.uniq[u];
     const int s0 = A.seg_off[u];
@@ -1103,7 +1164,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? 4 : 2) adam_features_kernel(Ada
   SLIDE_NG_DISPATCH(NV, ng, adam_features_loop, A);
 }
 
-// Long chains (a hot feature held by > kLongChain samples): work item =
+// Long chains (a hot feature held by > kW1LongChain samples): work item =
 // (feature, live 32-unit group), one CTA of kLongWarps warps, lane = unit.
 // The feature's pairs are cut into kLongWarps consecutive segments.  The
 // moments are linear recurrences, so each warp first folds its segment into
@@ -1217,19 +1278,19 @@ void launch_adam_features(int hp, const AdamParams& ap, const int32_t* n_uniq, i
                           const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
                           const int32_t* sorted_k, const int32_t* x_slot, const float* x_val, int64_t x_base,
                           const float* h, const float* dh, const float2* bc, const int32_t* live, float* w1t,
-                          float* m1t, float* v1t, unsigned long long* touched, int32_t* long_list, int32_t* n_long,
-                          cudaStream_t s) {
+                          float* m1t, float* v1t, unsigned long long* touched, const int32_t* long_list,
+                          const int32_t* n_long, cudaStream_t s, cudaStream_t s_long) {
   if (max_uniq <= 0) return;
-  SLIDE_CUDA(cudaMemsetAsync(n_long, 0, 4, s));
   int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * 16);
   AdamFeatArgs A{hp, ap, n_uniq, uniq, seg_off, seg_cnt, sorted_k, x_slot, x_val, x_base, h, dh, bc, live,
                  w1t, m1t, v1t, touched, long_list, n_long};
   SLIDE_NV_DISPATCH(hp, (adam_features_kernel<NV><<<grid, 256, 0, s>>>(A)));
   SLIDE_LAUNCH_CHECK();
-  // long chains: at most max_uniq * (1 / (kLongChain + 1)) of them
-  const int64_t max_long = std::min<int64_t>(max_uniq, ceil_div(max_uniq, kLongChain)) * (hp / 32);
+  // long chains (on s_long, beside the short ones): at most
+  // max_uniq / (kW1LongChain + 1) of them
+  const int64_t max_long = std::min<int64_t>(max_uniq, ceil_div(max_uniq, kW1LongChain)) * (hp / 32);
   const int lgrid = (int)std::min<int64_t>(std::max<int64_t>(max_long, 1), (int64_t)kSms * 16);
-  adam_features_long_kernel<<<lgrid, kLongWarps * 32, 0, s>>>(A);
+  adam_features_long_kernel<<<lgrid, kLongWarps * 32, 0, s_long>>>(A);
   SLIDE_LAUNCH_CHECK();
 }
 

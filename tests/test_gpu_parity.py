@@ -551,11 +551,14 @@ def test_pipelined_batches_equal_per_call_steps():
     np.testing.assert_array_equal(a.w1t.cpu().numpy(), b.w1t.cpu().numpy())
 
 
-def test_live_unit_permutation_tracks_the_batch():
+@pytest.mark.parametrize("alive", ["half", "36"])
+def test_live_unit_permutation_tracks_the_batch(alive):
     """The hidden forward's live-unit list (the units nonzero in some sample,
     ascending, then the dead ones) equals h's nonzero columns after every
     step; with half the hidden units dead (bias -5) the row kernels walk only
-    the live groups and the trained state still matches the oracle."""
+    the live groups, and with 36 live units (bias +0.5, the rest -5) the W2
+    Adam takes the 4 units past the first group in scan form; the trained
+    state matches the oracle either way."""
     from paper_1903_03129_b200.configs import TINY as w
     from paper_1903_03129_b200.data import synthetic_corpus
 
@@ -564,7 +567,11 @@ def test_live_unit_permutation_tracks_the_batch():
     spec = LshLayerConfig("simhash", k=w.k, l=w.l, capacity=w.cap, sampler=SamplerConfig("vanilla", beta=w.beta))
     net = SlideNetwork(w.input_dim, [w.hidden, w.n_out], cfg, lsh_layers={1: spec})
     b = np.array(net.layers[0].b)
-    b[::2] = -5.0  # even units dead for every input
+    if alive == "half":
+        b[::2] = -5.0  # even units dead for every input
+    else:
+        b[:] = -5.0
+        b[np.random.default_rng(3).choice(w.hidden, 36, replace=False)] = 0.5
     net.layers[0].b[:] = b
     hp = net.hidden_pad
     lsh = oracle_lsh_from_net(net, spec)  # the tables as built at construction (no rebuild in these steps)
@@ -579,6 +586,8 @@ def test_live_unit_permutation_tracks_the_batch():
         on = np.flatnonzero((h > 0).any(0))
         n = int(live[0])
         assert 0 < n <= hp // 2 and n == on.size
+        if alive != "half":
+            assert n == 36
         np.testing.assert_array_equal(live[1:1 + n], on)
         np.testing.assert_array_equal(np.sort(live[1:]), np.arange(hp))
         assert np.all(np.diff(live[1 + n:]) > 0)
