@@ -653,12 +653,11 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     launch_own_filter(b, act, cap_max, c->g, c->G, cnt, c->cnt_all.ensure<int32_t>(b), s);
   // pair count stays on the device (offs[b]); buffers are sized by the bound
   int32_t* offs = c->offs.ensure<int32_t>(b + 1);
-  launch_offsets(b, cnt, offs, s);
   const int64_t P_max = (int64_t)b * cap_max;
   int32_t* prow = c->prow.ensure<int32_t>(P_max);
   int32_t* pslot = c->pslot.ensure<int32_t>(P_max);
   uint8_t* plab = c->plab.ensure<uint8_t>(P_max);
-  launch_pairs(b, act, cap_max, offs, c->G, prow, pslot, plab, s);
+  launch_pairs(b, act, cap_max, cnt, offs, c->G, prow, pslot, plab, s);
   c->timer.mark(s, kStCompact);
   float* z = c->z.ensure<float>(P_max);
   float* prob = c->prob.ensure<float>(P_max);

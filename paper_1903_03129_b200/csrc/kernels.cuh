@@ -49,9 +49,9 @@ void launch_fallback(const FallbackArgs& a, int b, cudaStream_t s);
 void launch_explicit_active(int b, int64_t n, const int32_t* fptr, const int32_t* fidx, const int32_t* y_ptr,
                             const int32_t* y_idx, int64_t cap_max, int32_t* act, int32_t* cnt, int32_t* empty,
                             cudaStream_t s);
-void launch_offsets(int b, const int32_t* cnt, int32_t* offs, cudaStream_t s);
-void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* offs, int shard_count, int32_t* prow,
-                  int32_t* pslot, uint8_t* plab, cudaStream_t s);
+// pair lists from the per-slot active sets; also writes offs (B + 1) from cnt
+void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* cnt, int32_t* offs, int shard_count,
+                  int32_t* prow, int32_t* pslot, uint8_t* plab, cudaStream_t s);
 void launch_own_filter(int b, int32_t* act, int64_t cap_max, int g, int G, int32_t* cnt, int32_t* cnt_all,
                        cudaStream_t s);
 // sharded softmax phases (per sample over the owned pairs)

@@ -469,27 +469,37 @@ void launch_explicit_active(int b, int64_t n, const int32_t* fptr, const int32_t
 // ------------------------------------------------------------- compaction
 // Exclusive scan of per-slot counts (B <= 1024) and the sample-major pair
 // list: row id, slot, label flag.
-__global__ void offsets_kernel(int b, const int32_t* __restrict__ cnt, int32_t* __restrict__ offs) {
-  using Scan = cub::BlockScan<int, 1024>;
-  __shared__ typename Scan::TempStorage tmp;
-  int v = threadIdx.x < b ? cnt[threadIdx.x] : 0, o, total;
-  Scan(tmp).ExclusiveSum(v, o, total);
-  if (threadIdx.x < b) offs[threadIdx.x] = o;
-  if (threadIdx.x == 0) offs[b] = total;
-}
-
-void launch_offsets(int b, const int32_t* cnt, int32_t* offs, cudaStream_t s) {
-  SLIDE_CHECK(b <= 1024, kNotSupported, "batch size above 1024 not supported on the device path");
-  offsets_kernel<<<1, 1024, 0, s>>>(b, cnt, offs);
-  SLIDE_LAUNCH_CHECK();
-}
-
 // Pair rows are local W2 rows: id / shard_count (identity when unsharded).
-__global__ void pairs_kernel(const int32_t* __restrict__ act, int64_t cap_max, const int32_t* __restrict__ offs,
-                             int shard_count, int32_t* __restrict__ prow, int32_t* __restrict__ pslot,
-                             uint8_t* __restrict__ plab) {
+// Each CTA (one sample) sums the counts of the samples before it itself --
+// no separate offsets pass; CTA 0 also writes every offset for the later
+// stages (the counts are B <= 1024 ints).
+__global__ void __launch_bounds__(1024) pairs_kernel(int b, const int32_t* __restrict__ act, int64_t cap_max,
+                                                     const int32_t* __restrict__ cnt, int shard_count,
+                                                     int32_t* __restrict__ offs, int32_t* __restrict__ prow,
+                                                     int32_t* __restrict__ pslot, uint8_t* __restrict__ plab) {
+  using Red = cub::BlockReduce<int, 1024>;
+  using Scan = cub::BlockScan<int, 1024>;
+  __shared__ union {
+    typename Red::TempStorage r;
+    typename Scan::TempStorage s;
+  } tmp;
+  __shared__ int s_o;
   const int i = blockIdx.x;
-  const int o = offs[i], n = offs[i + 1] - o;
+  const int c = threadIdx.x < b ? cnt[threadIdx.x] : 0;
+  if (i == 0) {
+    int o, total;
+    Scan(tmp.s).ExclusiveSum(c, o, total);
+    if (threadIdx.x < b) offs[threadIdx.x] = o;
+    if (threadIdx.x == 0) {
+      offs[b] = total;
+      s_o = 0;
+    }
+  } else {
+    const int o = Red(tmp.r).Sum(threadIdx.x < i ? c : 0);
+    if (threadIdx.x == 0) s_o = o;
+  }
+  __syncthreads();
+  const int o = s_o, n = cnt[i];
   const int32_t* src = act + (int64_t)i * cap_max;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     uint32_t v = (uint32_t)src[k];
@@ -500,9 +510,10 @@ __global__ void pairs_kernel(const int32_t* __restrict__ act, int64_t cap_max, c
   }
 }
 
-void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* offs, int shard_count, int32_t* prow,
-                  int32_t* pslot, uint8_t* plab, cudaStream_t s) {
-  pairs_kernel<<<b, 1024, 0, s>>>(act, cap_max, offs, shard_count, prow, pslot, plab);
+void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* cnt, int32_t* offs, int shard_count,
+                  int32_t* prow, int32_t* pslot, uint8_t* plab, cudaStream_t s) {
+  SLIDE_CHECK(b <= 1024, kNotSupported, "batch size above 1024 not supported on the device path");
+  pairs_kernel<<<b, 1024, 0, s>>>(b, act, cap_max, cnt, shard_count, offs, prow, pslot, plab);
   SLIDE_LAUNCH_CHECK();
 }
 
