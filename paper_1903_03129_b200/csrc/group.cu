@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kGT) gd_scan_kernel(int64_t K, int wpk, const 
   const int r = (int)(pre >> 31), po = (int)(pre & 0x7fffffffull);
   if (c) {
     uniq[r] = (int32_t)key;
-    key_rank[key] = r;
+    key_rank[key] = po;  // dense mode: the key's segment offset (all the placement needs)
     seg_off[r] = po;
     seg_cnt[r] = c;
     if (ll.list && c > ll.min_len) ll.list[atomicAdd(ll.n, 1)] = r;
@@ -287,7 +287,7 @@ __global__ void gd_place_kernel(const int32_t* __restrict__ keys, const int32_t*
     int r = 0;
     for (int w = 0; w < (s >> 5); ++w) r += __popc(m[w]);
     r += __popc(m[s >> 5] & ((1u << (s & 31)) - 1u));
-    const int pos = seg_off[key_rank[key]] + r;
+    const int pos = key_rank[key] + r;  // (dense mode: key_rank holds the segment offset)
     order[pos] = (int32_t)q;
     if (inv) {
       inv[q] = pos;
