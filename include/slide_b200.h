@@ -164,9 +164,13 @@ int slide_graph_step(slide_ctx* ctx, const slide_batch* batch, int64_t iteration
                      int64_t* active_host);
 /* The same step split for pipelining (train_batches_csr): _async enqueues
  * the H2D copies, the step and the D2H of losses / set sizes without a host
- * wait (the batch's host buffers must stay untouched until _wait returns);
- * _wait blocks for it and fills loss_host / active_host.  One step in flight
- * per context. */
+ * wait (the batch's host buffers must stay untouched until that step's
+ * _wait returns); _wait blocks for the OLDEST step in flight and fills
+ * loss_host / active_host.  Up to two steps in flight per context, so step
+ * k+1 is queued behind step k before the host waits for k; anything a
+ * barrier enqueues on the context stream between the two (a table rebuild)
+ * runs after step k and before step k+1.  slide_graph_step needs none in
+ * flight. */
 int slide_graph_step_async(slide_ctx* ctx, const slide_batch* batch, int64_t iteration);
 int slide_graph_step_wait(slide_ctx* ctx, double* loss_host, int64_t* active_host);
 

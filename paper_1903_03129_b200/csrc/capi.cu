@@ -56,7 +56,7 @@ enum Stage {
 struct slide_ctx {
   StageTimer timer;
   DBuf counters;  // u64: 0 touched W2 coords, 1 touched W1 coords, 2 unique rows, 3 unique features
-  int64_t host_counts[8] = {0};  // 0 pairs, 1 nnz, 2 samples, 3 rebuilds, 4 fallback slots
+  int64_t host_counts[8] = {0};  // 0 pairs, 1 nnz, 2 samples, 3 rebuilds, 4 fallback slots, 5 graph re-captures
   slide_net_desc d{};
   cudaStream_t s = nullptr;
   // side stream of the backward pass (W1 grouping and W1 Adam run beside
@@ -72,7 +72,6 @@ struct slide_ctx {
   // set by the fused step callers: forward already queues the W1 grouping
   // on the side stream (it needs only the inputs)
   bool w1_prefork = false, w1_grouped = false;
-  int64_t g_pending = 0;  // batch size of the graph step in flight (async API)
   int hp = 0;
   TablesHost tab;
   DBuf sh_packed, sh_packed_t, dw_perms, dw_donors, rowkeys;
@@ -97,11 +96,26 @@ struct slide_ctx {
   DBuf iter_dev, gx_ptr, gx_idx, gx_val, gy_ptr, gy_idx;
   int64_t g_last_pmax = 0;  // host bookkeeping of the captured step
   unsigned long long g_kernels = 0;  // hand-written kernels per replay
-  int32_t* pinned_ptrs = nullptr;  // rebased x_ptr | y_ptr staging
-  int64_t* pinned_iter = nullptr;
-  int64_t pinned_ptrs_n = 0;
+  // Graph steps in flight (async API): up to two, each with its own pinned
+  // staging (rebased x_ptr | y_ptr, iteration) and result slots and an
+  // event after its last copy; a slot is reused two launches later, after
+  // its results were taken.
+  struct GSlot {
+    int32_t* ptrs = nullptr;
+    int64_t ptrs_n = 0;
+    int64_t* iter = nullptr;
+    double* loss = nullptr;
+    int32_t* cnt = nullptr;
+    int64_t res_n = 0;
+    cudaEvent_t ev = nullptr;
+    bool used = false;
+  } gslot[2];
+  int g_next = 0;      // slot of the next launch
+  int g_q[2] = {0, 0};  // pending slots, oldest first
+  int64_t g_qb[2] = {0, 0};
+  int g_qn = 0;
   cudaStream_t gstream = nullptr;
-  cudaEvent_t gev_in = nullptr, gev_out = nullptr;
+  cudaEvent_t gev_in = nullptr;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   int graph_state = 0;  // 0: shapes new (run eagerly), 1: capture next, 2: replay
@@ -303,10 +317,15 @@ int slide_destroy(slide_ctx* c) {
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     if (c->graph) cudaGraphDestroy(c->graph);
     for (DBuf* b : {&c->iter_dev, &c->gx_ptr, &c->gx_idx, &c->gx_val, &c->gy_ptr, &c->gy_idx}) b->release();
-    if (c->pinned_ptrs) cudaFreeHost(c->pinned_ptrs);
-    if (c->pinned_iter) cudaFreeHost(c->pinned_iter);
+    if (c->gstream) cudaStreamSynchronize(c->gstream);
+    for (auto& g : c->gslot) {
+      if (g.ptrs) cudaFreeHost(g.ptrs);
+      if (g.iter) cudaFreeHost(g.iter);
+      if (g.loss) cudaFreeHost(g.loss);
+      if (g.cnt) cudaFreeHost(g.cnt);
+      if (g.ev) cudaEventDestroy(g.ev);
+    }
     if (c->gev_in) cudaEventDestroy(c->gev_in);
-    if (c->gev_out) cudaEventDestroy(c->gev_out);
     if (c->gstream) cudaStreamDestroy(c->gstream);
     if (c->pinned_loss) cudaFreeHost(c->pinned_loss);
     if (c->pinned_cnt) cudaFreeHost(c->pinned_cnt);
@@ -893,12 +912,20 @@ static void graph_step_launch(slide_ctx* c, const slide_batch* bt, int64_t itera
     const int64_t y0 = bt->y_ptr_host[0], nlab = bt->y_ptr_host[B] - y0;
     int64_t max_lab = 0;
     for (int64_t i = 0; i < B; ++i) max_lab = std::max<int64_t>(max_lab, bt->y_ptr_host[i + 1] - bt->y_ptr_host[i]);
+    SLIDE_CHECK(c->g_qn < 2, kValueError, "two graph steps are already in flight");
     if (!c->gstream) {
       SLIDE_CUDA(cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
       SLIDE_CUDA(cudaEventCreateWithFlags(&c->gev_in, cudaEventDisableTiming));
-      SLIDE_CUDA(cudaEventCreateWithFlags(&c->gev_out, cudaEventDisableTiming));
-      SLIDE_CUDA(cudaHostAlloc((void**)&c->pinned_iter, 8, cudaHostAllocDefault));
+      for (auto& g : c->gslot) {
+        SLIDE_CUDA(cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming));
+        SLIDE_CUDA(cudaHostAlloc((void**)&g.iter, 8, cudaHostAllocDefault));
+      }
     }
+    const int slot = c->g_next;
+    auto& gsl = c->gslot[slot];
+    // the launch two steps back used this staging: its copies are done once
+    // its event fired (its results were taken already: g_qn < 2)
+    if (gsl.used) SLIDE_CUDA(cudaEventSynchronize(gsl.ev));
     auto& st = c->st;
     if (!st.on || st.batch != B || nnz > st.nnz_cap || max_lab > st.lab_cap || nlab > st.ylab_cap) {
       if (c->gexec) cudaGraphExecDestroy(c->gexec);
@@ -918,28 +945,36 @@ static void graph_step_launch(slide_ctx* c, const slide_batch* bt, int64_t itera
       c->iter_dev.ensure<int64_t>(1);
       c->graph_state = 0;
     }
-    if (c->pinned_ptrs_n < 2 * (B + 1)) {
-      if (c->pinned_ptrs) cudaFreeHost(c->pinned_ptrs);
-      SLIDE_CUDA(cudaHostAlloc((void**)&c->pinned_ptrs, 2 * (B + 1) * 4, cudaHostAllocDefault));
-      c->pinned_ptrs_n = 2 * (B + 1);
+    if (gsl.ptrs_n < 2 * (B + 1)) {
+      if (gsl.ptrs) cudaFreeHost(gsl.ptrs);
+      SLIDE_CUDA(cudaHostAlloc((void**)&gsl.ptrs, 2 * (B + 1) * 4, cudaHostAllocDefault));
+      gsl.ptrs_n = 2 * (B + 1);
+    }
+    if (gsl.res_n < B) {
+      if (gsl.loss) cudaFreeHost(gsl.loss);
+      if (gsl.cnt) cudaFreeHost(gsl.cnt);
+      SLIDE_CUDA(cudaHostAlloc((void**)&gsl.loss, B * 8, cudaHostAllocDefault));
+      SLIDE_CUDA(cudaHostAlloc((void**)&gsl.cnt, B * 4, cudaHostAllocDefault));
+      gsl.res_n = B;
     }
     cudaStream_t user = c->s, gs = c->gstream;
+    // eager runs and captures read host-side sizes: nothing may be in flight
+    if (c->graph_state < 2 || c->graph_gen != g_slide_realloc_gen) SLIDE_CUDA(cudaStreamSynchronize(gs));
     SLIDE_CUDA(cudaEventRecord(c->gev_in, user));
     SLIDE_CUDA(cudaStreamWaitEvent(gs, c->gev_in, 0));
-    SLIDE_CUDA(cudaStreamSynchronize(gs));  // pinned staging is reused: previous step's copies are done
     for (int64_t i = 0; i <= B; ++i) {
-      c->pinned_ptrs[i] = (int32_t)(bt->x_ptr_host[i] - x0);
-      c->pinned_ptrs[B + 1 + i] = (int32_t)(bt->y_ptr_host[i] - y0);
+      gsl.ptrs[i] = (int32_t)(bt->x_ptr_host[i] - x0);
+      gsl.ptrs[B + 1 + i] = (int32_t)(bt->y_ptr_host[i] - y0);
     }
-    *c->pinned_iter = iteration;
-    SLIDE_CUDA(cudaMemcpyAsync(c->gx_ptr.p, c->pinned_ptrs, (B + 1) * 4, cudaMemcpyHostToDevice, gs));
-    SLIDE_CUDA(cudaMemcpyAsync(c->gy_ptr.p, c->pinned_ptrs + B + 1, (B + 1) * 4, cudaMemcpyHostToDevice, gs));
+    *gsl.iter = iteration;
+    SLIDE_CUDA(cudaMemcpyAsync(c->gx_ptr.p, gsl.ptrs, (B + 1) * 4, cudaMemcpyHostToDevice, gs));
+    SLIDE_CUDA(cudaMemcpyAsync(c->gy_ptr.p, gsl.ptrs + B + 1, (B + 1) * 4, cudaMemcpyHostToDevice, gs));
     if (nnz) {
       SLIDE_CUDA(cudaMemcpyAsync(c->gx_idx.p, bt->x_idx + x0, nnz * 4, cudaMemcpyDefault, gs));
       SLIDE_CUDA(cudaMemcpyAsync(c->gx_val.p, bt->x_val + x0, nnz * 4, cudaMemcpyDefault, gs));
     }
     if (nlab) SLIDE_CUDA(cudaMemcpyAsync(c->gy_idx.p, bt->y_idx + y0, nlab * 4, cudaMemcpyDefault, gs));
-    SLIDE_CUDA(cudaMemcpyAsync(c->iter_dev.p, c->pinned_iter, 8, cudaMemcpyHostToDevice, gs));
+    SLIDE_CUDA(cudaMemcpyAsync(c->iter_dev.p, gsl.iter, 8, cudaMemcpyHostToDevice, gs));
     slide_batch v{};
     v.batch = B;
     v.x_ptr = c->gx_ptr.as<int32_t>();
@@ -947,8 +982,8 @@ static void graph_step_launch(slide_ctx* c, const slide_batch* bt, int64_t itera
     v.x_val = c->gx_val.as<float>();
     v.y_ptr = c->gy_ptr.as<int32_t>();
     v.y_idx = c->gy_idx.as<int32_t>();
-    v.x_ptr_host = c->pinned_ptrs;
-    v.y_ptr_host = c->pinned_ptrs + B + 1;
+    v.x_ptr_host = gsl.ptrs;
+    v.y_ptr_host = gsl.ptrs + B + 1;
     c->s = gs;
     const bool timing = c->timer.on;
     c->st_active = true;
@@ -960,7 +995,10 @@ static void graph_step_launch(slide_ctx* c, const slide_batch* bt, int64_t itera
       // a buffer the graph points into moved (e.g. a table rebuild with more
       // bucket runs than before): one eager step re-sizes every buffer for
       // the new tables (a capture must not allocate), then capture again
-      if (c->graph_state == 2 && c->graph_gen != g_slide_realloc_gen) c->graph_state = 0;
+      if (c->graph_state == 2 && c->graph_gen != g_slide_realloc_gen) {
+        c->graph_state = 0;
+        ++c->host_counts[5];
+      }
       if (c->graph_state < 2) c->timer.on = c->graph_state == 0 && timing;
       if (c->graph_state == 0) {
         c->w1_prefork = true;
@@ -1022,35 +1060,37 @@ static void graph_step_launch(slide_ctx* c, const slide_batch* bt, int64_t itera
     c->s = user;
     c->timer.on = timing;
     c->st_active = false;
-    if (c->pinned_n < B) {
-      if (c->pinned_loss) cudaFreeHost(c->pinned_loss);
-      if (c->pinned_cnt) cudaFreeHost(c->pinned_cnt);
-      SLIDE_CUDA(cudaHostAlloc((void**)&c->pinned_loss, B * 8, cudaHostAllocDefault));
-      SLIDE_CUDA(cudaHostAlloc((void**)&c->pinned_cnt, B * 4, cudaHostAllocDefault));
-      c->pinned_n = B;
-    }
-    SLIDE_CUDA(cudaMemcpyAsync(c->pinned_loss, c->loss.p, B * 8, cudaMemcpyDeviceToHost, gs));
-    SLIDE_CUDA(cudaMemcpyAsync(c->pinned_cnt, c->cnt.p, B * 4, cudaMemcpyDeviceToHost, gs));
-    SLIDE_CUDA(cudaEventRecord(c->gev_out, gs));
-    SLIDE_CUDA(cudaStreamWaitEvent(user, c->gev_out, 0));
-    c->g_pending = B;
+    SLIDE_CUDA(cudaMemcpyAsync(gsl.loss, c->loss.p, B * 8, cudaMemcpyDeviceToHost, gs));
+    SLIDE_CUDA(cudaMemcpyAsync(gsl.cnt, c->cnt.p, B * 4, cudaMemcpyDeviceToHost, gs));
+    SLIDE_CUDA(cudaEventRecord(gsl.ev, gs));
+    SLIDE_CUDA(cudaStreamWaitEvent(user, gsl.ev, 0));
+    gsl.used = true;
+    c->g_q[c->g_qn] = slot;
+    c->g_qb[c->g_qn] = B;
+    ++c->g_qn;
+    c->g_next = slot ^ 1;
 }
 
+// results of the oldest graph step in flight
 static void graph_step_finish(slide_ctx* c, double* loss_host, int64_t* active_host) {
-  SLIDE_CHECK(c->g_pending > 0, kValueError, "no graph step in flight");
-  const int64_t B = c->g_pending;
-  c->g_pending = 0;
-  SLIDE_CUDA(cudaEventSynchronize(c->gev_out));
+  SLIDE_CHECK(c->g_qn > 0, kValueError, "no graph step in flight");
+  auto& gsl = c->gslot[c->g_q[0]];
+  const int64_t B = c->g_qb[0];
+  c->g_q[0] = c->g_q[1];
+  c->g_qb[0] = c->g_qb[1];
+  --c->g_qn;
+  SLIDE_CUDA(cudaEventSynchronize(gsl.ev));
   for (int64_t i = 0; i < B; ++i) {
-    if (loss_host) loss_host[i] = c->pinned_loss[i];
-    if (active_host) active_host[i] = c->pinned_cnt[i];
-    c->host_counts[0] += c->pinned_cnt[i];
+    if (loss_host) loss_host[i] = gsl.loss[i];
+    if (active_host) active_host[i] = gsl.cnt[i];
+    c->host_counts[0] += gsl.cnt[i];
   }
 }
 
 int slide_graph_step(slide_ctx* c, const slide_batch* bt, int64_t iteration, double* loss_host,
                      int64_t* active_host) {
   return guarded([&] {
+    SLIDE_CHECK(c->g_qn == 0, kValueError, "collect the asynchronous graph steps in flight first");
     graph_step_launch(c, bt, iteration);
     graph_step_finish(c, loss_host, active_host);
   });
@@ -1058,7 +1098,6 @@ int slide_graph_step(slide_ctx* c, const slide_batch* bt, int64_t iteration, dou
 
 int slide_graph_step_async(slide_ctx* c, const slide_batch* bt, int64_t iteration) {
   return guarded([&] {
-    SLIDE_CHECK(c->g_pending == 0, kValueError, "a graph step is already in flight");
     graph_step_launch(c, bt, iteration);
   });
 }

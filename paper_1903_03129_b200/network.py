@@ -528,11 +528,14 @@ class SlideNetwork:
 
     def train_batches_csr(self, batches, first_iteration: int = 1, schedule: str = "snapshot") -> list:
         """``train_batch_csr`` over consecutive batches (iterations
-        first_iteration, first_iteration + 1, ...), pipelined on the host:
-        while step k runs on the device (H2D, graph, D2H of its losses), the
-        host stages batch k+1 into the other pinned buffer set; then it waits
-        for step k's losses and runs the rebuild barrier before launching
-        k+1.  Same results as calling train_batch_csr per batch."""
+        first_iteration, first_iteration + 1, ...), pipelined: step k+1 (its
+        H2D copies, the graph, the D2H of its losses) is queued on the device
+        behind step k before the host waits for step k's losses, and the
+        host stages batch k+2 meanwhile.  The rebuild barrier that follows
+        step k is enqueued on the context stream between the two (the
+        schedule depends only on the iteration), so the results equal
+        train_batch_csr per batch; only the losses arrive one step late (no
+        divergence check between the two steps)."""
         batches = list(batches)
         if (schedule != "snapshot" or not self.use_graphs or self.shard_count > 1
                 or any(c.batch != self.cfg.batch_size for c in batches)):
@@ -543,20 +546,28 @@ class SlideNetwork:
         B = self.cfg.batch_size
         loss = np.empty(B, dtype=np.float64)
         active = np.empty(B, dtype=np.int64)
-        staged = self._pinned_batch(batches[0], 0)
-        for k, csr in enumerate(batches):
+        lsh = self.layers[1].lsh
+        keeps = {}
+
+        def launch(k):
+            # pinned set k % 2 was step k-2's, whose results were taken
+            bt, keep = self._pinned_batch(batches[k], k % 2)
+            keeps[k % 2] = keep
+            if lsh is not None:
+                lsh.sync_to_device()
+            _lib.call("slide_graph_step_async", self._ctx, _lib.C.byref(bt), first_iteration + k)
+            return self.h2d_bytes
+
+        h2d = launch(0)
+        for k in range(len(batches)):
             it = first_iteration + k
-            if self.layers[1].lsh is not None:
-                self.layers[1].lsh.sync_to_device()
-            bt, keep = staged
-            h2d = self.h2d_bytes
-            _lib.call("slide_graph_step_async", self._ctx, _lib.C.byref(bt), it)
-            if k + 1 < len(batches):  # overlaps the device step
-                staged = self._pinned_batch(batches[k + 1], (k + 1) % 2)
+            rebuilt = self._rebuild_after(it)  # stream-ordered after step k, before step k+1
+            h2d_next = launch(k + 1) if k + 1 < len(batches) else 0
             _lib.call("slide_graph_step_wait", self._ctx, loss.ctypes.data, active.ctypes.data)
+            out.append(self._stats(loss, active, rebuilt))
             self.h2d_bytes = h2d
-            out.append(self._barrier(it, loss, active))
-            self._live = keep
+            h2d = h2d_next
+        self._live = keeps
         return out
 
     #: snapshot steps replay one captured CUDA graph per batch shape
@@ -610,13 +621,20 @@ class SlideNetwork:
         return loss, active
 
     def _barrier(self, iteration, loss, active) -> BatchStats:
-        rebuilt = []
-        fractions = {}
+        return self._stats(loss, active, self._rebuild_after(iteration))
+
+    def _rebuild_after(self, iteration) -> list:
+        """The rebuild barrier after a batch (network.py:368-373): the layers
+        rebuilt (enqueued on the context stream)."""
         lsh = self.layers[1].lsh
-        if lsh is not None:
-            lsh.mark_weights_changed()
-            if lsh.maybe_rebuild(iteration):
-                rebuilt.append(1)
+        if lsh is None:
+            return []
+        lsh.mark_weights_changed()
+        return [1] if lsh.maybe_rebuild(iteration) else []
+
+    def _stats(self, loss, active, rebuilt) -> BatchStats:
+        fractions = {}
+        if self.layers[1].lsh is not None:
             fractions[1] = float(np.mean(active / self.n_out))
         return BatchStats(float(np.mean(loss)), fractions, rebuilt)
 

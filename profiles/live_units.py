@@ -17,7 +17,7 @@ corpus = synthetic_corpus(w.corpus, w.batch * n, seed=int(sys.argv[3]) if len(sy
 bs = bench.csr_batches(corpus, w.batch, n)
 for it, b in enumerate(bs, 1):
     st = net.train_batch_csr(b, it, schedule="snapshot")
-    if it in (1, 2, 5, 10, 20, 30, 40, 50, 60):
+    if it in (1, 2, 5, 10, 20, 30, 40, 50, 60) or it % 10 == 0:
         h = net._read(0, w.batch * net.hidden_pad if hasattr(net, "hidden_pad") else w.batch * 128, np.float32).reshape(w.batch, -1)
         nz = h > 0
         C = nz.any(0).sum()
