@@ -332,11 +332,23 @@ def run_ours(args, rank, world):
     peak, peak_kind = peaks()
     achieved = sb[dom] / (stage_ms[dom] / 1e3) / 1e9
     traffic = None
+    issue = None
     try:  # dram bytes per launch from the committed `ncu --set full` capture of that kernel
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             tr = json.load(fh).get(w.name, {}).get(dom)
         if tr:
             traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+            inst = tr.get("warp_instructions")
+            if inst:
+                # the kernel is issue-bound, not HBM-bound: its instruction
+                # count (same capture) over its event time against 4 warp
+                # instructions per SM cycle at the sampled clock
+                sm_hz = (clk.summary().get("sm_mhz") or 1965) * 1e6
+                peak_i = 148 * 4 * sm_hz / 1e9
+                got_i = inst / (stage_ms[dom] / 1e3) / 1e9
+                issue = {"bound": "issue", "warp_instructions_per_launch": inst, "achieved": got_i,
+                         "peak": peak_i, "unit": "G warp-inst/s", "frac": got_i / peak_i,
+                         "source": tr.get("source")}
     except Exception:
         traffic = None
     ms_per_step = total_ms / K
@@ -355,7 +367,7 @@ def run_ours(args, rank, world):
                    "parallelism": f"output layer column-sharded x{world} (NCCL all-reduces)" if world > 1 else "1 GPU",
                    "l2": "flushed between steps (256 MiB write, outside the events)"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind, "issue": issue,
                      "algorithmic_bytes_per_launch": sb[dom], "ms_per_launch": stage_ms[dom]},
         "step_roofline": {"bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (ms_per_step / 1e3) / 1e9,
                           "frac": step_bytes / (ms_per_step / 1e3) / 1e9 / peak},
@@ -395,9 +407,97 @@ def cpu_port_rate(w, n_samples, threads=1):
     return n_samples / dt, dt
 
 
+_REF = {}
+
+
+def _ref_slot(task):
+    """One slot's forward + backward on the pre-step state (a forked worker;
+    the state arrays are shared memory, so it sees the parent's updates;
+    the slot's input comes with the task)."""
+    from oracle import slide_oracle as O
+
+    r = _REF
+    i, it, (xi, xv, y) = task
+    rng = np.random.default_rng((0, it, i))
+    tr = O.slot_forward(r["st"], r["lsh"], xi, xv, y, rng, r["n_out"])
+    return O.slot_backward(r["st"], tr, y), tr.loss
+
+
+def _ref_update(p):
+    """Worker p of P applies every slot's Adam updates (slot order) to its
+    share of the rows: output rows with id % P == p, input features with
+    id % P == p.  Rows are independent in the reference's update
+    (network.py:428-451: per-row step counters, per-row moments), so the
+    partition reproduces the serial result; the hidden units' step counters
+    advance identically in every worker, and worker 0 alone writes the
+    hidden biases and counters."""
+    from oracle import slide_oracle as O
+
+    r = _REF
+    st, cfg, P = r["st"], r["cfg"], r["P"]
+    w1, m1, v1 = st.w1t.T, st.m1t.T, st.v1t.T
+    steps1 = st.steps1.copy()  # local hidden-unit counters (worker 0's are written back)
+    b1 = st.b1 if p == 0 else st.b1.copy()
+    mb1 = st.mb1 if p == 0 else st.mb1.copy()
+    vb1 = st.vb1 if p == 0 else st.vb1.copy()
+    for g in r["grads"]:
+        sel = g.active % P == p
+        rows, d = g.active[sel], g.delta[sel]
+        if g.h_idx.size == 0:
+            O._adam_rows(st.w2, st.m2, st.v2, st.b2, st.mb2, st.vb2, st.steps2, rows, None, None, d, cfg)
+            continue
+        O._adam_rows(st.w2, st.m2, st.v2, st.b2, st.mb2, st.vb2, st.steps2, rows, g.h_idx,
+                     np.outer(d, g.h_val), d, cfg)
+        fs = g.x_idx % P == p
+        cols = g.x_idx[fs]
+        O._adam_rows(w1, m1, v1, b1, mb1, vb1, steps1, g.h_idx, cols if cols.size else None,
+                     np.outer(g.dh, g.x_val[fs]) if cols.size else None, g.dh, cfg)
+    if p == 0:
+        st.steps1[:] = steps1
+    return p
+
+
+def reference_parallel_step(st, lsh, batch, it, cfg, cores, pool, ctx):
+    """One snapshot step of the reference path on `cores` processes: the
+    slots' forward/backward in `pool` (forked with _REF["st"] / ["lsh"] /
+    ["n_out"] set), the row-partitioned updates in fresh workers, then the
+    rebuild barrier (True when the tables were rebuilt: re-fork `pool`)."""
+    res = pool.map(_ref_slot, [(i, it, x) for i, x in enumerate(batch)], chunksize=1)
+    _REF.update(grads=[g for g, _ in res], cfg=cfg, P=cores)
+    with ctx.Pool(cores) as up:
+        up.map(_ref_update, range(cores), chunksize=1)
+    if lsh is not None and lsh.schedule.due(it):
+        lsh.build(st.w2)
+        lsh.schedule.advance()
+        return True
+    return False
+
+
+def _shared_state(st):
+    """The NetState's arrays moved into anonymous shared memory (fork-inherited)."""
+    import dataclasses
+    import mmap
+
+    out = {}
+    for f in dataclasses.fields(st):
+        a = getattr(st, f.name)
+        if isinstance(a, np.ndarray) and a.size:
+            buf = mmap.mmap(-1, a.nbytes)
+            b = np.frombuffer(buf, dtype=a.dtype).reshape(a.shape)
+            b[...] = a
+            out[f.name] = b
+    return dataclasses.replace(st, **out)
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the reference algorithm's CPU path (oracle port),
-    K bounded steps on rank 0."""
+    """--impl reference: the reference algorithm's CPU path (oracle port), K
+    bounded steps on rank 0 with every host core: the reference's HOGWILD
+    batch (workers = cpu_count, network.py:340-379) in its deterministic
+    snapshot member -- the slots' forward/backward run in parallel worker
+    processes on the pre-step weights, the Adam updates are applied in slot
+    order."""
+    import multiprocessing as mp
+
     from threadpoolctl import threadpool_limits
 
     from oracle import slide_oracle as O
@@ -405,30 +505,49 @@ def run_reference(args, rank, world):
     from paper_1903_03129_b200.data import synthetic_corpus
 
     w = WORKLOADS[args.workload]
-    per_step = max(1, min(w.batch, 4))
+    cores = os.cpu_count() or 1
+    per_step = max(1, min(w.batch, 4 * cores))
     with threadpool_limits(1):
-        st = O.init_state(w.input_dim, w.hidden, w.n_out, seed=0)
+        st = _shared_state(O.init_state(w.input_dim, w.hidden, w.n_out, seed=0))
         spec = O.LshSpec(w.family, w.k, w.l, w.cap, w.policy, bin_size=w.bin_size, strategy=w.strategy, beta=w.beta)
         lsh = O.OutputLsh(spec, w.hidden, 0, w.n0, w.decay)
         lsh.build(st.w2)
         corpus = synthetic_corpus(w.corpus, (args.warmup + args.steps) * per_step, seed=1000)
         trip = corpus.triples()
-        for it in range(1, args.warmup + 1):
-            O.train_step(st, lsh, trip[(it - 1) * per_step : it * per_step], it, 0, w.n_out, O.AdamCfg(lr=w.lr))
-        t0 = time.perf_counter()
-        for it in range(args.warmup + 1, args.warmup + args.steps + 1):
-            O.train_step(st, lsh, trip[(it - 1) * per_step : it * per_step], it, 0, w.n_out, O.AdamCfg(lr=w.lr))
-        dt = time.perf_counter() - t0
+        _REF.update(st=st, lsh=lsh, n_out=w.n_out)
+        cfg = O.AdamCfg(lr=w.lr)
+        ctx = mp.get_context("fork")
+        pool = None
+
+        def step(it):
+            nonlocal pool
+            batch = trip[(it - 1) * per_step : it * per_step]
+            if pool is None:  # forked after the tables exist (rebuilds re-fork)
+                pool = ctx.Pool(cores)
+            if reference_parallel_step(st, lsh, batch, it, cfg, cores, pool, ctx):
+                pool.close()
+                pool = None
+
+        try:
+            for it in range(1, args.warmup + 1):
+                step(it)
+            t0 = time.perf_counter()
+            for it in range(args.warmup + 1, args.warmup + args.steps + 1):
+                step(it)
+            dt = time.perf_counter() - t0
+        finally:
+            if pool is not None:
+                pool.close()
     v = args.steps * per_step / dt
+    sample = f"{args.steps} steps x {per_step} samples of {w.name}, rebuild not reached"
     return {
         "impl": "reference", "metric": "train samples/sec (LSH-sparse fwd+bwd+Adam), % of HBM roofline, 1/2/4/8 GPU",
         "value": v, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (SURVEY 8(d) Zipf generator)",
-        "config": {"workload": w.name, "batch": w.batch, "schedule": "sequential (reference workers=1)",
+        "config": {"workload": w.name, "batch": w.batch, "schedule": f"snapshot (reference workers={cores})",
                    "sample": f"{per_step} samples per step (bounded)"},
-        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": 1, "kind": "port",
-                         "sample": f"{args.steps} steps x {per_step} samples of {w.name}, rebuild not reached"},
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 

@@ -143,3 +143,40 @@ def test_host_sampler_helper_matches_golden(golden):
         n = g["lens"][case]
         np.testing.assert_array_equal(np.sort(rep.active_ids), g["ids"][off : off + n])
         off += n
+
+
+def test_reference_arm_parallel_step_equals_serial_snapshot():
+    """bench.py --impl reference runs the reference path on every host core
+    (slots' forward/backward in worker processes, the Adam updates
+    partitioned by row); its state after two steps equals the serial
+    snapshot oracle bit for bit."""
+    import multiprocessing as mp
+
+    import bench
+    from oracle import slide_oracle as O
+    from paper_1903_03129_b200.data import CorpusSpec, synthetic_corpus
+
+    D, H, N = 300, 16, 120
+    spec = CorpusSpec(D, N, ("uniform", 3, 12), 1.1, ("uniform", 1, 3), 1.1, True)
+    trip = synthetic_corpus(spec, 24, seed=5).triples()
+    lspec = O.LshSpec("simhash", 3, 6, 8, "fifo", strategy="vanilla", beta=20)
+    cfg = O.AdamCfg(lr=1e-2)
+
+    def fresh():
+        st = O.init_state(D, H, N, seed=3)
+        lsh = O.OutputLsh(lspec, H, 0, 50, 0.0)
+        lsh.build(st.w2)
+        return st, lsh
+
+    want, lw = fresh()
+    for it in (1, 2):
+        O.train_step(want, lw, trip[(it - 1) * 12 : it * 12], it, 0, N, cfg, mode="snapshot")
+    st, lsh = fresh()
+    st = bench._shared_state(st)
+    bench._REF.update(st=st, lsh=lsh, n_out=N)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(3) as pool:
+        for it in (1, 2):
+            bench.reference_parallel_step(st, lsh, trip[(it - 1) * 12 : it * 12], it, cfg, 3, pool, ctx)
+    for name in ("w1t", "m1t", "v1t", "b1", "mb1", "vb1", "steps1", "w2", "m2", "v2", "b2", "mb2", "vb2", "steps2"):
+        np.testing.assert_array_equal(getattr(st, name), getattr(want, name), err_msg=name)
