@@ -518,6 +518,7 @@ def run_reference(args, rank, world):
         cfg = O.AdamCfg(lr=w.lr)
         ctx = mp.get_context("fork")
         pool = None
+        rebuilds = [0]
 
         def step(it):
             nonlocal pool
@@ -527,6 +528,7 @@ def run_reference(args, rank, world):
             if reference_parallel_step(st, lsh, batch, it, cfg, cores, pool, ctx):
                 pool.close()
                 pool = None
+                rebuilds[0] += it > args.warmup
 
         try:
             for it in range(1, args.warmup + 1):
@@ -539,7 +541,8 @@ def run_reference(args, rank, world):
             if pool is not None:
                 pool.close()
     v = args.steps * per_step / dt
-    sample = f"{args.steps} steps x {per_step} samples of {w.name}, rebuild not reached"
+    sample = (f"{args.steps} steps x {per_step} samples of {w.name}, {rebuilds[0]} table rebuild(s) "
+              f"(numpy, serial) in the timed steps")
     return {
         "impl": "reference", "metric": "train samples/sec (LSH-sparse fwd+bwd+Adam), % of HBM roofline, 1/2/4/8 GPU",
         "value": v, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
