@@ -436,7 +436,7 @@ def _ref_update(p):
     r = _REF
     st, cfg, P = r["st"], r["cfg"], r["P"]
     w1, m1, v1 = st.w1t.T, st.m1t.T, st.v1t.T
-    steps1 = st.steps1.copy()  # local hidden-unit counters (worker 0's are written back)
+    steps1 = r["steps1"].copy()  # pre-step hidden-unit counters (worker 0's are written back)
     b1 = st.b1 if p == 0 else st.b1.copy()
     mb1 = st.mb1 if p == 0 else st.mb1.copy()
     vb1 = st.vb1 if p == 0 else st.vb1.copy()
@@ -463,7 +463,9 @@ def reference_parallel_step(st, lsh, batch, it, cfg, cores, pool, ctx):
     ["n_out"] set), the row-partitioned updates in fresh workers, then the
     rebuild barrier (True when the tables were rebuilt: re-fork `pool`)."""
     res = pool.map(_ref_slot, [(i, it, x) for i, x in enumerate(batch)], chunksize=1)
-    _REF.update(grads=[g for g, _ in res], cfg=cfg, P=cores)
+    # the hidden counters are snapshotted before any update worker runs: worker
+    # 0 writes st.steps1 back when it finishes, possibly before another starts
+    _REF.update(grads=[g for g, _ in res], cfg=cfg, P=cores, steps1=st.steps1.copy())
     with ctx.Pool(cores) as up:
         up.map(_ref_update, range(cores), chunksize=1)
     if lsh is not None and lsh.schedule.due(it):
