@@ -100,16 +100,24 @@ struct slide_ctx {
   // staging (rebased x_ptr | y_ptr, iteration) and result slots and an
   // event after its last copy; a slot is reused two launches later, after
   // its results were taken.
+  // Inputs are staged per slot on the copy stream (pinned header H2D, host
+  // arrays H2D into gin) while the previous step runs; one copy-in kernel on
+  // the graph stream moves them into the graph's buffers.  Results are
+  // packed per slot (gout) on the graph stream and read back on the copy
+  // stream beside the next step.
   struct GSlot {
-    int32_t* ptrs = nullptr;
+    int32_t* ptrs = nullptr;  // pinned header: x_ptr | y_ptr (rebased), then the iteration (int64)
     int64_t ptrs_n = 0;
-    int64_t* iter = nullptr;
-    double* loss = nullptr;
+    int64_t* iter = nullptr;  // inside the header
+    double* loss = nullptr;   // pinned results: loss (B doubles) | cnt (B int32)
     int32_t* cnt = nullptr;
     int64_t res_n = 0;
-    cudaEvent_t ev = nullptr;
+    DBuf gin, gout;
+    cudaEvent_t ev = nullptr;  // results in pinned memory (copy stream)
+    cudaEvent_t ev_staged = nullptr, ev_consumed = nullptr, ev_dev = nullptr;
     bool used = false;
   } gslot[2];
+  cudaStream_t cstream = nullptr;
   int g_next = 0;      // slot of the next launch
   int g_q[2] = {0, 0};  // pending slots, oldest first
   int64_t g_qb[2] = {0, 0};
@@ -318,15 +326,18 @@ int slide_destroy(slide_ctx* c) {
     if (c->graph) cudaGraphDestroy(c->graph);
     for (DBuf* b : {&c->iter_dev, &c->gx_ptr, &c->gx_idx, &c->gx_val, &c->gy_ptr, &c->gy_idx}) b->release();
     if (c->gstream) cudaStreamSynchronize(c->gstream);
+    if (c->cstream) cudaStreamSynchronize(c->cstream);
     for (auto& g : c->gslot) {
       if (g.ptrs) cudaFreeHost(g.ptrs);
-      if (g.iter) cudaFreeHost(g.iter);
       if (g.loss) cudaFreeHost(g.loss);
-      if (g.cnt) cudaFreeHost(g.cnt);
-      if (g.ev) cudaEventDestroy(g.ev);
+      for (cudaEvent_t e : {g.ev, g.ev_staged, g.ev_consumed, g.ev_dev})
+        if (e) cudaEventDestroy(e);
+      g.gin.release();
+      g.gout.release();
     }
     if (c->gev_in) cudaEventDestroy(c->gev_in);
     if (c->gstream) cudaStreamDestroy(c->gstream);
+    if (c->cstream) cudaStreamDestroy(c->cstream);
     if (c->pinned_loss) cudaFreeHost(c->pinned_loss);
     if (c->pinned_cnt) cudaFreeHost(c->pinned_cnt);
     for (cudaEvent_t e : c->timer.pool) cudaEventDestroy(e);
@@ -898,6 +909,40 @@ int slide_train_batch(slide_ctx* c, const slide_batch* bt, int64_t iteration, in
   });
 }
 
+// Word copies of up to 8 segments in one launch (graph-step staging in and
+// results out).
+struct CopyIn {
+  uint32_t* dst[8];
+  const uint32_t* src[8];
+  int64_t words[8];
+  int n = 0;
+  void add(void* d, const void* s, int64_t w) {
+    if (w <= 0) return;
+    dst[n] = static_cast<uint32_t*>(d);
+    src[n] = static_cast<const uint32_t*>(s);
+    words[n] = w;
+    ++n;
+  }
+};
+
+__global__ void copy_in_kernel(CopyIn a) {
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  for (int k = 0; k < a.n; ++k) {
+    uint32_t* __restrict__ d = a.dst[k];
+    const uint32_t* __restrict__ s = a.src[k];
+    for (int64_t q = t0; q < a.words[k]; q += nt) d[q] = __ldcs(s + q);
+  }
+}
+
+static void launch_copy_in(const CopyIn& a, cudaStream_t s) {
+  if (a.n == 0) return;
+  int64_t w = 0;
+  for (int k = 0; k < a.n; ++k) w = std::max(w, a.words[k]);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(w, 256 * 2), kSms * 4));
+  copy_in_kernel<<<grid, 256, 0, s>>>(a);
+  SLIDE_LAUNCH_CHECK();
+}
+
 // One snapshot step as a CUDA graph (see header).  The first call with new
 // shapes runs eagerly (and sizes every buffer), the second captures, the
 // rest replay: no host work between the kernels, one sync per step.
@@ -916,10 +961,10 @@ static void graph_step_launch(slide_ctx* c, const slide_batch* bt, int64_t itera
     if (!c->gstream) {
       SLIDE_CUDA(cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
       SLIDE_CUDA(cudaEventCreateWithFlags(&c->gev_in, cudaEventDisableTiming));
-      for (auto& g : c->gslot) {
-        SLIDE_CUDA(cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming));
-        SLIDE_CUDA(cudaHostAlloc((void**)&g.iter, 8, cudaHostAllocDefault));
-      }
+      SLIDE_CUDA(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+      for (auto& g : c->gslot)
+        for (cudaEvent_t* e : {&g.ev, &g.ev_staged, &g.ev_consumed, &g.ev_dev})
+          SLIDE_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
     const int slot = c->g_next;
     auto& gsl = c->gslot[slot];
@@ -945,36 +990,64 @@ static void graph_step_launch(slide_ctx* c, const slide_batch* bt, int64_t itera
       c->iter_dev.ensure<int64_t>(1);
       c->graph_state = 0;
     }
-    if (gsl.ptrs_n < 2 * (B + 1)) {
+    const int64_t pw = (2 * (B + 1) + 1) & ~(int64_t)1;  // header words before the iteration (8-aligned)
+    if (gsl.ptrs_n < pw + 2) {
       if (gsl.ptrs) cudaFreeHost(gsl.ptrs);
-      SLIDE_CUDA(cudaHostAlloc((void**)&gsl.ptrs, 2 * (B + 1) * 4, cudaHostAllocDefault));
-      gsl.ptrs_n = 2 * (B + 1);
+      SLIDE_CUDA(cudaHostAlloc((void**)&gsl.ptrs, (pw + 2) * 4, cudaHostAllocDefault));
+      gsl.ptrs_n = pw + 2;
     }
+    gsl.iter = reinterpret_cast<int64_t*>(gsl.ptrs + pw);
     if (gsl.res_n < B) {
       if (gsl.loss) cudaFreeHost(gsl.loss);
-      if (gsl.cnt) cudaFreeHost(gsl.cnt);
-      SLIDE_CUDA(cudaHostAlloc((void**)&gsl.loss, B * 8, cudaHostAllocDefault));
-      SLIDE_CUDA(cudaHostAlloc((void**)&gsl.cnt, B * 4, cudaHostAllocDefault));
+      SLIDE_CUDA(cudaHostAlloc((void**)&gsl.loss, B * 12, cudaHostAllocDefault));
       gsl.res_n = B;
     }
-    cudaStream_t user = c->s, gs = c->gstream;
+    gsl.cnt = reinterpret_cast<int32_t*>(gsl.loss + B);
+    // per-slot device staging: header | x_idx | x_val | y_idx at the capacities
+    const int64_t o_xi = (pw + 2) * 4, o_xv = o_xi + st.nnz_cap * 4, o_yi = o_xv + st.nnz_cap * 4;
+    char* gin = gsl.gin.ensure<char>(o_yi + st.ylab_cap * 4);
+    char* gout = gsl.gout.ensure<char>(B * 12);
+    cudaStream_t user = c->s, gs = c->gstream, cs = c->cstream;
     // eager runs and captures read host-side sizes: nothing may be in flight
     if (c->graph_state < 2 || c->graph_gen != g_slide_realloc_gen) SLIDE_CUDA(cudaStreamSynchronize(gs));
-    SLIDE_CUDA(cudaEventRecord(c->gev_in, user));
-    SLIDE_CUDA(cudaStreamWaitEvent(gs, c->gev_in, 0));
     for (int64_t i = 0; i <= B; ++i) {
       gsl.ptrs[i] = (int32_t)(bt->x_ptr_host[i] - x0);
       gsl.ptrs[B + 1 + i] = (int32_t)(bt->y_ptr_host[i] - y0);
     }
     *gsl.iter = iteration;
-    SLIDE_CUDA(cudaMemcpyAsync(c->gx_ptr.p, gsl.ptrs, (B + 1) * 4, cudaMemcpyHostToDevice, gs));
-    SLIDE_CUDA(cudaMemcpyAsync(c->gy_ptr.p, gsl.ptrs + B + 1, (B + 1) * 4, cudaMemcpyHostToDevice, gs));
-    if (nnz) {
-      SLIDE_CUDA(cudaMemcpyAsync(c->gx_idx.p, bt->x_idx + x0, nnz * 4, cudaMemcpyDefault, gs));
-      SLIDE_CUDA(cudaMemcpyAsync(c->gx_val.p, bt->x_val + x0, nnz * 4, cudaMemcpyDefault, gs));
+    // staging on the copy stream, beside the step in flight: the copy-in two
+    // steps back has read this slot's staging; host arrays are ready by
+    // program order (device arrays are read by the copy-in kernel itself,
+    // after the caller's stream)
+    const void* probe = nnz ? (const void*)bt->x_idx : (const void*)bt->y_idx;
+    cudaPointerAttributes pa{};
+    const bool dev_src = (nnz || nlab) && cudaPointerGetAttributes(&pa, probe) == cudaSuccess &&
+                         (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged);
+    cudaGetLastError();  // unregistered host memory reports an error on some drivers
+    if (gsl.used) SLIDE_CUDA(cudaStreamWaitEvent(cs, gsl.ev_consumed, 0));
+    SLIDE_CUDA(cudaMemcpyAsync(gin, gsl.ptrs, (pw + 2) * 4, cudaMemcpyHostToDevice, cs));
+    if (!dev_src) {
+      if (nnz) {
+        SLIDE_CUDA(cudaMemcpyAsync(gin + o_xi, bt->x_idx + x0, nnz * 4, cudaMemcpyDefault, cs));
+        SLIDE_CUDA(cudaMemcpyAsync(gin + o_xv, bt->x_val + x0, nnz * 4, cudaMemcpyDefault, cs));
+      }
+      if (nlab) SLIDE_CUDA(cudaMemcpyAsync(gin + o_yi, bt->y_idx + y0, nlab * 4, cudaMemcpyDefault, cs));
     }
-    if (nlab) SLIDE_CUDA(cudaMemcpyAsync(c->gy_idx.p, bt->y_idx + y0, nlab * 4, cudaMemcpyDefault, gs));
-    SLIDE_CUDA(cudaMemcpyAsync(c->iter_dev.p, gsl.iter, 8, cudaMemcpyHostToDevice, gs));
+    SLIDE_CUDA(cudaEventRecord(gsl.ev_staged, cs));
+    SLIDE_CUDA(cudaEventRecord(c->gev_in, user));
+    SLIDE_CUDA(cudaStreamWaitEvent(gs, c->gev_in, 0));
+    SLIDE_CUDA(cudaStreamWaitEvent(gs, gsl.ev_staged, 0));
+    {
+      CopyIn ci{};
+      ci.add(c->gx_ptr.p, gin, B + 1);
+      ci.add(c->gy_ptr.p, gin + (B + 1) * 4, B + 1);
+      ci.add(c->iter_dev.p, gin + pw * 4, 2);
+      ci.add(c->gx_idx.p, dev_src ? (const void*)(bt->x_idx + x0) : gin + o_xi, nnz);
+      ci.add(c->gx_val.p, dev_src ? (const void*)(bt->x_val + x0) : gin + o_xv, nnz);
+      ci.add(c->gy_idx.p, dev_src ? (const void*)(bt->y_idx + y0) : gin + o_yi, nlab);
+      launch_copy_in(ci, gs);
+    }
+    SLIDE_CUDA(cudaEventRecord(gsl.ev_consumed, gs));
     slide_batch v{};
     v.batch = B;
     v.x_ptr = c->gx_ptr.as<int32_t>();
@@ -1060,10 +1133,20 @@ static void graph_step_launch(slide_ctx* c, const slide_batch* bt, int64_t itera
     c->s = user;
     c->timer.on = timing;
     c->st_active = false;
-    SLIDE_CUDA(cudaMemcpyAsync(gsl.loss, c->loss.p, B * 8, cudaMemcpyDeviceToHost, gs));
-    SLIDE_CUDA(cudaMemcpyAsync(gsl.cnt, c->cnt.p, B * 4, cudaMemcpyDeviceToHost, gs));
-    SLIDE_CUDA(cudaEventRecord(gsl.ev, gs));
-    SLIDE_CUDA(cudaStreamWaitEvent(user, gsl.ev, 0));
+    // results: packed into the slot's device buffer on the graph stream, read
+    // back on the copy stream (beside the next step); the caller's stream
+    // continues after the device work
+    {
+      CopyIn co{};
+      co.add(gout, c->loss.p, 2 * B);
+      co.add(gout + B * 8, c->cnt.p, B);
+      launch_copy_in(co, gs);
+    }
+    SLIDE_CUDA(cudaEventRecord(gsl.ev_dev, gs));
+    SLIDE_CUDA(cudaStreamWaitEvent(cs, gsl.ev_dev, 0));
+    SLIDE_CUDA(cudaMemcpyAsync(gsl.loss, gout, B * 12, cudaMemcpyDeviceToHost, cs));
+    SLIDE_CUDA(cudaEventRecord(gsl.ev, cs));
+    SLIDE_CUDA(cudaStreamWaitEvent(user, gsl.ev_dev, 0));
     gsl.used = true;
     c->g_q[c->g_qn] = slot;
     c->g_qb[c->g_qn] = B;
