@@ -518,8 +518,13 @@ int slide_query_union(slide_ctx* c, const float* q, int64_t n, int64_t n_ids, in
 // --------------------------------------------------------------------- step
 static void side_stream_init(slide_ctx* c) {
   if (c->s2) return;
-  SLIDE_CUDA(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
-  SLIDE_CUDA(cudaStreamCreateWithFlags(&c->s3, cudaStreamNonBlocking));
+  // the side branches (W1 grouping / Adam, per-row logits, long chains) at
+  // the highest priority: their CTAs go first when the persistent W2 Adam
+  // frees a slot, so the shorter W1 branch is not starved behind it
+  int lo = 0, hi = 0;
+  SLIDE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  SLIDE_CUDA(cudaStreamCreateWithPriority(&c->s2, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
+  SLIDE_CUDA(cudaStreamCreateWithPriority(&c->s3, cudaStreamNonBlocking, hi));
   for (cudaEvent_t* e : {&c->ev_fork, &c->ev_dh, &c->ev_join, &c->ev_pre, &c->ev_lg, &c->ev_lg_join, &c->ev_w1l})
     SLIDE_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
 }

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Sparse forward / backward / Adam kernels (reference network.py:241-336,
 // 428-451).  Row layout: every weight row (a W1^T feature row, a W2 output
 // row) is hp floats, hp a multiple of 128, so one warp moves a row with one
@@ -1004,7 +1005,12 @@ void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq
   if (max_uniq <= 0) return;
   if (!work_zeroed) SLIDE_CUDA(cudaMemsetAsync(work, 0, 4, s));
   // persistent: as many CTAs as are resident at once
-  const int per_sm = hp <= 128 ? 4 : 2;
+  static const int env_per_sm = [] {
+    const char* e = getenv("SLIDE_ADAM_ROWS_PER_SM");  // experiments only
+    return e ? atoi(e) : 0;
+  }();
+  // one CTA slot per SM stays free for the W1 branch running beside it
+  const int per_sm = env_per_sm > 0 ? env_per_sm : (hp <= 128 ? 3 : 2);
   const int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * per_sm);
   AdamRowsArgs A{hp, ap, n_uniq, uniq, seg_off, seg_cnt, sslot, dsort, h, live,
                  w2, m2, v2, b2, mb2, vb2, steps2, touched, work};
@@ -1284,13 +1290,13 @@ void launch_adam_features(int hp, const AdamParams& ap, const int32_t* n_uniq, i
   int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * 16);
   AdamFeatArgs A{hp, ap, n_uniq, uniq, seg_off, seg_cnt, sorted_k, x_slot, x_val, x_base, h, dh, bc, live,
                  w1t, m1t, v1t, touched, long_list, n_long};
-  SLIDE_NV_DISPATCH(hp, (adam_features_kernel<NV><<<grid, 256, 0, s>>>(A)));
-  SLIDE_LAUNCH_CHECK();
-  // long chains (on s_long, beside the short ones): at most
-  // max_uniq / (kW1LongChain + 1) of them
+  // long chains first (on s_long, beside the short ones; they are the
+  // branch's tail): at most max_uniq / (kW1LongChain + 1) of them
   const int64_t max_long = std::min<int64_t>(max_uniq, ceil_div(max_uniq, kW1LongChain)) * (hp / 32);
   const int lgrid = (int)std::min<int64_t>(std::max<int64_t>(max_long, 1), (int64_t)kSms * 16);
   adam_features_long_kernel<<<lgrid, kLongWarps * 32, 0, s_long>>>(A);
+  SLIDE_LAUNCH_CHECK();
+  SLIDE_NV_DISPATCH(hp, (adam_features_kernel<NV><<<grid, 256, 0, s>>>(A)));
   SLIDE_LAUNCH_CHECK();
 }
 
