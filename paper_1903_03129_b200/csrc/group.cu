@@ -33,12 +33,16 @@ __device__ __forceinline__ int64_t dev_count(const int32_t* n_dev, int64_t n_hos
 // inclusive prefix); the kernel before each scan zeroes status and counter.
 constexpr int kGT = 256;  // threads (= items) per tile
 
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// The status word carries its value itself (flag and prefix in one aligned
+// 64-bit word), so relaxed gpu-scope accesses suffice: no other data is
+// published through it.  (ld.acquire compiles to an L1 invalidation per
+// load -- CCTL.IVALL -- which dominated the scan's stall samples.)
+__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -47,14 +51,14 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 __device__ __forceinline__ int tile_lookback(int tile, int agg, unsigned long long* status) {
   const int lane = threadIdx.x & 31;
   if (tile == 0) {
-    if (lane == 0) st_release(status, (2ull << 32) | (uint32_t)agg);
+    if (lane == 0) st_status(status, (2ull << 32) | (uint32_t)agg);
     return 0;
   }
-  if (lane == 0) st_release(status + tile, (1ull << 32) | (uint32_t)agg);
+  if (lane == 0) st_status(status + tile, (1ull << 32) | (uint32_t)agg);
   int acc = 0;
   for (int top = tile - 1;;) {
     const int idx = top - lane;
-    const unsigned long long v = idx >= 0 ? ld_acquire(status + idx) : (2ull << 32);
+    const unsigned long long v = idx >= 0 ? ld_status(status + idx) : (2ull << 32);
     const uint32_t flag = (uint32_t)(v >> 32);
     const unsigned inc = __ballot_sync(0xffffffffu, flag == 2), none = __ballot_sync(0xffffffffu, flag == 0);
     const unsigned need = inc ? (inc & (0u - inc)) * 2u - 1u : 0xffffffffu;  // lanes up to the closest prefix
@@ -66,7 +70,7 @@ __device__ __forceinline__ int tile_lookback(int tile, int agg, unsigned long lo
     if (inc) break;
     top -= 32;
   }
-  if (lane == 0) st_release(status + tile, (2ull << 32) | (uint32_t)(acc + agg));
+  if (lane == 0) st_status(status + tile, (2ull << 32) | (uint32_t)(acc + agg));
   return acc;
 }
 
@@ -218,14 +222,14 @@ __device__ __forceinline__ unsigned long long tile_lookback2(int tile, unsigned 
   // bit 63 set (inclusive); 0 = not yet published
   constexpr unsigned long long kInc = 1ull << 63;
   if (tile == 0) {
-    if (lane == 0) st_release(status, kInc | (agg + 1));
+    if (lane == 0) st_status(status, kInc | (agg + 1));
     return 0;
   }
-  if (lane == 0) st_release(status + tile, agg + 1);
+  if (lane == 0) st_status(status + tile, agg + 1);
   unsigned long long acc = 0;
   for (int top = tile - 1;;) {
     const int idx = top - lane;
-    const unsigned long long v = idx >= 0 ? ld_acquire(status + idx) : (kInc | 1ull);
+    const unsigned long long v = idx >= 0 ? ld_status(status + idx) : (kInc | 1ull);
     const unsigned inc = __ballot_sync(0xffffffffu, (v & kInc) != 0), none = __ballot_sync(0xffffffffu, v == 0);
     const unsigned need = inc ? (inc & (0u - inc)) * 2u - 1u : 0xffffffffu;
     if (none & need) continue;
@@ -236,10 +240,97 @@ __device__ __forceinline__ unsigned long long tile_lookback2(int tile, unsigned 
     if (inc) break;
     top -= 32;
   }
-  if (lane == 0) st_release(status + tile, kInc | (acc + agg + 1));
+  if (lane == 0) st_status(status + tile, kInc | (acc + agg + 1));
   return acc;
 }
 
+// Block-wide look-back for the two-value scan: every thread of the tile
+// reads one predecessor's status (kGT per round instead of 32), so a tile
+// whose predecessors have only published aggregates resolves in one round
+// trip instead of one per 32 tiles.  Called by all threads; returns the
+// exclusive prefix.
+__device__ __forceinline__ unsigned long long tile_lookback2_block(int tile, unsigned long long agg,
+                                                                   unsigned long long* status) {
+  using Red = cub::BlockReduce<unsigned long long, kGT>;
+  __shared__ typename Red::TempStorage red;
+  __shared__ int s_lim;
+  __shared__ unsigned long long s_acc;
+  constexpr unsigned long long kInc = 1ull << 63;
+  if (tile == 0) {
+    if (threadIdx.x == 0) st_status(status, kInc | (agg + 1));
+    return 0;
+  }
+  if (threadIdx.x == 0) {
+    st_status(status + tile, agg + 1);
+    s_acc = 0;
+  }
+  unsigned long long acc = 0;
+  for (int top = tile - 1;; top -= kGT) {
+    if (threadIdx.x == 0) s_lim = top - kGT;  // no inclusive prefix in this window yet
+    __syncthreads();
+    const int idx = top - (int)threadIdx.x;
+    unsigned long long v = 0;
+    if (idx >= 0) {
+      do v = ld_status(status + idx);
+      while (v == 0);
+      if (v & kInc) atomicMax(&s_lim, idx);
+    } else {
+      atomicMax(&s_lim, -1);  // before tile 0: an inclusive prefix of 0
+    }
+    __syncthreads();
+    const int lim = s_lim;
+    const unsigned long long x = idx >= 0 && idx >= lim ? (v & ~kInc) - 1 : 0ull;
+    const unsigned long long sum = Red(red).Sum(x);
+    if (threadIdx.x == 0) s_acc += sum;
+    __syncthreads();
+    if (lim > top - kGT) break;
+  }
+  acc = s_acc;
+  if (threadIdx.x == 0) st_status(status + tile, kInc | (acc + agg + 1));
+  return acc;
+}
+
+// kKPT keys per thread: every mask word of the thread's keys is loaded at
+// once (the scan is latency-bound), a tile covers kGT * kKPT keys
+constexpr int kKPT = 4;
+
+template <int MAXW>
+__device__ __forceinline__ void load_masks(const uint32_t* __restrict__ mask, int64_t k0, int64_t K, int wpk,
+                                           uint32_t (&m)[kKPT][MAXW == 0 ? 1 : MAXW], int (&c)[kKPT]) {
+  if constexpr (MAXW == 4) {
+    if (wpk == 4) {  // one 16-byte row per key
+#pragma unroll
+      for (int j = 0; j < kKPT; ++j) {
+        const uint4 v = k0 + j < K ? __ldcg(reinterpret_cast<const uint4*>(mask) + k0 + j) : make_uint4(0, 0, 0, 0);
+        m[j][0] = v.x, m[j][1] = v.y, m[j][2] = v.z, m[j][3] = v.w;
+      }
+#pragma unroll
+      for (int j = 0; j < kKPT; ++j) c[j] = __popc(m[j][0]) + __popc(m[j][1]) + __popc(m[j][2]) + __popc(m[j][3]);
+      return;
+    }
+  }
+  if constexpr (MAXW > 0) {
+#pragma unroll
+    for (int j = 0; j < kKPT; ++j)
+#pragma unroll
+      for (int w = 0; w < MAXW; ++w) m[j][w] = k0 + j < K && w < wpk ? __ldcg(mask + (k0 + j) * wpk + w) : 0u;
+#pragma unroll
+    for (int j = 0; j < kKPT; ++j) {
+      c[j] = 0;
+#pragma unroll
+      for (int w = 0; w < MAXW; ++w) c[j] += __popc(m[j][w]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kKPT; ++j) {
+      c[j] = 0;
+      if (k0 + j < K)
+        for (int w = 0; w < wpk; ++w) c[j] += __popc(__ldcg(mask + (k0 + j) * wpk + w));
+    }
+  }
+}
+
+template <int MAXW>
 __global__ void __launch_bounds__(kGT) gd_scan_kernel(int64_t K, int wpk, const uint32_t* __restrict__ mask,
                                                       int32_t* __restrict__ uniq, int32_t* __restrict__ key_rank,
                                                       int32_t* __restrict__ seg_off, int32_t* __restrict__ seg_cnt,
@@ -251,47 +342,91 @@ __global__ void __launch_bounds__(kGT) gd_scan_kernel(int64_t K, int wpk, const 
   if (threadIdx.x == 0) s_tile = atomicAdd(tc.ctr, 1);
   __syncthreads();
   const int tile = s_tile;
-  const int64_t key = (int64_t)tile * kGT + threadIdx.x;
-  int c = 0;
-  if (key < K)
-    for (int w = 0; w < wpk; ++w) c += __popc(mask[key * wpk + w]);
-  const unsigned long long mine = c ? ((1ull << 31) | (unsigned long long)c) : 0ull;
+  const int64_t k0 = ((int64_t)tile * kGT + threadIdx.x) * kKPT;
+  uint32_t m[kKPT][MAXW == 0 ? 1 : MAXW];
+  int c[kKPT];
+  load_masks<MAXW>(mask, k0, K, wpk, m, c);
+  unsigned long long nk = 0, np = 0;
+#pragma unroll
+  for (int j = 0; j < kKPT; ++j) nk += c[j] ? 1 : 0, np += (unsigned)c[j];
+  const unsigned long long mine = (nk << 31) | np;
   unsigned long long off, agg;
   Scan2(tmp).ExclusiveSum(mine, off, agg);
-  if (threadIdx.x < 32) {
-    const unsigned long long base = tile_lookback2(tile, agg, tc.status);
-    if (threadIdx.x == 0) s_base = base;
+  const unsigned long long pre = tile_lookback2_block(tile, agg, tc.status) + off;
+  int r = (int)(pre >> 31), po = (int)(pre & 0x7fffffffull);
+#pragma unroll
+  for (int j = 0; j < kKPT; ++j) {
+    if (c[j]) {
+      const int64_t key = k0 + j;
+      uniq[r] = (int32_t)key;
+      key_rank[key] = po;  // dense mode: the key's segment offset (all the placement needs)
+      seg_off[r] = po;
+      seg_cnt[r] = c[j];
+      if (ll.list && c[j] > ll.min_len) ll.list[atomicAdd(ll.n, 1)] = r;
+      ++r;
+      po += c[j];
+    }
   }
-  __syncthreads();
-  const unsigned long long pre = s_base + off;
-  const int r = (int)(pre >> 31), po = (int)(pre & 0x7fffffffull);
-  if (c) {
-    uniq[r] = (int32_t)key;
-    key_rank[key] = po;  // dense mode: the key's segment offset (all the placement needs)
-    seg_off[r] = po;
-    seg_cnt[r] = c;
-    if (ll.list && c > ll.min_len) ll.list[atomicAdd(ll.n, 1)] = r;
-  }
-  if (key == K - 1) *n_uniq = r + (c ? 1 : 0);
+  if (k0 <= K - 1 && K - 1 < k0 + kKPT) *n_uniq = r;
 }
 
-__global__ void gd_place_kernel(const int32_t* __restrict__ keys, const int32_t* __restrict__ slots, const int32_t* n_dev,
-                                int64_t n_host, const int32_t* __restrict__ key_rank, int wpk,
-                                const uint32_t* __restrict__ mask, const int32_t* __restrict__ seg_off,
-                                int32_t* __restrict__ order, int32_t* __restrict__ inv, int32_t* __restrict__ sslot) {
+// kPPT pairs per thread, every load of the group issued before any store
+constexpr int kPPT = 4;
+
+__global__ void __launch_bounds__(256) gd_place_kernel(const int32_t* __restrict__ keys,
+                                                       const int32_t* __restrict__ slots, const int32_t* n_dev,
+                                                       int64_t n_host, const int32_t* __restrict__ key_rank, int wpk,
+                                                       const uint32_t* __restrict__ mask,
+                                                       const int32_t* __restrict__ seg_off,
+                                                       int32_t* __restrict__ order, int32_t* __restrict__ inv,
+                                                       int32_t* __restrict__ sslot) {
   const int64_t n = dev_count(n_dev, n_host);
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-    const int key = keys[q];
-    const int s = slots[q];
-    const uint32_t* m = mask + (int64_t)key * wpk;
-    int r = 0;
-    for (int w = 0; w < (s >> 5); ++w) r += __popc(m[w]);
-    r += __popc(m[s >> 5] & ((1u << (s & 31)) - 1u));
-    const int pos = key_rank[key] + r;  // (dense mode: key_rank holds the segment offset)
-    order[pos] = (int32_t)q;
-    if (inv) {
-      inv[q] = pos;
-      sslot[pos] = s;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q0 < n; q0 += T * kPPT) {
+    int key[kPPT], s[kPPT];
+#pragma unroll
+    for (int j = 0; j < kPPT; ++j) {
+      const int64_t q = q0 + j * T;
+      key[j] = q < n ? __ldcs(keys + q) : -1;
+      s[j] = q < n ? __ldcs(slots + q) : 0;
+    }
+    int base[kPPT], r[kPPT];
+    if (wpk == 4) {  // the whole 16-byte mask row
+#pragma unroll
+      for (int j = 0; j < kPPT; ++j) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        base[j] = 0;
+        if (key[j] >= 0) {
+          v = __ldcg(reinterpret_cast<const uint4*>(mask) + key[j]);
+          base[j] = __ldcg(key_rank + key[j]);
+        }
+        const int w = s[j] >> 5;
+        const uint32_t lo = (1u << (s[j] & 31)) - 1u;
+        r[j] = (w > 0 ? __popc(v.x) : __popc(v.x & lo)) + (w > 1 ? __popc(v.y) : w == 1 ? __popc(v.y & lo) : 0) +
+               (w > 2 ? __popc(v.z) : w == 2 ? __popc(v.z & lo) : 0) + (w == 3 ? __popc(v.w & lo) : 0);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kPPT; ++j) {
+        base[j] = key[j] >= 0 ? __ldcg(key_rank + key[j]) : 0;
+        r[j] = 0;
+        if (key[j] >= 0) {
+          const uint32_t* mk = mask + (int64_t)key[j] * wpk;
+          for (int w = 0; w < (s[j] >> 5); ++w) r[j] += __popc(__ldcg(mk + w));
+          r[j] += __popc(__ldcg(mk + (s[j] >> 5)) & ((1u << (s[j] & 31)) - 1u));
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kPPT; ++j) {
+      if (key[j] < 0) continue;
+      const int64_t q = q0 + j * T;
+      const int pos = base[j] + r[j];  // (dense mode: key_rank holds the segment offset)
+      order[pos] = (int32_t)q;
+      if (inv) {
+        inv[q] = pos;
+        sslot[pos] = s[j];
+      }
     }
   }
 }
@@ -332,7 +467,7 @@ void GroupBy::prepare(int64_t key_space, int64_t slots, int64_t items_max) {
       mask_words = need;
       mask_dense = true;
     }
-    tiles_bits = ceil_div(key_space, kGT);
+    tiles_bits = ceil_div(key_space, (int64_t)kGT * kKPT);
     tiles_seg = 0;
     status.ensure<unsigned long long>(tiles_bits);
     return;
@@ -362,13 +497,21 @@ void GroupBy::run(const int32_t* keys, const int32_t* slots, const int32_t* n_de
   }
   if (dense) {
     const TileCtl t{status.as<unsigned long long>(), ctrs.as<int32_t>()};
+    const int grid_place = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_max, 256 * kPPT), kSms * 8));
     gd_mask_kernel<<<grid_of(n_max), 256, 0, s>>>(keys, slots, n_dev, n_host, wpk, mask.as<uint32_t>(), t, tiles_bits);
     SLIDE_LAUNCH_CHECK();
-    gd_scan_kernel<<<(int)tiles_bits, kGT, 0, s>>>(K, wpk, mask.as<uint32_t>(), uniq.as<int32_t>(),
-                                                   key_rank.as<int32_t>(), seg_off.as<int32_t>(),
-                                                   seg_cnt.as<int32_t>(), n_uniq.as<int32_t>(), t, long_out);
+#define SLIDE_GDS(W)                                                                                   \
+  gd_scan_kernel<W><<<(int)tiles_bits, kGT, 0, s>>>(K, wpk, mask.as<uint32_t>(), uniq.as<int32_t>(),           \
+                                                    key_rank.as<int32_t>(), seg_off.as<int32_t>(),             \
+                                                    seg_cnt.as<int32_t>(), n_uniq.as<int32_t>(), t, long_out)
+    if (wpk <= 1) SLIDE_GDS(1);
+    else if (wpk <= 2) SLIDE_GDS(2);
+    else if (wpk <= 4) SLIDE_GDS(4);
+    else if (wpk <= 8) SLIDE_GDS(8);
+    else SLIDE_GDS(0);
+#undef SLIDE_GDS
     SLIDE_LAUNCH_CHECK();
-    gd_place_kernel<<<grid_of(n_max), 256, 0, s>>>(keys, slots, n_dev, n_host, key_rank.as<int32_t>(), wpk,
+    gd_place_kernel<<<grid_place, 256, 0, s>>>(keys, slots, n_dev, n_host, key_rank.as<int32_t>(), wpk,
                                                    mask.as<uint32_t>(), seg_off.as<int32_t>(), order.as<int32_t>(),
                                                    want_inv ? inv.as<int32_t>() : nullptr, sslot.as<int32_t>());
     SLIDE_LAUNCH_CHECK();
