@@ -66,7 +66,7 @@ struct slide_ctx {
   cudaEvent_t ev_fork = nullptr, ev_dh = nullptr, ev_join = nullptr, ev_pre = nullptr;
   // third stream: the per-row logits beside the dense-tile logits
   cudaStream_t s3 = nullptr;
-  cudaEvent_t ev_lg = nullptr, ev_lg_join = nullptr, ev_w1l = nullptr;
+  cudaEvent_t ev_lg = nullptr, ev_lg_join = nullptr, ev_w1l = nullptr, ev_hg = nullptr;
   DBuf hg_done;  // per-sample slice tickets of the hidden gradient (self-resetting)
   int64_t hg_done_n = 0;
   // set by the fused step callers: forward already queues the W1 grouping
@@ -317,7 +317,7 @@ int slide_destroy(slide_ctx* c) {
     c->gfeat.release();
     if (c->s2) cudaStreamSynchronize(c->s2);
     if (c->s3) cudaStreamSynchronize(c->s3);
-    for (cudaEvent_t e : {c->ev_fork, c->ev_dh, c->ev_join, c->ev_pre, c->ev_lg, c->ev_lg_join, c->ev_w1l})
+    for (cudaEvent_t e : {c->ev_fork, c->ev_dh, c->ev_join, c->ev_pre, c->ev_lg, c->ev_lg_join, c->ev_w1l, c->ev_hg})
       if (e) cudaEventDestroy(e);
     if (c->s2) cudaStreamDestroy(c->s2);
     if (c->s3) cudaStreamDestroy(c->s3);
@@ -525,7 +525,7 @@ static void side_stream_init(slide_ctx* c) {
   SLIDE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   SLIDE_CUDA(cudaStreamCreateWithPriority(&c->s2, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
   SLIDE_CUDA(cudaStreamCreateWithPriority(&c->s3, cudaStreamNonBlocking, hi));
-  for (cudaEvent_t* e : {&c->ev_fork, &c->ev_dh, &c->ev_join, &c->ev_pre, &c->ev_lg, &c->ev_lg_join, &c->ev_w1l})
+  for (cudaEvent_t* e : {&c->ev_fork, &c->ev_dh, &c->ev_join, &c->ev_pre, &c->ev_lg, &c->ev_lg_join, &c->ev_w1l, &c->ev_hg})
     SLIDE_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
 }
 
@@ -762,13 +762,6 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
     sw = c->s2;
     SLIDE_CUDA(cudaEventRecord(c->ev_fork, s));
     SLIDE_CUDA(cudaStreamWaitEvent(sw, c->ev_fork, 0));
-    if (c->grow_pending && update) {
-      // the row grouping's masks were last read by the logits: clear them on
-      // the third stream beside the rest of the backward pass
-      SLIDE_CUDA(cudaStreamWaitEvent(c->s3, c->ev_fork, 0));
-      gr.clear(c->s3);
-      c->grow_pending = false;
-    }
   }
   int32_t* xs = nnz > 0 ? c->xslot.ensure<int32_t>(nnz) : nullptr;
   gf.long_min = kW1LongChain;  // the grouping lists the long chains for the W1 Adam
@@ -783,13 +776,25 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
   const float* dh = ext_dh;
   if (!dh) {
     float* out = c->dh.ensure<float>((size_t)b * hp);
-    launch_hidden_grad(hp, b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->delta.as<float>(), d.w2,
-                       c->h.as<float>(), c->live.as<int32_t>(), out,
-                       c->partial.ensure<float>(hidden_grad_scratch(b, hp)),
-                       hg_tickets(c, b), update ? c->work.ensure<int32_t>(4) : nullptr, s);
+    if (P_max > 0 && b <= 1024)  // the errors in row-grouped order (dsort) and the grouping
+      launch_hidden_grad_rows(hp, b, gr.view(), c->dsort.as<float>(), d.w2, c->h.as<float>(), c->live.as<int32_t>(),
+                              out, c->partial.ensure<float>(hidden_grad_rows_scratch(b, hp)), update ? c->work.ensure<int32_t>(4) : nullptr, s);
+    else
+      launch_hidden_grad(hp, b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->delta.as<float>(), d.w2,
+                         c->h.as<float>(), c->live.as<int32_t>(), out,
+                         c->partial.ensure<float>(hidden_grad_scratch(b, hp)),
+                         hg_tickets(c, b), update ? c->work.ensure<int32_t>(4) : nullptr, s);
     dh = out;
   }
   c->timer.mark(s, kStHiddenGrad);
+  if (fork && c->grow_pending) {
+    // the row grouping's masks were last read by the hidden gradient: clear
+    // them on the third stream beside the rest of the backward pass
+    SLIDE_CUDA(cudaEventRecord(c->ev_hg, s));
+    SLIDE_CUDA(cudaStreamWaitEvent(c->s3, c->ev_hg, 0));
+    gr.clear(c->s3);
+    c->grow_pending = false;
+  }
   if (!update) {
     if (c->w1_grouped) {  // a pre-forked grouping must still be joined
       side_stream_init(c);

@@ -135,6 +135,11 @@ void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32
 // dst[inv[q]] = src[q] for q < *n_dev
 void launch_scatter_sorted(const int32_t* n_dev, int64_t n_max, const int32_t* inv, const float* src, float* dst,
                            cudaStream_t s);
+// hidden gradient from the row grouping (single-GPU step; errors in
+// row-grouped order, dsort); scratch floats: hidden_grad_rows_scratch
+size_t hidden_grad_rows_scratch(int b, int hp);
+void launch_hidden_grad_rows(int hp, int b, const GroupView& g, const float* dsort, const float* w2, const float* h,
+                             const int32_t* live, float* dh, float* part, int32_t* work_reset, cudaStream_t s);
 // floats of scratch launch_hidden_grad needs
 size_t hidden_grad_scratch(int b, int hp);
 // done: b zero-initialised ints (self-resetting); work_reset (optional): the

@@ -525,9 +525,10 @@ void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32
 // dh_i = W2[A_i, :]^T delta_i with the pre-update W2, kept on nz(h_i)
 // (network.py:328-332).  Sample i's pairs are cut into S slices, one CTA
 // each (B*S CTAs fill the GPU); every slice sums in a fixed order, the
-// slices are added in slice order -- deterministic.  (A dense register-tiled
-// Delta^T W2 over the distinct rows was tried: the Delta scatter and the
-// partial reduction cost more than the L2 re-reads of W2 rows it saves.)
+// slices are added in slice order -- deterministic.  Used for the sharded
+// partials; the single-GPU step uses hidden_grad_rows_kernel below (each W2
+// row read once per 32-slot window from the row grouping, 28 -> 15 us at
+// wide-in).
 struct HiddenGradArgs {
   int hp, b, slices;
   const int32_t *offs, *prow;
@@ -640,6 +641,154 @@ void launch_hidden_grad(int hp, int b, const int32_t* offs, const int32_t* prow,
   const int S = hidden_grad_slices(b);
   HiddenGradArgs A{hp, b, S, offs, prow, delta, w2, h, live, part, dh, done, work_reset};
   SLIDE_NV_DISPATCH(hp, (hidden_grad_kernel<NV><<<b * S, 256, 0, s>>>(A)));
+  SLIDE_LAUNCH_CHECK();
+}
+
+// Hidden gradient by rows (single-GPU step): the row-major grouping gives,
+// per distinct active row, its slots (mask) and errors (dsort, slot order).
+// CTA (window, chunk) takes 32 slots and a contiguous chunk of distinct
+// rows; each warp reads its rows' grouping entries and masks at once (one
+// row per lane), then walks the rows with the next row's errors and live
+// W2 columns in flight, adding the errors of the window's slots into 32 x
+// (32 NG) register accumulators.  The warps are summed in warp order into
+// the chunk's partial; hidden_grad_reduce_kernel sums the chunks in a fixed
+// order -- deterministic.  Each W2 row is read once per window instead of
+// once per (sample, row) pair.
+constexpr int kHgWin = 32;
+
+struct HiddenGradRowsArgs {
+  int hp, b, nwin, nchunk;
+  GroupView g;
+  const float *dsort, *w2, *h;
+  const int32_t* live;
+  float *part, *dh;
+  int32_t* work_reset;
+};
+
+// one pass per live group g0 (32 live columns).  Lane t holds slot
+// s_lo + t's error of the current row (0 where the row is not active for
+// it) and its 32 accumulators (one per live column); the row's live W2
+// columns go through a per-warp shared-memory line and are read back as
+// broadcast float4s: 8 loads + 32 FMAs per (row, window).
+__device__ __forceinline__ void hg_rows_body(const HiddenGradRowsArgs& A, float* red, float* wsm, int g0) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int win = blockIdx.x % A.nwin, chunk = blockIdx.x / A.nwin;
+  const int64_t nu = *A.g.n_uniq;
+  const int64_t u_beg = nu * chunk / A.nchunk, u_end = nu * (chunk + 1) / A.nchunk;
+  const int col = __ldg(A.live + 1 + g0 * 32 + lane);
+  const unsigned below = (1u << lane) - 1u;
+  float* ws = wsm + warp * 32;
+  float acc[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) acc[k] = 0.f;
+  for (int64_t ub = u_beg + warp; ub < u_end; ub += 8 * 32) {
+    // lane j: row ub + 8 j -- its W2 row, first sorted position, window bits
+    const int64_t uj = ub + 8 * lane;
+    const bool ok = uj < u_end;
+    const int row_l = ok ? __ldg(A.g.uniq + uj) : 0;
+    int p0_l = ok ? __ldg(A.g.seg_off + uj) : 0;
+    uint32_t bits_l = 0;
+    if (ok) {
+      const uint32_t* mk = A.g.mask + (A.g.mask_by_key ? (int64_t)row_l : uj) * A.g.wpk;
+      bits_l = __ldg(mk + win);
+      for (int w = 0; w < win; ++w) p0_l += __popc(__ldg(mk + w));
+    }
+    const int nr = (int)min((int64_t)32, (u_end - ub + 7) / 8);
+    // two-stage pipeline over the rows: errors + W2 columns of row j + 1
+    // are loaded while row j is added
+    auto fetch = [&](int j, float& e, float& w) {
+      const uint32_t bits = __shfl_sync(0xffffffffu, bits_l, j);
+      const int p0 = __shfl_sync(0xffffffffu, p0_l, j);
+      const int r = __shfl_sync(0xffffffffu, row_l, j);
+      e = (bits >> lane) & 1u ? __ldg(A.dsort + p0 + __popc(bits & below)) : 0.f;
+      w = bits ? __ldg(A.w2 + (int64_t)r * A.hp + col) : 0.f;
+    };
+    float e, w;
+    fetch(0, e, w);
+    for (int j = 0; j < nr; ++j) {
+      float e_n = 0.f, w_n = 0.f;
+      if (j + 1 < nr) fetch(j + 1, e_n, w_n);
+      __syncwarp();
+      ws[lane] = w;
+      __syncwarp();
+#pragma unroll
+      for (int k4 = 0; k4 < 8; ++k4) {
+        const float4 w4 = *reinterpret_cast<const float4*>(ws + 4 * k4);
+        acc[4 * k4 + 0] = fmaf(e, w4.x, acc[4 * k4 + 0]);
+        acc[4 * k4 + 1] = fmaf(e, w4.y, acc[4 * k4 + 1]);
+        acc[4 * k4 + 2] = fmaf(e, w4.z, acc[4 * k4 + 2]);
+        acc[4 * k4 + 3] = fmaf(e, w4.w, acc[4 * k4 + 3]);
+      }
+      e = e_n;
+      w = w_n;
+    }
+  }
+  // warps in warp order into red [32 slots][33], then the chunk's partial
+  for (int wp = 0; wp < 8; ++wp) {
+    if (warp == wp) {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) red[lane * 33 + k] = (wp ? red[lane * 33 + k] : 0.f) + acc[k];
+    }
+    __syncthreads();
+  }
+  const int s_lo = win * kHgWin;
+  for (int idx = threadIdx.x; idx < kHgWin * 32; idx += 256) {
+    const int t = idx >> 5, k = idx & 31;
+    if (s_lo + t < A.b) A.part[((int64_t)chunk * A.b + s_lo + t) * A.hp + g0 * 32 + k] = red[t * 33 + k];
+  }
+  __syncthreads();  // red is reused by the next pass
+}
+
+__global__ void __launch_bounds__(256, 4) hidden_grad_rows_kernel(HiddenGradRowsArgs A) {
+  __shared__ __align__(16) float hg_red[kHgWin * 33];
+  __shared__ __align__(16) float hg_w[8 * 32];
+  if (A.work_reset && blockIdx.x == 0 && threadIdx.x == 0) *A.work_reset = 0;
+  const int ng = max(1, (__ldg(A.live) + 31) >> 5);
+  for (int g0 = 0; g0 < ng; ++g0) hg_rows_body(A, hg_red, hg_w, g0);
+}
+
+// one CTA per sample: warp w sums chunks w, w + 8, ... (lane = live column),
+// the warps are added in warp order; dh = sum on h > 0, dead units 0
+__global__ void __launch_bounds__(256) hidden_grad_reduce_kernel(HiddenGradRowsArgs A) {
+  extern __shared__ __align__(16) float hg_sum[];  // [8][hp]
+  const int i = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kn = ((__ldg(A.live) + 31) >> 5) * 32;
+  for (int kk = lane; kk < kn; kk += 32) {
+    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+    int c = warp;
+    for (; c + 24 < A.nchunk; c += 32) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s4[j] += __ldcg(A.part + ((int64_t)(c + 8 * j) * A.b + i) * A.hp + kk);
+    }
+    float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    for (; c < A.nchunk; c += 8) sum += __ldcg(A.part + ((int64_t)c * A.b + i) * A.hp + kk);
+    hg_sum[warp * A.hp + kk] = sum;
+  }
+  __syncthreads();
+  for (int kk = threadIdx.x; kk < A.hp; kk += 256) {
+    float sum = 0.f;
+    if (kk < kn)
+      for (int w = 0; w < 8; ++w) sum += hg_sum[w * A.hp + kk];
+    const int64_t q = (int64_t)i * A.hp + __ldg(A.live + 1 + kk);
+    A.dh[q] = (A.h == nullptr || A.h[q] > 0.f) ? sum : 0.f;
+  }
+}
+
+static int hg_rows_chunks(int b) {
+  const int nwin = (int)ceil_div(b, kHgWin);
+  return std::max(1, kSms * 4 / nwin);  // one wave at 4 CTAs per SM
+}
+
+size_t hidden_grad_rows_scratch(int b, int hp) { return (size_t)hg_rows_chunks(b) * b * hp; }
+
+void launch_hidden_grad_rows(int hp, int b, const GroupView& g, const float* dsort, const float* w2, const float* h,
+                             const int32_t* live, float* dh, float* part, int32_t* work_reset, cudaStream_t s) {
+  if (b <= 0) return;
+  const int nwin = (int)ceil_div(b, kHgWin), nchunk = hg_rows_chunks(b);
+  HiddenGradRowsArgs A{hp, b, nwin, nchunk, g, dsort, w2, h, live, part, dh, work_reset};
+  hidden_grad_rows_kernel<<<nwin * nchunk, 256, 0, s>>>(A);
+  SLIDE_LAUNCH_CHECK();
+  hidden_grad_reduce_kernel<<<b, 256, 8 * hp * 4, s>>>(A);
   SLIDE_LAUNCH_CHECK();
 }
 
