@@ -589,7 +589,21 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   uint32_t* hmask = c->hmask.ensure<uint32_t>((size_t)b * (hp / 32));
   int32_t* live = c->live.ensure<int32_t>(1 + hp);
   c->timer.mark(s, kStStart);
-  launch_hidden_forward(hp, b, bt->x_ptr, bt->x_idx, bt->x_val, d.w1t, d.b1, h, hmask, live, live_ticket(c), s);
+  // SimHash query keys computed by the hidden forward itself when the
+  // per-sample query kernel would run (the same arithmetic)
+  QueryHash qh;
+  const bool fuse_qh = !bt->forced_ptr && d.family == 1 && c->sh_packed_t.p != nullptr && b <= kSms * 8 &&
+                       (int64_t)d.k * d.l <= kQhMaxBits;
+  if (fuse_qh) {
+    const SimHashDev f = simhash_of(c);
+    qh.packed_t = f.packed_t;
+    qh.k = f.k;
+    qh.l = f.l;
+    qh.c = f.c;
+    qh.keys = c->qkeys.ensure<uint32_t>((size_t)b * L);
+  }
+  launch_hidden_forward(hp, b, bt->x_ptr, bt->x_idx, bt->x_val, d.w1t, d.b1, h, hmask, live, live_ticket(c), s,
+                        fuse_qh ? &qh : nullptr);
   c->timer.mark(s, kStHidden);
   c->host_counts[2] += b;
 
@@ -611,7 +625,7 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     c->timer.mark(s, kStSelect);
   } else {
     uint32_t* qk = c->qkeys.ensure<uint32_t>((size_t)b * L);
-    hash_rows(c, h, b, qk);
+    if (!fuse_qh) hash_rows(c, h, b, qk);
     c->timer.mark(s, kStQueryHash);
     uint64_t* states = c->states.ensure<uint64_t>((size_t)b * 6);
     uint8_t* order = c->order.ensure<uint8_t>((size_t)b * L);

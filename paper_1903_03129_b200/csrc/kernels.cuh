@@ -119,9 +119,16 @@ struct AdamParams {
 // CTA writes live (1 + hp ints): the number of units nonzero anywhere in the
 // batch, then the live units ascending followed by the dead ones.  ticket:
 // one zero-initialised int (self-resetting).
+// SimHash query keys fused into the hidden forward (per-sample queries)
+constexpr int kQhMaxBits = 2048;
+struct QueryHash {
+  const uint16_t* packed_t = nullptr;  // (c, K*L) terms: idx | (sign < 0) << 15
+  int k = 0, l = 0, c = 0;
+  uint32_t* keys = nullptr;            // (b, L)
+};
 void launch_hidden_forward(int hp, int b, const int32_t* x_ptr, const int32_t* x_idx, const float* x_val,
                            const float* w1t, const float* b1, float* h, uint32_t* hmask, int32_t* live,
-                           int32_t* ticket, cudaStream_t s);
+                           int32_t* ticket, cudaStream_t s, const QueryHash* qh = nullptr);
 // the same live-unit list from an h written by other means
 void launch_live_cols_from_h(int hp, int b, const float* h, uint32_t* hmask, int32_t* live, cudaStream_t s);
 

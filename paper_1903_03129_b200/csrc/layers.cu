@@ -95,7 +95,11 @@ void launch_live_cols_from_h(int hp, int b, const float* h, uint32_t* hmask, int
   SLIDE_LAUNCH_CHECK();
 }
 
-template <int NV, int kFwdWarps = FwdWarps<NV>::value>
+// QH: the sample's SimHash query keys are computed by the same CTA from its
+// h row in shared memory (simhash_query_kernel's arithmetic: fp64 sums in
+// the packed term order, bit = sum > 0) -- one launch and one dependent
+// round trip fewer on the forward path.
+template <int NV, bool QH = false, int kFwdWarps = FwdWarps<NV>::value>
 __global__ void __launch_bounds__(kFwdWarps * 32) hidden_fwd_kernel(int hp, const int32_t* __restrict__ x_ptr,
                                                                     const int32_t* __restrict__ x_idx,
                                                                     const float* __restrict__ x_val,
@@ -103,7 +107,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) hidden_fwd_kernel(int hp, cons
                                                                     const float* __restrict__ b1,
                                                                     float* __restrict__ h, uint32_t* __restrict__ hmask,
                                                                     int32_t* __restrict__ live,
-                                                                    int32_t* __restrict__ ticket) {
+                                                                    int32_t* __restrict__ ticket, QueryHash qh) {
   __shared__ float red[kFwdWarps][NV * 128];
   const int i = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int a = x_ptr[i], e = x_ptr[i + 1];
@@ -155,9 +159,43 @@ __global__ void __launch_bounds__(kFwdWarps * 32) hidden_fwd_kernel(int hp, cons
     s += b1[c];
     const float hv = s > 0.f ? s : 0.f;
     h[(int64_t)i * hp + c] = hv;
+    if (QH) red[0][c] = hv;  // column c is read by this thread only
     // warps cover 32 consecutive units (hp % 32 == 0): one mask word each
     const unsigned bal = __ballot_sync(0xffffffffu, hv > 0.f);
     if (lane == 0) hmask[(int64_t)i * (hp >> 5) + (c >> 5)] = bal;
+  }
+  if constexpr (QH) {
+    __shared__ uint8_t qbits[kQhMaxBits];
+    __syncthreads();
+    const int KL = qh.k * qh.l;
+    const float* hs = &red[0][0];
+    for (int p = threadIdx.x; p < KL; p += kFwdWarps * 32) {
+      double acc = 0.0;
+      // the terms come from L2: 8 loads in flight, summed in term order
+      int j = 0;
+      for (; j + 8 <= qh.c; j += 8) {
+        uint16_t t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u] = __ldg(qh.packed_t + (j + u) * KL + p);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double v = (double)hs[t[u] & 0x7fff];
+          acc += (t[u] >> 15) ? -v : v;
+        }
+      }
+      for (; j < qh.c; ++j) {
+        const uint16_t t = __ldg(qh.packed_t + j * KL + p);
+        const double v = (double)hs[t & 0x7fff];
+        acc += (t >> 15) ? -v : v;
+      }
+      qbits[p] = acc > 0.0;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < qh.l; t += kFwdWarps * 32) {
+      uint32_t key = 0;
+      for (int kk = 0; kk < qh.k; ++kk) key |= (uint32_t)qbits[t * qh.k + kk] << kk;
+      qh.keys[(int64_t)i * qh.l + t] = key;
+    }
   }
   // the batch's last CTA to finish builds the live-unit permutation
   __shared__ int s_last;
@@ -173,10 +211,15 @@ __global__ void __launch_bounds__(kFwdWarps * 32) hidden_fwd_kernel(int hp, cons
 
 void launch_hidden_forward(int hp, int b, const int32_t* x_ptr, const int32_t* x_idx, const float* x_val,
                            const float* w1t, const float* b1, float* h, uint32_t* hmask, int32_t* live,
-                           int32_t* ticket, cudaStream_t s) {
+                           int32_t* ticket, cudaStream_t s, const QueryHash* qh) {
   if (b <= 0) return;
-  SLIDE_NV_DISPATCH(hp, (hidden_fwd_kernel<NV><<<b, FwdWarps<NV>::value * 32, 0, s>>>(hp, x_ptr, x_idx, x_val, w1t, b1,
-                                                                                     h, hmask, live, ticket)));
+  if (qh) {
+    SLIDE_NV_DISPATCH(hp, (hidden_fwd_kernel<NV, true><<<b, FwdWarps<NV>::value * 32, 0, s>>>(
+                              hp, x_ptr, x_idx, x_val, w1t, b1, h, hmask, live, ticket, *qh)));
+  } else {
+    SLIDE_NV_DISPATCH(hp, (hidden_fwd_kernel<NV><<<b, FwdWarps<NV>::value * 32, 0, s>>>(
+                              hp, x_ptr, x_idx, x_val, w1t, b1, h, hmask, live, ticket, QueryHash{})));
+  }
   SLIDE_LAUNCH_CHECK();
 }
 
