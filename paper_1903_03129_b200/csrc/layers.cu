@@ -426,26 +426,35 @@ __global__ void __launch_bounds__(256, 3) logits_tiles_kernel(int hp, int b, Gro
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) zt[(ty + 16 * j) * kZLd + tx + 16 * jj] = acc[j][jj];
     __syncthreads();
-    const int pbeg = base_s[0], pend = base_s[nrow - 1] + len_s[nrow - 1];
-    for (int p0 = pbeg + tid; p0 < pend; p0 += 256 * 4) {
-      int sl[4], od[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int pos = p0 + 256 * t;
-        sl[t] = pos < pend ? g.sslot[pos] - s0 : -1;
-        od[t] = pos < pend ? g.order[pos] : 0;
-      }
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        if (sl[t] < 0 || sl[t] >= kTN) continue;
-        const int pos = p0 + 256 * t;
-        int lo = 0, hi = nrow - 1;  // the row holding pos: last base_s <= pos
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (base_s[mid] <= pos) lo = mid;
-          else hi = mid - 1;
+    // each row's pairs are slot-ascending, so this sample block's pairs of
+    // a row are one sub-range of its segment, found from the row's slot
+    // mask: lane r < 8 of warp w sizes row w + 8 r, then the warp walks
+    // those rows' sub-ranges (coalesced slots and pair ids)
+    {
+      int lo_l = 0, n_l = 0;
+      const int rr = warp + 8 * lane;
+      if (lane < 8 && rr < nrow) {
+        const uint32_t* mk = g.mask_of(u0 + rr);
+        const int wa = s0 >> 5, wb = (s0 + kTN) >> 5;  // kTN = 64: whole words
+        int below = 0, in = 0;
+        for (int w = 0; w < g.wpk; ++w) {
+          const int c = __popc(__ldg(mk + w));
+          if (w < wa) below += c;
+          else if (w < wb) in += c;
         }
-        z[od[t]] = zt[lo * kZLd + sl[t]] + bias_s[lo];
+        lo_l = base_s[rr] + below;
+        n_l = in;
+      }
+#pragma unroll 2
+      for (int r = 0; r < 8; ++r) {
+        const int row = warp + 8 * r;
+        if (row >= nrow) break;
+        const int lo = __shfl_sync(0xffffffffu, lo_l, r), n = __shfl_sync(0xffffffffu, n_l, r);
+        for (int j = lane; j < n; j += 32) {
+          const int pos = lo + j;
+          const int sl = g.sslot[pos] - s0;
+          z[g.order[pos]] = zt[row * kZLd + sl] + bias_s[row];
+        }
       }
     }
     __syncthreads();  // zt / base / len / bias / wrow reuse by the next item
