@@ -520,14 +520,29 @@ __global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict
   const int i = blockIdx.x, tid = threadIdx.x;
   const int o = offs[i], n = offs[i + 1] - o;
   const int ny = y_ptr[i + 1] - y_ptr[i];
+  // the first kSmC logits per thread stay in registers (with their
+  // exponentials) across the three passes; a longer set re-reads the rest
+  constexpr int kSmC = 8;
+  float zr[kSmC], er[kSmC];
   float mx = -INFINITY;
-  for (int k = tid; k < n; k += 1024) mx = fmaxf(mx, z[o + k]);
+#pragma unroll
+  for (int j = 0; j < kSmC; ++j) {
+    const int k = tid + j * 1024;
+    zr[j] = k < n ? z[o + k] : -INFINITY;
+    mx = fmaxf(mx, zr[j]);
+  }
+  for (int k = tid + kSmC * 1024; k < n; k += 1024) mx = fmaxf(mx, z[o + k]);
   mx = RF(tmp.f).Reduce(mx, cub::Max());
   if (tid == 0) s_max = n > 0 ? mx : 0.f;
   __syncthreads();
   mx = s_max;
   float se = 0.f;
-  for (int k = tid; k < n; k += 1024) se += expf(z[o + k] - mx);
+#pragma unroll
+  for (int j = 0; j < kSmC; ++j) {
+    er[j] = tid + j * 1024 < n ? expf(zr[j] - mx) : 0.f;
+    se += er[j];
+  }
+  for (int k = tid + kSmC * 1024; k < n; k += 1024) se += expf(z[o + k] - mx);
   se = RF(tmp.f).Sum(se);
   if (tid == 0) s_sum = se;
   __syncthreads();
@@ -535,7 +550,23 @@ __global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict
   const float lse = logf(se);
   const float inv_ny = ny > 0 ? 1.f / (float)ny : 0.f;
   double lsum = 0.0;
-  for (int k = tid; k < n; k += 1024) {
+#pragma unroll
+  for (int j = 0; j < kSmC; ++j) {
+    const int k = tid + j * 1024;
+    if (k >= n) break;
+    const float zz = zr[j] - mx;
+    const float p = er[j] / se;
+    const int lab = plab[o + k];
+    prob[o + k] = p;
+    const float dl = lab ? p - inv_ny : p;
+    delta[o + k] = dl;
+    if (inv) dsort[inv[o + k]] = dl;
+    if (lab) {
+      double nl = -((double)zz - (double)lse);
+      lsum += nl < 690.7755278982137 ? nl : 690.7755278982137;
+    }
+  }
+  for (int k = tid + kSmC * 1024; k < n; k += 1024) {
     const float zz = z[o + k] - mx;
     const float p = expf(zz) / se;
     const int lab = plab[o + k];
