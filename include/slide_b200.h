@@ -170,7 +170,12 @@ int slide_graph_step(slide_ctx* ctx, const slide_batch* batch, int64_t iteration
  * k+1 is queued behind step k before the host waits for k; anything a
  * barrier enqueues on the context stream between the two (a table rebuild)
  * runs after step k and before step k+1.  slide_graph_step needs none in
- * flight. */
+ * flight.
+ * Host batch arrays and the rebased offsets are staged per in-flight slot
+ * on a context copy stream (beside the step in flight); a device batch is
+ * read by the step's copy-in kernel after the caller's stream.  The D2H of
+ * the results runs on the copy stream too; the caller's stream continues
+ * after the step's device work. */
 int slide_graph_step_async(slide_ctx* ctx, const slide_batch* batch, int64_t iteration);
 int slide_graph_step_wait(slide_ctx* ctx, double* loss_host, int64_t* active_host);
 
