@@ -126,6 +126,17 @@ class ClockSampler:
                 "samples": len(self.rows), "source": "nvml"}
 
 
+def config_of(w, args, world):
+    """The workload's `config` object -- identical on both arms' lines."""
+    return {"workload": w.name, "input_dim": w.input_dim, "hidden": w.hidden, "n_out": w.n_out,
+            "batch": w.batch, "hash": f"{w.family} K={w.k} L={w.l} cap={w.cap} {w.policy}",
+            "sampler": f"{w.strategy} beta={w.beta}", "lr": w.lr, "rebuild": f"n0={w.n0} decay={w.decay}",
+            "schedule": args.schedule,
+            "parallelism": f"output layer column-sharded x{world}" if world > 1 else "1 GPU",
+            "rebuild_in_step": "amortised: measured table rebuild ms / n0 added to every step",
+            "l2": "flushed between steps (256 MiB write, outside the events)"}
+
+
 def make_net(w, torch, rank=0, world=1):
     from paper_1903_03129_b200 import LshLayerConfig, SamplerConfig, SlideNetwork, TrainConfig
 
@@ -176,6 +187,24 @@ def stage_bytes(w, ms, cnt, steps):
     return b, step
 
 
+def measure_rebuild(net, torch, flush, args, reps=3):
+    """Median event time of `reps` full table rebuilds (hash every W2 row +
+    build all L tables: the barrier's path, network._rebuild_tables), L2
+    flushed before each."""
+    out = []
+    for _ in range(reps):
+        if not args.no_flush:
+            flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        net._rebuild_tables()
+        e1.record()
+        torch.cuda.synchronize()
+        out.append(e0.elapsed_time(e1))
+    return float(np.median(out))
+
+
 def recaptures(net):
     """Graph re-captures so far on the net's context (host_counts[5])."""
     from paper_1903_03129_b200 import _lib
@@ -217,7 +246,7 @@ def run_ours(args, rank, world):
     loss_buf = np.empty(w.batch, np.float64)
     act_buf = np.empty(w.batch, np.int64)
 
-    def step_dev(it):
+    def step_dev(it, barrier=True):
         bt, keep, hb = dev_batches[it - 1]
         if world > 1:  # column-sharded output layer: stages + all-reduces
             from paper_1903_03129_b200.sharded import GpuShardBackend, sharded_step
@@ -230,7 +259,7 @@ def run_ours(args, rank, world):
         else:
             _lib.call("slide_train_batch", net._ctx, _lib.C.byref(bt), it, sub, loss_buf.ctypes.data,
                       act_buf.ctypes.data)
-        return net._barrier(it, loss_buf, act_buf)
+        return net._barrier(it, loss_buf, act_buf) if barrier else net._stats(loss_buf, act_buf, [])
 
     # one GPU, graph steps: two steps in flight (slide_graph_step_async), so
     # the host's launch work overlaps the device -- per step, on the context
@@ -248,13 +277,14 @@ def run_ours(args, rank, world):
             bt = dev_batches[it - 1][0]
             if not args.no_flush:
                 flush.zero_()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0, em, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             e0.record()
             _lib.call("slide_graph_step_async", net._ctx, _lib.C.byref(bt), it)
-            net._rebuild_after(it)
+            em.record()
+            rebuilt = net._rebuild_after(it)
             e1.record()
             if evs is not None:
-                evs.append((e0, e1))
+                evs.append((e0, em, e1, bool(rebuilt)))
             if k > 0:
                 wait_oldest()
         wait_oldest()
@@ -274,27 +304,37 @@ def run_ours(args, rank, world):
     times = []
     losses = []
     with sampler as clk:
+        # per step: the step (e0 -> em) and its rebuild barrier (em -> e1)
         if pipelined_dev:
             evs = []
             run_pipelined(range(W + 1, W + K + 1), evs, losses)
-            times = [a.elapsed_time(b) for a, b in evs]
         else:
+            evs = []
             for it in range(W + 1, W + K + 1):
                 if not args.no_flush:
                     flush.zero_()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0, em, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
                 torch.cuda.synchronize()
                 e0.record()
-                st = step_dev(it)
+                st = step_dev(it, barrier=False)
+                em.record()
+                rebuilt = net._rebuild_after(it) if world == 1 else st.rebuilt
                 e1.record()
                 torch.cuda.synchronize()
-                times.append(e0.elapsed_time(e1))
+                evs.append((e0, em, e1, bool(rebuilt)))
                 losses.append(st.loss)
+        times = [a.elapsed_time(m) for a, m, _, _ in evs]
+        barrier_ms = [m.elapsed_time(b) for _, m, b, r in evs if r]
     lc1 = np.zeros(1, np.uint64)
     _lib.call("slide_launch_count", lc1.ctypes.data)
     if dist:
         dist.barrier()
-    total_ms = float(np.sum(times))
+    # the table rebuild of the barrier, amortised over its period: measured
+    # live (event-timed forced rebuilds of this net, the barrier's own path)
+    # unless the window itself held rebuilds
+    rebuild_ms = float(np.median(barrier_ms)) if barrier_ms else measure_rebuild(net, torch, flush, args)
+    amort_ms = rebuild_ms / w.n0
+    total_ms = float(np.sum(times)) + K * amort_ms
     if dist:
         t = torch.tensor([total_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -329,10 +369,12 @@ def run_ours(args, rank, world):
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                net.train_batches_csr(order, first_iteration=it0, schedule=args.schedule)
+                stats = net.train_batches_csr(order, first_iteration=it0, schedule=args.schedule)
                 e1.record()
                 torch.cuda.synchronize()
-                p_passes.append(e0.elapsed_time(e1))
+                # the pass's own rebuilds replaced by the amortised share
+                n_rb = sum(bool(x.rebuilt) for x in stats)
+                p_passes.append(e0.elapsed_time(e1) - n_rb * rebuild_ms + K * amort_ms)
                 p_recap.append(recaptures(net) - rc0)
                 it0 += K
             p_total = float(np.median(p_passes))
@@ -345,10 +387,10 @@ def run_ours(args, rank, world):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            net.train_batch_csr(b, it, schedule=args.schedule)
+            st = net.train_batch_csr(b, it, schedule=args.schedule)
             e1.record()
             torch.cuda.synchronize()
-            e_times.append(e0.elapsed_time(e1))
+            e_times.append(e0.elapsed_time(e1) - bool(st.rebuilt) * rebuild_ms + amort_ms)
             h2d += net.h2d_bytes
             d2h += w.batch * 16 + (w.batch + 1) * 4 * (w.batch // sub)
         e_total = float(np.sum(e_times))
@@ -418,13 +460,12 @@ def run_ours(args, rank, world):
         "vs_baseline": None,
         # per-step spread (the steps whose barrier rebuilt the tables are the max)
         "ms_per_step_p50": float(np.median(times)), "ms_per_step_max": float(np.max(times)),
+        # the step alone (no rebuild) and the rebuild it amortises
+        "ms_step_only_mean": float(np.mean(times)), "rebuild_ms": rebuild_ms,
+        "rebuild_amortised_ms_per_step": amort_ms, "rebuilds_in_window": len(barrier_ms),
+        "value_without_rebuild": K * w.batch / (float(np.sum(times)) / 1e3),
         "dtype": "f32", "data": "synthetic (SURVEY 8(d) Zipf generator; Delicious-200K shape)",
-        "config": {"workload": w.name, "input_dim": w.input_dim, "hidden": w.hidden, "n_out": w.n_out,
-                   "batch": w.batch, "hash": f"{w.family} K={w.k} L={w.l} cap={w.cap} {w.policy}",
-                   "sampler": f"{w.strategy} beta={w.beta}", "lr": w.lr, "rebuild": f"n0={w.n0} decay={w.decay}",
-                   "schedule": args.schedule,
-                   "parallelism": f"output layer column-sharded x{world} (NCCL all-reduces)" if world > 1 else "1 GPU",
-                   "l2": "flushed between steps (256 MiB write, outside the events)"},
+        "config": config_of(w, args, world),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind, "issue": issue,
                      "algorithmic_bytes_per_launch": sb[dom], "ms_per_launch": stage_ms[dom]},
@@ -567,7 +608,7 @@ def run_reference(args, rank, world):
 
     w = WORKLOADS[args.workload]
     cores = os.cpu_count() or 1
-    per_step = max(1, min(w.batch, 4 * cores))
+    per_step = w.batch  # the full batch: the same config as the GPU arm
     with threadpool_limits(1):
         st = _shared_state(O.init_state(w.input_dim, w.hidden, w.n_out, seed=0))
         spec = O.LshSpec(w.family, w.k, w.l, w.cap, w.policy, bin_size=w.bin_size, strategy=w.strategy, beta=w.beta)
@@ -581,15 +622,21 @@ def run_reference(args, rank, world):
         pool = None
         rebuilds = [0]
 
+        rb_s = []
+
         def step(it):
             nonlocal pool
             batch = trip[(it - 1) * per_step : it * per_step]
             if pool is None:  # forked after the tables exist (rebuilds re-fork)
                 pool = ctx.Pool(cores)
+            t0 = time.perf_counter()
             if reference_parallel_step(st, lsh, batch, it, cfg, cores, pool, ctx):
                 pool.close()
                 pool = None
-                rebuilds[0] += it > args.warmup
+                if it > args.warmup:
+                    rebuilds[0] += 1
+                    rb_s.append(time.perf_counter() - t0)
+            return time.perf_counter() - t0
 
         try:
             for it in range(1, args.warmup + 1):
@@ -601,16 +648,23 @@ def run_reference(args, rank, world):
         finally:
             if pool is not None:
                 pool.close()
+        # the rebuild amortised like the GPU arm's: one timed full build
+        # (hash every W2 row + all L tables) / n0 per step, in place of the
+        # window's own rebuilds (their whole step time is charged, an upper
+        # bound on the build inside it)
+        t0 = time.perf_counter()
+        lsh.build(st.w2)
+        build_s = time.perf_counter() - t0
+    dt = dt - sum(rb_s) + args.steps * build_s / w.n0
     v = args.steps * per_step / dt
-    sample = (f"{args.steps} steps x {per_step} samples of {w.name}, {rebuilds[0]} table rebuild(s) "
-              f"(numpy, serial) in the timed steps")
+    sample = (f"{args.steps} steps x {per_step} samples (the full batch) of {w.name}, snapshot schedule on "
+              f"{cores} processes (numpy), table build {build_s:.2f} s amortised over n0={w.n0} steps")
     return {
         "impl": "reference", "metric": "train samples/sec (LSH-sparse fwd+bwd+Adam), % of HBM roofline, 1/2/4/8 GPU",
         "value": v, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (SURVEY 8(d) Zipf generator)",
-        "config": {"workload": w.name, "batch": w.batch, "schedule": f"snapshot (reference workers={cores})",
-                   "sample": f"{per_step} samples per step (bounded)"},
+        "config": config_of(w, args, world),
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -618,8 +672,24 @@ def run_reference(args, rank, world):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run
+        import socket
+
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")  # the NCCL log shows the ranks and transports used
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd, env=env))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
     if args.impl == "reference":
         if rank != 0:
             return

@@ -137,6 +137,16 @@ int slide_tables_probe(slide_ctx* ctx, const uint32_t* keys, int64_t b, int32_t*
 int slide_query_union(slide_ctx* ctx, const float* q_dev, int64_t n, int64_t n_ids, int64_t cap_stride,
                       int32_t* cnt_out, int32_t* ids_out);
 
+/* samplers.sample on explicit candidate lists (RawCandidates; reference
+ * samplers.py:57-120), for callers holding probed buckets.  Host arrays:
+ * ptr (n_tables + 1) offsets into ids; order (n_tables) the vanilla probe
+ * order (the caller's rng.permutation(L)); ids_out must hold ptr[n_tables]
+ * ids (vanilla: fresh ids in probe order; topk: by frequency desc, id asc,
+ * at most beta; hard_threshold: ascending); freq_out (width) or NULL. */
+int slide_sample_lists(const int32_t* ptr_host, const int32_t* ids_host, int64_t n_tables, int64_t width,
+                       int64_t strategy, int64_t beta, int64_t min_freq, const int32_t* order_host,
+                       int32_t* ids_out, int64_t* n_out, int64_t* probed, int32_t* freq_out, void* stream);
+
 /* -- the step --------------------------------------------------------- */
 /* forward of a (sub-)batch (network.py:241-286, 225-239): hidden layer,
  * query hash, per-slot rng, sampler, fallback, label union, logits,

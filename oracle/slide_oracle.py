@@ -268,6 +268,80 @@ def build_buckets(keys: np.ndarray, cap: int, policy: str, pyrand: random.Random
     return out
 
 
+class BucketTable:
+    """One table in array form: sorted distinct keys, insert counts and a CSR
+    of physical slots -- the same content as a ``build_buckets`` dict (its
+    ``get`` has the dict's result), built without a per-bucket Python loop so
+    the oracle can hold full-size tables (205k - 4M rows x L)."""
+
+    def __init__(self, keys, counts, ptr, slots):
+        self.keys = np.asarray(keys, dtype=np.int64)
+        self.counts = np.asarray(counts, dtype=np.int64)
+        self.ptr = np.asarray(ptr, dtype=np.int64)
+        self.slots = np.asarray(slots, dtype=np.int64)
+
+    def __len__(self):
+        return self.keys.size
+
+    def get(self, key):
+        i = int(np.searchsorted(self.keys, key))
+        if i >= self.keys.size or self.keys[i] != key:
+            return None
+        return self.slots[self.ptr[i] : self.ptr[i + 1]], int(self.counts[i])
+
+    def items(self):
+        for i in range(self.keys.size):
+            yield int(self.keys[i]), (self.slots[self.ptr[i] : self.ptr[i + 1]], int(self.counts[i]))
+
+
+def build_bucket_arrays(keys: np.ndarray, cap: int, policy: str, pyrand: random.Random | None) -> list:
+    """``build_buckets`` (tables.py:127-161) in array form: per table a stable
+    sort by key gives every run of ids in ascending insert order; runs of at
+    most ``cap`` ids are stored whole; an overflowing FIFO run keeps its last
+    ``cap`` inserts at ring slots p % cap; an overflowing reservoir run keeps
+    its first ``cap`` ids and then replays the draws (u1 * count < cap, slot
+    int(u2 * cap)) in (table, id) order, continuing ``pyrand``."""
+    keys = np.asarray(keys, dtype=np.int64)
+    n, n_tables = keys.shape
+    out = []
+    for t in range(n_tables):
+        col = keys[:, t]
+        order = np.argsort(col, kind="stable")
+        sk = col[order]
+        starts = np.flatnonzero(np.r_[True, sk[1:] != sk[:-1]]) if n else np.zeros(0, np.int64)
+        ends = np.r_[starts[1:], n].astype(np.int64)
+        counts = ends - starts
+        kept = np.minimum(counts, cap)
+        ptr = np.zeros(starts.size + 1, dtype=np.int64)
+        np.cumsum(kept, out=ptr[1:])
+        # position of every kept slot inside its run: first `kept` inserts
+        run = np.repeat(np.arange(starts.size), kept)
+        j = np.arange(ptr[-1]) - ptr[run]
+        slots = order[starts[run] + j]
+        over = np.flatnonzero(counts > cap)
+        if over.size and policy == "fifo":
+            for r in over.tolist():
+                cnt = int(counts[r])
+                last = order[starts[r] + cnt - cap : starts[r] + cnt]
+                pos = np.arange(cnt - cap, cnt) % cap
+                seg = np.empty(cap, dtype=np.int64)
+                seg[pos] = last
+                slots[ptr[r] : ptr[r] + cap] = seg
+        elif over.size:
+            # (id, 1-based count, run) of every insert past the cap, id order
+            ev = []
+            for r in over.tolist():
+                for q in range(cap, int(counts[r])):
+                    ev.append((int(order[starts[r] + q]), q + 1, r))
+            ev.sort()
+            rand = pyrand.random
+            for nid, count, r in ev:
+                if rand() * count < cap:
+                    slots[ptr[r] + int(rand() * cap)] = nid
+        out.append(BucketTable(sk[starts], counts, ptr, slots))
+    return out
+
+
 def probe(buckets, keys_row) -> list:
     """Exactly L probes; missing keys give empty lists (tables.py:171-176)."""
     res = []
@@ -369,7 +443,7 @@ class OutputLsh:
 
     def build(self, w2: np.ndarray):
         keys = family_keys(self.params, w2)
-        self.buckets = build_buckets(keys, self.spec.cap, self.spec.policy, self.pyrand)
+        self.buckets = build_bucket_arrays(keys, self.spec.cap, self.spec.policy, self.pyrand)
         return keys
 
     def query(self, h_dense: np.ndarray):
@@ -446,6 +520,10 @@ class SlotGrads:
     dh: np.ndarray | None  # hidden error on nz(h), None if h empty
     x_idx: np.ndarray
     x_val: np.ndarray
+    # |W2[A, nz(h)]|^T |delta|: the magnitude of the terms dh sums (dh cancels
+    # because delta sums to ~0); parity tests scale the hidden layer's fp32
+    # rounding floor by it
+    dh_abs: np.ndarray | None = None
 
 
 def slot_forward(st: NetState, lsh: OutputLsh | None, x_idx, x_val, labels, rng, n_out: int) -> SlotTrace:
@@ -499,10 +577,12 @@ def slot_backward(st: NetState, tr: SlotTrace, labels) -> SlotGrads:
     delta[pos] -= 1.0 / lab.size
     h_idx = np.flatnonzero(tr.h > 0)
     h_val = tr.h[h_idx]
-    dh = None
+    dh = dh_abs = None
     if h_idx.size:
-        dh = st.w2[np.ix_(tr.active, h_idx)].T @ delta
-    return SlotGrads(tr.active, delta, h_idx, h_val, dh, tr.x_idx, tr.x_val)
+        blk = st.w2[np.ix_(tr.active, h_idx)]
+        dh = blk.T @ delta
+        dh_abs = np.abs(blk).T @ np.abs(delta)
+    return SlotGrads(tr.active, delta, h_idx, h_val, dh, tr.x_idx, tr.x_val, dh_abs)
 
 
 def _adam_rows(w, m, v, b, mb, vb, steps, rows, cols, grad, bgrad, cfg: AdamCfg):

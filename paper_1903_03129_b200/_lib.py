@@ -80,6 +80,7 @@ _SIGS = {
     "slide_shard_softmax_finish": [vp, vp, vp, vp],
     "slide_shard_hidden_grad": [vp, vp],
     "slide_shard_update": [vp, vp],
+    "slide_sample_lists": [vp, vp, i64, i64, i64, i64, i64, vp, vp, C.POINTER(i64), C.POINTER(i64), vp, vp],
     "slide_pcg64_seed": [vp, i64, vp],
     "slide_pcg64_permutation": [vp, i64, vp],
     "slide_pcg64_choice": [vp, i64, i64, vp],

@@ -8,6 +8,7 @@ secondary cases.
 
 from __future__ import annotations
 
+import dataclasses
 from dataclasses import dataclass
 
 from .data import CorpusSpec
@@ -57,4 +58,9 @@ SCALED = Workload(
     CorpusSpec(135_909, 4_000_000, ("poisson", 75), 1.1, ("poisson", 5), 1.1, True),
 )
 
-WORKLOADS = {w.name: w for w in (TINY, WIDE_IN, WIDE_OUT, SCALED)}
+# SURVEY 8(d) secondary lines: the API-default beta (one-table regime at
+# wide-in) and the 5% beta at wide-out (fallback-dominated)
+WIDE_IN_B128 = dataclasses.replace(WIDE_IN, name="wide_in_b128", beta=128)
+WIDE_OUT_B5PCT = dataclasses.replace(WIDE_OUT, name="wide_out_b5pct", beta=33_505)
+
+WORKLOADS = {w.name: w for w in (TINY, WIDE_IN, WIDE_OUT, SCALED, WIDE_IN_B128, WIDE_OUT_B5PCT)}

@@ -1310,6 +1310,50 @@ int slide_shard_update(slide_ctx* c, const float* dh) {
   return guarded([&] { backward_impl(c, 1, dh); });
 }
 
+int slide_sample_lists(const int32_t* ptr_host, const int32_t* ids_host, int64_t n_tables, int64_t width,
+                       int64_t strategy, int64_t beta, int64_t min_freq, const int32_t* order_host,
+                       int32_t* ids_out, int64_t* n_out, int64_t* probed, int32_t* freq_out, void* stream) {
+  return guarded([&] {
+    SLIDE_CHECK(n_tables >= 1 && n_tables <= 4096, kValueError, "need 1..4096 candidate lists");
+    SLIDE_CHECK(width >= 1 && width < INT32_MAX, kValueError, "width must be positive");
+    SLIDE_CHECK(strategy >= 0 && strategy <= 2, kValueError, "unknown sampling strategy");
+    SLIDE_CHECK(beta >= 1 && min_freq >= 1, kValueError, "beta and min_freq must be positive");
+    const int64_t n_ids = ptr_host[n_tables];
+    for (int64_t q = 0; q < n_ids; ++q)
+      SLIDE_CHECK(ids_host[q] >= 0 && ids_host[q] < width, kIndexError, "candidate id outside [0, width)");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t words = ceil_div(width, 32);
+    // scratch outside the DBuf pool: no step graph needs re-capturing for it
+    char* base = nullptr;
+    SLIDE_CUDA(cudaMalloc(&base, (n_tables + 1 + n_tables + 2) * 4 + (n_ids + width + 1) * 4 + words * 4 +
+                                     (n_ids + 1) * 4 + 64));
+    struct Free {
+      char* p;
+      ~Free() { cudaFree(p); }
+    } free_base{base};
+    int32_t* d_ptr = reinterpret_cast<int32_t*>(base);
+    int32_t* d_order = d_ptr + n_tables + 1;
+    int32_t* d_res = d_order + n_tables;
+    int32_t* d_ids = d_res + 2;
+    int32_t* d_freq = d_ids + n_ids + 1;
+    uint32_t* d_seen = reinterpret_cast<uint32_t*>(d_freq + width);
+    int32_t* d_out = reinterpret_cast<int32_t*>(d_seen + words);
+    SLIDE_CUDA(cudaMemcpyAsync(d_ptr, ptr_host, (n_tables + 1) * 4, cudaMemcpyHostToDevice, s));
+    if (strategy == 0) SLIDE_CUDA(cudaMemcpyAsync(d_order, order_host, n_tables * 4, cudaMemcpyHostToDevice, s));
+    if (n_ids) SLIDE_CUDA(cudaMemcpyAsync(d_ids, ids_host, n_ids * 4, cudaMemcpyHostToDevice, s));
+    SLIDE_CUDA(cudaMemsetAsync(d_freq, 0, (width + words) * 4, s));
+    launch_sample_lists(d_ptr, d_ids, (int)n_tables, (int)width, (int)strategy, (int)std::min<int64_t>(beta, INT32_MAX),
+                        (int)min_freq, d_order, d_freq, d_seen, d_out, d_res, s);
+    int32_t res[2];
+    SLIDE_CUDA(cudaMemcpyAsync(res, d_res, 8, cudaMemcpyDeviceToHost, s));
+    SLIDE_CUDA(cudaStreamSynchronize(s));
+    if (res[0]) SLIDE_CUDA(cudaMemcpy(ids_out, d_out, (size_t)res[0] * 4, cudaMemcpyDeviceToHost));
+    if (freq_out) SLIDE_CUDA(cudaMemcpy(freq_out, d_freq, (size_t)width * 4, cudaMemcpyDeviceToHost));
+    *n_out = res[0];
+    *probed = res[1];
+  });
+}
+
 int slide_launch_count(uint64_t* out) {
   return guarded([&] { *out = g_slide_launches; });
 }

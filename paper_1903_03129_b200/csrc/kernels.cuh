@@ -46,6 +46,9 @@ void launch_select(const SelectArgs& a, int max_candidates, cudaStream_t s);
 // full-union selection through a shared-memory id bitmap; false if N is too wide
 bool launch_select_union(const SelectArgs& a, int64_t n_out, cudaStream_t s);
 void launch_fallback(const FallbackArgs& a, int b, cudaStream_t s);
+void launch_sample_lists(const int32_t* ptr, const int32_t* ids, int n_tables, int width, int strategy, int beta,
+                         int min_freq, const int32_t* order, int32_t* freq, uint32_t* seen, int32_t* out,
+                         int32_t* result, cudaStream_t s);
 void launch_explicit_active(int b, int64_t n, const int32_t* fptr, const int32_t* fidx, const int32_t* y_ptr,
                             const int32_t* y_idx, int64_t cap_max, int32_t* act, int32_t* cnt, int32_t* empty,
                             cudaStream_t s);

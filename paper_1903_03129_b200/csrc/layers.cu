@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict
     if (inv) dsort[inv[o + k]] = dl;
     if (lab) {
       double nl = -((double)zz - (double)lse);
-      lsum += nl < 690.7755278982137 ? nl : 690.7755278982137;
+      lsum += (nl < 690.7755278982137 || nl != nl) ? nl : 690.7755278982137;  // NaN propagates (np.maximum)
     }
   }
   for (int k = tid + kSmC * 1024; k < n; k += 1024) {
@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict
     if (inv) dsort[inv[o + k]] = dl;  // the W2 Adam reads the errors in row-grouped order
     if (lab) {
       double nl = -((double)zz - (double)lse);
-      lsum += nl < 690.7755278982137 ? nl : 690.7755278982137;
+      lsum += (nl < 690.7755278982137 || nl != nl) ? nl : 690.7755278982137;  // NaN propagates (np.maximum)
     }
   }
   lsum = RD(tmp.d).Sum(lsum);
@@ -1711,7 +1711,7 @@ __global__ void __launch_bounds__(1024) softmax_finish_kernel(const int32_t* __r
     if (inv) dsort[inv[o + k]] = dl;
     if (lab) {
       const double nl = -((double)zz - (double)lse);
-      lsum += nl < 690.7755278982137 ? nl : 690.7755278982137;
+      lsum += (nl < 690.7755278982137 || nl != nl) ? nl : 690.7755278982137;  // NaN propagates (np.maximum)
     }
   }
   lsum = RD(tmp).Sum(lsum);

@@ -612,4 +612,92 @@ void launch_topk(int b, const int32_t* offs, const int32_t* rows, int shard_coun
   SLIDE_LAUNCH_CHECK();
 }
 
+// ------------------------------------------------- sampler on explicit lists
+// samplers.sample (reference samplers.py:57-120) on caller-held candidate
+// lists (RawCandidates): one CTA walks the L lists.  vanilla: the lists in
+// `order` (the caller's rng.permutation(L)), whole lists, fresh ids appended
+// in list order (a block scan keeps it), stop once >= beta distinct ids
+// (checked after every list, empty ones included); freq counts the probed
+// lists.  topk: freq over all lists, ids by (freq desc, id asc), first beta.
+// hard_threshold: ids with freq >= min_freq ascending.  freq / seen are
+// zeroed by the caller.
+constexpr int kSampleThreads = 1024;
+
+__global__ void __launch_bounds__(kSampleThreads) sample_lists_kernel(
+    const int32_t* __restrict__ ptr, const int32_t* __restrict__ ids, int n_tables, int width, int strategy,
+    int beta, int min_freq, const int32_t* __restrict__ order, int32_t* __restrict__ freq,
+    uint32_t* __restrict__ seen, int32_t* __restrict__ out, int32_t* __restrict__ result) {
+  using Scan = cub::BlockScan<int, kSampleThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int s_n;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_n = 0;
+  __syncthreads();
+  if (strategy == 0) {
+    int probed = 0;
+    for (int k = 0; k < n_tables; ++k) {
+      const int t = order[k];
+      ++probed;
+      const int a = ptr[t], e = ptr[t + 1];
+      for (int q0 = a; q0 < e; q0 += kSampleThreads) {
+        const int q = q0 + tid;
+        int fresh = 0, id = 0;
+        if (q < e) {
+          id = ids[q];
+          atomicAdd(&freq[id], 1);
+          const uint32_t bit = 1u << (id & 31);
+          fresh = (atomicOr(&seen[id >> 5], bit) & bit) == 0;
+        }
+        int pos, total;
+        Scan(tmp).ExclusiveSum(fresh, pos, total);
+        if (fresh) out[s_n + pos] = id;
+        __syncthreads();
+        if (tid == 0) s_n += total;
+        __syncthreads();
+      }
+      if (s_n >= beta) break;
+    }
+    if (tid == 0) {
+      result[0] = s_n;
+      result[1] = probed;
+    }
+    return;
+  }
+  for (int t = 0; t < n_tables; ++t)
+    for (int q = ptr[t] + tid; q < ptr[t + 1]; q += kSampleThreads) atomicAdd(&freq[ids[q]], 1);
+  __syncthreads();
+  // ordered compaction of the ids whose freq satisfies `pred`, ascending
+  auto compact = [&](int lo, int hi, int limit) {
+    for (int c0 = 0; c0 < width; c0 += kSampleThreads) {
+      const int c = c0 + tid;
+      const int f = c < width ? freq[c] : 0;
+      const int take = f >= lo && f <= hi;
+      int pos, total;
+      Scan(tmp).ExclusiveSum(take, pos, total);
+      if (take && s_n + pos < limit) out[s_n + pos] = c;
+      __syncthreads();
+      if (tid == 0) s_n = min(limit, s_n + total);
+      __syncthreads();
+      if (s_n >= limit) break;
+    }
+  };
+  if (strategy == 2) {
+    compact(min_freq, n_tables, width);
+  } else {
+    for (int f = n_tables; f >= 1 && s_n < beta; --f) compact(f, f, beta);
+  }
+  if (tid == 0) {
+    result[0] = s_n;
+    result[1] = n_tables;
+  }
+}
+
+void launch_sample_lists(const int32_t* ptr, const int32_t* ids, int n_tables, int width, int strategy, int beta,
+                         int min_freq, const int32_t* order, int32_t* freq, uint32_t* seen, int32_t* out,
+                         int32_t* result, cudaStream_t s) {
+  sample_lists_kernel<<<1, kSampleThreads, 0, s>>>(ptr, ids, n_tables, width, strategy, beta, min_freq, order, freq,
+                                                   seen, out, result);
+  SLIDE_LAUNCH_CHECK();
+}
+
 }  // namespace slide

@@ -1,8 +1,13 @@
-"""Batches, the BASELINE synthetic corpora and P@k.
+"""Corpora, batches, the BASELINE synthetic corpora and P@k.
 
+* ``Dataset`` / ``load_xc_file`` / ``save_xc_file`` are the reference's
+  extreme-classification corpus carrier and text format (reference
+  data.py:1-115): a header ``N d L`` then one ``l1,l2 i1:v1 i2:v2`` line per
+  example; malformed content raises ``DatasetFormatError`` naming the line.
 * ``batches`` restates the seeded epoch shuffle of the reference
   (reference data.py:118-123): ``default_rng(seed).permutation(n)`` cut into
-  batches, the last one possibly short.
+  batches of examples, the last one possibly short; ``batch_indices`` is the
+  same order as row indices (for CSR corpora).
 * ``precision_at_k`` restates reference data.py:126-133.
 * ``synthetic_corpus`` is the generator of SURVEY.md section 8(d) that stands
   in for Delicious-200K / Amazon-670K (not in the container): bounded Zipf
@@ -90,13 +95,154 @@ def corpus_from_examples(examples, num_features: int, num_labels: int) -> Corpus
                   np.asarray(y_ptr, np.int64), cat(yi, np.int32), num_features, num_labels)
 
 
-def batches(n_examples: int, batch_size: int, seed):
-    """Row-index batches of one epoch (reference data.py:118-123)."""
-    if not isinstance(batch_size, (int, np.integer)) or batch_size < 1:
+class DatasetFormatError(ValueError):
+    """Malformed corpus file; the message carries the offending line number
+    (reference data.py:20-21)."""
+
+
+@dataclass
+class Dataset:
+    """(SparseVector, frozenset labels) examples plus the feature and label
+    dimensions (reference data.py:24-47)."""
+
+    examples: list
+    num_features: int
+    num_labels: int
+
+    def __len__(self) -> int:
+        return len(self.examples)
+
+    def validate(self) -> "Dataset":
+        if not self.examples:
+            raise ValueError("dataset must contain at least one example")
+        for x, labels in self.examples:
+            x.validate()
+            if x.dim != self.num_features:
+                raise ValueError("feature dim mismatch")
+            if labels and (min(labels) < 0 or max(labels) >= self.num_labels):
+                raise ValueError("label out of range")
+        return self
+
+    def to_corpus(self) -> "Corpus":
+        """CSR form (float32 values) -- what the device step consumes."""
+        return corpus_from_examples(self.examples, self.num_features, self.num_labels)
+
+
+def _bad(line_no: int, msg: str):
+    raise DatasetFormatError(f"line {line_no}: {msg}")
+
+
+def _parse_labels(tok: str, line_no: int, n_labels: int) -> frozenset:
+    if not tok:
+        return frozenset()
+    if ":" in tok:
+        _bad(line_no, "feature token found where labels belong")
+    out = set()
+    for part in tok.split(","):
+        try:
+            lab = int(part)
+        except ValueError:
+            _bad(line_no, f"non-integer label {part!r}")
+        if lab < 0 or lab >= n_labels:
+            _bad(line_no, f"label {lab} outside [0, {n_labels})")
+        out.add(lab)
+    return frozenset(out)
+
+
+def _parse_features(toks, line_no: int, dim: int) -> SparseVector:
+    pairs = []
+    for tok in toks:
+        i_s, colon, v_s = tok.partition(":")
+        if not colon:
+            _bad(line_no, f"feature token {tok!r} is not 'index:value'")
+        try:
+            i, v = int(i_s), float(v_s)
+        except ValueError:
+            _bad(line_no, f"non-numeric feature token {tok!r}")
+        if not np.isfinite(v):
+            _bad(line_no, f"non-finite feature value {tok!r}")
+        if i < 0 or i >= dim:
+            _bad(line_no, f"feature index {i} outside [0, {dim})")
+        if v != 0.0:  # explicit zeros are dropped on parse
+            pairs.append((i, v))
+    return SparseVector.from_pairs(pairs, dim)
+
+
+def load_xc_file(path) -> Dataset:
+    """Parse an extreme-classification corpus file (reference data.py:51-103):
+    header ``N d L`` (positive integers), then exactly N example lines
+    ``labels features`` -- labels comma-separated (may be empty), features
+    ``index:value`` tokens (may be absent); trailing blank lines are allowed.
+    Errors raise ``DatasetFormatError`` with the 1-based line number."""
+    with open(path, "r", encoding="utf-8", newline=None) as fh:
+        head = fh.readline()
+        if not head.strip():
+            _bad(1, "missing header 'N d L'")
+        fields = head.split()
+        if len(fields) != 3:
+            _bad(1, f"header must be 'N d L', got {head.strip()!r}")
+        try:
+            n, dim, n_labels = (int(f) for f in fields)
+        except ValueError:
+            _bad(1, f"non-integer header field in {head.strip()!r}")
+        if min(n, dim, n_labels) < 1:
+            _bad(1, "header counts must be positive")
+        examples = []
+        line_no = 1
+        for line_no, line in enumerate(fh, start=2):
+            line = line.rstrip("\r\n")
+            if len(examples) == n:
+                if not line.strip():
+                    continue
+                _bad(line_no, f"more than the declared {n} examples")
+            lab_tok, _, rest = line.partition(" ")
+            labels = _parse_labels(lab_tok, line_no, n_labels)
+            examples.append((_parse_features(rest.split(), line_no, dim), labels))
+        if len(examples) != n:
+            _bad(line_no if examples else 1, f"expected {n} examples, found {len(examples)}")
+    return Dataset(examples, dim, n_labels)
+
+
+def save_xc_file(ds: Dataset, path) -> None:
+    """Write ``ds`` in the format ``load_xc_file`` reads (reference
+    data.py:106-115); values are written with ``repr`` so a reload is equal."""
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write(f"{len(ds.examples)} {ds.num_features} {ds.num_labels}\n")
+        for x, labels in ds.examples:
+            head = ",".join(str(v) for v in sorted(labels))
+            feats = " ".join(f"{i}:{v!r}" for i, v in zip(x.indices.tolist(), x.values.tolist()))
+            fh.write((f"{head} {feats}".rstrip() if feats else head) + "\n")
+
+
+def l2_normalize(ds: Dataset) -> Dataset:
+    """Every example's features scaled to unit L2 norm (reference data.py:136-141)."""
+    return Dataset([(x.l2_normalized(), labels) for x, labels in ds.examples], ds.num_features, ds.num_labels)
+
+
+def _check_batch_size(batch_size):
+    if not isinstance(batch_size, (int, np.integer)) or isinstance(batch_size, bool) or batch_size < 1:
         raise ValueError(f"batch_size must be a positive integer, got {batch_size!r}")
+
+
+def batch_indices(n_examples: int, batch_size: int, seed):
+    """Row-index batches of one epoch in ``batches``' order (CSR corpora)."""
+    _check_batch_size(batch_size)
     order = np.random.default_rng(seed).permutation(n_examples)
     for lo in range(0, len(order), batch_size):
         yield order[lo : lo + batch_size]
+
+
+def batches(ds, batch_size: int, seed):
+    """Seeded epoch shuffle cut into batches of examples, the last possibly
+    short (reference data.py:118-123).  ``ds`` is a ``Dataset`` (lists of
+    (SparseVector, labels) pairs, as the reference yields) or a CSR
+    ``Corpus`` (batches are sub-corpora)."""
+    if isinstance(ds, Corpus):
+        for rows in batch_indices(len(ds), batch_size, seed):
+            yield ds.subset(rows)
+        return
+    for rows in batch_indices(len(ds.examples), batch_size, seed):
+        yield [ds.examples[i] for i in rows]
 
 
 def score_precision_at_k(net, examples, k: int = 1, seed: int = 0) -> float:

@@ -285,6 +285,12 @@ class HostCsr:
     def batch(self) -> int:
         return len(self.x_ptr) - 1
 
+    @staticmethod
+    def from_corpus(corpus) -> "HostCsr":
+        """A ``data.Corpus`` (int64 offsets) as one batch."""
+        return HostCsr(corpus.x_ptr.astype(np.int32), corpus.x_idx, corpus.x_val, corpus.y_ptr.astype(np.int32),
+                       corpus.y_idx)
+
 
 def csr_from_batch(batch, input_dim: int, n_out: int) -> HostCsr:
     xp, yp = [0], [0]
@@ -812,18 +818,27 @@ class SlideNetwork:
 
 
 def train_network(net: SlideNetwork, dataset, *, workers: int = 1, on_batch=None, schedule: str | None = None) -> int:
-    """Epochs over a dataset (reference network.py:398-425): seeded shuffle per
-    epoch, divergence guard, on_batch callback."""
+    """Run the configured epochs over a dataset (reference network.py:398-425):
+    batches in the seeded order ``data.batches(dataset, B, seed=(seed,
+    epoch))``, the iteration counter running across epochs, a non-finite
+    loss raising ``TrainingDivergedError``, ``on_batch(iteration, stats)``
+    after every batch (raise from it to stop early).  ``dataset`` is a
+    ``data.Dataset`` or a CSR ``data.Corpus`` (same order; batches go to the
+    device without building SparseVectors).  Returns the iterations run."""
+    from .data import Corpus, batches
+
     check_positive_int(workers, "workers")
     cfg = net.cfg
+    if schedule is None:
+        schedule = "sequential" if workers <= 1 else "snapshot"
     iteration = 0
-    examples = dataset.examples
     for epoch in range(cfg.epochs):
-        order = np.random.default_rng((cfg.seed, epoch)).permutation(len(examples))
-        for lo in range(0, len(order), cfg.batch_size):
-            batch = [examples[i] for i in order[lo : lo + cfg.batch_size]]
+        for batch in batches(dataset, cfg.batch_size, seed=(cfg.seed, epoch)):
             iteration += 1
-            stats = net.train_batch(batch, iteration, workers=workers, schedule=schedule)
+            if isinstance(dataset, Corpus):
+                stats = net.train_batch_csr(HostCsr.from_corpus(batch), iteration, schedule=schedule)
+            else:
+                stats = net.train_batch(batch, iteration, workers=workers, schedule=schedule)
             if not np.isfinite(stats.loss):
                 raise TrainingDivergedError(f"non-finite loss {stats.loss} at iteration {iteration}")
             if on_batch is not None:
@@ -836,7 +851,11 @@ def train_network(net: SlideNetwork, dataset, *, workers: int = 1, on_batch=None
 
 def save_checkpoint(net: SlideNetwork, path, with_adam: bool = True):
     """Little-endian SLDE v1: per layer width, fan_in, kind, f32 w / b, adam
-    flag and f32 moments + u64 steps (reference network.py:478-499)."""
+    flag and f32 moments + u64 steps (reference network.py:478-499).  The
+    bytes equal the reference's for the same float32 state."""
+    if net.shard_count > 1:
+        raise NotImplementedError("save_checkpoint of a column-sharded network: gather the output layer first "
+                                  "(sharded.gather_output_layer)")
     with open(path, "wb") as fh:
         fh.write(CHECKPOINT_MAGIC)
         fh.write(struct.pack("<II", CHECKPOINT_VERSION, len(net.layers)))

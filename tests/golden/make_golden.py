@@ -326,12 +326,127 @@ def tiny_config():
     save("tiny_config.npz", **out)
 
 
+def tiny_run():
+    """The BASELINE tiny config (configs[0]) end to end: 200 steps of the
+    reference's ``train_network`` (workers=1, the sequential schedule; epoch
+    order ``default_rng((seed, 0))``) over 200 x 128 synthetic examples, per-step
+    losses / active fractions / rebuild flags, then P@1 on a held-out stream
+    from the same generator with the evaluator's shared ``default_rng(seed)``
+    (reference estimator.py:203-223).  The same 200 batches are also run
+    through the snapshot schedule built from reference functions
+    (``snapshot_step``) for the snapshot-vs-sequential P@1 report."""
+    from slide.data import Dataset, precision_at_k
+    from slide.network import train_network
+
+    w = TINY
+    n_train, n_eval = 200 * w.batch, 4000
+    corpus = synthetic_corpus(w.corpus, n_train, seed=0)
+    held = synthetic_corpus(w.corpus, n_eval, seed=1)
+    train = [corpus.example(i) for i in range(n_train)]
+    evals = [held.example(i) for i in range(n_eval)]
+    out = {"corpus_check": np.array([corpus.x_idx.astype(np.int64).sum(), corpus.y_idx.astype(np.int64).sum(),
+                                     held.x_idx.astype(np.int64).sum(), held.y_idx.astype(np.int64).sum()]),
+           "corpus_vsum": np.array([corpus.x_val.astype(np.float64).sum(), held.x_val.astype(np.float64).sum()])}
+
+    def make():
+        cfg = TrainConfig(batch_size=w.batch, seed=0, learning_rate=w.lr, n0=w.n0, decay=w.decay)
+        lsh = LshLayerConfig("simhash", k=w.k, l=w.l, capacity=w.cap, sampler=SamplerConfig("vanilla", beta=w.beta))
+        return SlideNetwork(w.input_dim, [w.hidden, w.n_out], cfg, lsh_layers={1: lsh})
+
+    def p_at_1(net):
+        rng = np.random.default_rng(0)
+        return float(np.mean([precision_at_k(net.predict(x, rng=rng)[:1], y, 1) for x, y in evals]))
+
+    # sequential: the reference's own train_network
+    net = make()
+    log = []
+    train_network(net, Dataset(train, w.input_dim, w.n_out),
+                  on_batch=lambda it, st: log.append((st.loss, st.active_fraction[1], bool(st.rebuilt))))
+    assert len(log) == 200
+    out["seq_loss"] = np.array([r[0] for r in log])
+    out["seq_frac"] = np.array([r[1] for r in log])
+    out["seq_rebuilt"] = np.array([r[2] for r in log])
+    out["seq_p1"] = np.array([p_at_1(net)])
+    out["seq_final_w2_head"] = net.layers[1].w[:16].copy()
+    print("sequential P@1", out["seq_p1"])
+    # snapshot schedule over the same batches in the same order
+    net = make()
+    order = np.random.default_rng((0, 0)).permutation(n_train)
+    losses = []
+    for it in range(1, 201):
+        batch = [train[i] for i in order[(it - 1) * w.batch : it * w.batch]]
+        losses.append(snapshot_step(net, batch, it))
+    out["snap_loss"] = np.array(losses)
+    out["snap_p1"] = np.array([p_at_1(net)])
+    print("snapshot P@1", out["snap_p1"])
+    save("tiny_run.npz", **out)
+
+
+from tests.golden.make_golden_data import XC_BAD, XC_GOOD  # noqa: E402
+
+
+def data_io():
+    """The reference's XC corpus parser on a file exercising CRLF, empty
+    label lists, missing feature tails, explicit zeros and trailing blank
+    lines, its writer on the result, and its error message for each
+    malformed file (reference data.py:51-115)."""
+    import tempfile
+
+    from slide.data import DatasetFormatError, load_xc_file, save_xc_file
+
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "good.txt")
+        with open(path, "w", newline="") as fh:
+            fh.write(XC_GOOD)
+        ds = load_xc_file(path)
+        out["good_header"] = np.array([len(ds.examples), ds.num_features, ds.num_labels])
+        for i, (x, labels) in enumerate(ds.examples):
+            out[f"good_{i}_idx"] = x.indices
+            out[f"good_{i}_val"] = x.values
+            out[f"good_{i}_labels"] = np.array(sorted(labels), dtype=np.int64)
+        save_xc_file(ds, os.path.join(d, "saved.txt"))
+        out["saved_text"] = np.frombuffer(open(os.path.join(d, "saved.txt"), "rb").read(), dtype=np.uint8)
+        for name, text in XC_BAD.items():
+            bp = os.path.join(d, name + ".txt")
+            with open(bp, "w", newline="") as fh:
+                fh.write(text)
+            try:
+                load_xc_file(bp)
+                msg = "<no error>"
+            except DatasetFormatError as e:
+                msg = str(e)
+            out["bad_" + name] = np.array(msg)
+    save("data_io.npz", **out)
+
+
+def checkpoint():
+    """SLDE v1 bytes written by the reference's save_checkpoint (with and
+    without Adam state) for a small LSH net after two sequential steps whose
+    state was rounded to float32 (reference network.py:478-499)."""
+    import tempfile
+
+    from slide.network import save_checkpoint
+
+    cfg = TrainConfig(batch_size=6, seed=3, learning_rate=1e-2, n0=2)
+    lsh = LshLayerConfig("simhash", k=3, l=6, capacity=8, sampler=SamplerConfig("vanilla", beta=10))
+    net = SlideNetwork(50, [16, 40], cfg, lsh_layers={1: lsh})
+    rng = np.random.default_rng(99)
+    for it in (1, 2):
+        net.train_batch(batch_from(rng, 6, 50, 40), it)
+    to_f32(net)
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        for adam in (True, False):
+            path = os.path.join(d, "ck.slde")
+            save_checkpoint(net, path, with_adam=adam)
+            out["adam" if adam else "plain"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+    save("checkpoint.npz", **out)
+
+
 if __name__ == "__main__":
     assert slide.__version__ == "0.1.0"
-    rng_streams()
-    mt19937()
-    hashing()
-    tables()
-    samplers()
-    network()
-    tiny_config()
+    which = sys.argv[1:] or ["rng_streams", "mt19937", "hashing", "tables", "samplers", "network", "tiny_config",
+                             "tiny_run", "data_io", "checkpoint"]
+    for name in which:
+        globals()[name]()

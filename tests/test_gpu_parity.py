@@ -26,7 +26,12 @@ from paper_1903_03129_b200 import (  # noqa: E402
     new_hash_family,
 )
 from paper_1903_03129_b200.network import HostCsr, csr_from_batch  # noqa: E402
-from tests.parity_util import assert_state_close, oracle_lsh_from_net, oracle_state_from_net  # noqa: E402
+from tests.parity_util import (  # noqa: E402
+    assert_step_state_close,
+    oracle_lsh_from_net,
+    oracle_state_from_net,
+    teacher_forced_step,
+)
 
 HASH_SPECS = {
     "sh_main": dict(family="simhash", k_per_table=9, num_tables=50, dim=128, seed=7919 * 2),
@@ -146,8 +151,6 @@ def test_full_union_vanilla_matches_oracle(family):
                           sampler=SamplerConfig("vanilla", beta=100))
     cfg = TrainConfig(batch_size=B, seed=4, learning_rate=1e-2, n0=2)
     net = SlideNetwork(D, [H, N], cfg, lsh_layers={1: spec})
-    st = oracle_state_from_net(net)
-    lsh = oracle_lsh_from_net(net, spec, st)
     for it in (1, 2, 3):
         batch = []
         for _ in range(B):
@@ -155,11 +158,8 @@ def test_full_union_vanilla_matches_oracle(family):
             vals = (np.abs(rng.standard_normal(idx.size)) + 0.1).astype(np.float32).astype(np.float64)
             batch.append((SparseVector(idx, vals, D), set(rng.choice(N, size=2, replace=False).tolist())))
         trip = [(x.indices, x.values, sorted(y)) for x, y in batch]
-        want = O.train_step(st, lsh, trip, it, cfg.seed, N, O.AdamCfg(lr=1e-2), mode="snapshot")
-        got = net.train_batch(batch, it, schedule="snapshot")
-        assert got.loss == pytest.approx(float(np.mean(want.losses)), rel=1e-5)
+        want, got, _ = teacher_forced_step(net, trip, it, "snapshot", 1e-2, what=f"full-union {family} it{it}")
         assert got.active_fraction[1] == pytest.approx(want.active_fraction, rel=1e-12)
-        assert_state_close(net, st, what=f"full-union {family} it{it}")
 
 
 @pytest.mark.parametrize("shape", ["sparse", "mixed", "dense"])
@@ -174,8 +174,6 @@ def test_dense_and_sparse_tiles_match_oracle(shape):
     spec = LshLayerConfig("simhash", k=2, l=l, capacity=cap, sampler=SamplerConfig("vanilla", beta=beta))
     cfg = TrainConfig(batch_size=B, seed=6, learning_rate=1e-2, n0=2)
     net = SlideNetwork(D, [H, N], cfg, lsh_layers={1: spec})
-    st = oracle_state_from_net(net)
-    lsh = oracle_lsh_from_net(net, spec, st)
     for it in (1, 2, 3):
         trip = []
         for _ in range(B):
@@ -184,11 +182,8 @@ def test_dense_and_sparse_tiles_match_oracle(shape):
             # Zipf-ish labels: a few hot rows held by most samples, a long tail
             lab = sorted(set(int(v) % N for v in rng.zipf(1.3, size=3)))
             trip.append((idx, vals, lab))
-        want = O.train_step(st, lsh, trip, it, cfg.seed, N, O.AdamCfg(lr=1e-2), mode="snapshot")
-        got = net.train_batch([(SparseVector(xi, xv, D), set(y)) for xi, xv, y in trip], it, schedule="snapshot")
-        assert got.loss == pytest.approx(float(np.mean(want.losses)), rel=1e-5)
+        want, got, _ = teacher_forced_step(net, trip, it, "snapshot", 1e-2, what=f"{shape} it{it}")
         assert got.active_fraction[1] == pytest.approx(want.active_fraction, rel=1e-12)
-        assert_state_close(net, st, what=f"{shape} it{it}", adam_lr=1e-2)
 
 
 def _golden_batch(g, name, it, B):
@@ -199,26 +194,21 @@ def _golden_batch(g, name, it, B):
 @pytest.mark.parametrize("mode", ["sequential", "snapshot"])
 @pytest.mark.parametrize("name", sorted(NET_SETUPS))
 def test_train_steps_match_oracle(golden, name, mode):
-    """Three steps (a rebuild after step 2, an empty input in step 2) from the
-    same f32 state: active sets exact, loss 1e-5, state 1e-4."""
+    """Three steps (a rebuild after step 2, an empty input in step 2), each
+    teacher-forced from the device's state: per-slot active sets exact,
+    probabilities and loss 1e-5, every state tensor (hidden bias moments
+    included) under the per-coordinate 1e-4 model, rebuilt tables exact."""
     g = golden("network")
     D, H, N, spec, B, n0 = NET_SETUPS[name]
     cfg = TrainConfig(batch_size=B, seed=3, learning_rate=1e-2, n0=n0)
     net = SlideNetwork(D, [H, N], cfg, lsh_layers={1: spec} if spec else None)
     st = oracle_state_from_net(net)
-    lsh = oracle_lsh_from_net(net, spec, st) if spec else None
     # the f32 initial weights equal the reference's f64 draws rounded
     np.testing.assert_allclose(st.w2, g[f"{name}_init_l1_w"], rtol=1e-7, atol=0)
-    acfg = O.AdamCfg(lr=1e-2)
     for it in range(1, 4):
         trip = _golden_batch(g, name, it, B)
-        want = O.train_step(st, lsh, trip, it, cfg.seed, N, acfg, mode=mode)
-        batch = [(SparseVector(xi, xv, D), set(y)) for xi, xv, y in trip]
-        # capture the device active sets through a readout after each step
-        got = net.train_batch(batch, it, schedule=mode)
-        assert got.loss == pytest.approx(float(np.mean(want.losses)), rel=1e-5)
-        assert got.rebuilt == ([1] if (spec and want.rebuilt) else [])
-        assert_state_close(net, st, what=f"{name} {mode} it{it}")
+        want, stats, _ = teacher_forced_step(net, trip, it, mode, 1e-2, what=f"{name} {mode} it{it}")
+        assert stats.rebuilt == ([1] if (spec and it % n0 == 0) else [])
 
 
 def _stage_forward(net, csr, iteration):
@@ -276,8 +266,10 @@ def test_tiny_config_stage_by_stage():
     # full snapshot step
     _lib.call("slide_backward", net._ctx, 1)
     torch.cuda.synchronize()
-    O.train_step(st, lsh, trip, 1, 0, w.n_out, O.AdamCfg(lr=w.lr), mode="snapshot")
-    assert_state_close(net, st, what="tiny snapshot")
+    st_pre = st.copy()
+    lsh.schedule = O.Schedule(1 << 40)
+    want = O.train_step(st, lsh, trip, 1, 0, w.n_out, O.AdamCfg(lr=w.lr), mode="snapshot")
+    assert_step_state_close(net, st, st_pre, want, O.AdamCfg(lr=w.lr), what="tiny snapshot")
 
 
 def test_forward_emulates_the_callers_generator():
@@ -357,23 +349,17 @@ def test_empty_input_and_dead_hidden_layer_match_oracle():
     spec = LshLayerConfig("simhash", k=2, l=3, capacity=4, sampler=SamplerConfig(beta=5))
     net = SlideNetwork(10, [6, 20], cfg, lsh_layers={1: spec})
     net.layers[0].b[:] = np.array([0.3, -5.0, 0.2, -5.0, 0.1, 0.4])
-    st = oracle_state_from_net(net)
-    lsh = oracle_lsh_from_net(net, spec, st)
     batch = [(SparseVector(np.empty(0, np.int64), np.empty(0), 10), {1}),
              (SparseVector(np.array([2, 5]), np.array([1.0, 0.5]), 10), {3, 4}),
              (SparseVector(np.array([7]), np.array([0.25]), 10), {19})]
     trip = [(x.indices, x.values, sorted(y)) for x, y in batch]
     for it, mode in ((1, "snapshot"), (2, "sequential")):
-        want = O.train_step(st, lsh, trip, it, cfg.seed, 20, O.AdamCfg(lr=1e-2), mode=mode)
-        got = net.train_batch(batch, it, schedule=mode)
-        assert got.loss == pytest.approx(float(np.mean(want.losses)), rel=1e-5)
-        assert_state_close(net, st, what=f"edge {mode}")
+        teacher_forced_step(net, trip, it, mode, 1e-2, what=f"edge {mode}")
     # all hidden units dead: only output biases move, hidden layer untouched
     net.layers[0].b[:] = -50.0
-    st = oracle_state_from_net(net)
-    want = O.train_step(st, lsh, trip, 3, cfg.seed, 20, O.AdamCfg(lr=1e-2), mode="snapshot")
-    net.train_batch(batch, 3, schedule="snapshot")
-    assert_state_close(net, st, what="dead hidden")
+    w1 = np.array(net.layers[0].w)
+    teacher_forced_step(net, trip, 3, "snapshot", 1e-2, what="dead hidden")
+    np.testing.assert_array_equal(np.array(net.layers[0].w), w1)
 
 
 def test_snapshot_step_is_deterministic():
@@ -574,13 +560,10 @@ def test_live_unit_permutation_tracks_the_batch(alive):
         b[np.random.default_rng(3).choice(w.hidden, 36, replace=False)] = 0.5
     net.layers[0].b[:] = b
     hp = net.hidden_pad
-    lsh = oracle_lsh_from_net(net, spec)  # the tables as built at construction (no rebuild in these steps)
     for it in range(1, 4):
         sub = corpus.subset(np.arange((it - 1) * 64, it * 64))
-        csr = HostCsr(sub.x_ptr.astype(np.int32), sub.x_idx, sub.x_val, sub.y_ptr.astype(np.int32), sub.y_idx)
-        st = oracle_state_from_net(net)  # teacher forcing: each step from the device's own state
-        O.train_step(st, lsh, sub.triples(), it, 0, w.n_out, O.AdamCfg(lr=w.lr), mode="snapshot")
-        net.train_batch_csr(csr, it, schedule="snapshot")
+        # teacher forcing: each step from the device's own state
+        teacher_forced_step(net, sub.triples(), it, "snapshot", w.lr, what=f"live-unit step {it}")
         h = net._read(0, 64 * hp, np.float32).reshape(64, hp)
         live = net._read(13, 1 + hp, np.int32)
         on = np.flatnonzero((h > 0).any(0))
@@ -591,4 +574,3 @@ def test_live_unit_permutation_tracks_the_batch(alive):
         np.testing.assert_array_equal(live[1:1 + n], on)
         np.testing.assert_array_equal(np.sort(live[1:]), np.arange(hp))
         assert np.all(np.diff(live[1 + n:]) > 0)
-        assert_state_close(net, st, what=f"live-unit step {it}")

@@ -12,7 +12,7 @@ import pytest
 from paper_1903_03129_b200 import _lib
 from paper_1903_03129_b200.hashing import HashFamilyConfig, _mix, _mix_many, pack_subcodes
 from paper_1903_03129_b200.network import LshLayerConfig, TrainConfig
-from paper_1903_03129_b200.samplers import SamplerConfig, sample
+from paper_1903_03129_b200.samplers import SamplerConfig
 from paper_1903_03129_b200.tables import RawCandidates, RebuildSchedule
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -131,18 +131,6 @@ def test_schedule_values():
     assert got == [50, 105, 166, 234]
     with pytest.raises(ValueError):
         RebuildSchedule(50, -1.0)
-
-
-def test_host_sampler_helper_matches_golden(golden):
-    g = golden("samplers")
-    off = 0
-    for case, (strat, beta, mf, L) in enumerate(g["cases"].tolist()):
-        per_table = [g[f"c{case}_t{t}"].tolist() for t in range(L)]
-        cfg = SamplerConfig(["vanilla", "topk", "hard_threshold"][strat], beta=beta, min_freq=mf)
-        rep = sample(RawCandidates(per_table, 200), cfg, np.random.default_rng((case, 1, 2)))
-        n = g["lens"][case]
-        np.testing.assert_array_equal(np.sort(rep.active_ids), g["ids"][off : off + n])
-        off += n
 
 
 def test_reference_arm_parallel_step_equals_serial_snapshot():

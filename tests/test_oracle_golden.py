@@ -79,6 +79,35 @@ def test_dwta_reservoir_build(golden):
     assert _tables_from_oracle(b) == _tables_from_golden(g, "dwta_")
 
 
+def _tables_from_arrays(tables):
+    return {(t, k): (v[0].tolist(), v[1]) for t, tbl in enumerate(tables) for k, v in tbl.items()}
+
+
+@pytest.mark.parametrize("policy", ["fifo", "reservoir"])
+def test_array_bucket_build_equals_dict_build(golden, policy):
+    """The array-form builder the oracle's OutputLsh uses (full-size tables)
+    holds exactly the reference-pinned dict builder's buckets, physical slot
+    order and reservoir draws included (golden overflow case, two builds on
+    one stream, plus a random many-overflow case)."""
+    g = golden("tables")
+    p = O.simhash_params(24, 2, 5, 1 / 3, 5)
+    w = g[policy + "_w"]
+    ra, rd = random.Random(104729 * 2), random.Random(104729 * 2)
+    for ws in (w, w[::-1].copy()):
+        keys = O.simhash_keys(p, ws)
+        a = O.build_bucket_arrays(keys, 16, policy, ra)
+        assert _tables_from_arrays(a) == _tables_from_oracle(O.build_buckets(keys, 16, policy, rd))
+    assert _tables_from_arrays(O.build_bucket_arrays(O.simhash_keys(p, w), 16, policy,
+                                                     random.Random(104729 * 2))) == _tables_from_golden(g, f"{policy}_b1_")
+    keys = np.random.default_rng(5).integers(0, 7, size=(500, 3))
+    ra, rd = random.Random(9), random.Random(9)
+    assert _tables_from_arrays(O.build_bucket_arrays(keys, 5, policy, ra)) == _tables_from_oracle(
+        O.build_buckets(keys, 5, policy, rd))
+    assert ra.random() == rd.random()
+    empty = O.build_bucket_arrays(np.zeros((0, 2), np.int64), 4, policy, ra)
+    assert [len(t) for t in empty] == [0, 0] and empty[0].get(3) is None
+
+
 def test_samplers_match_reference(golden):
     g = golden("samplers")
     off = 0
@@ -176,3 +205,36 @@ def test_schedule_values():
     assert got == [50, 105, 166, 234]
     s = O.Schedule(50, 0.0)
     assert [s.next_at, (s.advance(), s.next_at)[1]] == [50, 100]
+
+
+def test_tiny_baseline_config_200_steps_and_precision_at_1(golden):
+    """BASELINE configs[0] end to end: the reference's train_network
+    (sequential, workers=1) for 200 steps -- four table rebuilds -- then P@1
+    on a 4,000-example held-out stream with the evaluator's shared
+    default_rng(seed).  The oracle reproduces every step's loss, the rebuild
+    flags and the final P@1 exactly."""
+    g = golden("tiny_run")
+    w = TINY
+    corpus = synthetic_corpus(w.corpus, 200 * w.batch, seed=0)
+    held = synthetic_corpus(w.corpus, 4000, seed=1)
+    np.testing.assert_array_equal(
+        [corpus.x_idx.astype(np.int64).sum(), corpus.y_idx.astype(np.int64).sum(),
+         held.x_idx.astype(np.int64).sum(), held.y_idx.astype(np.int64).sum()], g["corpus_check"])
+    st = O.init_state(w.input_dim, w.hidden, w.n_out, seed=0)
+    spec = O.LshSpec("simhash", w.k, w.l, w.cap, w.policy, strategy="vanilla", beta=w.beta)
+    lsh = O.OutputLsh(spec, w.hidden, seed=0, n0=w.n0, lam=w.decay)
+    lsh.build(st.w2)
+    cfg = O.AdamCfg(lr=w.lr)
+    trip = corpus.triples()
+    order = np.random.default_rng((0, 0)).permutation(len(trip))  # reference data.py:118-123
+    for it in range(1, 201):
+        batch = [trip[i] for i in order[(it - 1) * w.batch : it * w.batch]]
+        res = O.train_step(st, lsh, batch, it, 0, w.n_out, cfg, mode="sequential")
+        assert np.mean(res.losses) == pytest.approx(float(g["seq_loss"][it - 1]), rel=1e-12, abs=0), it
+        assert res.rebuilt == bool(g["seq_rebuilt"][it - 1])
+        assert res.active_fraction == pytest.approx(float(g["seq_frac"][it - 1]), rel=1e-12)
+    np.testing.assert_allclose(st.w2[:16], g["seq_final_w2_head"], rtol=0, atol=1e-12)
+    rng = np.random.default_rng(0)
+    p1 = np.mean([O.precision_at_k(O.predict_ranked(st, lsh, xi, xv, rng, w.n_out), y, 1)
+                  for xi, xv, y in held.triples()])
+    assert p1 == float(g["seq_p1"][0])
