@@ -128,6 +128,11 @@ int slide_tables_mask(slide_ctx* ctx, uint64_t disabled);
 /* query_codes (tables.py:171-176): dev keys (b, L) -> dev (b, L) first slot
  * and occupancy of each probed bucket (0 when the key is absent) */
 int slide_tables_probe(slide_ctx* ctx, const uint32_t* keys, int64_t b, int32_t* starts, int32_t* lens);
+/* query_codes with bucket contents (tables.py:171-176), host in/out,
+ * synchronous: keys (b, L) -> per probe the occupancy, the insert count and
+ * the kept ids ascending at ids[q * capacity ..] (ids: b * L * capacity) */
+int slide_tables_probe_ids(slide_ctx* ctx, const uint32_t* keys_host, int64_t b, int32_t* lens_host,
+                           int32_t* counts_host, int32_t* ids_host);
 
 /* Query + union (rebuild microbenchmark): hash n query rows
  * (device, stride hidden_pad) and write per query the ascending union of its

@@ -59,6 +59,7 @@ _SIGS = {
     "slide_tables_info": [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)],
     "slide_tables_export": [vp, vp, vp, vp, vp, vp],
     "slide_tables_probe": [vp, vp, i64, vp, vp],
+    "slide_tables_probe_ids": [vp, vp, i64, vp, vp, vp],
     "slide_tables_load": [vp, vp, vp, vp, vp, i64, vp, i64, i64],
     "slide_tables_mask": [vp, u64],
     "slide_forward": [vp, C.POINTER(Batch), i64, i64, C.POINTER(i64)],

@@ -467,6 +467,53 @@ int slide_tables_probe(slide_ctx* c, const uint32_t* keys, int64_t b, int32_t* s
   });
 }
 
+// query_codes with contents (reference tables.py:171-176): per probe q of
+// (b, L) the bucket's occupancy, insert count and kept ids (ascending) at
+// ids[q * cap ..]; the caller rotates FIFO rings from the insert count.
+__global__ void probe_ids_kernel(TablesDev t, const uint32_t* keys, int64_t b, int32_t* lens, int32_t* counts,
+                                 int32_t* ids) {
+  const int64_t q = blockIdx.x;
+  if (q >= b * t.l) return;
+  const int tt = (int)(q % t.l);
+  const int run = tables_lookup(t, ((uint32_t)tt << t.key_bits) | keys[q]);
+  const int len = run >= 0 ? t.blen[run] : 0;
+  if (threadIdx.x == 0) {
+    lens[q] = len;
+    counts[q] = run >= 0 ? t.bcount[run] : 0;
+  }
+  for (int j = threadIdx.x; j < len; j += blockDim.x) ids[q * t.cap + j] = t.ids[t.bstart[run] + j];
+}
+
+int slide_tables_probe_ids(slide_ctx* c, const uint32_t* keys_host, int64_t b, int32_t* lens_host,
+                           int32_t* counts_host, int32_t* ids_host) {
+  return guarded([&] {
+    TablesDev t = c->tab.dev;
+    t.l = (int)c->d.l;
+    t.key_bits = (int)c->d.key_bits;
+    t.cap = (int)c->d.capacity;
+    const int64_t n = b * t.l;
+    if (n <= 0) return;
+    char* base = nullptr;
+    const size_t bytes = (size_t)n * (4 + 4 + 4 + 4 * (size_t)t.cap);
+    SLIDE_CUDA(cudaMalloc(&base, bytes));
+    struct Free {
+      char* p;
+      ~Free() { cudaFree(p); }
+    } free_base{base};
+    uint32_t* d_keys = reinterpret_cast<uint32_t*>(base);
+    int32_t* d_lens = reinterpret_cast<int32_t*>(d_keys + n);
+    int32_t* d_counts = d_lens + n;
+    int32_t* d_ids = d_counts + n;
+    SLIDE_CUDA(cudaMemcpyAsync(d_keys, keys_host, n * 4, cudaMemcpyHostToDevice, c->s));
+    probe_ids_kernel<<<(int)n, 128, 0, c->s>>>(t, d_keys, b, d_lens, d_counts, d_ids);
+    SLIDE_LAUNCH_CHECK();
+    SLIDE_CUDA(cudaMemcpyAsync(lens_host, d_lens, n * 4, cudaMemcpyDeviceToHost, c->s));
+    SLIDE_CUDA(cudaMemcpyAsync(counts_host, d_counts, n * 4, cudaMemcpyDeviceToHost, c->s));
+    SLIDE_CUDA(cudaMemcpyAsync(ids_host, d_ids, n * t.cap * 4, cudaMemcpyDeviceToHost, c->s));
+    SLIDE_CUDA(cudaStreamSynchronize(c->s));
+  });
+}
+
 // Query + union (the rebuild microbenchmark's second half):
 // hash n query rows (device, row stride ld = hidden_pad) and return, per
 // query, the ascending union of its L buckets -- hard_threshold(min_freq=1)

@@ -325,29 +325,37 @@ class LshTables:
         return self.query_codes(self.family.hash(v))
 
     def query_codes(self, codes) -> RawCandidates:
-        """Exactly L probes (reference tables.py:171-176)."""
-        import torch
-
-        from . import _device
-
+        """Exactly L probes (reference tables.py:171-176): each probed bucket's
+        kept ids come back from the device in the reference's physical slot
+        order (a full FIFO bucket is a ring whose head is its insert count
+        modulo the capacity, ref tables.py:130-145)."""
         self.sync_to_device()
         codes = np.asarray(codes, dtype=np.int64).reshape(1, -1)
+        L = self.family.l
+        if codes.shape[1] != L:
+            raise ValueError(f"expected {L} codes, got {codes.shape[1]}")
         if self._ctx is None:
-            return RawCandidates([[] for _ in range(self.family.l)], self.n_items)
-        kd = _device.to_dev(codes.astype(np.uint32).view(np.int32))
-        starts = torch.empty_like(kd)
-        lens = torch.empty_like(kd)
-        _lib.call("slide_tables_probe", self._ctx, kd.data_ptr(), 1, starts.data_ptr(), lens.data_ptr())
-        st = starts.cpu().numpy()[0]
-        ln = lens.cpu().numpy()[0]
+            return RawCandidates([[] for _ in range(L)], self.n_items)
+        if self._views is not None:  # host-side edits already pushed; views equal the device
+            return RawCandidates([list(v[int(codes[0, t])].slots) if int(codes[0, t]) in v else []
+                                  for t, v in enumerate(self._views)], self.n_items)
+        cap = self.capacity
+        keys = np.ascontiguousarray(codes.astype(np.uint32))
+        lens = np.empty(L, np.int32)
+        counts = np.empty(L, np.int32)
+        ids = np.empty(L * cap, np.int32)
+        _lib.call("slide_tables_probe_ids", self._ctx, keys.ctypes.data, 1, lens.ctypes.data, counts.ctypes.data,
+                  ids.ctypes.data)
         per = []
-        nb, ns, ni = _lib.i64(), _lib.i64(), _lib.i64()
-        _lib.call("slide_tables_info", self._ctx, _lib.C.byref(nb), _lib.C.byref(ns), _lib.C.byref(ni))
-        views = self.tables
-        for t in range(self.family.l):
-            hit = views[t].get(int(codes[0, t]))
-            per.append(list(hit.slots) if hit is not None else [])
-            assert (hit is None and ln[t] == 0) or (hit is not None and len(hit.slots) == ln[t])
+        for t in range(L):
+            kept = ids[t * cap : t * cap + lens[t]].tolist()
+            cnt = int(counts[t])
+            if self.policy == "fifo" and cnt > cap:
+                slots = [0] * cap
+                for j, nid in enumerate(kept):
+                    slots[(cnt - cap + j) % cap] = nid
+                kept = slots
+            per.append(kept)
         return RawCandidates(per, self.n_items)
 
     # -- maintenance ----------------------------------------------------------

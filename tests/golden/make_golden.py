@@ -382,6 +382,80 @@ def tiny_run():
     save("tiny_run.npz", **out)
 
 
+def _round_f32(net):
+    """The device's starting point: the reference's init rounded to fp32."""
+    for layer in net.layers:
+        for a in (layer.w, layer.b):
+            a[...] = a.astype(np.float32).astype(np.float64)
+
+
+def _p1_runs(corpus, evals, n_steps, rounded):
+    """Reference sequential (train_network, workers=1) and snapshot runs over
+    the same batches; P@1 on ``evals`` with the evaluator's shared rng."""
+    from slide.data import Dataset, precision_at_k
+    from slide.network import train_network
+
+    w = TINY
+    n_train = n_steps * w.batch
+    train = [corpus.example(i) for i in range(n_train)]
+
+    def make():
+        cfg = TrainConfig(batch_size=w.batch, seed=0, learning_rate=w.lr, n0=w.n0, decay=w.decay)
+        lsh = LshLayerConfig("simhash", k=w.k, l=w.l, capacity=w.cap, sampler=SamplerConfig("vanilla", beta=w.beta))
+        net = SlideNetwork(w.input_dim, [w.hidden, w.n_out], cfg, lsh_layers={1: lsh})
+        if rounded:
+            _round_f32(net)
+            net.layers[1].lsh.build(net.layers[1].w)
+        return net
+
+    def p_at_1(net):
+        rng = np.random.default_rng(0)
+        return float(np.mean([precision_at_k(net.predict(x, rng=rng)[:1], y, 1) for x, y in evals]))
+
+    net = make()
+    seq = []
+    train_network(net, Dataset(train, w.input_dim, w.n_out), on_batch=lambda it, st: seq.append(st.loss))
+    seq_p1 = p_at_1(net)
+    net = make()
+    order = np.random.default_rng((0, 0)).permutation(n_train)
+    snap = [snapshot_step(net, [train[i] for i in order[(it - 1) * w.batch : it * w.batch]], it)
+            for it in range(1, n_steps + 1)]
+    return np.array(seq), seq_p1, np.array(snap), p_at_1(net)
+
+
+def p1_runs():
+    """P@1-after-N-steps evidence (north_star: within 1 point of the
+    reference).  (1) The rounding spread on the BASELINE tiny corpus: the
+    reference's own 200-step runs restarted from its fp32-rounded init, next
+    to tiny_run.npz's f64-init runs -- the labels there are independent of
+    the features, so P@1 moves by points under rounding alone.  (2) A
+    learnable corpus (tests/learnable_corpus.py) at the tiny shape, where
+    P@1 measures the training algorithm: reference sequential and snapshot
+    runs from the f64 init and from the fp32-rounded one."""
+    from tests.learnable_corpus import learnable_corpus
+
+    w = TINY
+    out = {}
+    corpus = synthetic_corpus(w.corpus, 200 * w.batch, seed=0)
+    held = synthetic_corpus(w.corpus, 4000, seed=1)
+    evals = [held.example(i) for i in range(len(held))]
+    _, out["tiny_seq_p1_f32init"], _, out["tiny_snap_p1_f32init"] = _p1_runs(corpus, evals, 200, True)
+    lc = learnable_corpus(w.input_dim, w.n_out, 200 * w.batch, seed=0)
+    lh = learnable_corpus(w.input_dim, w.n_out, 4000, seed=1)
+    levals = [lh.example(i) for i in range(len(lh))]
+    for rounded in (False, True):
+        tag = "_f32init" if rounded else ""
+        sl, sp, nl, np1 = _p1_runs(lc, levals, 200, rounded)
+        out["learn_seq_loss" + tag], out["learn_seq_p1" + tag] = sl, np.array([sp])
+        out["learn_snap_loss" + tag], out["learn_snap_p1" + tag] = nl, np.array([np1])
+    out["tiny_seq_p1_f32init"] = np.array([out["tiny_seq_p1_f32init"]])
+    out["tiny_snap_p1_f32init"] = np.array([out["tiny_snap_p1_f32init"]])
+    out["learn_check"] = np.array([lc.x_idx.astype(np.int64).sum(), lc.y_idx.astype(np.int64).sum(),
+                                   lh.x_idx.astype(np.int64).sum(), lh.y_idx.astype(np.int64).sum()])
+    print({k: v for k, v in out.items() if "p1" in k})
+    save("p1_runs.npz", **out)
+
+
 from tests.golden.make_golden_data import XC_BAD, XC_GOOD  # noqa: E402
 
 
@@ -447,6 +521,6 @@ def checkpoint():
 if __name__ == "__main__":
     assert slide.__version__ == "0.1.0"
     which = sys.argv[1:] or ["rng_streams", "mt19937", "hashing", "tables", "samplers", "network", "tiny_config",
-                             "tiny_run", "data_io", "checkpoint"]
+                             "tiny_run", "p1_runs", "data_io", "checkpoint"]
     for name in which:
         globals()[name]()
