@@ -20,11 +20,13 @@ chosen so that one rebuild falls inside them.
 * cpu_baseline: the CPU oracle (a numpy restatement of the reference path,
   kind "port") on a bounded sample of the same workload, 1 thread.
 
-N>1 (torchrun): the output layer is column-sharded over the N GPUs (SURVEY
-8(e), paper_1903_03129_b200/sharded.py): every rank processes the same global
-batch, owns 1/N of the output rows, and the step all-reduces the softmax
-max / sum, the loss terms and the hidden gradient over NCCL (strong
-scaling); max-over-ranks device time.
+N>1 (torchrun): the layer is sharded over the N GPUs (SURVEY 8(e),
+paper_1903_03129_b200/sharded.py): W2 rows, their Adam state and their LSH
+tables by output id, W1 by hidden unit; the global batch is N x the
+workload's batch (weak scaling: per-rank work stays ~constant), and the step
+runs one all-gather (hidden slices) and five all-reduces (sampler counts,
+softmax max / sum, loss terms, hidden gradient) over NCCL; max-over-ranks
+device time.
 """
 
 from __future__ import annotations
@@ -129,7 +131,7 @@ class ClockSampler:
 def config_of(w, args, world):
     """The workload's `config` object -- identical on both arms' lines."""
     return {"workload": w.name, "input_dim": w.input_dim, "hidden": w.hidden, "n_out": w.n_out,
-            "batch": w.batch, "hash": f"{w.family} K={w.k} L={w.l} cap={w.cap} {w.policy}",
+            "batch": w.batch * world, "hash": f"{w.family} K={w.k} L={w.l} cap={w.cap} {w.policy}",
             "sampler": f"{w.strategy} beta={w.beta}", "lr": w.lr, "rebuild": f"n0={w.n0} decay={w.decay}",
             "schedule": args.schedule,
             "parallelism": f"output layer column-sharded x{world}" if world > 1 else "1 GPU",
@@ -140,7 +142,7 @@ def config_of(w, args, world):
 def make_net(w, torch, rank=0, world=1):
     from paper_1903_03129_b200 import LshLayerConfig, SamplerConfig, SlideNetwork, TrainConfig
 
-    cfg = TrainConfig(batch_size=w.batch, learning_rate=w.lr, n0=w.n0, decay=w.decay, seed=0)
+    cfg = TrainConfig(batch_size=w.batch * world, learning_rate=w.lr, n0=w.n0, decay=w.decay, seed=0)
     spec = LshLayerConfig(w.family, k=w.k, l=w.l, capacity=w.cap, policy=w.policy, wta_bin_size=w.bin_size,
                           sampler=SamplerConfig(w.strategy, beta=w.beta))
     shard = (rank, world) if world > 1 else None
@@ -227,15 +229,20 @@ def run_ours(args, rank, world):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
+        # NCCL over NVLink on B200s; SLIDE_BENCH_DIST=gloo exercises the same
+        # path with several ranks on one GPU (correctness only, not timing)
+        dist.init_process_group(os.environ.get("SLIDE_BENCH_DIST", "nccl"))
     w = WORKLOADS[args.workload]
     K, W = args.steps, args.warmup
     n_batches = W + K
-    # every rank sees the same global batch: the output layer is sharded
-    corpus = synthetic_corpus(w.corpus, n_batches * w.batch, seed=1000)
-    batches = csr_batches(corpus, w.batch, n_batches)
+    # N > 1: weak scaling -- a global batch of N x the workload's batch, every
+    # rank holds 1/N of the output rows (W2, its tables) and of the hidden
+    # units (W1), so per-rank work stays ~constant
+    B = w.batch * world
+    corpus = synthetic_corpus(w.corpus, n_batches * B, seed=1000)
+    batches = csr_batches(corpus, B, n_batches)
     net = make_net(w, torch, rank, world)
-    sub = 1 if args.schedule == "sequential" else w.batch
+    sub = 1 if args.schedule == "sequential" else B
     # device-resident inputs for `value`
     dev_batches = []
     for b in batches:
@@ -243,8 +250,8 @@ def run_ours(args, rank, world):
         dev_batches.append((bt, keep, b))
     torch.cuda.synchronize()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
-    loss_buf = np.empty(w.batch, np.float64)
-    act_buf = np.empty(w.batch, np.int64)
+    loss_buf = np.empty(B, np.float64)
+    act_buf = np.empty(B, np.int64)
 
     def step_dev(it, barrier=True):
         bt, keep, hb = dev_batches[it - 1]
@@ -252,9 +259,9 @@ def run_ours(args, rank, world):
             from paper_1903_03129_b200.sharded import GpuShardBackend, sharded_step
 
             hb.dev = (bt, keep)
-            loss, act = sharded_step(GpuShardBackend(net), hb, it, None)
-            return net._barrier(it, loss, act)
-        if sub == w.batch and net.use_graphs:  # the captured-graph snapshot step
+            loss, act = sharded_step(GpuShardBackend(net), hb, it, None).host()
+            return net._barrier(it, loss, act) if barrier else net._stats(loss, act, [])
+        if sub == B and net.use_graphs:  # the captured-graph snapshot step
             _lib.call("slide_graph_step", net._ctx, _lib.C.byref(bt), it, loss_buf.ctypes.data, act_buf.ctypes.data)
         else:
             _lib.call("slide_train_batch", net._ctx, _lib.C.byref(bt), it, sub, loss_buf.ctypes.data,
@@ -265,7 +272,7 @@ def run_ours(args, rank, world):
     # the host's launch work overlaps the device -- per step, on the context
     # stream: L2 flush, event, step, its rebuild barrier, event; the events
     # bracket exactly the step + barrier, the flush stays outside
-    pipelined_dev = world == 1 and sub == w.batch and net.use_graphs
+    pipelined_dev = world == 1 and sub == B and net.use_graphs
 
     def run_pipelined(its, evs=None, losses=None):
         def wait_oldest():
@@ -318,7 +325,7 @@ def run_ours(args, rank, world):
                 e0.record()
                 st = step_dev(it, barrier=False)
                 em.record()
-                rebuilt = net._rebuild_after(it) if world == 1 else st.rebuilt
+                rebuilt = net._rebuild_after(it)
                 e1.record()
                 torch.cuda.synchronize()
                 evs.append((e0, em, e1, bool(rebuilt)))
@@ -340,7 +347,7 @@ def run_ours(args, rank, world):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     # N > 1: the ranks share one global batch per step (sharded output layer)
-    value = K * w.batch / (total_ms / 1e3)
+    value = K * B / (total_ms / 1e3)
     # -- e2e: public API from host CSR, fresh net state continues.
     # (1) pipelined SlideNetwork.train_batches_csr over the K batches, timed
     #     as one region (each step: H2D of its batch, the step, D2H of its
@@ -392,19 +399,19 @@ def run_ours(args, rank, world):
             torch.cuda.synchronize()
             e_times.append(e0.elapsed_time(e1) - bool(st.rebuilt) * rebuild_ms + amort_ms)
             h2d += net.h2d_bytes
-            d2h += w.batch * 16 + (w.batch + 1) * 4 * (w.batch // sub)
+            d2h += B * 16 + (B + 1) * 4 * (B // sub)
         e_total = float(np.sum(e_times))
         if dist:
             t = torch.tensor([e_total], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_total = float(t.item())
-        sync_value = K * w.batch / (e_total / 1e3)
-        e2e = {"value": K * w.batch / (p_total / 1e3) if pipelined else sync_value, "unit": "samples/s",
+        sync_value = K * B / (e_total / 1e3)
+        e2e = {"value": K * B / (p_total / 1e3) if pipelined else sync_value, "unit": "samples/s",
                "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K),
                "api": ("SlideNetwork.train_batches_csr (pipelined: batch k+1 staged while step k runs), "
                        "L2 flushed once before the K steps" if pipelined else "SlideNetwork.train_batch_csr"),
                "sync_value": sync_value,
-               "pipelined_passes": [K * w.batch / (t / 1e3) for t in p_passes], "pipelined_recaptures": p_recap,
+               "pipelined_passes": [K * B / (t / 1e3) for t in p_passes], "pipelined_recaptures": p_recap,
                "sync_api": "SlideNetwork.train_batch_csr per step, L2 flushed between steps outside the events"}
     # -- profiled pass: per-stage event times + realised sets
     # -- profiled pass: per-stage event times + realised sets
@@ -417,7 +424,7 @@ def run_ours(args, rank, world):
             from paper_1903_03129_b200.sharded import GpuShardBackend, sharded_step
 
             hb.dev = (bt, keep)
-            loss, act = sharded_step(GpuShardBackend(net), hb, step_dev_it, None)
+            loss, act = sharded_step(GpuShardBackend(net), hb, step_dev_it, None).host()
             net._barrier(step_dev_it, loss, act)
             continue
         _lib.call("slide_train_batch", net._ctx, _lib.C.byref(bt), step_dev_it, sub, loss_buf.ctypes.data,
@@ -456,14 +463,14 @@ def run_ours(args, rank, world):
     out = {
         "metric": "train samples/sec (LSH-sparse fwd+bwd+Adam), % of HBM roofline, 1/2/4/8 GPU",
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None,
         # per-step spread (the steps whose barrier rebuilt the tables are the max)
         "ms_per_step_p50": float(np.median(times)), "ms_per_step_max": float(np.max(times)),
         # the step alone (no rebuild) and the rebuild it amortises
         "ms_step_only_mean": float(np.mean(times)), "rebuild_ms": rebuild_ms,
         "rebuild_amortised_ms_per_step": amort_ms, "rebuilds_in_window": len(barrier_ms),
-        "value_without_rebuild": K * w.batch / (float(np.sum(times)) / 1e3),
+        "value_without_rebuild": K * B / (float(np.sum(times)) / 1e3),
         "dtype": "f32", "data": "synthetic (SURVEY 8(d) Zipf generator; Delicious-200K shape)",
         "config": config_of(w, args, world),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -608,7 +615,7 @@ def run_reference(args, rank, world):
 
     w = WORKLOADS[args.workload]
     cores = os.cpu_count() or 1
-    per_step = w.batch  # the full batch: the same config as the GPU arm
+    per_step = w.batch * world  # the full (global) batch: the same config as the GPU arm
     with threadpool_limits(1):
         st = _shared_state(O.init_state(w.input_dim, w.hidden, w.n_out, seed=0))
         spec = O.LshSpec(w.family, w.k, w.l, w.cap, w.policy, bin_size=w.bin_size, strategy=w.strategy, beta=w.beta)

@@ -55,7 +55,8 @@ typedef struct slide_net_desc {
   /* Adam (TrainConfig, network.py:36-48) */
   double lr, beta1, beta2, eps;
   uint64_t seed;
-  /* parameters, device, row stride hidden_pad; W1 stored transposed (D, hp) */
+  /* parameters, device, row stride hidden_pad; W1 stored transposed (D, hp)
+   * -- sharded (shard_count > 1): this rank's units only, (D, H / G) */
   float *w1t, *m1t, *v1t, *b1, *mb1, *vb1;
   int64_t* steps1;
   float *w2, *m2, *v2, *b2, *mb2, *vb2;
@@ -214,24 +215,48 @@ int slide_topk(slide_ctx* ctx, int64_t k, int32_t* ids_out, int32_t* counts_out)
  * (network.py:303-313). */
 int slide_write(slide_ctx* ctx, int64_t what, const void* host_src, int64_t bytes);
 
-/* -- sharded step (shard_count > 1): the caller all-reduces between the
- *    stages over its process group (torch.distributed / NCCL).  Tables are
- *    built from the all-gathered keys of every rank's rows, so selection is
- *    replicated and identical to the single-GPU path; each rank keeps its
- *    owned (sample, row) pairs. -------------------------------------------- */
+/* -- column-sharded step (shard_count > 1).  Rank g owns the
+ *    output rows id % G == g (W2, its Adam state, its tables over those rows,
+ *    global ids in the buckets) and the hidden units [g H/G, (g+1) H/G)
+ *    (W1^T is a (D, H/G) array; b1 and its moments are replicated).  The
+ *    caller runs the collectives over its process group between the stages
+ *    (torch.distributed: NCCL on B200s); no stage synchronises the host.
+ *    Replaces the per-layer passes of network.py:262-336 and the table
+ *    build of tables.py:105-161 for one shard. ------------------------------ */
+/* tables: hash this rank's rows and build its tables; *max_count = largest
+ * local bucket (host).  all-reduce MAX; if G * max > cap (FIFO): pack every
+ * rank's runs (pack_size / pack, int32), all-gather (padded to the largest
+ * pack) and reconcile -- each rank keeps its members of every bucket's
+ * global last-cap ids.  Reservoir tables must not overflow (checked). */
+int slide_shard_build_local(slide_ctx* ctx, int64_t* max_count);
+int slide_shard_tables_pack_size(slide_ctx* ctx, int64_t* n);
+int slide_shard_tables_pack(slide_ctx* ctx, int32_t* out);
+int slide_shard_tables_reconcile(slide_ctx* ctx, const int32_t* packs, int64_t stride);
 /* keys (dev, local_rows x L) of this rank's W2 rows */
 int slide_shard_hash_rows(slide_ctx* ctx, uint32_t* keys);
-/* forward up to the local logits; max_out (dev, B): per-sample max over
- * owned pairs (-inf when none) -> all-reduce MAX */
-int slide_shard_forward(slide_ctx* ctx, const slide_batch* batch, int64_t iteration, float* max_out);
-/* sum_out (dev, B): sum of exp(z - gmax) over owned pairs -> all-reduce SUM */
+/* 1. part_out (dev, B x H/G): this rank's hidden pre-activations (no bias)
+ *    -> all-gather into (G, B, H/G) */
+int slide_shard_hidden(slide_ctx* ctx, const slide_batch* batch, float* part_out);
+/* 2. h = relu(gathered + b1), nonzero masks, live units */
+int slide_shard_assemble(slide_ctx* ctx, int64_t b, const float* parts);
+/* 3. query keys, slot streams and this rank's sampler counts: hist_out
+ *    (dev, B x (L+1) int32) -> all-reduce SUM */
+int slide_shard_select(slide_ctx* ctx, const slide_batch* batch, int64_t iteration, int32_t* hist_out);
+/* 4. the sampler rule with the global counts, fallback, label union, the
+ *    owned (sample, row) pairs and their logits; max_out (dev, B): per-sample
+ *    max over owned pairs (-inf when none) -> all-reduce MAX */
+int slide_shard_forward(slide_ctx* ctx, const slide_batch* batch, int64_t iteration, const int32_t* ghist,
+                        float* max_out);
+/* 5. sum_out (dev, B): sum of exp(z - gmax) over owned pairs -> all-reduce SUM */
 int slide_shard_softmax_sum(slide_ctx* ctx, const float* gmax, float* sum_out);
-/* p, delta on owned pairs; loss_out (dev, B, f64): sum over owned labels of
- * min(-log p, 690.78) -> all-reduce SUM, then divide by |Y_i| */
+/* 6. p, delta on owned pairs; loss_out (dev, 2B f64): [i] sum over owned
+ *    labels of min(-log p, 690.78), [B + i] owned active-set size ->
+ *    all-reduce SUM (loss_i = [i] / |Y_i|, |A_i| = [B + i]) */
 int slide_shard_softmax_finish(slide_ctx* ctx, const float* gmax, const float* gsum, double* loss_out);
-/* dh_out (dev, B x hidden_pad): W2_local^T delta (pre-update) -> all-reduce SUM */
+/* 7. dh_out (dev, B x hidden_pad): W2_local^T delta (pre-update) -> all-reduce SUM */
 int slide_shard_hidden_grad(slide_ctx* ctx, float* dh_out);
-/* Adam on the owned W2 rows and (replicated) W1 with the all-reduced dh */
+/* 8. Adam on the owned W2 rows, the replicated hidden biases / step
+ *    counters, and this rank's W1 units, with the all-reduced dh */
 int slide_shard_update(slide_ctx* ctx, const float* dh);
 
 /* -- measurement -------------------------------------------------------- */

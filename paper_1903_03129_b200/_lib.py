@@ -76,7 +76,14 @@ _SIGS = {
     "slide_profile_read": [vp, vp, vp],
     "slide_launch_count": [vp],
     "slide_shard_hash_rows": [vp, vp],
-    "slide_shard_forward": [vp, C.POINTER(Batch), i64, vp],
+    "slide_shard_forward": [vp, C.POINTER(Batch), i64, vp, vp],
+    "slide_shard_hidden": [vp, C.POINTER(Batch), vp],
+    "slide_shard_assemble": [vp, i64, vp],
+    "slide_shard_select": [vp, C.POINTER(Batch), i64, vp],
+    "slide_shard_build_local": [vp, C.POINTER(i64)],
+    "slide_shard_tables_pack_size": [vp, C.POINTER(i64)],
+    "slide_shard_tables_pack": [vp, vp],
+    "slide_shard_tables_reconcile": [vp, vp, i64],
     "slide_shard_softmax_sum": [vp, vp, vp],
     "slide_shard_softmax_finish": [vp, vp, vp, vp],
     "slide_shard_hidden_grad": [vp, vp],

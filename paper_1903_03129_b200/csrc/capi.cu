@@ -86,6 +86,15 @@ struct slide_ctx {
   // output-layer sharding: rank g of G owns ids with id % G == g
   int g = 0, G = 1;
   int64_t n_local = 0;
+  // hidden layer sharded by units: this rank's W1^T holds units [c0, c0 + hg)
+  int hg = 0, c0 = 0;
+  // sharded selection phases (slide_shard_select / slide_shard_forward):
+  // 1 = stop after the per-rank sampler counts, 2 = finish with the
+  // all-reduced counts; 0 = unsharded
+  int shard_phase = 0;
+  const int32_t* shard_ghist = nullptr;
+  int32_t* shard_hist = nullptr;
+  DBuf shard_pack;
   DBuf cnt_all;  // per-slot global active-set size (sharded statistics)
   // CUDA-graph step (slide_graph_step): static shapes + context-owned batch
   struct {
@@ -278,6 +287,13 @@ int slide_create(const slide_net_desc* desc, void* stream, slide_ctx** out) {
     c->g = (int)d.shard_rank;
     c->G = (int)G;
     c->n_local = (d.n_out - d.shard_rank + G - 1) / G;
+    if (G > 1) {
+      SLIDE_CHECK(d.hidden % G == 0 && (d.hidden / G) % 4 == 0 && d.hidden / G <= 128, kNotSupported,
+                  "sharded hidden layer: hidden / shard_count must be a multiple of 4 and <= 128");
+      SLIDE_CHECK(d.strategy != 1, kNotSupported, "the topk sampler is not supported on a sharded output layer");
+      c->hg = (int)(d.hidden / G);
+      c->c0 = (int)(d.shard_rank * c->hg);
+    }
     try {
       if (d.family == 1) {
         size_t n = (size_t)d.k * d.l * d.sh_c;
@@ -602,6 +618,8 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   cudaStream_t s = c->s;
   // static shapes (graph capture): capacities instead of this batch's sizes,
   // the batch sits in the context's own buffers (offsets start at 0)
+  SLIDE_CHECK(c->G == 1 || c->shard_phase != 0, kValueError,
+              "a sharded context runs the slide_shard_* stages (sharded.sharded_step)");
   const bool stat = c->st_active;
   int64_t x_base, nnz;
   int max_labels = 0;
@@ -620,7 +638,7 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   // fused step: the W1 feature grouping needs only the inputs -- queue it on
   // the side stream now, beside the whole forward pass (backward joins it)
   c->w1_grouped = false;
-  if (c->w1_prefork && !c->timer.on && nnz > 0) {
+  if (c->w1_prefork && !c->timer.on && nnz > 0 && c->G == 1) {
     side_stream_init(c);
     SLIDE_CUDA(cudaEventRecord(c->ev_pre, s));
     SLIDE_CUDA(cudaStreamWaitEvent(c->s2, c->ev_pre, 0));
@@ -639,7 +657,7 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   // SimHash query keys computed by the hidden forward itself when the
   // per-sample query kernel would run (the same arithmetic)
   QueryHash qh;
-  const bool fuse_qh = !bt->forced_ptr && d.family == 1 && c->sh_packed_t.p != nullptr && b <= kSms * 8 &&
+  const bool fuse_qh = c->G == 1 && !bt->forced_ptr && d.family == 1 && c->sh_packed_t.p != nullptr && b <= kSms * 8 &&
                        (int64_t)d.k * d.l <= kQhMaxBits;
   if (fuse_qh) {
     const SimHashDev f = simhash_of(c);
@@ -649,8 +667,10 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     qh.c = f.c;
     qh.keys = c->qkeys.ensure<uint32_t>((size_t)b * L);
   }
-  launch_hidden_forward(hp, b, bt->x_ptr, bt->x_idx, bt->x_val, d.w1t, d.b1, h, hmask, live, live_ticket(c), s,
-                        fuse_qh ? &qh : nullptr);
+  // sharded: h was assembled from the all-gathered unit shards (slide_shard_assemble)
+  if (c->G == 1)
+    launch_hidden_forward(hp, b, bt->x_ptr, bt->x_idx, bt->x_val, d.w1t, d.b1, h, hmask, live, live_ticket(c), s,
+                          fuse_qh ? &qh : nullptr);
   c->timer.mark(s, kStHidden);
   c->host_counts[2] += b;
 
@@ -672,7 +692,7 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     c->timer.mark(s, kStSelect);
   } else {
     uint32_t* qk = c->qkeys.ensure<uint32_t>((size_t)b * L);
-    if (!fuse_qh) hash_rows(c, h, b, qk);
+    if (!fuse_qh && c->shard_phase != 2) hash_rows(c, h, b, qk);
     c->timer.mark(s, kStQueryHash);
     uint64_t* states = c->states.ensure<uint64_t>((size_t)b * 6);
     uint8_t* order = c->order.ensure<uint8_t>((size_t)b * L);
@@ -683,7 +703,7 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     // slot stream is only needed by the (rare) fallback, which derives it
     const bool full_union = vanilla && d.beta >= lcap;
     const bool rng_first = !full_union || bt->rng_states;
-    if (rng_first)
+    if (rng_first && c->shard_phase != 2)
       launch_slot_rng(b, d.seed, iteration, iter_dev, slot_offset, L, vanilla, bt->rng_states, states, order, s);
     c->timer.mark(s, kStSlotRng);
     cap_max = std::max<int64_t>(lcap, want) + max_labels;
@@ -707,9 +727,12 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     a.act = act;
     a.cnt = cnt;
     a.empty = empty;
-    a.cand_ctr = c->timer.on ? c->counters.as<unsigned long long>() + 4 : nullptr;
+    a.cand_ctr = c->timer.on && c->shard_phase != 1 ? c->counters.as<unsigned long long>() + 4 : nullptr;
+    a.hist_out = c->shard_phase == 1 ? c->shard_hist : nullptr;
+    a.ghist = c->shard_phase == 2 ? c->shard_ghist : nullptr;
     if (!(full_union && launch_select_union(a, d.n_out, s))) launch_select(a, (int)(lcap + max_labels), s);
     c->timer.mark(s, kStSelect);
+    if (c->shard_phase == 1) return;  // the caller all-reduces the counts
     // fallback for slots whose sampler returned nothing
     FallbackArgs f;
     f.empty = empty;
@@ -888,10 +911,16 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
       SLIDE_CUDA(cudaEventRecord(c->ev_w1l, st));
       SLIDE_CUDA(cudaStreamWaitEvent(sl, c->ev_w1l, 0));
     }
-    launch_adam_features(hp, ap, gf.n_uniq.as<int32_t>(), gf.u_max, gf.uniq.as<int32_t>(), gf.seg_off.as<int32_t>(),
-                         gf.seg_cnt.as<int32_t>(), gf.order.as<int32_t>(), xs, c->last_xval, c->last_xbase,
-                         c->h.as<float>(), dh, bc, c->live.as<int32_t>(), d.w1t, d.m1t, d.v1t,
-                         ctr ? ctr + 1 : nullptr, gf.long_list.as<int32_t>(), gf.n_long.as<int32_t>(), st, sl);
+    if (c->G > 1)  // this rank's hidden units only (W1^T sharded by units)
+      launch_adam_w1_shard(hp, c->hg, c->c0, ap, gf.n_uniq.as<int32_t>(), gf.u_max, gf.uniq.as<int32_t>(),
+                           gf.seg_off.as<int32_t>(), gf.seg_cnt.as<int32_t>(), gf.order.as<int32_t>(), xs,
+                           c->last_xval, c->last_xbase, c->h.as<float>(), dh, bc, d.w1t, d.m1t, d.v1t,
+                           ctr ? ctr + 1 : nullptr, st);
+    else
+      launch_adam_features(hp, ap, gf.n_uniq.as<int32_t>(), gf.u_max, gf.uniq.as<int32_t>(), gf.seg_off.as<int32_t>(),
+                           gf.seg_cnt.as<int32_t>(), gf.order.as<int32_t>(), xs, c->last_xval, c->last_xbase,
+                           c->h.as<float>(), dh, bc, c->live.as<int32_t>(), d.w1t, d.m1t, d.v1t,
+                           ctr ? ctr + 1 : nullptr, gf.long_list.as<int32_t>(), gf.n_long.as<int32_t>(), st, sl);
     c->timer.mark(st, kStAdamFeat);
     gf.clear(st);
   };
@@ -1317,9 +1346,112 @@ int slide_shard_hash_rows(slide_ctx* c, uint32_t* keys) {
   });
 }
 
-int slide_shard_forward(slide_ctx* c, const slide_batch* bt, int64_t iteration, float* max_out) {
+__global__ void max_count_kernel(const int32_t* __restrict__ counts, int64_t n, int32_t* out) {
+  int m = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, counts[r]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// Column-sharded tables: hash this rank's W2 rows and build
+// its tables over them, ids stored as global ids (local r -> r G + g).
+// *max_count: the largest local bucket insert count; the caller all-reduces
+// it (MAX): while G * max <= cap no global bucket can overflow and the local
+// tables are exact, else the runs are exchanged (pack / reconcile).
+int slide_shard_build_local(slide_ctx* c, int64_t* max_count) {
+  return guarded([&] {
+    SLIDE_CHECK(c->G > 1 && c->d.family != 0, kValueError, "slide_shard_* needs a sharded context with tables");
+    const int64_t n = c->n_local;
+    uint32_t* keys = c->rowkeys.ensure<uint32_t>((size_t)std::max<int64_t>(n, 1) * c->d.l);
+    c->timer.mark(c->s, kStStart);
+    hash_rows(c, c->d.w2, n, keys);
+    c->timer.mark(c->s, kStRebuildHash);
+    tables_build(c->tab, keys, n, (int)c->d.l, (int)c->d.key_bits, (int)c->d.capacity, (int)c->d.policy, nullptr,
+                 c->s, c->G, c->g);
+    int32_t* mx = c->work.ensure<int32_t>(4) + 2;
+    SLIDE_CUDA(cudaMemsetAsync(mx, 0, 4, c->s));
+    if (c->tab.dev.n_runs > 0) {
+      max_count_kernel<<<(int)std::min<int64_t>(ceil_div(c->tab.dev.n_runs, 256), kSms * 4), 256, 0, c->s>>>(
+          c->tab.dev.bcount, c->tab.dev.n_runs, mx);
+      SLIDE_LAUNCH_CHECK();
+    }
+    int32_t h = 0;
+    SLIDE_CUDA(cudaMemcpyAsync(&h, mx, 4, cudaMemcpyDeviceToHost, c->s));
+    SLIDE_CUDA(cudaStreamSynchronize(c->s));
+    c->tab.n_items = c->d.n_out;
+    c->timer.mark(c->s, kStRebuildBuild);
+    c->host_counts[3] += 1;
+    *max_count = h;
+  });
+}
+
+int slide_shard_tables_pack_size(slide_ctx* c, int64_t* n) {
+  return guarded([&] { *n = tables_pack_size(c->tab); });
+}
+
+int slide_shard_tables_pack(slide_ctx* c, int32_t* out) {
+  return guarded([&] { tables_pack(c->tab, out, c->s); });
+}
+
+// packs: the all-gathered (G, stride) int32 packs of every rank (FIFO only)
+int slide_shard_tables_reconcile(slide_ctx* c, const int32_t* packs, int64_t stride) {
   return guarded([&] {
     SLIDE_CHECK(c->G > 1, kValueError, "slide_shard_* needs a sharded context");
+    SLIDE_CHECK(c->d.policy == 0, kNotSupported,
+                "sharded reservoir tables need every bucket within capacity (shard_count * max bucket <= cap)");
+    tables_reconcile(c->tab, packs, stride, c->G, c->g, (int)c->d.capacity, c->s);
+  });
+}
+
+int slide_shard_hidden(slide_ctx* c, const slide_batch* bt, float* part_out) {
+  return guarded([&] {
+    SLIDE_CHECK(c->G > 1, kValueError, "slide_shard_* needs a sharded context");
+    const int b = (int)bt->batch;
+    SLIDE_CHECK(b >= 1 && b <= 1024, kValueError, "batch must hold 1..1024 slots");
+    c->timer.mark(c->s, kStStart);
+    launch_shard_hidden(c->hp, c->hg, b, bt->x_ptr, bt->x_idx, bt->x_val, c->d.w1t, part_out, c->s);
+  });
+}
+
+int slide_shard_assemble(slide_ctx* c, int64_t b, const float* parts) {
+  return guarded([&] {
+    SLIDE_CHECK(c->G > 1, kValueError, "slide_shard_* needs a sharded context");
+    SLIDE_CHECK(b >= 1 && b <= 1024, kValueError, "batch must hold 1..1024 slots");
+    const int hp = c->hp;
+    float* h = c->h.ensure<float>((size_t)b * hp);
+    uint32_t* hmask = c->hmask.ensure<uint32_t>((size_t)b * (hp / 32));
+    int32_t* live = c->live.ensure<int32_t>(1 + hp);
+    launch_shard_assemble(hp, (int)c->d.hidden, c->hg, (int)b, parts, c->d.b1, h, hmask, live, live_ticket(c), c->s);
+    c->timer.mark(c->s, kStHidden);
+  });
+}
+
+int slide_shard_select(slide_ctx* c, const slide_batch* bt, int64_t iteration, int32_t* hist_out) {
+  return guarded([&] {
+    SLIDE_CHECK(c->G > 1, kValueError, "slide_shard_* needs a sharded context");
+    SLIDE_CHECK(c->d.family != 0 && !bt->forced_ptr, kNotSupported, "sharded selection needs LSH tables");
+    c->shard_phase = 1;
+    c->shard_hist = hist_out;
+    struct Reset {
+      slide_ctx* c;
+      ~Reset() { c->shard_phase = 0; }
+    } reset{c};
+    forward_impl(c, bt, iteration, 0, nullptr);
+  });
+}
+
+int slide_shard_forward(slide_ctx* c, const slide_batch* bt, int64_t iteration, const int32_t* ghist,
+                        float* max_out) {
+  return guarded([&] {
+    SLIDE_CHECK(c->G > 1, kValueError, "slide_shard_* needs a sharded context");
+    c->shard_phase = 2;
+    c->shard_ghist = ghist;
+    struct Reset {
+      slide_ctx* c;
+      ~Reset() { c->shard_phase = 0; }
+    } reset{c};
     forward_impl(c, bt, iteration, 0, nullptr);
     launch_softmax_max(c->last_b, c->offs.as<int32_t>(), c->z.as<float>(), max_out, c->s);
   });
@@ -1339,6 +1471,8 @@ int slide_shard_softmax_finish(slide_ctx* c, const float* gmax, const float* gsu
     launch_softmax_finish(b, c->offs.as<int32_t>(), c->plab.as<uint8_t>(), c->last_yptr, c->z.as<float>(), gmax,
                           gsum, c->prob.as<float>(), c->delta.as<float>(), loss_out, c->grow.inv.as<int32_t>(),
                           c->dsort.as<float>(), c->s);
+    // loss_out[b + i] = the rank's owned active-set size of slot i (summed over ranks: |A_i|)
+    launch_counts_to_f64(b, c->cnt.as<int32_t>(), loss_out + b, c->s);
   });
 }
 

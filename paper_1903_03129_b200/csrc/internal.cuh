@@ -123,8 +123,15 @@ struct TablesHost {
 
 // Build all L tables from row keys (n, L).  mt_state (625 words, host) is the
 // reservoir stream, consumed and updated when a bucket overflows.
+// id_mul / id_add: stored id of row r is r * id_mul + id_add (a column shard
+// of the output layer stores its rows' global ids; reservoir overflows are
+// then not replayed -- the sharded caller proves there are none)
 void tables_build(TablesHost& tb, const uint32_t* keys, int64_t n, int l, int key_bits, int cap,
-                  int policy, uint64_t* mt_state, cudaStream_t s);
+                  int policy, uint64_t* mt_state, cudaStream_t s, int id_mul = 1, int id_add = 0);
+// sharded FIFO reconciliation (see tables.cu)
+int64_t tables_pack_size(const TablesHost& tb);
+void tables_pack(const TablesHost& tb, int32_t* out, cudaStream_t s);
+void tables_reconcile(TablesHost& tb, const int32_t* packs, int64_t stride, int G, int g, int cap, cudaStream_t s);
 // Install host-made buckets (device copies of the arrays), directory rebuilt.
 void tables_load(TablesHost& tb, const uint32_t* skeys, const int32_t* counts, const int32_t* starts,
                  const int32_t* lens, int64_t n_runs, const int32_t* ids, int64_t n_slots, int64_t n_items, int l,

@@ -16,6 +16,15 @@ struct SelectArgs {
   int32_t* cnt;
   int32_t* empty;
   unsigned long long* cand_ctr;  // optional: total probed bucket slots
+  // column-sharded tables: a rank's buckets hold only its own
+  // ids, so the sampler's global quantities are sums over ranks.  Phase 1
+  // (hist_out set): write per sample (L + 1) counts -- [p] distinct ids
+  // first seen at probe position p (vanilla), [L] ids the rule selects
+  // without a global threshold (vanilla / full union: every distinct id;
+  // hard_threshold: freq >= min_freq) -- and stop.  Phase 2 (ghist set):
+  // the all-reduced counts decide vanilla's stop position and emptiness.
+  int32_t* hist_out = nullptr;
+  const int32_t* ghist = nullptr;
 };
 
 struct FallbackArgs {
@@ -55,6 +64,7 @@ void launch_explicit_active(int b, int64_t n, const int32_t* fptr, const int32_t
 // pair lists from the per-slot active sets; also writes offs (B + 1) from cnt
 void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* cnt, int32_t* offs, int shard_count,
                   int32_t* prow, int32_t* pslot, uint8_t* plab, cudaStream_t s);
+void launch_counts_to_f64(int b, const int32_t* cnt, double* out, cudaStream_t s);
 void launch_own_filter(int b, int32_t* act, int64_t cap_max, int g, int G, int32_t* cnt, int32_t* cnt_all,
                        cudaStream_t s);
 // sharded softmax phases (per sample over the owned pairs)
@@ -181,5 +191,16 @@ void launch_hidden_prep_bias(int hp, int b, const AdamParams& ap, const float* h
                              int32_t* tc, float2* bc, float* b1, float* mb1, float* vb1, cudaStream_t s);
 void launch_adam_hidden_bias(int hp, int b, const AdamParams& ap, const float* h, const float* dh, const int32_t* tc,
                              const float2* bc, float* b1, float* mb1, float* vb1, int64_t* steps1, cudaStream_t s);
+
+// hidden layer sharded by units; see layers.cu
+void launch_shard_hidden(int hp, int hg, int b, const int32_t* x_ptr, const int32_t* x_idx, const float* x_val,
+                         const float* w1s, float* part, cudaStream_t s);
+void launch_shard_assemble(int hp, int hidden, int hg, int b, const float* parts, const float* b1, float* h,
+                           uint32_t* hmask, int32_t* live, int32_t* ticket, cudaStream_t s);
+void launch_adam_w1_shard(int hp, int hg, int c0, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq,
+                          const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt, const int32_t* sorted_k,
+                          const int32_t* x_slot, const float* x_val, int64_t x_base, const float* h, const float* dh,
+                          const float2* bc, float* w1s, float* m1s, float* v1s, unsigned long long* touched,
+                          cudaStream_t s);
 
 }  // namespace slide

@@ -1736,3 +1736,158 @@ void launch_softmax_finish(int b, const int32_t* offs, const uint8_t* plab, cons
 }
 
 }  // namespace slide
+
+namespace slide {
+
+// ------------------------------------------ hidden layer sharded by units
+// W1^T is split by hidden units -- rank g holds the hg columns
+// [g hg, (g + 1) hg) as a (D, hg) array.  Phase 1 (shard_hidden_kernel):
+// the rank's pre-activation partial sums for every sample, in the exact
+// term order of hidden_fwd_kernel (KW partial chains over the nonzeros
+// k = w, w + KW, ... then the chains summed in chain order), so the
+// all-gathered row equals the unsharded one bit for bit.  Phase 2
+// (shard_assemble_kernel, after the all-gather): h = relu(row + b1), the
+// per-sample nonzero masks and, by the last CTA, the live-unit list.
+template <int KW>
+__global__ void shard_hidden_kernel(int hg, const int32_t* __restrict__ x_ptr, const int32_t* __restrict__ x_idx,
+                                    const float* __restrict__ x_val, const float* __restrict__ w1s,
+                                    float* __restrict__ part) {
+  extern __shared__ float red[];  // [KW][hg]
+  const int i = blockIdx.x;
+  const int nq = hg >> 2;
+  const int w = threadIdx.x / nq, q = threadIdx.x % nq;
+  const int a = x_ptr[i], e = x_ptr[i + 1];
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int k = a + w; k < e; k += KW) {
+    const float v = x_val[k];
+    const float4 r = ld4(w1s + (int64_t)x_idx[k] * hg + 4 * q);
+    acc.x = fmaf(v, r.x, acc.x);
+    acc.y = fmaf(v, r.y, acc.y);
+    acc.z = fmaf(v, r.z, acc.z);
+    acc.w = fmaf(v, r.w, acc.w);
+  }
+  *reinterpret_cast<float4*>(&red[w * hg + 4 * q]) = acc;
+  __syncthreads();
+  for (int c = threadIdx.x; c < hg; c += blockDim.x) {
+    float s = red[c];
+    for (int k = 1; k < KW; ++k) s += red[k * hg + c];
+    part[(int64_t)i * hg + c] = s;
+  }
+}
+
+void launch_shard_hidden(int hp, int hg, int b, const int32_t* x_ptr, const int32_t* x_idx, const float* x_val,
+                         const float* w1s, float* part, cudaStream_t s) {
+  if (b <= 0) return;
+  SLIDE_CHECK(hg % 4 == 0 && hg <= 128, kNotSupported, "hidden units per shard must be a multiple of 4, <= 128");
+  // the unsharded kernel's chain count for this padded width
+  const int kw = hp / 128 <= 2 ? 32 : 8;
+  const int threads = kw * (hg / 4);
+  const size_t smem = (size_t)kw * hg * 4;
+  if (kw == 32)
+    shard_hidden_kernel<32><<<b, threads, smem, s>>>(hg, x_ptr, x_idx, x_val, w1s, part);
+  else
+    shard_hidden_kernel<8><<<b, threads, smem, s>>>(hg, x_ptr, x_idx, x_val, w1s, part);
+  SLIDE_LAUNCH_CHECK();
+}
+
+// parts: the all-gathered (G, b, hg) partial rows; unit c = g hg + j
+__global__ void __launch_bounds__(256) shard_assemble_kernel(int hp, int hidden, int hg, int b,
+                                                             const float* __restrict__ parts,
+                                                             const float* __restrict__ b1, float* __restrict__ h,
+                                                             uint32_t* __restrict__ hmask, int32_t* __restrict__ live,
+                                                             int32_t* __restrict__ ticket) {
+  const int i = blockIdx.x, lane = threadIdx.x & 31;
+  for (int c = threadIdx.x; c < hp; c += blockDim.x) {
+    float s = 0.f;
+    if (c < hidden) s = parts[((int64_t)(c / hg) * b + i) * hg + c % hg];
+    s += b1[c];
+    const float hv = s > 0.f ? s : 0.f;
+    h[(int64_t)i * hp + c] = hv;
+    const unsigned bal = __ballot_sync(0xffffffffu, hv > 0.f);
+    if (lane == 0) hmask[(int64_t)i * (hp >> 5) + (c >> 5)] = bal;
+  }
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  build_live_cols(hp, gridDim.x, hmask, live);
+  if (threadIdx.x == 0) *ticket = 0;
+}
+
+void launch_shard_assemble(int hp, int hidden, int hg, int b, const float* parts, const float* b1, float* h,
+                           uint32_t* hmask, int32_t* live, int32_t* ticket, cudaStream_t s) {
+  if (b <= 0) return;
+  shard_assemble_kernel<<<b, 256, 0, s>>>(hp, hidden, hg, b, parts, b1, h, hmask, live, ticket);
+  SLIDE_LAUNCH_CHECK();
+}
+
+// W1 Adam on this rank's hg hidden units (reference network.py:428-451 for
+// layer 0): one warp per distinct input feature of the batch, lanes on the
+// shard's columns, the feature's samples walked in slot order; unit c moves
+// for sample i iff h_i[c] > 0, with its bias corrections bc[i][c] (the
+// replicated hidden_prep_bias_kernel's) and gradient dh_i[c] x_i[f].
+__global__ void __launch_bounds__(256) adam_w1_shard_kernel(int hp, int hg, int c0, AdamParams ap,
+                                                            const int32_t* __restrict__ n_uniq,
+                                                            const int32_t* __restrict__ uniq,
+                                                            const int32_t* __restrict__ seg_off,
+                                                            const int32_t* __restrict__ seg_cnt,
+                                                            const int32_t* __restrict__ sorted_k,
+                                                            const int32_t* __restrict__ x_slot,
+                                                            const float* __restrict__ x_val, int64_t x_base,
+                                                            const float* __restrict__ h, const float* __restrict__ dh,
+                                                            const float2* __restrict__ bc, float* __restrict__ w1s,
+                                                            float* __restrict__ m1s, float* __restrict__ v1s,
+                                                            unsigned long long* touched) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nu = *n_uniq;
+  const AdamK ak(ap);
+  for (int64_t u = gw; u < nu; u += nw) {
+    const int f = uniq[u], s0 = seg_off[u], len = seg_cnt[u];
+    int moved = 0;
+    for (int j0 = 0; j0 < hg; j0 += 32) {
+      const int j = j0 + lane;
+      const bool mine = j < hg;
+      const int c = c0 + (mine ? j : 0);
+      const int64_t ro = (int64_t)f * hg + (mine ? j : 0);
+      float w = mine ? w1s[ro] : 0.f, m = mine ? m1s[ro] : 0.f, v = mine ? v1s[ro] : 0.f;
+      for (int t = 0; t < len; ++t) {
+        const int k = sorted_k[s0 + t];
+        const unsigned off = (unsigned)(x_slot[k] * hp + c);
+        const float xv = x_val[x_base + k];
+        const float hv = __ldg(h + off);
+        const bool on = mine && hv > 0.f;
+        const float2 cc = on ? __ldg(bc + off) : make_float2(0.f, 1.f);
+        adam_coord_if(on, w, m, v, __ldg(dh + off) * xv, cc.x, cc.y, ak);
+        moved |= on;
+      }
+      if (mine) {
+        w1s[ro] = w;
+        m1s[ro] = m;
+        v1s[ro] = v;
+      }
+    }
+    if (touched) {
+      const int tc = __popc(__ballot_sync(0xffffffffu, moved));
+      if (lane == 0) atomicAdd(touched, (unsigned long long)tc);
+    }
+  }
+}
+
+void launch_adam_w1_shard(int hp, int hg, int c0, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq,
+                          const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt, const int32_t* sorted_k,
+                          const int32_t* x_slot, const float* x_val, int64_t x_base, const float* h, const float* dh,
+                          const float2* bc, float* w1s, float* m1s, float* v1s, unsigned long long* touched,
+                          cudaStream_t s) {
+  if (max_uniq <= 0) return;
+  const int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * 16);
+  adam_w1_shard_kernel<<<grid, 256, 0, s>>>(hp, hg, c0, ap, n_uniq, uniq, seg_off, seg_cnt, sorted_k, x_slot, x_val,
+                                            x_base, h, dh, bc, w1s, m1s, v1s, touched);
+  SLIDE_LAUNCH_CHECK();
+}
+
+}  // namespace slide

@@ -164,11 +164,25 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
       if (ufreq[u] & 127) atomicAdd(&s_hist[ufreq[u] & 127], 1);
   }
   __syncthreads();
+  if (a.hist_out) {  // sharded phase 1: this rank's counts, summed over ranks by the caller
+    int nsel_local = 0;
+    if (a.strategy == 2)
+      for (int u = u0; u < u1; ++u) nsel_local += (ufreq[u] & 127) >= a.min_freq;
+    else
+      for (int u = u0; u < u1; ++u) nsel_local += (ufreq[u] & 127) > 0;
+    int before, all;
+    Scan(scan_tmp).ExclusiveSum(nsel_local, before, all);
+    int32_t* ho = a.hist_out + (int64_t)i * (L + 1);
+    for (int p = tid; p < L; p += kSelThreads) ho[p] = a.strategy == 0 ? s_hist[p] : 0;
+    if (tid == 0) ho[L] = all;
+    return;
+  }
+  const int32_t* gh = a.ghist ? a.ghist + (int64_t)i * (L + 1) : nullptr;
   if (tid == 0) {
     if (a.strategy == 0) {
       int acc = 0, tau = L;
       for (int p = 0; p < L; ++p) {
-        acc += s_hist[p];
+        acc += gh ? gh[p] : s_hist[p];
         if (acc >= a.beta) {
           tau = p + 1;
           break;
@@ -227,6 +241,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     }
   }
   int any = __syncthreads_or(nsel > 0);
+  if (gh) any = gh[L] > 0;  // sharded: empty only when every rank's rule selects nothing
   if (!any) {
     if (tid == 0) {
       a.empty[i] = 1;
@@ -296,7 +311,13 @@ __global__ void __launch_bounds__(kUnionThreads) select_union_kernel(SelectArgs 
     if (a.cand_ctr) atomicAdd(a.cand_ctr, (unsigned long long)t);
   }
   __syncthreads();
-  if (s_tot == 0) {  // nothing retrieved: the fallback kernel takes this slot
+  if (a.hist_out) {  // sharded phase 1: this rank's retrieved count (ids are disjoint across ranks)
+    int32_t* ho = a.hist_out + (int64_t)i * (L + 1);
+    for (int p = tid; p <= L; p += kUnionThreads) ho[p] = p == L ? s_tot : 0;
+    return;
+  }
+  if (a.ghist ? a.ghist[(int64_t)i * (L + 1) + L] == 0 : s_tot == 0) {
+    // nothing retrieved (on any rank): the fallback kernel takes this slot
     if (tid == 0) {
       a.empty[i] = 1;
       a.cnt[i] = 0;
@@ -545,6 +566,17 @@ __global__ void __launch_bounds__(kOwnThreads) own_filter_kernel(int32_t* __rest
     cnt_all[i] = n;
     cnt[i] = total;
   }
+}
+
+__global__ void counts_to_f64_kernel(int b, const int32_t* __restrict__ cnt, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < b) out[i] = (double)cnt[i];
+}
+
+void launch_counts_to_f64(int b, const int32_t* cnt, double* out, cudaStream_t s) {
+  if (b <= 0) return;
+  counts_to_f64_kernel<<<(b + 255) / 256, 256, 0, s>>>(b, cnt, out);
+  SLIDE_LAUNCH_CHECK();
 }
 
 void launch_own_filter(int b, int32_t* act, int64_t cap_max, int g, int G, int32_t* cnt, int32_t* cnt_all,

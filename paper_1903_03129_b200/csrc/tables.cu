@@ -27,7 +27,8 @@ void TablesHost::release() {
 constexpr int kSortRows = 64;
 
 __global__ void __launch_bounds__(256) sort_input_kernel(const uint32_t* __restrict__ keys, int64_t n, int l, int kb,
-                                                         uint32_t* __restrict__ skeys, int32_t* __restrict__ vals) {
+                                                         uint32_t* __restrict__ skeys, int32_t* __restrict__ vals,
+                                                         int id_mul, int id_add) {
   extern __shared__ uint32_t tile[];  // [kSortRows][l + 1] (padded: conflict-free column reads)
   for (int64_t r0 = (int64_t)blockIdx.x * kSortRows; r0 < n; r0 += (int64_t)gridDim.x * kSortRows) {
     const int nr = (int)min((int64_t)kSortRows, n - r0);
@@ -38,7 +39,7 @@ __global__ void __launch_bounds__(256) sort_input_kernel(const uint32_t* __restr
       const int t = q / nr, i = q - t * nr;
       const int64_t o = (int64_t)t * n + r0 + i;
       skeys[o] = ((uint32_t)t << kb) | tile[i * (l + 1) + t];
-      vals[o] = (int32_t)(r0 + i);
+      vals[o] = (int32_t)((r0 + i) * id_mul + id_add);
     }
   }
 }
@@ -146,7 +147,7 @@ static void choose_dir(TablesHost& tb, TablesDev& d, int l, int kb, int64_t n_it
 static int grid_for(int64_t n, int bs = 256) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, bs), kSms * 16)); }
 
 void tables_build(TablesHost& tb, const uint32_t* keys, int64_t n, int l, int kb, int cap, int policy,
-                  uint64_t* mt_state, cudaStream_t s) {
+                  uint64_t* mt_state, cudaStream_t s, int id_mul, int id_add) {
   int tbits = 0;
   while ((1 << tbits) < l) ++tbits;
   SLIDE_CHECK(kb + tbits <= 32, kNotSupported, "table index + key bits must fit in 32 bits");
@@ -162,7 +163,7 @@ void tables_build(TablesHost& tb, const uint32_t* keys, int64_t n, int l, int kb
   int32_t* nr_d = tb.nruns.ensure<int32_t>(1);
   if (total > 0) {
     sort_input_kernel<<<grid_for(ceil_div(n, kSortRows), 1), 256, (size_t)kSortRows * (l + 1) * 4, s>>>(keys, n, l, kb, ska,
-                                                                                               va);
+                                                                                               va, id_mul, id_add);
     SLIDE_LAUNCH_CHECK();
   }
   const int end_bit = kb + tbits;
@@ -197,7 +198,7 @@ void tables_build(TablesHost& tb, const uint32_t* keys, int64_t n, int l, int kb
                                                  dir, hdir, hmask, bstart, blen, ovf);
     SLIDE_LAUNCH_CHECK();
   }
-  if (policy == 1 && n_runs > 0) {
+  if (policy == 1 && n_runs > 0 && id_mul == 1) {
     // reservoir: host replay of the overflowing inserts (tables.py:156-161)
     int32_t* ovf_off = tb.ovf_off.ensure<int32_t>(n_runs);
     size_t b4 = 0;
@@ -303,6 +304,128 @@ void tables_load(TablesHost& tb, const uint32_t* skeys, const int32_t* counts, c
   d.disabled = 0;
   tb.n_items = n_items;
   tb.built = true;
+}
+
+// ------------------------------------------------ column-sharded tables
+// rank g builds its tables from its own rows (global ids
+// r G + g, ascending within a bucket, like the unsharded insert order).  A
+// global FIFO bucket keeps its cap highest ids (tables.py:130-145); when a
+// bucket may overflow globally the ranks exchange their runs (packed below)
+// and each keeps the ids at or above the bucket's cap-th highest id over all
+// ranks.  Pack layout (int32): [R, S, skeys R, counts R, starts R, lens R,
+// ids S] -- the runs' keys ascending, insert counts, kept tails (start, len)
+// into the rank's sorted id array, which follows whole (S = its inserts).
+int64_t tables_pack_size(const TablesHost& tb) { return 2 + 4 * tb.dev.n_runs + tb.n_slots; }
+
+__global__ void pack_header_kernel(int32_t* out, int32_t r, int32_t sl) {
+  out[0] = r;
+  out[1] = sl;
+}
+
+void tables_pack(const TablesHost& tb, int32_t* out, cudaStream_t s) {
+  const int64_t r = tb.dev.n_runs, ns = tb.n_slots;
+  pack_header_kernel<<<1, 1, 0, s>>>(out, (int32_t)r, (int32_t)ns);
+  SLIDE_LAUNCH_CHECK();
+  if (r) {
+    SLIDE_CUDA(cudaMemcpyAsync(out + 2, tb.dev.run_keys, r * 4, cudaMemcpyDeviceToDevice, s));
+    SLIDE_CUDA(cudaMemcpyAsync(out + 2 + r, tb.dev.bcount, r * 4, cudaMemcpyDeviceToDevice, s));
+    SLIDE_CUDA(cudaMemcpyAsync(out + 2 + 2 * r, tb.dev.bstart, r * 4, cudaMemcpyDeviceToDevice, s));
+    SLIDE_CUDA(cudaMemcpyAsync(out + 2 + 3 * r, tb.dev.blen, r * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  if (ns) SLIDE_CUDA(cudaMemcpyAsync(out + 2 + 4 * r, tb.dev.ids, ns * 4, cudaMemcpyDeviceToDevice, s));
+}
+
+constexpr int kRecWarps = 8;
+
+// one warp per local run: the bucket's lists on every rank (<= cap ids each,
+// ascending) are staged in shared memory; the threshold T = the cap-th
+// highest id overall is found by bisection on the id value with warp-wide
+// counts; the local run keeps its ids >= T.
+__global__ void __launch_bounds__(kRecWarps * 32) reconcile_kernel(const int32_t* __restrict__ packs, int64_t stride,
+                                                                   int G, int g, int cap, int64_t n_runs,
+                                                                   const uint32_t* __restrict__ run_keys,
+                                                                   int32_t* __restrict__ bstart,
+                                                                   int32_t* __restrict__ blen,
+                                                                   int32_t* __restrict__ bcount,
+                                                                   const int32_t* __restrict__ ids) {
+  extern __shared__ int32_t lists[];  // [kRecWarps][G * cap]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* buf = lists + (size_t)warp * G * cap;
+  for (int64_t r = (int64_t)blockIdx.x * kRecWarps + warp; r < n_runs; r += (int64_t)gridDim.x * kRecWarps) {
+    const uint32_t sk = run_keys[r];
+    int total = 0, n = 0;
+    for (int q = 0; q < G; ++q) {
+      const int32_t* pk = packs + q * stride;
+      const int R = pk[0];
+      const uint32_t* keys = reinterpret_cast<const uint32_t*>(pk + 2);
+      int start = 0, len = 0, cnt = 0;
+      if (q == g) {
+        start = -1;
+        len = blen[r];
+        cnt = bcount[r];
+      } else if (lane == 0) {
+        int lo = 0, hi = R;  // first key >= sk
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (keys[mid] < sk) lo = mid + 1;
+          else hi = mid;
+        }
+        if (lo < R && keys[lo] == sk) {
+          cnt = pk[2 + R + lo];
+          start = pk[2 + 2 * R + lo];
+          len = pk[2 + 3 * R + lo];
+        }
+      }
+      start = __shfl_sync(0xffffffffu, start, 0);
+      len = __shfl_sync(0xffffffffu, len, 0);
+      cnt = __shfl_sync(0xffffffffu, cnt, 0);
+      total += cnt;
+      const int32_t* src = q == g ? ids + bstart[r] : pk + 2 + 4 * R + start;
+      for (int j = lane; j < len; j += 32) buf[n + j] = src[j];
+      n += len;
+    }
+    __syncwarp();
+    if (total > cap) {
+      // largest T with #(ids >= T) >= cap; ids are distinct and < 2^31
+      int64_t lo = 0, hi = 0x7fffffff;
+      while (lo < hi) {  // <= 31 rounds
+        const int64_t mid = lo + ((hi - lo + 1) >> 1);
+        int c = 0;
+        for (int j = lane; j < n; j += 32) c += buf[j] >= mid;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (c >= cap) lo = mid;
+        else hi = mid - 1;
+      }
+      const int32_t* own = ids + bstart[r];
+      const int len = blen[r];
+      int below = 0;
+      for (int j = lane; j < len; j += 32) below += (int64_t)own[j] < lo;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+      if (lane == 0) {
+        bstart[r] += below;
+        blen[r] = len - below;
+      }
+    }
+    if (lane == 0) bcount[r] = total;
+    __syncwarp();
+  }
+}
+
+void tables_reconcile(TablesHost& tb, const int32_t* packs, int64_t stride, int G, int g, int cap, cudaStream_t s) {
+  const int64_t r = tb.dev.n_runs;
+  if (r <= 0) return;
+  SLIDE_CHECK((int64_t)G * cap <= 4096, kNotSupported, "sharded table reconciliation needs shard_count * cap <= 4096");
+  const size_t smem = (size_t)kRecWarps * G * cap * 4;
+  if (smem > 48 * 1024)
+    SLIDE_CUDA(cudaFuncSetAttribute(reconcile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = (int)std::min<int64_t>(ceil_div(r, kRecWarps), (int64_t)kSms * 8);
+  reconcile_kernel<<<grid, kRecWarps * 32, smem, s>>>(packs, stride, G, g, cap, r, tb.dev.run_keys,
+                                                      const_cast<int32_t*>(tb.dev.bstart),
+                                                      const_cast<int32_t*>(tb.dev.blen),
+                                                      const_cast<int32_t*>(tb.dev.bcount), tb.dev.ids);
+  SLIDE_LAUNCH_CHECK();
 }
 
 }  // namespace slide

@@ -349,15 +349,22 @@ class SlideNetwork:
         f32 = dict(dtype=torch.float32, device=dev)
         # -- parameters: the reference's draw order (network.py:79-89, 187-193)
         rng = np.random.default_rng(cfg.seed)
-        self.w1t = torch.zeros((D, hp), **f32)
+        # sharded: W1^T holds this rank's hidden units [u0, u0 + hg)
+        if G > 1 and (H % G or (H // G) % 4 or H // G > 128):
+            raise NotImplementedError("sharded hidden layer: hidden / shard_count must be a multiple of 4, <= 128")
+        hg = H // G if G > 1 else hp
+        u0 = g * hg if G > 1 else 0
+        self.w1t = torch.zeros((D, hg), **f32)
         bound = 1.0 / np.sqrt(D)
         rows = max(1, (1 << 22) // D)
         for r0 in range(0, H, rows):
             r1 = min(H, r0 + rows)
             chunk = rng.uniform(-bound, bound, size=(r1 - r0, D)).astype(np.float32)
-            self.w1t[:, r0:r1] = torch.from_numpy(chunk).to(dev).T
-        self.m1t = torch.zeros((D, hp), **f32)
-        self.v1t = torch.zeros((D, hp), **f32)
+            a, b = max(r0, u0), min(r1, u0 + (H if G == 1 else hg))
+            if a < b:
+                self.w1t[:, a - u0 : b - u0] = torch.from_numpy(chunk[a - r0 : b - r0]).to(dev).T
+        self.m1t = torch.zeros((D, hg), **f32)
+        self.v1t = torch.zeros((D, hg), **f32)
         self.b1 = torch.zeros(hp, **f32)
         self.mb1 = torch.zeros(hp, **f32)
         self.vb1 = torch.zeros(hp, **f32)
@@ -427,10 +434,9 @@ class SlideNetwork:
         lsh = self.layers[1].lsh
         st = _lib.mt_state_from_random(lsh._rng)
         if self.shard_count > 1:
-            from .sharded import gather_row_keys
+            from .sharded import GpuShardBackend, rebuild_sharded
 
-            keys = gather_row_keys(self, self.group)
-            _lib.call("slide_build_tables_from_keys", self._ctx, keys.data_ptr(), self.n_out, st.ctypes.data)
+            rebuild_sharded(GpuShardBackend(self), self.group)
         else:
             _lib.call("slide_rebuild_tables", self._ctx, st.ctypes.data)
         _lib.mt_state_to_random(st, lsh._rng)
@@ -449,6 +455,11 @@ class SlideNetwork:
 
         dev = _device.device()
         self.h2d_bytes = 0
+        # the pinned staging buffers are reused: the previous upload's
+        # asynchronous copies must have read them before they are rewritten
+        ev = getattr(self, "_pin_ev", None)
+        if ev is not None:
+            ev.synchronize()
 
         def up(a, dt):
             # stage through a pinned host buffer so the copy is a true async DMA
@@ -474,6 +485,9 @@ class SlideNetwork:
         }
         hx = np.ascontiguousarray(csr.x_ptr, dtype=np.int32)
         hy = np.ascontiguousarray(csr.y_ptr, dtype=np.int32)
+        if rng_states is None and forced is None:
+            self._pin_ev = torch.cuda.Event()
+            self._pin_ev.record()
         bt = _lib.Batch()
         bt.batch = csr.batch
         bt.x_ptr, bt.x_idx, bt.x_val = t["x_ptr"].data_ptr(), t["x_idx"].data_ptr(), t["x_val"].data_ptr()
@@ -491,6 +505,9 @@ class SlideNetwork:
             t["fidx"] = up(fi if len(fi) else np.zeros(1), np.int32)
             bt.forced_ptr, bt.forced_idx, bt.forced_ptr_host = t["fptr"].data_ptr(), t["fidx"].data_ptr(), hf.ctypes.data
             keep.append(hf)
+        if rng_states is not None or forced is not None:
+            self._pin_ev = torch.cuda.Event()
+            self._pin_ev.record()
         return bt, keep
 
     def _read(self, what, n, dtype):
@@ -527,7 +544,7 @@ class SlideNetwork:
                 raise NotImplementedError("the sharded output layer runs the snapshot schedule")
             from .sharded import GpuShardBackend, sharded_step
 
-            loss, active = sharded_step(GpuShardBackend(self), csr, iteration, self.group)
+            loss, active = sharded_step(GpuShardBackend(self), csr, iteration, self.group).host()
         else:
             loss, active = self._step(csr, iteration, 1 if schedule == "sequential" else B)
         return self._barrier(iteration, loss, active)

@@ -389,7 +389,7 @@ def _round_f32(net):
             a[...] = a.astype(np.float32).astype(np.float64)
 
 
-def _p1_runs(corpus, evals, n_steps, rounded):
+def _p1_runs(corpus, evals, n_steps, rounded, noise=0.0, noise_seed=0):
     """Reference sequential (train_network, workers=1) and snapshot runs over
     the same batches; P@1 on ``evals`` with the evaluator's shared rng."""
     from slide.data import Dataset, precision_at_k
@@ -412,14 +412,28 @@ def _p1_runs(corpus, evals, n_steps, rounded):
         rng = np.random.default_rng(0)
         return float(np.mean([precision_at_k(net.predict(x, rng=rng)[:1], y, 1) for x, y in evals]))
 
+    nrng = np.random.default_rng(noise_seed)
+
+    def jitter(net):
+        if noise:
+            for layer in net.layers:
+                layer.w *= 1 + noise * nrng.standard_normal(layer.w.shape)
+
     net = make()
     seq = []
-    train_network(net, Dataset(train, w.input_dim, w.n_out), on_batch=lambda it, st: seq.append(st.loss))
+
+    def on_seq(it, st):
+        seq.append(st.loss)
+        jitter(net)
+
+    train_network(net, Dataset(train, w.input_dim, w.n_out), on_batch=on_seq)
     seq_p1 = p_at_1(net)
     net = make()
     order = np.random.default_rng((0, 0)).permutation(n_train)
-    snap = [snapshot_step(net, [train[i] for i in order[(it - 1) * w.batch : it * w.batch]], it)
-            for it in range(1, n_steps + 1)]
+    snap = []
+    for it in range(1, n_steps + 1):
+        snap.append(snapshot_step(net, [train[i] for i in order[(it - 1) * w.batch : it * w.batch]], it))
+        jitter(net)
     return np.array(seq), seq_p1, np.array(snap), p_at_1(net)
 
 
@@ -431,7 +445,10 @@ def p1_runs():
     the features, so P@1 moves by points under rounding alone.  (2) A
     learnable corpus (tests/learnable_corpus.py) at the tiny shape, where
     P@1 measures the training algorithm: reference sequential and snapshot
-    runs from the f64 init and from the fp32-rounded one."""
+    runs from the f64 init and from the fp32-rounded one.  (3) Rounding-noise
+    ensembles: the reference re-run with every weight multiplied by
+    (1 + 3e-8 N(0,1)) after every step (fp32 half-ulp noise, four seeds) --
+    the spread a correct fp32 implementation can land in."""
     from tests.learnable_corpus import learnable_corpus
 
     w = TINY
@@ -448,12 +465,64 @@ def p1_runs():
         sl, sp, nl, np1 = _p1_runs(lc, levals, 200, rounded)
         out["learn_seq_loss" + tag], out["learn_seq_p1" + tag] = sl, np.array([sp])
         out["learn_snap_loss" + tag], out["learn_snap_p1" + tag] = nl, np.array([np1])
+    for tag, (cor, ev) in (("tiny", (corpus, evals)), ("learn", (lc, levals))):
+        ens = [_p1_runs(cor, ev, 200, True, noise=3e-8, noise_seed=s) for s in range(4)]
+        out[f"{tag}_seq_p1_noise"] = np.array([e[1] for e in ens])
+        out[f"{tag}_snap_p1_noise"] = np.array([e[3] for e in ens])
     out["tiny_seq_p1_f32init"] = np.array([out["tiny_seq_p1_f32init"]])
     out["tiny_snap_p1_f32init"] = np.array([out["tiny_snap_p1_f32init"]])
     out["learn_check"] = np.array([lc.x_idx.astype(np.int64).sum(), lc.y_idx.astype(np.int64).sum(),
                                    lh.x_idx.astype(np.int64).sum(), lh.y_idx.astype(np.int64).sum()])
     print({k: v for k, v in out.items() if "p1" in k})
     save("p1_runs.npz", **out)
+
+
+def p1_seeds():
+    """The P@1 criterion as a distribution: on the learnable corpus (tiny
+    shape, 200 steps) a single run's P@1 swings by tens of points between
+    consecutive checkpoints (per-sample Adam at lr 1e-3), so the reference is
+    run for seeds 0..3 in both schedules and P@1 (2,000 held-out examples,
+    evaluator rng default_rng(0)) recorded after steps 150, 175 and 200."""
+    from slide.data import Dataset, precision_at_k
+    from slide.network import train_network
+
+    from tests.learnable_corpus import learnable_corpus
+
+    w = TINY
+    n_train = 200 * w.batch
+    lc = learnable_corpus(w.input_dim, w.n_out, n_train, seed=0)
+    lh = learnable_corpus(w.input_dim, w.n_out, 2000, seed=1)
+    train = [lc.example(i) for i in range(n_train)]
+    evals = [lh.example(i) for i in range(len(lh))]
+    marks = (150, 175, 200)
+
+    def p_at_1(net):
+        rng = np.random.default_rng(0)
+        return float(np.mean([precision_at_k(net.predict(x, rng=rng)[:1], y, 1) for x, y in evals]))
+
+    out = {"marks": np.array(marks)}
+    for seed in range(4):
+        def make():
+            cfg = TrainConfig(batch_size=w.batch, seed=seed, learning_rate=w.lr, n0=w.n0, decay=w.decay)
+            lsh = LshLayerConfig("simhash", k=w.k, l=w.l, capacity=w.cap,
+                                 sampler=SamplerConfig("vanilla", beta=w.beta))
+            return SlideNetwork(w.input_dim, [w.hidden, w.n_out], cfg, lsh_layers={1: lsh})
+
+        net = make()
+        got = []
+        train_network(net, Dataset(train, w.input_dim, w.n_out),
+                      on_batch=lambda it, st: got.append(p_at_1(net)) if it in marks else None)
+        out[f"seq_seed{seed}"] = np.array(got)
+        net = make()
+        order = np.random.default_rng((seed, 0)).permutation(n_train)
+        got = []
+        for it in range(1, 201):
+            snapshot_step(net, [train[i] for i in order[(it - 1) * w.batch : it * w.batch]], it)
+            if it in marks:
+                got.append(p_at_1(net))
+        out[f"snap_seed{seed}"] = np.array(got)
+        print(seed, out[f"seq_seed{seed}"], out[f"snap_seed{seed}"], flush=True)
+    save("p1_seeds.npz", **out)
 
 
 from tests.golden.make_golden_data import XC_BAD, XC_GOOD  # noqa: E402
@@ -521,6 +590,6 @@ def checkpoint():
 if __name__ == "__main__":
     assert slide.__version__ == "0.1.0"
     which = sys.argv[1:] or ["rng_streams", "mt19937", "hashing", "tables", "samplers", "network", "tiny_config",
-                             "tiny_run", "p1_runs", "data_io", "checkpoint"]
+                             "tiny_run", "p1_runs", "p1_seeds", "data_io", "checkpoint"]
     for name in which:
         globals()[name]()
