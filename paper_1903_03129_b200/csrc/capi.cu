@@ -127,6 +127,10 @@ struct slide_ctx {
     bool used = false;
   } gslot[2];
   cudaStream_t cstream = nullptr;
+  // results read back on their own stream: the next step's staging (cstream)
+  // must not queue behind this step's device-to-host copy, which waits for
+  // the step to finish -- it would put the staging on the critical path
+  cudaStream_t ostream = nullptr;
   int g_next = 0;      // slot of the next launch
   int g_q[2] = {0, 0};  // pending slots, oldest first
   int64_t g_qb[2] = {0, 0};
@@ -343,6 +347,7 @@ int slide_destroy(slide_ctx* c) {
     for (DBuf* b : {&c->iter_dev, &c->gx_ptr, &c->gx_idx, &c->gx_val, &c->gy_ptr, &c->gy_idx}) b->release();
     if (c->gstream) cudaStreamSynchronize(c->gstream);
     if (c->cstream) cudaStreamSynchronize(c->cstream);
+    if (c->ostream) cudaStreamSynchronize(c->ostream);
     for (auto& g : c->gslot) {
       if (g.ptrs) cudaFreeHost(g.ptrs);
       if (g.loss) cudaFreeHost(g.loss);
@@ -354,6 +359,7 @@ int slide_destroy(slide_ctx* c) {
     if (c->gev_in) cudaEventDestroy(c->gev_in);
     if (c->gstream) cudaStreamDestroy(c->gstream);
     if (c->cstream) cudaStreamDestroy(c->cstream);
+    if (c->ostream) cudaStreamDestroy(c->ostream);
     if (c->pinned_loss) cudaFreeHost(c->pinned_loss);
     if (c->pinned_cnt) cudaFreeHost(c->pinned_cnt);
     for (cudaEvent_t e : c->timer.pool) cudaEventDestroy(e);
@@ -1062,6 +1068,7 @@ static void graph_step_launch(slide_ctx* c, const slide_batch* bt, int64_t itera
       SLIDE_CUDA(cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
       SLIDE_CUDA(cudaEventCreateWithFlags(&c->gev_in, cudaEventDisableTiming));
       SLIDE_CUDA(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+      SLIDE_CUDA(cudaStreamCreateWithFlags(&c->ostream, cudaStreamNonBlocking));
       for (auto& g : c->gslot)
         for (cudaEvent_t* e : {&g.ev, &g.ev_staged, &g.ev_consumed, &g.ev_dev})
           SLIDE_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -1243,9 +1250,9 @@ static void graph_step_launch(slide_ctx* c, const slide_batch* bt, int64_t itera
       launch_copy_in(co, gs);
     }
     SLIDE_CUDA(cudaEventRecord(gsl.ev_dev, gs));
-    SLIDE_CUDA(cudaStreamWaitEvent(cs, gsl.ev_dev, 0));
-    SLIDE_CUDA(cudaMemcpyAsync(gsl.loss, gout, B * 12, cudaMemcpyDeviceToHost, cs));
-    SLIDE_CUDA(cudaEventRecord(gsl.ev, cs));
+    SLIDE_CUDA(cudaStreamWaitEvent(c->ostream, gsl.ev_dev, 0));
+    SLIDE_CUDA(cudaMemcpyAsync(gsl.loss, gout, B * 12, cudaMemcpyDeviceToHost, c->ostream));
+    SLIDE_CUDA(cudaEventRecord(gsl.ev, c->ostream));
     SLIDE_CUDA(cudaStreamWaitEvent(user, gsl.ev_dev, 0));
     gsl.used = true;
     c->g_q[c->g_qn] = slot;
