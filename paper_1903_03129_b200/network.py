@@ -773,7 +773,7 @@ class SlideNetwork:
         order = np.argsort(-trace.probs, kind="stable")
         return trace.active[-1][order]
 
-    def predict_batch(self, xs, topn: int = 5, rng=None, sampled: bool = True) -> list:
+    def predict_batch(self, xs, topn: int = 5, rng=None, sampled: bool = True, fresh_seed=None) -> list:
         """Ranked label ids (best first, at most ``topn``) for many inputs,
         equal to ``[self.predict(x, rng=rng)[:topn] for x in xs]`` with one
         generator shared across the queries in order -- the evaluator's
@@ -787,7 +787,11 @@ class SlideNetwork:
         flags, the host advances the caller's generator through exactly the
         reference's draws recording each query's starting state, and the
         second pass replays every slot from its own state; the device then
-        ranks each slot (``slide_topk``)."""
+        ranks each slot (``slide_topk``).
+
+        ``fresh_seed``: every query starts from its own ``default_rng(fresh_seed)``
+        instead -- the CLI evaluator's per-call generator (reference
+        cli.py:167-178 calling estimator.py:203-207 once per example)."""
         check_positive_int(topn, "topn")
         xs = list(xs)
         for x in xs:
@@ -818,7 +822,9 @@ class SlideNetwork:
                 empty = self._read(9, nb, np.int32)
                 states = np.empty((nb, 6), np.uint64)
                 L = lsh.family.l
-                for i in range(nb):
+                if fresh_seed is not None:
+                    states[:] = _lib.pcg64_state_from_generator(np.random.default_rng(fresh_seed))
+                for i in range(nb if fresh_seed is None else 0):
                     states[i] = _lib.pcg64_state_from_generator(rng)
                     if cfg.strategy == "vanilla":
                         rng.permutation(L)

@@ -587,9 +587,32 @@ def checkpoint():
     save("checkpoint.npz", **out)
 
 
+def cli():
+    """The reference CLI's config parsing and config hash (cli.py:99-123) on a
+    TOML exercising every section, plus its rejection of unknown keys."""
+    import tempfile
+
+    from slide.cli import config_hash, load_config
+
+    from tests.golden.make_golden_data import CLI_TOML
+
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "run.toml")
+        with open(path, "w") as fh:
+            fh.write(CLI_TOML)
+        cfg = load_config(path)
+    import dataclasses
+
+    from slide.cli import RunConfig
+
+    save("cli.npz", hash=np.array([config_hash(cfg)]), hash_default=np.array([config_hash(RunConfig())]),
+         beta=np.array([cfg.beta]), hidden=np.array(cfg.hidden),
+         fields=np.array([f.name for f in dataclasses.fields(RunConfig)]))
+
+
 if __name__ == "__main__":
     assert slide.__version__ == "0.1.0"
     which = sys.argv[1:] or ["rng_streams", "mt19937", "hashing", "tables", "samplers", "network", "tiny_config",
-                             "tiny_run", "p1_runs", "p1_seeds", "data_io", "checkpoint"]
+                             "tiny_run", "p1_runs", "p1_seeds", "data_io", "checkpoint", "cli"]
     for name in which:
         globals()[name]()

@@ -23,3 +23,28 @@ XC_BAD = {
     "too_many": "1 4 4\n1 2:1.0\n2 1:1.0\n",
     "too_few": "3 4 4\n1 2:1.0\n",
 }
+
+# a run config exercising every section (the CLI fixture)
+CLI_TOML = """
+[data]
+train = "train.txt"
+normalize = true
+[model]
+hidden = [64]
+lsh = "simhash"
+k = 5
+l = 8
+beta = 40
+bucket_capacity = 32
+[train]
+epochs = 2
+batch_size = 32
+learning_rate = 0.002
+n0 = 10
+seed = 7
+eval_every = 5
+eval_subsample = 100
+[bench]
+bench_sizes = [100, 1000]
+bench_neurons = 2000
+"""
