@@ -664,6 +664,7 @@ def run_reference(args, rank, world):
         build_s = time.perf_counter() - t0
     dt = dt - sum(rb_s) + args.steps * build_s / w.n0
     v = args.steps * per_step / dt
+    pkg = run_reference_package(args, w, per_step, corpus, cores)
     sample = (f"{args.steps} steps x {per_step} samples (the full batch) of {w.name}, snapshot schedule on "
               f"{cores} processes (numpy), table build {build_s:.2f} s amortised over n0={w.n0} steps")
     return {
@@ -674,7 +675,62 @@ def run_reference(args, rank, world):
         "config": config_of(w, args, world),
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_package": pkg,
     }
+
+
+def run_reference_package(args, w, per_step, corpus, cores):
+    """The reference package itself (``slide`` 0.1.0, pip-installed into
+    baseline/_ref when present -- git-ignored, it travels with the repo),
+    timed beside the port on the same batches: ``SlideNetwork.train_batch``
+    with ``workers = cpu_count`` threads (its HOGWILD path, network.py:340-379),
+    a bounded number of steps after one warm-up step, the table build
+    amortised over n0 like the other arms.  Reported, not the arm's value
+    (this tier's reference arm is the oracle port)."""
+    import importlib
+    from concurrent.futures import ThreadPoolExecutor
+
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "slide")) or os.environ.get("SLIDE_SKIP_REF_PACKAGE"):
+        return {"unavailable": "baseline/_ref holds no reference install"}
+    sys.path.insert(0, ref_dir)
+    try:
+        net_mod = importlib.import_module("slide.network")
+        smp = importlib.import_module("slide.samplers")
+        sp = importlib.import_module("slide.sparse")
+        cfg = net_mod.TrainConfig(batch_size=per_step, learning_rate=w.lr, n0=w.n0, decay=w.decay, seed=0)
+        spec = net_mod.LshLayerConfig(w.family, k=w.k, l=w.l, capacity=w.cap, policy=w.policy,
+                                      wta_bin_size=w.bin_size, sampler=smp.SamplerConfig(w.strategy, beta=w.beta))
+        t0 = time.perf_counter()
+        net = net_mod.SlideNetwork(w.input_dim, [w.hidden, w.n_out], cfg, lsh_layers={1: spec})
+        init_s = time.perf_counter() - t0
+        trip = corpus.triples()
+        steps = max(1, min(args.steps, 3))
+
+        def batch(it):
+            rows = trip[(it - 1) * per_step : it * per_step]
+            return [(sp.SparseVector(np.asarray(i, np.int64), np.asarray(v, np.float64), w.input_dim), list(y))
+                    for i, v, y in rows]
+
+        with ThreadPoolExecutor(max_workers=cores) as ex:
+            net.train_batch(batch(1), 1, workers=cores, executor=ex)
+            t0 = time.perf_counter()
+            for it in range(2, steps + 2):
+                net.train_batch(batch(it), it, workers=cores, executor=ex)
+            dt = time.perf_counter() - t0
+        layer = net.layers[1]
+        t0 = time.perf_counter()
+        layer.lsh.build(layer.w)
+        build_s = time.perf_counter() - t0
+        dt += steps * build_s / w.n0
+        return {"value": steps * per_step / dt, "unit": "samples/s", "cores": cores, "kind": "reference",
+                "sample": (f"{steps} steps x {per_step} samples of {w.name} after one warm-up step through "
+                           f"slide.SlideNetwork.train_batch(workers={cores}) from baseline/_ref; table build "
+                           f"{build_s:.2f} s amortised over n0={w.n0}; init {init_s:.1f} s")}
+    except Exception as exc:  # the port stays the arm's value
+        return {"unavailable": f"{type(exc).__name__}: {exc}"[:300]}
+    finally:
+        sys.path.remove(ref_dir)
 
 
 def main():
