@@ -92,6 +92,9 @@ struct slide_ctx {
   // 1 = stop after the per-rank sampler counts, 2 = finish with the
   // all-reduced counts; 0 = unsharded
   int shard_phase = 0;
+  // the last forward's row grouping ran place-free (see forward_impl)
+  bool rows_mode = false;
+  DBuf prob_tmp;
   const int32_t* shard_ghist = nullptr;
   int32_t* shard_hist = nullptr;
   DBuf shard_pack;
@@ -161,6 +164,11 @@ struct slide_ctx {
 };
 
 static thread_local std::string g_err;
+
+static bool getenv_flag(const char* name) {  // experiments only
+  const char* e = getenv(name);
+  return e && *e && *e != '0';
+}
 
 template <class F>
 static int guarded(F&& f) {
@@ -331,7 +339,7 @@ int slide_destroy(slide_ctx* c) {
     for (DBuf* b : {&c->sh_packed, &c->sh_packed_t, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->dsort, &c->hmask, &c->live, &c->live_ticket, &c->qkeys, &c->order,
                     &c->states, &c->act, &c->cnt, &c->empty, &c->offs, &c->prow, &c->pslot, &c->plab, &c->z,
                     &c->prob, &c->delta, &c->loss, &c->dh, &c->fb_ids, &c->fb_scratch, &c->fb_bitmap, &c->xslot,
-                    &c->tc, &c->bc, &c->counters, &c->partial, &c->long_list, &c->n_long, &c->work, &c->topk_out, &c->topk_cnt, &c->tc_scratch, &c->bias_table, &c->cnt_all})
+                    &c->tc, &c->bc, &c->counters, &c->partial, &c->long_list, &c->n_long, &c->work, &c->topk_out, &c->topk_cnt, &c->tc_scratch, &c->bias_table, &c->cnt_all, &c->prob_tmp, &c->shard_pack})
       b->release();
     c->grow.release();
     c->gfeat.release();
@@ -782,18 +790,29 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   int32_t* prow = c->prow.ensure<int32_t>(P_max);
   int32_t* pslot = c->pslot.ensure<int32_t>(P_max);
   uint8_t* plab = c->plab.ensure<uint8_t>(P_max);
-  launch_pairs(b, act, cap_max, cnt, offs, c->G, prow, pslot, plab, s);
-  c->timer.mark(s, kStCompact);
-  float* z = c->z.ensure<float>(P_max);
-  float* prob = c->prob.ensure<float>(P_max);
-  float* delta = c->delta.ensure<float>(P_max);
-  double* loss = c->loss.ensure<double>(b);
   // group the pairs by output row (slot order inside a row): the row-major
   // logits, hidden gradient and W2 Adam all walk this structure
   GroupBy& gr = c->grow;
   if (c->grow_pending) gr.clear(s);
   gr.want_inv = true;  // the softmax scatters the errors into row-grouped order
   gr.prepare(c->n_local, b, P_max);
+  // unsharded dense grouping: the pairs kernel fills the row slot masks
+  // itself and no placement pass runs -- the logits are written in row order
+  // and the softmax finds each pair's row position from the masks
+  c->rows_mode = c->G == 1 && gr.dense && !getenv_flag("SLIDE_PLACED_GROUPING");
+  gr.premarked = c->rows_mode;
+  gr.place = !c->rows_mode;
+  if (c->rows_mode) {
+    const GroupBy::MarkArgs m = gr.mark_args();
+    launch_pairs(b, act, cap_max, cnt, offs, c->G, prow, pslot, plab, s, m.mask, m.wpk, m.status, m.ctr, m.n_tiles);
+  } else {
+    launch_pairs(b, act, cap_max, cnt, offs, c->G, prow, pslot, plab, s);
+  }
+  c->timer.mark(s, kStCompact);
+  float* z = c->z.ensure<float>(P_max);
+  float* prob = c->prob.ensure<float>(P_max);
+  float* delta = c->delta.ensure<float>(P_max);
+  double* loss = c->loss.ensure<double>(b);
   float* dsort = c->dsort.ensure<float>(P_max);
   gr.run(prow, pslot, offs + b, 0, P_max, s);
   c->grow_pending = true;
@@ -816,7 +835,12 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   }
   c->timer.mark(s, kStLogits);
   // sharded: the softmax is completed by the slide_shard_softmax_* stages
-  if (c->G == 1) launch_softmax(b, offs, plab, bt->y_ptr, z, prob, delta, loss, gr.inv.as<int32_t>(), dsort, s);
+  if (c->G == 1) {
+    const GroupView rv = gr.view();
+    launch_softmax(b, offs, plab, bt->y_ptr, z, prob, delta, loss, gr.inv.as<int32_t>(), dsort, s,
+                   c->rows_mode ? prow : nullptr, c->rows_mode ? &rv : nullptr,
+                   c->rows_mode ? gr.sslot.as<int32_t>() : nullptr);
+  }
   c->timer.mark(s, kStSoftmax);
   c->have_forward = true;
   c->last_b = b;
@@ -1314,7 +1338,17 @@ int slide_read(slide_ctx* c, int64_t what, void* dst, int64_t max_bytes, int64_t
       case 8: src = c->dh.p; n = b * hp * 4; break;
       case 9: src = c->empty.p; n = b * 4; break;
       case 10: src = c->states.p; n = b * 48; break;
-      case 11: src = c->z.p; n = P * 4; break;
+      case 11:  // logits per pair, sample-major (row order under the place-free grouping)
+        if (c->rows_mode) {
+          float* tmp = c->prob_tmp.ensure<float>(std::max<int64_t>(P, 1));
+          launch_rows_pairs((int)b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->grow.view(), c->z.as<float>(),
+                            tmp, true, c->s);
+          src = tmp;
+        } else {
+          src = c->z.p;
+        }
+        n = P * 4;
+        break;
       case 12: src = c->G > 1 ? c->cnt_all.p : c->cnt.p; n = b * 4; break;
       case 13: src = c->live.p; n = (1 + hp) * 4; break;
       default: throw Error(kValueError, "unknown stage");
@@ -1586,9 +1620,14 @@ int slide_write(slide_ctx* c, int64_t what, const void* src, int64_t bytes) {
     SLIDE_CHECK(bytes == n, kValueError, "size mismatch for stage write");
     if (n) SLIDE_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, c->s));
     // replayed errors in the W2 Adam's row-grouped order
-    if (what == 6)
-      launch_scatter_sorted(c->offs.as<int32_t>() + c->last_b, c->last_Pmax, c->grow.inv.as<int32_t>(),
-                            c->delta.as<float>(), c->dsort.as<float>(), c->s);
+    if (what == 6) {
+      if (c->rows_mode)
+        launch_rows_pairs(c->last_b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->grow.view(),
+                          c->delta.as<float>(), c->dsort.as<float>(), false, c->s);
+      else
+        launch_scatter_sorted(c->offs.as<int32_t>() + c->last_b, c->last_Pmax, c->grow.inv.as<int32_t>(),
+                              c->delta.as<float>(), c->dsort.as<float>(), c->s);
+    }
     // a replayed h has its own live units
     if (what == 0)
       launch_live_cols_from_h(c->hp, c->last_b, c->h.as<float>(), c->hmask.as<uint32_t>(), c->live.as<int32_t>(), c->s);

@@ -498,8 +498,11 @@ void GroupBy::run(const int32_t* keys, const int32_t* slots, const int32_t* n_de
   if (dense) {
     const TileCtl t{status.as<unsigned long long>(), ctrs.as<int32_t>()};
     const int grid_place = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_max, 256 * kPPT), kSms * 8));
-    gd_mask_kernel<<<grid_of(n_max), 256, 0, s>>>(keys, slots, n_dev, n_host, wpk, mask.as<uint32_t>(), t, tiles_bits);
-    SLIDE_LAUNCH_CHECK();
+    if (!premarked) {
+      gd_mask_kernel<<<grid_of(n_max), 256, 0, s>>>(keys, slots, n_dev, n_host, wpk, mask.as<uint32_t>(), t,
+                                                    tiles_bits);
+      SLIDE_LAUNCH_CHECK();
+    }
 #define SLIDE_GDS(W)                                                                                   \
   gd_scan_kernel<W><<<(int)tiles_bits, kGT, 0, s>>>(K, wpk, mask.as<uint32_t>(), uniq.as<int32_t>(),           \
                                                     key_rank.as<int32_t>(), seg_off.as<int32_t>(),             \
@@ -511,10 +514,12 @@ void GroupBy::run(const int32_t* keys, const int32_t* slots, const int32_t* n_de
     else SLIDE_GDS(0);
 #undef SLIDE_GDS
     SLIDE_LAUNCH_CHECK();
-    gd_place_kernel<<<grid_place, 256, 0, s>>>(keys, slots, n_dev, n_host, key_rank.as<int32_t>(), wpk,
-                                                   mask.as<uint32_t>(), seg_off.as<int32_t>(), order.as<int32_t>(),
-                                                   want_inv ? inv.as<int32_t>() : nullptr, sslot.as<int32_t>());
-    SLIDE_LAUNCH_CHECK();
+    if (place) {
+      gd_place_kernel<<<grid_place, 256, 0, s>>>(keys, slots, n_dev, n_host, key_rank.as<int32_t>(), wpk,
+                                                     mask.as<uint32_t>(), seg_off.as<int32_t>(), order.as<int32_t>(),
+                                                     want_inv ? inv.as<int32_t>() : nullptr, sslot.as<int32_t>());
+      SLIDE_LAUNCH_CHECK();
+    }
     return;
   }
   uint32_t* b = bits.as<uint32_t>();

@@ -62,8 +62,12 @@ void launch_explicit_active(int b, int64_t n, const int32_t* fptr, const int32_t
                             const int32_t* y_idx, int64_t cap_max, int32_t* act, int32_t* cnt, int32_t* empty,
                             cudaStream_t s);
 // pair lists from the per-slot active sets; also writes offs (B + 1) from cnt
+// mark (optional, unsharded dense row grouping): the pairs' bits in the row
+// slot masks and the scan tiles reset -- the grouping's first pass fused in
 void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* cnt, int32_t* offs, int shard_count,
-                  int32_t* prow, int32_t* pslot, uint8_t* plab, cudaStream_t s);
+                  int32_t* prow, int32_t* pslot, uint8_t* plab, cudaStream_t s, uint32_t* mark_mask = nullptr,
+                  int mark_wpk = 0, unsigned long long* mark_status = nullptr, int32_t* mark_ctr = nullptr,
+                  int64_t mark_tiles = 0);
 void launch_counts_to_f64(int b, const int32_t* cnt, double* out, cudaStream_t s);
 void launch_own_filter(int b, int32_t* act, int64_t cap_max, int g, int G, int32_t* cnt, int32_t* cnt_all,
                        cudaStream_t s);
@@ -82,9 +86,27 @@ struct GroupView {
   int wpk;
   int64_t u_max;
   int mask_by_key;
-  const int32_t* sslot;  // slot of each sorted position (want_inv groupings), else null
+  const int32_t* sslot;  // slot of each sorted position (placed groupings), else null
+  // dense groupings: key_rank[key] = the key's first sorted position, so an
+  // item's position follows from its key's mask (place-free consumers)
+  const int32_t* key_rank;
   __device__ __forceinline__ const uint32_t* mask_of(int64_t u) const {
     return mask + (mask_by_key ? (int64_t)uniq[u] : u) * wpk;
+  }
+  // sorted position of item (key, slot), dense mode
+  __device__ __forceinline__ int pos_of(int key, int slot) const {
+    const uint32_t* mk = mask + (int64_t)key * wpk;
+    const int w = slot >> 5;
+    const uint32_t lo = (1u << (slot & 31)) - 1u;
+    const int base = __ldg(key_rank + key);
+    if (wpk == 4) {  // B <= 128: the key's whole mask in one 16-byte load
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(mk));
+      return base + (w > 0 ? __popc(v.x) : __popc(v.x & lo)) + (w > 1 ? __popc(v.y) : w == 1 ? __popc(v.y & lo) : 0) +
+             (w > 2 ? __popc(v.z) : w == 2 ? __popc(v.z & lo) : 0) + (w == 3 ? __popc(v.w & lo) : 0);
+    }
+    int r = __popc(__ldg(mk + w) & lo);
+    for (int q = 0; q < w; ++q) r += __popc(__ldg(mk + q));
+    return base + r;
   }
 };
 
@@ -102,6 +124,10 @@ struct GroupBy {
   DBuf long_list, n_long;
   // want_inv: also inv[q] = sorted position of item q and sslot[pos] = its slot
   bool want_inv = false;
+  // dense mode only: premarked -- the caller filled the masks and reset the
+  // scan tiles (mark_args()); place = false -- no placement pass, the
+  // consumers derive positions from the masks (GroupView::pos_of)
+  bool premarked = false, place = true;
   DBuf inv, sslot;
   int64_t K = 0, nwords = 0, u_max = 0, bits_words = 0, mask_words = 0, tiles_bits = 0, tiles_seg = 0;
   int wpk = 1;
@@ -114,8 +140,20 @@ struct GroupBy {
   void release();
   GroupView view() {
     return GroupView{n_uniq.as<int32_t>(), uniq.as<int32_t>(), seg_off.as<int32_t>(), seg_cnt.as<int32_t>(),
-                     order.as<int32_t>(), mask.as<uint32_t>(), wpk, u_max, dense ? 1 : 0,
-                     want_inv ? sslot.as<int32_t>() : nullptr};
+                     place ? order.as<int32_t>() : nullptr, mask.as<uint32_t>(), wpk, u_max, dense ? 1 : 0,
+                     want_inv && place ? sslot.as<int32_t>() : nullptr, key_rank.as<int32_t>()};
+  }
+  // what a fused marking pass needs (dense mode): masks, words per key, the
+  // scan's tile status / counter to reset and their number
+  struct MarkArgs {
+    uint32_t* mask;
+    int wpk;
+    unsigned long long* status;
+    int32_t* ctr;
+    int64_t n_tiles;
+  };
+  MarkArgs mark_args() {
+    return MarkArgs{mask.as<uint32_t>(), wpk, status.as<unsigned long long>(), ctrs.as<int32_t>(), tiles_bits};
   }
 };
 
@@ -150,8 +188,16 @@ void launch_live_cols_from_h(int hp, int b, const float* h, uint32_t* hmask, int
 void launch_logits_rows(int hp, int b, const GroupView& g, const int32_t* pslot, const float* w2, const float* b2,
                         const float* h, const int32_t* live, float* z, cudaStream_t s, cudaStream_t s_rows);
 
+// rows != null: z is in the row grouping's order (place-free dense
+// grouping); each pair's position comes from its row's slot mask, and the
+// kernel also writes sslot[pos] = slot for the W2 Adam
 void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
-                    float* prob, float* delta, double* loss, const int32_t* inv, float* dsort, cudaStream_t s);
+                    float* prob, float* delta, double* loss, const int32_t* inv, float* dsort, cudaStream_t s,
+                    const int32_t* prow = nullptr, const GroupView* rows = nullptr, int32_t* sslot = nullptr);
+// place-free row grouping: out[pair] = rows_src[pos(pair)] (to_pairs) or
+// rows_dst[pos(pair)] = src[pair] (to_rows), pairs in sample-major order
+void launch_rows_pairs(int b, const int32_t* offs, const int32_t* prow, const GroupView& g, const float* src,
+                       float* dst, bool to_pairs, cudaStream_t s);
 // dst[inv[q]] = src[q] for q < *n_dev
 void launch_scatter_sorted(const int32_t* n_dev, int64_t n_max, const int32_t* inv, const float* src, float* dst,
                            cudaStream_t s);

@@ -273,6 +273,35 @@ __device__ __forceinline__ float reduce4(float v0, float v1, float v2, float v3,
   return k;  // the sum for pair ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1)
 }
 
+// position of the r-th (0-based) set bit of w
+__device__ __forceinline__ int select_bit(uint32_t w, int r) {
+  int pos = 0;
+#pragma unroll
+  for (int sh = 16; sh > 0; sh >>= 1) {
+    const int c = __popc(w & ((1u << sh) - 1u));
+    if (c <= r) {
+      r -= c;
+      pos += sh;
+      w >>= sh;
+    }
+  }
+  return pos;
+}
+
+// slot of the t-th item of a key's mask (lane-held words wd, their
+// inclusive popcount prefix incl; wpk <= 32 words)
+__device__ __forceinline__ int mask_select(uint32_t wd, int incl, int wpk, int t) {
+  int lo = 0, hi = wpk - 1;  // first word whose inclusive count exceeds t
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__shfl_sync(0xffffffffu, incl, mid) > t) hi = mid;
+    else lo = mid + 1;
+  }
+  const uint32_t w = __shfl_sync(0xffffffffu, wd, lo);
+  const int before = __shfl_sync(0xffffffffu, incl, lo) - __popc(w);
+  return 32 * lo + select_bit(w, t - before);
+}
+
 template <int NV>
 __device__ __forceinline__ void logits_row_warp(int hp, int64_t u, const GroupView& g, const int32_t* __restrict__ pslot,
                                                 const float* __restrict__ w2, const float* __restrict__ b2,
@@ -287,9 +316,38 @@ __device__ __forceinline__ void logits_row_warp(int hp, int64_t u, const GroupVi
   float w[G];
 #pragma unroll
   for (int q = 0; q < G; ++q) w[q] = q < ng ? __ldg(w2 + (int64_t)r * hp + col[q]) : 0.f;
+  // place-free grouping: slots from the row's mask, logits in row order
+  const bool rows_mode = g.order == nullptr;
+  uint32_t wd = 0;
+  int incl = 0;
+  if (rows_mode) {
+    wd = lane < g.wpk ? __ldg(g.mask_of(u) + lane) : 0u;
+    incl = __popc(wd);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+  }
   for (int j0 = 0; j0 < len; j0 += 32) {
-    const int pl = j0 + lane < len ? g.order[s0 + j0 + lane] : 0;
-    const int sl = j0 + lane < len ? pslot[pl] : 0;
+    int pl, sl;
+    if (rows_mode) {
+      const int t = min(j0 + lane, len - 1);
+      if (g.wpk == 4) {  // the row's four words are in every lane (wd / incl of lanes 0..3)
+        const int c0 = __shfl_sync(0xffffffffu, incl, 0), c1 = __shfl_sync(0xffffffffu, incl, 1),
+                  c2 = __shfl_sync(0xffffffffu, incl, 2);
+        const int w = (t >= c0) + (t >= c1) + (t >= c2);
+        const uint32_t wv = __shfl_sync(0xffffffffu, wd, w);
+        const int before = w == 0 ? 0 : w == 1 ? c0 : w == 2 ? c1 : c2;
+        sl = 32 * w + select_bit(wv, t - before);
+      } else {
+        sl = mask_select(wd, incl, g.wpk, t);
+      }
+      pl = s0 + j0 + lane;
+    } else {
+      pl = j0 + lane < len ? g.order[s0 + j0 + lane] : 0;
+      sl = j0 + lane < len ? pslot[pl] : 0;
+    }
     const int nc = min(32, len - j0);
     for (int q2 = 0; q2 < nc; q2 += 4) {
       float v[4];
@@ -450,6 +508,18 @@ __global__ void __launch_bounds__(256, 3) logits_tiles_kernel(int hp, int b, Gro
         const int row = warp + 8 * r;
         if (row >= nrow) break;
         const int lo = __shfl_sync(0xffffffffu, lo_l, r), n = __shfl_sync(0xffffffffu, n_l, r);
+        if (g.order == nullptr) {
+          // place-free grouping: the block's 64 slots are mask words s0/32
+          // and s0/32 + 1; lane l takes slots s0 + l and s0 + 32 + l, the
+          // logits go to their row-order positions
+          const uint32_t* mk = g.mask_of(u0 + row);
+          const int wa = s0 >> 5;
+          const uint32_t m0 = wa < g.wpk ? __ldg(mk + wa) : 0u, m1 = wa + 1 < g.wpk ? __ldg(mk + wa + 1) : 0u;
+          const uint32_t lt = (1u << lane) - 1u;
+          if ((m0 >> lane) & 1u) z[lo + __popc(m0 & lt)] = zt[row * kZLd + lane] + bias_s[row];
+          if ((m1 >> lane) & 1u) z[lo + __popc(m0) + __popc(m1 & lt)] = zt[row * kZLd + 32 + lane] + bias_s[row];
+          continue;
+        }
         for (int j = lane; j < n; j += 32) {
           const int pos = lo + j;
           const int sl = g.sslot[pos] - s0;
@@ -504,12 +574,17 @@ void launch_logits_rows(int hp, int b, const GroupView& g, const int32_t* pslot,
 // p = softmax over the active set (max-shifted, network.py:282-285);
 // delta = p - [label]/|Y| (network.py:308-309); loss = mean over labels of
 // -log(max(p_y, 1e-300)) (network.py:154-158), taken as a log-softmax.
+// ROWS: z is in the place-free row grouping's order; a pair's position is
+// read off its row's slot mask (g.pos_of), its error and slot go to dsort /
+// sslot at that position
+template <bool ROWS>
 __global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict__ offs,
                                                       const uint8_t* __restrict__ plab,
                                                       const int32_t* __restrict__ y_ptr, const float* __restrict__ z,
                                                       float* __restrict__ prob, float* __restrict__ delta,
                                                       double* __restrict__ loss, const int32_t* __restrict__ inv,
-                                                      float* __restrict__ dsort) {
+                                                      float* __restrict__ dsort, const int32_t* __restrict__ prow,
+                                                      GroupView g, int32_t* __restrict__ sslot) {
   using RF = cub::BlockReduce<float, 1024>;
   using RD = cub::BlockReduce<double, 1024>;
   __shared__ union {
@@ -524,14 +599,17 @@ __global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict
   // exponentials) across the three passes; a longer set re-reads the rest
   constexpr int kSmC = 8;
   float zr[kSmC], er[kSmC];
+  int pr[kSmC];  // ROWS: the pair's row-order position
+  auto pos_of = [&](int k) { return ROWS ? g.pos_of(prow[o + k], i) : o + k; };
   float mx = -INFINITY;
 #pragma unroll
   for (int j = 0; j < kSmC; ++j) {
     const int k = tid + j * 1024;
-    zr[j] = k < n ? z[o + k] : -INFINITY;
+    pr[j] = k < n ? pos_of(k) : 0;
+    zr[j] = k < n ? z[pr[j]] : -INFINITY;
     mx = fmaxf(mx, zr[j]);
   }
-  for (int k = tid + kSmC * 1024; k < n; k += 1024) mx = fmaxf(mx, z[o + k]);
+  for (int k = tid + kSmC * 1024; k < n; k += 1024) mx = fmaxf(mx, z[pos_of(k)]);
   mx = RF(tmp.f).Reduce(mx, cub::Max());
   if (tid == 0) s_max = n > 0 ? mx : 0.f;
   __syncthreads();
@@ -542,7 +620,7 @@ __global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict
     er[j] = tid + j * 1024 < n ? expf(zr[j] - mx) : 0.f;
     se += er[j];
   }
-  for (int k = tid + kSmC * 1024; k < n; k += 1024) se += expf(z[o + k] - mx);
+  for (int k = tid + kSmC * 1024; k < n; k += 1024) se += expf(z[pos_of(k)] - mx);
   se = RF(tmp.f).Sum(se);
   if (tid == 0) s_sum = se;
   __syncthreads();
@@ -560,20 +638,31 @@ __global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict
     prob[o + k] = p;
     const float dl = lab ? p - inv_ny : p;
     delta[o + k] = dl;
-    if (inv) dsort[inv[o + k]] = dl;
+    if (ROWS) {
+      dsort[pr[j]] = dl;
+      sslot[pr[j]] = i;
+    } else if (inv) {
+      dsort[inv[o + k]] = dl;
+    }
     if (lab) {
       double nl = -((double)zz - (double)lse);
       lsum += (nl < 690.7755278982137 || nl != nl) ? nl : 690.7755278982137;  // NaN propagates (np.maximum)
     }
   }
   for (int k = tid + kSmC * 1024; k < n; k += 1024) {
-    const float zz = z[o + k] - mx;
+    const int pk = pos_of(k);
+    const float zz = z[pk] - mx;
     const float p = expf(zz) / se;
     const int lab = plab[o + k];
     prob[o + k] = p;
     const float dl = lab ? p - inv_ny : p;
     delta[o + k] = dl;
-    if (inv) dsort[inv[o + k]] = dl;  // the W2 Adam reads the errors in row-grouped order
+    if (ROWS) {  // the W2 Adam reads the errors and slots in row-grouped order
+      dsort[pk] = dl;
+      sslot[pk] = i;
+    } else if (inv) {
+      dsort[inv[o + k]] = dl;
+    }
     if (lab) {
       double nl = -((double)zz - (double)lse);
       lsum += (nl < 690.7755278982137 || nl != nl) ? nl : 690.7755278982137;  // NaN propagates (np.maximum)
@@ -598,9 +687,33 @@ void launch_scatter_sorted(const int32_t* n_dev, int64_t n_max, const int32_t* i
 }
 
 void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
-                    float* prob, float* delta, double* loss, const int32_t* inv, float* dsort, cudaStream_t s) {
+                    float* prob, float* delta, double* loss, const int32_t* inv, float* dsort, cudaStream_t s,
+                    const int32_t* prow, const GroupView* rows, int32_t* sslot) {
   if (b <= 0) return;
-  softmax_kernel<<<b, 1024, 0, s>>>(offs, plab, y_ptr, z, prob, delta, loss, inv, dsort);
+  if (rows)
+    softmax_kernel<true><<<b, 1024, 0, s>>>(offs, plab, y_ptr, z, prob, delta, loss, nullptr, dsort, prow, *rows,
+                                            sslot);
+  else
+    softmax_kernel<false><<<b, 1024, 0, s>>>(offs, plab, y_ptr, z, prob, delta, loss, inv, dsort, nullptr,
+                                             GroupView{}, nullptr);
+  SLIDE_LAUNCH_CHECK();
+}
+
+__global__ void rows_pairs_kernel(const int32_t* __restrict__ offs, const int32_t* __restrict__ prow, GroupView g,
+                                  const float* __restrict__ src, float* __restrict__ dst, int to_pairs) {
+  const int i = blockIdx.x;
+  const int o = offs[i], n = offs[i + 1] - o;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const int pos = g.pos_of(prow[o + k], i);
+    if (to_pairs) dst[o + k] = src[pos];
+    else dst[pos] = src[o + k];
+  }
+}
+
+void launch_rows_pairs(int b, const int32_t* offs, const int32_t* prow, const GroupView& g, const float* src,
+                       float* dst, bool to_pairs, cudaStream_t s) {
+  if (b <= 0) return;
+  rows_pairs_kernel<<<b, 256, 0, s>>>(offs, prow, g, src, dst, to_pairs ? 1 : 0);
   SLIDE_LAUNCH_CHECK();
 }
 

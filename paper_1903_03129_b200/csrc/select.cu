@@ -497,7 +497,15 @@ void launch_explicit_active(int b, int64_t n, const int32_t* fptr, const int32_t
 __global__ void __launch_bounds__(1024) pairs_kernel(int b, const int32_t* __restrict__ act, int64_t cap_max,
                                                      const int32_t* __restrict__ cnt, int shard_count,
                                                      int32_t* __restrict__ offs, int32_t* __restrict__ prow,
-                                                     int32_t* __restrict__ pslot, uint8_t* __restrict__ plab) {
+                                                     int32_t* __restrict__ pslot, uint8_t* __restrict__ plab,
+                                                     uint32_t* __restrict__ mask, int wpk,
+                                                     unsigned long long* __restrict__ status, int32_t* ctr,
+                                                     int64_t n_tiles) {
+  if (mask) {  // the row grouping's scan tiles, reset for its scan kernel
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_tiles; q += (int64_t)gridDim.x * blockDim.x)
+      status[q] = 0ull;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ctr = 0;
+  }
   using Red = cub::BlockReduce<int, 1024>;
   using Scan = cub::BlockScan<int, 1024>;
   __shared__ union {
@@ -525,16 +533,20 @@ __global__ void __launch_bounds__(1024) pairs_kernel(int b, const int32_t* __res
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     uint32_t v = (uint32_t)src[k];
     const uint32_t id = v & 0x7fffffffu;
-    prow[o + k] = (int32_t)(shard_count == 1 ? id : id / (uint32_t)shard_count);
+    const uint32_t row = shard_count == 1 ? id : id / (uint32_t)shard_count;
+    prow[o + k] = (int32_t)row;
     pslot[o + k] = i;
     plab[o + k] = (uint8_t)(v >> 31);
+    if (mask) atomicOr(&mask[(int64_t)row * wpk + (i >> 5)], 1u << (i & 31));  // the row's slot mask
   }
 }
 
 void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* cnt, int32_t* offs, int shard_count,
-                  int32_t* prow, int32_t* pslot, uint8_t* plab, cudaStream_t s) {
+                  int32_t* prow, int32_t* pslot, uint8_t* plab, cudaStream_t s, uint32_t* mark_mask, int mark_wpk,
+                  unsigned long long* mark_status, int32_t* mark_ctr, int64_t mark_tiles) {
   SLIDE_CHECK(b <= 1024, kNotSupported, "batch size above 1024 not supported on the device path");
-  pairs_kernel<<<b, 1024, 0, s>>>(b, act, cap_max, cnt, shard_count, offs, prow, pslot, plab);
+  pairs_kernel<<<b, 1024, 0, s>>>(b, act, cap_max, cnt, shard_count, offs, prow, pslot, plab, mark_mask, mark_wpk,
+                                  mark_status, mark_ctr, mark_tiles);
   SLIDE_LAUNCH_CHECK();
 }
 
