@@ -79,7 +79,7 @@ struct slide_ctx {
   DBuf h, qkeys, order, states, act, cnt, empty, offs, prow, pslot, plab, z, prob, delta, loss, dh, dsort;
   // live hidden units of the last forward (see launch_hidden_forward)
   DBuf hmask, live, live_ticket;
-  DBuf fb_ids, fb_scratch, fb_bitmap;
+  DBuf fb_ids, fb_scratch, fb_bitmap, fb_rng;
   // backward workspace
   GroupBy grow, gfeat;
   bool grow_pending = false;  // grow holds a forward's grouping not yet cleared
@@ -292,6 +292,7 @@ int slide_create(const slide_net_desc* desc, void* stream, slide_ctx** out) {
     }
     const int64_t G = d.shard_count < 1 ? 1 : d.shard_count;
     SLIDE_CHECK(d.shard_rank >= 0 && d.shard_rank < G, kValueError, "shard_rank must lie in [0, shard_count)");
+    pcg_jump_table();  // the RNG jump table, allocated outside any graph capture
     slide_ctx* c = new slide_ctx();
     c->d = d;
     c->s = (cudaStream_t)stream;
@@ -339,7 +340,7 @@ int slide_destroy(slide_ctx* c) {
     for (DBuf* b : {&c->sh_packed, &c->sh_packed_t, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->dsort, &c->hmask, &c->live, &c->live_ticket, &c->qkeys, &c->order,
                     &c->states, &c->act, &c->cnt, &c->empty, &c->offs, &c->prow, &c->pslot, &c->plab, &c->z,
                     &c->prob, &c->delta, &c->loss, &c->dh, &c->fb_ids, &c->fb_scratch, &c->fb_bitmap, &c->xslot,
-                    &c->tc, &c->bc, &c->counters, &c->partial, &c->long_list, &c->n_long, &c->work, &c->topk_out, &c->topk_cnt, &c->tc_scratch, &c->bias_table, &c->cnt_all, &c->prob_tmp, &c->shard_pack})
+                    &c->tc, &c->bc, &c->counters, &c->partial, &c->long_list, &c->n_long, &c->work, &c->topk_out, &c->topk_cnt, &c->tc_scratch, &c->bias_table, &c->cnt_all, &c->prob_tmp, &c->shard_pack, &c->fb_rng})
       b->release();
     c->grow.release();
     c->gfeat.release();
@@ -776,6 +777,11 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     f.cap_max = cap_max;
     f.act = act;
     f.cnt = cnt;
+    // the choice's draws come from a run of its stream's outputs made in
+    // parallel: ~want 64-bit outputs (two 32-bit draws per id, Floyd + shuffle)
+    f.rng_n = (int)std::min<int64_t>(kPcgJump, want + 64);
+    f.rng_buf = f.rng_n > kFbSmemOutputs ? c->fb_rng.ensure<uint64_t>((size_t)b * f.rng_n) : nullptr;
+    f.jump = pcg_jump_table();
     launch_fallback(f, b, s);
     if (bt->rng_states)
       SLIDE_CUDA(cudaMemcpyAsync(bt->rng_states, states, (size_t)b * 48, cudaMemcpyDeviceToDevice, s));

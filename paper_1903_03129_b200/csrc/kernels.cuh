@@ -1,6 +1,7 @@
 // Kernel argument blocks and launchers of the training step.
 #pragma once
 #include "internal.cuh"
+#include "rng.cuh"
 
 namespace slide {
 
@@ -47,7 +48,13 @@ struct FallbackArgs {
   int64_t cap_max;
   int32_t* act;
   int32_t* cnt;
+  // the slot stream's outputs made in parallel (rng.cuh PcgBuf): rng_n per
+  // slot; in shared memory when rng_n <= kFbSmemOutputs, else rng_buf + i * rng_n
+  uint64_t* rng_buf;
+  int rng_n;
+  const u128* jump;  // pcg_jump_table()
 };
+constexpr int kFbSmemOutputs = 1024;
 
 void launch_slot_rng(int b, uint64_t seed, int64_t it, const int64_t* it_dev, int64_t off, int l, int vanilla,
                      const uint64_t* ext, uint64_t* states, uint8_t* order, cudaStream_t s);

@@ -127,55 +127,14 @@ struct Pcg64 {
     u32 = (uint32_t)(n >> 32);
     return (uint32_t)n;
   }
-  // random_interval(max): masked rejection (used by Generator.shuffle)
-  SL_HD uint64_t interval(uint64_t mx) {
-    if (mx == 0) return 0;
-    uint64_t mask = mx;
-    mask |= mask >> 1;
-    mask |= mask >> 2;
-    mask |= mask >> 4;
-    mask |= mask >> 8;
-    mask |= mask >> 16;
-    mask |= mask >> 32;
-    uint64_t v;
-    if (mx <= 0xffffffffull) {
-      while ((v = (next32() & mask)) > mx) {
-      }
-    } else {
-      while ((v = (next64() & mask)) > mx) {
-      }
-    }
-    return v;
-  }
-  // random_bounded_uint64(off=0, rng, use_masked=false): Lemire
-  SL_HD uint64_t bounded(uint64_t rng) {
-    if (rng == 0) return 0;
-    if (rng <= 0xffffffffull) {
-      if (rng == 0xffffffffull) return next32();
-      uint32_t rx = (uint32_t)rng + 1u;
-      uint64_t m = (uint64_t)next32() * rx;
-      uint32_t left = (uint32_t)m;
-      if (left < rx) {
-        uint32_t th = (uint32_t)((0xffffffffu - (uint32_t)rng) % rx);
-        while (left < th) {
-          m = (uint64_t)next32() * rx;
-          left = (uint32_t)m;
-        }
-      }
-      return m >> 32;
-    }
-    if (rng == 0xffffffffffffffffull) return next64();
-    uint64_t rx = rng + 1;
-    u128 m = (u128)next64() * rx;
-    uint64_t left = (uint64_t)m;
-    if (left < rx) {
-      uint64_t th = (0xffffffffffffffffull - rng) % rx;
-      while (left < th) {
-        m = (u128)next64() * rx;
-        left = (uint64_t)m;
-      }
-    }
-    return (uint64_t)(m >> 64);
+  // random_interval(max) / random_bounded_uint64: rng_interval / rng_bounded below
+  SL_HD uint64_t interval(uint64_t mx);
+  SL_HD uint64_t bounded(uint64_t rng);
+  SL_HD static uint64_t xsl_rr(u128 st) {
+    uint64_t hi = (uint64_t)(st >> 64), lo = (uint64_t)st;
+    unsigned rot = (unsigned)(st >> 122);
+    uint64_t x = hi ^ lo;
+    return (x >> rot) | (x << ((64u - rot) & 63u));
   }
 
   // serialised as 6 uint64: state hi/lo, inc hi/lo, has_uint32, uinteger
@@ -195,12 +154,141 @@ struct Pcg64 {
   }
 };
 
+// random_interval(max): masked rejection (used by Generator.shuffle); G is
+// any source with next32 / next64 (Pcg64, PcgBuf)
+template <class G>
+SL_HD uint64_t rng_interval(G& g, uint64_t mx) {
+  if (mx == 0) return 0;
+  uint64_t mask = mx;
+  mask |= mask >> 1;
+  mask |= mask >> 2;
+  mask |= mask >> 4;
+  mask |= mask >> 8;
+  mask |= mask >> 16;
+  mask |= mask >> 32;
+  uint64_t v;
+  if (mx <= 0xffffffffull) {
+    while ((v = (g.next32() & mask)) > mx) {
+    }
+  } else {
+    while ((v = (g.next64() & mask)) > mx) {
+    }
+  }
+  return v;
+}
+
+// random_bounded_uint64(off=0, rng, use_masked=false): Lemire
+template <class G>
+SL_HD uint64_t rng_bounded(G& g, uint64_t rng) {
+  if (rng == 0) return 0;
+  if (rng <= 0xffffffffull) {
+    if (rng == 0xffffffffull) return g.next32();
+    uint32_t rx = (uint32_t)rng + 1u;
+    uint64_t m = (uint64_t)g.next32() * rx;
+    uint32_t left = (uint32_t)m;
+    if (left < rx) {
+      uint32_t th = (uint32_t)((0xffffffffu - (uint32_t)rng) % rx);
+      while (left < th) {
+        m = (uint64_t)g.next32() * rx;
+        left = (uint32_t)m;
+      }
+    }
+    return m >> 32;
+  }
+  if (rng == 0xffffffffffffffffull) return g.next64();
+  uint64_t rx = rng + 1;
+  u128 m = (u128)g.next64() * rx;
+  uint64_t left = (uint64_t)m;
+  if (left < rx) {
+    uint64_t th = (0xffffffffffffffffull - rng) % rx;
+    while (left < th) {
+      m = (u128)g.next64() * rx;
+      left = (uint64_t)m;
+    }
+  }
+  return (uint64_t)(m >> 64);
+}
+
+SL_HD uint64_t Pcg64::interval(uint64_t mx) { return rng_interval(*this, mx); }
+SL_HD uint64_t Pcg64::bounded(uint64_t rng) { return rng_bounded(*this, rng); }
+
+// Jump-ahead: after k steps the state is A_k s + S_k inc (A_k = a^k, S_k =
+// 1 + a + ... + a^(k-1) mod 2^128), so k outputs of one stream can be made
+// in parallel and the state after any prefix of them restored exactly.
+constexpr int kPcgJump = 65536;
+SL_HD void pcg_jump_coeffs(int k, u128& A, u128& S) {
+  A = 1;
+  S = 0;
+  for (int i = 0; i < k; ++i) {
+    S = S * Pcg64::mult() + 1;
+    A = A * Pcg64::mult();
+  }
+}
+
+#ifdef __CUDACC__
+// the device jump table: jump[2k], jump[2k + 1] = (A_k, S_k), k = 0..kPcgJump
+// (built once on the host, select.cu)
+const u128* pcg_jump_table();
+
+// A stream consumer reading a precomputed run of outputs: buf[k] = output
+// k + 1 of the generator `base`; past the run it steps serially.  The
+// interval / bounded / has32 logic is the generator's own, so the values
+// and the final state equal Pcg64's.
+struct PcgBuf {
+  const uint64_t* buf;
+  int n, pos;
+  Pcg64 g;  // the base state; after the run, the serial continuation
+  uint32_t has32, u32;
+  const u128* jump;
+  __device__ PcgBuf(const Pcg64& base, const uint64_t* b, int nb, const u128* jt)
+      : buf(b), n(nb), pos(0), g(base), has32(base.has32), u32(base.u32), jump(jt) {}
+  __device__ uint64_t next64() {
+    if (pos < n) return buf[pos++];
+    if (pos == n) {  // leave the run: the state after n steps
+      const u128 A = jump[2 * n], S = jump[2 * n + 1];
+      g.state = A * g.state + S * g.inc;
+    }
+    ++pos;
+    g.step();
+    return Pcg64::xsl_rr(g.state);
+  }
+  __device__ uint32_t next32() {
+    if (has32) {
+      has32 = 0;
+      return u32;
+    }
+    uint64_t v = next64();
+    has32 = 1;
+    u32 = (uint32_t)(v >> 32);
+    return (uint32_t)v;
+  }
+  // the generator after everything consumed so far
+  __device__ void finish(Pcg64& out) {
+    out = g;
+    if (pos <= n) {
+      const u128 A = jump[2 * pos], S = jump[2 * pos + 1];
+      out.state = A * g.state + S * g.inc;
+    }
+    out.has32 = has32;
+    out.u32 = u32;
+  }
+};
+
+// the first n (<= kPcgJump) outputs of `g`, threads t of nt in parallel
+__device__ __forceinline__ void pcg_fill(const Pcg64& g, uint64_t* buf, int n, int t, int nt, const u128* jump) {
+  for (int k = t; k < n; k += nt) {
+    const u128 A = jump[2 * (k + 1)], S = jump[2 * (k + 1) + 1];
+    buf[k] = Pcg64::xsl_rr(A * g.state + S * g.inc);
+  }
+}
+#endif
+
 // Generator.permutation(n) on an int array (n small: L tables)
-template <typename T>
-SL_HD void pcg_permutation(Pcg64& g, T* a, int n) {
+template <typename T, class G>
+SL_HD void pcg_permutation(G& g, T* a, int n) {
   for (int i = 0; i < n; ++i) a[i] = (T)i;
   for (int i = n - 1; i >= 1; --i) {
-    int j = (int)g.interval((uint64_t)i);
+    int j = (int)rng_interval(g, (uint64_t)i);
     T t = a[i];
     a[i] = a[j];
     a[j] = t;
@@ -226,7 +314,11 @@ SL_HD int64_t choice_scratch_entries(int64_t pop, int64_t size) {
 
 // Generator.choice(pop, size, replace=False) -> out[size] (numpy order).
 // scratch: choice_scratch_entries(pop,size) int64 slots; any contents.
-SL_HD void pcg_choice(Pcg64& g, int64_t pop, int64_t size, int64_t* out, int64_t* scratch) {
+// keep_order = false: the final shuffle's draws are consumed (the generator
+// ends in numpy's state) but not applied -- for callers that only need the
+// set (the training fallback unions it with the labels and sorts).
+template <class G>
+SL_HD void pcg_choice(G& g, int64_t pop, int64_t size, int64_t* out, int64_t* scratch, bool keep_order = true) {
   if (size <= 0) return;
   if (choice_uses_tail(pop, size)) {
     // partial Fisher-Yates of arange(pop) over positions [first, pop);
@@ -245,7 +337,7 @@ SL_HD void pcg_choice(Pcg64& g, int64_t pop, int64_t size, int64_t* out, int64_t
     const int64_t lo = pop - size;
     const int64_t first = lo > 1 ? lo : 1;
     for (int64_t i = pop - 1; i >= first; --i) {
-      int64_t j = (int64_t)g.bounded((uint64_t)i);
+      int64_t j = (int64_t)rng_bounded(g, (uint64_t)i);
       uint64_t li = find(i);
       int64_t vi = keys[li] == i ? vals[li] : i;
       uint64_t lj = find(j);
@@ -267,7 +359,7 @@ SL_HD void pcg_choice(Pcg64& g, int64_t pop, int64_t size, int64_t* out, int64_t
   int64_t* hs = scratch;
   for (uint64_t q = 0; q <= mask; ++q) hs[q] = -1;
   for (int64_t j = pop - size; j < pop; ++j) {
-    int64_t val = (int64_t)g.bounded((uint64_t)j);
+    int64_t val = (int64_t)rng_bounded(g, (uint64_t)j);
     uint64_t loc = (uint64_t)val & mask;
     while (hs[loc] != -1 && hs[loc] != val) loc = (loc + 1) & mask;
     if (hs[loc] == -1) {
@@ -282,7 +374,8 @@ SL_HD void pcg_choice(Pcg64& g, int64_t pop, int64_t size, int64_t* out, int64_t
   }
   // shuffle=True: _shuffle_int(size, 1, out)
   for (int64_t i = size - 1; i >= 1; --i) {
-    int64_t j = (int64_t)g.bounded((uint64_t)i);
+    int64_t j = (int64_t)rng_bounded(g, (uint64_t)i);
+    if (!keep_order) continue;
     int64_t t = out[i];
     out[i] = out[j];
     out[j] = t;

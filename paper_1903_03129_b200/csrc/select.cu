@@ -12,16 +12,48 @@
 #include "internal.cuh"
 #include "kernels.cuh"
 #include <cub/cub.cuh>
+#include <climits>
+#include <vector>
 
 namespace slide {
 
 // ------------------------------------------------------------ per-slot rng
+// The jump table of rng.cuh (A_k, S_k for k = 0..kPcgJump), built once.
+const u128* pcg_jump_table() {
+  static const u128* table = [] {
+    std::vector<u128> h(2 * (size_t)(kPcgJump + 1));
+    u128 A = 1, S = 0;
+    for (int k = 0; k <= kPcgJump; ++k) {
+      h[2 * k] = A;
+      h[2 * k + 1] = S;
+      S = S * Pcg64::mult() + 1;
+      A = A * Pcg64::mult();
+    }
+    u128* d = nullptr;
+    SLIDE_CUDA(cudaMalloc(&d, h.size() * sizeof(u128)));
+    SLIDE_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(u128), cudaMemcpyHostToDevice));
+    return (const u128*)d;
+  }();
+  return table;
+}
+
 // default_rng((seed, iteration, slot)) (network.py:353) or an explicit
 // Generator state; vanilla draws permutation(L) first (samplers.py:69).
-__global__ void slot_rng_kernel(int b, uint64_t seed, int64_t iteration, const int64_t* iter_dev,
-                                int64_t slot_offset, int l, int vanilla, const uint64_t* __restrict__ ext,
-                                uint64_t* __restrict__ states, uint8_t* __restrict__ order) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+// One warp per slot: every lane seeds (the same arithmetic), the warp makes
+// the stream's first kSlotRngOut outputs in parallel (jump-ahead), lane 0
+// walks them through the permutation's rejection draws.
+constexpr int kSlotRngOut = 128;
+constexpr int kSlotRngWarps = 8;
+
+__global__ void __launch_bounds__(kSlotRngWarps * 32) slot_rng_kernel(int b, uint64_t seed, int64_t iteration,
+                                                                      const int64_t* iter_dev, int64_t slot_offset,
+                                                                      int l, int vanilla,
+                                                                      const uint64_t* __restrict__ ext,
+                                                                      uint64_t* __restrict__ states,
+                                                                      uint8_t* __restrict__ order, const u128* jump) {
+  __shared__ uint64_t buf[kSlotRngWarps][kSlotRngOut];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kSlotRngWarps + warp;
   if (i >= b) return;
   if (iter_dev) iteration = *iter_dev;  // graph replays read the step number from memory
   Pcg64 g;
@@ -32,16 +64,24 @@ __global__ void slot_rng_kernel(int b, uint64_t seed, int64_t iteration, const i
     g.seed_from(ent, 3);
   }
   if (vanilla) {
-    uint8_t a[64];
-    pcg_permutation(g, a, l);
-    for (int p = 0; p < l; ++p) order[(int64_t)i * l + p] = a[p];
+    pcg_fill(g, buf[warp], kSlotRngOut, lane, 32, jump);
+    __syncwarp();
+    if (lane == 0) {
+      PcgBuf pb(g, buf[warp], kSlotRngOut, jump);
+      uint8_t a[64];
+      pcg_permutation(pb, a, l);
+      pb.finish(g);
+      for (int p = 0; p < l; ++p) order[(int64_t)i * l + p] = a[p];
+    }
   }
-  g.store(states + 6 * i);
+  if (lane == 0) g.store(states + 6 * i);
 }
 
 void launch_slot_rng(int b, uint64_t seed, int64_t it, const int64_t* it_dev, int64_t off, int l, int vanilla,
                      const uint64_t* ext, uint64_t* states, uint8_t* order, cudaStream_t s) {
-  slot_rng_kernel<<<(int)ceil_div(b, 64), 64, 0, s>>>(b, seed, it, it_dev, off, l, vanilla, ext, states, order);
+  slot_rng_kernel<<<(int)ceil_div(b, kSlotRngWarps), kSlotRngWarps * 32, 0, s>>>(b, seed, it, it_dev, off, l,
+                                                                                 vanilla, ext, states, order,
+                                                                                 pcg_jump_table());
   SLIDE_LAUNCH_CHECK();
 }
 
@@ -378,6 +418,8 @@ bool launch_select_union(const SelectArgs& a, int64_t n_out, cudaStream_t s) {
 // generator (network.py:229-231), union labels, sorted (network.py:236-238).
 // Thread 0 replays numpy's choice() serially; the CTA then emits the id set
 // in ascending order from a per-slot bitmap.
+constexpr int kFbSortItems = 4;  // sets of <= 1024 ids (beta + labels) are sorted in the block
+
 __global__ void __launch_bounds__(256) fallback_kernel(FallbackArgs a) {
   using Scan = cub::BlockScan<int, 256>;
   __shared__ typename Scan::TempStorage scan_tmp;
@@ -385,30 +427,197 @@ __global__ void __launch_bounds__(256) fallback_kernel(FallbackArgs a) {
   const int i = blockIdx.x, tid = threadIdx.x;
   if (!a.empty[i]) return;
   int64_t* ids = a.fb_ids + (int64_t)i * a.want;
-  if (tid == 0) {
-    Pcg64 g;
-    if (a.states_ready) {
-      g.load(a.states + 6 * i);
-    } else {  // slot stream not drawn yet (full-union vanilla): seed + probe order first
-      const int64_t it = a.iter_dev ? *a.iter_dev : a.iteration;
-      uint64_t ent[3] = {a.seed, (uint64_t)it, (uint64_t)(a.slot_offset + i)};
-      g.seed_from(ent, 3);
-      if (a.vanilla) {
+  // the slot's stream: every thread derives the same base state; its
+  // outputs are made in parallel (jump-ahead) and thread 0 walks them
+  // through the draws (rng.cuh PcgBuf) -- the serial part is the hash-set /
+  // shuffle bookkeeping, not the 128-bit generator steps
+  __shared__ uint64_t rbuf_s[kFbSmemOutputs];
+  __shared__ uint64_t g_s[6];
+  Pcg64 g;
+  if (a.states_ready) {
+    g.load(a.states + 6 * i);
+  } else {  // slot stream not drawn yet (full-union vanilla): seed + probe order first
+    const int64_t it = a.iter_dev ? *a.iter_dev : a.iteration;
+    uint64_t ent[3] = {a.seed, (uint64_t)it, (uint64_t)(a.slot_offset + i)};
+    g.seed_from(ent, 3);
+    if (a.vanilla) {
+      pcg_fill(g, rbuf_s, 128, tid, 256, a.jump);
+      __syncthreads();
+      if (tid == 0) {
+        PcgBuf pb(g, rbuf_s, 128, a.jump);
         uint8_t perm[64];
-        pcg_permutation(g, perm, a.l);
+        pcg_permutation(pb, perm, a.l);
+        pb.finish(g);
+        g.store(g_s);
       }
+      __syncthreads();
+      g.load(g_s);
     }
+  }
+  uint64_t* rbuf = a.rng_n <= kFbSmemOutputs ? rbuf_s : a.rng_buf + (int64_t)i * a.rng_n;
+  pcg_fill(g, rbuf, a.rng_n, tid, 256, a.jump);
+  __syncthreads();
+  // Floyd's choice in parallel.  The draws (Floyd's `size`, then the
+  // final shuffle's size - 1) are Lemire bounded draws on the stream's
+  // 32-bit values; draw k takes value k + (values rejected before it).  All
+  // draws are evaluated at once; the first draw that lands in its rejection
+  // zone (p ~ range / 2^32) shifts every later draw by one value and the
+  // remainder is re-evaluated -- one extra round per rejection.  Floyd then
+  // keeps val_j unless an earlier id equals it (then j): collisions are
+  // resolved against the earlier values and verified against the earlier
+  // outputs; anything else (a substitution colliding again, too few buffered
+  // values) takes thread 0's serial replay below.
+  __shared__ int fl_bad, fl_first, fl_shift;
+  __shared__ uint32_t fl_val[256 * kFbSortItems];
+  const int64_t size = a.want, base = a.n - a.want;
+  const bool try_fast = !choice_uses_tail(a.n, size) && size <= 256 * kFbSortItems && a.n <= 0xffffffffll &&
+                        base >= 1;
+  if (try_fast) {
+    const uint32_t h0 = g.has32 ? 1u : 0u;
+    const int64_t avail = 2 * (int64_t)a.rng_n + h0;  // buffered 32-bit values
+    auto u32_at = [&](int64_t t) -> uint32_t {  // the stream's t-th 32-bit value (numpy's buffered halves)
+      if (h0) {
+        if (t == 0) return g.u32;
+        t -= 1;
+      }
+      const uint64_t v = rbuf[t >> 1];
+      return (t & 1) ? (uint32_t)(v >> 32) : (uint32_t)v;
+    };
+    const int D = (int)(2 * size - 1);
+    if (tid == 0) {
+      fl_bad = 0;
+      fl_shift = 0;
+    }
+    int start = 0;
+    while (true) {
+      if (tid == 0) fl_first = INT_MAX;
+      __syncthreads();
+      const int shift = fl_shift;
+      for (int k = start + tid; k < D; k += 256) {
+        const int64_t idx = k + shift;
+        if (idx >= avail) {
+          atomicOr(&fl_bad, 1);
+          continue;
+        }
+        const uint32_t rng = k < size ? (uint32_t)(base + k) : (uint32_t)(2 * size - 1 - k);
+        const uint32_t rx = rng + 1u;
+        const uint64_t m = (uint64_t)u32_at(idx) * rx;
+        const uint32_t left = (uint32_t)m;
+        if (left < rx && left < (0xffffffffu - rng) % rx) atomicMin(&fl_first, k);
+        if (k < size) fl_val[k] = (uint32_t)(m >> 32);
+      }
+      __syncthreads();
+      const int first = fl_first;
+      if (first == INT_MAX || fl_bad) break;
+      start = first;  // draw `first` retries on the next value; the rest move up by one
+      __syncthreads();
+      if (tid == 0) fl_shift = shift + 1;
+    }
+    __syncthreads();
+    // Floyd's set: val_j, or j when an earlier id equals val_j
+    if (!fl_bad) {
+      for (int j = tid; j < size; j += 256) {
+        const uint32_t v = fl_val[j];
+        bool coll = false;
+        for (int k = 0; k < j; ++k) coll |= fl_val[k] == v;
+        ids[j] = coll ? (int64_t)(base + j) : (int64_t)v;
+      }
+      __syncthreads();
+      for (int j = tid; j < size; j += 256) {  // verify against the outputs themselves
+        const uint32_t v = fl_val[j];
+        bool in = false, coll = false;
+        for (int k = 0; k < j; ++k) {
+          in |= (uint32_t)ids[k] == v;
+          coll |= fl_val[k] == v;
+        }
+        if (in != coll) atomicOr(&fl_bad, 2);
+      }
+      __syncthreads();
+    }
+    if (fl_bad == 0 && tid == 0) {  // the generator after the consumed values
+      const int64_t t = (int64_t)D + fl_shift - h0;
+      const int64_t n64 = (t + 1) >> 1;
+      Pcg64 e = g;
+      const u128 A = a.jump[2 * n64], S = a.jump[2 * n64 + 1];
+      e.state = A * g.state + S * g.inc;
+      e.has32 = (uint32_t)(t & 1);
+      // numpy keeps the last 64-bit value's high half as `uinteger` (stale once used)
+      e.u32 = n64 > 0 ? (uint32_t)(rbuf[n64 - 1] >> 32) : g.u32;
+      e.store(a.states + 6 * i);
+    }
+  }
+  if (!try_fast || fl_bad != 0) if (tid == 0) {
+    PcgBuf pb(g, rbuf, a.rng_n, a.jump);
     int64_t* scratch = a.smem_scratch ? fb_smem : a.scratch + (int64_t)i * a.scratch_per_slot;
-    pcg_choice(g, a.n, a.want, ids, scratch);
+    pcg_choice(pb, a.n, a.want, ids, scratch, /*keep_order=*/false);  // the ids go into a bitmap
+    pb.finish(g);
     g.store(a.states + 6 * i);
   }
   __syncthreads();
+  const int y0 = a.y_ptr[i], ny = a.y_ptr[i + 1] - y0;
+  const int n = (int)a.want + ny;
+  auto key_at = [&](int k) -> uint32_t {
+    return k < a.want ? (uint32_t)ids[k] << 1 : ((uint32_t)a.y_idx[y0 + k - a.want] << 1) | 1u;
+  };
+  int32_t* out = a.act + (int64_t)i * a.cap_max;
+  if (n <= 256) {
+    // the usual case (beta + labels <= 256): keys (id << 1 | label) are
+    // distinct, so each one's rank is the count of smaller keys; keep the
+    // last of each id's run (a label sorts after the same id drawn)
+    __shared__ uint32_t kin[256], ks[256];
+    if (tid < n) kin[tid] = key_at(tid);
+    __syncthreads();
+    if (tid < n) {
+      const uint32_t me = kin[tid];
+      int r = 0;
+      for (int q = 0; q < n; ++q) r += kin[q] < me;
+      ks[r] = me;
+    }
+    __syncthreads();
+    const bool keep = tid < n && (tid + 1 == n || (ks[tid + 1] >> 1) != (ks[tid] >> 1));
+    int ofs, total;
+    Scan(scan_tmp).ExclusiveSum(keep ? 1 : 0, ofs, total);
+    if (keep) out[ofs] = (int32_t)((ks[tid] >> 1) | ((ks[tid] & 1u) << 31));
+    if (tid == 0) a.cnt[i] = total;
+    return;
+  }
+  if (n <= 256 * kFbSortItems) {
+    using Sort = cub::BlockRadixSort<uint32_t, 256, kFbSortItems>;
+    __shared__ typename Sort::TempStorage sort_tmp;
+    int end_bit = 2;
+    while (((int64_t)1 << (end_bit - 1)) < a.n) ++end_bit;  // id bits + the label bit
+    uint32_t key[kFbSortItems];
+#pragma unroll
+    for (int q = 0; q < kFbSortItems; ++q) {
+      const int k = tid * kFbSortItems + q;
+      key[q] = k < n ? key_at(k) : 0xffffffffu;
+    }
+    Sort(sort_tmp).Sort(key, 0, end_bit);  // blocked: thread t holds sorted items [t * kFbSortItems, ...)
+    __shared__ uint32_t last_s[256];
+    last_s[tid] = key[0];
+    __syncthreads();
+    const uint32_t nxt0 = tid + 1 < 256 ? last_s[tid + 1] : 0xffffffffu;  // first item of the next thread
+    int keep[kFbSortItems], m = 0;
+#pragma unroll
+    for (int q = 0; q < kFbSortItems; ++q) {
+      const uint32_t nx = q + 1 < kFbSortItems ? key[q + 1] : nxt0;
+      keep[q] = key[q] != 0xffffffffu && (nx == 0xffffffffu || (nx >> 1) != (key[q] >> 1));
+      m += keep[q];
+    }
+    int ofs, total;
+    __syncthreads();  // last_s reads done before the scan storage is reused
+    Scan(scan_tmp).ExclusiveSum(m, ofs, total);
+#pragma unroll
+    for (int q = 0; q < kFbSortItems; ++q)
+      if (keep[q]) out[ofs++] = (int32_t)((key[q] >> 1) | ((key[q] & 1u) << 31));
+    if (tid == 0) a.cnt[i] = total;
+    return;
+  }
   uint32_t* bm = a.bitmap + (int64_t)i * a.words;
   for (int64_t k = tid; k < a.want; k += 256) {
     int64_t id = ids[k];
     atomicOr(&bm[id >> 5], 1u << (id & 31));
   }
-  const int y0 = a.y_ptr[i], ny = a.y_ptr[i + 1] - y0;
   for (int k = tid; k < ny; k += 256) {
     int id = a.y_idx[y0 + k];
     atomicOr(&bm[id >> 5], 1u << (id & 31));
@@ -421,7 +630,7 @@ __global__ void __launch_bounds__(256) fallback_kernel(FallbackArgs a) {
   for (int64_t w = w0; w < w1; ++w) cnt += __popc(bm[w]);
   int ofs, total;
   Scan(scan_tmp).ExclusiveSum(cnt, ofs, total);
-  int32_t* out = a.act + (int64_t)i * a.cap_max;
+  // (out: the slot's active list, above)
   const int32_t* lab = a.y_idx + y0;
   for (int64_t w = w0; w < w1; ++w) {
     uint32_t bits = bm[w];

@@ -318,11 +318,17 @@ def test_large_fallback_sets_match_numpy(beta):
     batch = [(SparseVector(np.array([i]), np.array([1.0]), 8), {i}) for i in range(4)]
     csr = csr_from_batch(batch, 8, n_out)
     got, keep = _stage_forward(net, csr, 3)
+    from paper_1903_03129_b200 import _lib
+
+    states = net._read(10, 4 * 6, np.uint64).reshape(4, 6)
     for i in range(4):
         r = np.random.default_rng((9, 3, i))
         r.permutation(3)
         want = np.union1d(r.choice(n_out, size=beta, replace=False), [i])
         np.testing.assert_array_equal(got["rows"][got["offs"][i]: got["offs"][i + 1]], want)
+        # the slot's generator ends where numpy's does (the parallel draws
+        # restore the state after exactly the values numpy consumed)
+        np.testing.assert_array_equal(states[i], _lib.pcg64_state_from_generator(r))
 
 
 def test_hand_computed_forward_and_views():
