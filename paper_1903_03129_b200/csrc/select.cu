@@ -64,14 +64,67 @@ __global__ void __launch_bounds__(kSlotRngWarps * 32) slot_rng_kernel(int b, uin
     g.seed_from(ent, 3);
   }
   if (vanilla) {
+    __shared__ uint8_t perm_s[kSlotRngWarps][64];
     pcg_fill(g, buf[warp], kSlotRngOut, lane, 32, jump);
+    for (int p = lane; p < l; p += 32) perm_s[warp][p] = (uint8_t)p;
     __syncwarp();
     if (lane == 0) {
-      PcgBuf pb(g, buf[warp], kSlotRngOut, jump);
-      uint8_t a[64];
-      pcg_permutation(pb, a, l);
-      pb.finish(g);
-      for (int p = 0; p < l; ++p) order[(int64_t)i * l + p] = a[p];
+      // permutation(L): Fisher-Yates with random_interval's masked
+      // rejection, walked directly over the buffered 32-bit values
+      const uint64_t* bw = buf[warp];
+      const uint32_t h0 = g.has32 ? 1u : 0u;
+      const int avail = 2 * kSlotRngOut + (int)h0;
+      int t = 0;
+      bool ok = true;
+      for (int p = l - 1; p >= 1 && ok; --p) {
+        uint32_t mask = (uint32_t)p;
+        mask |= mask >> 1;
+        mask |= mask >> 2;
+        mask |= mask >> 4;
+        mask |= mask >> 8;
+        mask |= mask >> 16;
+        uint32_t v;
+        do {
+          if (t >= avail) {
+            ok = false;
+            break;
+          }
+          int64_t q = t++;
+          uint32_t u;
+          if (h0 && q == 0) {
+            u = g.u32;
+          } else {
+            q -= h0;
+            u = (q & 1) ? (uint32_t)(bw[q >> 1] >> 32) : (uint32_t)bw[q >> 1];
+          }
+          v = u & mask;
+        } while (v > (uint32_t)p);
+        if (!ok) break;
+        const uint8_t x = perm_s[warp][p];
+        perm_s[warp][p] = perm_s[warp][v];
+        perm_s[warp][v] = x;
+      }
+      if (ok) {  // the generator after t values
+        const int64_t tt = t - (int64_t)h0;
+        const int64_t n64 = tt > 0 ? (tt + 1) >> 1 : 0;
+        Pcg64 e = g;
+        const u128 A = jump[2 * n64], S = jump[2 * n64 + 1];
+        e.state = A * g.state + S * g.inc;
+        if (tt > 0) {
+          e.has32 = (uint32_t)(tt & 1);
+          e.u32 = (uint32_t)(bw[n64 - 1] >> 32);
+        } else {
+          e.has32 = t == 0 ? g.has32 : 0u;  // only the buffered value (if any) was used
+        }
+        g = e;
+      } else {  // more rejections than buffered values: the serial walk
+        PcgBuf pb(g, bw, kSlotRngOut, jump);
+        uint8_t a[64];
+        pcg_permutation(pb, a, l);
+        pb.finish(g);
+        for (int p = 0; p < l; ++p) perm_s[warp][p] = a[p];
+      }
+      for (int p = 0; p < l; ++p) order[(int64_t)i * l + p] = perm_s[warp][p];
     }
   }
   if (lane == 0) g.store(states + 6 * i);
