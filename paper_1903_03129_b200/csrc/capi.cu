@@ -623,6 +623,22 @@ static int32_t* hg_tickets(slide_ctx* c, int b) {
   return c->hg_done.as<int32_t>();
 }
 
+// Expected regime of the step's active sets from the configuration: sparse
+// when the batch's (sample, row) pairs are few against the output width --
+// a sample's set is ~min(beta, L * cap) ids (wide-out, scaled: ~1 sample per
+// active row), dense when the full union of L buckets is taken for every
+// sample (wide-in: ~45 samples per active row).
+static int64_t expected_pairs(const slide_ctx* c, int b) {
+  const slide_net_desc& d = c->d;
+  if (d.family == 0) return 0;
+  const int64_t lcap = d.l * d.capacity;
+  const int64_t per = (d.strategy == 0 && d.beta >= lcap) ? lcap : std::min<int64_t>(d.beta, lcap);
+  return (int64_t)b * per / std::max(c->G, 1);
+}
+static bool sparse_sets(const slide_ctx* c, int b) {
+  return c->d.family != 0 && expected_pairs(c, b) * 4 < c->n_local;
+}
+
 static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration, int64_t slot_offset,
                          int64_t* n_pairs) {
   const slide_net_desc& d = c->d;
@@ -801,6 +817,7 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   GroupBy& gr = c->grow;
   if (c->grow_pending) gr.clear(s);
   gr.want_inv = true;  // the softmax scatters the errors into row-grouped order
+  gr.items_hint = expected_pairs(c, b);
   gr.prepare(c->n_local, b, P_max);
   // unsharded dense grouping: the pairs kernel fills the row slot masks
   // itself and no placement pass runs -- the logits are written in row order
@@ -896,7 +913,11 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
   const float* dh = ext_dh;
   if (!dh) {
     float* out = c->dh.ensure<float>((size_t)b * hp);
-    if (P_max > 0 && b <= 1024)  // the errors in row-grouped order (dsort) and the grouping
+    // by rows (each W2 row read once per 32-slot window) when rows are shared
+    // by many samples; by samples when the active sets barely overlap (then
+    // every window would walk every row for ~one pair)
+    const bool hg_rows = !getenv_flag("SLIDE_HG_SAMPLES") && (getenv_flag("SLIDE_HG_ROWS") || !sparse_sets(c, b));
+    if (P_max > 0 && b <= 1024 && hg_rows)  // the errors in row-grouped order (dsort) and the grouping
       launch_hidden_grad_rows(hp, b, gr.view(), c->dsort.as<float>(), d.w2, c->h.as<float>(), c->live.as<int32_t>(),
                               out, c->partial.ensure<float>(hidden_grad_rows_scratch(b, hp)), update ? c->work.ensure<int32_t>(4) : nullptr, s);
     else

@@ -447,7 +447,8 @@ void GroupBy::prepare(int64_t key_space, int64_t slots, int64_t items_max) {
   u_max = std::min<int64_t>(key_space, std::max<int64_t>(items_max, 1));
   // dense-mask mode when the whole key space's masks are small (<= 32 MB)
   // and the scan over the key space is not much longer than the item list
-  dense = key_space * wpk * 4 <= ((int64_t)32 << 20) && key_space <= 4 * std::max<int64_t>(items_max, 1);
+  const int64_t items_est = items_hint > 0 ? std::min(items_hint, items_max) : items_max;
+  dense = key_space * wpk * 4 <= ((int64_t)32 << 20) && key_space <= 4 * std::max<int64_t>(items_est, 1);
   key_rank.ensure<int32_t>(key_space);
   uniq.ensure<int32_t>(u_max);
   seg_cnt.ensure<int32_t>(u_max);

@@ -135,6 +135,9 @@ struct GroupBy {
   // scan tiles (mark_args()); place = false -- no placement pass, the
   // consumers derive positions from the masks (GroupView::pos_of)
   bool premarked = false, place = true;
+  // expected item count (0: use the bound): the dense mode scans every key's
+  // mask, worth it only when the items are not much sparser than the keys
+  int64_t items_hint = 0;
   DBuf inv, sslot;
   int64_t K = 0, nwords = 0, u_max = 0, bits_words = 0, mask_words = 0, tiles_bits = 0, tiles_seg = 0;
   int wpk = 1;
