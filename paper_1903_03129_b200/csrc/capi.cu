@@ -67,6 +67,7 @@ struct slide_ctx {
   // third stream: the per-row logits beside the dense-tile logits
   cudaStream_t s3 = nullptr;
   cudaEvent_t ev_lg = nullptr, ev_lg_join = nullptr, ev_w1l = nullptr, ev_hg = nullptr;
+  cudaEvent_t ev_rng = nullptr, ev_rng_join = nullptr;  // slot streams beside the hidden forward
   DBuf hg_done;  // per-sample slice tickets of the hidden gradient (self-resetting)
   int64_t hg_done_n = 0;
   // set by the fused step callers: forward already queues the W1 grouping
@@ -346,7 +347,8 @@ int slide_destroy(slide_ctx* c) {
     c->gfeat.release();
     if (c->s2) cudaStreamSynchronize(c->s2);
     if (c->s3) cudaStreamSynchronize(c->s3);
-    for (cudaEvent_t e : {c->ev_fork, c->ev_dh, c->ev_join, c->ev_pre, c->ev_lg, c->ev_lg_join, c->ev_w1l, c->ev_hg})
+    for (cudaEvent_t e : {c->ev_fork, c->ev_dh, c->ev_join, c->ev_pre, c->ev_lg, c->ev_lg_join, c->ev_w1l, c->ev_hg,
+                          c->ev_rng, c->ev_rng_join})
       if (e) cudaEventDestroy(e);
     if (c->s2) cudaStreamDestroy(c->s2);
     if (c->s3) cudaStreamDestroy(c->s3);
@@ -603,7 +605,8 @@ static void side_stream_init(slide_ctx* c) {
   SLIDE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   SLIDE_CUDA(cudaStreamCreateWithPriority(&c->s2, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
   SLIDE_CUDA(cudaStreamCreateWithPriority(&c->s3, cudaStreamNonBlocking, hi));
-  for (cudaEvent_t* e : {&c->ev_fork, &c->ev_dh, &c->ev_join, &c->ev_pre, &c->ev_lg, &c->ev_lg_join, &c->ev_w1l, &c->ev_hg})
+  for (cudaEvent_t* e : {&c->ev_fork, &c->ev_dh, &c->ev_join, &c->ev_pre, &c->ev_lg, &c->ev_lg_join, &c->ev_w1l,
+                         &c->ev_hg, &c->ev_rng, &c->ev_rng_join})
     SLIDE_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
 }
 
@@ -698,6 +701,22 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     qh.c = f.c;
     qh.keys = c->qkeys.ensure<uint32_t>((size_t)b * L);
   }
+  // the slot streams need only (seed, iteration, slot): drawn on the third
+  // stream beside the hidden forward / query hash, joined before selection
+  const bool lsh_sel = !bt->forced_ptr && d.family != 0;
+  const bool early_vanilla = d.strategy == 0;
+  const bool early_full_union = early_vanilla && d.beta >= (int64_t)L * d.capacity;
+  const bool early_rng = lsh_sel && !c->timer.on && (!early_full_union || bt->rng_states) && c->shard_phase != 2;
+  if (early_rng) {
+    side_stream_init(c);
+    uint64_t* states0 = c->states.ensure<uint64_t>((size_t)b * 6);
+    uint8_t* order0 = c->order.ensure<uint8_t>((size_t)b * L);
+    SLIDE_CUDA(cudaEventRecord(c->ev_rng, s));
+    SLIDE_CUDA(cudaStreamWaitEvent(c->s3, c->ev_rng, 0));
+    launch_slot_rng(b, d.seed, iteration, iter_dev, slot_offset, L, early_vanilla, bt->rng_states, states0, order0,
+                    c->s3);
+    SLIDE_CUDA(cudaEventRecord(c->ev_rng_join, c->s3));
+  }
   // sharded: h was assembled from the all-gathered unit shards (slide_shard_assemble)
   if (c->G == 1)
     launch_hidden_forward(hp, b, bt->x_ptr, bt->x_idx, bt->x_val, d.w1t, d.b1, h, hmask, live, live_ticket(c), s,
@@ -734,7 +753,9 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     // slot stream is only needed by the (rare) fallback, which derives it
     const bool full_union = vanilla && d.beta >= lcap;
     const bool rng_first = !full_union || bt->rng_states;
-    if (rng_first && c->shard_phase != 2)
+    if (early_rng)
+      SLIDE_CUDA(cudaStreamWaitEvent(s, c->ev_rng_join, 0));
+    else if (rng_first && c->shard_phase != 2)
       launch_slot_rng(b, d.seed, iteration, iter_dev, slot_offset, L, vanilla, bt->rng_states, states, order, s);
     c->timer.mark(s, kStSlotRng);
     cap_max = std::max<int64_t>(lcap, want) + max_labels;
@@ -840,7 +861,10 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   gr.run(prow, pslot, offs + b, 0, P_max, s);
   c->grow_pending = true;
   c->timer.mark(s, kStGroupRows);
-  {
+  if (sparse_sets(c, b) && !c->rows_mode) {
+    // ~one sample per active row: pair by pair, sample-major
+    launch_logits_pairs(hp, offs + b, P_max, prow, pslot, d.w2, d.b2, h, live, z, s);
+  } else {
     // per-row logits of the sparse tiles beside the dense tiles (third stream)
     const bool fork = !c->timer.on;
     cudaStream_t sr = s;

@@ -195,6 +195,10 @@ void launch_live_cols_from_h(int hp, int b, const float* h, uint32_t* hmask, int
 
 // s_rows: the stream of the per-row (sparse tile) kernel, concurrent with
 // the dense tiles on s (the caller joins it)
+// sparse sets: z[p] = W2[prow[p]] . h[pslot[p]] + b2[prow[p]], p < *n_dev (sample-major)
+void launch_logits_pairs(int hp, const int32_t* n_dev, int64_t n_max, const int32_t* prow, const int32_t* pslot,
+                         const float* w2, const float* b2, const float* h, const int32_t* live, float* z,
+                         cudaStream_t s);
 void launch_logits_rows(int hp, int b, const GroupView& g, const int32_t* pslot, const float* w2, const float* b2,
                         const float* h, const int32_t* live, float* z, cudaStream_t s, cudaStream_t s_rows);
 

@@ -550,6 +550,49 @@ __global__ void __launch_bounds__(256) logits_rows_kernel(int hp, int b, GroupVi
   }
 }
 
+// Sparse active sets (wide-out, scaled: ~1 sample per active row): the
+// logits pair by pair in sample-major order, no row grouping -- 8 lanes per
+// pair, each lane 4 live units of every live group, an 8-lane butterfly.
+__global__ void __launch_bounds__(256) logits_pairs_kernel(int hp, const int32_t* __restrict__ n_dev,
+                                                           const int32_t* __restrict__ prow,
+                                                           const int32_t* __restrict__ pslot,
+                                                           const float* __restrict__ w2, const float* __restrict__ b2,
+                                                           const float* __restrict__ h,
+                                                           const int32_t* __restrict__ live, float* __restrict__ z) {
+  const int lane = threadIdx.x & 31, g8 = lane & 7;
+  const int64_t n = *n_dev;
+  const int ng = max(1, (__ldg(live) + 31) >> 5);
+  const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const int64_t np = ((int64_t)gridDim.x * blockDim.x) >> 3;
+  for (int64_t p = p0; p - (lane >> 3) < n; p += np) {  // the warp's 4 pairs stay together for the butterfly
+    const bool ok = p < n;
+    const int r = ok ? prow[p] : 0, sl = ok ? pslot[p] : 0;
+    const float* wr = w2 + (int64_t)r * hp;
+    const float* hr = h + (int64_t)sl * hp;
+    float acc = 0.f;
+    for (int q = 0; q < ng; ++q) {
+      int c[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) c[k] = __ldg(live + 1 + 32 * q + 4 * g8 + k);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc = fmaf(__ldg(wr + c[k]), __ldg(hr + c[k]), acc);
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (ok && g8 == 0) z[p] = acc + b2[r];
+  }
+}
+
+void launch_logits_pairs(int hp, const int32_t* n_dev, int64_t n_max, const int32_t* prow, const int32_t* pslot,
+                         const float* w2, const float* b2, const float* h, const int32_t* live, float* z,
+                         cudaStream_t s) {
+  if (n_max <= 0) return;
+  const int grid = (int)std::min<int64_t>(ceil_div(n_max, 32), (int64_t)kSms * 16);
+  logits_pairs_kernel<<<grid, 256, 0, s>>>(hp, n_dev, prow, pslot, w2, b2, h, live, z);
+  SLIDE_LAUNCH_CHECK();
+}
+
 void launch_logits_rows(int hp, int b, const GroupView& g, const int32_t* pslot, const float* w2, const float* b2,
                         const float* h, const int32_t* live, float* z, cudaStream_t s, cudaStream_t s_rows) {
   if (g.u_max <= 0) return;
