@@ -95,7 +95,10 @@ struct slide_ctx {
   int shard_phase = 0;
   // the last forward's row grouping ran place-free (see forward_impl)
   bool rows_mode = false;
-  DBuf prob_tmp;
+  // ... and its softmax was lazy (training steps: per-tile partials, the
+  // errors made by the hidden gradient / W2 Adam from the logits)
+  bool lazy = false;
+  DBuf prob_tmp, sm_part, sm_stat;
   const int32_t* shard_ghist = nullptr;
   int32_t* shard_hist = nullptr;
   DBuf shard_pack;
@@ -341,7 +344,7 @@ int slide_destroy(slide_ctx* c) {
     for (DBuf* b : {&c->sh_packed, &c->sh_packed_t, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->dsort, &c->hmask, &c->live, &c->live_ticket, &c->qkeys, &c->order,
                     &c->states, &c->act, &c->cnt, &c->empty, &c->offs, &c->prow, &c->pslot, &c->plab, &c->z,
                     &c->prob, &c->delta, &c->loss, &c->dh, &c->fb_ids, &c->fb_scratch, &c->fb_bitmap, &c->xslot,
-                    &c->tc, &c->bc, &c->counters, &c->partial, &c->long_list, &c->n_long, &c->work, &c->topk_out, &c->topk_cnt, &c->tc_scratch, &c->bias_table, &c->cnt_all, &c->prob_tmp, &c->shard_pack, &c->fb_rng})
+                    &c->tc, &c->bc, &c->counters, &c->partial, &c->long_list, &c->n_long, &c->work, &c->topk_out, &c->topk_cnt, &c->tc_scratch, &c->bias_table, &c->cnt_all, &c->prob_tmp, &c->shard_pack, &c->fb_rng, &c->sm_part, &c->sm_stat})
       b->release();
     c->grow.release();
     c->gfeat.release();
@@ -839,6 +842,7 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   if (c->grow_pending) gr.clear(s);
   gr.want_inv = true;  // the softmax scatters the errors into row-grouped order
   gr.items_hint = expected_pairs(c, b);
+  gr.want_lmask = c->G == 1 && c->w1_prefork;
   gr.prepare(c->n_local, b, P_max);
   // unsharded dense grouping: the pairs kernel fills the row slot masks
   // itself and no placement pass runs -- the logits are written in row order
@@ -846,9 +850,14 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   c->rows_mode = c->G == 1 && gr.dense && !getenv_flag("SLIDE_PLACED_GROUPING");
   gr.premarked = c->rows_mode;
   gr.place = !c->rows_mode;
+  // lazy when the samples' sets are large (full unions: thousands of pairs per
+  // sample, where the per-pair position lookups dominate the softmax)
+  c->lazy = c->rows_mode && c->w1_prefork && gr.lmask_words > 0 && !getenv_flag("SLIDE_EAGER_SOFTMAX") &&
+            (expected_pairs(c, b) >= (int64_t)b * 1024 || getenv_flag("SLIDE_LAZY_SOFTMAX"));
   if (c->rows_mode) {
     const GroupBy::MarkArgs m = gr.mark_args();
-    launch_pairs(b, act, cap_max, cnt, offs, c->G, prow, pslot, plab, s, m.mask, m.wpk, m.status, m.ctr, m.n_tiles);
+    launch_pairs(b, act, cap_max, cnt, offs, c->G, prow, pslot, plab, s, m.mask, m.wpk, m.status, m.ctr, m.n_tiles,
+                 c->lazy ? m.lmask : nullptr);
   } else {
     launch_pairs(b, act, cap_max, cnt, offs, c->G, prow, pslot, plab, s);
   }
@@ -882,7 +891,11 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
   }
   c->timer.mark(s, kStLogits);
   // sharded: the softmax is completed by the slide_shard_softmax_* stages
-  if (c->G == 1) {
+  if (c->G == 1 && c->lazy) {
+    launch_softmax_lazy(b, gr.view(), gr.lmask.as<uint32_t>(), z, bt->y_ptr, bt->y_idx,
+                        c->sm_part.ensure<float2>(softmax_lazy_parts(gr.u_max, b)),
+                        c->sm_stat.ensure<float>((size_t)3 * b), loss, s);
+  } else if (c->G == 1) {
     const GroupView rv = gr.view();
     launch_softmax(b, offs, plab, bt->y_ptr, z, prob, delta, loss, gr.inv.as<int32_t>(), dsort, s,
                    c->rows_mode ? prow : nullptr, c->rows_mode ? &rv : nullptr,
@@ -943,7 +956,9 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
     const bool hg_rows = !getenv_flag("SLIDE_HG_SAMPLES") && (getenv_flag("SLIDE_HG_ROWS") || !sparse_sets(c, b));
     if (P_max > 0 && b <= 1024 && hg_rows)  // the errors in row-grouped order (dsort) and the grouping
       launch_hidden_grad_rows(hp, b, gr.view(), c->dsort.as<float>(), d.w2, c->h.as<float>(), c->live.as<int32_t>(),
-                              out, c->partial.ensure<float>(hidden_grad_rows_scratch(b, hp)), update ? c->work.ensure<int32_t>(4) : nullptr, s);
+                              out, c->partial.ensure<float>(hidden_grad_rows_scratch(b, hp)), update ? c->work.ensure<int32_t>(4) : nullptr, s,
+                              c->lazy ? c->z.as<float>() : nullptr, c->lazy ? c->sm_stat.as<float>() : nullptr,
+                              c->lazy ? gr.lmask.as<uint32_t>() : nullptr);
     else
       launch_hidden_grad(hp, b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->delta.as<float>(), d.w2,
                          c->h.as<float>(), c->live.as<int32_t>(), out,
@@ -952,9 +967,10 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
     dh = out;
   }
   c->timer.mark(s, kStHiddenGrad);
-  if (fork && c->grow_pending) {
+  if (fork && c->grow_pending && !c->lazy) {
     // the row grouping's masks were last read by the hidden gradient: clear
-    // them on the third stream beside the rest of the backward pass
+    // them on the third stream beside the rest of the backward pass (a lazy
+    // softmax's W2 Adam still reads them: cleared after it, below)
     SLIDE_CUDA(cudaEventRecord(c->ev_hg, s));
     SLIDE_CUDA(cudaStreamWaitEvent(c->s3, c->ev_hg, 0));
     gr.clear(c->s3);
@@ -1016,7 +1032,9 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
                      gr.seg_cnt.as<int32_t>(), gr.sslot.as<int32_t>(), c->dsort.as<float>(),
                      c->h.as<float>(), c->live.as<int32_t>(), d.w2, d.m2, d.v2, d.b2, d.mb2, d.vb2, d.steps2, ctr,
                      work,
-                     /*work_zeroed=*/ext_dh == nullptr, s);
+                     /*work_zeroed=*/ext_dh == nullptr, s, c->lazy ? c->z.as<float>() : nullptr,
+                     c->lazy ? c->sm_stat.as<float>() : nullptr, c->lazy ? gr.mask.as<uint32_t>() : nullptr,
+                     c->lazy ? gr.lmask.as<uint32_t>() : nullptr, gr.wpk);
     c->timer.mark(s, kStAdamRows);
   }
   if (!fork) w1_update(s);
@@ -1383,8 +1401,18 @@ int slide_read(slide_ctx* c, int64_t what, void* dst, int64_t max_bytes, int64_t
       case 2: src = c->offs.p; n = (b + 1) * 4; break;
       case 3: src = c->prow.p; n = P * 4; break;
       case 4: src = c->plab.p; n = P; break;
-      case 5: src = c->prob.p; n = P * 4; break;
-      case 6: src = c->delta.p; n = P * 4; break;
+      case 5:
+      case 6:  // probabilities / errors per pair (made from the logits after a lazy softmax)
+        if (c->lazy) {
+          float* tmp = c->prob_tmp.ensure<float>(std::max<int64_t>(P, 1));
+          launch_lazy_pairs((int)b, c->offs.as<int32_t>(), c->prow.as<int32_t>(), c->plab.as<uint8_t>(),
+                            c->grow.view(), c->z.as<float>(), c->sm_stat.as<float>(), tmp, what == 6, c->s);
+          src = tmp;
+        } else {
+          src = what == 5 ? c->prob.p : c->delta.p;
+        }
+        n = P * 4;
+        break;
       case 7: src = c->loss.p; n = b * 8; break;
       case 8: src = c->dh.p; n = b * hp * 4; break;
       case 9: src = c->empty.p; n = b * 4; break;

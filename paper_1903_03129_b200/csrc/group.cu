@@ -432,10 +432,13 @@ __global__ void __launch_bounds__(256) gd_place_kernel(const int32_t* __restrict
 }
 
 __global__ void gd_clear_kernel(const int32_t* __restrict__ uniq, const int32_t* __restrict__ n_uniq, int wpk,
-                                uint32_t* __restrict__ mask) {
+                                uint32_t* __restrict__ mask, uint32_t* __restrict__ lmask) {
   const int64_t n = (int64_t)*n_uniq * wpk;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
-    mask[(int64_t)uniq[q / wpk] * wpk + q % wpk] = 0u;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = (int64_t)uniq[q / wpk] * wpk + q % wpk;
+    mask[o] = 0u;
+    if (lmask) lmask[o] = 0u;
+  }
 }
 
 static int grid_of(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), kSms * 8)); }
@@ -462,6 +465,10 @@ void GroupBy::prepare(int64_t key_space, int64_t slots, int64_t items_max) {
   ctrs.ensure<int32_t>(2);
   if (dense) {
     const int64_t need = key_space * wpk;
+    if (want_lmask && lmask_words < need) {
+      SLIDE_CUDA(cudaMemset(lmask.ensure<uint32_t>(need), 0, need * 4));  // kept zero between runs by clear()
+      lmask_words = need;
+    }
     if (mask_words < need || !mask_dense) {
       uint32_t* m = mask.ensure<uint32_t>(need);
       SLIDE_CUDA(cudaMemset(m, 0, need * 4));  // kept zero between runs by clear()
@@ -550,7 +557,7 @@ void GroupBy::run(const int32_t* keys, const int32_t* slots, const int32_t* n_de
 void GroupBy::clear(cudaStream_t s) {
   if (!dense) return;
   gd_clear_kernel<<<grid_of(u_max * wpk), 256, 0, s>>>(uniq.as<int32_t>(), n_uniq.as<int32_t>(), wpk,
-                                                       mask.as<uint32_t>());
+                                                       mask.as<uint32_t>(), lmask_words ? lmask.as<uint32_t>() : nullptr);
   SLIDE_LAUNCH_CHECK();
 }
 
@@ -558,7 +565,8 @@ void GroupBy::release() {
   for (DBuf* b : {&bits, &key_rank, &uniq, &seg_cnt, &seg_off, &n_uniq, &mask, &order, &inv, &sslot, &status, &ctrs,
                   &long_list, &n_long})
     b->release();
-  bits_words = mask_words = 0;
+  bits_words = mask_words = lmask_words = 0;
+  lmask.release();
   mask_dense = false;
 }
 

@@ -74,7 +74,7 @@ void launch_explicit_active(int b, int64_t n, const int32_t* fptr, const int32_t
 void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* cnt, int32_t* offs, int shard_count,
                   int32_t* prow, int32_t* pslot, uint8_t* plab, cudaStream_t s, uint32_t* mark_mask = nullptr,
                   int mark_wpk = 0, unsigned long long* mark_status = nullptr, int32_t* mark_ctr = nullptr,
-                  int64_t mark_tiles = 0);
+                  int64_t mark_tiles = 0, uint32_t* mark_lmask = nullptr);
 void launch_counts_to_f64(int b, const int32_t* cnt, double* out, cudaStream_t s);
 void launch_own_filter(int b, int32_t* act, int64_t cap_max, int g, int G, int32_t* cnt, int32_t* cnt_all,
                        cudaStream_t s);
@@ -138,6 +138,11 @@ struct GroupBy {
   // expected item count (0: use the bound): the dense mode scans every key's
   // mask, worth it only when the items are not much sparser than the keys
   int64_t items_hint = 0;
+  // dense mode: a second mask per key marking the items that are labels
+  // (the lazy softmax, see capi.cu); filled by the caller's marking pass
+  bool want_lmask = false;
+  DBuf lmask;
+  int64_t lmask_words = 0;
   DBuf inv, sslot;
   int64_t K = 0, nwords = 0, u_max = 0, bits_words = 0, mask_words = 0, tiles_bits = 0, tiles_seg = 0;
   int wpk = 1;
@@ -161,9 +166,11 @@ struct GroupBy {
     unsigned long long* status;
     int32_t* ctr;
     int64_t n_tiles;
+    uint32_t* lmask;
   };
   MarkArgs mark_args() {
-    return MarkArgs{mask.as<uint32_t>(), wpk, status.as<unsigned long long>(), ctrs.as<int32_t>(), tiles_bits};
+    return MarkArgs{mask.as<uint32_t>(), wpk, status.as<unsigned long long>(), ctrs.as<int32_t>(), tiles_bits,
+                    want_lmask && lmask_words ? lmask.as<uint32_t>() : nullptr};
   }
 };
 
@@ -208,6 +215,15 @@ void launch_logits_rows(int hp, int b, const GroupView& g, const int32_t* pslot,
 void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
                     float* prob, float* delta, double* loss, const int32_t* inv, float* dsort, cudaStream_t s,
                     const int32_t* prow = nullptr, const GroupView* rows = nullptr, int32_t* sslot = nullptr);
+// lazy softmax of a training step under the place-free grouping: per-tile
+// partials (part: softmax_lazy_parts(u_max, b) float2), per sample stat =
+// (M, 1/S, 1/|Y|) and the loss; pairs' errors are made where they are read
+void launch_softmax_lazy(int b, const GroupView& g, const uint32_t* lmask, const float* z, const int32_t* y_ptr,
+                         const int32_t* y_idx, float2* part, float* stat, double* loss, cudaStream_t s);
+int64_t softmax_lazy_parts(int64_t u_max, int b);
+// p (want_delta = false) or delta per pair, sample-major, of a lazy step
+void launch_lazy_pairs(int b, const int32_t* offs, const int32_t* prow, const uint8_t* plab, const GroupView& g,
+                       const float* z, const float* stat, float* out, bool want_delta, cudaStream_t s);
 // place-free row grouping: out[pair] = rows_src[pos(pair)] (to_pairs) or
 // rows_dst[pos(pair)] = src[pair] (to_rows), pairs in sample-major order
 void launch_rows_pairs(int b, const int32_t* offs, const int32_t* prow, const GroupView& g, const float* src,
@@ -219,7 +235,8 @@ void launch_scatter_sorted(const int32_t* n_dev, int64_t n_max, const int32_t* i
 // row-grouped order, dsort); scratch floats: hidden_grad_rows_scratch
 size_t hidden_grad_rows_scratch(int b, int hp);
 void launch_hidden_grad_rows(int hp, int b, const GroupView& g, const float* dsort, const float* w2, const float* h,
-                             const int32_t* live, float* dh, float* part, int32_t* work_reset, cudaStream_t s);
+                             const int32_t* live, float* dh, float* part, int32_t* work_reset, cudaStream_t s,
+                             const float* z = nullptr, const float* stat = nullptr, const uint32_t* lmask = nullptr);
 // floats of scratch launch_hidden_grad needs
 size_t hidden_grad_scratch(int b, int hp);
 // done: b zero-initialised ints (self-resetting); work_reset (optional): the
@@ -231,7 +248,9 @@ void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq
                       const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
                       const int32_t* sslot, const float* dsort, const float* h, const int32_t* live, float* w2,
                       float* m2, float* v2, float* b2, float* mb2, float* vb2, int64_t* steps2,
-                      unsigned long long* touched, int32_t* work, bool work_zeroed, cudaStream_t s);
+                      unsigned long long* touched, int32_t* work, bool work_zeroed, cudaStream_t s,
+                      const float* z = nullptr, const float* stat = nullptr, const uint32_t* mask = nullptr,
+                      const uint32_t* lmask = nullptr, int wpk = 0);
 void launch_accumulate(unsigned long long* dst, const int32_t* src, cudaStream_t s);
 // per slot: the k best active ids by probability (ties: lower id), -1 padded
 void launch_topk(int b, const int32_t* offs, const int32_t* rows, int shard_count, int shard_rank, const float* prob,

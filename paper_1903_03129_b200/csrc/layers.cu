@@ -742,6 +742,149 @@ void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32
   SLIDE_LAUNCH_CHECK();
 }
 
+// ------------------------------------------------ lazy softmax (rows mode)
+// Training steps under the place-free grouping do not materialise p / delta
+// per pair: per 64-row tile of the grouping and per slot, the online (max,
+// sum exp) of the slot's logits in those rows; per sample, the tiles
+// combined (max, then sum) and the label loss terms; the hidden gradient and
+// the W2 Adam then compute each pair's error from its logit where they read
+// it (row order, coalesced): delta = exp(z - M_i) / S_i - [label] / |Y_i|.
+constexpr int kLzRows = 16;  // rows per tile: every slot's loads of a tile in flight at once
+
+__global__ void __launch_bounds__(256) softmax_partials_kernel(GroupView g, const uint32_t* __restrict__ lmask,
+                                                               const float* __restrict__ z, int b,
+                                                               float2* __restrict__ part) {
+  __shared__ int s_off[kLzRows];
+  __shared__ uint32_t s_mk[kLzRows][32], s_pre[kLzRows][32];
+  const int64_t nu = *g.n_uniq;
+  const int64_t tiles = (nu + kLzRows - 1) / kLzRows;
+  const int wpk = g.wpk;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int nr = (int)min((int64_t)kLzRows, nu - t * kLzRows);
+    __syncthreads();  // the previous tile's readers are done
+    for (int q = threadIdx.x; q < nr * wpk; q += blockDim.x) {
+      const int r = q / wpk, w = q - r * wpk;
+      const int64_t u = t * kLzRows + r;
+      s_mk[r][w] = __ldg(g.mask_of(u) + w);
+      if (w == 0) s_off[r] = __ldg(g.seg_off + u);
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < nr; r += blockDim.x) {  // exclusive popcount prefix per row
+      uint32_t acc = 0;
+      for (int w = 0; w < wpk; ++w) {
+        s_pre[r][w] = acc;
+        acc += __popc(s_mk[r][w]);
+      }
+    }
+    __syncthreads();
+    for (int slot = threadIdx.x; slot < b; slot += blockDim.x) {
+      const int w = slot >> 5;
+      const uint32_t bit = 1u << (slot & 31), lo = bit - 1u;
+      float zv[kLzRows];
+#pragma unroll
+      for (int r = 0; r < kLzRows; ++r) {  // the slot's logits of the tile, all loads in flight
+        const uint32_t word = r < nr ? s_mk[r][w] : 0u;
+        zv[r] = (word & bit) ? __ldg(z + s_off[r] + s_pre[r][w] + __popc(word & lo)) : -INFINITY;
+      }
+      float m = -INFINITY;
+#pragma unroll
+      for (int r = 0; r < kLzRows; ++r) m = fmaxf(m, zv[r]);
+      float sum = 0.f;
+#pragma unroll
+      for (int r = 0; r < kLzRows; ++r) sum += zv[r] == -INFINITY ? 0.f : expf(zv[r] - m);
+      part[t * b + slot] = make_float2(m, sum);
+    }
+  }
+}
+
+// per sample: M, 1 / S, 1 / |Y| and the loss (reference network.py:154-158,
+// 282-285: -log p_y = M + log S - z_y per label, clamped at -log 1e-300)
+__global__ void __launch_bounds__(256) softmax_combine_kernel(GroupView g, const float2* __restrict__ part, int b,
+                                                              const int32_t* __restrict__ y_ptr,
+                                                              const int32_t* __restrict__ y_idx,
+                                                              const float* __restrict__ z, float* __restrict__ stat,
+                                                              double* __restrict__ loss) {
+  using RF = cub::BlockReduce<float, 256>;
+  using RD = cub::BlockReduce<double, 256>;
+  __shared__ union {
+    typename RF::TempStorage f;
+    typename RD::TempStorage d;
+  } tmp;
+  __shared__ float s_m, s_s;
+  const int i = blockIdx.x;
+  const int64_t tiles = (*g.n_uniq + kLzRows - 1) / kLzRows;
+  float m = -INFINITY;
+  for (int64_t t = threadIdx.x; t < tiles; t += blockDim.x) m = fmaxf(m, part[t * b + i].x);
+  m = RF(tmp.f).Reduce(m, cub::Max());
+  if (threadIdx.x == 0) s_m = m;
+  __syncthreads();
+  m = s_m;
+  float sum = 0.f;
+  for (int64_t t = threadIdx.x; t < tiles; t += blockDim.x) {
+    const float2 pt = part[t * b + i];
+    if (pt.y > 0.f) sum += pt.y * expf(pt.x - m);
+  }
+  __syncthreads();
+  sum = RF(tmp.f).Sum(sum);
+  if (threadIdx.x == 0) s_s = sum;
+  __syncthreads();
+  sum = s_s;
+  const int y0 = y_ptr[i], ny = y_ptr[i + 1] - y0;
+  const float lse = logf(sum);
+  double lsum = 0.0;
+  for (int k = threadIdx.x; k < ny; k += blockDim.x) {
+    const int row = y_idx[y0 + k];
+    const float zz = __ldg(z + g.pos_of(row, i)) - m;
+    const double nl = -((double)zz - (double)lse);
+    lsum += (nl < 690.7755278982137 || nl != nl) ? nl : 690.7755278982137;  // NaN propagates (np.maximum)
+  }
+  __syncthreads();
+  lsum = RD(tmp.d).Sum(lsum);
+  if (threadIdx.x == 0) {
+    loss[i] = ny > 0 ? lsum / ny : (double)NAN;
+    stat[3 * i] = m;
+    stat[3 * i + 1] = sum > 0.f ? 1.f / sum : 0.f;
+    stat[3 * i + 2] = ny > 0 ? 1.f / (float)ny : 0.f;
+  }
+}
+
+__device__ __forceinline__ float lazy_delta(float zz, const float* __restrict__ stat, int slot, bool lab) {
+  const float p = expf(zz - __ldg(stat + 3 * slot)) * __ldg(stat + 3 * slot + 1);
+  return lab ? p - __ldg(stat + 3 * slot + 2) : p;
+}
+
+void launch_softmax_lazy(int b, const GroupView& g, const uint32_t* lmask, const float* z, const int32_t* y_ptr,
+                         const int32_t* y_idx, float2* part, float* stat, double* loss, cudaStream_t s) {
+  if (b <= 0) return;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.u_max, kLzRows), (int64_t)kSms * 4));
+  softmax_partials_kernel<<<grid, 256, 0, s>>>(g, lmask, z, b, part);
+  SLIDE_LAUNCH_CHECK();
+  softmax_combine_kernel<<<b, 256, 0, s>>>(g, part, b, y_ptr, y_idx, z, stat, loss);
+  SLIDE_LAUNCH_CHECK();
+}
+
+int64_t softmax_lazy_parts(int64_t u_max, int b) { return std::max<int64_t>(1, ceil_div(u_max, kLzRows)) * b; }
+
+// readouts of a lazy step: per pair (sample-major) its p (what 5) or delta (6)
+__global__ void lazy_pairs_kernel(const int32_t* __restrict__ offs, const int32_t* __restrict__ prow,
+                                  const uint8_t* __restrict__ plab, GroupView g, const float* __restrict__ z,
+                                  const float* __restrict__ stat, float* __restrict__ out, int want_delta) {
+  const int i = blockIdx.x;
+  const int o = offs[i], n = offs[i + 1] - o;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const float zz = z[g.pos_of(prow[o + k], i)];
+    const float p = expf(zz - stat[3 * i]) * stat[3 * i + 1];
+    out[o + k] = want_delta && plab[o + k] ? p - stat[3 * i + 2] : p;
+  }
+}
+
+void launch_lazy_pairs(int b, const int32_t* offs, const int32_t* prow, const uint8_t* plab, const GroupView& g,
+                       const float* z, const float* stat, float* out, bool want_delta, cudaStream_t s) {
+  if (b <= 0) return;
+  lazy_pairs_kernel<<<b, 256, 0, s>>>(offs, prow, plab, g, z, stat, out, want_delta ? 1 : 0);
+  SLIDE_LAUNCH_CHECK();
+}
+
 __global__ void rows_pairs_kernel(const int32_t* __restrict__ offs, const int32_t* __restrict__ prow, GroupView g,
                                   const float* __restrict__ src, float* __restrict__ dst, int to_pairs) {
   const int i = blockIdx.x;
@@ -902,6 +1045,10 @@ struct HiddenGradRowsArgs {
   const int32_t* live;
   float *part, *dh;
   int32_t* work_reset;
+  // lazy softmax (z != null): errors made from the row-order logits, the
+  // per-sample stat (M, 1/S, 1/|Y|) and the label masks, instead of dsort
+  const float *z = nullptr, *stat = nullptr;
+  const uint32_t* lmask = nullptr;
 };
 
 // one pass per live group g0 (32 live columns).  Lane t holds slot
@@ -926,10 +1073,12 @@ __device__ __forceinline__ void hg_rows_body(const HiddenGradRowsArgs& A, float*
     const bool ok = uj < u_end;
     const int row_l = ok ? __ldg(A.g.uniq + uj) : 0;
     int p0_l = ok ? __ldg(A.g.seg_off + uj) : 0;
-    uint32_t bits_l = 0;
+    uint32_t bits_l = 0, lbits_l = 0;
     if (ok) {
-      const uint32_t* mk = A.g.mask + (A.g.mask_by_key ? (int64_t)row_l : uj) * A.g.wpk;
+      const int64_t mo = (A.g.mask_by_key ? (int64_t)row_l : uj) * A.g.wpk;
+      const uint32_t* mk = A.g.mask + mo;
       bits_l = __ldg(mk + win);
+      if (A.z) lbits_l = __ldg(A.lmask + mo + win);
       for (int w = 0; w < win; ++w) p0_l += __popc(__ldg(mk + w));
     }
     const int nr = (int)min((int64_t)32, (u_end - ub + 7) / 8);
@@ -937,9 +1086,16 @@ __device__ __forceinline__ void hg_rows_body(const HiddenGradRowsArgs& A, float*
     // are loaded while row j is added
     auto fetch = [&](int j, float& e, float& w) {
       const uint32_t bits = __shfl_sync(0xffffffffu, bits_l, j);
+      const uint32_t lbits = __shfl_sync(0xffffffffu, lbits_l, j);
       const int p0 = __shfl_sync(0xffffffffu, p0_l, j);
       const int r = __shfl_sync(0xffffffffu, row_l, j);
-      e = (bits >> lane) & 1u ? __ldg(A.dsort + p0 + __popc(bits & below)) : 0.f;
+      if ((bits >> lane) & 1u) {
+        const int pos = p0 + __popc(bits & below);
+        e = A.z ? lazy_delta(__ldg(A.z + pos), A.stat, win * kHgWin + lane, (lbits >> lane) & 1u)
+                : __ldg(A.dsort + pos);
+      } else {
+        e = 0.f;
+      }
       w = bits ? __ldg(A.w2 + (int64_t)r * A.hp + col) : 0.f;
     };
     float e, w;
@@ -1021,10 +1177,11 @@ static int hg_rows_chunks(int b) {
 size_t hidden_grad_rows_scratch(int b, int hp) { return (size_t)hg_rows_chunks(b) * b * hp; }
 
 void launch_hidden_grad_rows(int hp, int b, const GroupView& g, const float* dsort, const float* w2, const float* h,
-                             const int32_t* live, float* dh, float* part, int32_t* work_reset, cudaStream_t s) {
+                             const int32_t* live, float* dh, float* part, int32_t* work_reset, cudaStream_t s,
+                             const float* z, const float* stat, const uint32_t* lmask) {
   if (b <= 0) return;
   const int nwin = (int)ceil_div(b, kHgWin), nchunk = hg_rows_chunks(b);
-  HiddenGradRowsArgs A{hp, b, nwin, nchunk, g, dsort, w2, h, live, part, dh, work_reset};
+  HiddenGradRowsArgs A{hp, b, nwin, nchunk, g, dsort, w2, h, live, part, dh, work_reset, z, stat, lmask};
   hidden_grad_rows_kernel<<<nwin * nchunk, 256, 0, s>>>(A);
   SLIDE_LAUNCH_CHECK();
   hidden_grad_reduce_kernel<<<b, 256, 8 * hp * 4, s>>>(A);
@@ -1120,6 +1277,11 @@ struct AdamRowsArgs {
   int64_t* steps2;
   unsigned long long* touched;
   int32_t* work;
+  // lazy softmax (z != null): each pair's slot from its row's slot mask and
+  // its error from the row-order logit (see softmax_partials_kernel)
+  const float *z = nullptr, *stat = nullptr;
+  const uint32_t *mask = nullptr, *lmask = nullptr;
+  int wpk = 0;
 };
 
 // pairs whose activations are loaded ahead of their updates (8 / NG)
@@ -1184,12 +1346,36 @@ __device__ __forceinline__ void adam_rows_loop(const AdamRowsArgs& A, const int 
     const int64_t st = A.steps2[r];
     // lane j holds the j-th pair of a chunk; the next chunk's slot and error
     // are loaded while this one updates
+    uint32_t wd = 0, lwd = 0;
+    int incl = 0;
+    if (A.z) {  // lazy: the row's slot / label masks in lanes, their popcount prefix
+      wd = lane < A.wpk ? __ldg(A.mask + (int64_t)r * A.wpk + lane) : 0u;
+      lwd = lane < A.wpk ? __ldg(A.lmask + (int64_t)r * A.wpk + lane) : 0u;
+      incl = __popc(wd);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+    }
+    auto fetch = [&](int jj, int& sl, float& d) {  // every lane calls it (shuffles inside)
+      if (!A.z) {
+        if (jj < len) {
+          sl = A.sslot[s0 + jj];
+          d = A.dsort[s0 + jj];
+        }
+        return;
+      }
+      const int slot = mask_select(wd, incl, A.wpk, min(jj, len - 1));
+      const bool lab = (__shfl_sync(0xffffffffu, lwd, slot >> 5) >> (slot & 31)) & 1u;
+      if (jj < len) {
+        sl = slot;
+        d = lazy_delta(__ldg(A.z + s0 + jj), A.stat, slot, lab);
+      }
+    };
     int slot_n = 0;
     float d_n = 0.f;
-    if (lane < len) {
-      slot_n = A.sslot[s0 + lane];
-      d_n = A.dsort[s0 + lane];
-    }
+    fetch(lane, slot_n, d_n);
     for (int c0 = 0; c0 < len; c0 += 32) {
       const int j = c0 + lane;
       const bool valid = j < len;
@@ -1197,10 +1383,7 @@ __device__ __forceinline__ void adam_rows_loop(const AdamRowsArgs& A, const int 
       const float d_l = valid ? d_n : 0.f;
       float2 bc_l = make_float2(0.f, 1.f);
       if (valid) bc_l = bias_corr(A.ap, st + j + 1);
-      if (j + 32 < len) {
-        slot_n = A.sslot[s0 + j + 32];
-        d_n = A.dsort[s0 + j + 32];
-      }
+      if (c0 + 32 < len) fetch(j + 32, slot_n, d_n);
       const float e1_l = ak.omb1 * d_l, e2_l = ak.omb2 * d_l * d_l;
       const float s2_l = sqrt_approx(bc_l.y);
       __syncwarp();
@@ -1389,7 +1572,8 @@ void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq
                       const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
                       const int32_t* sslot, const float* dsort, const float* h, const int32_t* live, float* w2,
                       float* m2, float* v2, float* b2, float* mb2, float* vb2, int64_t* steps2,
-                      unsigned long long* touched, int32_t* work, bool work_zeroed, cudaStream_t s) {
+                      unsigned long long* touched, int32_t* work, bool work_zeroed, cudaStream_t s,
+                      const float* z, const float* stat, const uint32_t* mask, const uint32_t* lmask, int wpk) {
   if (max_uniq <= 0) return;
   if (!work_zeroed) SLIDE_CUDA(cudaMemsetAsync(work, 0, 4, s));
   // persistent: as many CTAs as are resident at once
@@ -1401,7 +1585,7 @@ void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq
   const int per_sm = env_per_sm > 0 ? env_per_sm : (hp <= 128 ? 3 : 2);
   const int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * per_sm);
   AdamRowsArgs A{hp, ap, n_uniq, uniq, seg_off, seg_cnt, sslot, dsort, h, live,
-                 w2, m2, v2, b2, mb2, vb2, steps2, touched, work};
+                 w2, m2, v2, b2, mb2, vb2, steps2, touched, work, z, stat, mask, lmask, wpk};
   if (touched) {
     SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, true><<<grid, 256, 0, s>>>(A)));
   } else {

@@ -762,7 +762,7 @@ __global__ void __launch_bounds__(1024) pairs_kernel(int b, const int32_t* __res
                                                      int32_t* __restrict__ pslot, uint8_t* __restrict__ plab,
                                                      uint32_t* __restrict__ mask, int wpk,
                                                      unsigned long long* __restrict__ status, int32_t* ctr,
-                                                     int64_t n_tiles) {
+                                                     int64_t n_tiles, uint32_t* __restrict__ lmask) {
   if (mask) {  // the row grouping's scan tiles, reset for its scan kernel
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_tiles; q += (int64_t)gridDim.x * blockDim.x)
       status[q] = 0ull;
@@ -800,15 +800,16 @@ __global__ void __launch_bounds__(1024) pairs_kernel(int b, const int32_t* __res
     pslot[o + k] = i;
     plab[o + k] = (uint8_t)(v >> 31);
     if (mask) atomicOr(&mask[(int64_t)row * wpk + (i >> 5)], 1u << (i & 31));  // the row's slot mask
+    if (lmask && (v >> 31)) atomicOr(&lmask[(int64_t)row * wpk + (i >> 5)], 1u << (i & 31));  // a label pair
   }
 }
 
 void launch_pairs(int b, const int32_t* act, int64_t cap_max, const int32_t* cnt, int32_t* offs, int shard_count,
                   int32_t* prow, int32_t* pslot, uint8_t* plab, cudaStream_t s, uint32_t* mark_mask, int mark_wpk,
-                  unsigned long long* mark_status, int32_t* mark_ctr, int64_t mark_tiles) {
+                  unsigned long long* mark_status, int32_t* mark_ctr, int64_t mark_tiles, uint32_t* mark_lmask) {
   SLIDE_CHECK(b <= 1024, kNotSupported, "batch size above 1024 not supported on the device path");
   pairs_kernel<<<b, 1024, 0, s>>>(b, act, cap_max, cnt, shard_count, offs, prow, pslot, plab, mark_mask, mark_wpk,
-                                  mark_status, mark_ctr, mark_tiles);
+                                  mark_status, mark_ctr, mark_tiles, mark_lmask);
   SLIDE_LAUNCH_CHECK();
 }
 
