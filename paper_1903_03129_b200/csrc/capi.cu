@@ -1045,7 +1045,7 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
     launch_accumulate(ctr + 5, c->offs.as<int32_t>() + b, s);
   }
   if (c->grow_pending) {
-    gr.clear(s);
+    if (!(c->lazy && P_max > 0)) gr.clear(s);  // (a lazy step's W2 Adam cleared the masks it walked)
     c->grow_pending = false;
   }
   if (fork) {  // join: the next step reads W1, h and the side streams' buffers

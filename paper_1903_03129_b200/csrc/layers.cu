@@ -1491,6 +1491,10 @@ __device__ __forceinline__ void adam_rows_loop(const AdamRowsArgs& A, const int 
       A.vb2[r] = vb;
       A.steps2[r] = st + len;
     }
+    if (A.z && lane < A.wpk) {  // lazy: the last reader of the row's masks clears them for the next step
+      const_cast<uint32_t*>(A.mask)[(int64_t)r * A.wpk + lane] = 0u;
+      const_cast<uint32_t*>(A.lmask)[(int64_t)r * A.wpk + lane] = 0u;
+    }
     if (COUNT) {
       int tc = __popc(tmask);
 #pragma unroll
