@@ -84,6 +84,12 @@ struct TablesDev {
   const int32_t* bcount = nullptr;  // per run: insert count
   const int32_t* ids = nullptr;     // bucket contents
   int64_t n_runs = 0;
+  // two-level directory for long keys (DWTA): per (table, top key bits)
+  // prefix p the first run whose prefix is >= p, stored reversed
+  // (coarse[coarse_n - 1 - p]); a lookup binary-searches the prefix's runs
+  const int32_t* coarse = nullptr;
+  int coarse_shift = 0;
+  int64_t coarse_n = 0;
 };
 
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
@@ -97,6 +103,17 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
 
 __device__ __forceinline__ int tables_lookup(const TablesDev& t, uint32_t skey) {
   if (t.empty || ((t.disabled >> (skey >> t.key_bits)) & 1ull)) return -1;
+  if (t.coarse) {
+    const int64_t p = skey >> t.coarse_shift;
+    int lo = t.coarse[t.coarse_n - 1 - p];
+    int hi = p + 1 < t.coarse_n ? t.coarse[t.coarse_n - 2 - p] : (int)t.n_runs;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (t.run_keys[mid] < skey) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo < t.n_runs && t.run_keys[lo] == skey ? lo : -1;
+  }
   if (t.dense_dir) {
     const int r = t.dir[skey];
     if (t.validated && ((uint64_t)(uint32_t)r >= (uint64_t)t.n_runs || t.run_keys[r] != skey)) return -1;
@@ -114,7 +131,7 @@ __device__ __forceinline__ int tables_lookup(const TablesDev& t, uint32_t skey) 
 struct TablesHost {
   TablesDev dev;
   DBuf skeys_a, skeys_b, vals_a, vals_b, uniq, counts, offsets, nruns, dir, hdir, bstart, blen, temp,
-      ovf_cnt, ovf_off, ovf_ev, patch;
+      ovf_cnt, ovf_off, ovf_ev, patch, coarse, ctemp;
   int64_t n_items = 0, n_slots = 0;
   int policy = 0;  // 0 fifo, 1 reservoir
   bool built = false;

@@ -16,32 +16,9 @@ namespace slide {
 
 void TablesHost::release() {
   for (DBuf* b : {&skeys_a, &skeys_b, &vals_a, &vals_b, &uniq, &counts, &offsets, &nruns, &dir, &hdir,
-                  &bstart, &blen, &temp, &ovf_cnt, &ovf_off, &ovf_ev, &patch})
+                  &bstart, &blen, &temp, &ovf_cnt, &ovf_off, &ovf_ev, &patch, &coarse, &ctemp})
     b->release();
   built = false;
-}
-
-// (n, L) row-major keys -> table-major (t << kb | key, id) inserts.  A CTA
-// stages 64 rows x L keys through shared memory so both the row-major reads
-// and the table-major writes are coalesced.
-constexpr int kSortRows = 64;
-
-__global__ void __launch_bounds__(256) sort_input_kernel(const uint32_t* __restrict__ keys, int64_t n, int l, int kb,
-                                                         uint32_t* __restrict__ skeys, int32_t* __restrict__ vals,
-                                                         int id_mul, int id_add) {
-  extern __shared__ uint32_t tile[];  // [kSortRows][l + 1] (padded: conflict-free column reads)
-  for (int64_t r0 = (int64_t)blockIdx.x * kSortRows; r0 < n; r0 += (int64_t)gridDim.x * kSortRows) {
-    const int nr = (int)min((int64_t)kSortRows, n - r0);
-    __syncthreads();
-    for (int q = threadIdx.x; q < nr * l; q += blockDim.x) tile[q + q / l] = keys[r0 * l + q];
-    __syncthreads();
-    for (int q = threadIdx.x; q < nr * l; q += blockDim.x) {
-      const int t = q / nr, i = q - t * nr;
-      const int64_t o = (int64_t)t * n + r0 + i;
-      skeys[o] = ((uint32_t)t << kb) | tile[i * (l + 1) + t];
-      vals[o] = (int32_t)((r0 + i) * id_mul + id_add);
-    }
-  }
 }
 
 __global__ void runs_kernel(const uint32_t* __restrict__ uniq, const int32_t* __restrict__ counts,
@@ -59,7 +36,7 @@ __global__ void runs_kernel(const uint32_t* __restrict__ uniq, const int32_t* __
     uint32_t sk = uniq[r];
     if (dense) {
       dir[sk] = (int32_t)r;
-    } else {
+    } else if (hdir) {
       uint64_t ent = ((uint64_t)sk << 32) | (uint32_t)r;
       uint64_t loc = hash32(sk) & hmask;
       while (true) {
@@ -80,6 +57,7 @@ __global__ void dir_kernel(const uint32_t* __restrict__ uniq, int64_t n_runs, in
       dir[sk] = (int32_t)r;
       continue;
     }
+    if (!hdir) return;  // two-level directory: built from the runs afterwards
     uint64_t ent = ((uint64_t)sk << 32) | (uint32_t)r;
     uint64_t loc = hash32(sk) & hmask;
     while (atomicCAS((unsigned long long*)&hdir[loc], ~0ull, (unsigned long long)ent) != ~0ull)
@@ -124,13 +102,57 @@ __global__ void patch_kernel(const int2* __restrict__ patches, int64_t n, int32_
 // same dense table but never cleared -- a lookup validates the entry against
 // the run's own key (stale entries of earlier builds fail the check), so a
 // build only scatters its runs.  Otherwise an open-addressing hash.
+__global__ void fill_kernel(int32_t* __restrict__ a, int64_t n, int32_t v) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) a[q] = v;
+}
+
+// the two-level directory's prefix marks: run r starts its prefix when the
+// previous run's prefix differs (runs are sorted by (table, key))
+__global__ void coarse_mark_kernel(const uint32_t* __restrict__ uniq, int64_t n_runs, int shift, int64_t n_p,
+                                   int32_t* __restrict__ crev) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_runs; r += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = uniq[r] >> shift;
+    if (r == 0 || (uniq[r - 1] >> shift) != p) crev[n_p - 1 - p] = (int32_t)r;
+  }
+}
+
+static int grid_for(int64_t n, int bs = 256);
+
+// Long keys: the two-level directory (built after the runs, see
+// build_coarse).  A dense (L << key_bits) table of run ids would be one
+// random 4-byte write per run into up to 4 GB (DWTA 24-bit keys at 4M rows:
+// 2.5 ms per build); the coarse table holds ~8 runs per prefix.
+static void build_coarse(TablesHost& tb, TablesDev& d, int l, int kb, int64_t n_runs, const uint32_t* uniq,
+                         cudaStream_t s) {
+  int cb = 1;
+  while (cb < kb && ((int64_t)l << (cb + 3)) < n_runs) ++cb;  // ~8 runs per prefix
+  const int64_t n_p = (int64_t)l << cb;
+  int32_t* crev = tb.coarse.ensure<int32_t>(n_p);
+  fill_kernel<<<grid_for(n_p, 256), 256, 0, s>>>(crev, n_p, (int32_t)n_runs);
+  SLIDE_LAUNCH_CHECK();
+  if (n_runs > 0) {
+    coarse_mark_kernel<<<grid_for(n_runs, 256), 256, 0, s>>>(uniq, n_runs, kb - cb, n_p, crev);
+    SLIDE_LAUNCH_CHECK();
+  }
+  size_t bytes = 0;
+  SLIDE_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, crev, crev, cub::Min(), (int)n_p, s));
+  void* tmp = tb.ctemp.ensure<uint8_t>(bytes);
+  SLIDE_CUDA(cub::DeviceScan::InclusiveScan(tmp, bytes, crev, crev, cub::Min(), (int)n_p, s));  // suffix minimum
+  d.coarse = crev;
+  d.coarse_shift = kb - cb;
+  d.coarse_n = n_p;
+}
+
 static void choose_dir(TablesHost& tb, TablesDev& d, int l, int kb, int64_t n_items, int64_t n_runs, cudaStream_t s) {
+  (void)n_items;
   const uint64_t nd = (uint64_t)l << kb;
-  d.dense_dir = kb <= 16 || (nd <= (1ull << 30) && nd <= 64ull * (uint64_t)std::max<int64_t>(n_items, 1));
-  d.validated = kb > 16;
+  d.dense_dir = kb <= 16;
+  d.validated = 0;
   d.dir = nullptr;
   d.hdir = nullptr;
   d.hash_mask = 0;
+  d.coarse = nullptr;
+  if (kb > 16) return;  // two-level directory, built from the runs (build_coarse)
   if (d.dense_dir) {
     int32_t* dir = tb.dir.ensure<int32_t>(nd);
     if (!d.validated) SLIDE_CUDA(cudaMemsetAsync(dir, 0xff, nd * 4, s));
@@ -144,7 +166,47 @@ static void choose_dir(TablesHost& tb, TablesDev& d, int l, int kb, int64_t n_it
   }
 }
 
-static int grid_for(int64_t n, int bs = 256) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, bs), kSms * 16)); }
+// (n, L) row-major keys -> the inserts (t << kb | key, id) in the same
+// row-major order: a stable sort by (table, key) then yields every bucket's
+// ids ascending, the order they were inserted in (tables.py:127-161) -- no
+// transpose needed.  Four inserts per thread, 16-byte loads.
+template <typename K>
+__global__ void __launch_bounds__(256) composite_keys_kernel(const uint32_t* __restrict__ keys, int64_t total, int l,
+                                                             int kb, K* __restrict__ skeys,
+                                                             int32_t* __restrict__ vals, int id_mul, int id_add) {
+  for (int64_t q0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; q0 < total;
+       q0 += (int64_t)gridDim.x * blockDim.x * 4) {
+    uint32_t k[4];
+    if (q0 + 4 <= total && (q0 & 3) == 0) {
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(keys + q0));
+      k[0] = v.x, k[1] = v.y, k[2] = v.z, k[3] = v.w;
+    } else {
+      for (int j = 0; j < 4; ++j) k[j] = q0 + j < total ? keys[q0 + j] : 0u;
+    }
+    const int64_t r0 = q0 / l;
+    int t = (int)(q0 - r0 * l);
+    int64_t r = r0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (q0 + j < total) {
+        skeys[q0 + j] = (K)(((uint32_t)t << kb) | k[j]);
+        vals[q0 + j] = (int32_t)(r * id_mul + id_add);
+      }
+      if (++t == l) {
+        t = 0;
+        ++r;
+      }
+    }
+  }
+}
+
+__global__ void widen_keys_kernel(const uint16_t* __restrict__ in, const int32_t* __restrict__ n_dev,
+                                  uint32_t* __restrict__ out) {
+  const int n = *n_dev;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) out[q] = in[q];
+}
+
+static int grid_for(int64_t n, int bs) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, bs), kSms * 16)); }
 
 void tables_build(TablesHost& tb, const uint32_t* keys, int64_t n, int l, int kb, int cap, int policy,
                   uint64_t* mt_state, cudaStream_t s, int id_mul, int id_add) {
@@ -161,20 +223,44 @@ void tables_build(TablesHost& tb, const uint32_t* keys, int64_t n, int l, int kb
   int32_t* counts = tb.counts.ensure<int32_t>(total);
   int32_t* offsets = tb.offsets.ensure<int32_t>(total);
   int32_t* nr_d = tb.nruns.ensure<int32_t>(1);
-  if (total > 0) {
-    sort_input_kernel<<<grid_for(ceil_div(n, kSortRows), 1), 256, (size_t)kSortRows * (l + 1) * 4, s>>>(keys, n, l, kb, ska,
-                                                                                               va, id_mul, id_add);
-    SLIDE_LAUNCH_CHECK();
-  }
   const int end_bit = kb + tbits;
-  size_t b1 = 0, b2 = 0, b3 = 0;
-  SLIDE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, ska, skb, va, vb, (int)total, 0, end_bit, s));
-  SLIDE_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, b2, skb, uniq, counts, nr_d, (int)total, s));
-  SLIDE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b3, counts, offsets, (int)total, s));
-  size_t tbytes = std::max(b1, std::max(b2, b3));
-  void* temp = tb.temp.ensure<uint8_t>(tbytes);
-  SLIDE_CUDA(cub::DeviceRadixSort::SortPairs(temp, tbytes, ska, skb, va, vb, (int)total, 0, end_bit, s));
-  SLIDE_CUDA(cub::DeviceRunLengthEncode::Encode(temp, tbytes, skb, uniq, counts, nr_d, (int)total, s));
+  const int cgrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 1024), (int64_t)kSms * 16));
+  size_t tbytes = 0;
+  void* temp = nullptr;
+  if (end_bit <= 16) {
+    // short keys (SimHash): 16-bit (table, key) keys -- a quarter less
+    // traffic in each radix pass and in the run-length encode
+    uint16_t* ska16 = reinterpret_cast<uint16_t*>(ska);
+    uint16_t* skb16 = reinterpret_cast<uint16_t*>(skb);
+    uint16_t* uniq16 = reinterpret_cast<uint16_t*>(offsets);  // scratch until the runs are counted
+    if (total > 0) {
+      composite_keys_kernel<uint16_t><<<cgrid, 256, 0, s>>>(keys, total, l, kb, ska16, va, id_mul, id_add);
+      SLIDE_LAUNCH_CHECK();
+    }
+    size_t b1 = 0, b2 = 0, b3 = 0;
+    SLIDE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, ska16, skb16, va, vb, (int)total, 0, end_bit, s));
+    SLIDE_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, b2, skb16, uniq16, counts, nr_d, (int)total, s));
+    SLIDE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b3, counts, offsets, (int)total, s));
+    tbytes = std::max(b1, std::max(b2, b3));
+    temp = tb.temp.ensure<uint8_t>(tbytes);
+    SLIDE_CUDA(cub::DeviceRadixSort::SortPairs(temp, tbytes, ska16, skb16, va, vb, (int)total, 0, end_bit, s));
+    SLIDE_CUDA(cub::DeviceRunLengthEncode::Encode(temp, tbytes, skb16, uniq16, counts, nr_d, (int)total, s));
+    widen_keys_kernel<<<grid_for(std::min<int64_t>(total, (int64_t)1 << end_bit)), 256, 0, s>>>(uniq16, nr_d, uniq);
+    SLIDE_LAUNCH_CHECK();
+  } else {
+    if (total > 0) {
+      composite_keys_kernel<uint32_t><<<cgrid, 256, 0, s>>>(keys, total, l, kb, ska, va, id_mul, id_add);
+      SLIDE_LAUNCH_CHECK();
+    }
+    size_t b1 = 0, b2 = 0, b3 = 0;
+    SLIDE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, ska, skb, va, vb, (int)total, 0, end_bit, s));
+    SLIDE_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, b2, skb, uniq, counts, nr_d, (int)total, s));
+    SLIDE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b3, counts, offsets, (int)total, s));
+    tbytes = std::max(b1, std::max(b2, b3));
+    temp = tb.temp.ensure<uint8_t>(tbytes);
+    SLIDE_CUDA(cub::DeviceRadixSort::SortPairs(temp, tbytes, ska, skb, va, vb, (int)total, 0, end_bit, s));
+    SLIDE_CUDA(cub::DeviceRunLengthEncode::Encode(temp, tbytes, skb, uniq, counts, nr_d, (int)total, s));
+  }
   int32_t n_runs = 0;
   SLIDE_CUDA(cudaMemcpyAsync(&n_runs, nr_d, 4, cudaMemcpyDeviceToHost, s));
   SLIDE_CUDA(cudaStreamSynchronize(s));
@@ -198,6 +284,7 @@ void tables_build(TablesHost& tb, const uint32_t* keys, int64_t n, int l, int kb
                                                  dir, hdir, hmask, bstart, blen, ovf);
     SLIDE_LAUNCH_CHECK();
   }
+  if (kb > 16) build_coarse(tb, d, l, kb, n_runs, uniq, s);
   if (policy == 1 && n_runs > 0 && id_mul == 1) {
     // reservoir: host replay of the overflowing inserts (tables.py:156-161)
     int32_t* ovf_off = tb.ovf_off.ensure<int32_t>(n_runs);
@@ -291,10 +378,11 @@ void tables_load(TablesHost& tb, const uint32_t* skeys, const int32_t* counts, c
   choose_dir(tb, d, l, kb, n_items, n_runs, s);
   d.run_keys = uniq;
   if (n_runs) {
-    dir_kernel<<<grid_for(n_runs), 256, 0, s>>>(uniq, n_runs, d.dense_dir, tb.dir.as<int32_t>(), tb.hdir.as<uint64_t>(),
-                                                d.hash_mask);
+    dir_kernel<<<grid_for(n_runs), 256, 0, s>>>(uniq, n_runs, d.dense_dir, const_cast<int32_t*>(d.dir),
+                                                const_cast<uint64_t*>(d.hdir), d.hash_mask);
     SLIDE_LAUNCH_CHECK();
   }
+  if (kb > 16) build_coarse(tb, d, l, kb, n_runs, uniq, s);
   SLIDE_CUDA(cudaStreamSynchronize(s));  // host arrays may go away
   d.bstart = bstart;
   d.blen = blen;
