@@ -206,13 +206,16 @@ __global__ void __launch_bounds__(256) dwta_kernel(DwtaDev f, const float* __res
 // tie / nonzero rules and the same donor densification as dwta_kernel.
 constexpr int kDwRows = 16;
 constexpr int kDwMaxM = 16;
+// the transposed tile's row stride: 20 floats (16-byte aligned quads, and the
+// transposing stores of consecutive columns hit 8 banks instead of 2)
+constexpr int kDwLd = kDwRows + 4;
 
 __global__ void __launch_bounds__(256) dwta_rows_kernel(DwtaDev f, const float* __restrict__ x, int64_t n, int ld,
                                                         uint32_t* __restrict__ keys) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int KL = f.k * f.l;
-  float* xs = reinterpret_cast<float*>(sm);  // [dim][kDwRows]
-  int16_t* perm = reinterpret_cast<int16_t*>(xs + kDwRows * f.dim);
+  float* xs = reinterpret_cast<float*>(sm);  // [dim][kDwLd]
+  int16_t* perm = reinterpret_cast<int16_t*>(xs + kDwLd * f.dim);
   uint8_t* codes = reinterpret_cast<uint8_t*>(perm + ((f.n_perms * f.dim + 7) & ~7));
   uint8_t* occ = codes + kDwRows * KL;
   for (int q = threadIdx.x; q < f.n_perms * f.dim; q += blockDim.x) perm[q] = f.perms[q];
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(256) dwta_rows_kernel(DwtaDev f, const float* 
     __syncthreads();
     for (int q = threadIdx.x; q < kDwRows * f.dim; q += blockDim.x) {
       const int r = q / f.dim, c = q - r * f.dim;
-      xs[c * kDwRows + r] = r < nr ? x[(row0 + r) * ld + c] : 0.f;
+      xs[c * kDwLd + r] = r < nr ? x[(row0 + r) * ld + c] : 0.f;
     }
     __syncthreads();
     for (int g = threadIdx.x; g < KL; g += blockDim.x) {
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(256) dwta_rows_kernel(DwtaDev f, const float* 
 #pragma unroll
         for (int o = 0; o < kDwMaxM; ++o) {
           if (o >= cnt) break;
-          const float4 v4 = *reinterpret_cast<const float4*>(xs + idx[o] * kDwRows + r4 * 4);
+          const float4 v4 = *reinterpret_cast<const float4*>(xs + idx[o] * kDwLd + r4 * 4);
           const float v[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -298,7 +301,7 @@ void launch_dwta_keys(const DwtaDev& f, const float* x, int64_t n, int ld, uint3
     return;
   }
   const int KL = f.k * f.l;
-  const size_t smem = (size_t)kDwRows * f.dim * 4 + (size_t)((f.n_perms * f.dim + 7) & ~7) * 2 + (size_t)2 * kDwRows * KL;
+  const size_t smem = (size_t)kDwLd * f.dim * 4 + (size_t)((f.n_perms * f.dim + 7) & ~7) * 2 + (size_t)2 * kDwRows * KL;
   if (f.m > kDwMaxM || smem > 227 * 1024) {
     launch_dwta_t<8>(f, x, n, ld, keys, s);
     return;
