@@ -20,9 +20,23 @@ import torch.multiprocessing as mp  # noqa: E402
 D, H, N, B = 300, 128, 997, 16
 
 
+def _shape(family):
+    if family == "tiny":  # BASELINE configs[0]: 10,000 -> 128 -> 5,000, B = 128
+        from paper_1903_03129_b200.configs import TINY
+
+        return TINY.input_dim, TINY.hidden, TINY.n_out, TINY.batch
+    return D, H, N, B
+
+
 def _setup(family):
     from paper_1903_03129_b200 import LshLayerConfig, SamplerConfig, TrainConfig
 
+    if family == "tiny":
+        from paper_1903_03129_b200.configs import TINY as w
+
+        cfg = TrainConfig(batch_size=w.batch, seed=0, learning_rate=w.lr, n0=2)
+        return cfg, LshLayerConfig(w.family, k=w.k, l=w.l, capacity=w.cap, policy=w.policy,
+                                   sampler=SamplerConfig(w.strategy, beta=w.beta))
     cfg = TrainConfig(batch_size=B, seed=5, learning_rate=1e-2, n0=2)
     if family == "simhash":
         spec = LshLayerConfig("simhash", k=4, l=8, capacity=16, sampler=SamplerConfig("vanilla", beta=40))
@@ -32,14 +46,21 @@ def _setup(family):
     return cfg, spec
 
 
-def _csrs():
+def _csrs(family="simhash"):
     from paper_1903_03129_b200.data import CorpusSpec, synthetic_corpus
     from paper_1903_03129_b200.network import HostCsr
 
-    corpus = synthetic_corpus(CorpusSpec(D, N, ("uniform", 3, 20), 1.1, ("uniform", 1, 4), 1.1, True), 3 * B, seed=9)
+    if family == "tiny":
+        from paper_1903_03129_b200.configs import TINY
+
+        bs = TINY.batch
+        corpus = synthetic_corpus(TINY.corpus, 3 * bs, seed=9)
+    else:
+        bs = B
+        corpus = synthetic_corpus(CorpusSpec(D, N, ("uniform", 3, 20), 1.1, ("uniform", 1, 4), 1.1, True), 3 * B, seed=9)
     out = []
     for s in range(3):
-        sub = corpus.subset(np.arange(s * B, (s + 1) * B))
+        sub = corpus.subset(np.arange(s * bs, (s + 1) * bs))
         out.append(HostCsr(sub.x_ptr.astype(np.int32), sub.x_idx, sub.x_val, sub.y_ptr.astype(np.int32), sub.y_idx))
     return out
 
@@ -52,14 +73,15 @@ def _worker(rank, world, port, family, q):
         from paper_1903_03129_b200 import SlideNetwork, sharded
 
         cfg, spec = _setup(family)
-        net = SlideNetwork(D, [H, N], cfg, lsh_layers={1: spec}, shard=(rank, world))
+        d, h, n, _ = _shape(family)
+        net = SlideNetwork(d, [h, n], cfg, lsh_layers={1: spec}, shard=(rank, world))
         losses, fracs = [], []
-        for it, csr in enumerate(_csrs(), start=1):
+        for it, csr in enumerate(_csrs(family), start=1):
             st = net.train_batch_csr(csr, it, schedule="snapshot")
             losses.append(st.loss)
             fracs.append(st.active_fraction[1])
-        w2 = sharded.all_gather_rows(net.w2.cpu(), N).numpy()
-        v2 = sharded.all_gather_rows(net.v2.cpu(), N).numpy()
+        w2 = sharded.all_gather_rows(net.w2.cpu(), n).numpy()
+        v2 = sharded.all_gather_rows(net.v2.cpu(), n).numpy()
         w1 = sharded.all_gather_units(net.w1t.cpu()).numpy()
         q.put((rank, losses, fracs, w1, w2, v2))
     except BaseException as e:  # surface a rank's failure instead of hanging the parent
@@ -69,15 +91,16 @@ def _worker(rank, world, port, family, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("family,world", [("simhash", 2), ("simhash", 4), ("dwta", 2)])
+@pytest.mark.parametrize("family,world", [("simhash", 2), ("simhash", 4), ("dwta", 2), ("tiny", 2)])
 def test_shards_match_one_gpu(family, world):
     from paper_1903_03129_b200 import SlideNetwork
 
     cfg, spec = _setup(family)
-    ref = SlideNetwork(D, [H, N], cfg, lsh_layers={1: spec})
+    d, h, n, _ = _shape(family)
+    ref = SlideNetwork(d, [h, n], cfg, lsh_layers={1: spec})
     ref.use_graphs = False
     want_l, want_f = [], []
-    for it, csr in enumerate(_csrs(), start=1):
+    for it, csr in enumerate(_csrs(family), start=1):
         st = ref.train_batch_csr(csr, it, schedule="snapshot")
         want_l.append(st.loss)
         want_f.append(st.active_fraction[1])
@@ -101,5 +124,5 @@ def test_shards_match_one_gpu(family, world):
     for rank, losses, fracs, w1t, w2, v2 in res:
         np.testing.assert_allclose(losses, want_l, rtol=1e-5)
         np.testing.assert_allclose(fracs, want_f, rtol=0, atol=0)  # identical active sets
-        np.testing.assert_allclose(w1t, w1_ref[:, :H], rtol=1e-4, atol=1e-6)
+        np.testing.assert_allclose(w1t, w1_ref[:, :h], rtol=1e-4, atol=1e-6)
         np.testing.assert_allclose(w2, w2_ref[:, : w2.shape[1]], rtol=1e-4, atol=1e-6)
