@@ -282,6 +282,175 @@ __global__ void __launch_bounds__(256) dwta_rows_kernel(DwtaDev f, const float* 
   }
 }
 
+// Rebuild path, lanes = rows.  A tile of 64 rows sits transposed in shared
+// memory ([dim + 1][66], zeros stored as -inf so "only nonzeros take part,
+// the first of equal values wins" is one strict compare per element; the
+// extra row is all -inf and pads ragged / short bins).  Lane l holds rows 2l
+// and 2l + 1: a bin position is ONE conflict-free 8-byte load per lane whose
+// address is uniform across the warp up to the lane offset, so the shared-
+// memory pipe moves exactly the 2 x 4 bytes per (row, position) the bin
+// needs (the bin-per-thread form gathers 16-byte quads at random dims: ~2.4
+// bank conflicts per load).  A warp walks whole tables: the K codes of a key
+// are packed in registers and stored straight to the key array.  The codes
+// (bit 7 = empty bin) are also kept per tile; only a tile that saw an empty
+// bin runs the donor densification (hashing.py:219-231) and rewrites its
+// keys from them -- dense weight rows never do.
+constexpr int kDtRows = 64;            // rows per tile (2 per lane)
+constexpr int kDtLd = kDtRows + 2;     // transposed row stride (8-byte aligned, 2-way store conflicts)
+constexpr int kDtWarps = 8;
+
+__host__ __device__ inline size_t dt_xs_bytes(int dim) { return ((size_t)(dim + 1) * kDtLd * 4 + 15) & ~(size_t)15; }
+
+// Largest of MM values and its position, ties to the lowest position: a
+// binary tournament (strict > keeps the left entry), MM - 1 compares instead
+// of a chain of MM -- the compare / select work runs on the half-rate ALU
+// pipe, which bounds this kernel.
+template <int MM>
+__device__ __forceinline__ void dt_winner(const float (&v)[MM], float& best, int& code) {
+  float bv[MM / 2];
+  int bc[MM / 2];
+#pragma unroll
+  for (int i = 0; i < MM / 2; ++i) {
+    const bool t = v[2 * i + 1] > v[2 * i];
+    bv[i] = t ? v[2 * i + 1] : v[2 * i];
+    bc[i] = t ? 2 * i + 1 : 2 * i;
+  }
+#pragma unroll
+  for (int n = MM / 2; n > 1; n >>= 1) {
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const bool t = bv[2 * i + 1] > bv[2 * i];
+      bv[i] = t ? bv[2 * i + 1] : bv[2 * i];
+      bc[i] = t ? bc[2 * i + 1] : bc[2 * i];
+    }
+  }
+  best = bv[0];
+  code = bc[0];
+}
+
+template <int MM>
+__global__ void __launch_bounds__(kDtWarps * 32) dwta_tile_kernel(DwtaDev f, const float* __restrict__ x, int64_t n,
+                                                                   int ld, uint32_t* __restrict__ keys) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int KL = f.k * f.l;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* xs = reinterpret_cast<float*>(sm);                                    // [dim + 1][kDtLd]
+  uint32_t* offs = reinterpret_cast<uint32_t*>(sm + dt_xs_bytes(f.dim));       // [KL][MM] byte offsets into xs
+  uint8_t* codes = reinterpret_cast<uint8_t*>(offs + (size_t)KL * MM);         // [KL][kDtRows]
+  const float ninf = __int_as_float(0xff800000);
+  // every bin's positions as byte offsets of their transposed rows; positions
+  // past the bin's end point at the -inf row
+  for (int q = threadIdx.x; q < KL * MM; q += blockDim.x) {
+    const int g = q / MM, o = q - g * MM;
+    const int pq = g / f.bins_per_perm, b = g - pq * f.bins_per_perm;
+    const int lo = b * f.m, cnt = min(f.m, f.dim - lo);
+    const int dimi = o < cnt ? (int)f.perms[pq * f.dim + lo + o] : f.dim;
+    offs[q] = (uint32_t)dimi * (kDtLd * 4);
+  }
+  for (int q = threadIdx.x; q < kDtLd; q += blockDim.x) xs[f.dim * kDtLd + q] = ninf;
+  const int d4 = f.dim >> 2;  // float4s per row (dim % 4 == 0, checked by the launcher)
+  const char* xl = reinterpret_cast<const char*>(xs) + lane * 8;
+  const int64_t n_tiles = (n + kDtRows - 1) / kDtRows;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t row0 = tile * kDtRows;
+    const int nr = (int)(n - row0 < kDtRows ? n - row0 : kDtRows);
+    __syncthreads();  // the previous tile's readers are done
+    // coalesced 16-byte loads (8 lanes along a row, 4 rows per warp access),
+    // transposed 4-byte stores
+    for (int u = threadIdx.x; u < kDtRows * d4; u += blockDim.x) {
+      const int c_lo = u & 7, r_lo = (u >> 3) & 3, rest = u >> 5;
+      const int c_hi = rest % (d4 >> 3), r_hi = rest / (d4 >> 3);
+      const int c4 = c_hi * 8 + c_lo, r = r_hi * 4 + r_lo;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < nr) v = __ldcs(reinterpret_cast<const float4*>(x + (row0 + r) * ld) + c4);
+      const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        xs[(c4 * 4 + j) * kDtLd + r] = (f.dense_mode || e[j] != 0.f) ? e[j] : ninf;
+    }
+    __syncthreads();
+    int any_empty = 0;
+    for (int t = warp; t < f.l; t += kDtWarps) {
+      uint32_t key0 = 0, key1 = 0;
+      for (int kk = 0; kk < f.k; ++kk) {
+        const int g = t * f.k + kk;
+        uint32_t po[MM];
+#pragma unroll
+        for (int o4 = 0; o4 < MM / 4; ++o4) {
+          const uint4 p4 = *reinterpret_cast<const uint4*>(offs + (size_t)g * MM + o4 * 4);
+          po[o4 * 4 + 0] = p4.x, po[o4 * 4 + 1] = p4.y, po[o4 * 4 + 2] = p4.z, po[o4 * 4 + 3] = p4.w;
+        }
+        float2 v[MM];
+#pragma unroll
+        for (int o = 0; o < MM; ++o) v[o] = *reinterpret_cast<const float2*>(xl + po[o]);
+        float vx[MM], vy[MM];
+#pragma unroll
+        for (int o = 0; o < MM; ++o) vx[o] = v[o].x, vy[o] = v[o].y;
+        float b0, b1;
+        int c0, c1;
+        dt_winner<MM>(vx, b0, c0);
+        dt_winner<MM>(vy, b1, c1);
+        const bool e0 = b0 == ninf, e1 = b1 == ninf;
+        any_empty |= ((e0 && lane * 2 < nr) || (e1 && lane * 2 + 1 < nr)) ? 1 : 0;  // (rows past the end are all -inf)
+        *reinterpret_cast<uint16_t*>(codes + (size_t)g * kDtRows + lane * 2) =
+            (uint16_t)((e0 ? 0x80 : c0) | ((e1 ? 0x80 : c1) << 8));
+        key0 |= (uint32_t)c0 << (f.bits * kk);
+        key1 |= (uint32_t)c1 << (f.bits * kk);
+      }
+      const int r = lane * 2;
+      if (r < nr) keys[(row0 + r) * f.l + t] = key0;
+      if (r + 1 < nr) keys[(row0 + r + 1) * f.l + t] = key1;
+    }
+    if (!__syncthreads_or(any_empty)) continue;
+    // densification: empty bins copy their first occupied donor's code (flag kept
+    // so that a filled bin is never taken for an occupied donor)
+    for (int q = threadIdx.x; q < KL * kDtRows; q += blockDim.x) {
+      const int g = q / kDtRows, r = q - g * kDtRows;
+      if (r >= nr || !(codes[q] & 0x80)) continue;
+      int code = 0;
+      for (int a = 0; a < 100; ++a) {
+        const int d = f.donors[g * 100 + a];
+        const uint8_t cd = codes[d * kDtRows + r];
+        if (!(cd & 0x80)) {
+          code = cd;
+          break;
+        }
+      }
+      codes[q] = (uint8_t)(0x80 | code);
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nr * f.l; q += blockDim.x) {
+      const int r = q / f.l, t = q - r * f.l;
+      uint32_t key = 0;
+      for (int kk = 0; kk < f.k; ++kk)
+        key |= (uint32_t)(codes[(size_t)(t * f.k + kk) * kDtRows + r] & 0x7f) << (f.bits * kk);
+      keys[(row0 + r) * f.l + t] = key;
+    }
+  }
+}
+
+template <int MM>
+static bool launch_dwta_tile_t(const DwtaDev& f, const float* x, int64_t n, int ld, uint32_t* keys, cudaStream_t s) {
+  const int KL = f.k * f.l;
+  const size_t smem = dt_xs_bytes(f.dim) + (size_t)KL * MM * 4 + (size_t)KL * kDtRows;
+  if (smem > 227 * 1024) return false;
+  SLIDE_CUDA(cudaFuncSetAttribute(dwta_tile_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 1;
+  SLIDE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dwta_tile_kernel<MM>, kDtWarps * 32, smem));
+  const int grid = (int)std::min<int64_t>(ceil_div(n, kDtRows), (int64_t)kSms * std::max(per_sm, 1));
+  dwta_tile_kernel<MM><<<grid, kDtWarps * 32, smem, s>>>(f, x, n, ld, keys);
+  SLIDE_LAUNCH_CHECK();
+  return true;
+}
+
+// false when the shape does not fit (the callers fall back)
+static bool launch_dwta_tile(const DwtaDev& f, const float* x, int64_t n, int ld, uint32_t* keys, cudaStream_t s) {
+  if (f.dim % 32 || ld % 4 || (reinterpret_cast<uintptr_t>(x) & 15) || f.m > 16 || f.m < 1) return false;
+  if (f.m <= 4) return launch_dwta_tile_t<4>(f, x, n, ld, keys, s);
+  if (f.m <= 8) return launch_dwta_tile_t<8>(f, x, n, ld, keys, s);
+  return launch_dwta_tile_t<16>(f, x, n, ld, keys, s);
+}
+
 template <int ROWS>
 static void launch_dwta_t(const DwtaDev& f, const float* x, int64_t n, int ld, uint32_t* keys, cudaStream_t s) {
   const int KL = f.k * f.l;
@@ -300,6 +469,8 @@ void launch_dwta_keys(const DwtaDev& f, const float* x, int64_t n, int ld, uint3
     launch_dwta_t<1>(f, x, n, ld, keys, s);
     return;
   }
+  static const bool old_rows = getenv("SLIDE_DWTA_OLD") != nullptr;  // A/B timing only
+  if (!old_rows && launch_dwta_tile(f, x, n, ld, keys, s)) return;
   const int KL = f.k * f.l;
   const size_t smem = (size_t)kDwLd * f.dim * 4 + (size_t)((f.n_perms * f.dim + 7) & ~7) * 2 + (size_t)2 * kDwRows * KL;
   if (f.m > kDwMaxM || smem > 227 * 1024) {

@@ -497,12 +497,23 @@ def test_batched_query_union_equals_per_query_probes(family):
         np.testing.assert_array_equal(got[i], want)
 
 
-@pytest.mark.parametrize("name", ["dw_main", "dw_scaled"])
+REBUILD_SPECS = {
+    "dw_main": HASH_SPECS["dw_main"],
+    "dw_scaled": HASH_SPECS["dw_scaled"],
+    # 4- and 16-wide bins, a ragged last bin (96 = 19 x 5 + 1)
+    "dw_m4": dict(family="dwta", k_per_table=6, num_tables=20, dim=64, wta_bin_size=4, seed=3),
+    "dw_m16": dict(family="dwta", k_per_table=4, num_tables=30, dim=128, wta_bin_size=16, seed=4),
+    "dw_ragged96": dict(family="dwta", k_per_table=5, num_tables=12, dim=96, wta_bin_size=5, seed=6),
+}
+
+
+@pytest.mark.parametrize("name", list(REBUILD_SPECS))
 def test_dwta_rebuild_path_matches_oracle(name):
-    """> 148 x 8 rows take the 16-row transposed rebuild kernel: keys equal
-    the oracle's, including sparse rows whose empty bins borrow donor codes
-    and rows with ties."""
-    spec = HASH_SPECS[name]
+    """> 148 x 8 rows take the tiled rebuild kernel (64 rows per tile, lanes =
+    rows): keys equal the oracle's, including sparse rows whose empty bins
+    borrow donor codes (the tile's densification pass), rows with ties, and a
+    partial last tile."""
+    spec = REBUILD_SPECS[name]
     fam = new_hash_family(HashFamilyConfig(**spec))
     rng = np.random.default_rng(12)
     n, d = 5000, spec["dim"]
@@ -512,6 +523,17 @@ def test_dwta_rebuild_path_matches_oracle(name):
     w = w.astype(np.float64)
     params = O.dwta_params(d, spec["k_per_table"], spec["num_tables"], spec["wta_bin_size"], spec["seed"])
     np.testing.assert_array_equal(fam.hash_batch(w), O.dwta_keys(params, w))
+
+
+def test_wta_rebuild_path_equals_dwta_on_dense_rows():
+    """The tiled kernel in WTA mode (zeros take part): on rows without zeros
+    WTA and DWTA agree (hashing.py:262-274)."""
+    rng = np.random.default_rng(5)
+    w = rng.standard_normal((3000, 128)).astype(np.float32).astype(np.float64)
+    w[w == 0] = 1.0
+    wta = new_hash_family(HashFamilyConfig("wta", 8, 10, 128, wta_bin_size=8, seed=8))
+    dwta = new_hash_family(HashFamilyConfig("dwta", 8, 10, 128, wta_bin_size=8, seed=8))
+    np.testing.assert_array_equal(wta.hash_batch(w), dwta.hash_batch(w))
 
 
 def test_pipelined_batches_equal_per_call_steps():
