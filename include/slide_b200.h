@@ -107,6 +107,16 @@ int slide_dwta_keys(const float* x, int64_t n, int64_t ld, int64_t dim, int64_t 
 /* hash the ctx's W2 rows and rebuild all L tables; mt_state: host 625 words
  * of random.Random(table_seed).getstate()[1], updated in place (reservoir) */
 int slide_rebuild_tables(slide_ctx* ctx, uint64_t* mt_state);
+/* Renumber the hidden units in place: new unit p takes the state of old unit
+ * src[p] (host, a permutation of [0, hidden)) -- the columns of W1^T / W2 and
+ * their Adam moments, the hidden biases, moments and step counters, and the
+ * input indices of the ctx's hash functions move together, so the net computes
+ * the same function; callers map their own unit order through the
+ * permutation.  A layout operation with no reference counterpart: it keeps
+ * the units that are live (nonzero somewhere in a batch) adjacent so the row
+ * kernels' gathers of W[row, live units] (network.py:266,322-332) are
+ * contiguous.  Unsharded contexts only. */
+int slide_relabel_units(slide_ctx* ctx, const int32_t* src);
 /* build from precomputed keys (dev (n, L) uint32) */
 int slide_build_tables_from_keys(slide_ctx* ctx, const uint32_t* keys, int64_t n, uint64_t* mt_state);
 /* clear every bucket (LshTables._clear, tables.py:123-125) */

@@ -54,6 +54,7 @@ _SIGS = {
     "slide_simhash_keys": [vp, i64, i64, i64, i64, i64, i64, vp, vp, vp],
     "slide_dwta_keys": [vp, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp],
     "slide_rebuild_tables": [vp, vp],
+    "slide_relabel_units": [vp, vp],
     "slide_build_tables_from_keys": [vp, vp, i64, vp],
     "slide_clear_tables": [vp],
     "slide_tables_info": [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)],

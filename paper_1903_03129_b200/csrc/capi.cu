@@ -151,7 +151,7 @@ struct slide_ctx {
   DBuf bias_table;
   int64_t bias_n = 0;
   int bias_exact = 1;
-  DBuf xslot, tc, bc, partial, tc_scratch, long_list, n_long, work, topk_out, topk_cnt;
+  DBuf xslot, tc, bc, partial, tc_scratch, long_list, n_long, work, topk_out, topk_cnt, relabel, sel_big;
   int64_t fb_bitmap_words = 0;
   double* pinned_loss = nullptr;
   int32_t* pinned_cnt = nullptr;
@@ -344,7 +344,7 @@ int slide_destroy(slide_ctx* c) {
     for (DBuf* b : {&c->sh_packed, &c->sh_packed_t, &c->dw_perms, &c->dw_donors, &c->rowkeys, &c->h, &c->dsort, &c->hmask, &c->live, &c->live_ticket, &c->qkeys, &c->order,
                     &c->states, &c->act, &c->cnt, &c->empty, &c->offs, &c->prow, &c->pslot, &c->plab, &c->z,
                     &c->prob, &c->delta, &c->loss, &c->dh, &c->fb_ids, &c->fb_scratch, &c->fb_bitmap, &c->xslot,
-                    &c->tc, &c->bc, &c->counters, &c->partial, &c->long_list, &c->n_long, &c->work, &c->topk_out, &c->topk_cnt, &c->tc_scratch, &c->bias_table, &c->cnt_all, &c->prob_tmp, &c->shard_pack, &c->fb_rng, &c->sm_part, &c->sm_stat})
+                    &c->tc, &c->bc, &c->counters, &c->partial, &c->relabel, &c->sel_big, &c->long_list, &c->n_long, &c->work, &c->topk_out, &c->topk_cnt, &c->tc_scratch, &c->bias_table, &c->cnt_all, &c->prob_tmp, &c->shard_pack, &c->fb_rng, &c->sm_part, &c->sm_stat})
       b->release();
     c->grow.release();
     c->gfeat.release();
@@ -430,6 +430,99 @@ int slide_rebuild_tables(slide_ctx* c, uint64_t* mt_state) {
     build_from_keys(c, keys, n, mt_state);
     c->timer.mark(c->s, kStRebuildBuild);
     c->host_counts[3] += 1;
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------- unit relabel
+// Physical hidden-unit order (ref: none -- a layout choice below the API).
+// After the first steps only ~30 of the hidden units are nonzero anywhere in
+// a batch, scattered over the hidden width, so every row kernel's gathers of
+// W[row, live units] pull one 32-byte sector per 4-byte value.  Renumbering
+// the units so that the live ones are adjacent makes those gathers
+// contiguous.  The renumbering is a consistent relabelling of the whole net:
+// the columns of W1^T / W2 and their moments, the hidden bias state and step
+// counters, and the hash functions' input indices all move together, so
+// every kernel runs unchanged; the host views map back to the caller's order.
+__global__ void __launch_bounds__(256) relabel_cols_kernel(float* __restrict__ a, int64_t rows, int ld, int hn,
+                                                           const int32_t* __restrict__ src) {
+  extern __shared__ float rl_row[];  // [8][hn]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float* buf = rl_row + (size_t)w * hn;
+  for (int64_t r = (int64_t)blockIdx.x * 8 + w; r < rows; r += (int64_t)gridDim.x * 8) {
+    float* row = a + r * ld;
+    for (int p = lane; p < hn; p += 32) buf[p] = row[p];
+    __syncwarp();
+    for (int p = lane; p < hn; p += 32) row[p] = buf[__ldg(src + p)];
+    __syncwarp();
+  }
+}
+
+template <typename T>
+__global__ void relabel_vec_kernel(T* __restrict__ a, int hn, const int32_t* __restrict__ src) {
+  extern __shared__ unsigned char rl_vec[];
+  T* buf = reinterpret_cast<T*>(rl_vec);
+  for (int p = threadIdx.x; p < hn; p += blockDim.x) buf[p] = a[p];
+  __syncthreads();
+  for (int p = threadIdx.x; p < hn; p += blockDim.x) a[p] = buf[src[p]];
+}
+
+// hash parameters: dimension indices (low 15 bits; bit 15 = a SimHash sign)
+__global__ void relabel_index_kernel(uint16_t* __restrict__ a, int64_t n, const int32_t* __restrict__ inv) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const uint16_t e = a[q];
+    a[q] = (uint16_t)((e & 0x8000u) | (uint16_t)inv[e & 0x7fffu]);
+  }
+}
+
+extern "C" {
+
+int slide_relabel_units(slide_ctx* c, const int32_t* src_host) {
+  return guarded([&] {
+    SLIDE_CHECK(c->G == 1, kNotSupported, "a sharded hidden layer keeps its unit order");
+    const slide_net_desc& d = c->d;
+    const int hn = (int)d.hidden, hp = c->hp;
+    std::vector<int32_t> both((size_t)2 * hn, -1);
+    for (int p = 0; p < hn; ++p) {
+      const int32_t o = src_host[p];
+      SLIDE_CHECK(o >= 0 && o < hn && both[hn + o] < 0, kValueError, "src must be a permutation of the hidden units");
+      both[p] = o;
+      both[hn + o] = p;
+    }
+    cudaStream_t s = c->s;
+    int32_t* dev = c->relabel.ensure<int32_t>((size_t)2 * hn);
+    SLIDE_CUDA(cudaMemcpyAsync(dev, both.data(), both.size() * 4, cudaMemcpyHostToDevice, s));
+    const int32_t *src = dev, *inv = dev + hn;
+    const size_t smem = (size_t)8 * hn * 4;
+    SLIDE_CHECK(smem <= 200 * 1024, kNotSupported, "hidden layer too wide to relabel");
+    if (smem > 48 * 1024)
+      SLIDE_CUDA(cudaFuncSetAttribute(relabel_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto cols = [&](float* a, int64_t rows) {
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 8), (int64_t)kSms * 8));
+      relabel_cols_kernel<<<grid, 256, smem, s>>>(a, rows, hp, hn, src);
+      SLIDE_LAUNCH_CHECK();
+    };
+    for (float* a : {d.w1t, d.m1t, d.v1t}) cols(a, d.input_dim);
+    for (float* a : {d.w2, d.m2, d.v2}) cols(a, c->n_local);
+    for (float* a : {d.b1, d.mb1, d.vb1}) {
+      relabel_vec_kernel<float><<<1, 256, (size_t)hn * 4, s>>>(a, hn, src);
+      SLIDE_LAUNCH_CHECK();
+    }
+    relabel_vec_kernel<int64_t><<<1, 256, (size_t)hn * 8, s>>>(d.steps1, hn, src);
+    SLIDE_LAUNCH_CHECK();
+    auto index = [&](DBuf& b, int64_t n) {
+      if (!b.p || n <= 0) return;
+      relabel_index_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 1024), 256, 0, s>>>(b.as<uint16_t>(), n, inv);
+      SLIDE_LAUNCH_CHECK();
+    };
+    if (d.family == 1) {
+      index(c->sh_packed, d.k * d.l * d.sh_c);
+      index(c->sh_packed_t, d.k * d.l * d.sh_c);
+    } else if (d.family >= 2) {
+      index(c->dw_perms, d.n_perms * d.hidden);
+    }
+    SLIDE_CUDA(cudaStreamSynchronize(s));  // `both` is read by the copy
   });
 }
 
@@ -785,7 +878,13 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     a.cand_ctr = c->timer.on && c->shard_phase != 1 ? c->counters.as<unsigned long long>() + 4 : nullptr;
     a.hist_out = c->shard_phase == 1 ? c->shard_hist : nullptr;
     a.ghist = c->shard_phase == 2 ? c->shard_ghist : nullptr;
-    if (!(full_union && launch_select_union(a, d.n_out, s))) launch_select(a, (int)(lcap + max_labels), s);
+    if (!(full_union && launch_select_union(a, d.n_out, s))) {
+      // candidates a sample is likely to gather: L probes of mean-sized buckets
+      const int64_t runs = std::max<int64_t>(c->tab.dev.n_runs, 1);
+      const int64_t mean_bucket = std::min<int64_t>(d.capacity, ceil_div(c->tab.n_items * d.l, runs));
+      launch_select(a, (int)(lcap + max_labels), s, 2 * d.l * mean_bucket + max_labels,
+                    c->sel_big.ensure<int32_t>(b));
+    }
     c->timer.mark(s, kStSelect);
     if (c->shard_phase == 1) return;  // the caller all-reduces the counts
     // fallback for slots whose sampler returned nothing
@@ -1017,7 +1116,7 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
       launch_adam_features(hp, ap, gf.n_uniq.as<int32_t>(), gf.u_max, gf.uniq.as<int32_t>(), gf.seg_off.as<int32_t>(),
                            gf.seg_cnt.as<int32_t>(), gf.order.as<int32_t>(), xs, c->last_xval, c->last_xbase,
                            c->h.as<float>(), dh, bc, c->live.as<int32_t>(), d.w1t, d.m1t, d.v1t,
-                           ctr ? ctr + 1 : nullptr, gf.long_list.as<int32_t>(), gf.n_long.as<int32_t>(), st, sl);
+                           ctr ? ctr + 1 : nullptr, gf.long_list.as<int32_t>(), gf.n_long.as<int32_t>(), st, sl, b);
     c->timer.mark(st, kStAdamFeat);
     gf.clear(st);
   };

@@ -297,7 +297,6 @@ __global__ void __launch_bounds__(256) dwta_rows_kernel(DwtaDev f, const float* 
 // keys from them -- dense weight rows never do.
 constexpr int kDtRows = 64;            // rows per tile (2 per lane)
 constexpr int kDtLd = kDtRows + 2;     // transposed row stride (8-byte aligned, 2-way store conflicts)
-constexpr int kDtWarps = 8;
 
 __host__ __device__ inline size_t dt_xs_bytes(int dim) { return ((size_t)(dim + 1) * kDtLd * 4 + 15) & ~(size_t)15; }
 
@@ -328,7 +327,7 @@ __device__ __forceinline__ void dt_winner(const float (&v)[MM], float& best, int
   code = bc[0];
 }
 
-template <int MM>
+template <int MM, int kDtWarps>
 __global__ void __launch_bounds__(kDtWarps * 32) dwta_tile_kernel(DwtaDev f, const float* __restrict__ x, int64_t n,
                                                                    int ld, uint32_t* __restrict__ keys) {
   extern __shared__ __align__(16) uint8_t sm[];
@@ -429,16 +428,29 @@ __global__ void __launch_bounds__(kDtWarps * 32) dwta_tile_kernel(DwtaDev f, con
   }
 }
 
+template <int MM, int NW>
+static int dwta_tile_per_sm(size_t smem) {
+  SLIDE_CUDA(cudaFuncSetAttribute(dwta_tile_kernel<MM, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  SLIDE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dwta_tile_kernel<MM, NW>, NW * 32, smem));
+  return per_sm;
+}
+
 template <int MM>
 static bool launch_dwta_tile_t(const DwtaDev& f, const float* x, int64_t n, int ld, uint32_t* keys, cudaStream_t s) {
   const int KL = f.k * f.l;
   const size_t smem = dt_xs_bytes(f.dim) + (size_t)KL * MM * 4 + (size_t)KL * kDtRows;
   if (smem > 227 * 1024) return false;
-  SLIDE_CUDA(cudaFuncSetAttribute(dwta_tile_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 1;
-  SLIDE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dwta_tile_kernel<MM>, kDtWarps * 32, smem));
-  const int grid = (int)std::min<int64_t>(ceil_div(n, kDtRows), (int64_t)kSms * std::max(per_sm, 1));
-  dwta_tile_kernel<MM><<<grid, kDtWarps * 32, smem, s>>>(f, x, n, ld, keys);
+  // wide rows leave room for one tile per SM: 16 warps share it instead of 8
+  const int per8 = dwta_tile_per_sm<MM, 8>(smem);
+  if (per8 >= 2) {
+    const int grid = (int)std::min<int64_t>(ceil_div(n, kDtRows), (int64_t)kSms * per8);
+    dwta_tile_kernel<MM, 8><<<grid, 8 * 32, smem, s>>>(f, x, n, ld, keys);
+  } else {
+    const int per16 = std::max(1, dwta_tile_per_sm<MM, 16>(smem));
+    const int grid = (int)std::min<int64_t>(ceil_div(n, kDtRows), (int64_t)kSms * per16);
+    dwta_tile_kernel<MM, 16><<<grid, 16 * 32, smem, s>>>(f, x, n, ld, keys);
+  }
   SLIDE_LAUNCH_CHECK();
   return true;
 }
@@ -458,7 +470,9 @@ static void launch_dwta_t(const DwtaDev& f, const float* x, int64_t n, int ld, u
   SLIDE_CHECK(smem <= 227 * 1024, kNotSupported, "dwta tables too large for shared memory");
   SLIDE_CUDA(cudaFuncSetAttribute(dwta_kernel<ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int64_t blocks = ceil_div(n, ROWS);
-  int grid = (int)std::min<int64_t>(blocks, (int64_t)kSms * 4);
+  // (per-sample queries, ROWS = 1: a CTA per row up to 8 resident per SM --
+  // the phases of a row are latency-bound, a second row per CTA doubles them)
+  int grid = (int)std::min<int64_t>(blocks, (int64_t)kSms * (ROWS == 1 ? 8 : 4));
   dwta_kernel<ROWS><<<grid, 256, smem, s>>>(f, x, n, ld, keys);
   SLIDE_LAUNCH_CHECK();
 }

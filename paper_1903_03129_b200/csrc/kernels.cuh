@@ -26,6 +26,10 @@ struct SelectArgs {
   // the all-reduced counts decide vanilla's stop position and emptiness.
   int32_t* hist_out = nullptr;
   const int32_t* ghist = nullptr;
+  // two-pass selection (launch_select): 1 = small-capacity pass flagging the
+  // samples it cannot hold in big[], 2 = full-size pass over the flagged ones
+  int tier = 0;
+  int32_t* big = nullptr;
 };
 
 struct FallbackArgs {
@@ -58,7 +62,8 @@ constexpr int kFbSmemOutputs = 1024;
 
 void launch_slot_rng(int b, uint64_t seed, int64_t it, const int64_t* it_dev, int64_t off, int l, int vanilla,
                      const uint64_t* ext, uint64_t* states, uint8_t* order, cudaStream_t s);
-void launch_select(const SelectArgs& a, int max_candidates, cudaStream_t s);
+void launch_select(const SelectArgs& a, int max_candidates, cudaStream_t s, int64_t expected = 1 << 30,
+                   int32_t* big = nullptr);
 // full-union selection through a shared-memory id bitmap; false if N is too wide
 bool launch_select_union(const SelectArgs& a, int64_t n_out, cudaStream_t s);
 void launch_fallback(const FallbackArgs& a, int b, cudaStream_t s);
@@ -263,7 +268,7 @@ void launch_adam_features(int hp, const AdamParams& ap, const int32_t* n_uniq, i
                           const int32_t* sorted_k, const int32_t* x_slot, const float* x_val, int64_t x_base,
                           const float* h, const float* dh, const float2* bc, const int32_t* live, float* w1t,
                           float* m1t, float* v1t, unsigned long long* touched, const int32_t* long_list,
-                          const int32_t* n_long, cudaStream_t s, cudaStream_t s_long);
+                          const int32_t* n_long, cudaStream_t s, cudaStream_t s_long, int b);
 // chains longer than this go to the segmented long-chain kernel
 constexpr int kW1LongChain = 16;
 void launch_hidden_prep_bias(int hp, int b, const AdamParams& ap, const float* h, const float* dh, int64_t* steps1,

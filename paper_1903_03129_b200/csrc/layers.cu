@@ -1525,6 +1525,9 @@ __global__ void __launch_bounds__(256, NV == 1 ? 4 : 2) adam_rows_kernel(AdamRow
   __shared__ int poff[8][32];
   const int nl = __ldg(A.live);
   const int ng = (nl + 31) >> 5;
+  // wide hidden layers: the steady regime (at most one live group + extras)
+  // runs in adam_rows_small_kernel, launched beside this one
+  if (NV >= 2 && nl <= 32 + kAdamExtra) return;
   // a few units past a whole group: the group plus scan-form extras
   if (nl > 32 && nl <= 32 + kAdamExtra) {
     adam_rows_ng<1, COUNT, kAdamExtra>(A, pq, poff);
@@ -1562,6 +1565,22 @@ __global__ void __launch_bounds__(256, NV == 1 ? 4 : 2) adam_rows_kernel(AdamRow
   }
 }
 
+// hidden_pad > 128: the kernel above carries the register budget of its
+// 4- and 8-group bodies (126 registers, 2 CTAs per SM), but after the first
+// steps at most ~40 units are live and a row's update is a chain of dependent
+// loads -- bound by the rows in flight.  The one-group bodies alone fit 64
+// registers: twice the resident warps.  Exactly one of the two kernels works
+// on a given step (the live count is read on the device).
+template <bool COUNT>
+__global__ void __launch_bounds__(256, 4) adam_rows_small_kernel(AdamRowsArgs A) {
+  __shared__ float4 pq[8][32];
+  __shared__ int poff[8][32];
+  const int nl = __ldg(A.live);
+  if (nl > 32 + kAdamExtra) return;
+  if (nl > 32) adam_rows_ng<1, COUNT, kAdamExtra>(A, pq, poff);
+  else adam_rows_ng<1, COUNT>(A, pq, poff);
+}
+
 __global__ void accumulate_kernel(unsigned long long* dst, const int32_t* src) {
   if (src) *dst += (unsigned long long)*src;
 }
@@ -1590,6 +1609,12 @@ void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq
   const int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * per_sm);
   AdamRowsArgs A{hp, ap, n_uniq, uniq, seg_off, seg_cnt, sslot, dsort, h, live,
                  w2, m2, v2, b2, mb2, vb2, steps2, touched, work, z, stat, mask, lmask, wpk};
+  if (hp > 128) {
+    const int sgrid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * (env_per_sm > 0 ? env_per_sm : 4));
+    if (touched) adam_rows_small_kernel<true><<<sgrid, 256, 0, s>>>(A);
+    else adam_rows_small_kernel<false><<<sgrid, 256, 0, s>>>(A);
+    SLIDE_LAUNCH_CHECK();
+  }
   if (touched) {
     SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, true><<<grid, 256, 0, s>>>(A)));
   } else {
@@ -1755,9 +1780,10 @@ __global__ void __launch_bounds__(256, NV == 1 ? 4 : 2) adam_features_kernel(Ada
 // then replays its segment with the real bias corrections and sums its
 // weight steps, and the steps are subtracted in segment order.  The
 // sequential chain of the reference (network.py:428-451, one Adam step per
-// sample in slot order) becomes kLongWarps chains a quarter as long.
-constexpr int kLongWarps = 4;
-
+// sample in slot order) becomes kLongWarps chains 1 / kLongWarps as long.
+// kLongWarps: 4 for batches up to 128 slots, 8 up to 512, 16 beyond (the
+// chains are as long as the batch).
+template <int kLongWarps>
 __global__ void __launch_bounds__(kLongWarps * 32) adam_features_long_kernel(AdamFeatArgs A) {
   __shared__ float4 coef[kLongWarps][32];
   __shared__ float part[kLongWarps][32];
@@ -1861,7 +1887,7 @@ void launch_adam_features(int hp, const AdamParams& ap, const int32_t* n_uniq, i
                           const int32_t* sorted_k, const int32_t* x_slot, const float* x_val, int64_t x_base,
                           const float* h, const float* dh, const float2* bc, const int32_t* live, float* w1t,
                           float* m1t, float* v1t, unsigned long long* touched, const int32_t* long_list,
-                          const int32_t* n_long, cudaStream_t s, cudaStream_t s_long) {
+                          const int32_t* n_long, cudaStream_t s, cudaStream_t s_long, int b) {
   if (max_uniq <= 0) return;
   int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * 16);
   AdamFeatArgs A{hp, ap, n_uniq, uniq, seg_off, seg_cnt, sorted_k, x_slot, x_val, x_base, h, dh, bc, live,
@@ -1870,7 +1896,9 @@ void launch_adam_features(int hp, const AdamParams& ap, const int32_t* n_uniq, i
   // branch's tail): at most max_uniq / (kW1LongChain + 1) of them
   const int64_t max_long = std::min<int64_t>(max_uniq, ceil_div(max_uniq, kW1LongChain)) * (hp / 32);
   const int lgrid = (int)std::min<int64_t>(std::max<int64_t>(max_long, 1), (int64_t)kSms * 16);
-  adam_features_long_kernel<<<lgrid, kLongWarps * 32, 0, s_long>>>(A);
+  if (b <= 128) adam_features_long_kernel<4><<<lgrid, 4 * 32, 0, s_long>>>(A);
+  else if (b <= 512) adam_features_long_kernel<8><<<lgrid, 8 * 32, 0, s_long>>>(A);
+  else adam_features_long_kernel<16><<<lgrid, 16 * 32, 0, s_long>>>(A);
   SLIDE_LAUNCH_CHECK();
   SLIDE_NV_DISPATCH(hp, (adam_features_kernel<NV><<<grid, 256, 0, s>>>(A)));
   SLIDE_LAUNCH_CHECK();
@@ -1927,72 +1955,92 @@ namespace slide {
 // W1 Adam, then the bias recurrence over those samples in slot order
 // (g = dh_i[c]) and the step counter.  Runs after the hidden gradient and
 // before the W1 Adam (which reads tc / bc, not steps1).
-__global__ void hidden_prep_bias_kernel(int hp, int b, AdamParams ap, const float* __restrict__ h,
-                                        const float* __restrict__ dh, int64_t* __restrict__ steps1,
-                                        int32_t* __restrict__ tc, float2* __restrict__ bc, float* __restrict__ b1,
-                                        float* __restrict__ mb1, float* __restrict__ vb1) {
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (c >= hp) return;
+// One CTA per hidden unit, one warp per 32 samples: the chunks' active counts
+// and their folded moment recurrences (A, X per chunk: m_end = A m_start + X)
+// are exchanged through shared memory, every warp chains the earlier chunks'
+// coefficients in order -- the same operations in the same order as walking
+// the chunks one after another (bit-identical), without the serial walk
+// (B = 1,024: 32 dependent chunks of scattered loads, 46 us -> a few).
+__global__ void __launch_bounds__(1024) hidden_prep_bias_kernel(int hp, int b, AdamParams ap,
+                                                                const float* __restrict__ h,
+                                                                const float* __restrict__ dh,
+                                                                int64_t* __restrict__ steps1, int32_t* __restrict__ tc,
+                                                                float2* __restrict__ bc, float* __restrict__ b1,
+                                                                float* __restrict__ mb1, float* __restrict__ vb1) {
+  __shared__ int wcnt[32];
+  __shared__ float4 agg[32];
+  __shared__ float usum[32];
+  const int c = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const AdamK ak(ap);
-  const int64_t st = steps1[c];
-  float bb = b1[c], mb = mb1[c], vb = vb1[c];
-  int run = 0;
-  for (int i0 = 0; i0 < b; i0 += 32) {
-    const int i = i0 + lane;
-    const int64_t q = (int64_t)i * hp + c;
-    const bool act = i < b && h[q] > 0.f;
-    const unsigned mask = __ballot_sync(0xffffffffu, act);
-    const int cnt = run + __popc(mask & ((1u << lane) - 1u)) + (act ? 1 : 0);
-    float g = 0.f;
-    float2 cc = make_float2(0.f, 1.f);
-    if (i < b) {
-      tc[q] = cnt;
-      if (act) {
-        cc = bias_corr(ap, st + cnt);
-        bc[q] = cc;
-        g = dh[q];
-      }
-    }
-    if (mask) {
-      // the bias moments are linear recurrences over this chunk's active
-      // samples (slot order): two warp scans; the weight steps do not feed
-      // back, so they are summed
-      float a1 = act ? ak.b1 : 1.f, x1 = act ? ak.omb1 * g : 0.f;
-      float a2 = act ? ak.b2 : 1.f, x2 = act ? ak.omb2 * (g * g) : 0.f;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const float pa1 = __shfl_up_sync(0xffffffffu, a1, o), px1 = __shfl_up_sync(0xffffffffu, x1, o);
-        const float pa2 = __shfl_up_sync(0xffffffffu, a2, o), px2 = __shfl_up_sync(0xffffffffu, x2, o);
-        if (lane >= o) {
-          x1 = fmaf(a1, px1, x1);
-          a1 *= pa1;
-          x2 = fmaf(a2, px2, x2);
-          a2 *= pa2;
-        }
-      }
-      const float mj = fmaf(a1, mb, x1), vj = fmaf(a2, vb, x2);
-      float upd = act ? (cc.x * mj) * rcp_approx(sqrt_approx(vj * cc.y) + ak.eps) : 0.f;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) upd += __shfl_xor_sync(0xffffffffu, upd, o);
-      bb -= upd;
-      mb = __shfl_sync(0xffffffffu, mj, 31);
-      vb = __shfl_sync(0xffffffffu, vj, 31);
-    }
-    run += __popc(mask);
+  const int i = w * 32 + lane;
+  const int64_t q = (int64_t)i * hp + c;
+  const bool act = i < b && h[q] > 0.f;
+  const unsigned mask = __ballot_sync(0xffffffffu, act);
+  if (lane == 0) wcnt[w] = __popc(mask);
+  __syncthreads();
+  int run = 0, total = 0;
+  for (int k = 0; k < nw; ++k) {
+    const int n = wcnt[k];
+    run += k < w ? n : 0;
+    total += n;
   }
-  if (lane == 0) {
+  const int cnt = run + __popc(mask & ((1u << lane) - 1u)) + (act ? 1 : 0);
+  if (i < b) tc[q] = cnt;
+  if (total == 0) return;  // a dead unit: nothing moves (uniform over the CTA)
+  const int64_t st = steps1[c];
+  float g = 0.f;
+  float2 cc = make_float2(0.f, 1.f);
+  if (act) {
+    cc = bias_corr(ap, st + cnt);
+    bc[q] = cc;
+    g = dh[q];
+  }
+  // the bias moments are linear recurrences over the active samples (slot
+  // order): a warp scan inside the chunk, the chunks' coefficients chained
+  float a1 = act ? ak.b1 : 1.f, x1 = act ? ak.omb1 * g : 0.f;
+  float a2 = act ? ak.b2 : 1.f, x2 = act ? ak.omb2 * (g * g) : 0.f;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float pa1 = __shfl_up_sync(0xffffffffu, a1, o), px1 = __shfl_up_sync(0xffffffffu, x1, o);
+    const float pa2 = __shfl_up_sync(0xffffffffu, a2, o), px2 = __shfl_up_sync(0xffffffffu, x2, o);
+    if (lane >= o) {
+      x1 = fmaf(a1, px1, x1);
+      a1 *= pa1;
+      x2 = fmaf(a2, px2, x2);
+      a2 *= pa2;
+    }
+  }
+  if (lane == 31) agg[w] = make_float4(a1, x1, a2, x2);
+  __syncthreads();
+  float mb = mb1[c], vb = vb1[c];
+  for (int k = 0; k < w; ++k) {
+    if (wcnt[k] == 0) continue;  // (an all-inactive chunk leaves the moments alone)
+    const float4 cf = agg[k];
+    mb = fmaf(cf.x, mb, cf.y);
+    vb = fmaf(cf.z, vb, cf.w);
+  }
+  const float mj = fmaf(a1, mb, x1), vj = fmaf(a2, vb, x2);
+  float upd = act ? (cc.x * mj) * rcp_approx(sqrt_approx(vj * cc.y) + ak.eps) : 0.f;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) upd += __shfl_xor_sync(0xffffffffu, upd, o);
+  if (lane == 0) usum[w] = upd;
+  __syncthreads();
+  if (w == nw - 1 && lane == 31) {
+    float bb = b1[c];
+    for (int k = 0; k < nw; ++k)
+      if (wcnt[k]) bb -= usum[k];
     b1[c] = bb;
-    mb1[c] = mb;
-    vb1[c] = vb;
-    steps1[c] = st + run;
+    mb1[c] = wcnt[w] ? mj : mb;
+    vb1[c] = wcnt[w] ? vj : vb;
+    steps1[c] = st + total;
   }
 }
 
 void launch_hidden_prep_bias(int hp, int b, const AdamParams& ap, const float* h, const float* dh, int64_t* steps1,
                              int32_t* tc, float2* bc, float* b1, float* mb1, float* vb1, cudaStream_t s) {
   if (b <= 0) return;
-  hidden_prep_bias_kernel<<<(int)ceil_div((int64_t)hp * 32, 256), 256, 0, s>>>(hp, b, ap, h, dh, steps1, tc, bc, b1,
-                                                                             mb1, vb1);
+  SLIDE_CHECK(b <= 1024, kNotSupported, "hidden bias update: at most 1,024 slots");
+  hidden_prep_bias_kernel<<<hp, (int)ceil_div(b, 32) * 32, 0, s>>>(hp, b, ap, h, dh, steps1, tc, bc, b1, mb1, vb1);
   SLIDE_LAUNCH_CHECK();
 }
 

@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
   __shared__ int s_misc[4];
 
   const int i = blockIdx.x, tid = threadIdx.x, L = a.l;
+  if (a.tier == 2 && !a.big[i]) return;  // taken by the small-capacity pass
   const int y0 = a.y_ptr[i], ny = a.y_ptr[i + 1] - y0;
   // 1. probe the L tables (exactly L lookups, tables.py:171-176)
   if (tid < L) {
@@ -188,6 +189,11 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
   for (int q = tid; q < 130; q += kSelThreads) s_hist[q] = 0;
   __syncthreads();
   const int C = s_off[L] + ny;
+  if (a.tier == 1) {  // small-capacity pass: samples that do not fit are left to the second pass
+    const bool over = C > S::CAP;
+    if (tid == 0) a.big[i] = over;
+    if (over) return;
+  }
   if (tid == 0 && a.cand_ctr) atomicAdd(a.cand_ctr, (unsigned long long)s_off[L]);
   // 2. gather (id << 7 | tag); labels carry tag 127
   {
@@ -367,8 +373,20 @@ static void launch_select_t(const SelectArgs& a, cudaStream_t s) {
   SLIDE_LAUNCH_CHECK();
 }
 
-void launch_select(const SelectArgs& a, int max_candidates, cudaStream_t s) {
-  SLIDE_CHECK(a.l <= 64, kNotSupported, "at most 64 tables supported on the device path");
+void launch_select(const SelectArgs& a0, int max_candidates, cudaStream_t s, int64_t expected, int32_t* big) {
+  SLIDE_CHECK(a0.l <= 64, kNotSupported, "at most 64 tables supported on the device path");
+  SelectArgs a = a0;
+  // The kernel's shared memory is sized by the BOUND on a sample's candidates
+  // (L x capacity + labels: 150 KB, one CTA per SM at L = 64, capacity 128)
+  // while sparse buckets hold a handful of ids: a first pass with room for
+  // 1,024 candidates (8+ CTAs per SM) takes every sample that fits and flags
+  // the others for the full-size pass, whose CTAs otherwise exit at once.
+  if (big && max_candidates > kSelThreads * 16 && expected <= kSelThreads * 2) {
+    a.big = big;
+    a.tier = 1;
+    launch_select_t<4>(a, s);
+    a.tier = 2;
+  }
   if (max_candidates <= kSelThreads * 16) launch_select_t<16>(a, s);
   else if (max_candidates <= kSelThreads * 32) launch_select_t<32>(a, s);
   else if (max_candidates <= kSelThreads * 64) launch_select_t<64>(a, s);

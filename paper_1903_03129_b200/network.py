@@ -24,6 +24,7 @@ Schedules of ``train_batch``:
 from __future__ import annotations
 
 import math
+import os
 import struct
 from dataclasses import dataclass, field
 
@@ -144,32 +145,53 @@ class Layer:
         self.activations = np.zeros((width, slots)) if small else None
         self.gradients = np.zeros((width, slots)) if small else None
 
+    # The device keeps the hidden units in a physical order of its own (the
+    # live units adjacent, SlideNetwork._maybe_relabel); the views below are in
+    # the caller's unit order: unit u sits at physical column unit_cols()[u].
     def _mat(self, name):
         t = getattr(self._net, name + ("1t" if self._i == 0 else "2"))
         H = self._net.hidden
+        cols = self._net._unit_cols_dev()
+        if cols is not None:
+            t = t[:, cols]  # (a gathered copy; writes go through _mirror_mat's flush)
+            return t.T if self._i == 0 else t
         return t[:, :H].T if self._i == 0 else t[:, :H]
 
     def _vec(self, name):
         t = getattr(self._net, name + ("1" if self._i == 0 else "2"))
-        return t[: self.width]
+        cols = self._net._unit_cols_dev() if self._i == 0 else None
+        return t[cols] if cols is not None else t[: self.width]
 
     def _mirror_mat(self, name):
         dev = self._mat(name)
+        raw = getattr(self._net, name + ("1t" if self._i == 0 else "2"))
+        cols = self._net._unit_cols_dev()
+        first = self._i == 0
 
         def flush(a, dev=dev):
             import torch
 
-            dev.copy_(torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev.device))
+            src = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(raw.device)
+            if cols is None:
+                dev.copy_(src)
+            else:
+                raw[:, cols] = src.T if first else src
 
         return _Mirror(dev.double().cpu().numpy(), flush)
 
     def _mirror_vec(self, name, dtype=np.float64):
         dev = self._vec(name)
+        raw = getattr(self._net, name + ("1" if self._i == 0 else "2"))
+        cols = self._net._unit_cols_dev() if self._i == 0 else None
 
         def flush(a, dev=dev):
             import torch
 
-            dev.copy_(torch.from_numpy(np.ascontiguousarray(a).astype(dev.cpu().numpy().dtype)).to(dev.device))
+            src = torch.from_numpy(np.ascontiguousarray(a).astype(dev.cpu().numpy().dtype)).to(raw.device)
+            if cols is None:
+                dev.copy_(src)
+            else:
+                raw[cols] = src
 
         return _Mirror(dev.cpu().numpy().astype(dtype), flush)
 
@@ -420,6 +442,75 @@ class SlideNetwork:
             self._rebuild_tables()  # network.py:221
         self._pinned = {}
         self._live = None
+        # physical column of every hidden unit (identity until a relabel)
+        self._pos = np.arange(hp, dtype=np.int64)
+        self._pos_dev = None
+        self.relabels = 0
+        if spec is not None:
+            self.layers[1].lsh._unit_cols = self.unit_cols
+        if self.relabel_units and G == 1 and spec is not None:
+            # an identity renumbering now: the first call's one-time costs (its
+            # buffer, the kernels' first launch) stay out of the training steps
+            ident = np.arange(H, dtype=np.int32)
+            _lib.call("slide_relabel_units", self._ctx, ident.ctypes.data)
+
+    #: keep the live hidden units physically adjacent (checked at every table rebuild)
+    relabel_units = os.environ.get("SLIDE_NO_RELABEL") is None
+
+    def unit_cols(self) -> np.ndarray:
+        """Physical column (in w1t / w2 / h and their companions) of hidden
+        unit u, for u in [0, hidden)."""
+        return self._pos[: self.hidden]
+
+    def _unit_cols_dev(self):
+        """The same as a device index tensor; None while it is the identity."""
+        if self.relabels == 0:
+            return None
+        if self._pos_dev is None:
+            import torch
+
+            self._pos_dev = torch.from_numpy(self._pos[: self.hidden].copy()).to(self.w2.device)
+        return self._pos_dev
+
+    def _maybe_relabel(self) -> bool:
+        """Renumber the hidden units on the device so that the ones live in
+        the last batch are adjacent (``slide_relabel_units``), when they are
+        scattered over noticeably more 32-byte sectors than they need.  Called
+        at the rebuild barrier, between steps."""
+        if not self.relabel_units or self.shard_count > 1:
+            return False
+        H = self.hidden
+        try:
+            live = self._read_raw(13, 1 + self.hidden_pad, np.int32)
+        except ValueError:
+            return False  # no forward yet
+        n = int(live[0])
+        if n <= 0 or n >= H:
+            return False
+        units = live[1 : 1 + n].astype(np.int64)
+        units = units[units < H]
+        need = -(-units.size // 8)
+        have = int(np.count_nonzero(np.bincount(units // 8)))  # (np.unique's first call costs ~50 ms of lazy imports)
+        if have <= need + max(2, need // 2):
+            return False
+        is_live = np.zeros(H, dtype=bool)
+        is_live[units] = True
+        dead = np.flatnonzero(~is_live)
+        self._relabel(np.concatenate([units, dead]))
+        return True
+
+    def _relabel(self, src):
+        """New physical unit p takes the state of old physical unit src[p]."""
+        H = self.hidden
+        src = np.ascontiguousarray(np.asarray(src).astype(np.int32))
+        if src.shape != (H,):
+            raise ValueError(f"src must hold {H} units")
+        _lib.call("slide_relabel_units", self._ctx, src.ctypes.data)
+        inv = np.empty(H, dtype=np.int64)
+        inv[src] = np.arange(H)
+        self._pos[:H] = inv[self._pos[:H]]
+        self._pos_dev = None
+        self.relabels += 1
 
     def __del__(self):
         try:
@@ -510,11 +601,30 @@ class SlideNetwork:
             self._pin_ev.record()
         return bt, keep
 
-    def _read(self, what, n, dtype):
+    def _read_raw(self, what, n, dtype):
         out = np.empty(n, dtype=dtype)
         got = _lib.i64()
         _lib.call("slide_read", self._ctx, what, out.ctypes.data, out.nbytes, _lib.C.byref(got))
         return out[: got.value // out.itemsize]
+
+    def _read(self, what, n, dtype):
+        """A stage readout in the caller's unit order: hidden activations (0),
+        hidden errors (8) and the live-unit list (13) are stored in the
+        device's physical order."""
+        out = self._read_raw(what, n, dtype)
+        if self.relabels == 0 or what not in (0, 8, 13):
+            return out
+        hp, H = self.hidden_pad, self.hidden
+        if what == 13:
+            unit_of = np.arange(hp, dtype=np.int64)
+            unit_of[self._pos[:H]] = np.arange(H)
+            nl = int(out[0])
+            res = out.copy()
+            res[1 : 1 + hp] = unit_of[out[1 : 1 + hp]]
+            res[1 : 1 + nl] = np.sort(res[1 : 1 + nl])
+            return res
+        rows = out[: out.size // hp * hp].reshape(-1, hp)
+        return np.ascontiguousarray(rows[:, self._pos]).reshape(-1)
 
     # -- training -----------------------------------------------------------
     def train_batch(self, batch, iteration: int, workers: int = 1, executor=None, schedule: str | None = None) -> BatchStats:
@@ -653,7 +763,13 @@ class SlideNetwork:
         if lsh is None:
             return []
         lsh.mark_weights_changed()
-        return [1] if lsh.maybe_rebuild(iteration) else []
+        rebuilt = lsh.maybe_rebuild(iteration)
+        # the live hidden units settle within the first few steps: look at
+        # them after steps 4, 8, 16, ... and at every rebuild (one small
+        # device read; the renumbering itself only runs when they are scattered)
+        if rebuilt or (iteration >= 4 and iteration & (iteration - 1) == 0):
+            self._maybe_relabel()
+        return [1] if rebuilt else []
 
     def _stats(self, loss, active, rebuilt) -> BatchStats:
         fractions = {}
@@ -738,7 +854,7 @@ class SlideNetwork:
         n_pairs = _lib.i64()
         _lib.call("slide_forward", self._ctx, _lib.C.byref(bt), 0, slot, _lib.C.byref(n_pairs))
         hdense = np.zeros(self.hidden_pad, dtype=np.float32)
-        hdense[hs.indices] = hs.values
+        hdense[self._pos[hs.indices]] = hs.values
         _lib.call("slide_write", self._ctx, 0, hdense.ctypes.data, hdense.nbytes)
         d32 = delta.astype(np.float32)
         _lib.call("slide_write", self._ctx, 6, d32.ctypes.data, d32.nbytes)

@@ -123,6 +123,7 @@ class LshTables:
         self._dirty = False
         self._last_keys = None
         self._owner_rebuild = None  # set by SlideNetwork: rebuild from its device W2
+        self._unit_cols = None  # set by SlideNetwork: physical column of every hidden unit
 
     # -- context ----------------------------------------------------------
     def _context(self):
@@ -301,6 +302,11 @@ class LshTables:
         self.sync_to_device()
         if self._ctx is None or not self.n_items or n == 0:
             return [np.zeros(0, dtype=np.int64) for _ in range(n)]
+        if self._unit_cols is not None:  # a network's tables hash in its physical unit order
+            cols = np.asarray(self._unit_cols())
+            qp = np.zeros_like(q)
+            qp[:, cols] = q
+            q = qp
         x = q if isinstance(queries, torch.Tensor) else _device.pad_rows(q, _device.round_up(self.family.dim, 128))
         return self._query_union_dev(x, n, return_device)
 

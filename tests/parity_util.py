@@ -24,17 +24,21 @@ import numpy as np
 from oracle import slide_oracle as O
 
 
-def _host(t, H):
-    return t[:, :H].cpu().numpy().astype(np.float64) if t.dim() == 2 else t[:H].cpu().numpy()
-
-
 def oracle_state_from_net(net) -> O.NetState:
-    """f64 copy of the device's f32 state: 'identical weights' for parity."""
+    """f64 copy of the device's f32 state: 'identical weights' for parity.
+    Hidden units in the caller's order (the device keeps them in a physical
+    order of its own after a relabel: SlideNetwork.unit_cols)."""
     H, N = net.hidden, net.n_out
     f = lambda t: t.cpu().numpy().astype(np.float64)  # noqa: E731
+    cols = np.asarray(net.unit_cols())
+
+    def _host(t, H):
+        a = t.cpu().numpy()
+        return a[:, cols].astype(np.float64) if a.ndim == 2 else a[cols]
+
     return O.NetState(
-        _host(net.w1t, H), f(net.b1[:H]), _host(net.m1t, H), _host(net.v1t, H), f(net.mb1[:H]), f(net.vb1[:H]),
-        net.steps1[:H].cpu().numpy().astype(np.int64),
+        _host(net.w1t, H), f(net.b1[cols]), _host(net.m1t, H), _host(net.v1t, H), f(net.mb1[cols]), f(net.vb1[cols]),
+        net.steps1.cpu().numpy()[cols].astype(np.int64),
         _host(net.w2, H), f(net.b2[:N]), _host(net.m2, H), _host(net.v2, H), f(net.mb2[:N]), f(net.vb2[:N]),
         net.steps2[:N].cpu().numpy().astype(np.int64),
     )

@@ -78,7 +78,12 @@ def test_tiny_200_steps_sequential_matches_reference(golden):
           f"{np.mean(ref[-50:]):.4f}; worst err/tol {worst}")
     assert np.max(rel[:5]) < 1e-4
     assert abs(np.mean(losses[-50:]) - np.mean(ref[-50:])) < 0.05 * np.mean(ref[-50:])
-    assert abs(p1 - g["seq_p1"][0]) <= 0.01
+    # within one point of the reference -- of the interval the reference's own
+    # P@1 spans when its initial weights move by 1e-7 relative (p1_runs.npz:
+    # 0.0225 .. 0.034 over four perturbed runs; the chaotic trajectory, not the
+    # arithmetic, decides where in it a run lands)
+    noise = np.concatenate([golden("p1_runs")["tiny_seq_p1_noise"], g["seq_p1"]])
+    assert noise.min() - 0.01 <= p1 <= noise.max() + 0.01
 
 
 def test_tiny_200_steps_snapshot_precision_reported(golden):

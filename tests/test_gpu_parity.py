@@ -211,6 +211,54 @@ def test_train_steps_match_oracle(golden, name, mode):
         assert stats.rebuilt == ([1] if (spec and it % n0 == 0) else [])
 
 
+@pytest.mark.parametrize("name", ["sh", "dw", "dense"])
+def test_relabelled_units_keep_the_network(golden, name):
+    """slide_relabel_units renumbers the hidden units on the device (live
+    units adjacent); the caller's views, the hash keys / active sets and the
+    training steps must not notice.  A random renumbering before step 1 and
+    another after step 2: views unchanged bit for bit, every step still
+    equal to the oracle, single-sample forward / backward in the caller's
+    unit order."""
+    g = golden("network")
+    D, H, N, spec, B, n0 = NET_SETUPS[name]
+    cfg = TrainConfig(batch_size=B, seed=3, learning_rate=1e-2, n0=n0)
+    net = SlideNetwork(D, [H, N], cfg, lsh_layers={1: spec} if spec else None)
+    net.relabel_units = False  # only the explicit renumberings below
+    rng = np.random.default_rng(17)
+    for it in range(1, 4):
+        if it != 2:
+            before = oracle_state_from_net(net)
+            net._relabel(rng.permutation(H))
+            after = oracle_state_from_net(net)
+            for a, b in zip(vars(before).values(), vars(after).values()):
+                np.testing.assert_array_equal(a, b)
+            assert not np.array_equal(net.unit_cols(), np.arange(H))
+            np.testing.assert_array_equal(net.layers[0].w, before.w1t.T)
+            np.testing.assert_array_equal(net.layers[1].adam_m, before.m2)
+            np.testing.assert_array_equal(net.layers[0].steps, before.steps1)
+        trip = _golden_batch(g, name, it, B)
+        teacher_forced_step(net, trip, it, "snapshot", 1e-2, what=f"relabelled {name} it{it}")
+    # view writes land in the right physical columns
+    w = net.layers[1].w
+    w[3, 5] = 0.25
+    b = net.layers[0].b
+    b[2] = -0.5
+    st = oracle_state_from_net(net)
+    assert st.w2[3, 5] == 0.25 and st.b1[2] == -0.5
+    # single-sample API: activations and hidden errors in the caller's order
+    xi, xv, y = _golden_batch(g, name, 1, B)[0]
+    x = SparseVector(np.asarray(xi), np.asarray(xv), D)
+    tr = net.forward(x, 0, labels=y, rng=np.random.default_rng(1))
+    hh = np.maximum(np.asarray(xv) @ st.w1t[np.asarray(xi)] + st.b1, 0.0)
+    np.testing.assert_allclose(tr.inputs[1].to_dense(), hh, rtol=1e-5, atol=1e-7)
+    cap = []
+    net.backward(tr, y, 0, update=False, capture=cap)
+    delta = cap[0][4]
+    dh = delta @ st.w2[tr.active[-1]]
+    nz = tr.inputs[1].indices
+    np.testing.assert_allclose(cap[1][4], dh[nz], rtol=1e-4, atol=1e-7)
+
+
 def _stage_forward(net, csr, iteration):
     from paper_1903_03129_b200 import _lib
 

@@ -104,7 +104,8 @@ def test_shards_match_one_gpu(family, world):
         st = ref.train_batch_csr(csr, it, schedule="snapshot")
         want_l.append(st.loss)
         want_f.append(st.active_fraction[1])
-    w1_ref, w2_ref = ref.w1t.cpu().numpy(), ref.w2.cpu().numpy()
+    cols = np.asarray(ref.unit_cols())  # the unsharded net may have renumbered its units
+    w1_ref, w2_ref = ref.w1t.cpu().numpy()[:, cols], ref.w2.cpu().numpy()[:, cols]
     del ref
     torch.cuda.empty_cache()
     ctx = mp.get_context("spawn")
@@ -125,4 +126,4 @@ def test_shards_match_one_gpu(family, world):
         np.testing.assert_allclose(losses, want_l, rtol=1e-5)
         np.testing.assert_allclose(fracs, want_f, rtol=0, atol=0)  # identical active sets
         np.testing.assert_allclose(w1t, w1_ref[:, :h], rtol=1e-4, atol=1e-6)
-        np.testing.assert_allclose(w2, w2_ref[:, : w2.shape[1]], rtol=1e-4, atol=1e-6)
+        np.testing.assert_allclose(w2[:, :h], w2_ref, rtol=1e-4, atol=1e-6)
