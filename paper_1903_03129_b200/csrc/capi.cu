@@ -998,7 +998,8 @@ static void forward_impl(slide_ctx* c, const slide_batch* bt, int64_t iteration,
     const GroupView rv = gr.view();
     launch_softmax(b, offs, plab, bt->y_ptr, z, prob, delta, loss, gr.inv.as<int32_t>(), dsort, s,
                    c->rows_mode ? prow : nullptr, c->rows_mode ? &rv : nullptr,
-                   c->rows_mode ? gr.sslot.as<int32_t>() : nullptr);
+                   c->rows_mode ? gr.sslot.as<int32_t>() : nullptr,
+                   /*small_sets=*/d.family != 0 && expected_pairs(c, b) / std::max(b, 1) + max_labels <= 1024);
   }
   c->timer.mark(s, kStSoftmax);
   c->have_forward = true;

@@ -147,10 +147,15 @@ __global__ void __launch_bounds__(256) dwta_kernel(DwtaDev f, const float* __res
   int16_t* perm = reinterpret_cast<int16_t*>(xs + ROWS * f.dim);
   uint8_t* codes = reinterpret_cast<uint8_t*>(perm + ((f.n_perms * f.dim + 1) & ~1));
   uint8_t* occ = codes + ROWS * KL;
+  // a row without any occupied bin (an all-zero activation row: every hidden
+  // unit dead for that sample) has nothing to borrow: all its codes are 0 --
+  // without the 100-step donor walk of every one of its bins (40 us a row)
+  __shared__ int row_any[ROWS];
   for (int q = threadIdx.x; q < f.n_perms * f.dim; q += blockDim.x) perm[q] = f.perms[q];
   for (int64_t row0 = (int64_t)blockIdx.x * ROWS; row0 < n; row0 += (int64_t)gridDim.x * ROWS) {
     const int nr = (int)(n - row0 < ROWS ? n - row0 : ROWS);
     __syncthreads();
+    if (threadIdx.x < ROWS) row_any[threadIdx.x] = 0;
     for (int q = threadIdx.x; q < ROWS * f.dim; q += blockDim.x) {
       int r = q / f.dim, c = q - r * f.dim;
       xs[q] = r < nr ? x[(row0 + r) * ld + c] : 0.f;
@@ -174,13 +179,14 @@ __global__ void __launch_bounds__(256) dwta_kernel(DwtaDev f, const float* __res
       }
       codes[q] = (uint8_t)code;
       occ[q] = (uint8_t)oc;
+      if (oc) row_any[r] = 1;
     }
     __syncthreads();
     for (int q = threadIdx.x; q < ROWS * KL; q += blockDim.x) {
       if (occ[q]) continue;
       int r = q / KL, g = q - r * KL;
       int code = 0;
-      for (int a = 0; a < 100; ++a) {
+      for (int a = 0; a < 100 && row_any[r]; ++a) {
         int d = f.donors[g * 100 + a];
         if (occ[r * KL + d]) {
           code = codes[r * KL + d];

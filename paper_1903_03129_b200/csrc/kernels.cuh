@@ -219,7 +219,8 @@ void launch_logits_rows(int hp, int b, const GroupView& g, const int32_t* pslot,
 // kernel also writes sslot[pos] = slot for the W2 Adam
 void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
                     float* prob, float* delta, double* loss, const int32_t* inv, float* dsort, cudaStream_t s,
-                    const int32_t* prow = nullptr, const GroupView* rows = nullptr, int32_t* sslot = nullptr);
+                    const int32_t* prow = nullptr, const GroupView* rows = nullptr, int32_t* sslot = nullptr,
+                    bool small_sets = false);
 // lazy softmax of a training step under the place-free grouping: per-tile
 // partials (part: softmax_lazy_parts(u_max, b) float2), per sample stat =
 // (M, 1/S, 1/|Y|) and the loss; pairs' errors are made where they are read

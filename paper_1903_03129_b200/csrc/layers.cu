@@ -620,16 +620,19 @@ void launch_logits_rows(int hp, int b, const GroupView& g, const int32_t* pslot,
 // ROWS: z is in the place-free row grouping's order; a pair's position is
 // read off its row's slot mask (g.pos_of), its error and slot go to dsort /
 // sslot at that position
-template <bool ROWS>
-__global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict__ offs,
+// T threads per sample: 1,024 for large active sets, 128 when a sample holds
+// at most ~1,000 pairs (the block-wide reductions of 32 warps cost more than
+// the set's arithmetic there; B = 1,024 samples: 23 -> a few us).
+template <bool ROWS, int T>
+__global__ void __launch_bounds__(T) softmax_kernel(const int32_t* __restrict__ offs,
                                                       const uint8_t* __restrict__ plab,
                                                       const int32_t* __restrict__ y_ptr, const float* __restrict__ z,
                                                       float* __restrict__ prob, float* __restrict__ delta,
                                                       double* __restrict__ loss, const int32_t* __restrict__ inv,
                                                       float* __restrict__ dsort, const int32_t* __restrict__ prow,
                                                       GroupView g, int32_t* __restrict__ sslot) {
-  using RF = cub::BlockReduce<float, 1024>;
-  using RD = cub::BlockReduce<double, 1024>;
+  using RF = cub::BlockReduce<float, T>;
+  using RD = cub::BlockReduce<double, T>;
   __shared__ union {
     typename RF::TempStorage f;
     typename RD::TempStorage d;
@@ -647,12 +650,12 @@ __global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict
   float mx = -INFINITY;
 #pragma unroll
   for (int j = 0; j < kSmC; ++j) {
-    const int k = tid + j * 1024;
+    const int k = tid + j * T;
     pr[j] = k < n ? pos_of(k) : 0;
     zr[j] = k < n ? z[pr[j]] : -INFINITY;
     mx = fmaxf(mx, zr[j]);
   }
-  for (int k = tid + kSmC * 1024; k < n; k += 1024) mx = fmaxf(mx, z[pos_of(k)]);
+  for (int k = tid + kSmC * T; k < n; k += T) mx = fmaxf(mx, z[pos_of(k)]);
   mx = RF(tmp.f).Reduce(mx, cub::Max());
   if (tid == 0) s_max = n > 0 ? mx : 0.f;
   __syncthreads();
@@ -660,10 +663,10 @@ __global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict
   float se = 0.f;
 #pragma unroll
   for (int j = 0; j < kSmC; ++j) {
-    er[j] = tid + j * 1024 < n ? expf(zr[j] - mx) : 0.f;
+    er[j] = tid + j * T < n ? expf(zr[j] - mx) : 0.f;
     se += er[j];
   }
-  for (int k = tid + kSmC * 1024; k < n; k += 1024) se += expf(z[pos_of(k)] - mx);
+  for (int k = tid + kSmC * T; k < n; k += T) se += expf(z[pos_of(k)] - mx);
   se = RF(tmp.f).Sum(se);
   if (tid == 0) s_sum = se;
   __syncthreads();
@@ -673,7 +676,7 @@ __global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict
   double lsum = 0.0;
 #pragma unroll
   for (int j = 0; j < kSmC; ++j) {
-    const int k = tid + j * 1024;
+    const int k = tid + j * T;
     if (k >= n) break;
     const float zz = zr[j] - mx;
     const float p = er[j] / se;
@@ -692,7 +695,7 @@ __global__ void __launch_bounds__(1024) softmax_kernel(const int32_t* __restrict
       lsum += (nl < 690.7755278982137 || nl != nl) ? nl : 690.7755278982137;  // NaN propagates (np.maximum)
     }
   }
-  for (int k = tid + kSmC * 1024; k < n; k += 1024) {
+  for (int k = tid + kSmC * T; k < n; k += T) {
     const int pk = pos_of(k);
     const float zz = z[pk] - mx;
     const float p = expf(zz) / se;
@@ -731,14 +734,22 @@ void launch_scatter_sorted(const int32_t* n_dev, int64_t n_max, const int32_t* i
 
 void launch_softmax(int b, const int32_t* offs, const uint8_t* plab, const int32_t* y_ptr, const float* z,
                     float* prob, float* delta, double* loss, const int32_t* inv, float* dsort, cudaStream_t s,
-                    const int32_t* prow, const GroupView* rows, int32_t* sslot) {
+                    const int32_t* prow, const GroupView* rows, int32_t* sslot, bool small_sets) {
   if (b <= 0) return;
-  if (rows)
-    softmax_kernel<true><<<b, 1024, 0, s>>>(offs, plab, y_ptr, z, prob, delta, loss, nullptr, dsort, prow, *rows,
-                                            sslot);
-  else
-    softmax_kernel<false><<<b, 1024, 0, s>>>(offs, plab, y_ptr, z, prob, delta, loss, inv, dsort, nullptr,
-                                             GroupView{}, nullptr);
+  if (rows) {
+    if (small_sets)
+      softmax_kernel<true, 128><<<b, 128, 0, s>>>(offs, plab, y_ptr, z, prob, delta, loss, nullptr, dsort, prow,
+                                                  *rows, sslot);
+    else
+      softmax_kernel<true, 1024><<<b, 1024, 0, s>>>(offs, plab, y_ptr, z, prob, delta, loss, nullptr, dsort, prow,
+                                                    *rows, sslot);
+  } else if (small_sets) {
+    softmax_kernel<false, 128><<<b, 128, 0, s>>>(offs, plab, y_ptr, z, prob, delta, loss, inv, dsort, nullptr,
+                                                 GroupView{}, nullptr);
+  } else {
+    softmax_kernel<false, 1024><<<b, 1024, 0, s>>>(offs, plab, y_ptr, z, prob, delta, loss, inv, dsort, nullptr,
+                                                   GroupView{}, nullptr);
+  }
   SLIDE_LAUNCH_CHECK();
 }
 
@@ -1290,6 +1301,7 @@ struct AdamPf {
   static constexpr int value = NG >= 4 ? 2 : 8 / NG;
 };
 constexpr int kAdamExtra = 8;  // live units past whole groups taken in scan form
+constexpr int kAdamSmallLive = 64 + kAdamExtra;  // hidden_pad > 128: up to two live groups + extras run in adam_rows_small_kernel
 
 // The persistent row loop for NG live 32-unit groups (compile-time, so the
 // per-pair body has no group guards and the next kAdamPf pairs' activations
@@ -1526,8 +1538,8 @@ __global__ void __launch_bounds__(256, NV == 1 ? 4 : 2) adam_rows_kernel(AdamRow
   const int nl = __ldg(A.live);
   const int ng = (nl + 31) >> 5;
   // wide hidden layers: the steady regime (at most one live group + extras)
-  // runs in adam_rows_small_kernel, launched beside this one
-  if (NV >= 2 && nl <= 32 + kAdamExtra) return;
+  // runs in adam_rows_small_kernel, launched before this one
+  if (NV >= 2 && nl <= kAdamSmallLive) return;
   // a few units past a whole group: the group plus scan-form extras
   if (nl > 32 && nl <= 32 + kAdamExtra) {
     adam_rows_ng<1, COUNT, kAdamExtra>(A, pq, poff);
@@ -1572,13 +1584,15 @@ __global__ void __launch_bounds__(256, NV == 1 ? 4 : 2) adam_rows_kernel(AdamRow
 // registers: twice the resident warps.  Exactly one of the two kernels works
 // on a given step (the live count is read on the device).
 template <bool COUNT>
-__global__ void __launch_bounds__(256, 4) adam_rows_small_kernel(AdamRowsArgs A) {
+__global__ void __launch_bounds__(256, 3) adam_rows_small_kernel(AdamRowsArgs A) {
   __shared__ float4 pq[8][32];
   __shared__ int poff[8][32];
   const int nl = __ldg(A.live);
-  if (nl > 32 + kAdamExtra) return;
-  if (nl > 32) adam_rows_ng<1, COUNT, kAdamExtra>(A, pq, poff);
-  else adam_rows_ng<1, COUNT>(A, pq, poff);
+  if (nl > kAdamSmallLive) return;
+  if (nl <= 32) adam_rows_ng<1, COUNT>(A, pq, poff);
+  else if (nl <= 32 + kAdamExtra) adam_rows_ng<1, COUNT, kAdamExtra>(A, pq, poff);
+  else if (nl <= 64) adam_rows_ng<2, COUNT>(A, pq, poff);
+  else adam_rows_ng<2, COUNT, kAdamExtra>(A, pq, poff);
 }
 
 __global__ void accumulate_kernel(unsigned long long* dst, const int32_t* src) {
@@ -1610,7 +1624,7 @@ void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq
   AdamRowsArgs A{hp, ap, n_uniq, uniq, seg_off, seg_cnt, sslot, dsort, h, live,
                  w2, m2, v2, b2, mb2, vb2, steps2, touched, work, z, stat, mask, lmask, wpk};
   if (hp > 128) {
-    const int sgrid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * (env_per_sm > 0 ? env_per_sm : 4));
+    const int sgrid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * (env_per_sm > 0 ? env_per_sm : 3));
     if (touched) adam_rows_small_kernel<true><<<sgrid, 256, 0, s>>>(A);
     else adam_rows_small_kernel<false><<<sgrid, 256, 0, s>>>(A);
     SLIDE_LAUNCH_CHECK();
