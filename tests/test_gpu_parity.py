@@ -259,6 +259,46 @@ def test_relabelled_units_keep_the_network(golden, name):
     np.testing.assert_allclose(cap[1][4], dh[nz], rtol=1e-4, atol=1e-7)
 
 
+def test_two_pass_selection_mixed_samples():
+    """Sparse buckets with one hot bucket per table: the selection runs its
+    1,024-candidate pass first and the bound-sized pass (L x capacity + labels
+    = 5,120 + candidates) only for the samples flagged by it.  Half of the W2
+    rows are copies of one vector v and the hidden layer is rigged so that a
+    sample's activations are either exactly v (it probes the copies' full
+    bucket in all 40 tables: 5,120 candidates) or all zero (key 0 everywhere:
+    a handful) -- both kinds in one batch, against the oracle."""
+    rng = np.random.default_rng(5)
+    D, H, N, B = 64, 32, 3000, 24
+    spec = LshLayerConfig("simhash", k=10, l=40, capacity=128, sampler=SamplerConfig("vanilla", beta=64))
+    cfg = TrainConfig(batch_size=B, seed=2, learning_rate=1e-3, n0=1000)
+    net = SlideNetwork(D, [H, N], cfg, lsh_layers={1: spec})
+    v = (np.abs(rng.standard_normal(H)) + 0.1).astype(np.float32).astype(np.float64)
+    w1 = np.zeros((H, D))
+    w1[:, 0] = -4.0 * v  # feature 0 (value 1) switches every unit off
+    net.layers[0].w = w1
+    net.layers[0].b = v
+    w2 = np.asarray(net.layers[1].w).copy()
+    w2[:1500] = v
+    net.layers[1].w = w2
+    net._rebuild_tables()
+    sizes = set()
+    for it in (1, 2):
+        trip = []
+        for i in range(B):
+            idx = np.sort(rng.choice(np.arange(1, D), size=int(rng.integers(2, 6)), replace=False))
+            if i % 3 == 0:
+                idx = np.concatenate([[0], idx])
+            vals = np.ones(idx.size)
+            # (labels outside the copies: with both labels among them the hidden
+            # error v * sum(delta) cancels to rounding noise, which Adam normalises)
+            labels = sorted(rng.choice(np.arange(1500, N), size=2, replace=False).tolist())
+            trip.append((idx.astype(np.int64), vals, labels))
+        want, got, _ = teacher_forced_step(net, trip, it, "snapshot", 1e-3, what=f"two-pass select it{it}")
+        sizes |= {len(t.active) for t in want.traces}
+    # both kinds were in the batches: the copies' bucket (128 ids + labels) and beta-sized sets
+    assert max(sizes) >= 128 and min(sizes) < 128
+
+
 def _stage_forward(net, csr, iteration):
     from paper_1903_03129_b200 import _lib
 
