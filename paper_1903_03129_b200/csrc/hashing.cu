@@ -341,7 +341,9 @@ __global__ void __launch_bounds__(kDtWarps * 32) dwta_tile_kernel(DwtaDev f, con
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* xs = reinterpret_cast<float*>(sm);                                    // [dim + 1][kDtLd]
   uint32_t* offs = reinterpret_cast<uint32_t*>(sm + dt_xs_bytes(f.dim));       // [KL][MM] byte offsets into xs
-  uint8_t* codes = reinterpret_cast<uint8_t*>(offs + (size_t)KL * MM);         // [KL][kDtRows]
+  // [KL][kDtRows] codes, bit 7 = empty; bins of up to 8 positions pack two rows per byte
+  constexpr bool kPacked = MM <= 8;
+  uint8_t* codes = reinterpret_cast<uint8_t*>(offs + (size_t)KL * MM);
   const float ninf = __int_as_float(0xff800000);
   // every bin's positions as byte offsets of their transposed rows; positions
   // past the bin's end point at the -inf row
@@ -397,8 +399,11 @@ __global__ void __launch_bounds__(kDtWarps * 32) dwta_tile_kernel(DwtaDev f, con
         dt_winner<MM>(vy, b1, c1);
         const bool e0 = b0 == ninf, e1 = b1 == ninf;
         any_empty |= ((e0 && lane * 2 < nr) || (e1 && lane * 2 + 1 < nr)) ? 1 : 0;  // (rows past the end are all -inf)
-        *reinterpret_cast<uint16_t*>(codes + (size_t)g * kDtRows + lane * 2) =
-            (uint16_t)((e0 ? 0x80 : c0) | ((e1 ? 0x80 : c1) << 8));
+        if (kPacked)  // two rows' codes per byte: 3 code bits + the empty flag each
+          codes[(size_t)g * (kDtRows / 2) + lane] = (uint8_t)((e0 ? 8 : c0) | ((e1 ? 8 : c1) << 4));
+        else
+          *reinterpret_cast<uint16_t*>(codes + (size_t)g * kDtRows + lane * 2) =
+              (uint16_t)((e0 ? 0x80 : c0) | ((e1 ? 0x80 : c1) << 8));
         key0 |= (uint32_t)c0 << (f.bits * kk);
         key1 |= (uint32_t)c1 << (f.bits * kk);
       }
@@ -409,26 +414,43 @@ __global__ void __launch_bounds__(kDtWarps * 32) dwta_tile_kernel(DwtaDev f, con
     if (!__syncthreads_or(any_empty)) continue;
     // densification: empty bins copy their first occupied donor's code (flag kept
     // so that a filled bin is never taken for an occupied donor)
-    for (int q = threadIdx.x; q < KL * kDtRows; q += blockDim.x) {
-      const int g = q / kDtRows, r = q - g * kDtRows;
-      if (r >= nr || !(codes[q] & 0x80)) continue;
-      int code = 0;
-      for (int a = 0; a < 100; ++a) {
-        const int d = f.donors[g * 100 + a];
-        const uint8_t cd = codes[d * kDtRows + r];
-        if (!(cd & 0x80)) {
-          code = cd;
-          break;
+    auto code_of = [&](int g, int r) -> int {  // bit 7: empty
+      if (!kPacked) return codes[(size_t)g * kDtRows + r];
+      const int nib = (codes[(size_t)g * (kDtRows / 2) + (r >> 1)] >> (4 * (r & 1))) & 15;
+      return (nib & 7) | ((nib & 8) << 4);
+    };
+    // (packed: a thread owns a byte = rows 2p, 2p + 1 of a bin; occupied nibbles never change)
+    for (int q = threadIdx.x; q < KL * (kDtRows / 2); q += blockDim.x) {
+      const int g = q / (kDtRows / 2), p = q - g * (kDtRows / 2);
+      int filled[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = 2 * p + e;
+        int cd = code_of(g, r);
+        if (r < nr && (cd & 0x80)) {
+          int code = 0;
+          for (int a = 0; a < 100; ++a) {
+            const int dcd = code_of(f.donors[g * 100 + a], r);
+            if (!(dcd & 0x80)) {
+              code = dcd;
+              break;
+            }
+          }
+          cd = 0x80 | code;
         }
+        filled[e] = cd;
       }
-      codes[q] = (uint8_t)(0x80 | code);
+      if (kPacked)
+        codes[(size_t)g * (kDtRows / 2) + p] =
+            (uint8_t)((filled[0] & 7) | ((filled[0] & 0x80) >> 4) | ((filled[1] & 7) << 4) | (filled[1] & 0x80));
+      else
+        *reinterpret_cast<uint16_t*>(codes + (size_t)g * kDtRows + 2 * p) = (uint16_t)(filled[0] | (filled[1] << 8));
     }
     __syncthreads();
     for (int q = threadIdx.x; q < nr * f.l; q += blockDim.x) {
       const int r = q / f.l, t = q - r * f.l;
       uint32_t key = 0;
-      for (int kk = 0; kk < f.k; ++kk)
-        key |= (uint32_t)(codes[(size_t)(t * f.k + kk) * kDtRows + r] & 0x7f) << (f.bits * kk);
+      for (int kk = 0; kk < f.k; ++kk) key |= (uint32_t)(code_of(t * f.k + kk, r) & 0x7f) << (f.bits * kk);
       keys[(row0 + r) * f.l + t] = key;
     }
   }
@@ -445,7 +467,7 @@ static int dwta_tile_per_sm(size_t smem) {
 template <int MM>
 static bool launch_dwta_tile_t(const DwtaDev& f, const float* x, int64_t n, int ld, uint32_t* keys, cudaStream_t s) {
   const int KL = f.k * f.l;
-  const size_t smem = dt_xs_bytes(f.dim) + (size_t)KL * MM * 4 + (size_t)KL * kDtRows;
+  const size_t smem = dt_xs_bytes(f.dim) + (size_t)KL * MM * 4 + (size_t)KL * (MM <= 8 ? kDtRows / 2 : kDtRows);
   if (smem > 227 * 1024) return false;
   // wide rows leave room for one tile per SM: 16 warps share it instead of 8
   const int per8 = dwta_tile_per_sm<MM, 8>(smem);

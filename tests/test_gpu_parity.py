@@ -225,11 +225,16 @@ def test_relabelled_units_keep_the_network(golden, name):
     net = SlideNetwork(D, [H, N], cfg, lsh_layers={1: spec} if spec else None)
     net.relabel_units = False  # only the explicit renumberings below
     rng = np.random.default_rng(17)
+    queries = rng.standard_normal((5, H))
     for it in range(1, 4):
         if it != 2:
             before = oracle_state_from_net(net)
+            unions = net.layers[1].lsh.query_union_batch(queries) if spec else None
             net._relabel(rng.permutation(H))
             after = oracle_state_from_net(net)
+            if spec:  # external queries (caller's unit order) probe the same buckets
+                for a, b in zip(unions, net.layers[1].lsh.query_union_batch(queries)):
+                    np.testing.assert_array_equal(a, b)
             for a, b in zip(vars(before).values(), vars(after).values()):
                 np.testing.assert_array_equal(a, b)
             assert not np.array_equal(net.unit_cols(), np.arange(H))
