@@ -276,9 +276,15 @@ void tables_build(TablesHost& tb, const uint32_t* keys, int64_t n, int l, int kb
   int32_t* dir = const_cast<int32_t*>(d.dir);
   uint64_t* hdir = const_cast<uint64_t*>(d.hdir);
   const uint64_t hmask = d.hash_mask;
-  int32_t* bstart = tb.bstart.ensure<int32_t>(std::max<int64_t>(n_runs, 1));
-  int32_t* blen = tb.blen.ensure<int32_t>(std::max<int64_t>(n_runs, 1));
-  int32_t* ovf = policy == 1 ? tb.ovf_cnt.ensure<int32_t>(std::max<int64_t>(n_runs, 1)) : nullptr;
+  // per-run arrays sized by the bound (runs <= inserts), like uniq / counts /
+  // offsets above: a rebuild whose run count passed the previous one must not
+  // free and re-allocate GB-sized buffers between two training steps (seen as
+  // 50-700 ms rebuild barriers at the scaled shape) nor move what a captured
+  // step graph points at
+  const int64_t run_cap = std::max<int64_t>(total, 1);
+  int32_t* bstart = tb.bstart.ensure<int32_t>(run_cap);
+  int32_t* blen = tb.blen.ensure<int32_t>(run_cap);
+  int32_t* ovf = policy == 1 ? tb.ovf_cnt.ensure<int32_t>(run_cap) : nullptr;
   if (n_runs > 0) {
     runs_kernel<<<grid_for(n_runs), 256, 0, s>>>(uniq, counts, offsets, n_runs, cap, policy == 0, d.dense_dir,
                                                  dir, hdir, hmask, bstart, blen, ovf);
@@ -287,7 +293,7 @@ void tables_build(TablesHost& tb, const uint32_t* keys, int64_t n, int l, int kb
   if (kb > 16) build_coarse(tb, d, l, kb, n_runs, uniq, s);
   if (policy == 1 && n_runs > 0 && id_mul == 1) {
     // reservoir: host replay of the overflowing inserts (tables.py:156-161)
-    int32_t* ovf_off = tb.ovf_off.ensure<int32_t>(n_runs);
+    int32_t* ovf_off = tb.ovf_off.ensure<int32_t>(run_cap);
     size_t b4 = 0;
     SLIDE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b4, ovf, ovf_off, (int)n_runs, s));
     if (b4 > tbytes) {
