@@ -68,6 +68,9 @@ struct slide_ctx {
   cudaStream_t s3 = nullptr;
   cudaEvent_t ev_lg = nullptr, ev_lg_join = nullptr, ev_w1l = nullptr, ev_hg = nullptr;
   cudaEvent_t ev_rng = nullptr, ev_rng_join = nullptr;  // slot streams beside the hidden forward
+  // fourth stream: the W2 Adam's hot rows beside its persistent kernel (sparse-set steps)
+  cudaStream_t s4 = nullptr;
+  cudaEvent_t ev_vl = nullptr, ev_vl_join = nullptr;
   DBuf hg_done;  // per-sample slice tickets of the hidden gradient (self-resetting)
   int64_t hg_done_n = 0;
   // set by the fused step callers: forward already queues the W1 grouping
@@ -355,6 +358,12 @@ int slide_destroy(slide_ctx* c) {
       if (e) cudaEventDestroy(e);
     if (c->s2) cudaStreamDestroy(c->s2);
     if (c->s3) cudaStreamDestroy(c->s3);
+    if (c->s4) {
+      cudaStreamSynchronize(c->s4);
+      cudaEventDestroy(c->ev_vl);
+      cudaEventDestroy(c->ev_vl_join);
+      cudaStreamDestroy(c->s4);
+    }
     c->hg_done.release();
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     if (c->graph) cudaGraphDestroy(c->graph);
@@ -1127,6 +1136,21 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
     w1_update(sw);
   }
   // W2: rows in ascending order, each row's samples in slot order
+  AdamVlong vl{nullptr, nullptr, nullptr};
+  const AdamVlong* vlp = nullptr;
+  if (sparse_sets(c, b) && !c->lazy && !getenv_flag("SLIDE_ADAM_ONE_KERNEL")) {
+    if (fork) {
+      if (!c->s4) {
+        int lo = 0, hi = 0;
+        SLIDE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        SLIDE_CUDA(cudaStreamCreateWithPriority(&c->s4, cudaStreamNonBlocking, hi));
+        SLIDE_CUDA(cudaEventCreateWithFlags(&c->ev_vl, cudaEventDisableTiming));
+        SLIDE_CUDA(cudaEventCreateWithFlags(&c->ev_vl_join, cudaEventDisableTiming));
+      }
+      vl = AdamVlong{c->s4, c->ev_vl, c->ev_vl_join};
+    }
+    vlp = &vl;
+  }
   if (P_max > 0) {
     launch_adam_rows(hp, b, ap, gr.n_uniq.as<int32_t>(), gr.u_max, gr.uniq.as<int32_t>(), gr.seg_off.as<int32_t>(),
                      gr.seg_cnt.as<int32_t>(), gr.sslot.as<int32_t>(), c->dsort.as<float>(),
@@ -1134,7 +1158,7 @@ static void backward_impl(slide_ctx* c, int64_t update, const float* ext_dh = nu
                      work,
                      /*work_zeroed=*/ext_dh == nullptr, s, c->lazy ? c->z.as<float>() : nullptr,
                      c->lazy ? c->sm_stat.as<float>() : nullptr, c->lazy ? gr.mask.as<uint32_t>() : nullptr,
-                     c->lazy ? gr.lmask.as<uint32_t>() : nullptr, gr.wpk);
+                     c->lazy ? gr.lmask.as<uint32_t>() : nullptr, gr.wpk, vlp);
     c->timer.mark(s, kStAdamRows);
   }
   if (!fork) w1_update(s);

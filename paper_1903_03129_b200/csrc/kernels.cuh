@@ -250,13 +250,20 @@ size_t hidden_grad_scratch(int b, int hp);
 void launch_hidden_grad(int hp, int b, const int32_t* offs, const int32_t* prow, const float* delta, const float* w2,
                         const float* h, const int32_t* live, float* dh, float* part, int32_t* done,
                         int32_t* work_reset, cudaStream_t s);
+// sparse-set steps: the rows held by very many samples run in their own
+// kernel (stream != null: beside the persistent kernel, forked / joined with
+// the two events)
+struct AdamVlong {
+  cudaStream_t stream;
+  cudaEvent_t fork, join;
+};
 void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq, int64_t max_uniq,
                       const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_cnt,
                       const int32_t* sslot, const float* dsort, const float* h, const int32_t* live, float* w2,
                       float* m2, float* v2, float* b2, float* mb2, float* vb2, int64_t* steps2,
                       unsigned long long* touched, int32_t* work, bool work_zeroed, cudaStream_t s,
                       const float* z = nullptr, const float* stat = nullptr, const uint32_t* mask = nullptr,
-                      const uint32_t* lmask = nullptr, int wpk = 0);
+                      const uint32_t* lmask = nullptr, int wpk = 0, const AdamVlong* vl = nullptr);
 void launch_accumulate(unsigned long long* dst, const int32_t* src, cudaStream_t s);
 // per slot: the k best active ids by probability (ties: lower id), -1 padded
 void launch_topk(int b, const int32_t* offs, const int32_t* rows, int shard_count, int shard_rank, const float* prob,

@@ -1293,6 +1293,7 @@ struct AdamRowsArgs {
   const float *z = nullptr, *stat = nullptr;
   const uint32_t *mask = nullptr, *lmask = nullptr;
   int wpk = 0;
+  int vlong = 0;  // > 0: rows held by more samples than this belong to adam_rows_vlong_kernel
 };
 
 // pairs whose activations are loaded ahead of their updates (8 / NG)
@@ -1338,6 +1339,10 @@ __device__ __forceinline__ void adam_rows_loop(const AdamRowsArgs& A, const int 
     uint32_t tmask = 0;
     const int r = A.uniq[u];
     const int s0 = A.seg_off[u], len = A.seg_cnt[u];
+    if (A.vlong && len > A.vlong) {
+      u = __shfl_sync(0xffffffffu, u_next, 0);
+      continue;
+    }
     float* wr = A.w2 + (int64_t)r * hp;
     float* mr = A.m2 + (int64_t)r * hp;
     float* vr = A.v2 + (int64_t)r * hp;
@@ -1595,6 +1600,178 @@ __global__ void __launch_bounds__(256, 3) adam_rows_small_kernel(AdamRowsArgs A)
   else adam_rows_ng<2, COUNT, kAdamExtra>(A, pq, poff);
 }
 
+// Sparse-set steps (wide-out, scaled): a few hot rows (Zipf labels) are held
+// by hundreds of samples while every other row has one or two.  The
+// persistent kernel gives a row to one warp; ncu at the scaled shape: 138 us
+// at 12% active warps and 2.5M instructions -- the whole launch is one warp
+// walking a 1,024-pair row (~0.13 us a pair: an L2 round trip per 8-pair
+// batch, then dependent FMA / MUFU chains with nothing else to issue).  So
+// those rows get a CTA each, as the W1 long chains do
+// (adam_features_long_kernel): lane = live unit, the row's pairs cut into 16
+// consecutive segments; the moments are linear recurrences, so every warp
+// folds its segment into (A1, X1, A2, X2), the segments' start moments follow
+// from the earlier coefficients, every warp replays its segment with the real
+// bias corrections summing its weight steps, and the steps are subtracted in
+// segment order.  Two unit groups and the bias (activation 1) share a walk.
+// Runs on a side stream beside the persistent kernel, which skips these rows;
+// the grouping's entries are dealt round-robin to the CTAs (hot labels have
+// neighbouring ids).
+constexpr int kAdamVeryLong = 64;
+constexpr int kVlWarps = 16;
+
+template <bool COUNT>
+__global__ void __launch_bounds__(kVlWarps * 32) adam_rows_vlong_kernel(AdamRowsArgs A) {
+  // per warp and lane: (A1, X1, A2, X2) of two unit groups and the bias
+  __shared__ float4 coef[kVlWarps][3][32];
+  __shared__ float part[kVlWarps][3][32];
+  __shared__ uint32_t movedw[kVlWarps][2];
+  __shared__ int s_rows[kVlWarps * 32];
+  __shared__ int s_n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int hp = A.hp;
+  const int ng = max(1, (__ldg(A.live) + 31) >> 5);
+  const int nu = *A.n_uniq;
+  const AdamK ak(A.ap);
+  for (int base = 0; base < nu; base += gridDim.x * blockDim.x) {
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    const int idx = base + threadIdx.x * gridDim.x + blockIdx.x;
+    if (idx < nu && A.seg_cnt[idx] > kAdamVeryLong) s_rows[atomicAdd(&s_n, 1)] = idx;
+    __syncthreads();
+    const int n_rows = s_n;
+    for (int ri = 0; ri < n_rows; ++ri) {
+      const int uu = s_rows[ri];
+      const int r = A.uniq[uu], s0 = A.seg_off[uu], len = A.seg_cnt[uu];
+      const int64_t st = A.steps2[r];
+      const int j0 = len * warp / kVlWarps, j1 = len * (warp + 1) / kVlWarps;
+      // two unit groups per walk (the steady regime has one or two); the bias
+      // rides with the first walk (activation 1, every lane the same value)
+      for (int q0 = 0; q0 < ng; q0 += 2) {
+        const bool bias = q0 == 0, two = q0 + 1 < ng;
+        const int c0 = __ldg(A.live + 1 + q0 * 32 + lane);
+        const int c1 = two ? __ldg(A.live + 1 + (q0 + 1) * 32 + lane) : 0;
+        const int64_t ro0 = (int64_t)r * hp + c0, ro1 = (int64_t)r * hp + c1;
+        // moments at the row's start, read before the last warp writes them back
+        float m[3], v[3];
+        m[0] = __ldcg(A.m2 + ro0), v[0] = __ldcg(A.v2 + ro0);
+        m[1] = two ? __ldcg(A.m2 + ro1) : 0.f, v[1] = two ? __ldcg(A.v2 + ro1) : 0.f;
+        m[2] = bias ? __ldcg(A.mb2 + r) : 0.f, v[2] = bias ? __ldcg(A.vb2 + r) : 0.f;
+        // walk this warp's segment: fn(pair is inside, error, h0, h1, c1, sqrt(c2))
+        auto walk = [&](auto fn, auto with_bc) {
+          for (int jb = j0; jb < j1; jb += 32) {
+            int off_l = 0;
+            float d_l = 0.f, c1_l = 0.f, s2_l = 1.f;
+            if (jb + lane < j1) {
+              off_l = A.sslot[s0 + jb + lane] * hp;
+              d_l = A.dsort[s0 + jb + lane];
+              if (decltype(with_bc)::value) {
+                const float2 bc = bias_corr(A.ap, st + jb + lane + 1);
+                c1_l = bc.x;
+                s2_l = sqrt_approx(bc.y);
+              }
+            }
+            const int nc = min(32, j1 - jb);
+            for (int t0 = 0; t0 < nc; t0 += 8) {
+              float h0[8], h1[8];
+#pragma unroll
+              for (int t = 0; t < 8; ++t) {
+                const unsigned off = (unsigned)__shfl_sync(0xffffffffu, off_l, (t0 + t) & 31);
+                h0[t] = __ldg(A.h + (off + (unsigned)c0));
+                h1[t] = two ? __ldg(A.h + (off + (unsigned)c1)) : 0.f;
+              }
+#pragma unroll
+              for (int t = 0; t < 8; ++t) {
+                const float d = __shfl_sync(0xffffffffu, d_l, (t0 + t) & 31);
+                const float cc1 = __shfl_sync(0xffffffffu, c1_l, (t0 + t) & 31);
+                const float s2 = __shfl_sync(0xffffffffu, s2_l, (t0 + t) & 31);
+                fn(t0 + t < nc, d, h0[t], h1[t], cc1, s2);
+              }
+            }
+          }
+        };
+        // phase 1: the segment's moment recurrences as (A1, X1, A2, X2)
+        float a1[3] = {1.f, 1.f, 1.f}, x1[3] = {0.f, 0.f, 0.f}, a2[3] = {1.f, 1.f, 1.f}, x2[3] = {0.f, 0.f, 0.f};
+        walk([&](bool in, float d, float h0, float h1, float, float) {
+          const float hh[3] = {h0, h1, 1.f};
+#pragma unroll
+          for (int e = 0; e < 3; ++e) {
+            const bool on = in && (e == 2 ? bias : hh[e] > 0.f);
+            const float g = d * hh[e];
+            const float nx1 = fmaf(ak.b1, x1[e], ak.omb1 * g), nx2 = fmaf(ak.b2, x2[e], ak.omb2 * (g * g));
+            x1[e] = on ? nx1 : x1[e];
+            x2[e] = on ? nx2 : x2[e];
+            a1[e] = on ? a1[e] * ak.b1 : a1[e];
+            a2[e] = on ? a2[e] * ak.b2 : a2[e];
+          }
+        }, std::false_type{});
+#pragma unroll
+        for (int e = 0; e < 3; ++e) coef[warp][e][lane] = make_float4(a1[e], x1[e], a2[e], x2[e]);
+        __syncthreads();
+        for (int k = 0; k < warp; ++k) {
+#pragma unroll
+          for (int e = 0; e < 3; ++e) {
+            const float4 cf = coef[k][e][lane];
+            m[e] = fmaf(cf.x, m[e], cf.y);
+            v[e] = fmaf(cf.z, v[e], cf.w);
+          }
+        }
+        // phase 2: replay with the bias corrections, sum the weight steps
+        float psum[3] = {0.f, 0.f, 0.f};
+        bool moved[2] = {false, false};
+        walk([&](bool in, float d, float h0, float h1, float cc1, float s2) {
+          const float hh[3] = {h0, h1, 1.f};
+#pragma unroll
+          for (int e = 0; e < 3; ++e) {
+            const bool on = in && (e == 2 ? bias : hh[e] > 0.f);
+            const float g = d * hh[e];
+            const float mn = fmaf(ak.b1, m[e], ak.omb1 * g), vn = fmaf(ak.b2, v[e], ak.omb2 * (g * g));
+            const float stp = (cc1 * mn) * rcp_approx(fmaf(sqrt_approx(vn), s2, ak.eps));
+            m[e] = on ? mn : m[e];
+            v[e] = on ? vn : v[e];
+            psum[e] += on ? stp : 0.f;
+            if (e < 2) moved[e] |= on;
+          }
+        }, std::true_type{});
+#pragma unroll
+        for (int e = 0; e < 3; ++e) part[warp][e][lane] = psum[e];
+        const uint32_t mv0 = __ballot_sync(0xffffffffu, moved[0]), mv1 = __ballot_sync(0xffffffffu, moved[1]);
+        if (lane == 0) movedw[warp][0] = mv0, movedw[warp][1] = mv1;
+        if (warp == kVlWarps - 1) {  // the chain's end state
+          A.m2[ro0] = m[0];
+          A.v2[ro0] = v[0];
+          if (two) {
+            A.m2[ro1] = m[1];
+            A.v2[ro1] = v[1];
+          }
+          if (bias && lane == 0) {
+            A.mb2[r] = m[2];
+            A.vb2[r] = v[2];
+          }
+        }
+        __syncthreads();
+        if (warp == 0 || (warp == 1 && two) || (warp == 2 && bias)) {
+          // warp e finishes entry e: the steps are subtracted in segment order
+          const int e = warp;
+          float* dst = e == 0 ? A.w2 + ro0 : e == 1 ? A.w2 + ro1 : A.b2 + r;
+          float w = __ldcg(dst);
+#pragma unroll
+          for (int k = 0; k < kVlWarps; ++k) w -= part[k][e][lane];
+          if (e < 2 || lane == 0) *dst = w;
+          if (COUNT && e < 2 && lane == 0) {
+            uint32_t any = 0;
+#pragma unroll
+            for (int k = 0; k < kVlWarps; ++k) any |= movedw[k][e];
+            atomicAdd(A.touched, (unsigned long long)__popc(any));
+          }
+        }
+        __syncthreads();  // coef / part / movedw reuse
+      }
+      if (threadIdx.x == 0) A.steps2[r] = st + len;
+    }
+    __syncthreads();  // s_rows / s_n reuse
+  }
+}
+
 __global__ void accumulate_kernel(unsigned long long* dst, const int32_t* src) {
   if (src) *dst += (unsigned long long)*src;
 }
@@ -1610,7 +1787,8 @@ void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq
                       const int32_t* sslot, const float* dsort, const float* h, const int32_t* live, float* w2,
                       float* m2, float* v2, float* b2, float* mb2, float* vb2, int64_t* steps2,
                       unsigned long long* touched, int32_t* work, bool work_zeroed, cudaStream_t s,
-                      const float* z, const float* stat, const uint32_t* mask, const uint32_t* lmask, int wpk) {
+                      const float* z, const float* stat, const uint32_t* mask, const uint32_t* lmask, int wpk,
+                      const AdamVlong* vl) {
   if (max_uniq <= 0) return;
   if (!work_zeroed) SLIDE_CUDA(cudaMemsetAsync(work, 0, 4, s));
   // persistent: as many CTAs as are resident at once
@@ -1623,6 +1801,21 @@ void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq
   const int grid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * per_sm);
   AdamRowsArgs A{hp, ap, n_uniq, uniq, seg_off, seg_cnt, sslot, dsort, h, live,
                  w2, m2, v2, b2, mb2, vb2, steps2, touched, work, z, stat, mask, lmask, wpk};
+  if (vl && !z) {
+    // the hot rows first, on their own stream: their CTAs are placed before
+    // the persistent kernel's, which skips them
+    cudaStream_t sv = vl->stream ? vl->stream : s;
+    if (vl->stream) {
+      SLIDE_CUDA(cudaEventRecord(vl->fork, s));
+      SLIDE_CUDA(cudaStreamWaitEvent(sv, vl->fork, 0));
+    }
+    const int vgrid = (int)std::min<int64_t>(ceil_div(max_uniq, kAdamVeryLong), (int64_t)kSms * 2);
+    if (touched) adam_rows_vlong_kernel<true><<<vgrid, kVlWarps * 32, 0, sv>>>(A);
+    else adam_rows_vlong_kernel<false><<<vgrid, kVlWarps * 32, 0, sv>>>(A);
+    SLIDE_LAUNCH_CHECK();
+    if (vl->stream) SLIDE_CUDA(cudaEventRecord(vl->join, sv));
+    A.vlong = kAdamVeryLong;
+  }
   if (hp > 128) {
     const int sgrid = (int)std::min<int64_t>(ceil_div(max_uniq, 8), (int64_t)kSms * (env_per_sm > 0 ? env_per_sm : 3));
     if (touched) adam_rows_small_kernel<true><<<sgrid, 256, 0, s>>>(A);
@@ -1635,6 +1828,7 @@ void launch_adam_rows(int hp, int b, const AdamParams& ap, const int32_t* n_uniq
     SLIDE_NV_DISPATCH(hp, (adam_rows_kernel<NV, false><<<grid, 256, 0, s>>>(A)));
   }
   SLIDE_LAUNCH_CHECK();
+  if (vl && !z && vl->stream) SLIDE_CUDA(cudaStreamWaitEvent(s, vl->join, 0));
 }
 
 // ------------------------------------------------------- Adam, W1 features
