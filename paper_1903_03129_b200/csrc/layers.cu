@@ -1989,8 +1989,8 @@ __global__ void __launch_bounds__(256, NV == 1 ? 4 : 2) adam_features_kernel(Ada
 // weight steps, and the steps are subtracted in segment order.  The
 // sequential chain of the reference (network.py:428-451, one Adam step per
 // sample in slot order) becomes kLongWarps chains 1 / kLongWarps as long.
-// kLongWarps: 4 for batches up to 128 slots, 8 up to 512, 16 beyond (the
-// chains are as long as the batch).
+// kLongWarps: 4 for batches up to 128 slots, 8 beyond (the chains are as
+// long as the batch).
 template <int kLongWarps>
 __global__ void __launch_bounds__(kLongWarps * 32) adam_features_long_kernel(AdamFeatArgs A) {
   __shared__ float4 coef[kLongWarps][32];
@@ -2104,9 +2104,11 @@ void launch_adam_features(int hp, const AdamParams& ap, const int32_t* n_uniq, i
   // branch's tail): at most max_uniq / (kW1LongChain + 1) of them
   const int64_t max_long = std::min<int64_t>(max_uniq, ceil_div(max_uniq, kW1LongChain)) * (hp / 32);
   const int lgrid = (int)std::min<int64_t>(std::max<int64_t>(max_long, 1), (int64_t)kSms * 16);
+  // (16 warps were tried for B = 1,024: a 512-thread CTA only finds room once
+  // the short-chain kernel's 256-thread CTAs have drained, so the long chains
+  // started when the short ones ended; 8 warps run beside them)
   if (b <= 128) adam_features_long_kernel<4><<<lgrid, 4 * 32, 0, s_long>>>(A);
-  else if (b <= 512) adam_features_long_kernel<8><<<lgrid, 8 * 32, 0, s_long>>>(A);
-  else adam_features_long_kernel<16><<<lgrid, 16 * 32, 0, s_long>>>(A);
+  else adam_features_long_kernel<8><<<lgrid, 8 * 32, 0, s_long>>>(A);
   SLIDE_LAUNCH_CHECK();
   SLIDE_NV_DISPATCH(hp, (adam_features_kernel<NV><<<grid, 256, 0, s>>>(A)));
   SLIDE_LAUNCH_CHECK();
