@@ -264,6 +264,37 @@ def test_relabelled_units_keep_the_network(golden, name):
     np.testing.assert_allclose(cap[1][4], dh[nz], rtol=1e-4, atol=1e-7)
 
 
+@pytest.mark.parametrize("H", [128, 96, 256])
+def test_hot_rows_in_sparse_set_steps(H):
+    """Sparse-set regime (sets x 4 < N) with labels shared by most of the batch:
+    rows held by more than 64 samples take the CTA-per-row W2 Adam
+    (adam_rows_vlong_kernel: 16 segments with folded moment recurrences, two
+    unit groups and the bias per walk) beside the persistent kernel.  Three
+    teacher-forced steps from step 1, where every hidden unit is live (four
+    unit groups at H = 128: two walks; eight at H = 256 through the
+    wide-hidden kernels; a ragged last group at H = 96) down to the few-group
+    regime."""
+    rng = np.random.default_rng(31)
+    D, N, B = 300, 20000, 128
+    spec = LshLayerConfig("dwta", k=4, l=8, capacity=16, policy="fifo", wta_bin_size=4,
+                          sampler=SamplerConfig("vanilla", beta=32))
+    cfg = TrainConfig(batch_size=B, seed=9, learning_rate=1e-3, n0=1000)
+    net = SlideNetwork(D, [H, N], cfg, lsh_layers={1: spec})
+    held = []
+    for it in (1, 2, 3):
+        trip = []
+        for i in range(B):
+            idx = np.sort(rng.choice(D, size=int(rng.integers(3, 12)), replace=False))
+            vals = (rng.random(idx.size) + 0.05).astype(np.float32).astype(np.float64)
+            labels = {7, int(rng.integers(0, N))}  # row 7: every sample; row 11: ~2/3 of them
+            if i % 3:
+                labels.add(11)
+            trip.append((idx.astype(np.int64), vals, sorted(labels)))
+        want, got, _ = teacher_forced_step(net, trip, it, "snapshot", 1e-3, what=f"hot rows H{H} it{it}")
+        held.append(sum(7 in t.active for t in want.traces))
+    assert min(held) == B  # the hot row really was held by the whole batch
+
+
 def test_two_pass_selection_mixed_samples():
     """Sparse buckets with one hot bucket per table: the selection runs its
     1,024-candidate pass first and the bound-sized pass (L x capacity + labels
