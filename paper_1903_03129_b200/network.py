@@ -164,32 +164,41 @@ class Layer:
 
     def _mirror_mat(self, name):
         dev = self._mat(name)
-        raw = getattr(self._net, name + ("1t" if self._i == 0 else "2"))
-        cols = self._net._unit_cols_dev()
+        net = self._net
+        raw = getattr(net, name + ("1t" if self._i == 0 else "2"))
         first = self._i == 0
+        H = net.hidden
 
-        def flush(a, dev=dev):
+        def flush(a):
             import torch
 
+            # the unit order of the moment of the write (a mirror may outlive a renumbering)
+            cols = net._unit_cols_dev()
             src = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(raw.device)
+            if first:
+                src = src.T
             if cols is None:
-                dev.copy_(src)
+                raw[:, :H] = src
             else:
-                raw[:, cols] = src.T if first else src
+                raw[:, cols] = src
 
         return _Mirror(dev.double().cpu().numpy(), flush)
 
     def _mirror_vec(self, name, dtype=np.float64):
         dev = self._vec(name)
-        raw = getattr(self._net, name + ("1" if self._i == 0 else "2"))
-        cols = self._net._unit_cols_dev() if self._i == 0 else None
+        net = self._net
+        raw = getattr(net, name + ("1" if self._i == 0 else "2"))
+        first = self._i == 0
+        width = self.width
+        np_dtype = dev.cpu().numpy().dtype
 
-        def flush(a, dev=dev):
+        def flush(a):
             import torch
 
-            src = torch.from_numpy(np.ascontiguousarray(a).astype(dev.cpu().numpy().dtype)).to(raw.device)
+            cols = net._unit_cols_dev() if first else None
+            src = torch.from_numpy(np.ascontiguousarray(a).astype(np_dtype)).to(raw.device)
             if cols is None:
-                dev.copy_(src)
+                raw[:width] = src
             else:
                 raw[cols] = src
 

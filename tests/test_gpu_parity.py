@@ -243,13 +243,17 @@ def test_relabelled_units_keep_the_network(golden, name):
             np.testing.assert_array_equal(net.layers[0].steps, before.steps1)
         trip = _golden_batch(g, name, it, B)
         teacher_forced_step(net, trip, it, "snapshot", 1e-2, what=f"relabelled {name} it{it}")
-    # view writes land in the right physical columns
+    # view writes land in the right physical columns -- also through a view
+    # taken before a renumbering
     w = net.layers[1].w
     w[3, 5] = 0.25
     b = net.layers[0].b
     b[2] = -0.5
+    w1 = net.layers[0].w
+    net._relabel(rng.permutation(H))
+    w1[1, 4] = 0.125
     st = oracle_state_from_net(net)
-    assert st.w2[3, 5] == 0.25 and st.b1[2] == -0.5
+    assert st.w2[3, 5] == 0.25 and st.b1[2] == -0.5 and st.w1t[4, 1] == 0.125
     # single-sample API: activations and hidden errors in the caller's order
     xi, xv, y = _golden_batch(g, name, 1, B)[0]
     x = SparseVector(np.asarray(xi), np.asarray(xv), D)
