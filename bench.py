@@ -481,7 +481,9 @@ def run_ours(args, rank, world):
         "stages_ms_per_step": {k: round(v, 4) for k, v in stage_ms.items()},
         "realised_per_step": {"pairs": cnt[8] / K, "unique_rows": cnt[2] / K, "unique_features": cnt[3] / K,
                               "touched_w2": cnt[0] / K, "touched_w1": cnt[1] / K, "input_nnz": cnt[9] / K,
-                              "probed_slots": cnt[4] / K, "rebuilds_in_profile": int(cnt[11])},
+                              "probed_slots": cnt[4] / K, "rebuilds_in_profile": int(cnt[11]),
+                              # hidden-unit renumberings so far (live units kept adjacent)
+                              "unit_relabels": int(getattr(net, "relabels", 0))},
         "gpu_launches": int(lc1[0] - lc0[0]),
         "clocks": clk.summary(),
         "loss_first_last": [losses[0], losses[-1]],
